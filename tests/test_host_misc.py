@@ -1,0 +1,53 @@
+"""Host-side pieces: synthetic inputs, weight blob, speedup bounds (no GPU)."""
+import os
+
+import numpy as np
+import pytest
+
+from paper_2303_03848_b200 import report, synth
+
+
+def test_speedup_bound_golden(golden):
+    g = golden("spec_examples.json")["speedup_bound"]
+    for c in g["cases"]:
+        assert report.speedup_bound(c["K"], c["P"], c["ratio"]) == pytest.approx(c["s"], rel=1e-6), g["cite"]
+
+
+def test_speedup_bound_is_pipelined_cost_model():
+    """Eq. (8) equals P c_f / ((P+K) c_c + K c_f) (Q19) and dominates the blocking bound."""
+    for K, P, cc, cf in [(3, 16, 1.0, 40.0), (2, 8, 0.3, 1.0), (5, 64, 2.0, 3.0)]:
+        assert report.speedup_bound(K, P, cc / cf) == pytest.approx(P * cf / ((P + K) * cc + K * cf), rel=1e-12)
+        assert report.speedup_bound_blocking(K, P, cc / cf) <= report.speedup_bound(K, P, cc / cf)
+
+
+def test_kaiming_statistics():
+    """empirical weight variance within 10% of 2/fan_in; deterministic per seed."""
+    net = synth.kaiming_net([50] * 12, seed=4)
+    w = np.concatenate([W.ravel() for W in net.W])
+    assert abs(w.var() / (2.0 / 50) - 1.0) < 0.1
+    net2 = synth.kaiming_net([50] * 12, seed=4)
+    assert all(np.array_equal(a, b) for a, b in zip(net.W, net2.W))
+    assert all(np.all(np.abs(b) <= 1 / np.sqrt(50)) for b in net.b)
+
+
+def test_blob_roundtrip(tmp_path):
+    net = synth.kaiming_net(synth.PINN_3x20, seed=2, in_scale=[1, 2, 3, 4], out_scale=0.5)
+    path = os.path.join(tmp_path, "w.bin")
+    synth.save_blob(net, path)
+    back = synth.load_blob(path)
+    assert back.dims == net.dims and back.activation == net.activation and back.out_scale == 0.5
+    assert np.array_equal(back.scales(), net.scales())
+    for a, b in zip(net.W + net.b, back.W + back.b):
+        assert np.array_equal(a, b)
+
+
+def test_configs_match_baseline():
+    c = {k: synth.config(k) for k in ("C1", "C2", "C3", "C4", "C5")}
+    assert (c["C1"].M, c["C1"].N) == (64, 4)
+    assert (c["C2"].M, c["C2"].N) == (1024, 32)
+    assert (c["C3"].M, c["C3"].N) == (1 << 20, 64)
+    assert (c["C4"].M, c["C4"].N, c["C4"].B) == (256, 16, 4096)
+    assert np.allclose(c["C4"].L, 4 * c["C4"].strike)
+    assert (c["C5"].M, c["C5"].N) == (1 << 18, 64)
+    for p in c.values():
+        assert p.fine_steps == 100 and p.fine_theta == 1.0 and p.T == 1.0
