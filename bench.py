@@ -1,0 +1,348 @@
+#!/usr/bin/env python
+"""Benchmark of the Parareal + PINN hot path (BASELINE.json metric) on N GPUs.
+
+One step = one full Parareal solve (all SURVEY.md §8(a) rows: payoff, k=0 coarse sweep,
+K fine sweeps with the correction + coarse chain, δ reductions, output) through the C ABI.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--coarse pinn|ie] [--iters 3]
+  python bench.py --impl reference ...   # the CPU oracle as the reference arm (rank 0 only)
+
+Default workload: configs[1] (C2: 1024 points x 32 slices, PINN 3x20 coarse, fixed K=3 as the
+paper reports runtimes for K=3).  value = grid-point-steps of the problem solved
+(B·M·N·n_f per solve: the serial fine work Parareal replaces) per second of device time.
+Inputs (C2) are far below L2 size, so L2 is flushed (256 MiB write) before every timed step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Parareal speedup vs serial fine; fine grid-point-steps/s; PINN evals/s"
+UNIT = "grid-point-steps/s"
+FLUSH_BYTES = 256 << 20
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--coarse", default="pinn", choices=["pinn", "ie"])
+    ap.add_argument("--iters", type=int, default=3, help="fixed Parareal iterations K (tol = 0)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def problem_for(args):
+    from paper_2303_03848_b200 import synth
+    coarse = synth.COARSE_PINN if args.coarse == "pinn" else synth.COARSE_IMPLICIT_EULER
+    p = synth.config(args.config, coarse=coarse, coarse_steps=1, tol=0.0)
+    return p.replace(max_iter=min(args.iters, p.N))
+
+
+def work_units(p) -> float:
+    """Grid-point-steps of the problem: B·M·N·n_f (the serial fine solve's point-steps)."""
+    return float(p.B) * p.M * p.N * p.fine_steps
+
+
+def pinn_flops(dims) -> float:
+    return float(sum(2 * dims[l] * dims[l + 1] for l in range(len(dims) - 1)))
+
+
+class Clocks:
+    """nvidia-smi sampler for the timed region (B200_PROFILING.md clocks line)."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device, self.rows, self.proc = device, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), "--query-gpu=" + self.Q,
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return d, "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+# --------------------------------------------------------------------------- reference arm
+def cpu_oracle_run(p, net, budget_s: float, max_runs: int):
+    """Time the CPU oracle (as it stands) on the full workload; returns (sec per solve, runs, cores)."""
+    import oracle
+    times = []
+    t_start = time.perf_counter()
+    while len(times) < max_runs:
+        t0 = time.perf_counter()
+        oracle.parareal(p, net)
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() - t_start > budget_s:
+            break
+    return statistics.mean(times), len(times), 1
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from paper_2303_03848_b200 import synth
+    p = problem_for(args)
+    net = synth.kaiming_net(synth.PINN_3x20, seed=0) if p.coarse == synth.COARSE_PINN else None
+    import oracle
+    for _ in range(max(0, min(args.warmup, 1))):
+        oracle.parareal(p, net)
+    per, runs, cores = cpu_oracle_run(p, net, budget_s=1e9, max_runs=max(1, args.steps))
+    value = work_units(p) / per
+    sample = "full %s workload (M=%d, N=%d, B=%d, K=%d), %d timed solves" % (args.config, p.M, p.N, p.B,
+                                                                             p.max_iter, runs)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": runs, "warmup": args.warmup, "ms_per_step": per * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_dict(args, p),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+def config_dict(args, p):
+    return {"workload": "%s: European call, M=%d grid points x N=%d slices x B=%d instances, %d IE fine "
+                        "steps/slice, %s coarse, K=%d fixed iterations" % (
+                            args.config, p.M, p.N, p.B, p.fine_steps,
+                            "PINN [4,20,20,20,1] tanh" if args.coarse == "pinn" else "implicit-Euler (1 step/slice)",
+                            p.max_iter),
+            "M": p.M, "N": p.N, "B": p.B, "fine_steps": p.fine_steps, "K": p.max_iter,
+            "coarse": args.coarse, "parallelism": "time-slices/%d" % args.gpus,
+            "l2": "flushed (256 MiB write) before every timed step" if p.M * p.B * 4 * (p.N + 1) * 3 < (126 << 20)
+            else "working set larger than L2"}
+
+
+# --------------------------------------------------------------------------- our arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    from paper_2303_03848_b200 import parareal, synth
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        print("warning: --gpus %d but WORLD_SIZE %d" % (args.gpus, world), file=sys.stderr)
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    p = problem_for(args)
+    if p.N % world:
+        raise SystemExit("N=%d not divisible by %d GPUs" % (p.N, world))
+    net = synth.kaiming_net(synth.PINN_3x20, seed=0)
+    nccl_id = None
+    if world > 1:
+        obj = [parareal.get_nccl_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    stream = torch.cuda.current_stream()
+    ctx = parareal.Context(p, rank=rank, world=world, device=local, nccl_id=nccl_id, stream=stream.cuda_stream)
+    if p.coarse == synth.COARSE_PINN:
+        ctx.load_weights(net)
+    ws = torch.empty(ctx.workspace_bytes(), dtype=torch.uint8, device="cuda")
+    ctx.bind_workspace(ws)
+    out = torch.empty((p.B, p.M), dtype=torch.float32, device="cuda")
+    flush = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device="cuda")
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    for _ in range(max(args.warmup, 3)):
+        ctx.solve_device(out)
+    torch.cuda.synchronize()
+    # ---------------- timed region: device time of K solves (events on the launching stream)
+    step_ms, reps = [], []
+    barrier()
+    torch.cuda.synchronize()
+    with Clocks(local) as clk:
+        for _ in range(args.steps):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            reps.append(ctx.solve_device(out))
+            e1.record(stream)
+            e1.synchronize()
+            step_ms.append(e0.elapsed_time(e1))
+    torch.cuda.synchronize()
+    barrier()
+    total = torch.tensor([sum(step_ms)], dtype=torch.float64, device="cuda")
+    if dist is not None:
+        dist.all_reduce(total, op=dist.ReduceOp.MAX)
+    total_ms = float(total.item())
+    ms_step = total_ms / args.steps
+    value = work_units(p) * args.steps / (total_ms / 1e3)
+    launches = int(sum(r["kernel_launches"] for r in reps))
+    # ---------------- serial fine baseline (one GPU) and Eq. (8) context
+    serial_ms = None
+    if rank == 0:
+        for _ in range(2):
+            ctx.serial_fine_device(out)
+        sm = []
+        for _ in range(max(3, min(args.steps, 10))):
+            flush.zero_()
+            torch.cuda.synchronize()
+            sm.append(ctx.serial_fine_device(out))
+        serial_ms = statistics.median(sm)
+    K = p.max_iter
+    ph = {k: statistics.median([r[k] for r in reps]) for k in ("ms_fine", "ms_coarse", "ms_comm", "ms_setup",
+                                                               "ms_total")}
+    # ---------------- roofline of the dominant kernel (per-launch average, events per phase)
+    pk, pk_src = peaks()
+    clk_mhz = float(pk.get("sm_max_mhz", 1965.0))
+    n_sm = torch.cuda.get_device_properties(local).multi_processor_count
+    fine_dominant = ph["ms_fine"] >= ph["ms_coarse"]
+    nloc = p.N // world
+    if fine_dominant:
+        # resident fine sweep: fp64 FMA pipe; 9 algorithmic fp64 flop per point-step
+        pt_steps = float(p.B) * p.M * p.fine_steps * sum(max(0, nloc - max(0, k - 1 - rank * nloc)) for k in
+                                                           range(1, K + 1)) / K
+        if p.M <= 2048:
+            peak = n_sm * 64 * 2 * clk_mhz * 1e6 / 1e12
+            roof = {"kernel": "k_fine_sweep (resident, fp64)", "bound": "alu",
+                    "achieved": 9.0 * pt_steps / (ph["ms_fine"] / K / 1e3) / 1e12, "peak": peak,
+                    "unit": "TFLOP/s", "peak_source": "fp64 pipe: %d SMs x 64 FMA/clk x 2 x %.0f MHz" % (n_sm, clk_mhz)}
+        else:
+            peak = float(pk["hbm_gbs"])
+            roof = {"kernel": "k_streamed_pass (fine sweep)", "bound": "hbm",
+                    "achieved": 16.0 * pt_steps / (ph["ms_fine"] / K / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
+                    "peak_source": pk_src}
+    else:
+        evals = float(p.B) * p.M * (nloc * (K + 1)) / (K + 1)
+        if p.coarse == synth.COARSE_PINN:
+            peak = n_sm * 128 * 2 * clk_mhz * 1e6 / 1e12
+            roof = {"kernel": "k_pinn_chain (fp32 SIMT)", "bound": "alu",
+                    "achieved": pinn_flops(synth.PINN_3x20) * evals / (ph["ms_coarse"] / (K + 1) / 1e3) / 1e12,
+                    "peak": peak, "unit": "TFLOP/s",
+                    "peak_source": "fp32 FMA pipe: %d SMs x 128 FMA/clk x 2 x %.0f MHz" % (n_sm, clk_mhz)}
+        else:
+            peak = n_sm * 64 * 2 * clk_mhz * 1e6 / 1e12
+            roof = {"kernel": "k_resident_chain (numerical G, fp64)", "bound": "alu",
+                    "achieved": 9.0 * evals / (ph["ms_coarse"] / (K + 1) / 1e3) / 1e12, "peak": peak,
+                    "unit": "TFLOP/s", "peak_source": "fp64 pipe"}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["traffic"] = None
+    # ---------------- e2e through the host-buffer ABI call (pinned H2D of V_T, D2H of V_0)
+    e2e = None
+    if not args.no_e2e:
+        vt_host = torch.from_numpy(ctx.initial_state()).pin_memory() if rank == 0 else None
+        v0_host = torch.empty((p.B, p.M), dtype=torch.float32).pin_memory()
+        ctx.solve_host_ptrs(vt_host.data_ptr() if rank == 0 else None, v0_host.data_ptr())
+        barrier()
+        torch.cuda.synchronize()
+        ems = []
+        for _ in range(args.steps):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            ctx.solve_host_ptrs(vt_host.data_ptr() if rank == 0 else None, v0_host.data_ptr())
+            e1.record(stream)
+            e1.synchronize()
+            ems.append(e0.elapsed_time(e1))
+        et = torch.tensor([sum(ems)], dtype=torch.float64, device="cuda")
+        if dist is not None:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        e2e = {"value": work_units(p) * args.steps / (float(et.item()) / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": 4 * p.B * p.M, "d2h_bytes_per_step": 4 * p.B * p.M}
+    # ---------------- CPU oracle baseline (rank 0, N=1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from paper_2303_03848_b200 import synth as S
+        netc = net if p.coarse == S.COARSE_PINN else None
+        per, runs, cores = cpu_oracle_run(p, netc, budget_s=10.0, max_runs=20)
+        cpu = {"value": work_units(p) / per, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": "full %s workload, %d serial fp64 oracle solves (%.3f s each)" % (args.config, runs, per)}
+    if rank == 0:
+        from paper_2303_03848_b200 import report
+        ratio = None
+        fine_slice_ms = ph["ms_fine"] / K / max(1, nloc) if K else None
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f32 state / f64 implicit solves / f32 PINN",
+                "data": "synthetic (payoff initial state, Kaiming-random PINN weights seed 0)",
+                "config": config_dict(args, p),
+                "speedup_vs_serial_fine": (serial_ms / ms_step) if serial_ms else None,
+                "serial_fine_ms": serial_ms,
+                "phases_ms": ph,
+                "pinn_evals_per_s": (float(p.B) * p.M * sum(p.N - k for k in range(0, K + 1)) / (ph["ms_coarse"] / 1e3))
+                if p.coarse == synth.COARSE_PINN and ph["ms_coarse"] > 0 else None,
+                "fine_point_steps_executed_per_s": float(p.B) * p.M * p.fine_steps * sum(p.N - k + 1 for k in range(1, K + 1))
+                / (ph["ms_fine"] / 1e3) if ph["ms_fine"] > 0 else None,
+                "eq8_bound_context": None,
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+                "clocks": clk.summary()}
+        if serial_ms and ph["ms_coarse"] > 0:
+            c_f = serial_ms / p.N
+            c_c = ph["ms_coarse"] / (K + 1) / p.N
+            line["eq8_bound_context"] = {"c_c_ms": c_c, "c_f_ms": c_f,
+                                         "pipelined": report.speedup_bound(K, p.N, c_c / c_f),
+                                         "blocking": report.speedup_bound_blocking(K, p.N, c_c / c_f)}
+        print(json.dumps(line))
+    ctx.close()
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,341 @@
+// fine_resident.cuh — K1: on-chip implicit-Euler propagator for M ≤ 4096.
+//
+// One "system" = one (instance, slice) state vector of M interior points
+// (§3.2), owned by NT threads with P consecutive points each.
+// The state, the fp64 LU factors of M_f = I − dτA and every scan coefficient
+// live in registers for all implicit steps of the slice; HBM is touched once
+// per slice (load U_n, store F̂_n or D_n = F̂_n − Ĝ_n).
+//
+// Per implicit step (implicit Euler; reading Q1) the constant-matrix
+// Thomas solve M_f x⁺ = x + dτ(a_M+b_M) g(τ⁺) e_M splits into two first-order
+// linear recurrences (forward elimination y_j = r_j − m_j y_{j−1}, back
+// substitution x_j = y_j/p_j − (u_j/p_j) x_{j+1}).  Each is evaluated as a
+// chunked scan of affine maps v ↦ A + B·v: a sequential pass over the
+// thread's P points, a Hillis–Steele warp scan of the A parts (the B parts
+// are products of constant factors, so every level coefficient is
+// precomputed once per kernel), a fold over the ≤16 warp totals in shared
+// memory, and a fix-up with precomputed prefix products.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace pr {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+struct ResidentArgs {
+  int M, Mp, B;
+  // factors of the scheme used by this launch: [nsets][Mp] each (fp64)
+  const double *fm, *fip, *fcu;
+  const int *fset;          // [B] factor-set index per instance
+  const double *bcoef;      // [B] dτ (a_M + b_M) of this scheme (boundary term of row M)
+  const double *Lb, *Kb, *rb;
+  int upper_bc;             // 0 asymptotic call value, 1 zero
+  double dT, dtau;          // slice length, implicit step
+  int steps;                // implicit steps per slice
+  int n_base;               // global index of local slice 0
+  // ---- sweep mode (independent slices; blockIdx → (slice, instance))
+  int ln0, nsl;             // local slices [ln0, ln0+nsl)
+  const float *U;           // [Nloc+1][B][Mp]   inputs U_n
+  const float *Gh;          // [Nloc][B][Mp]     Ĝ_n (D mode)
+  float *D;                 // [Nloc][B][Mp]     D_n = F̂_n − Ĝ_n
+  float *Fk;                // [B][Mp]           F̂ of local slice fk_ln
+  int fk_ln;                // -1: none
+  float *Fout;              // non-null: F̂ of every job → Fout[(ln-ln0)][B][Mp] (test hook)
+  // ---- chain mode (serial in n, one system per instance)
+  float *Uw;                // writable rows Uw + ln·ustride: reads row c_ln0, writes row ln+1
+  size_t ustride;           // elements between slice rows of Uw (0 → one row updated in place)
+  float *GhW;               // nullable: Ĝ_n = g
+  const float *Dc;          // nullable: U_{n+1} = g + D_n
+  const float *Fcopy;       // nullable: first U[c_ln0] := Fcopy (+ δ partial)
+  int c_ln0, c_ln1;
+  double *partials;         // nullable: [(ln)·B + b]·nch + 0 → (num, den)
+  int nch;
+};
+
+__device__ __forceinline__ double g_upper(const ResidentArgs &a, int b, double tau) {
+  // Reading Q3: V(L, τ) = L − K e^{−rτ} (default) or 0 (paper-literal P:161)
+  return a.upper_bc ? 0.0 : a.Lb[b] - a.Kb[b] * exp(-a.rb[b] * tau);
+}
+
+template <int P, int NT>
+struct Tri {
+  static constexpr int NW = NT / 32;
+  double nm[P], ip[P], ncu[P], qf[P], qb[P];
+  double cfL[5], cbL[5];
+  double cf_exc, cb_exc;
+  int lane, w;
+
+  // shared layout per system: ctf[NW], ctb[NW], sy[2][NW]
+  __device__ void setup(const ResidentArgs &a, int set, int t, double *sh) {
+    lane = t & 31;
+    w = t >> 5;
+    const double *fm = a.fm + (size_t)set * a.Mp;
+    const double *fip = a.fip + (size_t)set * a.Mp;
+    const double *fcu = a.fcu + (size_t)set * a.Mp;
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      const int j = t * P + i;
+      if (j < a.M) {
+        nm[i] = -fm[j];
+        ip[i] = fip[j];
+        ncu[i] = -fcu[j];
+      } else {  // identity padding rows
+        nm[i] = 0.0;
+        ip[i] = 1.0;
+        ncu[i] = 0.0;
+      }
+    }
+    double c = 1.0;
+#pragma unroll
+    for (int i = 0; i < P; ++i) { c *= nm[i]; qf[i] = c; }
+    c = 1.0;
+#pragma unroll
+    for (int i = P - 1; i >= 0; --i) { c *= ncu[i]; qb[i] = c; }
+    // warp-scan level coefficients (products of constant maps)
+    double cf = qf[P - 1], cb = qb[0];
+#pragma unroll
+    for (int l = 0; l < 5; ++l) {
+      const int d = 1 << l;
+      const double pf = __shfl_up_sync(kFull, cf, d);
+      const double pb = __shfl_down_sync(kFull, cb, d);
+      cfL[l] = (lane >= d) ? cf : 0.0;
+      cbL[l] = (lane + d <= 31) ? cb : 0.0;
+      if (lane >= d) cf *= pf;
+      if (lane + d <= 31) cb *= pb;
+    }
+    const double ef = __shfl_up_sync(kFull, cf, 1);
+    const double eb = __shfl_down_sync(kFull, cb, 1);
+    cf_exc = (lane == 0) ? 1.0 : ef;
+    cb_exc = (lane == 31) ? 1.0 : eb;
+    if (NW > 1) {
+      if (lane == 31) sh[w] = cf;       // total forward product of warp w
+      if (lane == 0) sh[NW + w] = cb;   // total backward product of warp w
+    }
+  }
+
+  // One implicit step in place on x[P] (fp64).  bc_i: point index inside this thread that
+  // receives the boundary term (−1 if none); bcg = dτ(a_M+b_M) g(τ⁺).
+  __device__ __forceinline__ void step(double (&x)[P], int bc_i, double bcg, double *sh) {
+#pragma unroll
+    for (int i = 0; i < P; ++i)
+      if (i == bc_i) x[i] += bcg;
+    // ---- forward elimination y_j = r_j − m_j y_{j−1}
+#pragma unroll
+    for (int i = 1; i < P; ++i) x[i] = fma(nm[i], x[i - 1], x[i]);
+    double v = x[P - 1];
+#pragma unroll
+    for (int l = 0; l < 5; ++l) v = fma(cfL[l], __shfl_up_sync(kFull, v, 1 << l), v);
+    double ve = __shfl_up_sync(kFull, v, 1);
+    if (lane == 0) ve = 0.0;
+    double in = 0.0;
+    if (NW > 1) {
+      double *sy = sh + 2 * NW;
+      if (lane == 31) sy[w] = v;
+      __syncthreads();
+#pragma unroll 1
+      for (int q = 0; q < w; ++q) in = fma(sh[q], in, sy[q]);
+    }
+    const double yin = fma(cf_exc, in, ve);
+#pragma unroll
+    for (int i = 0; i < P; ++i) x[i] = fma(qf[i], yin, x[i]);
+    // ---- back substitution x_j = y_j/p_j − (u_j/p_j) x_{j+1}
+    x[P - 1] *= ip[P - 1];
+#pragma unroll
+    for (int i = P - 2; i >= 0; --i) x[i] = fma(ncu[i], x[i + 1], x[i] * ip[i]);
+    v = x[0];
+#pragma unroll
+    for (int l = 0; l < 5; ++l) v = fma(cbL[l], __shfl_down_sync(kFull, v, 1 << l), v);
+    ve = __shfl_down_sync(kFull, v, 1);
+    if (lane == 31) ve = 0.0;
+    in = 0.0;
+    if (NW > 1) {
+      double *sy = sh + 3 * NW;
+      if (lane == 0) sy[w] = v;
+      __syncthreads();
+#pragma unroll 1
+      for (int q = NW - 1; q > w; --q) in = fma(sh[NW + q], in, sy[q]);
+    }
+    const double xin = fma(cb_exc, in, ve);
+#pragma unroll
+    for (int i = 0; i < P; ++i) x[i] = fma(qb[i], xin, x[i]);
+  }
+};
+
+// Fixed-order block reduction of two doubles over the threads of one system (NT threads).
+template <int NT>
+__device__ __forceinline__ void sys_reduce2(double &a, double &b, int t, double *red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(kFull, a, o);
+    b += __shfl_xor_sync(kFull, b, o);
+  }
+  if (NT > 32) {
+    constexpr int NW = NT / 32;
+    __syncthreads();
+    if ((t & 31) == 0) { red[2 * (t >> 5)] = a; red[2 * (t >> 5) + 1] = b; }
+    __syncthreads();
+    a = 0.0; b = 0.0;
+#pragma unroll 1
+    for (int q = 0; q < NW; ++q) { a += red[2 * q]; b += red[2 * q + 1]; }
+  }
+}
+
+template <int P, int NT>
+__device__ __forceinline__ void run_steps(Tri<P, NT> &tri, const ResidentArgs &a, int b, int n,
+                                          int t, double (&x)[P], double *sh) {
+  const int bc_t = (a.M - 1) / P, bc_ip = (a.M - 1) % P;
+  const int bc_i = (t == bc_t) ? bc_ip : -1;
+  const double coef = a.bcoef[b];
+  const double tau0 = n * a.dT;
+#pragma unroll 1
+  for (int m = 0; m < a.steps; ++m) {
+    double bcg = 0.0;
+    if (bc_i >= 0) bcg = coef * g_upper(a, b, (tau0 + m * a.dtau) + a.dtau);
+    tri.step(x, bc_i, bcg, sh);
+  }
+}
+
+// SWEEP: every (slice, instance) system independently; blockIdx.x = system group.
+template <int P, int NT, int SPB>
+__global__ void __launch_bounds__(NT * SPB) k_fine_sweep(ResidentArgs a) {
+  constexpr int NW = NT / 32;
+  __shared__ double shm[SPB][4 * NW + 2];
+  const int sys = blockIdx.x * SPB + threadIdx.x / NT;
+  const int t = threadIdx.x % NT;
+  const int nsys = a.nsl * a.B;
+  const bool live = sys < nsys;
+  const int s = live ? sys : nsys - 1;  // dead systems shadow a live one (barriers stay uniform)
+  const int ln = a.ln0 + s / a.B, b = s % a.B;
+  double *sh = shm[threadIdx.x / NT];
+  Tri<P, NT> tri;
+  tri.setup(a, a.fset[b], t, sh);
+  if (NW > 1) __syncthreads();
+  const float *u = a.U + ((size_t)ln * a.B + b) * a.Mp;
+  double x[P];
+#pragma unroll
+  for (int i = 0; i < P; ++i) {
+    const int j = t * P + i;
+    x[i] = (j < a.M) ? (double)u[j] : 0.0;
+  }
+  run_steps<P, NT>(tri, a, b, a.n_base + ln, t, x, sh);
+  if (!live) return;
+  const size_t row = ((size_t)ln * a.B + b) * a.Mp;
+  if (a.Fout) {
+    float *o = a.Fout + ((size_t)(ln - a.ln0) * a.B + b) * a.Mp;
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      const int j = t * P + i;
+      if (j < a.M) o[j] = (float)x[i];
+    }
+  } else if (ln == a.fk_ln) {
+    float *o = a.Fk + (size_t)b * a.Mp;
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      const int j = t * P + i;
+      if (j < a.M) o[j] = (float)x[i];
+    }
+  } else {
+    const float *gh = a.Gh + row;
+    float *d = a.D + row;
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      const int j = t * P + i;
+      if (j < a.M) d[j] = (float)(x[i] - (double)gh[j]);
+    }
+  }
+}
+
+// CHAIN: one system per instance walks slices c_ln0..c_ln1-1 serially (numerical coarse
+// G with the Parareal correction; or the serial fine solve, Eq. 6).
+template <int P, int NT, int SPB>
+__global__ void __launch_bounds__(NT * SPB) k_resident_chain(ResidentArgs a) {
+  constexpr int NW = NT / 32;
+  __shared__ double shm[SPB][4 * NW + 2];
+  __shared__ double red[SPB][2 * NW + 2];
+  const int sys = blockIdx.x * SPB + threadIdx.x / NT;
+  const int t = threadIdx.x % NT;
+  const bool live = sys < a.B;
+  const int b = live ? sys : a.B - 1;
+  double *sh = shm[threadIdx.x / NT];
+  double *rd = red[threadIdx.x / NT];
+  Tri<P, NT> tri;
+  tri.setup(a, a.fset[b], t, sh);
+  if (NW > 1) __syncthreads();
+  const size_t sstride = (size_t)a.B * a.Mp;
+  double x[P];
+  float *u0 = a.Uw + (size_t)a.c_ln0 * a.ustride + (size_t)b * a.Mp;
+  if (a.Fcopy) {
+    // U^k_k := F̂_{k−1} (reading Q12: copied, not recomputed) + δ partial of slice k
+    const float *f = a.Fcopy + (size_t)b * a.Mp;
+    double num = 0.0, den = 0.0;
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      const int j = t * P + i;
+      float nv = 0.f;
+      if (j < a.M) {
+        nv = f[j];
+        const double dd = (double)nv - (double)u0[j];
+        num += dd * dd;
+        den += (double)nv * nv;
+      }
+      x[i] = (double)nv;
+    }
+    sys_reduce2<NT>(num, den, t, rd);
+    if (live) {
+#pragma unroll
+      for (int i = 0; i < P; ++i) {
+        const int j = t * P + i;
+        if (j < a.M) u0[j] = (float)x[i];
+      }
+      if (a.partials && t == 0) {
+        double *pp = a.partials + (((size_t)a.c_ln0 * a.B + b) * a.nch) * 2;
+        pp[0] = num;
+        pp[1] = den;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      const int j = t * P + i;
+      x[i] = (j < a.M) ? (double)u0[j] : 0.0;
+    }
+  }
+#pragma unroll 1
+  for (int ln = a.c_ln0; ln < a.c_ln1; ++ln) {
+    run_steps<P, NT>(tri, a, b, a.n_base + ln, t, x, sh);
+    const size_t row = (size_t)ln * sstride + (size_t)b * a.Mp;
+    float *un = a.Uw + (size_t)(ln + 1) * a.ustride + (size_t)b * a.Mp;
+    double num = 0.0, den = 0.0;
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      const int j = t * P + i;
+      float nv = 0.f;
+      if (j < a.M) {
+        if (a.GhW && live) a.GhW[row + j] = (float)x[i];
+        nv = a.Dc ? (float)(x[i] + (double)a.Dc[row + j]) : (float)x[i];
+        if (a.partials) {
+          const double dd = (double)nv - (double)un[j];
+          num += dd * dd;
+          den += (double)nv * nv;
+        }
+      }
+      x[i] = (double)nv;  // continue from the stored fp32 value (same input the fine sweep sees)
+    }
+    if (a.partials) sys_reduce2<NT>(num, den, t, rd);
+    if (live) {
+#pragma unroll
+      for (int i = 0; i < P; ++i) {
+        const int j = t * P + i;
+        if (j < a.M) un[j] = (float)x[i];
+      }
+      if (a.partials && t == 0) {
+        double *pp = a.partials + (((size_t)(ln + 1) * a.B + b) * a.nch) * 2;
+        pp[0] = num;
+        pp[1] = den;
+      }
+    }
+  }
+}
+
+}  // namespace pr

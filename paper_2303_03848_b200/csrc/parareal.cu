@@ -1,0 +1,1175 @@
+// parareal.cu — host side of the C ABI (include/parareal.h): validation,
+// fp64 factorisation, workspace, the Parareal iteration (Eq. 7,
+// schedule reading Q12), NCCL hand-off of slice-boundary states between
+// ranks, reporting.  All device work is issued on one stream.
+#include "../../include/parareal.h"
+
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "fine_resident.cuh"
+#include "fine_streamed.cuh"
+#include "misc_kernels.cuh"
+#include "pinn_chain.cuh"
+
+// ============================================================================ NCCL (dlopen)
+// NCCL is resolved at run time so the library loads without it (world == 1 never touches
+// it).  Under torch the wheel's libnccl.so.2 is already mapped and dlopen returns it.
+namespace {
+typedef struct ncclComm *ncclComm_t;
+typedef struct { char internal[128]; } ncclUniqueId;
+typedef int ncclResult_t;
+enum { kNcclFloat32 = 7, kNcclFloat64 = 8, kNcclMax = 2 };
+
+struct Nccl {
+  bool tried = false, ok = false;
+  std::string why;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
+  ncclResult_t (*Send)(const void *, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void *, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void *, void *, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char *(*GetErrorString)(ncclResult_t) = nullptr;
+};
+std::mutex g_nccl_mu;
+Nccl g_nccl;
+
+Nccl &nccl() {
+  std::lock_guard<std::mutex> lk(g_nccl_mu);
+  if (g_nccl.tried) return g_nccl;
+  g_nccl.tried = true;
+  void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) {
+    g_nccl.why = std::string("dlopen(libnccl.so.2) failed: ") + dlerror();
+    return g_nccl;
+  }
+#define PR_SYM(field, name)                                          \
+  g_nccl.field = reinterpret_cast<decltype(g_nccl.field)>(dlsym(h, name)); \
+  if (!g_nccl.field) { g_nccl.why = "missing NCCL symbol " name; return g_nccl; }
+  PR_SYM(GetUniqueId, "ncclGetUniqueId");
+  PR_SYM(CommInitRank, "ncclCommInitRank");
+  PR_SYM(CommDestroy, "ncclCommDestroy");
+  PR_SYM(CommAbort, "ncclCommAbort");
+  PR_SYM(Send, "ncclSend");
+  PR_SYM(Recv, "ncclRecv");
+  PR_SYM(AllReduce, "ncclAllReduce");
+  PR_SYM(GroupStart, "ncclGroupStart");
+  PR_SYM(GroupEnd, "ncclGroupEnd");
+  PR_SYM(GetErrorString, "ncclGetErrorString");
+#undef PR_SYM
+  g_nccl.ok = true;
+  return g_nccl;
+}
+
+thread_local std::string g_init_error = "no error";
+
+std::string fmt(const char *f, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, f);
+  vsnprintf(buf, sizeof buf, f, ap);
+  va_end(ap);
+  return buf;
+}
+
+// fp64 LU factors of one implicit-Euler matrix  I − dτ A, per factor set.
+struct Scheme {
+  double dtau = 0;
+  int steps = 0;
+  double *m = nullptr, *ip = nullptr, *cu = nullptr;  // device [nsets][Mp]
+  double *bcoef = nullptr;                          // device [B]
+};
+
+constexpr int kResidentMaxM = 2048;
+constexpr int kPinnTPB = 128;
+}  // namespace
+
+// ============================================================================ context
+struct pr_ctx {
+  std::string err = "no error";
+  bool poisoned = false;
+  // problem
+  int M = 0, Mp = 0, B = 0, N = 0, nf = 0, nc = 0, coarse = 0, max_iter = 0, upper_bc = 0;
+  double T = 0, dT = 0, tol = 0;
+  std::vector<double> K, sig, r, L;
+  // placement
+  int rank = 0, world = 1, device = 0, n0 = 0, n1 = 0, Nloc = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  ncclComm_t comm = nullptr;
+  // constants on device
+  int nsets = 0;
+  int *d_fset = nullptr;
+  double *d_L = nullptr, *d_K = nullptr, *d_r = nullptr;
+  std::vector<int> fset;
+  std::vector<std::pair<double, double>> sets;  // (sigma, r)
+  Scheme fine, crs;
+  // workspace
+  void *ws = nullptr;
+  size_t ws_bytes = 0;
+  bool own_ws = false, ws_ready = false;
+  float *U = nullptr, *Gh = nullptr, *D = nullptr, *Fk = nullptr, *tmp = nullptr;
+  double *partials = nullptr;
+  unsigned long long *d_delta = nullptr;
+  int nch = 1;
+  double *h_delta = nullptr;  // pinned [max_iter]
+  // streamed-kernel state
+  pr::StreamedState sst;
+  // PINN
+  bool have_pinn = false;
+  int IN = 4, W = 0, LH = 0, act = 0, nfloats = 0;
+  float cs[4] = {1, 1, 1, 1}, out_scale = 1;
+  float *d_wts = nullptr;
+  // options
+  int opt_fine_kernel = 0;
+  int opt_graphs = 0;
+  int64_t launches = 0;
+  bool solved = false;
+  // timing
+  std::vector<cudaEvent_t> ev;
+  int ev_used = 0;
+};
+
+namespace {
+
+pr_status fail(pr_ctx *c, pr_status s, const std::string &msg) {
+  if (c) {
+    c->err = msg;
+    if (s == PR_ERR_CUDA || s == PR_ERR_NCCL) c->poisoned = true;
+  } else {
+    g_init_error = msg;
+  }
+  return s;
+}
+
+#define CU(call)                                                                              \
+  do {                                                                                        \
+    cudaError_t e_ = (call);                                                                  \
+    if (e_ != cudaSuccess)                                                                    \
+      return fail(c, e_ == cudaErrorMemoryAllocation ? PR_ERR_OUT_OF_MEMORY : PR_ERR_CUDA,    \
+                  fmt("%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__)); \
+  } while (0)
+
+#define NC(call)                                                                              \
+  do {                                                                                        \
+    ncclResult_t e_ = (call);                                                                 \
+    if (e_ != 0)                                                                              \
+      return fail(c, PR_ERR_NCCL, fmt("%s failed: %s", #call, nccl().GetErrorString(e_)));    \
+  } while (0)
+
+#define LAUNCHED()                                                                            \
+  do {                                                                                        \
+    c->launches++;                                                                            \
+    cudaError_t e_ = cudaGetLastError();                                                      \
+    if (e_ != cudaSuccess)                                                                    \
+      return fail(c, PR_ERR_CUDA, fmt("kernel launch failed: %s (%s:%d)", cudaGetErrorString(e_), \
+                                      __FILE__, __LINE__));                                   \
+  } while (0)
+
+pr_status check_ctx(pr_ctx *c) {
+  if (!c) return fail(nullptr, PR_ERR_INVALID_ARGUMENT, "ctx is NULL");
+  if (c->poisoned) return PR_ERR_STATE;
+  return PR_OK;
+}
+
+// Host fp64 factorisation of I − dτA for (σ, r): m_j, 1/p_j, u_j/p_j (Mp-padded).
+pr_status factorise(pr_ctx *c, double dtau, std::vector<double> &m, std::vector<double> &ip,
+                    std::vector<double> &cu) {
+  const int M = c->M, Mp = c->Mp;
+  m.assign((size_t)c->nsets * Mp, 0.0);
+  ip.assign((size_t)c->nsets * Mp, 1.0);
+  cu.assign((size_t)c->nsets * Mp, 0.0);
+  for (int s = 0; s < c->nsets; ++s) {
+    const double sg = c->sets[s].first, rr = c->sets[s].second;
+    double p_prev = 0, u_prev = 0;
+    for (int i = 0; i < M; ++i) {
+      const double j = i + 1;
+      const double a = 0.5 * sg * sg * j * j, b = 0.5 * rr * j;
+      const double d = 1.0 + dtau * (2.0 * a + rr);   // diagonal of I − dτA
+      const double l = -dtau * (a - b);               // sub-diagonal (coefficient of V_{j−1})
+      const double u = -dtau * (a + b);               // super-diagonal (coefficient of V_{j+1})
+      double mm = 0.0, p = d;
+      if (i > 0) {
+        mm = l / p_prev;
+        p = d - mm * u_prev;
+      }
+      if (!(p > 0.0))
+        return fail(c, PR_ERR_NUMERICAL, fmt("non-positive pivot %g at j=%d (sigma=%g r=%g dtau=%g)", p,
+                                             i + 1, sg, rr, dtau));
+      m[(size_t)s * Mp + i] = mm;
+      ip[(size_t)s * Mp + i] = 1.0 / p;
+      cu[(size_t)s * Mp + i] = (i < M - 1) ? u / p : 0.0;
+      p_prev = p;
+      u_prev = u;
+    }
+  }
+  return PR_OK;
+}
+
+pr_status upload_scheme(pr_ctx *c, Scheme &sc, int steps) {
+  sc.steps = steps;
+  sc.dtau = c->dT / steps;
+  std::vector<double> m, ip, cu;
+  pr_status st = factorise(c, sc.dtau, m, ip, cu);
+  if (st) return st;
+  const size_t n = m.size();
+  CU(cudaMalloc(&sc.m, n * sizeof(double)));
+  CU(cudaMalloc(&sc.ip, n * sizeof(double)));
+  CU(cudaMalloc(&sc.cu, n * sizeof(double)));
+  CU(cudaMemcpy(sc.m, m.data(), n * sizeof(double), cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(sc.ip, ip.data(), n * sizeof(double), cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(sc.cu, cu.data(), n * sizeof(double), cudaMemcpyHostToDevice));
+  std::vector<double> bc(c->B);
+  for (int b = 0; b < c->B; ++b) {
+    const double sg = c->sig[b], rr = c->r[b], j = c->M;
+    bc[b] = sc.dtau * (0.5 * sg * sg * j * j + 0.5 * rr * j);  // dτ (a_M + b_M)
+  }
+  CU(cudaMalloc(&sc.bcoef, c->B * sizeof(double)));
+  CU(cudaMemcpy(sc.bcoef, bc.data(), c->B * sizeof(double), cudaMemcpyHostToDevice));
+  return PR_OK;
+}
+
+void free_scheme(Scheme &s) {
+  cudaFree(s.m);
+  cudaFree(s.ip);
+  cudaFree(s.cu);
+  cudaFree(s.bcoef);
+  s = Scheme();
+}
+
+bool use_resident(const pr_ctx *c) {
+  if (c->opt_fine_kernel == 1) return true;
+  if (c->opt_fine_kernel == 2) return false;
+  return c->M <= kResidentMaxM;
+}
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+size_t layout(pr_ctx *c, char *base) {
+  // carve the workspace; returns total bytes.  base == nullptr → size only.
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    char *p = base ? base + off : nullptr;
+    off = align_up(off + bytes, 256);
+    return p;
+  };
+  const size_t row = (size_t)c->B * c->Mp;
+  c->U = (float *)take((size_t)(c->Nloc + 1) * row * sizeof(float));
+  c->Gh = (float *)take((size_t)std::max(c->Nloc, 1) * row * sizeof(float));
+  c->D = (float *)take((size_t)std::max(c->Nloc, 1) * row * sizeof(float));
+  c->Fk = (float *)take(row * sizeof(float));
+  c->tmp = (float *)take(2 * row * sizeof(float));
+  c->partials = (double *)take((size_t)(c->Nloc + 1) * c->B * c->nch * 2 * sizeof(double));
+  c->d_delta = (unsigned long long *)take((size_t)c->max_iter * sizeof(unsigned long long));
+  char *sb = take(pr::streamed_state_bytes(c->M, c->Mp, c->B, std::max(c->Nloc, 1)));
+  if (base) pr::streamed_state_bind(c->sst, sb, c->M, c->Mp, c->B, std::max(c->Nloc, 1));
+  return off;
+}
+
+pr_status ensure_ws(pr_ctx *c) {
+  if (c->ws_ready) return PR_OK;
+  const size_t need = layout(c, nullptr);
+  if (!c->ws) {
+    CU(cudaMalloc(&c->ws, need));
+    c->own_ws = true;
+    c->ws_bytes = need;
+  }
+  layout(c, (char *)c->ws);
+  CU(cudaMemsetAsync(c->ws, 0, need, c->stream));
+  c->ws_ready = true;
+  return PR_OK;
+}
+
+cudaEvent_t next_event(pr_ctx *c) {
+  if (c->ev_used >= (int)c->ev.size()) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+    c->ev.push_back(e);
+  }
+  return c->ev[c->ev_used++];
+}
+
+// ---------------------------------------------------------------- resident launches
+pr::ResidentArgs base_args(pr_ctx *c, const Scheme &sc) {
+  pr::ResidentArgs a;
+  std::memset(&a, 0, sizeof a);
+  a.M = c->M;
+  a.Mp = c->Mp;
+  a.B = c->B;
+  a.fm = sc.m;
+  a.fip = sc.ip;
+  a.fcu = sc.cu;
+  a.fset = c->d_fset;
+  a.bcoef = sc.bcoef;
+  a.Lb = c->d_L;
+  a.Kb = c->d_K;
+  a.rb = c->d_r;
+  a.upper_bc = c->upper_bc;
+  a.dT = c->dT;
+  a.dtau = sc.dtau;
+  a.steps = sc.steps;
+  a.n_base = c->n0;
+  a.fk_ln = -1;
+  a.nch = c->nch;
+  a.ustride = (size_t)c->B * c->Mp;
+  return a;
+}
+
+template <int P, int NT, int SPB>
+void launch_res(bool chain, const pr::ResidentArgs &a, int nsys, cudaStream_t s) {
+  const int grid = (nsys + SPB - 1) / SPB;
+  if (chain)
+    pr::k_resident_chain<P, NT, SPB><<<grid, NT * SPB, 0, s>>>(a);
+  else
+    pr::k_fine_sweep<P, NT, SPB><<<grid, NT * SPB, 0, s>>>(a);
+}
+
+void dispatch_res(bool chain, int M, const pr::ResidentArgs &a, int nsys, cudaStream_t s) {
+  if (M <= 64) launch_res<2, 32, 4>(chain, a, nsys, s);
+  else if (M <= 128) launch_res<4, 32, 4>(chain, a, nsys, s);
+  else if (M <= 256) launch_res<8, 32, 4>(chain, a, nsys, s);
+  else if (M <= 512) launch_res<8, 64, 2>(chain, a, nsys, s);
+  else if (M <= 1024) launch_res<8, 128, 1>(chain, a, nsys, s);
+  else launch_res<8, 256, 1>(chain, a, nsys, s);
+}
+
+// ---------------------------------------------------------------- PINN launches
+typedef void (*PinnKernel)(pr::PinnArgs);
+template <int IN, int ACT>
+PinnKernel pinn_kernel_w(int W) {
+  switch (W) {
+    case 8: return pr::k_pinn_chain<IN, 8, ACT, 2>;
+    case 16: return pr::k_pinn_chain<IN, 16, ACT, 2>;
+    case 20: return pr::k_pinn_chain<IN, 20, ACT, 2>;
+    case 32: return pr::k_pinn_chain<IN, 32, ACT, 2>;
+    case 50: return pr::k_pinn_chain<IN, 50, ACT, 1>;
+    case 64: return pr::k_pinn_chain<IN, 64, ACT, 1>;
+  }
+  return nullptr;
+}
+PinnKernel pinn_kernel(int IN, int W, int act) {
+  if (IN == 4) return act ? pinn_kernel_w<4, 1>(W) : pinn_kernel_w<4, 0>(W);
+  return act ? pinn_kernel_w<2, 1>(W) : pinn_kernel_w<2, 0>(W);
+}
+int pinn_pts(int W) { return W <= 32 ? 2 : 1; }
+
+pr::PinnArgs pinn_args(pr_ctx *c) {
+  pr::PinnArgs a;
+  std::memset(&a, 0, sizeof a);
+  a.M = c->M;
+  a.Mp = c->Mp;
+  a.B = c->B;
+  a.wts = c->d_wts;
+  a.nfloats = c->nfloats;
+  a.LH = c->LH;
+  a.cs0 = c->cs[0];
+  a.cs1 = c->cs[1];
+  a.cs2 = c->cs[2];
+  a.cs3 = c->cs[3];
+  a.out_scale = c->out_scale;
+  a.T = c->T;
+  a.dT = c->dT;
+  a.n_base = c->n0;
+  a.Lb = c->d_L;
+  a.nch = c->nch;
+  return a;
+}
+
+pr_status launch_pinn(pr_ctx *c, const pr::PinnArgs &a) {
+  PinnKernel k = pinn_kernel(c->IN, c->W, c->act);
+  if (!k) return fail(c, PR_ERR_UNSUPPORTED, "no PINN kernel for this width");
+  const int pts = pinn_pts(c->W);
+  dim3 grid((c->M + kPinnTPB * pts - 1) / (kPinnTPB * pts), c->B);
+  const size_t smem = (size_t)c->nfloats * sizeof(float);
+  k<<<grid, kPinnTPB, smem, c->stream>>>(a);
+  LAUNCHED();
+  return PR_OK;
+}
+
+int pinn_chunks(const pr_ctx *c, int W) {
+  const int pts = pinn_pts(W);
+  return (c->M + kPinnTPB * pts - 1) / (kPinnTPB * pts);
+}
+
+// ---------------------------------------------------------------- phases of one iteration
+// Fine sweep over local slices [ln_lo, Nloc) reading U^{k−1}: D_n = F̂_n − Ĝ_n, and
+// F̂ of local slice fk_ln (= k−1 when owned here) into Fk.
+pr_status fine_sweep(pr_ctx *c, int ln_lo, int fk_ln) {
+  const int nsl = c->Nloc - ln_lo;
+  if (nsl <= 0) return PR_OK;
+  if (use_resident(c)) {
+    pr::ResidentArgs a = base_args(c, c->fine);
+    a.ln0 = ln_lo;
+    a.nsl = nsl;
+    a.U = c->U;
+    a.Gh = c->Gh;
+    a.D = c->D;
+    a.Fk = c->Fk;
+    a.fk_ln = fk_ln;
+    dispatch_res(false, c->M, a, nsl * c->B, c->stream);
+    LAUNCHED();
+    return PR_OK;
+  }
+  pr::StreamedJob j;
+  j.U = c->U; j.Gh = c->Gh; j.D = c->D; j.Fk = c->Fk; j.fk_ln = fk_ln; j.Fout = nullptr;
+  j.ln0 = ln_lo; j.nsl = nsl; j.n_base = c->n0;
+  int nl = 0;
+  cudaError_t e = pr::streamed_sweep(c->sst, c->fine.m, c->fine.ip, c->fine.cu, c->d_fset, c->fine.bcoef,
+                                     c->d_L, c->d_K, c->d_r, c->upper_bc, c->dT, c->fine.dtau, c->fine.steps,
+                                     c->M, c->Mp, c->B, j, c->stream, &nl);
+  c->launches += nl;
+  if (e != cudaSuccess) return fail(c, PR_ERR_CUDA, fmt("streamed sweep: %s", cudaGetErrorString(e)));
+  return PR_OK;
+}
+
+// Coarse chain with correction over local slices [ln0, Nloc).  k == 0: no correction, no δ.
+pr_status coarse_chain(pr_ctx *c, int k, int ln0, bool copy) {
+  const bool corr = k > 0;
+  if (c->coarse == PR_COARSE_PINN) {
+    pr::PinnArgs a = pinn_args(c);
+    a.ln0 = ln0;
+    a.ln1 = c->Nloc;
+    a.U = c->U;
+    a.Gh = c->Gh;
+    a.D = corr ? c->D : nullptr;
+    a.Fcopy = copy ? c->Fk : nullptr;
+    a.partials = corr ? c->partials : nullptr;
+    if (ln0 >= c->Nloc && !copy) return PR_OK;
+    if (ln0 >= c->Nloc) {  // copy only (chain empty): still need U_k := F̂_{k−1} and its δ
+      a.ln1 = ln0;
+    }
+    return launch_pinn(c, a);
+  }
+  if (!use_resident(c)) {
+    pr::StreamedChainJob j;
+    j.U = c->U; j.Gh = c->Gh; j.D = corr ? c->D : nullptr; j.Fcopy = copy ? c->Fk : nullptr;
+    j.partials = corr ? c->partials : nullptr; j.nch = c->nch;
+    j.ln0 = ln0; j.ln1 = c->Nloc; j.n_base = c->n0; j.ustride = (size_t)c->B * c->Mp;
+    int nl = 0;
+    cudaError_t e = pr::streamed_chain(c->sst, c->crs.m, c->crs.ip, c->crs.cu, c->d_fset, c->crs.bcoef, c->d_L,
+                                       c->d_K, c->d_r, c->upper_bc, c->dT, c->crs.dtau, c->crs.steps, c->M,
+                                       c->Mp, c->B, j, c->stream, &nl);
+    c->launches += nl;
+    if (e != cudaSuccess) return fail(c, PR_ERR_CUDA, fmt("streamed chain: %s", cudaGetErrorString(e)));
+    return PR_OK;
+  }
+  pr::ResidentArgs a = base_args(c, c->crs);
+  a.Uw = c->U;
+  a.GhW = c->Gh;
+  a.Dc = corr ? c->D : nullptr;
+  a.Fcopy = copy ? c->Fk : nullptr;
+  a.c_ln0 = ln0;
+  a.c_ln1 = c->Nloc;
+  a.partials = corr ? c->partials : nullptr;
+  if (ln0 >= c->Nloc && !copy) return PR_OK;
+  dispatch_res(true, c->M, a, c->B, c->stream);
+  LAUNCHED();
+  return PR_OK;
+}
+
+pr_status delta_reduce(pr_ctx *c, int k, int ln_lo, int ln_hi, int nch) {
+  unsigned long long *slot = c->d_delta + (k - 1);
+  CU(cudaMemsetAsync(slot, 0, sizeof(unsigned long long), c->stream));
+  if (ln_hi >= ln_lo) {
+    const int total = (ln_hi - ln_lo + 1) * c->B;
+    pr::k_delta<<<(total + 255) / 256, 256, 0, c->stream>>>(c->partials, c->B, nch, ln_lo, ln_hi, slot);
+    LAUNCHED();
+  }
+  if (c->world > 1) {
+    NC(nccl().AllReduce(slot, slot, 1, kNcclFloat64, kNcclMax, c->comm, c->stream));
+  }
+  return PR_OK;
+}
+
+pr_status load_initial(pr_ctx *c, const float *V_T, bool device_ptr) {
+  const size_t row = (size_t)c->B * c->Mp;
+  if (V_T) {
+    if (c->Mp == c->M) {
+      CU(cudaMemcpyAsync(c->U, V_T, row * sizeof(float),
+                         device_ptr ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->stream));
+    } else {
+      CU(cudaMemcpy2DAsync(c->U, c->Mp * sizeof(float), V_T, c->M * sizeof(float), c->M * sizeof(float), c->B,
+                           device_ptr ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->stream));
+    }
+  } else {
+    dim3 grid((c->Mp + 255) / 256, c->B);
+    pr::k_payoff<<<grid, 256, 0, c->stream>>>(c->U, c->M, c->Mp, c->B, c->d_L, c->d_K);
+    LAUNCHED();
+  }
+  return PR_OK;
+}
+
+pr_status store_rows(pr_ctx *c, float *dst, const float *src, bool device_ptr) {
+  if (c->Mp == c->M) {
+    CU(cudaMemcpyAsync(dst, src, (size_t)c->B * c->M * sizeof(float),
+                       device_ptr ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->stream));
+  } else {
+    CU(cudaMemcpy2DAsync(dst, c->M * sizeof(float), src, c->Mp * sizeof(float), c->M * sizeof(float), c->B,
+                         device_ptr ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->stream));
+  }
+  return PR_OK;
+}
+
+struct PhaseTimer {
+  pr_ctx *c;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> spans;
+  cudaEvent_t a = nullptr;
+  int cur = -1;
+  void begin(int phase) {
+    a = next_event(c);
+    cur = phase;
+    if (a) cudaEventRecord(a, c->stream);
+  }
+  void end() {
+    cudaEvent_t b = next_event(c);
+    if (a && b) {
+      cudaEventRecord(b, c->stream);
+      spans.push_back({cur, {a, b}});
+    }
+  }
+};
+enum { PH_COARSE = 0, PH_FINE = 1, PH_COMM = 2, PH_SETUP = 3 };
+
+// The per-rank schedule of iteration k (include/parareal.h pr_plan).
+pr_plan make_plan(int N, int world, int rank, int k) {
+  const int per = N / world, n0 = rank * per, n1 = n0 + per;
+  pr_plan P;
+  std::memset(&P, 0, sizeof P);
+  P.fk_local = -1;
+  P.delta_lo = 1;
+  P.delta_hi = 0;
+  if (k == 0) {  // initial coarse sweep U_{n+1} = G(U_n)
+    P.recv_first = rank > 0;
+    P.chain_lo = 0;
+    P.chain_hi = per;
+    P.send_last = rank < world - 1;
+    return P;
+  }
+  // (i) fine sweep over active slices n = k−1..N−1 (frozen prefix n < k−1)
+  if (k - 1 < n1) {
+    P.fine_lo = std::max(0, k - 1 - n0);
+    P.fine_hi = per;
+    P.fk_local = (k - 1 >= n0) ? k - 1 - n0 : -1;
+  }
+  // (ii) coarse chain with correction starting at slice k
+  if (k - 1 >= n0 && k - 1 < n1) {         // this rank computed F̂_{k−1}: U_k := F̂_{k−1}
+    P.copy = 1;
+    P.chain_lo = k - n0;
+    P.chain_hi = per;
+    P.delta_lo = k - n0;
+    P.delta_hi = per;
+  } else if (n0 >= k && rank > 0) {         // U_{n0} arrives from rank−1's chain
+    P.recv_first = 1;
+    P.chain_lo = 0;
+    P.chain_hi = per;
+    P.delta_lo = 1;                         // U_{n0}'s δ is reduced by rank−1 (its U_{n1})
+    P.delta_hi = per;
+  }                                         // else: frozen rank, no chain
+  P.send_last = (n1 >= k) && rank < world - 1;
+  return P;
+}
+
+pr_status solve_impl(pr_ctx *c, const float *V_T, float *V_0, bool device_ptr, pr_report *rep) {
+  pr_status st = check_ctx(c);
+  if (st) return st;
+  if (c->coarse == PR_COARSE_PINN && !c->have_pinn)
+    return fail(c, PR_ERR_STATE, "coarse == PR_COARSE_PINN but no weights loaded (parareal_load_pinn_weights)");
+  if ((st = ensure_ws(c))) return st;
+  c->ev_used = 0;
+  const int64_t launches0 = c->launches;
+  PhaseTimer pt{c};
+  cudaEvent_t e0 = next_event(c), e1 = nullptr;
+  cudaEventRecord(e0, c->stream);
+  const int R = c->world, r = c->rank;
+  const size_t row = (size_t)c->B * c->Mp;
+  // δ partials are rewritten slice by slice; clear stale chunks of earlier solves
+  CU(cudaMemsetAsync(c->partials, 0, (size_t)(c->Nloc + 1) * c->B * c->nch * 2 * sizeof(double), c->stream));
+  // ---- k = 0: U_0 and the initial coarse sweep U_{n+1} = G(U_n)
+  pt.begin(PH_SETUP);
+  if (r == 0 && (st = load_initial(c, V_T, device_ptr))) return st;
+  pt.end();
+  {
+    const pr_plan P0 = make_plan(c->N, R, r, 0);
+    if (P0.recv_first) {
+      pt.begin(PH_COMM);
+      NC(nccl().Recv(c->U, row, kNcclFloat32, r - 1, c->comm, c->stream));
+      pt.end();
+    }
+    pt.begin(PH_COARSE);
+    if ((st = coarse_chain(c, 0, P0.chain_lo, false))) return st;
+    pt.end();
+    if (P0.send_last) {
+      pt.begin(PH_COMM);
+      NC(nccl().Send(c->U + (size_t)c->Nloc * row, row, kNcclFloat32, r + 1, c->comm, c->stream));
+      pt.end();
+    }
+  }
+  int K = 0, conv = 0;
+  for (int k = 1; k <= c->max_iter; ++k) {
+    const pr_plan P = make_plan(c->N, R, r, k);
+    // (i) fine sweep F̂_n = F(U^{k−1}_n), n = k−1..N−1 (parallel across slices)
+    pt.begin(PH_FINE);
+    if (P.fine_hi > P.fine_lo && (st = fine_sweep(c, P.fine_lo, P.fk_local))) return st;
+    pt.end();
+    // (ii) coarse chain with correction, serial in n across ranks
+    if (P.recv_first) {
+      pt.begin(PH_COMM);
+      NC(nccl().Recv(c->U, row, kNcclFloat32, r - 1, c->comm, c->stream));
+      pt.end();
+    }
+    if (P.copy || P.recv_first) {
+      pt.begin(PH_COARSE);
+      if ((st = coarse_chain(c, k, P.chain_lo, P.copy != 0))) return st;
+      pt.end();
+    }
+    if (P.send_last) {
+      pt.begin(PH_COMM);
+      NC(nccl().Send(c->U + (size_t)c->Nloc * row, row, kNcclFloat32, r + 1, c->comm, c->stream));
+      pt.end();
+    }
+    const int dlo = P.delta_lo, dhi = P.delta_hi;
+    // (iii) δ^k and the stop rule (Q13)
+    if ((st = delta_reduce(c, k, dlo, dhi, c->nch))) return st;
+    K = k;
+    if (c->tol > 0.0) {
+      CU(cudaMemcpyAsync(c->h_delta + (k - 1), c->d_delta + (k - 1), sizeof(double), cudaMemcpyDeviceToHost,
+                         c->stream));
+      CU(cudaStreamSynchronize(c->stream));
+      if (c->h_delta[k - 1] < c->tol) {
+        conv = 1;
+        break;
+      }
+    }
+  }
+  // final state U^K_N: last rank → rank 0 (→ V_0)
+  if (R > 1) {
+    pt.begin(PH_COMM);
+    if (r == R - 1) NC(nccl().Send(c->U + (size_t)c->Nloc * row, row, kNcclFloat32, 0, c->comm, c->stream));
+    if (r == 0) NC(nccl().Recv(c->tmp, row, kNcclFloat32, R - 1, c->comm, c->stream));
+    pt.end();
+  }
+  if (r == 0 && V_0) {
+    const float *src = (R > 1) ? c->tmp : c->U + (size_t)c->Nloc * row;
+    if ((st = store_rows(c, V_0, src, device_ptr))) return st;
+  }
+  e1 = next_event(c);
+  cudaEventRecord(e1, c->stream);
+  CU(cudaMemcpyAsync(c->h_delta, c->d_delta, K * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
+  c->solved = true;
+  if (rep) {
+    rep->iterations = K;
+    rep->converged = (c->tol > 0.0 && K > 0 && c->h_delta[K - 1] < c->tol) ? 1 : conv;
+    if (rep->delta)
+      for (int i = 0; i < K; ++i) rep->delta[i] = c->h_delta[i];
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    rep->ms_total = ms;
+    double ph[4] = {0, 0, 0, 0};
+    for (auto &s : pt.spans) {
+      float m = 0;
+      cudaEventElapsedTime(&m, s.second.first, s.second.second);
+      ph[s.first] += m;
+    }
+    rep->ms_coarse = ph[PH_COARSE];
+    rep->ms_fine = ph[PH_FINE];
+    rep->ms_comm = ph[PH_COMM];
+    rep->ms_setup = ph[PH_SETUP];
+    rep->kernel_launches = c->launches - launches0;
+  }
+  return PR_OK;
+}
+
+pr_status serial_fine_impl(pr_ctx *c, const float *V_T, float *V_0, bool device_ptr, double *ms) {
+  pr_status st = check_ctx(c);
+  if (st) return st;
+  if ((st = ensure_ws(c))) return st;
+  c->ev_used = 0;
+  cudaEvent_t e0 = next_event(c), e1 = next_event(c);
+  cudaEventRecord(e0, c->stream);
+  // initial state into tmp row 0
+  float *save = c->U;
+  c->U = c->tmp;
+  st = load_initial(c, V_T, device_ptr);
+  c->U = save;
+  if (st) return st;
+  if (use_resident(c)) {
+    pr::ResidentArgs a = base_args(c, c->fine);
+    a.n_base = 0;
+    a.Uw = c->tmp;
+    a.ustride = 0;  // one row, updated in place slice after slice
+    a.c_ln0 = 0;
+    a.c_ln1 = c->N;
+    dispatch_res(true, c->M, a, c->B, c->stream);
+    LAUNCHED();
+  } else {
+    pr::StreamedChainJob j;
+    j.U = c->tmp; j.Gh = nullptr; j.D = nullptr; j.Fcopy = nullptr; j.partials = nullptr; j.nch = 1;
+    j.ln0 = 0; j.ln1 = c->N; j.n_base = 0; j.ustride = 0;
+    int nl = 0;
+    cudaError_t e = pr::streamed_chain(c->sst, c->fine.m, c->fine.ip, c->fine.cu, c->d_fset, c->fine.bcoef,
+                                       c->d_L, c->d_K, c->d_r, c->upper_bc, c->dT, c->fine.dtau, c->fine.steps,
+                                       c->M, c->Mp, c->B, j, c->stream, &nl);
+    c->launches += nl;
+    if (e != cudaSuccess) return fail(c, PR_ERR_CUDA, fmt("streamed serial fine: %s", cudaGetErrorString(e)));
+  }
+  cudaEventRecord(e1, c->stream);
+  if (V_0 && (st = store_rows(c, V_0, c->tmp, device_ptr))) return st;
+  CU(cudaStreamSynchronize(c->stream));
+  if (ms) {
+    float m = 0;
+    cudaEventElapsedTime(&m, e0, e1);
+    *ms = m;
+  }
+  return PR_OK;
+}
+
+}  // namespace
+
+// ============================================================================ ABI
+extern "C" {
+
+const char *parareal_status_string(pr_status s) {
+  switch (s) {
+    case PR_OK: return "PR_OK";
+    case PR_ERR_INVALID_ARGUMENT: return "PR_ERR_INVALID_ARGUMENT";
+    case PR_ERR_OUT_OF_MEMORY: return "PR_ERR_OUT_OF_MEMORY";
+    case PR_ERR_CUDA: return "PR_ERR_CUDA";
+    case PR_ERR_NCCL: return "PR_ERR_NCCL";
+    case PR_ERR_STATE: return "PR_ERR_STATE";
+    case PR_ERR_NUMERICAL: return "PR_ERR_NUMERICAL";
+    case PR_ERR_UNSUPPORTED: return "PR_ERR_UNSUPPORTED";
+  }
+  return "unknown pr_status";
+}
+
+const char *parareal_last_error(const pr_ctx *ctx) { return ctx ? ctx->err.c_str() : g_init_error.c_str(); }
+
+pr_status parareal_get_nccl_id(uint8_t out[128]) {
+  pr_ctx *c = nullptr;
+  if (!out) return fail(c, PR_ERR_INVALID_ARGUMENT, "out is NULL");
+  Nccl &n = nccl();
+  if (!n.ok) return fail(c, PR_ERR_NCCL, n.why);
+  ncclUniqueId id;
+  NC(n.GetUniqueId(&id));
+  std::memcpy(out, id.internal, 128);
+  return PR_OK;
+}
+
+pr_status parareal_init(const pr_problem *p, const pr_dist *dist, pr_ctx **out) {
+  pr_ctx *c = nullptr;
+  if (!out) return fail(c, PR_ERR_INVALID_ARGUMENT, "out is NULL");
+  *out = nullptr;
+  if (!p) return fail(c, PR_ERR_INVALID_ARGUMENT, "problem is NULL");
+  if (p->struct_size != sizeof(pr_problem))
+    return fail(c, PR_ERR_INVALID_ARGUMENT, fmt("problem.struct_size=%u, expected %zu (ABI mismatch)", p->struct_size,
+                                                sizeof(pr_problem)));
+  if (p->M < 1) return fail(c, PR_ERR_INVALID_ARGUMENT, fmt("problem.M=%d must be >= 1", p->M));
+  if (p->B < 1) return fail(c, PR_ERR_INVALID_ARGUMENT, fmt("problem.B=%d must be >= 1", p->B));
+  if (!p->strike || !p->sigma || !p->rate || !p->L)
+    return fail(c, PR_ERR_INVALID_ARGUMENT, "problem.strike/sigma/rate/L must be non-NULL [B] arrays");
+  for (int b = 0; b < p->B; ++b) {
+    if (!(p->sigma[b] > 0)) return fail(c, PR_ERR_INVALID_ARGUMENT, fmt("problem.sigma[%d]=%g must be > 0", b, p->sigma[b]));
+    if (!(p->rate[b] >= 0)) return fail(c, PR_ERR_INVALID_ARGUMENT, fmt("problem.rate[%d]=%g must be >= 0", b, p->rate[b]));
+    if (!(p->strike[b] >= 0)) return fail(c, PR_ERR_INVALID_ARGUMENT, fmt("problem.strike[%d]=%g must be >= 0", b, p->strike[b]));
+    if (!(p->L[b] > p->strike[b]))
+      return fail(c, PR_ERR_INVALID_ARGUMENT, fmt("problem.L[%d]=%g must exceed strike %g", b, p->L[b], p->strike[b]));
+  }
+  if (!(p->T > 0)) return fail(c, PR_ERR_INVALID_ARGUMENT, fmt("problem.T=%g must be > 0", p->T));
+  if (p->upper_bc != PR_BC_CALL_ASYMPTOTIC && p->upper_bc != PR_BC_ZERO)
+    return fail(c, PR_ERR_INVALID_ARGUMENT, fmt("problem.upper_bc=%d unknown", p->upper_bc));
+  if (p->N < 1) return fail(c, PR_ERR_INVALID_ARGUMENT, fmt("problem.N=%d must be >= 1", p->N));
+  if (p->fine_steps < 1) return fail(c, PR_ERR_INVALID_ARGUMENT, fmt("problem.fine_steps=%d must be >= 1", p->fine_steps));
+  if (p->coarse != PR_COARSE_PINN && p->coarse != PR_COARSE_IMPLICIT_EULER)
+    return fail(c, PR_ERR_INVALID_ARGUMENT, fmt("problem.coarse=%d unknown", p->coarse));
+  if (p->coarse == PR_COARSE_IMPLICIT_EULER && p->coarse_steps < 1)
+    return fail(c, PR_ERR_INVALID_ARGUMENT, fmt("problem.coarse_steps=%d must be >= 1", p->coarse_steps));
+  if (p->max_iter < 1 || p->max_iter > p->N)
+    return fail(c, PR_ERR_INVALID_ARGUMENT, fmt("problem.max_iter=%d must be in [1, N=%d]", p->max_iter, p->N));
+  if (!(p->tol >= 0)) return fail(c, PR_ERR_INVALID_ARGUMENT, fmt("problem.tol=%g must be >= 0", p->tol));
+  if (p->fine_theta != 1.0)
+    return fail(c, PR_ERR_UNSUPPORTED, fmt("problem.fine_theta=%g: only implicit Euler (1.0) is implemented", p->fine_theta));
+  pr_dist dd = {0, 1, 0, nullptr, nullptr};
+  if (dist) dd = *dist;
+  if (dd.world < 1 || dd.rank < 0 || dd.rank >= dd.world)
+    return fail(c, PR_ERR_INVALID_ARGUMENT, fmt("dist.rank=%d/world=%d invalid", dd.rank, dd.world));
+  if (p->N % dd.world)
+    return fail(c, PR_ERR_INVALID_ARGUMENT, fmt("problem.N=%d must be divisible by dist.world=%d", p->N, dd.world));
+  if (dd.world > 1 && !dd.nccl_id) return fail(c, PR_ERR_INVALID_ARGUMENT, "dist.nccl_id is NULL with world > 1");
+  if ((size_t)p->M * p->B > (size_t)1 << 31)
+    return fail(c, PR_ERR_UNSUPPORTED, "M*B above 2^31 points per slice");
+
+  c = new pr_ctx();
+  pr_status st = PR_OK;
+  auto bail = [&](pr_status s) {
+    g_init_error = c->err;
+    parareal_free(c);
+    return s;
+  };
+  c->M = p->M;
+  c->Mp = (p->M + 31) / 32 * 32;
+  c->B = p->B;
+  c->N = p->N;
+  c->nf = p->fine_steps;
+  c->nc = p->coarse_steps;
+  c->coarse = p->coarse;
+  c->max_iter = p->max_iter;
+  c->upper_bc = p->upper_bc;
+  c->T = p->T;
+  c->dT = p->T / p->N;
+  c->tol = p->tol;
+  c->K.assign(p->strike, p->strike + p->B);
+  c->sig.assign(p->sigma, p->sigma + p->B);
+  c->r.assign(p->rate, p->rate + p->B);
+  c->L.assign(p->L, p->L + p->B);
+  c->rank = dd.rank;
+  c->world = dd.world;
+  c->device = dd.device;
+  const int per = p->N / dd.world;
+  c->n0 = dd.rank * per;
+  c->n1 = c->n0 + per;
+  c->Nloc = per;
+  {
+    cudaError_t e = cudaSetDevice(dd.device);
+    if (e != cudaSuccess) {
+      c->err = fmt("cudaSetDevice(%d): %s", dd.device, cudaGetErrorString(e));
+      return bail(PR_ERR_CUDA);
+    }
+  }
+  if (dd.stream) {
+    c->stream = (cudaStream_t)dd.stream;
+  } else {
+    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+      c->err = "cudaStreamCreate failed";
+      return bail(PR_ERR_CUDA);
+    }
+    c->own_stream = true;
+  }
+  // distinct (σ, r) factor sets: the operator does not depend on K or L (a_j, b_j of P:156)
+  std::map<std::pair<double, double>, int> idx;
+  for (int b = 0; b < c->B; ++b) {
+    auto key = std::make_pair(c->sig[b], c->r[b]);
+    auto it = idx.find(key);
+    if (it == idx.end()) {
+      it = idx.emplace(key, (int)c->sets.size()).first;
+      c->sets.push_back(key);
+    }
+    c->fset.push_back(it->second);
+  }
+  c->nsets = (int)c->sets.size();
+  {
+    auto up = [&](void **d, const void *h, size_t n) { return cudaMalloc(d, n) == cudaSuccess && cudaMemcpy(*d, h, n, cudaMemcpyHostToDevice) == cudaSuccess; };
+    if (!up((void **)&c->d_fset, c->fset.data(), c->B * sizeof(int)) ||
+        !up((void **)&c->d_L, c->L.data(), c->B * sizeof(double)) ||
+        !up((void **)&c->d_K, c->K.data(), c->B * sizeof(double)) ||
+        !up((void **)&c->d_r, c->r.data(), c->B * sizeof(double))) {
+      c->err = "allocating/uploading instance parameters failed";
+      return bail(PR_ERR_OUT_OF_MEMORY);
+    }
+  }
+  if ((st = upload_scheme(c, c->fine, c->nf))) return bail(st);
+  if (c->coarse == PR_COARSE_IMPLICIT_EULER && (st = upload_scheme(c, c->crs, c->nc))) return bail(st);
+  if (cudaMallocHost(&c->h_delta, std::max(c->max_iter, 1) * sizeof(double)) != cudaSuccess) {
+    c->err = "cudaMallocHost(delta) failed";
+    return bail(PR_ERR_OUT_OF_MEMORY);
+  }
+  // δ partial chunks per (slice, instance): upper bound over every producer (PINN CTAs with one
+  // point per thread, 256-wide copy blocks, streamed tiles, one resident system)
+  c->nch = std::max(1, (c->M + kPinnTPB - 1) / kPinnTPB);
+  if (dd.world > 1) {
+    Nccl &n = nccl();
+    if (!n.ok) {
+      c->err = n.why;
+      return bail(PR_ERR_NCCL);
+    }
+    ncclUniqueId id;
+    std::memcpy(id.internal, dd.nccl_id, 128);
+    ncclResult_t e = n.CommInitRank(&c->comm, dd.world, id, dd.rank);
+    if (e != 0) {
+      c->err = fmt("ncclCommInitRank: %s", n.GetErrorString(e));
+      c->comm = nullptr;
+      return bail(PR_ERR_NCCL);
+    }
+  }
+  *out = c;
+  return PR_OK;
+}
+
+pr_status parareal_workspace_bytes(const pr_ctx *ctx, size_t *bytes) {
+  pr_ctx *c = const_cast<pr_ctx *>(ctx);
+  pr_status st = check_ctx(c);
+  if (st) return st;
+  if (!bytes) return fail(c, PR_ERR_INVALID_ARGUMENT, "bytes is NULL");
+  pr_ctx tmp_view = *c;  // layout() only writes pointer fields of the copy
+  *bytes = layout(&tmp_view, nullptr);
+  return PR_OK;
+}
+
+pr_status parareal_bind_workspace(pr_ctx *c, void *ptr, size_t bytes) {
+  pr_status st = check_ctx(c);
+  if (st) return st;
+  if (c->ws_ready) return fail(c, PR_ERR_STATE, "workspace already in use (bind before the first solve)");
+  if (!ptr || ((uintptr_t)ptr % 256)) return fail(c, PR_ERR_INVALID_ARGUMENT, "device_ptr is NULL or not 256-B aligned");
+  pr_ctx tmp_view = *c;
+  const size_t need = layout(&tmp_view, nullptr);
+  if (bytes < need) return fail(c, PR_ERR_INVALID_ARGUMENT, fmt("workspace of %zu bytes < required %zu", bytes, need));
+  c->ws = ptr;
+  c->ws_bytes = bytes;
+  c->own_ws = false;
+  return PR_OK;
+}
+
+pr_status parareal_load_pinn_weights(pr_ctx *c, int32_t n_linear, const int32_t *dims, const float *const *W,
+                                     const float *const *b, int32_t activation, const float *in_scale,
+                                     float out_scale, int32_t precision) {
+  pr_status st = check_ctx(c);
+  if (st) return st;
+  if (n_linear < 2) return fail(c, PR_ERR_INVALID_ARGUMENT, fmt("n_linear=%d must be >= 2 (at least one hidden layer)", n_linear));
+  if (!dims || !W || !b) return fail(c, PR_ERR_INVALID_ARGUMENT, "dims/W/b must be non-NULL");
+  if (dims[0] != 2 && dims[0] != 4) return fail(c, PR_ERR_INVALID_ARGUMENT, fmt("dims[0]=%d must be 2 or 4", dims[0]));
+  if (dims[n_linear] != 1) return fail(c, PR_ERR_INVALID_ARGUMENT, fmt("dims[%d]=%d must be 1", n_linear, dims[n_linear]));
+  const int Wd = dims[1];
+  for (int l = 1; l < n_linear; ++l)
+    if (dims[l] != Wd) return fail(c, PR_ERR_UNSUPPORTED, fmt("dims[%d]=%d: hidden widths must all equal dims[1]=%d", l, dims[l], Wd));
+  if (activation != PR_ACT_TANH && activation != PR_ACT_RELU)
+    return fail(c, PR_ERR_INVALID_ARGUMENT, fmt("activation=%d unknown", activation));
+  if (precision != PR_PREC_FP32) {
+    if (precision < 0 || precision > PR_PREC_TF32_TC) return fail(c, PR_ERR_INVALID_ARGUMENT, fmt("precision=%d unknown", precision));
+    return fail(c, PR_ERR_UNSUPPORTED, "tensor-core PINN precisions are not in this build");
+  }
+  if (!pinn_kernel(dims[0], Wd, activation))
+    return fail(c, PR_ERR_UNSUPPORTED, fmt("hidden width %d not instantiated (8,16,20,32,50,64)", Wd));
+  for (int l = 0; l < n_linear; ++l)
+    if (!W[l] || !b[l]) return fail(c, PR_ERR_INVALID_ARGUMENT, fmt("W[%d]/b[%d] is NULL", l, l));
+  const int IN = dims[0], LH = n_linear - 1;
+  std::vector<float> pk;
+  for (int l = 0; l < n_linear; ++l) {
+    pk.insert(pk.end(), W[l], W[l] + (size_t)dims[l + 1] * dims[l]);
+    pk.insert(pk.end(), b[l], b[l] + dims[l + 1]);
+  }
+  const size_t bytes = pk.size() * sizeof(float);
+  if (bytes > 200 * 1024) return fail(c, PR_ERR_UNSUPPORTED, fmt("network of %zu bytes exceeds the shared-memory budget", bytes));
+  PinnKernel k = pinn_kernel(IN, Wd, activation);
+  CU(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  if (c->d_wts) cudaFree(c->d_wts);
+  c->d_wts = nullptr;
+  CU(cudaMalloc(&c->d_wts, bytes));
+  CU(cudaMemcpy(c->d_wts, pk.data(), bytes, cudaMemcpyHostToDevice));
+  c->IN = IN;
+  c->W = Wd;
+  c->LH = LH;
+  c->act = activation;
+  c->nfloats = (int)pk.size();
+  for (int i = 0; i < 4; ++i) c->cs[i] = 1.f;
+  if (in_scale)
+    for (int i = 0; i < IN; ++i) c->cs[i] = in_scale[i];
+  c->out_scale = out_scale;
+  c->have_pinn = true;
+  return PR_OK;
+}
+
+pr_status parareal_solve(pr_ctx *c, const float *V_T, float *V_0, pr_report *rep) {
+  pr_status st = check_ctx(c);
+  if (st) return st;
+  if (c->rank == 0 && !V_0) return fail(c, PR_ERR_INVALID_ARGUMENT, "V_0 is NULL on rank 0");
+  return solve_impl(c, V_T, V_0, false, rep);
+}
+
+pr_status parareal_solve_device(pr_ctx *c, const float *d_V_T, float *d_V_0, pr_report *rep) {
+  pr_status st = check_ctx(c);
+  if (st) return st;
+  return solve_impl(c, d_V_T, d_V_0, true, rep);
+}
+
+pr_status parareal_serial_fine(pr_ctx *c, const float *V_T, float *V_0, double *ms) {
+  pr_status st = check_ctx(c);
+  if (st) return st;
+  return serial_fine_impl(c, V_T, V_0, false, ms);
+}
+
+pr_status parareal_serial_fine_device(pr_ctx *c, const float *d_V_T, float *d_V_0, double *ms) {
+  pr_status st = check_ctx(c);
+  if (st) return st;
+  return serial_fine_impl(c, d_V_T, d_V_0, true, ms);
+}
+
+pr_status parareal_initial_state(pr_ctx *c, float *V_T) {
+  pr_status st = check_ctx(c);
+  if (st) return st;
+  if (!V_T) return fail(c, PR_ERR_INVALID_ARGUMENT, "V_T is NULL");
+  if ((st = ensure_ws(c))) return st;
+  float *save = c->U;
+  c->U = c->tmp;
+  st = load_initial(c, nullptr, false);
+  c->U = save;
+  if (st) return st;
+  if ((st = store_rows(c, V_T, c->tmp, false))) return st;
+  CU(cudaStreamSynchronize(c->stream));
+  return PR_OK;
+}
+
+pr_status parareal_apply_fine(pr_ctx *c, int32_t n, const float *U_in, float *U_out) {
+  pr_status st = check_ctx(c);
+  if (st) return st;
+  if (n < 0 || n >= c->N) return fail(c, PR_ERR_INVALID_ARGUMENT, fmt("n=%d outside [0, N=%d)", n, c->N));
+  if (!U_in || !U_out) return fail(c, PR_ERR_INVALID_ARGUMENT, "U_in/U_out is NULL");
+  if ((st = ensure_ws(c))) return st;
+  float *save = c->U;
+  c->U = c->tmp;
+  st = load_initial(c, U_in, false);
+  c->U = save;
+  if (st) return st;
+  const size_t row = (size_t)c->B * c->Mp;
+  if (use_resident(c)) {
+    pr::ResidentArgs a = base_args(c, c->fine);
+    a.n_base = n;
+    a.ln0 = 0;
+    a.nsl = 1;
+    a.U = c->tmp;
+    a.Fout = c->tmp + row;
+    dispatch_res(false, c->M, a, c->B, c->stream);
+    LAUNCHED();
+  } else {
+    pr::StreamedJob j;
+    j.U = c->tmp; j.Gh = nullptr; j.D = nullptr; j.Fk = nullptr; j.fk_ln = -1; j.Fout = c->tmp + row;
+    j.ln0 = 0; j.nsl = 1; j.n_base = n;
+    int nl = 0;
+    cudaError_t e = pr::streamed_sweep(c->sst, c->fine.m, c->fine.ip, c->fine.cu, c->d_fset, c->fine.bcoef,
+                                       c->d_L, c->d_K, c->d_r, c->upper_bc, c->dT, c->fine.dtau, c->fine.steps,
+                                       c->M, c->Mp, c->B, j, c->stream, &nl);
+    c->launches += nl;
+    if (e != cudaSuccess) return fail(c, PR_ERR_CUDA, fmt("streamed apply: %s", cudaGetErrorString(e)));
+  }
+  if ((st = store_rows(c, U_out, c->tmp + row, false))) return st;
+  CU(cudaStreamSynchronize(c->stream));
+  return PR_OK;
+}
+
+pr_status parareal_apply_coarse(pr_ctx *c, int32_t n, const float *U_in, float *U_out) {
+  pr_status st = check_ctx(c);
+  if (st) return st;
+  if (n < 0 || n >= c->N) return fail(c, PR_ERR_INVALID_ARGUMENT, fmt("n=%d outside [0, N=%d)", n, c->N));
+  if (!U_in || !U_out) return fail(c, PR_ERR_INVALID_ARGUMENT, "U_in/U_out is NULL");
+  if (c->coarse == PR_COARSE_PINN && !c->have_pinn) return fail(c, PR_ERR_STATE, "no PINN weights loaded");
+  if ((st = ensure_ws(c))) return st;
+  float *save = c->U;
+  c->U = c->tmp;
+  st = load_initial(c, U_in, false);
+  c->U = save;
+  if (st) return st;
+  const size_t row = (size_t)c->B * c->Mp;
+  if (c->coarse == PR_COARSE_PINN) {
+    pr::PinnArgs a = pinn_args(c);
+    a.n_base = n;
+    a.ln0 = 0;
+    a.ln1 = 1;
+    a.U = c->tmp;
+    a.Gout = c->tmp + row;
+    if ((st = launch_pinn(c, a))) return st;
+    if ((st = store_rows(c, U_out, c->tmp + row, false))) return st;
+  } else if (use_resident(c)) {
+    pr::ResidentArgs a = base_args(c, c->crs);
+    a.n_base = n;
+    a.Uw = c->tmp;
+    a.ustride = 0;
+    a.c_ln0 = 0;
+    a.c_ln1 = 1;
+    dispatch_res(true, c->M, a, c->B, c->stream);
+    LAUNCHED();
+    if ((st = store_rows(c, U_out, c->tmp, false))) return st;
+  } else {
+    pr::StreamedChainJob j;
+    j.U = c->tmp; j.Gh = nullptr; j.D = nullptr; j.Fcopy = nullptr; j.partials = nullptr; j.nch = 1;
+    j.ln0 = 0; j.ln1 = 1; j.n_base = n; j.ustride = 0;
+    int nl = 0;
+    cudaError_t e = pr::streamed_chain(c->sst, c->crs.m, c->crs.ip, c->crs.cu, c->d_fset, c->crs.bcoef, c->d_L,
+                                       c->d_K, c->d_r, c->upper_bc, c->dT, c->crs.dtau, c->crs.steps, c->M, c->Mp,
+                                       c->B, j, c->stream, &nl);
+    c->launches += nl;
+    if (e != cudaSuccess) return fail(c, PR_ERR_CUDA, fmt("streamed coarse apply: %s", cudaGetErrorString(e)));
+    if ((st = store_rows(c, U_out, c->tmp, false))) return st;
+  }
+  CU(cudaStreamSynchronize(c->stream));
+  return PR_OK;
+}
+
+pr_status parareal_copy_iterates(pr_ctx *c, int32_t n_first, int32_t n_count, float *host) {
+  pr_status st = check_ctx(c);
+  if (st) return st;
+  if (!c->solved) return fail(c, PR_ERR_STATE, "no solve has run on this context");
+  if (!host || n_count < 0 || n_first < c->n0 || n_first + n_count > c->n1 + 1)
+    return fail(c, PR_ERR_INVALID_ARGUMENT, fmt("[n_first=%d, +%d) not within this rank's [%d, %d]", n_first, n_count,
+                                                c->n0, c->n1));
+  const size_t row = (size_t)c->B * c->Mp;
+  for (int i = 0; i < n_count; ++i) {
+    if ((st = store_rows(c, host + (size_t)i * c->B * c->M, c->U + (size_t)(n_first - c->n0 + i) * row, false)))
+      return st;
+  }
+  CU(cudaStreamSynchronize(c->stream));
+  return PR_OK;
+}
+
+pr_status parareal_plan_iteration(int32_t N, int32_t world, int32_t rank, int32_t k, pr_plan *out) {
+  pr_ctx *c = nullptr;
+  if (!out) return fail(c, PR_ERR_INVALID_ARGUMENT, "out is NULL");
+  if (N < 1 || world < 1 || N % world || rank < 0 || rank >= world || k < 0)
+    return fail(c, PR_ERR_INVALID_ARGUMENT, fmt("plan(N=%d, world=%d, rank=%d, k=%d) invalid", N, world, rank, k));
+  *out = make_plan(N, world, rank, k);
+  return PR_OK;
+}
+
+pr_status parareal_set_option(pr_ctx *c, int32_t key, int64_t value) {
+  pr_status st = check_ctx(c);
+  if (st) return st;
+  switch (key) {
+    case PR_OPT_FINE_KERNEL:
+      if (value < 0 || value > 2) return fail(c, PR_ERR_INVALID_ARGUMENT, "PR_OPT_FINE_KERNEL must be 0, 1 or 2");
+      if (value == 1 && c->M > kResidentMaxM)
+        return fail(c, PR_ERR_UNSUPPORTED, fmt("resident fine kernel needs M <= %d", kResidentMaxM));
+      c->opt_fine_kernel = (int)value;
+      return PR_OK;
+    case PR_OPT_USE_GRAPHS:
+      if (value < 0 || value > 1) return fail(c, PR_ERR_INVALID_ARGUMENT, "PR_OPT_USE_GRAPHS must be 0 or 1");
+      c->opt_graphs = (int)value;
+      return PR_OK;
+  }
+  return fail(c, PR_ERR_INVALID_ARGUMENT, fmt("unknown option key %d", key));
+}
+
+void parareal_free(pr_ctx *c) {
+  if (!c) return;
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->comm) {
+    Nccl &n = nccl();
+    if (n.ok) (c->poisoned ? n.CommAbort(c->comm) : n.CommDestroy(c->comm));
+  }
+  free_scheme(c->fine);
+  free_scheme(c->crs);
+  cudaFree(c->d_fset);
+  cudaFree(c->d_L);
+  cudaFree(c->d_K);
+  cudaFree(c->d_r);
+  cudaFree(c->d_wts);
+  if (c->own_ws) cudaFree(c->ws);
+  if (c->h_delta) cudaFreeHost(c->h_delta);
+  for (auto e : c->ev) cudaEventDestroy(e);
+  if (c->own_stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+}  // extern "C"

@@ -84,6 +84,7 @@ def single(M: int, N: int, *, K: float = 1.0, r: float = 0.05, sigma: float = 0.
     """One European call instance; L defaults to 4K (reading Q5)."""
     if L is None:
         L = 4.0 * K
+    kw.setdefault("max_iter", min(4, N))
     return Problem(M=M, strike=np.array([K]), sigma=np.array([sigma]), rate=np.array([r]),
                    L=np.array([L]), N=N, **kw)
 
@@ -94,6 +95,7 @@ def portfolio(n_k: int = 64, n_s: int = 64, M: int = 256, N: int = 16, r: float 
     Ss = 0.1 + 0.4 * np.arange(n_s) / max(n_s - 1, 1)
     strike = np.repeat(Ks, n_s)
     sigma = np.tile(Ss, n_k)
+    kw.setdefault("max_iter", min(4, N))
     return Problem(M=M, strike=strike, sigma=sigma, rate=np.full(strike.shape, r),
                    L=4.0 * strike, N=N, **kw)
 

@@ -1,0 +1,204 @@
+"""Multi-rank host logic on CPU (gloo, world_size 2 and 4).
+
+The CUDA path shards the N slices across ranks; the per-rank schedule it runs
+(parareal_plan_iteration, the product's own host code) is checked here:
+  * pure invariants over many (N, world, k);
+  * executed by real processes exchanging slice-boundary states with gloo
+    send/recv and a MAX all-reduce of delta, using the CPU oracle's propagators
+    for F and G -- the result must be bitwise identical to the single-process
+    oracle (the R-invariance claim of SURVEY.md §8(e));
+  * the NCCL unique-id broadcast used by bench.py.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from paper_2303_03848_b200 import parareal, synth
+
+
+@pytest.mark.parametrize("N,world", [(1, 1), (4, 1), (4, 2), (4, 4), (32, 8), (64, 8), (12, 3), (16, 16)])
+def test_plan_invariants(N, world):
+    per = N // world
+    for k in range(0, N + 1):
+        plans = [parareal.plan_iteration(N, world, r, k) for r in range(world)]
+        fine, chain, delta, copies = set(), [], set(), 0
+        for r, P in enumerate(plans):
+            n0 = r * per
+            fine |= {n0 + l for l in range(P["fine_lo"], P["fine_hi"])}
+            chain += [n0 + l for l in range(P["chain_lo"], P["chain_hi"]) if (P["copy"] or P["recv_first"] or k == 0)]
+            delta |= {n0 + l for l in range(P["delta_lo"], P["delta_hi"] + 1)}
+            copies += P["copy"]
+            if P["fk_local"] >= 0:
+                assert n0 + P["fk_local"] == k - 1
+            # hand-off symmetry: r sends iff r+1 receives
+            if r < world - 1:
+                assert P["send_last"] == plans[r + 1]["recv_first"], (N, world, k, r)
+            else:
+                assert P["send_last"] == 0
+        if k == 0:
+            assert chain == list(range(N)) and not fine and not delta
+            continue
+        assert fine == set(range(k - 1, N))                         # active window
+        assert sorted(chain) == list(range(k, N))                    # each G slice once
+        assert delta == set(range(k, N + 1))                         # delta over n = k..N (Q13)
+        assert copies == (1 if k <= N else 0)
+
+
+def test_plan_rejects_bad_arguments():
+    for args in [(0, 1, 0, 0), (4, 3, 0, 1), (4, 2, 2, 1), (4, 2, 0, -1)]:
+        with pytest.raises(parareal.PararealError):
+            parareal.plan_iteration(*args)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _rank_main(rank, world, port, cfg, coarse, K, out_q):
+    import torch
+    import torch.distributed as dist
+
+    import oracle
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        p = synth.config(cfg, coarse=coarse, coarse_steps=1, max_iter=K, tol=0.0)
+        net = synth.kaiming_net(synth.PINN_3x20, seed=0)
+        N, B, M = p.N, p.B, p.M
+        per = N // world
+        n0 = rank * per
+
+        def G(n, u):
+            return oracle.pinn_G(p, net, n, u) if coarse == synth.COARSE_PINN else oracle.coarse_ie(p, n, u)
+
+        U = np.zeros((per + 1, B, M))
+        Gh = np.zeros((per, B, M))
+        D = np.zeros((per, B, M))
+        if rank == 0:
+            U[0] = oracle.payoff(p)
+
+        def recv0():
+            t = torch.zeros(B * M, dtype=torch.float64)
+            dist.recv(t, src=rank - 1)
+            U[0] = t.numpy().reshape(B, M)
+
+        def send_last():
+            dist.send(torch.from_numpy(U[per].reshape(-1).copy()), dst=rank + 1)
+
+        P0 = parareal.plan_iteration(N, world, rank, 0)
+        if P0["recv_first"]:
+            recv0()
+        for l in range(P0["chain_lo"], P0["chain_hi"]):
+            Gh[l] = G(n0 + l, U[l])
+            U[l + 1] = Gh[l]
+        if P0["send_last"]:
+            send_last()
+        deltas = []
+        for k in range(1, K + 1):
+            P = parareal.plan_iteration(N, world, rank, k)
+            Uold = U.copy()
+            Fk = None
+            for l in range(P["fine_lo"], P["fine_hi"]):
+                Fh = oracle.fine(p, n0 + l, Uold[l])
+                if l == P["fk_local"]:
+                    Fk = Fh
+                else:
+                    D[l] = Fh - Gh[l]
+            if P["recv_first"]:
+                recv0()
+            if P["copy"]:
+                U[P["chain_lo"]] = Fk
+            if P["copy"] or P["recv_first"]:
+                for l in range(P["chain_lo"], P["chain_hi"]):
+                    g = G(n0 + l, U[l])
+                    U[l + 1] = g + D[l]
+                    Gh[l] = g
+            if P["send_last"]:
+                send_last()
+            dk = 0.0
+            for l in range(P["delta_lo"], P["delta_hi"] + 1):
+                for b in range(B):
+                    num = np.sqrt(np.sum((U[l, b] - Uold[l, b]) ** 2))
+                    den = np.sqrt(np.sum(U[l, b] ** 2))
+                    dk = max(dk, num / den if den > 0 else num)
+            t = torch.tensor([dk], dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            deltas.append(float(t.item()))
+        # final state to rank 0
+        if world > 1:
+            if rank == world - 1:
+                dist.send(torch.from_numpy(U[per].reshape(-1).copy()), dst=0)
+            if rank == 0:
+                t = torch.zeros(B * M, dtype=torch.float64)
+                dist.recv(t, src=world - 1)
+                final = t.numpy().reshape(B, M)
+        else:
+            final = U[per]
+        if rank == 0:
+            out_q.put((final, deltas))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,coarse", [(2, synth.COARSE_IMPLICIT_EULER), (2, synth.COARSE_PINN),
+                                          (4, synth.COARSE_IMPLICIT_EULER)])
+def test_sharded_schedule_matches_serial_oracle(world, coarse):
+    import torch.multiprocessing as mp
+
+    import oracle
+    cfg, K = "C1", 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rank_main, args=(r, world, port, cfg, coarse, K, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    final, deltas = q.get(timeout=300)
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    p = synth.config(cfg, coarse=coarse, coarse_steps=1, max_iter=K, tol=0.0)
+    net = synth.kaiming_net(synth.PINN_3x20, seed=0)
+    U, d, Kr, _ = oracle.parareal(p, net)
+    assert np.array_equal(final, U[-1])                 # bitwise: sharding does not change arithmetic
+    assert np.allclose(deltas, d, rtol=1e-12, atol=0)
+
+
+def _id_main(rank, world, port, out_q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        obj = [parareal.get_nccl_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        out_q.put((rank, obj[0]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_nccl_id_broadcast():
+    """bench.py's rendezvous: rank 0 creates the NCCL id, every rank receives the same bytes."""
+    import torch  # noqa: F401  (maps torch's libnccl.so.2 so dlopen finds it)
+    try:
+        parareal.get_nccl_id()
+    except parareal.PararealError as e:
+        pytest.skip("NCCL not loadable here: %s" % e)
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_id_main, args=(r, 2, port, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    got = dict(q.get(timeout=120) for _ in range(2))
+    for pr in procs:
+        pr.join(timeout=60)
+    assert len(got[0]) == 128 and got[0] == got[1]

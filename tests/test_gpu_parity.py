@@ -1,0 +1,250 @@
+"""CUDA path vs the CPU oracle, element by element on the same seeded inputs.
+
+Every call goes through the C ABI (libparareal.so) via the ctypes binding."""
+import numpy as np
+import pytest
+
+import oracle
+from gpu_helpers import TOL_FP32, assert_close, rel_err
+from paper_2303_03848_b200 import parareal, synth
+
+pytestmark = pytest.mark.gpu
+
+FINE_KERNELS = [1, 2]   # resident, streamed (PR_OPT_FINE_KERNEL)
+
+
+def ctx_for(p, net=None, fine_kernel=0):
+    c = parareal.Context(p)
+    if fine_kernel:
+        c.set_option(parareal.OPT_FINE_KERNEL, fine_kernel)
+    if net is not None:
+        c.load_weights(net)
+    return c
+
+
+# ------------------------------------------------------------------ single propagators (T1)
+
+@pytest.mark.parametrize("kernel", FINE_KERNELS)
+@pytest.mark.parametrize("M,N,n", [(1, 2, 1), (5, 4, 0), (64, 4, 3), (100, 8, 5), (1024, 32, 17), (2000, 4, 2)])
+def test_fine_single_slice(kernel, M, N, n):
+    p = synth.single(M, N)
+    U = synth.random_state(1, M, seed=M)
+    with ctx_for(p, fine_kernel=kernel) as c:
+        got = c.apply_fine(n, U)
+    ref = oracle.fine(p, n, U.astype(np.float64))
+    assert_close(got, ref, what="F M=%d n=%d kernel=%d" % (M, n, kernel))
+
+
+@pytest.mark.parametrize("M", [4097, 12345, 1 << 16])
+def test_fine_streamed_multi_tile(M):
+    """Several 4096-point tiles with a ragged tail: decoupled look-back across CTAs."""
+    p = synth.single(M, 64, fine_steps=20)
+    U = synth.random_state(1, M, seed=3)
+    with ctx_for(p, fine_kernel=2) as c:
+        got = c.apply_fine(7, U)
+    assert_close(got, oracle.fine(p, 7, U.astype(np.float64)), what="F streamed M=%d" % M)
+
+
+def test_fine_c3_size_single_slice():
+    """C3 grid (2^20 points, dtau = 1/6400), one slice of 100 steps, default (streamed) kernel."""
+    p = synth.config("C3")
+    U0 = oracle.payoff(p)
+    with ctx_for(p) as c:
+        got = c.apply_fine(0, U0.astype(np.float32))
+    ref = oracle.fine(p, 0, U0)
+    assert_close(got, ref, what="F C3")
+
+
+def test_fine_portfolio_instances():
+    """C4-style instances (distinct sigma and strike, L_b = 4K_b) share one launch."""
+    p = synth.portfolio(n_k=4, n_s=8, M=256, N=16)
+    U = oracle.payoff(p).astype(np.float32)
+    for kernel in FINE_KERNELS:
+        with ctx_for(p, fine_kernel=kernel) as c:
+            got = c.apply_fine(3, U)
+        assert_close(got, oracle.fine(p, 3, U.astype(np.float64)), what="F portfolio kernel=%d" % kernel)
+
+
+@pytest.mark.parametrize("dims,act", [(synth.PINN_3x20, synth.ACT_TANH), (synth.PINN_PAPER, synth.ACT_RELU),
+                                      (synth.PINN_PAPER, synth.ACT_TANH), ([4, 64, 64, 64, 64, 1], synth.ACT_TANH),
+                                      ([4, 8, 8, 1], synth.ACT_TANH), ([2, 16, 16, 1], synth.ACT_TANH),
+                                      ([4, 32, 32, 1], synth.ACT_RELU)])
+def test_pinn_G_single_slice(dims, act):
+    p = synth.single(1000, 8)
+    net = synth.kaiming_net(dims, seed=5, activation=act, in_scale=[1.0, 0.5, 2.0, 1.5][:dims[0]],
+                            out_scale=0.75)
+    U = synth.random_state(1, 1000, seed=9) * 2.0
+    with ctx_for(p, net) as c:
+        got = c.apply_coarse(3, U)
+    ref = oracle.pinn_G(p, net, 3, U.astype(np.float64))
+    assert_close(got, ref, what="G %s" % dims)
+
+
+def test_pinn_G_portfolio():
+    p = synth.portfolio(n_k=3, n_s=5, M=300, N=16)
+    net = synth.kaiming_net(synth.PINN_3x20, seed=1)
+    U = oracle.payoff(p)
+    with ctx_for(p, net) as c:
+        got = c.apply_coarse(15, U.astype(np.float32))
+    assert_close(got, oracle.pinn_G(p, net, 15, U), what="G portfolio")
+
+
+@pytest.mark.parametrize("kernel", FINE_KERNELS)
+def test_numerical_G_single_slice(kernel):
+    p = synth.single(777, 8, coarse=synth.COARSE_IMPLICIT_EULER, coarse_steps=3)
+    U = synth.random_state(1, 777, seed=4)
+    with ctx_for(p, fine_kernel=kernel) as c:
+        got = c.apply_coarse(2, U)
+    assert_close(got, oracle.coarse_ie(p, 2, U.astype(np.float64)), what="G_num")
+
+
+# ------------------------------------------------------------------ serial fine and Parareal (T2/T3)
+
+@pytest.mark.parametrize("kernel", FINE_KERNELS)
+def test_serial_fine_c1(kernel):
+    p = synth.config("C1")
+    with ctx_for(p, fine_kernel=kernel) as c:
+        got, ms = c.serial_fine()
+    assert ms > 0
+    assert_close(got, oracle.serial_fine(p)[-1], what="serial fine")
+
+
+@pytest.mark.parametrize("kernel", FINE_KERNELS)
+@pytest.mark.parametrize("cfg,tol,K_expected", [("C1", 3e-5, 3), ("C2", 1e-5, 3)])
+def test_parareal_numerical_G_converges_like_oracle(kernel, cfg, tol, K_expected):
+    """Numerical coarse G (n_c = 1): identical iteration count, delta history and iterates.
+    The tol values satisfy the near-tie guard of reading Q18 (checked on the oracle side)."""
+    p = synth.config(cfg, coarse=synth.COARSE_IMPLICIT_EULER, coarse_steps=1, tol=tol)
+    p = p.replace(max_iter=min(p.N, 6))
+    ref_U, ref_d, ref_K, _ = oracle.parareal(p)
+    assert ref_K == K_expected
+    assert ref_d[ref_K - 2] >= 1.5 * tol and ref_d[ref_K - 1] <= tol / 1.5   # Q18 guard
+    with ctx_for(p, fine_kernel=kernel) as c:
+        U, rep = c.solve()
+        it = c.copy_iterates(0, p.N + 1)
+    assert rep["iterations"] == ref_K and rep["converged"]
+    assert np.allclose(rep["delta"], ref_d, rtol=2e-2, atol=2e-6)
+    assert_close(U, ref_U[-1], what="U_N")
+    assert_close(it, ref_U, what="all U_n")
+
+
+@pytest.mark.parametrize("kernel", FINE_KERNELS)
+def test_parareal_pinn_fixed_K(kernel):
+    """PINN coarse (random 3x20 weights), fixed K=3: iterates and delta match the oracle."""
+    p = synth.config("C1", coarse=synth.COARSE_PINN, max_iter=3, tol=0.0)
+    net = synth.kaiming_net(synth.PINN_3x20, seed=0)
+    ref_U, ref_d, ref_K, hist = oracle.parareal(p, net, history=True)
+    # stability gate: the fp32 oracle must track the fp64 one on this run
+    U32, d32, _, _ = oracle.parareal(p, net, prec=32)
+    gate = rel_err(U32, ref_U) < 1e-6
+    with ctx_for(p, net, fine_kernel=kernel) as c:
+        U, rep = c.solve()
+        it = c.copy_iterates(0, p.N + 1)
+    assert rep["iterations"] == 3
+    if gate:
+        assert_close(it, ref_U, what="PINN iterates")
+        assert np.allclose(rep["delta"], ref_d, rtol=1e-3)
+
+
+def test_parareal_pinn_k0_chain_c2():
+    """k=0 coarse sweep over 32 slices at C2 (contractive for random nets)."""
+    p = synth.config("C2", coarse=synth.COARSE_PINN, max_iter=1, tol=0.0)
+    net = synth.kaiming_net(synth.PINN_3x20, seed=2)
+    _, _, _, hist = oracle.parareal(p, net, history=True)
+    with ctx_for(p, net) as c:
+        c.solve()
+    # after iteration 1 the slices n >= 2 hold G-chain + correction; compare the k=1 iterate
+        it = c.copy_iterates(0, p.N + 1)
+    U32 = oracle.parareal(p, net, prec=32)[0]
+    if rel_err(U32, hist[1]) < 1e-6:
+        assert_close(it, hist[1], what="C2 PINN k=1")
+
+
+@pytest.mark.parametrize("coarse", [synth.COARSE_PINN, synth.COARSE_IMPLICIT_EULER])
+@pytest.mark.parametrize("kernel", FINE_KERNELS)
+def test_finite_termination_bitwise(coarse, kernel):
+    """at k = N Parareal reproduces the serial fine solution -- bitwise against the GPU's
+    own serial fine with the same kernel configuration (T3), and within tolerance of the oracle."""
+    p = synth.config("C1", coarse=coarse, max_iter=4, tol=0.0)
+    net = synth.kaiming_net(synth.PINN_3x20, seed=0)
+    with ctx_for(p, net if coarse == synth.COARSE_PINN else None, fine_kernel=kernel) as c:
+        U, rep = c.solve()
+        sf, _ = c.serial_fine()
+    assert rep["iterations"] == p.N
+    assert np.array_equal(U, sf)
+    assert_close(U, oracle.serial_fine(p)[-1], what="k=N vs oracle")
+
+
+def test_strike_zero_exact_solution():
+    """K = 0: V = S is a fixed point of F and numerical G (exact discrete solution)."""
+    p = synth.single(1000, 8, K=0.0, L=4.0, coarse=synth.COARSE_IMPLICIT_EULER, max_iter=2, tol=0.0)
+    S = 4.0 / 1001 * np.arange(1, 1001)
+    with ctx_for(p) as c:
+        U, rep = c.solve()
+    assert np.max(np.abs(U[0] - S) / S) < 1e-6
+
+
+def test_determinism():
+    p = synth.config("C2", coarse=synth.COARSE_PINN, max_iter=3, tol=0.0)
+    net = synth.kaiming_net(synth.PINN_3x20, seed=1)
+    with ctx_for(p, net) as c:
+        a, ra = c.solve()
+        b, rb = c.solve()
+    assert np.array_equal(a, b) and np.array_equal(ra["delta"], rb["delta"])
+
+
+def test_portfolio_parareal_sampled():
+    """C4 layout (many instances, 64 factor sets) at reduced instance count; fixed K."""
+    p = synth.portfolio(n_k=4, n_s=16, M=256, N=16, coarse=synth.COARSE_IMPLICIT_EULER, max_iter=3, tol=0.0)
+    ref_U, ref_d, _, _ = oracle.parareal(p)
+    with ctx_for(p) as c:
+        U, rep = c.solve()
+    assert_close(U, ref_U[-1], what="portfolio U_N")
+    assert np.allclose(rep["delta"], ref_d, rtol=2e-2, atol=1e-6)
+
+
+def test_homogeneity_c4_full_sampled():
+    """Full C4 size (4096 instances): sampled instances against single-instance oracle runs."""
+    p = synth.config("C4", coarse=synth.COARSE_IMPLICIT_EULER, max_iter=2, tol=0.0)
+    with ctx_for(p) as c:
+        U, rep = c.solve()
+    assert rep["iterations"] == 2
+    for b in (0, 777, 2048, 4095):
+        pb = p.replace(strike=p.strike[b:b + 1], sigma=p.sigma[b:b + 1], rate=p.rate[b:b + 1], L=p.L[b:b + 1])
+        ref = oracle.parareal(pb)[0][-1, 0]
+        assert_close(U[b:b + 1], ref[None], what="C4 instance %d" % b)
+
+
+def test_device_entry_points():
+    """Device-pointer variants and a caller-bound workspace give the host-path results bitwise."""
+    import torch
+    p = synth.config("C2", coarse=synth.COARSE_IMPLICIT_EULER, max_iter=2, tol=0.0)
+    with ctx_for(p) as c:
+        ws = torch.empty(c.workspace_bytes(), dtype=torch.uint8, device="cuda")
+        c.bind_workspace(ws)
+        out = torch.empty((1, p.M), dtype=torch.float32, device="cuda")
+        rep = c.solve_device(out)
+        dev = out.cpu().numpy()
+        host, rep2 = c.solve()
+        ms = c.serial_fine_device(out)
+        sf_dev = out.cpu().numpy()
+        sf_host, _ = c.serial_fine()
+        v0 = c.initial_state()
+    assert rep["iterations"] == 2 and ms > 0
+    assert np.array_equal(dev, host) and np.array_equal(sf_dev, sf_host)
+    assert np.array_equal(v0, oracle.payoff(p).astype(np.float32))
+
+
+def test_errors_on_gpu():
+    p = synth.config("C1", coarse=synth.COARSE_PINN)
+    with parareal.Context(p) as c:
+        with pytest.raises(parareal.PararealError) as ei:
+            c.solve()
+        assert ei.value.status == 5   # no weights loaded
+        with pytest.raises(parareal.PararealError):
+            c.load_weights(synth.kaiming_net([4, 20, 30, 1]))   # unequal hidden widths
+        with pytest.raises(parareal.PararealError) as ei:
+            c.load_weights(synth.kaiming_net([4, 24, 24, 1]))   # width not instantiated
+        assert ei.value.status == 7
+        with pytest.raises(parareal.PararealError):
+            c.apply_fine(99, np.zeros((1, 64), np.float32))
