@@ -128,36 +128,50 @@ def test_parareal_numerical_G_converges_like_oracle(kernel, cfg, tol, K_expected
     assert_close(it, ref_U, what="all U_n")
 
 
+def _gate_or_amplification(gpu, ref64, ref32, what):
+    """Stability gate of SURVEY.md §8(c): if the fp32 oracle stays within the parity tolerance of
+    the fp64 oracle, the GPU must too; otherwise the trajectory amplifies rounding and the GPU's
+    deviation must stay at the fp32 oracle's own level (factor 10)."""
+    try:
+        assert_close(ref32, ref64, what="gate")
+        gate = True
+    except AssertionError:
+        gate = False
+    if gate:
+        assert_close(gpu, ref64, what=what)
+    else:
+        assert rel_err(gpu, ref64) <= 10 * max(rel_err(ref32, ref64), 1e-6), (what, rel_err(gpu, ref64),
+                                                                             rel_err(ref32, ref64))
+    return gate
+
+
 @pytest.mark.parametrize("kernel", FINE_KERNELS)
 def test_parareal_pinn_fixed_K(kernel):
-    """PINN coarse (random 3x20 weights), fixed K=3: iterates and delta match the oracle."""
+    """PINN coarse (random 3x20 weights), fixed K=3: iterates and delta vs the oracle."""
     p = synth.config("C1", coarse=synth.COARSE_PINN, max_iter=3, tol=0.0)
     net = synth.kaiming_net(synth.PINN_3x20, seed=0)
     ref_U, ref_d, ref_K, hist = oracle.parareal(p, net, history=True)
-    # stability gate (SURVEY.md §8(c)): the fp32 oracle must track the fp64 one on this run
     U32, d32, _, _ = oracle.parareal(p, net, prec=32)
-    gate = rel_err(U32, ref_U) < 1e-6
     with ctx_for(p, net, fine_kernel=kernel) as c:
         U, rep = c.solve()
         it = c.copy_iterates(0, p.N + 1)
     assert rep["iterations"] == 3
-    if gate:
-        assert_close(it, ref_U, what="PINN iterates")
-        assert np.allclose(rep["delta"], ref_d, rtol=1e-3)
+    _gate_or_amplification(it, ref_U, U32, "PINN iterates C1")
+    assert np.allclose(rep["delta"], ref_d, rtol=1e-2)
 
 
-def test_parareal_pinn_k0_chain_c2():
-    """k=0 coarse sweep over 32 slices at C2 (contractive for random nets)."""
+def test_parareal_pinn_k1_c2():
+    """C2 (32 slices), PINN coarse, one iteration: all boundary states U^1_n vs the oracle."""
     p = synth.config("C2", coarse=synth.COARSE_PINN, max_iter=1, tol=0.0)
     net = synth.kaiming_net(synth.PINN_3x20, seed=2)
     _, _, _, hist = oracle.parareal(p, net, history=True)
+    h32 = oracle.parareal(p, net, prec=32, history=True)[3]
     with ctx_for(p, net) as c:
         c.solve()
-    # after iteration 1 the slices n >= 2 hold G-chain + correction; compare the k=1 iterate
         it = c.copy_iterates(0, p.N + 1)
-    U32 = oracle.parareal(p, net, prec=32)[0]
-    if rel_err(U32, hist[1]) < 1e-6:
-        assert_close(it, hist[1], what="C2 PINN k=1")
+    _gate_or_amplification(it, hist[1], h32[1], "C2 PINN k=1")
+    # the exact part of the iterate: U^1_0 = U_0 and U^1_1 = F(U_0) (P:138)
+    assert_close(it[:2], hist[1][:2], what="C2 PINN exact prefix")
 
 
 @pytest.mark.parametrize("coarse", [synth.COARSE_PINN, synth.COARSE_IMPLICIT_EULER])
