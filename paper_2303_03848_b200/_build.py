@@ -9,11 +9,15 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libparareal.so")
-SOURCES = ["parareal.cu", "fine_resident.cuh", "fine_streamed.cuh", "pinn_chain.cuh", "misc_kernels.cuh"]
+UNITS = ["parareal.cu", "res.cu", "streamed.cu", "pinn_smem.cu", "pinn_param.cu", "misc.cu"]
+HEADERS = ["launch.h", "fine_resident.cuh", "fine_streamed.cuh", "pinn_chain.cuh"]
+SOURCES = UNITS + HEADERS
 HEADER = os.path.join(ROOT, "include", "parareal.h")
 
 NVCC_FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
-              "-Xcompiler", "-fPIC", "-shared", "-cudart", "static", "-ldl"]
+              "-Xcompiler", "-fPIC"]
+LINK_FLAGS = ["-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-cudart", "static", "-ldl"]
+BUILD_DIR = os.path.join(ROOT, "build")
 
 
 def _nvcc() -> str:
@@ -32,11 +36,34 @@ def stale() -> bool:
 
 
 def build_cuda(force: bool = False, verbose: bool = False) -> str:
-    """nvcc -gencode arch=compute_100a,code=sm_100a ... → paper_2303_03848_b200/libparareal.so"""
+    """Each translation unit: nvcc -gencode arch=compute_100a,code=sm_100a -c (in parallel), then
+    link → paper_2303_03848_b200/libparareal.so (cudart static; NCCL is dlopen'ed at run time)."""
     if not force and not stale():
         return LIB
+    from concurrent.futures import ThreadPoolExecutor
+    os.makedirs(BUILD_DIR, exist_ok=True)
+    nv = _nvcc()
+    hdr_t = max(os.path.getmtime(os.path.join(CSRC, h)) for h in HEADERS + []) if HEADERS else 0
+    hdr_t = max(hdr_t, os.path.getmtime(HEADER))
+
+    def compile_unit(u):
+        src = os.path.join(CSRC, u)
+        obj = os.path.join(BUILD_DIR, u.replace(".cu", ".o"))
+        if not force and os.path.exists(obj) and os.path.getmtime(obj) > max(os.path.getmtime(src), hdr_t):
+            return obj
+        cmd = [nv] + NVCC_FLAGS + ["-c", "-o", obj + ".tmp", src]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode:
+            raise RuntimeError("nvcc failed for %s:\n%s" % (u, r.stderr))
+        os.replace(obj + ".tmp", obj)
+        return obj
+
+    with ThreadPoolExecutor(max_workers=min(len(UNITS), os.cpu_count() or 4)) as ex:
+        objs = list(ex.map(compile_unit, UNITS))
     tmp = LIB + ".tmp%d" % os.getpid()
-    cmd = [_nvcc()] + NVCC_FLAGS + ["-o", tmp, os.path.join(CSRC, "parareal.cu")]
+    cmd = [nv] + LINK_FLAGS + ["-o", tmp] + objs
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)

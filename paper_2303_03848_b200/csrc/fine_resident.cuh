@@ -15,10 +15,11 @@
 // are products of constant factors, so every level coefficient is
 // precomputed once per kernel), a fold over the ≤16 warp totals in shared
 // memory, and a fix-up with precomputed prefix products.
-#pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#ifndef PR_FINE_RESIDENT_ARGS
+#define PR_FINE_RESIDENT_ARGS
 namespace pr {
 
 constexpr unsigned kFull = 0xffffffffu;
@@ -53,6 +54,12 @@ struct ResidentArgs {
   int nch;
 };
 
+}  // namespace pr
+#endif  // PR_FINE_RESIDENT_ARGS
+
+#if !defined(PR_ARGS_ONLY) && !defined(PR_FINE_RESIDENT_IMPL)
+#define PR_FINE_RESIDENT_IMPL
+namespace pr {
 __device__ __forceinline__ double g_upper(const ResidentArgs &a, int b, double tau) {
   // Reading Q3: V(L, τ) = L − K e^{−rτ} (default) or 0 (paper-literal P:161)
   return a.upper_bc ? 0.0 : a.Lb[b] - a.Kb[b] * exp(-a.rb[b] * tau);
@@ -181,18 +188,29 @@ __device__ __forceinline__ void sys_reduce2(double &a, double &b, int t, double 
   }
 }
 
+constexpr int kBcChunk = 128;  // boundary terms tabulated per chunk of implicit steps
+
+// All implicit steps of slice n.  The boundary term dτ(a_M+b_M)·g(τ_{m+1}) of each step needs an
+// fp64 exp; it is tabulated in shared memory for kBcChunk steps at a time (one exp per thread)
+// so no exp sits on the per-step critical path.
 template <int P, int NT>
 __device__ __forceinline__ void run_steps(Tri<P, NT> &tri, const ResidentArgs &a, int b, int n,
-                                          int t, double (&x)[P], double *sh) {
+                                          int t, double (&x)[P], double *sh, double *bct) {
   const int bc_t = (a.M - 1) / P, bc_ip = (a.M - 1) % P;
   const int bc_i = (t == bc_t) ? bc_ip : -1;
   const double coef = a.bcoef[b];
   const double tau0 = n * a.dT;
 #pragma unroll 1
-  for (int m = 0; m < a.steps; ++m) {
-    double bcg = 0.0;
-    if (bc_i >= 0) bcg = coef * g_upper(a, b, (tau0 + m * a.dtau) + a.dtau);
-    tri.step(x, bc_i, bcg, sh);
+  for (int m0 = 0; m0 < a.steps; m0 += kBcChunk) {
+    __syncthreads();  // readers of the previous chunk are done
+    for (int i = t; i < kBcChunk; i += NT) {
+      const int m = m0 + i;
+      if (m < a.steps) bct[i] = coef * g_upper(a, b, (tau0 + m * a.dtau) + a.dtau);
+    }
+    __syncthreads();
+    const int mend = min(a.steps - m0, kBcChunk);
+#pragma unroll 1
+    for (int mm = 0; mm < mend; ++mm) tri.step(x, bc_i, bc_i >= 0 ? bct[mm] : 0.0, sh);
   }
 }
 
@@ -201,6 +219,7 @@ template <int P, int NT, int SPB>
 __global__ void __launch_bounds__(NT * SPB) k_fine_sweep(ResidentArgs a) {
   constexpr int NW = NT / 32;
   __shared__ double shm[SPB][4 * NW + 2];
+  __shared__ double bctab[SPB][kBcChunk];
   const int sys = blockIdx.x * SPB + threadIdx.x / NT;
   const int t = threadIdx.x % NT;
   const int nsys = a.nsl * a.B;
@@ -218,7 +237,7 @@ __global__ void __launch_bounds__(NT * SPB) k_fine_sweep(ResidentArgs a) {
     const int j = t * P + i;
     x[i] = (j < a.M) ? (double)u[j] : 0.0;
   }
-  run_steps<P, NT>(tri, a, b, a.n_base + ln, t, x, sh);
+  run_steps<P, NT>(tri, a, b, a.n_base + ln, t, x, sh, bctab[threadIdx.x / NT]);
   if (!live) return;
   const size_t row = ((size_t)ln * a.B + b) * a.Mp;
   if (a.Fout) {
@@ -253,6 +272,7 @@ __global__ void __launch_bounds__(NT * SPB) k_resident_chain(ResidentArgs a) {
   constexpr int NW = NT / 32;
   __shared__ double shm[SPB][4 * NW + 2];
   __shared__ double red[SPB][2 * NW + 2];
+  __shared__ double bctab[SPB][kBcChunk];
   const int sys = blockIdx.x * SPB + threadIdx.x / NT;
   const int t = threadIdx.x % NT;
   const bool live = sys < a.B;
@@ -303,7 +323,7 @@ __global__ void __launch_bounds__(NT * SPB) k_resident_chain(ResidentArgs a) {
   }
 #pragma unroll 1
   for (int ln = a.c_ln0; ln < a.c_ln1; ++ln) {
-    run_steps<P, NT>(tri, a, b, a.n_base + ln, t, x, sh);
+    run_steps<P, NT>(tri, a, b, a.n_base + ln, t, x, sh, bctab[threadIdx.x / NT]);
     const size_t row = (size_t)ln * sstride + (size_t)b * a.Mp;
     float *un = a.Uw + (size_t)(ln + 1) * a.ustride + (size_t)b * a.Mp;
     double num = 0.0, den = 0.0;
@@ -339,3 +359,4 @@ __global__ void __launch_bounds__(NT * SPB) k_resident_chain(ResidentArgs a) {
 }
 
 }  // namespace pr
+#endif  // PR_FINE_RESIDENT_IMPL

@@ -4,29 +4,59 @@
 // (I − dτA) x⁺ = x + dτ(a_M+b_M) g(τ⁺) e_M is a forward
 // elimination  y_j = r_j − m_j y_{j−1}  and a back substitution
 // x_j = y_j/p_j − (u_j/p_j) x_{j+1}, each a linear recurrence evaluated as a
-// scan of affine maps.  Here a system (one instance × one slice, up to 2^20
-// points and more) is cut into tiles of TILE points, one CTA per tile, and a
-// pass is one kernel: a local sequential pass per thread, a CTA scan, and a
-// single-pass decoupled look-back across tiles (tile aggregates published
-// with release/acquire flags; CTAs take tiles in scan order from a global
-// ticket counter so a predecessor is always resident or finished).
-// Traffic: 16 B per point-step of fp32 state (read+write per pass); the fp64
-// factors (8 B forward, 16 B backward) are re-read from L2.
-#pragma once
+// scan of affine maps v ↦ A + B·v.  A system (one instance × one slice, up to
+// 2^20 points and more) is cut into tiles of kSTile points, one CTA per tile;
+// a pass is one kernel: a sequential pass over 16 points per thread, a CTA
+// scan, and a look-back across tiles.
+//
+// Look-back.  The tile multipliers B (products of the constant factors) are
+// precomputed on the host, so a CTA publishes only its offset A, in one
+// 16-byte {A, epoch} word (single 128-bit store/load: no fences).  The value
+// entering tile i is the composition of the aggregates of its predecessors
+// i−1, …, i−W_i, where W_i (host-computed) is the first window whose
+// multiplier product falls below kLookbackEps: the tiles further back change
+// it by < kLookbackEps·|y| (eight orders below fp64 rounding).  No CTA waits
+// on an inclusive prefix, so there is no dependency chain across the wave,
+// and the composition order is fixed: results are bitwise reproducible.
+// CTAs take tiles in scan order from a global ticket, so every predecessor a
+// CTA waits for is resident or finished.
+//
+// Layout.  The fp64 factors and the sweep-private fp32 ping-pong buffers are
+// stored thread-interleaved (see il_index) so every warp access is coalesced.
+// Traffic: 16 B per point-step of fp32 state from HBM; factors 8 B (forward)
+// and 16 B (backward) per point per pass from L2.
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <string.h>
 
+#ifndef PR_FINE_STREAMED_ARGS
+#define PR_FINE_STREAMED_ARGS
 namespace pr {
 
 constexpr int kSPS = 16;                 // points per thread
-constexpr int kSNT = 256;                // threads per tile
-constexpr int kSTile = kSPS * kSNT;      // 4096 points per tile
+constexpr int kSNT = 128;                // data threads per tile (+1 look-back warp)
+constexpr int kSTile = kSPS * kSNT;      // 2048 points per tile
+constexpr double kLookbackEps = 1e-24;   // look-back truncation (see above)
+
+// Interleaved ("thread-major") layout: point j of a row sits at
+// tile·kSTile + i·kSNT + t  (tile = j / kSTile, t = (j % kSTile) / kSPS, i = j % kSPS),
+// so the i-th point of every thread of a warp is one contiguous segment.
+inline size_t il_index(size_t j) {
+  return (j / kSTile) * kSTile + (j % kSPS) * kSNT + (j % kSTile) / kSPS;
+}
+inline int streamed_Mt(int M) { return (M + kSTile - 1) / kSTile * kSTile; }
+inline int streamed_ntiles(int M) { return (M + kSTile - 1) / kSTile; }
+
+// Constant data of one implicit scheme (I − dτA) for K2, per factor set.
+struct StreamedFactors {
+  const double *m, *ip, *cu;     // interleaved [nsets][Mt], identity-padded beyond M
+  const double *tileB;           // [2][nsets][ntiles] tile multiplier, indexed by scan position
+  const int *tileW;              // [2][nsets][ntiles] look-back window (predecessors)
+};
 
 struct StreamedState {
-  float *X = nullptr, *Y = nullptr;      // [nsys][Mp] ping-pong state
-  unsigned long long *flags = nullptr;   // [nsys][ntiles]
-  double *vals = nullptr;                // [nsys][ntiles][3]: aggA, aggB, incl
+  float *X = nullptr, *Y = nullptr;      // [nsys][Mt] ping-pong state (interleaved)
+  double *status = nullptr;              // [nsys][ntiles] × {A, epoch} (16 B)
   unsigned long long *ticket = nullptr;  // global ticket counter
   unsigned long long epoch = 0;          // host: last epoch used
   unsigned long long ticket_base = 0;    // host: tickets consumed so far
@@ -35,19 +65,21 @@ struct StreamedState {
 };
 
 inline size_t streamed_state_bytes(int M, int Mp, int B, int Nloc) {
+  (void)Mp;
   const size_t nsys = (size_t)B * (size_t)(Nloc > 0 ? Nloc : 1);
-  const size_t nt = (size_t)((M + kSTile - 1) / kSTile);
-  return 2 * nsys * Mp * sizeof(float) + nsys * nt * (8 + 24) + 512;
+  return 2 * nsys * (size_t)streamed_Mt(M) * sizeof(float) + nsys * streamed_ntiles(M) * 16 + 512;
 }
 inline void streamed_state_bind(StreamedState &s, char *base, int M, int Mp, int B, int Nloc) {
+  (void)Mp;
   const size_t nsys = (size_t)B * (size_t)(Nloc > 0 ? Nloc : 1);
-  s.ntiles = (M + kSTile - 1) / kSTile;
+  const size_t Mt = (size_t)streamed_Mt(M);
+  s.ntiles = streamed_ntiles(M);
   s.nsys_max = nsys;
   size_t off = 0;
-  s.X = (float *)(base + off); off += nsys * Mp * sizeof(float);
-  s.Y = (float *)(base + off); off += nsys * Mp * sizeof(float);
-  s.flags = (unsigned long long *)(base + off); off += nsys * s.ntiles * 8;
-  s.vals = (double *)(base + off); off += nsys * s.ntiles * 24;
+  s.X = (float *)(base + off); off += nsys * Mt * sizeof(float);
+  s.Y = (float *)(base + off); off += nsys * Mt * sizeof(float);
+  off = (off + 255) / 256 * 256;
+  s.status = (double *)(base + off); off += nsys * s.ntiles * 16;
   off = (off + 255) / 256 * 256;
   s.ticket = (unsigned long long *)(base + off);
   s.epoch = 0;
@@ -58,11 +90,11 @@ inline void streamed_state_bind(StreamedState &s, char *base, int M, int Mp, int
 enum { EPI_X = 0, EPI_SWEEP = 1, EPI_CHAIN = 2 };
 
 struct PassArgs {
-  int M, Mp, B, ntiles, nsys;
-  const double *fm, *fip, *fcu;  // LU factors [nsets][Mp]: forward uses m, backward 1/p and u/p
+  int M, Mp, Mt, B, ntiles, nsys, nsets;
+  StreamedFactors f;
   const int *fset;
-  const float *in;           // [nsys][Mp]
-  float *out;                // [nsys][Mp] (EPI_X / forward)
+  const float *in;           // [nsys][Mp] natural rows (first pass of a slice) or [nsys][Mt] interleaved
+  float *out;                // [nsys][Mt] interleaved (forward passes, EPI_X)
   // forward boundary term
   const double *bcoef, *Lb, *Kb, *rb;
   int upper_bc;
@@ -82,19 +114,57 @@ struct PassArgs {
   double *partials;          // nullable: [(b)·nch + tile]·2 (caller offsets by slice)
   int nch;
   // look-back
-  unsigned long long *flags;
-  double *vals;
+  double *status;
   unsigned long long *ticket;
   unsigned long long ticket_base, epoch;
 };
 
-__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long *p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
+struct StreamedJob {       // fine sweep over local slices [ln0, ln0+nsl)
+  const float *U, *Gh;
+  float *D, *Fk, *Fout;
+  int fk_ln, ln0, nsl, n_base;
+};
+struct StreamedChainJob {  // chain over local slices [ln0, ln1), one system per instance
+  float *U, *Gh;
+  const float *D, *Fcopy;
+  double *partials;
+  int nch, ln0, ln1, n_base;
+  size_t ustride;          // 0 → in place
+};
+
+struct StreamedProblem {   // what every pass of one scheme shares
+  StreamedFactors f;
+  int nsets;
+  const int *fset;
+  const double *bcoef, *L, *K, *r;
+  int upper_bc;
+  double dT, dtau;
+  int steps, M, Mp, B;
+};
+
+cudaError_t streamed_sweep(StreamedState &st, const StreamedProblem &p, const StreamedJob &j, cudaStream_t s,
+                           int *nl);
+cudaError_t streamed_chain(StreamedState &st, const StreamedProblem &p, const StreamedChainJob &j,
+                           cudaStream_t s, int *nl);
+
+}  // namespace pr
+#endif  // PR_FINE_STREAMED_ARGS
+
+#if !defined(PR_ARGS_ONLY) && !defined(PR_FINE_STREAMED_IMPL)
+#define PR_FINE_STREAMED_IMPL
+namespace pr {
+
+// {A, epoch} status word: one 128-bit relaxed store / load (single-copy atomic for an aligned
+// 16-byte access), so a reader that sees this pass's epoch also sees its value -- no fence.
+// The load must be .relaxed (not a weak ld): ptxas may hoist a weak load out of the spin loop.
+__device__ __forceinline__ void st_status(double *p, double v, unsigned long long e) {
+  asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(__double_as_longlong(v)), "l"(e)
+               : "memory");
 }
-__device__ __forceinline__ void st_release(unsigned long long *p, unsigned long long v) {
-  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+__device__ __forceinline__ void ld_status(const double *p, double &v, unsigned long long &e) {
+  unsigned long long a;
+  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(e) : "l"(p) : "memory");
+  v = __longlong_as_double(a);
 }
 
 template <int DIR>
@@ -102,13 +172,55 @@ __device__ __forceinline__ double shfl_prev(double v, int d) {
   return DIR == 0 ? __shfl_up_sync(0xffffffffu, v, d) : __shfl_down_sync(0xffffffffu, v, d);
 }
 
-// Compose y ↦ A + B·y maps: `a` after `b` (b is applied first).
-struct Aff {
-  double A, B;
-};
+__device__ __forceinline__ void bar_data() {  // named barrier over the kSNT data threads only
+  asm volatile("bar.sync 1, %0;" ::"n"(kSNT) : "memory");
+}
 
+// Look-back warp: the value entering tile `pos` = composition of the aggregates of its W_pos
+// predecessors (scan order), written to *yin by lane 0.
 template <int DIR>
-__global__ void __launch_bounds__(kSNT) k_streamed_pass(PassArgs a) {
+__device__ __forceinline__ void look_back(const PassArgs &a, int s, int pos, int set, int lane, double *yin) {
+  if (pos == 0) {
+    if (lane == 0) *yin = 0.0;
+    return;
+  }
+  const size_t tb = ((size_t)DIR * a.nsets + set) * a.ntiles;
+  const int W = a.f.tileW[tb + pos];
+  double accA = 0.0, accB = 1.0;
+  for (int base = 0; base < W; base += 32) {
+    const int k = base + lane;          // predecessor at distance k+1 in scan order
+    double mA = 0.0, mB = 1.0;          // identity beyond the window
+    if (k < W) {
+      const int p = pos - 1 - k;
+      mB = a.f.tileB[tb + p];
+      double v;
+      unsigned long long e;
+      do { ld_status(a.status + 2 * ((size_t)s * a.ntiles + p), v, e); } while (e != a.epoch);
+      mA = v;
+    }
+    // ordered composition lane 0 ∘ lane 1 ∘ … ∘ lane 31 (fixed tree: deterministic)
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const double oA = __shfl_down_sync(0xffffffffu, mA, d);
+      const double oB = __shfl_down_sync(0xffffffffu, mB, d);
+      if ((lane & (2 * d - 1)) == 0) {
+        mA = fma(mB, oA, mA);
+        mB *= oB;
+      }
+    }
+    mA = __shfl_sync(0xffffffffu, mA, 0);
+    mB = __shfl_sync(0xffffffffu, mB, 0);
+    accA = fma(accB, mA, accA);
+    accB *= mB;
+  }
+  if (lane == 0) *yin = accA;
+}
+
+// One pass over one tile.  kSNT data threads (kSPS points each) plus one look-back warp that
+// composes the predecessors' aggregates while the data warps load and scan their tile, so the
+// look-back latency overlaps the tile's own memory traffic instead of following it.
+template <int DIR, bool IN_IL, bool OUT_IL>
+__global__ void __launch_bounds__(kSNT + 32) k_streamed_pass(PassArgs a) {
   constexpr int NW = kSNT / 32;
   __shared__ double sA[NW], sB[NW];
   __shared__ double s_yin;
@@ -116,44 +228,49 @@ __global__ void __launch_bounds__(kSNT) k_streamed_pass(PassArgs a) {
   __shared__ double red[2 * NW];
   if (threadIdx.x == 0) s_ticket = atomicAdd(a.ticket, 1ull) - a.ticket_base;
   __syncthreads();
+  // Tickets are interleaved across the independent systems of the launch (slices × instances):
+  // the predecessor of (s, pos) holds ticket tk − nsys, so with many systems it has long
+  // published its aggregate when this tile needs it.
   const unsigned long long tk = s_ticket;
-  const int s = (int)(tk / a.ntiles);
-  const int pos = (int)(tk % a.ntiles);               // position in scan order
+  const int s = (int)(tk % a.nsys);
+  const int pos = (int)(tk / a.nsys);                 // position in scan order
   const int tile = DIR == 0 ? pos : a.ntiles - 1 - pos;
   const int b = s % a.B;
   const int ln = a.ln0 + s / a.B;
   const int set = a.fset[b];
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  if (w == NW) {  // ---- look-back warp
+    look_back<DIR>(a, s, pos, set, lane, &s_yin);
+    __syncthreads();  // s_yin published to the data warps
+    return;
+  }
   const int j0 = tile * kSTile + t * kSPS;
-  const float *in = a.in + (size_t)s * a.Mp;
-  const double *fa = (DIR == 0 ? a.fm : a.fip) + (size_t)set * a.Mp;
-  const double *fb = DIR ? a.fcu + (size_t)set * a.Mp : nullptr;
+  const size_t til = (size_t)tile * kSTile + t;   // interleaved offset of this thread's point 0
+  const double *fa = (DIR == 0 ? a.f.m : a.f.ip) + (size_t)set * a.Mt + til;
+  const double *fb = DIR ? a.f.cu + (size_t)set * a.Mt + til : nullptr;
 
   double x[kSPS], ca[kSPS], cb[kSPS];
-  const bool full = j0 + kSPS <= a.M;
-  if (full) {
+  // factors: interleaved, identity-padded (m=0, 1/p=1, u/p=0 beyond M) → no guards
 #pragma unroll
-    for (int i = 0; i < kSPS; i += 4) {
-      const float4 v = *reinterpret_cast<const float4 *>(in + j0 + i);
-      x[i] = v.x; x[i + 1] = v.y; x[i + 2] = v.z; x[i + 3] = v.w;
-    }
+  for (int i = 0; i < kSPS; ++i) {
+    ca[i] = __ldg(fa + i * kSNT);
+    if (DIR) cb[i] = __ldg(fb + i * kSNT);
+  }
+  if (IN_IL) {
+    const float *in = a.in + (size_t)s * a.Mt + til;
 #pragma unroll
-    for (int i = 0; i < kSPS; i += 2) {
-      const double2 f = *reinterpret_cast<const double2 *>(fa + j0 + i);
-      ca[i] = f.x; ca[i + 1] = f.y;
-      if (DIR) {
-        const double2 g = *reinterpret_cast<const double2 *>(fb + j0 + i);
-        cb[i] = g.x; cb[i + 1] = g.y;
-      }
-    }
+    for (int i = 0; i < kSPS; ++i) x[i] = __ldcs(in + i * kSNT);
   } else {
+    const float *in = a.in + (size_t)s * a.Mp;
+    if (j0 + kSPS <= a.M) {
 #pragma unroll
-    for (int i = 0; i < kSPS; ++i) {
-      const int j = j0 + i;
-      const bool ok = j < a.M;
-      x[i] = ok ? (double)in[j] : 0.0;
-      ca[i] = ok ? fa[j] : (DIR ? 1.0 : 0.0);
-      if (DIR) cb[i] = ok ? fb[j] : 0.0;
+      for (int i = 0; i < kSPS; i += 4) {
+        const float4 v = *reinterpret_cast<const float4 *>(in + j0 + i);
+        x[i] = v.x; x[i + 1] = v.y; x[i + 2] = v.z; x[i + 3] = v.w;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < kSPS; ++i) x[i] = (j0 + i < a.M) ? (double)in[j0 + i] : 0.0;
     }
   }
   // local sequential pass with zero input, and the thread's map (A, B)
@@ -181,7 +298,7 @@ __global__ void __launch_bounds__(kSNT) k_streamed_pass(PassArgs a) {
       Bt *= cb[i];
     }
   }
-  double At = DIR == 0 ? x[kSPS - 1] : x[0];
+  const double At = DIR == 0 ? x[kSPS - 1] : x[0];
   // CTA inclusive scan in scan order (DIR 0: ascending threads; DIR 1: descending)
   const int sl = DIR == 0 ? lane : 31 - lane;  // scan-order lane
   double iA = At, iB = Bt;
@@ -195,86 +312,21 @@ __global__ void __launch_bounds__(kSNT) k_streamed_pass(PassArgs a) {
   }
   const int sw = DIR == 0 ? w : NW - 1 - w;    // scan-order warp
   if (sl == 31) { sA[sw] = iA; sB[sw] = iB; }
-  __syncthreads();
+  bar_data();
+  // ---- publish this tile's offset at once (successors' look-back warps are waiting on it)
+  if (t == 0) {
+    double TA = 0.0;
+    for (int q = 0; q < NW; ++q) TA = fma(sB[q], TA, sA[q]);
+    st_status(a.status + 2 * ((size_t)s * a.ntiles + pos), TA, a.epoch);
+  }
+  // exclusive prefix of this thread within the tile (independent of the look-back)
   double wA = 0.0, wB = 1.0;  // prefix of preceding warps (in scan order)
   for (int q = 0; q < sw; ++q) { wA = fma(sB[q], wA, sA[q]); wB *= sB[q]; }
-  // exclusive prefix of this thread within the tile
   double eA = shfl_prev<DIR>(iA, 1), eB = shfl_prev<DIR>(iB, 1);
   if (sl == 0) { eA = 0.0; eB = 1.0; }
-  // compose with preceding warps: excl = (e) ∘ (w)
   const double xA = fma(eB, wA, eA), xB = eB * wB;
-  // ---- tile aggregate, publish, look-back (warp 0 of the CTA)
-  const size_t fidx = (size_t)s * a.ntiles + tile;
-  const unsigned long long E = a.epoch << 2;
-  if (t == 0) {
-    double TA = 0.0, TB = 1.0;
-    for (int q = 0; q < NW; ++q) { TA = fma(sB[q], TA, sA[q]); TB *= sB[q]; }
-    double *v = a.vals + fidx * 3;
-    if (pos == 0) {
-      v[2] = TA;
-      s_yin = 0.0;
-      __threadfence();
-      st_release(a.flags + fidx, E | 2ull);
-    } else {
-      v[0] = TA;
-      v[1] = TB;
-      __threadfence();
-      st_release(a.flags + fidx, E | 1ull);
-    }
-  }
-  if (w == 0 && pos > 0) {
-    double accA = 0.0, accB = 1.0;
-    int qpos = pos - 1;  // nearest predecessor, scan order
-    while (true) {
-      const int p = qpos - lane;  // lane 0 = nearest
-      double mA = 0.0, mB = 1.0;  // identity
-      int kind = 0;
-      if (p >= 0) {
-        const int ptile = DIR == 0 ? p : a.ntiles - 1 - p;
-        const size_t pidx = (size_t)s * a.ntiles + ptile;
-        unsigned long long f;
-        do { f = ld_acquire(a.flags + pidx); } while ((f & ~3ull) != E);
-        kind = (int)(f & 3ull);
-        const double *pv = a.vals + pidx * 3;
-        if (kind == 2) { mA = pv[2]; mB = 0.0; }
-        else { mA = pv[0]; mB = pv[1]; }
-      } else {
-        kind = 2;  // before the first tile: the input value is 0
-        mA = 0.0;
-        mB = 0.0;
-      }
-      const unsigned stop = __ballot_sync(0xffffffffu, kind == 2);
-      const int first = stop ? __ffs(stop) - 1 : 32;  // nearest lane holding a final value
-      if (lane > first) { mA = 0.0; mB = 1.0; }
-      // ordered composition lane 0 ∘ lane 1 ∘ ... ∘ lane 31
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const double oA = __shfl_down_sync(0xffffffffu, mA, d);
-        const double oB = __shfl_down_sync(0xffffffffu, mB, d);
-        if ((lane & (2 * d - 1)) == 0) {
-          mA = fma(mB, oA, mA);
-          mB *= oB;
-        }
-      }
-      mA = __shfl_sync(0xffffffffu, mA, 0);
-      mB = __shfl_sync(0xffffffffu, mB, 0);
-      accA = fma(accB, mA, accA);
-      accB *= mB;
-      if (first < 32) break;
-      qpos -= 32;
-    }
-    if (lane == 0) {
-      s_yin = accA;
-      // inclusive value of this tile: aggregate applied to the input
-      double TA = 0.0, TB = 1.0;
-      for (int q = 0; q < NW; ++q) { TA = fma(sB[q], TA, sA[q]); TB *= sB[q]; }
-      a.vals[fidx * 3 + 2] = fma(TB, accA, TA);
-      __threadfence();
-      st_release(a.flags + fidx, E | 2ull);
-    }
-  }
-  __syncthreads();
-  const double yin = fma(xB, s_yin, xA);  // value entering this thread's first point
+  __syncthreads();  // the look-back warp has written s_yin
+  const double yin = fma(xB, s_yin, xA);
   // fix-up with running prefix products
   double q = 1.0;
   if (DIR == 0) {
@@ -285,17 +337,10 @@ __global__ void __launch_bounds__(kSNT) k_streamed_pass(PassArgs a) {
     for (int i = kSPS - 1; i >= 0; --i) { q *= cb[i]; x[i] = fma(q, yin, x[i]); }
   }
   // ---- stores / epilogues
-  if (DIR == 0 || a.epi == EPI_X) {
-    float *o = a.out + (size_t)s * a.Mp;
-    if (full) {
+  if (OUT_IL) {
+    float *o = a.out + (size_t)s * a.Mt + til;
 #pragma unroll
-      for (int i = 0; i < kSPS; i += 4)
-        *reinterpret_cast<float4 *>(o + j0 + i) = make_float4((float)x[i], (float)x[i + 1], (float)x[i + 2], (float)x[i + 3]);
-    } else {
-#pragma unroll
-      for (int i = 0; i < kSPS; ++i)
-        if (j0 + i < a.M) o[j0 + i] = (float)x[i];
-    }
+    for (int i = 0; i < kSPS; ++i) __stcs(o + i * kSNT, (float)x[i]);
     return;
   }
   if (a.epi == EPI_SWEEP) {
@@ -337,7 +382,7 @@ __global__ void __launch_bounds__(kSNT) k_streamed_pass(PassArgs a) {
         den += __shfl_xor_sync(0xffffffffu, den, o);
       }
       if (lane == 0) { red[2 * w] = num; red[2 * w + 1] = den; }
-      __syncthreads();
+      bar_data();
       if (t == 0) {
         num = 0.0; den = 0.0;
         for (int q2 = 0; q2 < NW; ++q2) { num += red[2 * q2]; den += red[2 * q2 + 1]; }
@@ -379,74 +424,61 @@ __global__ void k_copy_delta(float *Uk, const float *F, int M, int Mp, double *p
   }
 }
 
-struct StreamedJob {       // fine sweep over local slices [ln0, ln0+nsl)
-  const float *U, *Gh;
-  float *D, *Fk, *Fout;
-  int fk_ln, ln0, nsl, n_base;
-};
-struct StreamedChainJob {  // chain over local slices [ln0, ln1), one system per instance
-  float *U, *Gh;
-  const float *D, *Fcopy;
-  double *partials;
-  int nch, ln0, ln1, n_base;
-  size_t ustride;          // 0 → in place
-};
-
-inline cudaError_t launch_pass(StreamedState &st, int dir, PassArgs a, cudaStream_t s) {
+static cudaError_t launch_pass(StreamedState &st, int dir, bool in_il, PassArgs a, cudaStream_t s) {
   a.ntiles = st.ntiles;
-  a.flags = st.flags;
-  a.vals = st.vals;
+  a.status = st.status;
   a.ticket = st.ticket;
   a.ticket_base = st.ticket_base;
   a.epoch = ++st.epoch;
   const unsigned long long grid = (unsigned long long)a.nsys * st.ntiles;
   st.ticket_base += grid;
-  if (dir == 0) k_streamed_pass<0><<<(unsigned)grid, kSNT, 0, s>>>(a);
-  else k_streamed_pass<1><<<(unsigned)grid, kSNT, 0, s>>>(a);
+  if (dir == 0) {
+    if (in_il) k_streamed_pass<0, true, true><<<(unsigned)grid, kSNT + 32, 0, s>>>(a);
+    else k_streamed_pass<0, false, true><<<(unsigned)grid, kSNT + 32, 0, s>>>(a);
+  } else {
+    if (a.epi == EPI_X) k_streamed_pass<1, true, true><<<(unsigned)grid, kSNT + 32, 0, s>>>(a);
+    else k_streamed_pass<1, true, false><<<(unsigned)grid, kSNT + 32, 0, s>>>(a);
+  }
   return cudaGetLastError();
 }
 
-inline PassArgs pass_base(const double *m, const double *ip, const double *cu, const int *fset,
-                          const double *bcoef, const double *L, const double *K, const double *r, int upper_bc,
-                          double dT, double dtau, int M, int Mp, int B) {
+static PassArgs pass_base(const StreamedProblem &p) {
   PassArgs a;
   memset(&a, 0, sizeof a);
-  a.M = M; a.Mp = Mp; a.B = B;
-  a.fm = m; a.fip = ip; a.fcu = cu; a.fset = fset;
-  a.bcoef = bcoef; a.Lb = L; a.Kb = K; a.rb = r; a.upper_bc = upper_bc;
-  a.dT = dT; a.dtau = dtau;
+  a.M = p.M; a.Mp = p.Mp; a.B = p.B; a.Mt = streamed_Mt(p.M); a.nsets = p.nsets;
+  a.f = p.f; a.fset = p.fset;
+  a.bcoef = p.bcoef; a.Lb = p.L; a.Kb = p.K; a.rb = p.r; a.upper_bc = p.upper_bc;
+  a.dT = p.dT; a.dtau = p.dtau;
   return a;
 }
 
 // `steps` implicit steps on a.nsys systems: in0 → ... → the epilogue set in `a` (last step).
-inline cudaError_t streamed_steps(StreamedState &st, const PassArgs &a, const float *in0, int steps,
+static cudaError_t streamed_steps(StreamedState &st, const PassArgs &a, const float *in0, int steps,
                                   cudaStream_t s, int *nl) {
   for (int m = 0; m < steps; ++m) {
     PassArgs f = a;
     f.step_m = m;
     f.in = (m == 0) ? in0 : st.X;
     f.out = st.Y;
-    cudaError_t e = launch_pass(st, 0, f, s);
+    cudaError_t e = launch_pass(st, 0, m > 0, f, s);
     if (e != cudaSuccess) return e;
     PassArgs g = a;
     g.step_m = m;
     g.in = st.Y;
     g.out = st.X;
     if (m < steps - 1) g.epi = EPI_X;
-    e = launch_pass(st, 1, g, s);
+    e = launch_pass(st, 1, true, g, s);
     if (e != cudaSuccess) return e;
     *nl += 2;
   }
   return cudaSuccess;
 }
 
-inline cudaError_t streamed_sweep(StreamedState &st, const double *m, const double *ip, const double *cu,
-                                  const int *fset, const double *bcoef, const double *L, const double *K,
-                                  const double *r, int upper_bc, double dT, double dtau, int steps, int M, int Mp,
-                                  int B, const StreamedJob &j, cudaStream_t s, int *nl) {
-  PassArgs a = pass_base(m, ip, cu, fset, bcoef, L, K, r, upper_bc, dT, dtau, M, Mp, B);
-  const size_t off = (size_t)j.ln0 * B * Mp;
-  a.nsys = j.nsl * B;
+cudaError_t streamed_sweep(StreamedState &st, const StreamedProblem &p, const StreamedJob &j, cudaStream_t s,
+                           int *nl) {
+  PassArgs a = pass_base(p);
+  const size_t off = (size_t)j.ln0 * p.B * p.Mp;
+  a.nsys = j.nsl * p.B;
   a.n_base = j.n_base;
   a.ln0 = j.ln0;
   a.epi = EPI_SWEEP;
@@ -456,39 +488,39 @@ inline cudaError_t streamed_sweep(StreamedState &st, const double *m, const doub
   a.Fout = j.Fout;
   a.fk_sys_lo = a.fk_sys_hi = 0;
   if (j.fk_ln >= j.ln0) {
-    a.fk_sys_lo = (j.fk_ln - j.ln0) * B;
-    a.fk_sys_hi = a.fk_sys_lo + B;
+    a.fk_sys_lo = (j.fk_ln - j.ln0) * p.B;
+    a.fk_sys_hi = a.fk_sys_lo + p.B;
   }
-  return streamed_steps(st, a, j.U + off, steps, s, nl);
+  return streamed_steps(st, a, j.U + off, p.steps, s, nl);
 }
 
-inline cudaError_t streamed_chain(StreamedState &st, const double *m, const double *ip, const double *cu,
-                                  const int *fset, const double *bcoef, const double *L, const double *K,
-                                  const double *r, int upper_bc, double dT, double dtau, int steps, int M, int Mp,
-                                  int B, const StreamedChainJob &j, cudaStream_t s, int *nl) {
+cudaError_t streamed_chain(StreamedState &st, const StreamedProblem &p, const StreamedChainJob &j,
+                           cudaStream_t s, int *nl) {
   if (j.Fcopy) {
-    dim3 grid((M + 255) / 256, B);
-    k_copy_delta<<<grid, 256, 0, s>>>(j.U + (size_t)j.ln0 * j.ustride, j.Fcopy, M, Mp,
-                                      j.partials ? j.partials + (size_t)j.ln0 * B * j.nch * 2 : nullptr, B, j.nch);
+    dim3 grid((p.M + 255) / 256, p.B);
+    k_copy_delta<<<grid, 256, 0, s>>>(j.U + (size_t)j.ln0 * j.ustride, j.Fcopy, p.M, p.Mp,
+                                      j.partials ? j.partials + (size_t)j.ln0 * p.B * j.nch * 2 : nullptr, p.B,
+                                      j.nch);
     *nl += 1;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
-  PassArgs a = pass_base(m, ip, cu, fset, bcoef, L, K, r, upper_bc, dT, dtau, M, Mp, B);
-  a.nsys = B;
+  PassArgs a = pass_base(p);
+  a.nsys = p.B;
   a.epi = EPI_CHAIN;
   a.nch = j.nch;
   for (int ln = j.ln0; ln < j.ln1; ++ln) {
     a.n_base = j.n_base + ln;  // one slice per launch: system s = instance b, ln0 = 0
     a.ln0 = 0;
     a.Unext = j.U + (size_t)(ln + 1) * j.ustride;
-    a.GhW = j.Gh ? j.Gh + (size_t)ln * B * Mp : nullptr;
-    a.Dc = j.D ? j.D + (size_t)ln * B * Mp : nullptr;
-    a.partials = j.partials ? j.partials + (size_t)(ln + 1) * B * j.nch * 2 : nullptr;
-    cudaError_t e = streamed_steps(st, a, j.U + (size_t)ln * j.ustride, steps, s, nl);
+    a.GhW = j.Gh ? j.Gh + (size_t)ln * p.B * p.Mp : nullptr;
+    a.Dc = j.D ? j.D + (size_t)ln * p.B * p.Mp : nullptr;
+    a.partials = j.partials ? j.partials + (size_t)(ln + 1) * p.B * j.nch * 2 : nullptr;
+    cudaError_t e = streamed_steps(st, a, j.U + (size_t)ln * j.ustride, p.steps, s, nl);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
 }
 
 }  // namespace pr
+#endif  // PR_FINE_STREAMED_IMPL

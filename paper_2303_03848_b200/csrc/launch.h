@@ -1,0 +1,35 @@
+// launch.h — argument structs and the launchers each kernel translation unit exports to
+// the host code (parareal.cu).  Kernel bodies are compiled only in their own .cu file.
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+#define PR_ARGS_ONLY
+#include "fine_resident.cuh"
+#include "fine_streamed.cuh"
+#include "pinn_chain.cuh"
+#undef PR_ARGS_ONLY
+
+namespace pr {
+// K1 (res.cu): sweep (chain=false) or serial chain (chain=true) over nsys systems
+cudaError_t launch_resident(bool chain, int M, const ResidentArgs &a, int nsys, cudaStream_t s);
+// K3, shared-memory weights (pinn_smem.cu)
+bool pinn_smem_supported(int IN, int W, int act);
+int pinn_smem_pts(int W);
+cudaError_t pinn_smem_prepare(int IN, int W, int act, int smem_bytes);
+cudaError_t launch_pinn_smem(int IN, int W, int act, const PinnArgs &a, dim3 grid, size_t smem, cudaStream_t s);
+// K3 latency mode: kPinnSplitG threads per point (pinn_smem.cu)
+constexpr int kPinnSplitG = 4;
+bool pinn_split_supported(int IN, int W, int act);
+cudaError_t pinn_split_prepare(int IN, int W, int act, int smem_bytes);
+cudaError_t launch_pinn_split(int IN, int W, int act, const PinnArgs &a, dim3 grid, size_t smem, cudaStream_t s);
+// K3, constant-bank weights (pinn_param.cu)
+bool pinn_param_supported(int IN, int W, int LH, int act);
+cudaError_t launch_pinn_param(int IN, int W, int LH, int act, const float *pk, const PinnArgs &a, dim3 grid,
+                              cudaStream_t s);
+// K6/K7 (misc.cu)
+cudaError_t launch_payoff(float *U0, int M, int Mp, int B, const double *Lb, const double *Kb, cudaStream_t s);
+cudaError_t launch_delta(const double *partials, int B, int nch, int ln_lo, int ln_hi, unsigned long long *dmax,
+                         cudaStream_t s);
+}  // namespace pr

@@ -18,10 +18,7 @@
 #include <utility>
 #include <vector>
 
-#include "fine_resident.cuh"
-#include "fine_streamed.cuh"
-#include "misc_kernels.cuh"
-#include "pinn_chain.cuh"
+#include "launch.h"
 
 // ============================================================================ NCCL (dlopen)
 // NCCL is resolved at run time so the library loads without it (world == 1 never touches
@@ -91,7 +88,10 @@ std::string fmt(const char *f, ...) {
 struct Scheme {
   double dtau = 0;
   int steps = 0;
-  double *m = nullptr, *ip = nullptr, *cu = nullptr;  // device [nsets][Mp]
+  double *m = nullptr, *ip = nullptr, *cu = nullptr;  // device [nsets][Mp] (K1)
+  double *im = nullptr, *iip = nullptr, *icu = nullptr;  // device [nsets][Mt], interleaved (K2)
+  double *tileB = nullptr;                          // device [2][nsets][ntiles] (K2 look-back)
+  int *tileW = nullptr;
   double *bcoef = nullptr;                          // device [B]
 };
 
@@ -135,7 +135,9 @@ struct pr_ctx {
   int IN = 4, W = 0, LH = 0, act = 0, nfloats = 0;
   float cs[4] = {1, 1, 1, 1}, out_scale = 1;
   float *d_wts = nullptr;
+  std::vector<float> h_wts;  // packed copy for the parameter-space kernels
   // options
+  int opt_pinn_kernel = 0;
   int opt_fine_kernel = 0;
   int opt_graphs = 0;
   int64_t launches = 0;
@@ -234,6 +236,58 @@ pr_status upload_scheme(pr_ctx *c, Scheme &sc, int steps) {
   CU(cudaMemcpy(sc.m, m.data(), n * sizeof(double), cudaMemcpyHostToDevice));
   CU(cudaMemcpy(sc.ip, ip.data(), n * sizeof(double), cudaMemcpyHostToDevice));
   CU(cudaMemcpy(sc.cu, cu.data(), n * sizeof(double), cudaMemcpyHostToDevice));
+  // the same factors in K2's thread-interleaved layout, identity-padded to Mt
+  const int Mt = pr::streamed_Mt(c->M);
+  std::vector<double> im((size_t)c->nsets * Mt, 0.0), iip((size_t)c->nsets * Mt, 1.0), icu((size_t)c->nsets * Mt, 0.0);
+  for (int s = 0; s < c->nsets; ++s)
+    for (int j = 0; j < c->M; ++j) {
+      const size_t d = (size_t)s * Mt + pr::il_index(j), o = (size_t)s * c->Mp + j;
+      im[d] = m[o];
+      iip[d] = ip[o];
+      icu[d] = cu[o];
+    }
+  const size_t ni = im.size() * sizeof(double);
+  CU(cudaMalloc(&sc.im, ni));
+  CU(cudaMalloc(&sc.iip, ni));
+  CU(cudaMalloc(&sc.icu, ni));
+  CU(cudaMemcpy(sc.im, im.data(), ni, cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(sc.iip, iip.data(), ni, cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(sc.icu, icu.data(), ni, cudaMemcpyHostToDevice));
+  // K2 look-back data, indexed by scan position (dir 0: tiles ascending, dir 1: descending):
+  // tile multiplier B = Π(−m_j) resp. Π(−u_j/p_j) over the tile, and the window W = number of
+  // predecessors whose aggregates are composed: the first W with |Π_{k≤W} B_{pos−k}| below
+  // kLookbackEps (all predecessors if never).
+  const int nt = pr::streamed_ntiles(c->M);
+  std::vector<double> tB((size_t)2 * c->nsets * nt);
+  std::vector<int> tW((size_t)2 * c->nsets * nt);
+  for (int dir = 0; dir < 2; ++dir)
+    for (int s = 0; s < c->nsets; ++s) {
+      const size_t base = ((size_t)dir * c->nsets + s) * nt;
+      for (int pos = 0; pos < nt; ++pos) {
+        const int tile = dir == 0 ? pos : nt - 1 - pos;
+        double prod = 1.0;
+        for (int j = tile * pr::kSTile; j < std::min((tile + 1) * pr::kSTile, c->M); ++j)
+          prod *= dir == 0 ? -m[(size_t)s * c->Mp + j] : -cu[(size_t)s * c->Mp + j];
+        if ((tile + 1) * pr::kSTile > c->M && dir == 0) prod = 0.0;  // identity padding: m = 0
+        tB[base + pos] = prod;
+      }
+      for (int pos = 0; pos < nt; ++pos) {
+        double P = 1.0;
+        int W = pos;
+        for (int k = 1; k <= pos; ++k) {
+          P *= tB[base + pos - k];
+          if (std::fabs(P) < pr::kLookbackEps) {
+            W = k;
+            break;
+          }
+        }
+        tW[base + pos] = W;
+      }
+    }
+  CU(cudaMalloc(&sc.tileB, tB.size() * sizeof(double)));
+  CU(cudaMalloc(&sc.tileW, tW.size() * sizeof(int)));
+  CU(cudaMemcpy(sc.tileB, tB.data(), tB.size() * sizeof(double), cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(sc.tileW, tW.data(), tW.size() * sizeof(int), cudaMemcpyHostToDevice));
   std::vector<double> bc(c->B);
   for (int b = 0; b < c->B; ++b) {
     const double sg = c->sig[b], rr = c->r[b], j = c->M;
@@ -245,11 +299,39 @@ pr_status upload_scheme(pr_ctx *c, Scheme &sc, int steps) {
 }
 
 void free_scheme(Scheme &s) {
+  cudaFree(s.tileB);
+  cudaFree(s.tileW);
+  cudaFree(s.im);
+  cudaFree(s.iip);
+  cudaFree(s.icu);
   cudaFree(s.m);
   cudaFree(s.ip);
   cudaFree(s.cu);
   cudaFree(s.bcoef);
   s = Scheme();
+}
+
+pr::StreamedProblem sprob(const pr_ctx *c, const Scheme &sc) {
+  pr::StreamedProblem p;
+  p.f.m = sc.im;
+  p.f.ip = sc.iip;
+  p.f.cu = sc.icu;
+  p.f.tileB = sc.tileB;
+  p.f.tileW = sc.tileW;
+  p.nsets = c->nsets;
+  p.fset = c->d_fset;
+  p.bcoef = sc.bcoef;
+  p.L = c->d_L;
+  p.K = c->d_K;
+  p.r = c->d_r;
+  p.upper_bc = c->upper_bc;
+  p.dT = c->dT;
+  p.dtau = sc.dtau;
+  p.steps = sc.steps;
+  p.M = c->M;
+  p.Mp = c->Mp;
+  p.B = c->B;
+  return p;
 }
 
 bool use_resident(const pr_ctx *c) {
@@ -330,43 +412,25 @@ pr::ResidentArgs base_args(pr_ctx *c, const Scheme &sc) {
   return a;
 }
 
-template <int P, int NT, int SPB>
-void launch_res(bool chain, const pr::ResidentArgs &a, int nsys, cudaStream_t s) {
-  const int grid = (nsys + SPB - 1) / SPB;
-  if (chain)
-    pr::k_resident_chain<P, NT, SPB><<<grid, NT * SPB, 0, s>>>(a);
-  else
-    pr::k_fine_sweep<P, NT, SPB><<<grid, NT * SPB, 0, s>>>(a);
-}
-
 void dispatch_res(bool chain, int M, const pr::ResidentArgs &a, int nsys, cudaStream_t s) {
-  if (M <= 64) launch_res<2, 32, 4>(chain, a, nsys, s);
-  else if (M <= 128) launch_res<4, 32, 4>(chain, a, nsys, s);
-  else if (M <= 256) launch_res<8, 32, 4>(chain, a, nsys, s);
-  else if (M <= 512) launch_res<8, 64, 2>(chain, a, nsys, s);
-  else if (M <= 1024) launch_res<8, 128, 1>(chain, a, nsys, s);
-  else launch_res<8, 256, 1>(chain, a, nsys, s);
+  pr::launch_resident(chain, M, a, nsys, s);
 }
 
 // ---------------------------------------------------------------- PINN launches
-typedef void (*PinnKernel)(pr::PinnArgs);
-template <int IN, int ACT>
-PinnKernel pinn_kernel_w(int W) {
-  switch (W) {
-    case 8: return pr::k_pinn_chain<IN, 8, ACT, 2>;
-    case 16: return pr::k_pinn_chain<IN, 16, ACT, 2>;
-    case 20: return pr::k_pinn_chain<IN, 20, ACT, 2>;
-    case 32: return pr::k_pinn_chain<IN, 32, ACT, 2>;
-    case 50: return pr::k_pinn_chain<IN, 50, ACT, 1>;
-    case 64: return pr::k_pinn_chain<IN, 64, ACT, 1>;
-  }
-  return nullptr;
+// Few grid points (B·M ≤ kSplitMaxPoints): the coarse chain is latency-bound, so the latency
+// mode (kPinnSplitG threads per point) runs it; otherwise constant-bank weights when instantiated,
+// else shared-memory weights.  PR_OPT_PINN_KERNEL: 0 auto, 1 shared memory, 2 latency mode.
+constexpr long kSplitMaxPoints = 65536;
+bool split_allowed(const pr_ctx *c) { return (long)c->B * c->M <= kSplitMaxPoints; }
+bool use_split_pinn(const pr_ctx *c) {
+  if (c->opt_pinn_kernel == 1) return false;
+  if (c->opt_pinn_kernel == 0 && !split_allowed(c)) return false;
+  return pr::pinn_split_supported(c->IN, c->W, c->act);
 }
-PinnKernel pinn_kernel(int IN, int W, int act) {
-  if (IN == 4) return act ? pinn_kernel_w<4, 1>(W) : pinn_kernel_w<4, 0>(W);
-  return act ? pinn_kernel_w<2, 1>(W) : pinn_kernel_w<2, 0>(W);
+bool use_param_pinn(const pr_ctx *c) {
+  if (c->opt_pinn_kernel != 0 || use_split_pinn(c)) return false;
+  return pr::pinn_param_supported(c->IN, c->W, c->LH, c->act);
 }
-int pinn_pts(int W) { return W <= 32 ? 2 : 1; }
 
 pr::PinnArgs pinn_args(pr_ctx *c) {
   pr::PinnArgs a;
@@ -391,19 +455,25 @@ pr::PinnArgs pinn_args(pr_ctx *c) {
 }
 
 pr_status launch_pinn(pr_ctx *c, const pr::PinnArgs &a) {
-  PinnKernel k = pinn_kernel(c->IN, c->W, c->act);
-  if (!k) return fail(c, PR_ERR_UNSUPPORTED, "no PINN kernel for this width");
-  const int pts = pinn_pts(c->W);
+  if (use_split_pinn(c)) {
+    constexpr int ppc = kPinnTPB / pr::kPinnSplitG;  // points per CTA
+    dim3 grid((c->M + ppc - 1) / ppc, c->B);
+    pr::launch_pinn_split(c->IN, c->W, c->act, a, grid, (size_t)c->nfloats * sizeof(float), c->stream);
+    LAUNCHED();
+    return PR_OK;
+  }
+  if (use_param_pinn(c)) {
+    dim3 grid((c->M + kPinnTPB - 1) / kPinnTPB, c->B);
+    pr::launch_pinn_param(c->IN, c->W, c->LH, c->act, c->h_wts.data(), a, grid, c->stream);
+    LAUNCHED();
+    return PR_OK;
+  }
+  if (!pr::pinn_smem_supported(c->IN, c->W, c->act)) return fail(c, PR_ERR_UNSUPPORTED, "no PINN kernel for this width");
+  const int pts = pr::pinn_smem_pts(c->W);
   dim3 grid((c->M + kPinnTPB * pts - 1) / (kPinnTPB * pts), c->B);
-  const size_t smem = (size_t)c->nfloats * sizeof(float);
-  k<<<grid, kPinnTPB, smem, c->stream>>>(a);
+  pr::launch_pinn_smem(c->IN, c->W, c->act, a, grid, (size_t)c->nfloats * sizeof(float), c->stream);
   LAUNCHED();
   return PR_OK;
-}
-
-int pinn_chunks(const pr_ctx *c, int W) {
-  const int pts = pinn_pts(W);
-  return (c->M + kPinnTPB * pts - 1) / (kPinnTPB * pts);
 }
 
 // ---------------------------------------------------------------- phases of one iteration
@@ -429,9 +499,7 @@ pr_status fine_sweep(pr_ctx *c, int ln_lo, int fk_ln) {
   j.U = c->U; j.Gh = c->Gh; j.D = c->D; j.Fk = c->Fk; j.fk_ln = fk_ln; j.Fout = nullptr;
   j.ln0 = ln_lo; j.nsl = nsl; j.n_base = c->n0;
   int nl = 0;
-  cudaError_t e = pr::streamed_sweep(c->sst, c->fine.m, c->fine.ip, c->fine.cu, c->d_fset, c->fine.bcoef,
-                                     c->d_L, c->d_K, c->d_r, c->upper_bc, c->dT, c->fine.dtau, c->fine.steps,
-                                     c->M, c->Mp, c->B, j, c->stream, &nl);
+  cudaError_t e = pr::streamed_sweep(c->sst, sprob(c, c->fine), j, c->stream, &nl);
   c->launches += nl;
   if (e != cudaSuccess) return fail(c, PR_ERR_CUDA, fmt("streamed sweep: %s", cudaGetErrorString(e)));
   return PR_OK;
@@ -461,9 +529,7 @@ pr_status coarse_chain(pr_ctx *c, int k, int ln0, bool copy) {
     j.partials = corr ? c->partials : nullptr; j.nch = c->nch;
     j.ln0 = ln0; j.ln1 = c->Nloc; j.n_base = c->n0; j.ustride = (size_t)c->B * c->Mp;
     int nl = 0;
-    cudaError_t e = pr::streamed_chain(c->sst, c->crs.m, c->crs.ip, c->crs.cu, c->d_fset, c->crs.bcoef, c->d_L,
-                                       c->d_K, c->d_r, c->upper_bc, c->dT, c->crs.dtau, c->crs.steps, c->M,
-                                       c->Mp, c->B, j, c->stream, &nl);
+    cudaError_t e = pr::streamed_chain(c->sst, sprob(c, c->crs), j, c->stream, &nl);
     c->launches += nl;
     if (e != cudaSuccess) return fail(c, PR_ERR_CUDA, fmt("streamed chain: %s", cudaGetErrorString(e)));
     return PR_OK;
@@ -487,7 +553,8 @@ pr_status delta_reduce(pr_ctx *c, int k, int ln_lo, int ln_hi, int nch) {
   CU(cudaMemsetAsync(slot, 0, sizeof(unsigned long long), c->stream));
   if (ln_hi >= ln_lo) {
     const int total = (ln_hi - ln_lo + 1) * c->B;
-    pr::k_delta<<<(total + 255) / 256, 256, 0, c->stream>>>(c->partials, c->B, nch, ln_lo, ln_hi, slot);
+    (void)total;
+    pr::launch_delta(c->partials, c->B, nch, ln_lo, ln_hi, slot, c->stream);
     LAUNCHED();
   }
   if (c->world > 1) {
@@ -507,8 +574,7 @@ pr_status load_initial(pr_ctx *c, const float *V_T, bool device_ptr) {
                            device_ptr ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->stream));
     }
   } else {
-    dim3 grid((c->Mp + 255) / 256, c->B);
-    pr::k_payoff<<<grid, 256, 0, c->stream>>>(c->U, c->M, c->Mp, c->B, c->d_L, c->d_K);
+    pr::launch_payoff(c->U, c->M, c->Mp, c->B, c->d_L, c->d_K, c->stream);
     LAUNCHED();
   }
   return PR_OK;
@@ -722,9 +788,7 @@ pr_status serial_fine_impl(pr_ctx *c, const float *V_T, float *V_0, bool device_
     j.U = c->tmp; j.Gh = nullptr; j.D = nullptr; j.Fcopy = nullptr; j.partials = nullptr; j.nch = 1;
     j.ln0 = 0; j.ln1 = c->N; j.n_base = 0; j.ustride = 0;
     int nl = 0;
-    cudaError_t e = pr::streamed_chain(c->sst, c->fine.m, c->fine.ip, c->fine.cu, c->d_fset, c->fine.bcoef,
-                                       c->d_L, c->d_K, c->d_r, c->upper_bc, c->dT, c->fine.dtau, c->fine.steps,
-                                       c->M, c->Mp, c->B, j, c->stream, &nl);
+    cudaError_t e = pr::streamed_chain(c->sst, sprob(c, c->fine), j, c->stream, &nl);
     c->launches += nl;
     if (e != cudaSuccess) return fail(c, PR_ERR_CUDA, fmt("streamed serial fine: %s", cudaGetErrorString(e)));
   }
@@ -891,6 +955,7 @@ pr_status parareal_init(const pr_problem *p, const pr_dist *dist, pr_ctx **out) 
   // δ partial chunks per (slice, instance): upper bound over every producer (PINN CTAs with one
   // point per thread, 256-wide copy blocks, streamed tiles, one resident system)
   c->nch = std::max(1, (c->M + kPinnTPB - 1) / kPinnTPB);
+  if (split_allowed(c)) c->nch = std::max(1, (c->M * pr::kPinnSplitG + kPinnTPB - 1) / kPinnTPB);
   if (dd.world > 1) {
     Nccl &n = nccl();
     if (!n.ok) {
@@ -952,24 +1017,30 @@ pr_status parareal_load_pinn_weights(pr_ctx *c, int32_t n_linear, const int32_t 
     if (precision < 0 || precision > PR_PREC_TF32_TC) return fail(c, PR_ERR_INVALID_ARGUMENT, fmt("precision=%d unknown", precision));
     return fail(c, PR_ERR_UNSUPPORTED, "tensor-core PINN precisions are not in this build");
   }
-  if (!pinn_kernel(dims[0], Wd, activation))
+  if (!pr::pinn_smem_supported(dims[0], Wd, activation))
     return fail(c, PR_ERR_UNSUPPORTED, fmt("hidden width %d not instantiated (8,16,20,32,50,64)", Wd));
   for (int l = 0; l < n_linear; ++l)
     if (!W[l] || !b[l]) return fail(c, PR_ERR_INVALID_ARGUMENT, fmt("W[%d]/b[%d] is NULL", l, l));
   const int IN = dims[0], LH = n_linear - 1;
+  // packed W_l then b_l per layer; the layers feeding a tanh are pre-scaled by 2·log2(e) so the
+  // kernels evaluate tanh(z) = 1 − 2/(2^{z'} + 1) on z' = 2·log2(e)·z (pinn_chain.cuh)
+  const double kTanhScale = 2.0 * 1.4426950408889634;  // 2·log2(e)
   std::vector<float> pk;
   for (int l = 0; l < n_linear; ++l) {
-    pk.insert(pk.end(), W[l], W[l] + (size_t)dims[l + 1] * dims[l]);
-    pk.insert(pk.end(), b[l], b[l] + dims[l + 1]);
+    const bool pre = activation == PR_ACT_TANH && l < n_linear - 1;
+    const size_t nw = (size_t)dims[l + 1] * dims[l];
+    for (size_t i = 0; i < nw; ++i) pk.push_back(pre ? (float)(kTanhScale * W[l][i]) : W[l][i]);
+    for (int i = 0; i < dims[l + 1]; ++i) pk.push_back(pre ? (float)(kTanhScale * b[l][i]) : b[l][i]);
   }
   const size_t bytes = pk.size() * sizeof(float);
   if (bytes > 200 * 1024) return fail(c, PR_ERR_UNSUPPORTED, fmt("network of %zu bytes exceeds the shared-memory budget", bytes));
-  PinnKernel k = pinn_kernel(IN, Wd, activation);
-  CU(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  CU(pr::pinn_smem_prepare(IN, Wd, activation, (int)bytes));
+  if (pr::pinn_split_supported(IN, Wd, activation)) CU(pr::pinn_split_prepare(IN, Wd, activation, (int)bytes));
   if (c->d_wts) cudaFree(c->d_wts);
   c->d_wts = nullptr;
   CU(cudaMalloc(&c->d_wts, bytes));
   CU(cudaMemcpy(c->d_wts, pk.data(), bytes, cudaMemcpyHostToDevice));
+  c->h_wts = pk;
   c->IN = IN;
   c->W = Wd;
   c->LH = LH;
@@ -1049,9 +1120,7 @@ pr_status parareal_apply_fine(pr_ctx *c, int32_t n, const float *U_in, float *U_
     j.U = c->tmp; j.Gh = nullptr; j.D = nullptr; j.Fk = nullptr; j.fk_ln = -1; j.Fout = c->tmp + row;
     j.ln0 = 0; j.nsl = 1; j.n_base = n;
     int nl = 0;
-    cudaError_t e = pr::streamed_sweep(c->sst, c->fine.m, c->fine.ip, c->fine.cu, c->d_fset, c->fine.bcoef,
-                                       c->d_L, c->d_K, c->d_r, c->upper_bc, c->dT, c->fine.dtau, c->fine.steps,
-                                       c->M, c->Mp, c->B, j, c->stream, &nl);
+    cudaError_t e = pr::streamed_sweep(c->sst, sprob(c, c->fine), j, c->stream, &nl);
     c->launches += nl;
     if (e != cudaSuccess) return fail(c, PR_ERR_CUDA, fmt("streamed apply: %s", cudaGetErrorString(e)));
   }
@@ -1097,9 +1166,7 @@ pr_status parareal_apply_coarse(pr_ctx *c, int32_t n, const float *U_in, float *
     j.U = c->tmp; j.Gh = nullptr; j.D = nullptr; j.Fcopy = nullptr; j.partials = nullptr; j.nch = 1;
     j.ln0 = 0; j.ln1 = 1; j.n_base = n; j.ustride = 0;
     int nl = 0;
-    cudaError_t e = pr::streamed_chain(c->sst, c->crs.m, c->crs.ip, c->crs.cu, c->d_fset, c->crs.bcoef, c->d_L,
-                                       c->d_K, c->d_r, c->upper_bc, c->dT, c->crs.dtau, c->crs.steps, c->M, c->Mp,
-                                       c->B, j, c->stream, &nl);
+    cudaError_t e = pr::streamed_chain(c->sst, sprob(c, c->crs), j, c->stream, &nl);
     c->launches += nl;
     if (e != cudaSuccess) return fail(c, PR_ERR_CUDA, fmt("streamed coarse apply: %s", cudaGetErrorString(e)));
     if ((st = store_rows(c, U_out, c->tmp, false))) return st;
@@ -1142,6 +1209,12 @@ pr_status parareal_set_option(pr_ctx *c, int32_t key, int64_t value) {
       if (value == 1 && c->M > kResidentMaxM)
         return fail(c, PR_ERR_UNSUPPORTED, fmt("resident fine kernel needs M <= %d", kResidentMaxM));
       c->opt_fine_kernel = (int)value;
+      return PR_OK;
+    case PR_OPT_PINN_KERNEL:
+      if (value < 0 || value > 2) return fail(c, PR_ERR_INVALID_ARGUMENT, "PR_OPT_PINN_KERNEL must be 0, 1 or 2");
+      if (value == 2 && !split_allowed(c))
+        return fail(c, PR_ERR_UNSUPPORTED, fmt("latency-mode PINN kernel needs B*M <= %ld", kSplitMaxPoints));
+      c->opt_pinn_kernel = (int)value;
       return PR_OK;
     case PR_OPT_USE_GRAPHS:
       if (value < 0 || value > 1) return fail(c, PR_ERR_INVALID_ARGUMENT, "PR_OPT_USE_GRAPHS must be 0 or 1");

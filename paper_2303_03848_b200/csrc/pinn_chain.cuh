@@ -9,10 +9,11 @@
 // with its weights in shared memory (uniform addresses → broadcast reads),
 // activations in registers, hidden width W a template parameter so every
 // layer is a fully unrolled W×W FMA block.
-#pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#ifndef PR_PINN_CHAIN_ARGS
+#define PR_PINN_CHAIN_ARGS
 namespace pr {
 
 struct PinnArgs {
@@ -35,10 +36,28 @@ struct PinnArgs {
   float *Gout;             // test hook: non-null → write G_{ln0}(U[ln0]) only, no chain
 };
 
+}  // namespace pr
+#endif  // PR_PINN_CHAIN_ARGS
+
+#if !defined(PR_ARGS_ONLY) && !defined(PR_PINN_CHAIN_IMPL)
+#define PR_PINN_CHAIN_IMPL
+namespace pr {
+// tanh with the argument pre-scaled: the host multiplies the weights and biases of every
+// tanh layer by 2·log2(e), so the layer produces z' = 2·log2(e)·z and
+//     tanh(z) = 1 − 2 / (2^{z'} + 1)          (MUFU.EX2, FADD, MUFU.RCP, FFMA: 4 instructions)
+// ex2.approx and rcp.approx are accurate to ~2^-22 relative, so |error| ≲ 2e-7 absolute; the
+// limits are exact (2^{z'} → ∞ gives 1, → 0 gives −1).  This is NOT tanh.approx.f32 (2^-11).
+__device__ __forceinline__ float tanh_prescaled(float zs) {
+  float e, r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(zs));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(e + 1.0f));
+  return fmaf(-2.0f, r, 1.0f);
+}
+
 template <int ACT>
 __device__ __forceinline__ float act(float z) {
   if (ACT == 1) return fmaxf(z, 0.0f);
-  return tanhf(z);
+  return tanh_prescaled(z);
 }
 
 // fixed-order CTA reduction of (a, b); result valid in thread 0
@@ -107,22 +126,26 @@ __device__ __forceinline__ void mlp_eval(const float *__restrict__ sw, int LH, c
   }
 }
 
-template <int IN, int W, int ACT, int PTS>
-__global__ void __launch_bounds__(128) k_pinn_chain(PinnArgs a) {
-  extern __shared__ float sw[];
+// The chain over slices shared by all network evaluators (`ev(x, y)` evaluates the MLP).
+// G threads cooperate on one point when G > 1 (PTS = 1): all of them evaluate (the evaluator
+// exchanges activations by shuffles), only the group's first thread stores and counts δ.
+template <int IN, int PTS, class Eval, int G = 1>
+__device__ __forceinline__ void pinn_chain_body(const PinnArgs &a, Eval ev) {
+  static_assert(G == 1 || PTS == 1, "grouped evaluation handles one point per group");
   __shared__ double red[2 * 32];
-  for (int i = threadIdx.x; i < a.nfloats; i += blockDim.x) sw[i] = a.wts[i];
-  __syncthreads();
   const int b = blockIdx.y;
   const double Lb = a.Lb[b];
   const float gscale = (float)(Lb * (double)a.out_scale);
+  const float invL = (float)(1.0 / Lb);
   const size_t sstride = (size_t)a.B * a.Mp;
+  const bool leader = (G == 1) || (threadIdx.x % G == 0);
   int j[PTS];
   bool ok[PTS];
   float s_over_L[PTS], u[PTS];
 #pragma unroll
   for (int p = 0; p < PTS; ++p) {
-    j[p] = blockIdx.x * (blockDim.x * PTS) + p * blockDim.x + threadIdx.x;
+    j[p] = (G == 1) ? blockIdx.x * (blockDim.x * PTS) + p * blockDim.x + threadIdx.x
+                    : blockIdx.x * (blockDim.x / G) + threadIdx.x / G;
     ok[p] = j[p] < a.M;
     // S_j / L_b = j dS / L_b with dS = L_b / (M+1)  (reading Q4, Q8)
     const double dS = Lb / (a.M + 1);
@@ -137,11 +160,17 @@ __global__ void __launch_bounds__(128) k_pinn_chain(PinnArgs a) {
       u[p] = 0.f;
       if (ok[p]) {
         u[p] = f[j[p]];
-        const double dd = (double)u[p] - (double)u0[j[p]];
-        num += dd * dd;
-        den += (double)u[p] * u[p];
-        u0[j[p]] = u[p];
+        if (leader) {
+          const double dd = (double)u[p] - (double)u0[j[p]];
+          num += dd * dd;
+          den += (double)u[p] * u[p];
+        }
       }
+    }
+    __syncthreads();  // every thread of the CTA has read U[ln0] before it is overwritten
+#pragma unroll
+    for (int p = 0; p < PTS; ++p) {
+      if (ok[p] && leader) u0[j[p]] = u[p];
     }
     if (a.partials) {
       cta_reduce2(num, den, red);
@@ -159,26 +188,35 @@ __global__ void __launch_bounds__(128) k_pinn_chain(PinnArgs a) {
 #pragma unroll 1
   for (int ln = a.ln0; ln < ln_end; ++ln) {
     const int n = a.n_base + ln;
-    const double t_from = a.T - n * a.dT, t_to = a.T - (n + 1) * a.dT;
+    // t_from/T, t_to/T (reading Q7): uniform per slice
+    const float tf = (float)((a.T - n * a.dT) / a.T), tt = (float)((a.T - (n + 1) * a.dT) / a.T);
+    // issue this slice's loads (D_n, old U_{n+1}) before the network so their latency hides
+    // behind it (loads ahead of this iteration's stores: no aliasing hazard)
+    const size_t row = (size_t)ln * sstride + (size_t)b * a.Mp;
+    float dn[PTS], uo[PTS];
+#pragma unroll
+    for (int p = 0; p < PTS; ++p) {
+      dn[p] = (a.D && ok[p]) ? __ldcg(a.D + row + j[p]) : 0.f;
+      uo[p] = (a.partials && ok[p]) ? __ldcg(a.U + row + sstride + j[p]) : 0.f;
+    }
     float x[PTS][IN], y[PTS];
 #pragma unroll
     for (int p = 0; p < PTS; ++p) {
       if (IN == 4) {
-        x[p][0] = (float)(t_from / a.T) * a.cs0;
-        x[p][1] = (float)(t_to / a.T) * a.cs1;
-        x[p][2] = (float)((double)u[p] / Lb) * a.cs2;
+        x[p][0] = tf * a.cs0;
+        x[p][1] = tt * a.cs1;
+        x[p][2] = (u[p] * invL) * a.cs2;  // V/L_b (reading Q8); fp32, ≤ 1.5 ulp
         x[p][3] = s_over_L[p] * a.cs3;
       } else {
-        x[p][0] = (float)(t_to / a.T) * a.cs0;
+        x[p][0] = tt * a.cs0;
         x[p][IN - 1] = s_over_L[p] * a.cs1;
       }
     }
-    mlp_eval<IN, W, ACT, PTS>(sw, a.LH, x, y);
-    const size_t row = (size_t)ln * sstride + (size_t)b * a.Mp;
+    ev(x, y);
     if (a.Gout) {
 #pragma unroll
       for (int p = 0; p < PTS; ++p)
-        if (ok[p]) a.Gout[(size_t)b * a.Mp + j[p]] = gscale * y[p];
+        if (ok[p] && leader) a.Gout[(size_t)b * a.Mp + j[p]] = gscale * y[p];
       return;
     }
     float *un = a.U + row + sstride;
@@ -188,14 +226,16 @@ __global__ void __launch_bounds__(128) k_pinn_chain(PinnArgs a) {
       const float g = gscale * y[p];
       float nv = 0.f;
       if (ok[p]) {
-        if (a.Gh) a.Gh[row + j[p]] = g;
-        nv = a.D ? g + a.D[row + j[p]] : g;
-        if (a.partials) {
-          const double dd = (double)nv - (double)un[j[p]];
-          num += dd * dd;
-          den += (double)nv * nv;
+        nv = a.D ? g + dn[p] : g;
+        if (leader) {
+          if (a.Gh) a.Gh[row + j[p]] = g;
+          if (a.partials) {
+            const double dd = (double)nv - (double)uo[p];
+            num += dd * dd;
+            den += (double)nv * nv;
+          }
+          un[j[p]] = nv;
         }
-        un[j[p]] = nv;
       }
       u[p] = nv;
     }
@@ -210,4 +250,111 @@ __global__ void __launch_bounds__(128) k_pinn_chain(PinnArgs a) {
   }
 }
 
+
+// Latency mode for few grid points: G threads share one point, thread q owning neurons
+// [q·W/G, (q+1)·W/G) of every layer; after each layer the W activations are gathered with
+// warp shuffles.  Per-thread work per slice drops ~G× (the coarse chain is serial in n, so at
+// small M its length is what the GPU can hide least).  Weights in shared memory.
+template <int IN, int W, int G, int ACT>
+__device__ __forceinline__ float mlp_split(const float *__restrict__ sw, int LH, const float (&x)[IN]) {
+  constexpr int NPT = W / G;
+  const int lane = threadIdx.x & 31, q = lane % G, gbase = lane - q;
+  float own[NPT], h[W];
+#pragma unroll
+  for (int k = 0; k < NPT; ++k) {
+    const int o = q * NPT + k;
+    float z = sw[W * IN + o];
+#pragma unroll
+    for (int i = 0; i < IN; ++i) z = fmaf(sw[o * IN + i], x[i], z);
+    own[k] = act<ACT>(z);
+  }
+  const float *lw = sw + W * IN + W;
+#pragma unroll 1
+  for (int l = 1; l < LH; ++l) {
+#pragma unroll
+    for (int i = 0; i < W; ++i) h[i] = __shfl_sync(0xffffffffu, own[i % NPT], gbase + i / NPT);
+#pragma unroll
+    for (int k = 0; k < NPT; ++k) {
+      const int o = q * NPT + k;
+      float z = lw[W * W + o];
+#pragma unroll
+      for (int i = 0; i < W; ++i) z = fmaf(lw[o * W + i], h[i], z);
+      own[k] = act<ACT>(z);
+    }
+    lw += W * W + W;
+  }
+  float y = 0.f;
+#pragma unroll
+  for (int k = 0; k < NPT; ++k) y = fmaf(lw[q * NPT + k], own[k], y);
+#pragma unroll
+  for (int d = 1; d < G; d <<= 1) y += __shfl_xor_sync(0xffffffffu, y, d);
+  return y + lw[W];
+}
+
+template <int IN, int W, int G, int ACT>
+__global__ void __launch_bounds__(128) k_pinn_chain_split(PinnArgs a) {
+  extern __shared__ float sw[];
+  for (int i = threadIdx.x; i < a.nfloats; i += blockDim.x) sw[i] = a.wts[i];
+  __syncthreads();
+  static_assert(W % G == 0 && (G & (G - 1)) == 0, "G must be a power of two dividing W");
+  auto ev = [&](const float (&x)[1][IN], float (&y)[1]) { y[0] = mlp_split<IN, W, G, ACT>(sw, a.LH, x[0]); };
+  pinn_chain_body<IN, 1, decltype(ev), G>(a, ev);
+}
+
+template <int IN, int W, int ACT, int PTS>
+__global__ void __launch_bounds__(128) k_pinn_chain(PinnArgs a) {
+  extern __shared__ float sw[];
+  for (int i = threadIdx.x; i < a.nfloats; i += blockDim.x) sw[i] = a.wts[i];
+  __syncthreads();
+  pinn_chain_body<IN, PTS>(a, [&](const float (&x)[PTS][IN], float (&y)[PTS]) {
+    mlp_eval<IN, W, ACT, PTS>(sw, a.LH, x, y);
+  });
+}
+
+// Small networks: every weight is a kernel parameter (constant bank), so each FFMA takes its
+// weight as a c[0x0][imm] operand -- no shared-memory loads and only two register reads per
+// FMA.  Layers fully unrolled (LH is a template parameter).
+template <int IN, int W, int LH>
+struct ParamNet {
+  static constexpr int kFloats = W * IN + W + (LH - 1) * (W * W + W) + W + 1;
+  float w[kFloats];
+};
+
+template <int IN, int W, int LH, int ACT>
+__device__ __forceinline__ float mlp_param(const ParamNet<IN, W, LH> &P, const float (&x)[IN]) {
+  float h[W];
+#pragma unroll
+  for (int o = 0; o < W; ++o) {
+    float z = P.w[W * IN + o];
+#pragma unroll
+    for (int i = 0; i < IN; ++i) z = fmaf(P.w[o * IN + i], x[i], z);
+    h[o] = act<ACT>(z);
+  }
+#pragma unroll
+  for (int l = 1; l < LH; ++l) {
+    constexpr int base0 = W * IN + W;
+    const int base = base0 + (l - 1) * (W * W + W);
+    float z[W];
+#pragma unroll
+    for (int o = 0; o < W; ++o) {
+      z[o] = P.w[base + W * W + o];
+#pragma unroll
+      for (int i = 0; i < W; ++i) z[o] = fmaf(P.w[base + o * W + i], h[i], z[o]);
+    }
+#pragma unroll
+    for (int o = 0; o < W; ++o) h[o] = act<ACT>(z[o]);
+  }
+  constexpr int ob = W * IN + W + (LH - 1) * (W * W + W);
+  float y = P.w[ob + W];
+#pragma unroll
+  for (int i = 0; i < W; ++i) y = fmaf(P.w[ob + i], h[i], y);
+  return y;
+}
+
+template <int IN, int W, int LH, int ACT>
+__global__ void __launch_bounds__(128) k_pinn_chain_param(PinnArgs a, const __grid_constant__ ParamNet<IN, W, LH> P) {
+  pinn_chain_body<IN, 1>(a, [&](const float (&x)[1][IN], float (&y)[1]) { y[0] = mlp_param<IN, W, LH, ACT>(P, x[0]); });
+}
+
 }  // namespace pr
+#endif  // PR_PINN_CHAIN_IMPL

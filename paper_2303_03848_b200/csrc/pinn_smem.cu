@@ -1,0 +1,60 @@
+// pinn_smem.cu — K3 with shared-memory weights (any instantiated width, runtime depth).
+#include "launch.h"
+#include "pinn_chain.cuh"
+
+namespace pr {
+typedef void (*SmemKernel)(PinnArgs);
+template <int IN, int ACT>
+static SmemKernel smem_kernel_w(int W) {
+  switch (W) {
+    case 8: return k_pinn_chain<IN, 8, ACT, 2>;
+    case 16: return k_pinn_chain<IN, 16, ACT, 2>;
+    case 20: return k_pinn_chain<IN, 20, ACT, 2>;
+    case 32: return k_pinn_chain<IN, 32, ACT, 2>;
+    case 50: return k_pinn_chain<IN, 50, ACT, 1>;
+    case 64: return k_pinn_chain<IN, 64, ACT, 1>;
+  }
+  return nullptr;
+}
+static SmemKernel smem_kernel(int IN, int W, int act) {
+  if (IN == 4) return act ? smem_kernel_w<4, 1>(W) : smem_kernel_w<4, 0>(W);
+  if (IN == 2) return act ? smem_kernel_w<2, 1>(W) : smem_kernel_w<2, 0>(W);
+  return nullptr;
+}
+bool pinn_smem_supported(int IN, int W, int act) { return smem_kernel(IN, W, act) != nullptr; }
+int pinn_smem_pts(int W) { return W <= 32 ? 2 : 1; }
+cudaError_t pinn_smem_prepare(int IN, int W, int act, int smem_bytes) {
+  SmemKernel k = smem_kernel(IN, W, act);
+  if (!k) return cudaErrorInvalidValue;
+  return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+}
+cudaError_t launch_pinn_smem(int IN, int W, int act, const PinnArgs &a, dim3 grid, size_t smem, cudaStream_t s) {
+  SmemKernel k = smem_kernel(IN, W, act);
+  if (!k) return cudaErrorInvalidValue;
+  k<<<grid, 128, smem, s>>>(a);
+  return cudaGetLastError();
+}
+}  // namespace pr
+
+namespace pr {
+// latency mode (G = 4 threads per point), shared-memory weights
+typedef void (*SplitKernel)(PinnArgs);
+static SplitKernel split_kernel(int IN, int W, int act) {
+  if (W != 20) return nullptr;
+  if (IN == 4) return act ? k_pinn_chain_split<4, 20, 4, 1> : k_pinn_chain_split<4, 20, 4, 0>;
+  if (IN == 2 && act == 0) return k_pinn_chain_split<2, 20, 4, 0>;
+  return nullptr;
+}
+bool pinn_split_supported(int IN, int W, int act) { return split_kernel(IN, W, act) != nullptr; }
+cudaError_t pinn_split_prepare(int IN, int W, int act, int smem_bytes) {
+  SplitKernel k = split_kernel(IN, W, act);
+  if (!k) return cudaErrorInvalidValue;
+  return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+}
+cudaError_t launch_pinn_split(int IN, int W, int act, const PinnArgs &a, dim3 grid, size_t smem, cudaStream_t s) {
+  SplitKernel k = split_kernel(IN, W, act);
+  if (!k) return cudaErrorInvalidValue;
+  k<<<grid, 128, smem, s>>>(a);
+  return cudaGetLastError();
+}
+}  // namespace pr

@@ -80,6 +80,20 @@ def test_pinn_G_single_slice(dims, act):
     assert_close(got, ref, what="G %s" % dims)
 
 
+@pytest.mark.parametrize("pinn_kernel", [0, 1, 2])
+@pytest.mark.parametrize("dims,act", [(synth.PINN_3x20, synth.ACT_TANH), (synth.PINN_3x20, synth.ACT_RELU),
+                                      ([2, 20, 20, 20, 1], synth.ACT_TANH)])
+def test_pinn_G_both_weight_paths(pinn_kernel, dims, act):
+    """Constant-bank weights (auto for these shapes) and shared-memory weights agree with the oracle."""
+    p = synth.single(3000, 8)
+    net = synth.kaiming_net(dims, seed=11, activation=act)
+    U = synth.random_state(1, 3000, seed=12) * 3.0
+    with ctx_for(p, net) as c:
+        c.set_option(parareal.OPT_PINN_KERNEL, pinn_kernel)
+        got = c.apply_coarse(6, U)
+    assert_close(got, oracle.pinn_G(p, net, 6, U.astype(np.float64)), what="G %s path %d" % (dims, pinn_kernel))
+
+
 def test_pinn_G_portfolio():
     p = synth.portfolio(n_k=3, n_s=5, M=300, N=16)
     net = synth.kaiming_net(synth.PINN_3x20, seed=1)
@@ -205,6 +219,21 @@ def test_determinism():
         a, ra = c.solve()
         b, rb = c.solve()
     assert np.array_equal(a, b) and np.array_equal(ra["delta"], rb["delta"])
+
+
+def test_streamed_determinism_and_parity():
+    """K2 (streamed, multi-tile, windowed look-back): bitwise run-to-run reproducible and within
+    tolerance of the oracle over a short Parareal run with numerical G."""
+    p = synth.single(20000, 8, fine_steps=10, coarse=synth.COARSE_IMPLICIT_EULER, coarse_steps=2, max_iter=2,
+                     tol=0.0)
+    with ctx_for(p, fine_kernel=2) as c:
+        a, ra = c.solve()
+        b, rb = c.solve()
+        it = c.copy_iterates(0, p.N + 1)
+    assert np.array_equal(a, b) and np.array_equal(ra["delta"], rb["delta"])
+    ref_U, ref_d, _, _ = oracle.parareal(p)
+    assert_close(it, ref_U, what="streamed Parareal iterates")
+    assert np.allclose(ra["delta"], ref_d, rtol=2e-2)
 
 
 def test_portfolio_parareal_sampled():
