@@ -44,6 +44,7 @@ def parse():
     ap.add_argument("--iters", type=int, default=3, help="fixed Parareal iterations K (tol = 0)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-c3-sweep", action="store_true", help="skip the C3 fine-sweep HBM roofline leg")
     return ap.parse_args()
 
 
@@ -168,6 +169,89 @@ def config_dict(args, p):
             else "working set larger than L2"}
 
 
+def ncu_traffic(kernel_prefix):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of a kernel, from the committed
+    `ncu --set full` capture summary (profiles/ncu_traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            d = json.load(f)
+    except Exception:
+        return None
+    for name, rec in d.get("kernels", {}).items():
+        if name.startswith(kernel_prefix):
+            return rec
+    return None
+
+
+def roofline(p, ph, K, world, rank, pk, pk_src, clk_mhz, n_sm, synth):
+    """Roofline of the step's dominant kernel (DESIGN.md §6 work per unit)."""
+    nloc = p.N // world
+    if ph["ms_fine"] >= ph["ms_coarse"]:
+        # average active slices per fine sweep on this rank (slices n >= k-1 at iteration k)
+        act = sum(max(0, nloc - max(0, k - 1 - rank * nloc)) for k in range(1, K + 1)) / K
+        pt_steps = float(p.B) * p.M * p.fine_steps * act
+        sweep_s = ph["ms_fine"] / K / 1e3
+        if p.M <= 2048:
+            roof = {"kernel": "k_fine_sweep (resident K1, fp64)", "bound": "alu",
+                    "achieved": 9.0 * pt_steps / sweep_s / 1e12, "peak": n_sm * 64 * 2 * clk_mhz * 1e6 / 1e12,
+                    "unit": "TFLOP/s", "peak_source": "fp64 pipe: %d SMs x 64 FMA/clk x 2 x %.0f MHz (DESIGN.md)"
+                    % (n_sm, clk_mhz), "work_per_unit": "9 fp64 flop per point-step", "launch_unit": "one sweep"}
+            tr = ncu_traffic("k_fine_sweep")
+        else:
+            roof = {"kernel": "k_streamed_pass (K2)", "bound": "hbm", "achieved": 16.0 * pt_steps / sweep_s / 1e9,
+                    "peak": float(pk["hbm_gbs"]), "unit": "GB/s", "peak_source": pk_src,
+                    "work_per_unit": "16 B per point-step", "launch_unit": "one pass (8 B per point)"}
+            tr = ncu_traffic("k_streamed_pass")
+    else:
+        evals = float(p.B) * p.M * nloc
+        chain_s = ph["ms_coarse"] / (K + 1) / 1e3
+        if p.coarse == synth.COARSE_PINN:
+            roof = {"kernel": "k_pinn_chain* (K3, fp32 SIMT)", "bound": "alu",
+                    "achieved": pinn_flops(synth.PINN_3x20) * evals / chain_s / 1e12,
+                    "peak": n_sm * 128 * 2 * clk_mhz * 1e6 / 1e12, "unit": "TFLOP/s",
+                    "peak_source": "fp32 FMA pipe: %d SMs x 128 FMA/clk x 2 x %.0f MHz (DESIGN.md)" % (n_sm, clk_mhz),
+                    "work_per_unit": "1760 flop + 60 tanh per point-eval", "launch_unit": "one coarse chain"}
+            tr = ncu_traffic("k_pinn_chain")
+        else:
+            roof = {"kernel": "k_resident_chain (numerical G, fp64)", "bound": "alu",
+                    "achieved": 9.0 * evals * p.coarse_steps / chain_s / 1e12,
+                    "peak": n_sm * 64 * 2 * clk_mhz * 1e6 / 1e12, "unit": "TFLOP/s", "peak_source": "fp64 pipe",
+                    "work_per_unit": "9 fp64 flop per point-step", "launch_unit": "one coarse chain"}
+            tr = ncu_traffic("k_resident_chain")
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["traffic"] = tr["dram_bytes_per_launch"] if tr else None
+    if tr:
+        roof["traffic_source"] = tr.get("source")
+    return roof
+
+
+def c3_fine_sweep_roofline(parareal, synth, torch, stream, pk, pk_src, flush):
+    """One Parareal iteration at C3 (2^20 points x 64 slices): its fine sweep runs the streamed
+    kernel over all 64 slices x 100 steps; HBM roofline from the CUDA-event phase time."""
+    p = synth.config("C3", coarse=synth.COARSE_PINN, max_iter=1, tol=0.0)
+    ctx = parareal.Context(p, stream=stream.cuda_stream)
+    try:
+        ctx.load_weights(synth.kaiming_net(synth.PINN_3x20, seed=0))
+        out = torch.empty((p.B, p.M), dtype=torch.float32, device="cuda")
+        ctx.solve_device(out)
+        ms = []
+        for _ in range(3):
+            flush.zero_()
+            torch.cuda.synchronize()
+            ms.append(ctx.solve_device(out)["ms_fine"])
+        t = statistics.median(ms) / 1e3
+        pt_steps = float(p.M) * p.N * p.fine_steps
+        ach = 16.0 * pt_steps / t / 1e9
+        tr = ncu_traffic("k_streamed_pass")
+        return {"kernel": "k_streamed_pass (K2)", "workload": "C3 fine sweep: 64 slices x 2^20 points x 100 IE steps",
+                "bound": "hbm", "achieved": ach, "peak": float(pk["hbm_gbs"]), "unit": "GB/s",
+                "frac": ach / float(pk["hbm_gbs"]), "peak_source": pk_src, "ms_per_sweep": t * 1e3,
+                "point_steps_per_s": pt_steps / t, "work_per_unit": "16 B per point-step (fp32 read+write, 2 passes)",
+                "traffic": tr["dram_bytes_per_launch"] if tr else None}
+    finally:
+        ctx.close()
+
+
 # --------------------------------------------------------------------------- our arm
 def main():
     args = parse()
@@ -251,37 +335,12 @@ def main():
     pk, pk_src = peaks()
     clk_mhz = float(pk.get("sm_max_mhz", 1965.0))
     n_sm = torch.cuda.get_device_properties(local).multi_processor_count
-    fine_dominant = ph["ms_fine"] >= ph["ms_coarse"]
-    nloc = p.N // world
-    if fine_dominant:
-        # resident fine sweep: fp64 FMA pipe; 9 algorithmic fp64 flop per point-step
-        pt_steps = float(p.B) * p.M * p.fine_steps * sum(max(0, nloc - max(0, k - 1 - rank * nloc)) for k in
-                                                           range(1, K + 1)) / K
-        if p.M <= 2048:
-            peak = n_sm * 64 * 2 * clk_mhz * 1e6 / 1e12
-            roof = {"kernel": "k_fine_sweep (resident, fp64)", "bound": "alu",
-                    "achieved": 9.0 * pt_steps / (ph["ms_fine"] / K / 1e3) / 1e12, "peak": peak,
-                    "unit": "TFLOP/s", "peak_source": "fp64 pipe: %d SMs x 64 FMA/clk x 2 x %.0f MHz" % (n_sm, clk_mhz)}
-        else:
-            peak = float(pk["hbm_gbs"])
-            roof = {"kernel": "k_streamed_pass (fine sweep)", "bound": "hbm",
-                    "achieved": 16.0 * pt_steps / (ph["ms_fine"] / K / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
-                    "peak_source": pk_src}
-    else:
-        evals = float(p.B) * p.M * (nloc * (K + 1)) / (K + 1)
-        if p.coarse == synth.COARSE_PINN:
-            peak = n_sm * 128 * 2 * clk_mhz * 1e6 / 1e12
-            roof = {"kernel": "k_pinn_chain (fp32 SIMT)", "bound": "alu",
-                    "achieved": pinn_flops(synth.PINN_3x20) * evals / (ph["ms_coarse"] / (K + 1) / 1e3) / 1e12,
-                    "peak": peak, "unit": "TFLOP/s",
-                    "peak_source": "fp32 FMA pipe: %d SMs x 128 FMA/clk x 2 x %.0f MHz" % (n_sm, clk_mhz)}
-        else:
-            peak = n_sm * 64 * 2 * clk_mhz * 1e6 / 1e12
-            roof = {"kernel": "k_resident_chain (numerical G, fp64)", "bound": "alu",
-                    "achieved": 9.0 * evals / (ph["ms_coarse"] / (K + 1) / 1e3) / 1e12, "peak": peak,
-                    "unit": "TFLOP/s", "peak_source": "fp64 pipe"}
-    roof["frac"] = roof["achieved"] / roof["peak"]
-    roof["traffic"] = None
+    roof = roofline(p, ph, K, world, rank, pk, pk_src, clk_mhz, n_sm, synth)
+    # ---------------- north-star gate: the HBM-streamed fine sweep (K2) at the C3 grid, measured
+    # live in the same run (one fine sweep over 64 slices x 2^20 points x 100 steps)
+    fine_c3 = None
+    if rank == 0 and world == 1 and not args.no_c3_sweep and args.config != "C3":
+        fine_c3 = c3_fine_sweep_roofline(parareal, synth, torch, stream, pk, pk_src, flush)
     # ---------------- e2e through the host-buffer ABI call (pinned H2D of V_T, D2H of V_0)
     e2e = None
     if not args.no_e2e:
@@ -314,8 +373,6 @@ def main():
                "sample": "full %s workload, %d serial fp64 oracle solves (%.3f s each)" % (args.config, runs, per)}
     if rank == 0:
         from paper_2303_03848_b200 import report
-        ratio = None
-        fine_slice_ms = ph["ms_fine"] / K / max(1, nloc) if K else None
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f32 state / f64 implicit solves / f32 PINN",
@@ -329,7 +386,8 @@ def main():
                 "fine_point_steps_executed_per_s": float(p.B) * p.M * p.fine_steps * sum(p.N - k + 1 for k in range(1, K + 1))
                 / (ph["ms_fine"] / 1e3) if ph["ms_fine"] > 0 else None,
                 "eq8_bound_context": None,
-                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+                "roofline": roof, "roofline_fine_sweep_c3": fine_c3, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": launches,
                 "clocks": clk.summary()}
         if serial_ms and ph["ms_coarse"] > 0:
             c_f = serial_ms / p.N

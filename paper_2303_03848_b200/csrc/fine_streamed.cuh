@@ -18,8 +18,11 @@
 // it by < kLookbackEps·|y| (eight orders below fp64 rounding).  No CTA waits
 // on an inclusive prefix, so there is no dependency chain across the wave,
 // and the composition order is fixed: results are bitwise reproducible.
-// CTAs take tiles in scan order from a global ticket, so every predecessor a
-// CTA waits for is resident or finished.
+// A dedicated look-back warp requests the window, multipliers and status words
+// of the 64 nearest predecessors in one round trip while the data warps load.
+// Tiles map to CTA indices interleaved across the launch's independent systems
+// (CTAs are dispatched in index order), so a tile's predecessor started nsys
+// CTAs earlier.
 //
 // Layout.  The fp64 factors and the sweep-private fp32 ping-pong buffers are
 // stored thread-interleaved (see il_index) so every warp access is coalesced.
@@ -185,9 +188,46 @@ __device__ __forceinline__ void look_back(const PassArgs &a, int s, int pos, int
     return;
   }
   const size_t tb = ((size_t)DIR * a.nsets + set) * a.ntiles;
+  const double *sts = a.status + 2 * (size_t)s * a.ntiles;
+  // Speculative first round: the window size, the multipliers and the status words of the 64
+  // nearest predecessors are requested together (one L2 round trip); the window then masks them
+  // and only the in-window ones are waited for.
   const int W = a.f.tileW[tb + pos];
+  double sv[2], bv[2];
+  unsigned long long se[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int k = lane + 32 * h, p = pos - 1 - k;
+    bv[h] = (p >= 0) ? a.f.tileB[tb + p] : 1.0;
+    sv[h] = 0.0;
+    se[h] = a.epoch;
+    if (p >= 0) ld_status(sts + 2 * p, sv[h], se[h]);
+  }
   double accA = 0.0, accB = 1.0;
-  for (int base = 0; base < W; base += 32) {
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int k = lane + 32 * h;
+    double mA = 0.0, mB = 1.0;          // identity beyond the window
+    if (k < W) {
+      while (se[h] != a.epoch) ld_status(sts + 2 * (pos - 1 - k), sv[h], se[h]);
+      mA = sv[h];
+      mB = bv[h];
+    }
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const double oA = __shfl_down_sync(0xffffffffu, mA, d);
+      const double oB = __shfl_down_sync(0xffffffffu, mB, d);
+      if ((lane & (2 * d - 1)) == 0) {
+        mA = fma(mB, oA, mA);
+        mB *= oB;
+      }
+    }
+    mA = __shfl_sync(0xffffffffu, mA, 0);
+    mB = __shfl_sync(0xffffffffu, mB, 0);
+    accA = fma(accB, mA, accA);
+    accB *= mB;
+  }
+  for (int base = 64; base < W; base += 32) {  // rare: windows beyond 64 tiles
     const int k = base + lane;          // predecessor at distance k+1 in scan order
     double mA = 0.0, mB = 1.0;          // identity beyond the window
     if (k < W) {
@@ -224,14 +264,12 @@ __global__ void __launch_bounds__(kSNT + 32) k_streamed_pass(PassArgs a) {
   constexpr int NW = kSNT / 32;
   __shared__ double sA[NW], sB[NW];
   __shared__ double s_yin;
-  __shared__ unsigned long long s_ticket;
   __shared__ double red[2 * NW];
-  if (threadIdx.x == 0) s_ticket = atomicAdd(a.ticket, 1ull) - a.ticket_base;
-  __syncthreads();
-  // Tickets are interleaved across the independent systems of the launch (slices × instances):
-  // the predecessor of (s, pos) holds ticket tk − nsys, so with many systems it has long
-  // published its aggregate when this tile needs it.
-  const unsigned long long tk = s_ticket;
+  // Tile order: CTAs are dispatched in increasing index order (the assumption CUB's single-pass
+  // scan makes), so every predecessor a CTA waits for is resident or finished.  Indices are
+  // interleaved across the independent systems of the launch (slices × instances): the
+  // predecessor of (s, pos) is CTA tk − nsys, which with many systems published long before.
+  const unsigned long long tk = blockIdx.x;
   const int s = (int)(tk % a.nsys);
   const int pos = (int)(tk / a.nsys);                 // position in scan order
   const int tile = DIR == 0 ? pos : a.ntiles - 1 - pos;

@@ -185,20 +185,42 @@ __device__ __forceinline__ void pinn_chain_body(const PinnArgs &a, Eval ev) {
     for (int p = 0; p < PTS; ++p) u[p] = ok[p] ? u0[j[p]] : 0.f;
   }
   const int ln_end = a.Gout ? a.ln0 + 1 : a.ln1;
+  // δ partials: per-warp sums buffered per slice in shared memory and flushed (fixed order:
+  // warps in index order) every kPartBuf slices, instead of a CTA barrier per slice
+  constexpr int kPartBuf = 32;
+  __shared__ double wpart[kPartBuf][4][2];
+  const int wid = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  auto flush = [&](int ln_first, int count) {
+    __syncthreads();
+    if (threadIdx.x < count) {
+      double num = 0.0, den = 0.0;
+      for (int q = 0; q < nwarp; ++q) { num += wpart[threadIdx.x][q][0]; den += wpart[threadIdx.x][q][1]; }
+      double *pp = a.partials + (((size_t)(ln_first + threadIdx.x + 1) * a.B + b) * a.nch + blockIdx.x) * 2;
+      pp[0] = num;
+      pp[1] = den;
+    }
+    __syncthreads();
+  };
+  // D_n and the old U_{n+1} are loaded one slice ahead (their latency hides behind the
+  // previous slice's network); loads precede this kernel's stores to the same rows.
+  float dn[PTS], uo[PTS];
+  auto prefetch = [&](int ln, float (&d)[PTS], float (&o)[PTS]) {
+    const size_t row = (size_t)ln * sstride + (size_t)b * a.Mp;
+#pragma unroll
+    for (int p = 0; p < PTS; ++p) {
+      d[p] = (a.D && ok[p] && ln < ln_end) ? __ldcg(a.D + row + j[p]) : 0.f;
+      o[p] = (a.partials && ok[p] && ln < ln_end) ? __ldcg(a.U + row + sstride + j[p]) : 0.f;
+    }
+  };
+  prefetch(a.ln0, dn, uo);
 #pragma unroll 1
   for (int ln = a.ln0; ln < ln_end; ++ln) {
     const int n = a.n_base + ln;
     // t_from/T, t_to/T (reading Q7): uniform per slice
     const float tf = (float)((a.T - n * a.dT) / a.T), tt = (float)((a.T - (n + 1) * a.dT) / a.T);
-    // issue this slice's loads (D_n, old U_{n+1}) before the network so their latency hides
-    // behind it (loads ahead of this iteration's stores: no aliasing hazard)
     const size_t row = (size_t)ln * sstride + (size_t)b * a.Mp;
-    float dn[PTS], uo[PTS];
-#pragma unroll
-    for (int p = 0; p < PTS; ++p) {
-      dn[p] = (a.D && ok[p]) ? __ldcg(a.D + row + j[p]) : 0.f;
-      uo[p] = (a.partials && ok[p]) ? __ldcg(a.U + row + sstride + j[p]) : 0.f;
-    }
+    float dnx[PTS], uox[PTS];
+    prefetch(ln + 1, dnx, uox);
     float x[PTS][IN], y[PTS];
 #pragma unroll
     for (int p = 0; p < PTS; ++p) {
@@ -238,14 +260,18 @@ __device__ __forceinline__ void pinn_chain_body(const PinnArgs &a, Eval ev) {
         }
       }
       u[p] = nv;
+      dn[p] = dnx[p];
+      uo[p] = uox[p];
     }
     if (a.partials) {
-      cta_reduce2(num, den, red);
-      if (threadIdx.x == 0) {
-        double *pp = a.partials + (((size_t)(ln + 1) * a.B + b) * a.nch + blockIdx.x) * 2;
-        pp[0] = num;
-        pp[1] = den;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        num += __shfl_xor_sync(0xffffffffu, num, o);
+        den += __shfl_xor_sync(0xffffffffu, den, o);
       }
+      const int slot = (ln - a.ln0) % kPartBuf;
+      if ((threadIdx.x & 31) == 0) { wpart[slot][wid][0] = num; wpart[slot][wid][1] = den; }
+      if (slot == kPartBuf - 1 || ln == ln_end - 1) flush(ln - slot, slot + 1);
     }
   }
 }
