@@ -89,7 +89,9 @@ struct Scheme {
   double dtau = 0;
   int steps = 0;
   double *m = nullptr, *ip = nullptr, *cu = nullptr;  // device [nsets][Mp] (K1)
-  double *im = nullptr, *iip = nullptr, *icu = nullptr;  // device [nsets][Mt], interleaved (K2)
+  double *iip = nullptr;                            // device [nsets][Mt] 1/p, interleaved (K2)
+  double *coef = nullptr;                           // device [nsets][2] dτr/2, dτσ²/2 (K2)
+  double *thrB = nullptr;                           // device [2][nsets][Mt/kSPS] (K2 thread multipliers)
   double *tileB = nullptr;                          // device [2][nsets][ntiles] (K2 look-back)
   int *tileW = nullptr;
   double *bcoef = nullptr;                          // device [B]
@@ -236,25 +238,42 @@ pr_status upload_scheme(pr_ctx *c, Scheme &sc, int steps) {
   CU(cudaMemcpy(sc.m, m.data(), n * sizeof(double), cudaMemcpyHostToDevice));
   CU(cudaMemcpy(sc.ip, ip.data(), n * sizeof(double), cudaMemcpyHostToDevice));
   CU(cudaMemcpy(sc.cu, cu.data(), n * sizeof(double), cudaMemcpyHostToDevice));
-  // the same factors in K2's thread-interleaved layout, identity-padded to Mt
+  // K2: 1/p in the thread-interleaved layout (1 beyond M), the closed-form off-diagonal
+  // coefficients, and the per-thread multipliers Π(−m_j) (dir 0) / Π(−u_j/p_j) (dir 1)
   const int Mt = pr::streamed_Mt(c->M);
-  std::vector<double> im((size_t)c->nsets * Mt, 0.0), iip((size_t)c->nsets * Mt, 1.0), icu((size_t)c->nsets * Mt, 0.0);
+  const size_t nthr = (size_t)Mt / pr::kSPS;
+  // K2's forward pass runs on w = y/p: multiplier m̃_j = l_j/p_j (none in row 0)
+  std::vector<double> mt((size_t)c->nsets * c->Mp, 0.0);
   for (int s = 0; s < c->nsets; ++s)
-    for (int j = 0; j < c->M; ++j) {
-      const size_t d = (size_t)s * Mt + pr::il_index(j), o = (size_t)s * c->Mp + j;
-      im[d] = m[o];
-      iip[d] = ip[o];
-      icu[d] = cu[o];
+    for (int i = 1; i < c->M; ++i) {
+      const double sg = c->sets[s].first, rr = c->sets[s].second, j = i + 1;
+      const double a = 0.5 * sg * sg * j * j, b = 0.5 * rr * j;
+      mt[(size_t)s * c->Mp + i] = -sc.dtau * (a - b) * ip[(size_t)s * c->Mp + i];
     }
-  const size_t ni = im.size() * sizeof(double);
-  CU(cudaMalloc(&sc.im, ni));
-  CU(cudaMalloc(&sc.iip, ni));
-  CU(cudaMalloc(&sc.icu, ni));
-  CU(cudaMemcpy(sc.im, im.data(), ni, cudaMemcpyHostToDevice));
-  CU(cudaMemcpy(sc.iip, iip.data(), ni, cudaMemcpyHostToDevice));
-  CU(cudaMemcpy(sc.icu, icu.data(), ni, cudaMemcpyHostToDevice));
+  std::vector<double> iip((size_t)c->nsets * Mt, 1.0), coef((size_t)c->nsets * 2), thB((size_t)2 * c->nsets * nthr);
+  for (int s = 0; s < c->nsets; ++s) {
+    for (int j = 0; j < c->M; ++j) iip[(size_t)s * Mt + pr::il_index(j)] = ip[(size_t)s * c->Mp + j];
+    coef[2 * s] = sc.dtau * (0.5 * c->sets[s].second);
+    coef[2 * s + 1] = sc.dtau * (0.5 * c->sets[s].first * c->sets[s].first);
+    for (int dir = 0; dir < 2; ++dir)
+      for (size_t q = 0; q < nthr; ++q) {
+        double prod = 1.0;
+        for (int i = 0; i < pr::kSPS; ++i) {
+          const size_t j = q * pr::kSPS + i;
+          const double f = j < (size_t)c->M ? (dir == 0 ? mt[(size_t)s * c->Mp + j] : cu[(size_t)s * c->Mp + j]) : 0.0;
+          prod *= -f;
+        }
+        thB[((size_t)dir * c->nsets + s) * nthr + q] = prod;
+      }
+  }
+  CU(cudaMalloc(&sc.iip, iip.size() * sizeof(double)));
+  CU(cudaMalloc(&sc.coef, coef.size() * sizeof(double)));
+  CU(cudaMalloc(&sc.thrB, thB.size() * sizeof(double)));
+  CU(cudaMemcpy(sc.iip, iip.data(), iip.size() * sizeof(double), cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(sc.coef, coef.data(), coef.size() * sizeof(double), cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(sc.thrB, thB.data(), thB.size() * sizeof(double), cudaMemcpyHostToDevice));
   // K2 look-back data, indexed by scan position (dir 0: tiles ascending, dir 1: descending):
-  // tile multiplier B = Π(−m_j) resp. Π(−u_j/p_j) over the tile, and the window W = number of
+  // tile multiplier B = Π(−l_j/p_j) resp. Π(−u_j/p_j) over the tile, and the window W = number of
   // predecessors whose aggregates are composed: the first W with |Π_{k≤W} B_{pos−k}| below
   // kLookbackEps (all predecessors if never).
   const int nt = pr::streamed_ntiles(c->M);
@@ -267,7 +286,7 @@ pr_status upload_scheme(pr_ctx *c, Scheme &sc, int steps) {
         const int tile = dir == 0 ? pos : nt - 1 - pos;
         double prod = 1.0;
         for (int j = tile * pr::kSTile; j < std::min((tile + 1) * pr::kSTile, c->M); ++j)
-          prod *= dir == 0 ? -m[(size_t)s * c->Mp + j] : -cu[(size_t)s * c->Mp + j];
+          prod *= dir == 0 ? -mt[(size_t)s * c->Mp + j] : -cu[(size_t)s * c->Mp + j];
         if ((tile + 1) * pr::kSTile > c->M && dir == 0) prod = 0.0;  // identity padding: m = 0
         tB[base + pos] = prod;
       }
@@ -301,9 +320,9 @@ pr_status upload_scheme(pr_ctx *c, Scheme &sc, int steps) {
 void free_scheme(Scheme &s) {
   cudaFree(s.tileB);
   cudaFree(s.tileW);
-  cudaFree(s.im);
   cudaFree(s.iip);
-  cudaFree(s.icu);
+  cudaFree(s.coef);
+  cudaFree(s.thrB);
   cudaFree(s.m);
   cudaFree(s.ip);
   cudaFree(s.cu);
@@ -313,9 +332,9 @@ void free_scheme(Scheme &s) {
 
 pr::StreamedProblem sprob(const pr_ctx *c, const Scheme &sc) {
   pr::StreamedProblem p;
-  p.f.m = sc.im;
   p.f.ip = sc.iip;
-  p.f.cu = sc.icu;
+  p.f.coef = sc.coef;
+  p.f.thrB = sc.thrB;
   p.f.tileB = sc.tileB;
   p.f.tileW = sc.tileW;
   p.nsets = c->nsets;
