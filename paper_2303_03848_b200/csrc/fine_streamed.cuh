@@ -8,40 +8,45 @@
 //   backward  x_j = w_j − c_j x_{j+1},        c_j = u_j/p_j
 // (the usual elimination y_j = r_j − (l_j/p_{j−1}) y_{j−1}, x_j = y_j/p_j − c_j x_{j+1},
 // with the division by p_j moved into the forward pass).  A system (one instance ×
-// one slice, up to 2^20 points and more) is cut into tiles of kSTile points (one
-// CTA) and threads of kSPS points; one pass is one kernel launch.
+// one slice, up to 2^20 points and more) is cut into tiles of kSTile points and
+// threads of kSPS points; one pass is one kernel launch.
 //
-// Pre-aggregated passes.  Over a thread's kSPS points a recurrence is an
-// affine map v ↦ A + B·v of the value entering the thread.  B is a product of
-// constant factors (host table), and A is linear in the pass's *input* — the
+// Pre-aggregated, pre-scanned passes.  Over a thread's kSPS points a recurrence
+// is an affine map v ↦ A_t + B_t·v of the value entering the thread.  B_t is a
+// product of constant factors; A_t is linear in the pass's *input* — the
 // previous pass's *output*.  So every pass, as it produces its outputs, also
-// accumulates the next pass's per-thread A (and, reduced over the CTA, the
-// per-tile A) and publishes them.  A pass therefore starts with every
-// aggregate it needs already in memory: the value entering its tile is the
-// composition of its predecessors' tile aggregates (look-back), the value
-// entering each thread a CTA scan of its tile's thread aggregates, and each
-// thread then runs its recurrence once, sequentially, from the exact entering
-// value — no waiting on other CTAs, no second pass over registers.  The first
-// pass of a slice takes its aggregates from k_agg0.
+// accumulates the next pass's A_t, scans them over its tile (in the next pass's
+// direction) and publishes, per thread, the exclusive in-tile prefix E_t and,
+// per tile, the tile total.  A pass therefore starts with everything it needs
+// in memory: the value entering thread t is  v_t = E_t + P_t·y_tile  (P_t, the
+// product of the preceding threads' multipliers, is a host table), where
+// y_tile, the value entering the tile, is the composition of its
+// predecessors' tile totals (look-back).  Each thread then runs its recurrence
+// once, from the exact entering value: no waiting on other CTAs, no second pass.
+// The first pass of a slice takes its aggregates from k_agg0.
 //
-// S systems per CTA.  A CTA runs the same tile of S systems that share one
-// factor set (S consecutive slices of one instance): the factor loads, their
-// derivation and the multiplier scan are done once for the S systems.
-//
-// Look-back truncation.  Tile i composes the aggregates of predecessors
+// Look-back truncation.  Tile i composes the totals of predecessors
 // i−1 … i−W_i only, W_i (host-computed) being the first window whose
 // multiplier product falls below kLookbackEps: tiles further back change the
 // entering value by < kLookbackEps·|y| (eight orders below fp64 rounding).
 // Fixed composition orders → bitwise reproducible results.
 //
 // Factors.  Only 1/p_j is stored (fp64, interleaved); m̃_j and c_j are formed
-// in registers from the closed-form off-diagonals l_j = −dτ(a_j−b_j),
-// u_j = −dτ(a_j+b_j) (a_j = σ²j²/2, b_j = rj/2, j = 1..M).
-// Per point and pass: 4 B state read + 4 B written (HBM); 8/S B of 1/p (L2).
+// from the closed-form off-diagonals l_j = −dτ(a_j−b_j), u_j = −dτ(a_j+b_j)
+// (a_j = σ²j²/2, b_j = rj/2, j = 1..M).
+//
+// Two kernels.  k_pass_res (the middle passes of a sweep, interleaved in and
+// out) is persistent: each CTA takes a contiguous tile-major range of items
+// (one tile of SP·H systems sharing a factor set), keeps the tile's factors in
+// shared memory across its items, and streams the items' state in with bulk
+// async copies (cp.async.bulk + mbarrier) NST items ahead.  k_streamed_pass
+// (first pass of a slice from natural-layout rows, last pass with the
+// epilogues, and chain mode) is one CTA per tile with register-resident data.
+// Per point and pass: 4 B state read + 4 B written (HBM).
 #include <cuda_runtime.h>
 #include <stdint.h>
-#include <string.h>
 #include <stdlib.h>
+#include <string.h>
 #include <type_traits>
 
 #ifndef PR_FINE_STREAMED_ARGS
@@ -66,15 +71,16 @@ inline int streamed_ntiles(int M) { return (M + kSTile - 1) / kSTile; }
 struct StreamedFactors {
   const double *ip;              // interleaved [nsets][Mt] 1/p_j, 1 beyond M
   const double *coef;            // [nsets][2]: dτ·r/2, dτ·σ²/2  (l_j = j(c0 − c1 j), u_j = −j(c0 + c1 j))
-  const double *thrB;            // [2][nsets][Mt/kSPS] thread multiplier Π(−m̃_j) / Π(−c_j)
+  const double *thrP;            // [2][nsets][Mt/kSPS] P_t: product of the multipliers of the threads
+                                 //   preceding t in its tile, in the pass direction (dir 0: Π(−m̃), 1: Π(−c))
   const double *tileB;           // [2][nsets][ntiles] tile multiplier, indexed by scan position
   const int *tileW;              // [2][nsets][ntiles] look-back window (predecessors)
 };
 
 struct StreamedState {
   float *X = nullptr, *Y = nullptr;   // [nsys][Mt] ping-pong state (interleaved)
-  double *aggT[2] = {nullptr, nullptr};  // [nsys][Mt/kSPS] thread aggregates: [0] read by forward passes, [1] by backward
-  double *aggL[2] = {nullptr, nullptr};  // [nsys][ntiles] tile aggregates (tile index)
+  double *aggT[2] = {nullptr, nullptr};  // [nsys][Mt/kSPS] E_t: [0] read by forward passes, [1] by backward
+  double *aggL[2] = {nullptr, nullptr};  // [nsys][ntiles] tile totals (tile index)
   int ntiles = 0;
   size_t nsys_max = 0;
 };
@@ -109,7 +115,7 @@ enum { EPI_X = 0, EPI_SWEEP = 1, EPI_CHAIN = 2 };
 
 struct PassArgs {
   int M, Mp, Mt, B, ntiles, nsys, nsets;
-  int nsl, ngroups;          // systems s = ls·B + b, ls < nsl; CTA group g ↔ (b = g % B, slices (g/B)·S …)
+  int nsl, ngroups;          // systems s = ls·B + b (ls < nsl); group g ↔ (b = g % B, slices (g/B)·SG …)
   StreamedFactors f;
   const int *fset;
   const float *in;           // [nsys][Mp] natural rows (first pass of a slice) or [nsys][Mt] interleaved
@@ -171,6 +177,8 @@ cudaError_t streamed_chain(StreamedState &st, const StreamedProblem &p, const St
 #define PR_FINE_STREAMED_IMPL
 namespace pr {
 
+constexpr int kNW = kSNT / 32;  // warps per tile
+
 template <int DIR>
 __device__ __forceinline__ double shfl_prev(double v, int d) {
   return DIR == 0 ? __shfl_up_sync(0xffffffffu, v, d) : __shfl_down_sync(0xffffffffu, v, d);
@@ -211,83 +219,76 @@ __device__ __forceinline__ void load_natural(const float *in, int j0, int M, flo
   }
 }
 
-// Ordered composition of S per-thread maps (A_q, B) (common multiplier B) over the CTA in the
-// scan order of direction D (0: threads ascending, 1: descending), fixed tree.  Thread 0 gets T.
-template <int D, int NW, int S>
-__device__ __forceinline__ void cta_compose(double (&A)[S], double B, double *red, int t, double (&T)[S]) {
-  const int lane = t & 31, w = t >> 5;
+// Inclusive warp scan, in the order of direction D, of SP maps (A_q, B) with a common B.
+// Returns the exclusive values (eA_q, eB) of the lane; lane 31 (scan order) holds the totals.
+template <int D, int SP>
+__device__ __forceinline__ void warp_scan(double (&A)[SP], double &B, double (&eA)[SP], double &eB, int lane) {
+  const int sl = D == 0 ? lane : 31 - lane;
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
-    const double oB = __shfl_down_sync(0xffffffffu, B, d);
+    const double pB = shfl_prev<D>(B, d);
 #pragma unroll
-    for (int q = 0; q < S; ++q) {
-      const double oA = __shfl_down_sync(0xffffffffu, A[q], d);
-      if ((lane & (2 * d - 1)) == 0) A[q] = D == 0 ? fma(oB, A[q], oA) : fma(B, oA, A[q]);
+    for (int q = 0; q < SP; ++q) {
+      const double pA = shfl_prev<D>(A[q], d);
+      if (sl >= d) A[q] = fma(B, pA, A[q]);
     }
-    if ((lane & (2 * d - 1)) == 0) B *= oB;
+    if (sl >= d) B *= pB;
   }
-  __syncthreads();  // red[] may still be read by an earlier phase
-  if (lane == 0) {
+  eB = shfl_prev<D>(B, 1);
 #pragma unroll
-    for (int q = 0; q < S; ++q) red[(S + 1) * w + q] = A[q];
-    red[(S + 1) * w + S] = B;
+  for (int q = 0; q < SP; ++q) eA[q] = shfl_prev<D>(A[q], 1);
+  if (sl == 0) {
+    eB = 1.0;
+#pragma unroll
+    for (int q = 0; q < SP; ++q) eA[q] = 0.0;
   }
-  __syncthreads();
-  if (t == 0) {
+}
+
+// Composition of the nearest predecessors' tile totals (lane l: distance base+l+1),
+// fixed tree (deterministic).  Warp-level; result in lane 0.
+__device__ __forceinline__ void compose_window(double &mA, double &mB, int lane) {
 #pragma unroll
-    for (int q = 0; q < S; ++q) {
-      double v = 0.0;
-      if (D == 0) {
-        for (int k = 0; k < NW; ++k) v = fma(red[(S + 1) * k + S], v, red[(S + 1) * k + q]);
-      } else {
-        for (int k = NW - 1; k >= 0; --k) v = fma(red[(S + 1) * k + S], v, red[(S + 1) * k + q]);
-      }
-      T[q] = v;
+  for (int d = 1; d < 32; d <<= 1) {
+    const double oA = __shfl_down_sync(0xffffffffu, mA, d);
+    const double oB = __shfl_down_sync(0xffffffffu, mB, d);
+    if ((lane & (2 * d - 1)) == 0) {
+      mA = fma(mB, oA, mA);
+      mB *= oB;
     }
   }
 }
 
-// The value entering the tile at scan position `pos` of system s: composition of the tile
-// aggregates of its W_pos predecessors (published by the previous launch).  Warp-level; lane 0.
+// The value entering the tile at scan position `pos` of system s, composing the window from
+// predecessor distance base0+1 on onto (accA, accB).  Warp-level; result in lane 0.
 template <int DIR>
-__device__ __forceinline__ double look_back(const PassArgs &a, int s, int pos, int set, int lane) {
-  if (pos == 0) return 0.0;
+__device__ __forceinline__ double look_back(const PassArgs &a, int s, int pos, int set, int lane, int base0,
+                                            double accA, double accB) {
   const size_t tb = ((size_t)DIR * a.nsets + set) * a.ntiles;
   const double *agg = a.aggL_cur + (size_t)s * a.ntiles;
-  const int W = __ldg(a.f.tileW + tb + pos);
-  double accA = 0.0, accB = 1.0;
-  for (int base = 0; base < W; base += 32) {
-    const int k = base + lane;          // predecessor at distance k+1 in scan order
-    double mA = 0.0, mB = 1.0;          // identity beyond the window
+  const int W = pos > 0 ? __ldg(a.f.tileW + tb + pos) : 0;
+  for (int base = base0; base < W; base += 32) {
+    const int k = base + lane;
+    double mA = 0.0, mB = 1.0;
     if (k < W) {
       const int p = pos - 1 - k;
       mA = agg[DIR == 0 ? p : a.ntiles - 1 - p];
       mB = __ldg(a.f.tileB + tb + p);
     }
-    // ordered composition lane 0 ∘ lane 1 ∘ … ∘ lane 31 (fixed tree: deterministic)
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const double oA = __shfl_down_sync(0xffffffffu, mA, d);
-      const double oB = __shfl_down_sync(0xffffffffu, mB, d);
-      if ((lane & (2 * d - 1)) == 0) {
-        mA = fma(mB, oA, mA);
-        mB *= oB;
-      }
-    }
-    accA = fma(accB, mA, accA);  // lane 0 holds the window's composition
+    compose_window(mA, mB, lane);
+    accA = fma(accB, mA, accA);
     accB *= mB;
   }
   return accA;
 }
 
-// Aggregates of the first (forward) pass of a slice, from its natural-layout input rows
-// (one system per CTA): w_last = Σ_i r_i/p_i Π_{k>i}(−m̃_k) + Π(−m̃)·w_in.
+// ---------------------------------------------------------------- k_agg0
+// Aggregates of the first (forward) pass of a slice, from its natural-layout input rows:
+// A_t = Σ_i r_i/p_i Π_{k>i}(−m̃_k) (w-form forward map of the thread), scanned over the tile.
 __global__ void __launch_bounds__(kSNT) k_agg0(PassArgs a) {
-  constexpr int NW = kSNT / 32;
-  __shared__ double red[2 * NW];
+  __shared__ double tot[kNW][2];
   const int s = blockIdx.x % a.nsys, tile = blockIdx.x / a.nsys;
   const int b = s % a.B, ln = a.ln0 + s / a.B, set = a.fset[b];
-  const int t = threadIdx.x;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   const int j0 = tile * kSTile + t * kSPS;
   float x[kSPS];
   double ipv[kSPS];
@@ -309,50 +310,59 @@ __global__ void __launch_bounds__(kSNT) k_agg0(PassArgs a) {
     A[0] = fma(r * ipv[i], P, A[0]);
     P *= -mt;
   }
+  double eA[1], eB;
+  warp_scan<0, 1>(A, P, eA, eB, lane);
+  if (lane == 31) { tot[w][0] = A[0]; tot[w][1] = P; }
+  __syncthreads();
+  double wA = 0.0;
+  for (int k = 0; k < w; ++k) wA = fma(tot[k][1], wA, tot[k][0]);
   const size_t nthr = (size_t)a.Mt / kSPS;
-  a.aggT_next[(size_t)s * nthr + (size_t)tile * kSNT + t] = A[0];
-  double T[1];
-  cta_compose<0, NW, 1>(A, P, red, t, T);
-  if (t == 0) a.aggL_next[(size_t)s * a.ntiles + tile] = T[0];
+  a.aggT_next[(size_t)s * nthr + (size_t)tile * kSNT + t] = fma(eB, wA, eA[0]);
+  if (t == 0) {
+    double T = 0.0;
+    for (int k = 0; k < kNW; ++k) T = fma(tot[k][1], T, tot[k][0]);
+    a.aggL_next[(size_t)s * a.ntiles + tile] = T;
+  }
 }
 
-// One pass over one tile of S systems (kSNT threads × kSPS points each).  NEXT: also publish
-// the next pass's thread and tile aggregates.
-template <int DIR, bool IN_IL, bool OUT_IL, bool NEXT, int S>
+// ---------------------------------------------------------------- k_streamed_pass
+// One CTA per tile of SP systems (the same tile of SP consecutive slices of one instance), data
+// in registers.  Used for the first pass of a slice (natural input), the last pass (epilogues)
+// and chain mode.  NEXT: also publish the next pass's aggregates.
+template <int DIR, bool IN_IL, bool OUT_IL, bool NEXT, int SP>
 __global__ void __launch_bounds__(kSNT) k_streamed_pass(PassArgs a) {
-  constexpr int NW = kSNT / 32;
   constexpr int ND = 1 - DIR;  // direction of the next pass
-  static_assert(S <= NW, "one look-back warp per system");
-  __shared__ double sA[S][NW], sB[NW];
-  __shared__ double s_yin[S];
-  __shared__ double red[(S + 1) * NW];
+  static_assert(SP <= kNW, "one look-back warp per system");
+  __shared__ double s_yin[SP];
+  __shared__ double tot[kNW][SP + 1];
+  __shared__ double red[2 * kNW];
   const int g = (int)(blockIdx.x % a.ngroups);
   const int pos = (int)(blockIdx.x / a.ngroups);       // position in scan order
   const int tile = DIR == 0 ? pos : a.ntiles - 1 - pos;
   const int b = g % a.B;
-  const int ls0 = (g / a.B) * S;                       // first launch-local slice of the group
+  const int ls0 = (g / a.B) * SP;                      // first launch-local slice of the group
   const int set = a.fset[b];
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   const int j0 = tile * kSTile + t * kSPS;
   const size_t til = (size_t)tile * kSTile + t;   // interleaved offset of this thread's point 0
   const size_t nthr = (size_t)a.Mt / kSPS;
   const size_t thr = (size_t)tile * kSNT + t;     // thread index within the system
-  int sys[S];
-  bool ok[S];
+  int sys[SP];
+  bool ok[SP];
 #pragma unroll
-  for (int q = 0; q < S; ++q) {
+  for (int q = 0; q < SP; ++q) {
     ok[q] = ls0 + q < a.nsl;
     sys[q] = ok[q] ? (ls0 + q) * a.B + b : (ls0 * a.B + b);  // invalid → duplicate of the first (no stores)
   }
 
-  // ---- issue every load: thread aggregates and multiplier, the state, 1/p
-  double tA[S];
+  // ---- issue every load
+  double E[SP];
 #pragma unroll
-  for (int q = 0; q < S; ++q) tA[q] = a.aggT_cur[(size_t)sys[q] * nthr + thr];
-  const double tB = __ldg(a.f.thrB + ((size_t)DIR * a.nsets + set) * nthr + thr);
-  float x[S][kSPS];
+  for (int q = 0; q < SP; ++q) E[q] = a.aggT_cur[(size_t)sys[q] * nthr + thr];
+  const double P = __ldg(a.f.thrP + ((size_t)DIR * a.nsets + set) * nthr + thr);
+  float x[SP][kSPS];
 #pragma unroll
-  for (int q = 0; q < S; ++q) {
+  for (int q = 0; q < SP; ++q) {
     if (IN_IL) {
       const float *in = a.in + (size_t)sys[q] * a.Mt + til;
 #pragma unroll
@@ -368,105 +378,64 @@ __global__ void __launch_bounds__(kSNT) k_streamed_pass(PassArgs a) {
     for (int i = 0; i < kSPS; ++i) ipv[i] = __ldg(ip + i * kSNT);
   }
   const double c0 = __ldg(a.f.coef + 2 * set), c1 = __ldg(a.f.coef + 2 * set + 1);
-  // ---- the value entering the tile (one warp per system), and the CTA scan of the thread maps
-  if (w >= NW - S) {
-    const int q = NW - 1 - w;
-    const double y = look_back<DIR>(a, sys[q], pos, set, lane);
+  // ---- the value entering the tile (one warp per system)
+  if (w >= kNW - SP) {
+    const int q = kNW - 1 - w;
+    const double y = pos > 0 ? look_back<DIR>(a, sys[q], pos, set, lane, 0, 0.0, 1.0) : 0.0;
     if (lane == 0) s_yin[q] = y;
   }
-  const int sl = DIR == 0 ? lane : 31 - lane;  // scan-order lane
-  double iA[S], iB = tB;
+  __syncthreads();
+  double v[SP];
 #pragma unroll
-  for (int q = 0; q < S; ++q) iA[q] = tA[q];
+  for (int q = 0; q < SP; ++q) v[q] = fma(P, s_yin[q], E[q]);
+  // ---- the recurrence, once, from the exact entering value; next pass's map on the fly
+  double An[SP], Pn = 1.0;
 #pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const double pB = shfl_prev<DIR>(iB, d);
-#pragma unroll
-    for (int q = 0; q < S; ++q) {
-      const double pA = shfl_prev<DIR>(iA[q], d);
-      if (sl >= d) iA[q] = fma(iB, pA, iA[q]);
-    }
-    if (sl >= d) iB *= pB;
-  }
-  const int sw = DIR == 0 ? w : NW - 1 - w;    // scan-order warp
-  if (sl == 31) {
-#pragma unroll
-    for (int q = 0; q < S; ++q) sA[q][sw] = iA[q];
-    sB[sw] = iB;
-  }
-  __syncthreads();  // sA/sB and s_yin ready
-  double eB = shfl_prev<DIR>(iB, 1);
-  if (sl == 0) eB = 1.0;
-  double wB = 1.0;
-  for (int k = 0; k < sw; ++k) wB *= sB[k];
-  double v[S];  // value entering this thread, per system
-#pragma unroll
-  for (int q = 0; q < S; ++q) {
-    double wA = 0.0;  // prefix of preceding warps (in scan order)
-    for (int k = 0; k < sw; ++k) wA = fma(sB[k], wA, sA[q][k]);
-    double eA = shfl_prev<DIR>(iA[q], 1);
-    if (sl == 0) eA = 0.0;
-    v[q] = fma(eB * wB, s_yin[q], fma(eB, wA, eA));
-  }
-  // ---- the recurrence, once, from the exact entering value; next pass's aggregate on the fly
-  double An[S], Pn = 1.0;
-#pragma unroll
-  for (int q = 0; q < S; ++q) An[q] = 0.0;
+  for (int q = 0; q < SP; ++q) An[q] = 0.0;
   const double J0 = (double)(j0 + 1);
   auto run = [&](auto edge_tag) {
     constexpr bool EDGE = decltype(edge_tag)::value;
-    double bcv[S];
+    double bcv[SP];
 #pragma unroll
-    for (int q = 0; q < S; ++q) {
+    for (int q = 0; q < SP; ++q) {
       bcv[q] = 0.0;
       if (EDGE && j0 <= a.M - 1 && a.M - 1 < j0 + kSPS && (DIR == 0 || NEXT))
         bcv[q] = bc_term(a, b, a.n_base + a.ln0 + ls0 + q, a.step_m + DIR);
     }
-    if (DIR == 0) {
 #pragma unroll
-      for (int i = 0; i < kSPS; ++i) {
-        const int j = j0 + i;
-        double mt, cj;
-        factors<EDGE>(c0, c1, J0 + i, ipv[i], j, a.M, mt, cj);
+    for (int ii = 0; ii < kSPS; ++ii) {
+      const int i = DIR == 0 ? ii : kSPS - 1 - ii;
+      const int j = j0 + i;
+      double mt, cj;
+      factors<EDGE>(c0, c1, J0 + i, ipv[i], j, a.M, mt, cj);
 #pragma unroll
-        for (int q = 0; q < S; ++q) {
+      for (int q = 0; q < SP; ++q) {
+        if (DIR == 0) {
           const double r = (EDGE && j == a.M - 1) ? (double)x[q][i] + bcv[q] : (double)x[q][i];
           v[q] = fma(-mt, v[q], r * ipv[i]);
-          x[q][i] = (float)v[q];
           // backward map of the thread: x_{j0} = Σ_i w_i Π_{k<i}(−c_k) + Pn·x_{j0+kSPS}
           if (NEXT) An[q] = fma(v[q], Pn, An[q]);
-        }
-        if (NEXT) Pn *= -cj;
-      }
-    } else {
-#pragma unroll
-      for (int i = kSPS - 1; i >= 0; --i) {
-        const int j = j0 + i;
-        double mt, cj;
-        factors<EDGE>(c0, c1, J0 + i, ipv[i], j, a.M, mt, cj);
-#pragma unroll
-        for (int q = 0; q < S; ++q) {
+        } else {
           v[q] = fma(-cj, v[q], (double)x[q][i]);
-          x[q][i] = (float)v[q];
           // forward map of step m+1: w_last = Σ_i r_i/p_i Π_{k>i}(−m̃_k) + Pn·w_{j0−1}
           if (NEXT) {
             const double r = (EDGE && j == a.M - 1) ? v[q] + bcv[q] : v[q];
             An[q] = fma(r * ipv[i], Pn, An[q]);
           }
         }
-        if (NEXT) Pn *= -mt;
+        x[q][i] = (float)v[q];
       }
+      if (NEXT) Pn *= DIR == 0 ? -cj : -mt;
     }
   };
   // Aggregates use the unrounded outputs: the next pass then sees the recurrence applied to
   // inputs within fp32 rounding of the stored ones — the same perturbation storage makes.
-  const bool edge = j0 == 0 || j0 + kSPS > a.M - 1;
-  if (edge) run(std::true_type{});
+  if (j0 == 0 || j0 + kSPS > a.M - 1) run(std::true_type{});
   else run(std::false_type{});
   // ---- stores / epilogues
   if (OUT_IL) {
 #pragma unroll
-    for (int q = 0; q < S; ++q) {
+    for (int q = 0; q < SP; ++q) {
       if (!ok[q]) continue;
       float *op = a.out + (size_t)sys[q] * a.Mt + til;
 #pragma unroll
@@ -474,7 +443,7 @@ __global__ void __launch_bounds__(kSNT) k_streamed_pass(PassArgs a) {
     }
   } else if (a.epi == EPI_SWEEP) {
 #pragma unroll
-    for (int q = 0; q < S; ++q) {
+    for (int q = 0; q < SP; ++q) {
       if (!ok[q]) continue;
       const int s = sys[q];
       float *op;
@@ -498,7 +467,7 @@ __global__ void __launch_bounds__(kSNT) k_streamed_pass(PassArgs a) {
           if (j0 + i < a.M) op[j0 + i] = x[q][i];
       }
     }
-  } else {  // EPI_CHAIN (S = 1): g = x; Ĝ_n = g; U_{n+1} = g + D_n; δ partial against the old U_{n+1}
+  } else {  // EPI_CHAIN (SP = 1): g = x; Ĝ_n = g; U_{n+1} = g + D_n; δ partial against the old U_{n+1}
     const size_t row = (size_t)b * a.Mp;
     float old[kSPS], dc[kSPS];
     if (a.partials) load_natural(a.Unext + row, j0, a.M, old);
@@ -524,30 +493,336 @@ __global__ void __launch_bounds__(kSNT) k_streamed_pass(PassArgs a) {
         num += __shfl_xor_sync(0xffffffffu, num, q2);
         den += __shfl_xor_sync(0xffffffffu, den, q2);
       }
-      __syncthreads();
       if (lane == 0) { red[2 * w] = num; red[2 * w + 1] = den; }
       __syncthreads();
       if (t == 0) {
         num = 0.0; den = 0.0;
-        for (int q2 = 0; q2 < NW; ++q2) { num += red[2 * q2]; den += red[2 * q2 + 1]; }
+        for (int q2 = 0; q2 < kNW; ++q2) { num += red[2 * q2]; den += red[2 * q2 + 1]; }
         double *pp = a.partials + ((size_t)b * a.nch + tile) * 2;
         pp[0] = num;
         pp[1] = den;
       }
     }
   }
+  // ---- the next pass's aggregates: exclusive in-tile prefixes E_t and tile totals
   if (NEXT) {
+    double eA[SP], eB;
+    warp_scan<ND, SP>(An, Pn, eA, eB, lane);
+    const int sl = ND == 0 ? lane : 31 - lane;
+    const int sw = ND == 0 ? w : kNW - 1 - w;
+    if (sl == 31) {
 #pragma unroll
-    for (int q = 0; q < S; ++q)
-      if (ok[q]) a.aggT_next[(size_t)sys[q] * nthr + thr] = An[q];
-    double T[S];
-    cta_compose<ND, NW, S>(An, Pn, red, t, T);
+      for (int q = 0; q < SP; ++q) tot[sw][q] = An[q];
+      tot[sw][SP] = Pn;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < SP; ++q) {
+      double wA = 0.0;
+      for (int k = 0; k < sw; ++k) wA = fma(tot[k][SP], wA, tot[k][q]);
+      if (ok[q]) a.aggT_next[(size_t)sys[q] * nthr + thr] = fma(eB, wA, eA[q]);
+    }
     if (t == 0) {
 #pragma unroll
-      for (int q = 0; q < S; ++q)
-        if (ok[q]) a.aggL_next[(size_t)sys[q] * a.ntiles + tile] = T[q];
+      for (int q = 0; q < SP; ++q) {
+        double T = 0.0;
+        for (int k = 0; k < kNW; ++k) T = fma(tot[k][SP], T, tot[k][q]);
+        if (ok[q]) a.aggL_next[(size_t)sys[q] * a.ntiles + tile] = T;
+      }
     }
   }
+}
+
+// ---------------------------------------------------------------- k_pass_res (persistent)
+// Items in tile-major order (item = pos·ngroups + g); a group is SP·H systems sharing a factor
+// set: half h (kSNT threads) runs systems h·SP … h·SP+SP−1 of the group, SP per thread.
+// One __syncthreads per item: the look-back broadcast and scan scratch are double-buffered by
+// item parity, and an item's next-pass prefixes/totals and its stage refill are finished after
+// the next item's barrier (which every warp reaches only once done with the item).
+template <int SP, int H, int NST>
+struct ResSmem {
+  double ip[kSTile], mt[kSTile], cj[kSTile];  // interleaved, this CTA's current tile
+  float x[NST][H][SP][kSTile];
+};
+template <int SP, int H, int NST>
+constexpr size_t res_smem_bytes() { return sizeof(ResSmem<SP, H, NST>); }
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "PR_MBAR_WAIT%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra PR_MBAR_WAIT%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+// Item cursor in tile-major order: item = pos·ngroups + g, g = lg·B + b.
+template <int SG>
+struct ResCursor {
+  int pos, g, b, lg;
+  __device__ __forceinline__ void init(const PassArgs &a, unsigned k) {
+    const unsigned ng = (unsigned)a.ngroups;
+    pos = (int)(k / ng);
+    g = (int)(k - (unsigned)pos * ng);
+    lg = g / a.B;
+    b = g - lg * a.B;
+  }
+  __device__ __forceinline__ void step(const PassArgs &a) {
+    if (++g == a.ngroups) { g = 0; b = 0; lg = 0; ++pos; return; }
+    if (++b == a.B) { b = 0; ++lg; }
+  }
+  template <int DIR>
+  __device__ __forceinline__ int tile(const PassArgs &a) const { return DIR == 0 ? pos : a.ntiles - 1 - pos; }
+  __device__ __forceinline__ bool ok(const PassArgs &a, int slot) const { return lg * SG + slot < a.nsl; }
+  __device__ __forceinline__ int sys(const PassArgs &a, int slot) const {
+    return (ok(a, slot) ? lg * SG + slot : lg * SG) * a.B + b;
+  }
+};
+
+template <int DIR, int SP, int H, int NST>
+__global__ void __launch_bounds__(H *kSNT) k_pass_res(PassArgs a) {
+  constexpr int ND = 1 - DIR;
+  constexpr int SG = SP * H;  // systems per item
+  static_assert(SP <= kNW, "one look-back warp per system");
+  extern __shared__ __align__(128) unsigned char res_smem_raw[];
+  ResSmem<SP, H, NST> &sm = *reinterpret_cast<ResSmem<SP, H, NST> *>(res_smem_raw);
+  __shared__ __align__(8) uint64_t full[NST];
+  __shared__ double s_yin[2][H][SP];
+  __shared__ double tot[2][H][kNW][SP + 1];
+  const int t = threadIdx.x, h = t / kSNT, tt = t % kSNT, lane = t & 31, wl = tt >> 5;
+  const unsigned nitems = (unsigned)a.ngroups * (unsigned)a.ntiles;
+  const unsigned lo = (unsigned)(((unsigned long long)blockIdx.x * nitems) / gridDim.x);
+  const unsigned hi = (unsigned)(((unsigned long long)(blockIdx.x + 1) * nitems) / gridDim.x);
+  const size_t nthr = (size_t)a.Mt / kSPS;
+  const int swN = ND == 0 ? wl : kNW - 1 - wl;  // this warp's position in the next pass's order
+  const int slN = ND == 0 ? lane : 31 - lane;
+  const uint64_t pol_stream = policy_evict_first();
+  using Cur = ResCursor<SG>;
+
+  Cur cur, nxt, iss, prev;
+  auto issue = [&](int stage) {  // one thread: stream item `iss` into `stage`
+    mbar_expect_tx(&full[stage], (uint32_t)(SG * kSTile * sizeof(float)));
+    const int tile = iss.template tile<DIR>(a);
+#pragma unroll
+    for (int hh = 0; hh < H; ++hh)
+#pragma unroll
+      for (int q = 0; q < SP; ++q)
+        bulk_g2s(sm.x[stage][hh][q], a.in + (size_t)iss.sys(a, hh * SP + q) * a.Mt + (size_t)tile * kSTile,
+                 kSTile * sizeof(float), &full[stage], pol_stream);
+    iss.step(a);
+  };
+  if (t == 0) {
+    for (int i = 0; i < NST; ++i) mbar_init(&full[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  cur.init(a, lo);
+  nxt = cur;
+  iss = cur;
+  prev = cur;
+  if (t == 0)
+    for (int i = 0; i < NST && lo + i < hi; ++i) issue(i);
+  // register prefetch of an item's entering prefixes and look-back operands (own systems),
+  // two items ahead (slot i & 1); the factor set of the last instance seen is cached
+  struct Pre {
+    double E[SP], P, LA, LB;
+    int W, set;
+  };
+  Pre pre[2];
+  int cb = -1, cset = 0;
+  auto prefetch = [&](const Cur &c, Pre &r) {
+    const int tile = c.template tile<DIR>(a);
+    if (c.b != cb) {
+      cb = c.b;
+      cset = a.fset[cb];
+    }
+    const int set = cset;
+    r.set = set;
+    const size_t thr = (size_t)tile * kSNT + tt;
+#pragma unroll
+    for (int q = 0; q < SP; ++q) r.E[q] = a.aggT_cur[(size_t)c.sys(a, h * SP + q) * nthr + thr];
+    r.P = __ldg(a.f.thrP + ((size_t)DIR * a.nsets + set) * nthr + thr);
+    r.LA = 0.0;
+    r.LB = 1.0;
+    r.W = 0;
+    if (wl >= kNW - SP && c.pos > 0) {
+      const int q = kNW - 1 - wl;
+      const size_t tb = ((size_t)DIR * a.nsets + set) * a.ntiles;
+      r.W = __ldg(a.f.tileW + tb + c.pos);
+      const int p = c.pos - 1 - lane;
+      if (p >= 0) {
+        r.LA = a.aggL_cur[(size_t)c.sys(a, h * SP + q) * a.ntiles + (DIR == 0 ? p : a.ntiles - 1 - p)];
+        r.LB = __ldg(a.f.tileB + tb + p);
+      }
+    }
+  };
+  // the previous item's next-pass aggregates (its warp totals are in tot[pb]), after a barrier
+  double qA[SP], qB = 1.0;  // the previous item's exclusive in-warp prefixes (next-pass order)
+  auto finish = [&](int pb) {
+    const int tile = prev.template tile<DIR>(a);
+#pragma unroll
+    for (int q = 0; q < SP; ++q) {
+      double wA = 0.0;
+      for (int k = 0; k < swN; ++k) wA = fma(tot[pb][h][k][SP], wA, tot[pb][h][k][q]);
+      const int slot = h * SP + q;
+      if (prev.ok(a, slot))
+        a.aggT_next[(size_t)prev.sys(a, slot) * nthr + (size_t)tile * kSNT + tt] = fma(qB, wA, qA[q]);
+    }
+    if (tt < SP) {  // thread q of each half: tile total of system q
+      const int q = tt;
+      double T = 0.0;
+      for (int k = 0; k < kNW; ++k) T = fma(tot[pb][h][k][SP], T, tot[pb][h][k][q]);
+      const int slot = h * SP + q;
+      if (prev.ok(a, slot)) a.aggL_next[(size_t)prev.sys(a, slot) * a.ntiles + tile] = T;
+    }
+  };
+  if (lo < hi) prefetch(nxt, pre[0]);
+  nxt.step(a);
+  if (lo + 1 < hi) prefetch(nxt, pre[1]);
+  nxt.step(a);
+  int fac_tile = -1, fac_set = -1;
+  int n = 0;
+  for (unsigned k = lo; k < hi; ++k, ++n) {
+    const int stage = n % NST;
+    const int pb = n & 1;
+    const uint32_t parity = (uint32_t)(n / NST) & 1u;
+    double E[SP], P, LA, LB;
+    int W, set;
+    if (n & 1) {  // (static register indexing)
+#pragma unroll
+      for (int q = 0; q < SP; ++q) E[q] = pre[1].E[q];
+      P = pre[1].P; LA = pre[1].LA; LB = pre[1].LB; W = pre[1].W; set = pre[1].set;
+      if (k + 2 < hi) prefetch(nxt, pre[1]);
+    } else {
+#pragma unroll
+      for (int q = 0; q < SP; ++q) E[q] = pre[0].E[q];
+      P = pre[0].P; LA = pre[0].LA; LB = pre[0].LB; W = pre[0].W; set = pre[0].set;
+      if (k + 2 < hi) prefetch(nxt, pre[0]);
+    }
+    if (k + 2 < hi) nxt.step(a);
+    const int tile = cur.template tile<DIR>(a);
+    // ---- the value entering the tile (warps kNW−SP … kNW−1 of each half)
+    if (wl >= kNW - SP) {
+      const int q = kNW - 1 - wl;
+      double mA = lane < W ? LA : 0.0, mB = lane < W ? LB : 1.0;
+      compose_window(mA, mB, lane);
+      double y = mA;
+      if (W > 32) y = look_back<DIR>(a, cur.sys(a, h * SP + q), cur.pos, set, lane, 32, mA, mB);  // rare
+      if (lane == 0) s_yin[pb][h][q] = y;
+    }
+    __syncthreads();  // the barrier of the item
+    if (n > 0) {
+      finish(pb ^ 1);
+      if (t == 0 && k - 1 + NST < hi) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue((n - 1) % NST);
+      }
+    }
+    // ---- factors of a new tile: 1/p from global, m̃ and c derived once
+    if (tile != fac_tile || set != fac_set) {
+      const double *ipg = a.f.ip + (size_t)set * a.Mt + (size_t)tile * kSTile;
+      const double c0 = __ldg(a.f.coef + 2 * set), c1 = __ldg(a.f.coef + 2 * set + 1);
+      constexpr int kPer = kSTile / (H * kSNT);
+      double ipl[kPer];
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) ipl[u] = __ldg(ipg + t + u * H * kSNT);  // all loads in flight
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) {
+        const int e = t + u * H * kSNT;
+        const int j = tile * kSTile + (e % kSNT) * kSPS + e / kSNT;
+        double mtj, cjj;
+        factors<true>(c0, c1, (double)(j + 1), ipl[u], j, a.M, mtj, cjj);
+        sm.ip[e] = ipl[u];
+        sm.mt[e] = mtj;
+        sm.cj[e] = cjj;
+      }
+      fac_tile = tile;
+      fac_set = set;
+      __syncthreads();
+    }
+    double v[SP];
+#pragma unroll
+    for (int q = 0; q < SP; ++q) v[q] = fma(P, s_yin[pb][h][q], E[q]);
+    // ---- the recurrence over the staged tile
+    mbar_wait(&full[stage], parity);
+    const int j0 = tile * kSTile + tt * kSPS;
+    const double *ips = sm.ip + tt, *mts = sm.mt + tt, *cjs = sm.cj + tt;
+    double An[SP], Pn = 1.0;
+    float *op[SP];
+    const float *xs[SP];
+    bool okq[SP];
+#pragma unroll
+    for (int q = 0; q < SP; ++q) {
+      An[q] = 0.0;
+      okq[q] = cur.ok(a, h * SP + q);
+      op[q] = a.out + (size_t)cur.sys(a, h * SP + q) * a.Mt + (size_t)tile * kSTile + tt;
+      xs[q] = sm.x[stage][h][q] + tt;
+    }
+    auto run = [&](auto bc_tag) {
+      constexpr bool BC = decltype(bc_tag)::value;
+      double bcv[SP];
+      const int ibc = a.M - 1 - j0;
+#pragma unroll
+      for (int q = 0; q < SP; ++q)
+        bcv[q] = BC ? bc_term(a, cur.b, a.n_base + a.ln0 + cur.lg * SG + h * SP + q, a.step_m + DIR) : 0.0;
+#pragma unroll
+      for (int ii = 0; ii < kSPS; ++ii) {
+        const int i = DIR == 0 ? ii : kSPS - 1 - ii;
+        const double ipj = ips[i * kSNT];
+        const double f1 = DIR == 0 ? mts[i * kSNT] : cjs[i * kSNT];  // this pass's multiplier
+        const double f2 = DIR == 0 ? cjs[i * kSNT] : mts[i * kSNT];  // the next pass's
+#pragma unroll
+        for (int q = 0; q < SP; ++q) {
+          const double xin = (double)xs[q][i * kSNT];
+          if (DIR == 0) {
+            const double r = (BC && i == ibc) ? xin + bcv[q] : xin;
+            v[q] = fma(-f1, v[q], r * ipj);
+            An[q] = fma(v[q], Pn, An[q]);
+          } else {
+            v[q] = fma(-f1, v[q], xin);
+            const double r = (BC && i == ibc) ? v[q] + bcv[q] : v[q];
+            An[q] = fma(r * ipj, Pn, An[q]);
+          }
+          if (okq[q]) __stcs(op[q] + i * kSNT, (float)v[q]);
+        }
+        Pn *= -f2;
+      }
+    };
+    if (j0 <= a.M - 1 && a.M - 1 < j0 + kSPS) run(std::true_type{});
+    else run(std::false_type{});
+    // ---- next-pass aggregates: in-warp scan now, cross-warp after the next barrier
+    warp_scan<ND, SP>(An, Pn, qA, qB, lane);
+    if (slN == 31) {
+#pragma unroll
+      for (int q = 0; q < SP; ++q) tot[pb][h][swN][q] = An[q];
+      tot[pb][h][swN][SP] = Pn;
+    }
+    prev = cur;
+    cur.step(a);
+  }
+  __syncthreads();
+  if (n > 0) finish((n - 1) & 1);
 }
 
 // U_k := F̂_{k−1} with the δ partial of slice k (reading Q12), elementwise.
@@ -580,43 +855,90 @@ __global__ void k_copy_delta(float *Uk, const float *F, int M, int Mp, double *p
   }
 }
 
-// Systems per CTA for a launch over nsl slices (S consecutive slices share a factor set).
-static int pick_S(int nsl, int epi) {
-  if (epi == EPI_CHAIN) return 1;
-  if (const char *e = getenv("PR_K2_S")) {  // tuning override (1, 2 or 4)
-    const int v = atoi(e);
-    if (v == 1 || v == 2 || v == 4) return nsl >= v ? v : 1;
-  }
-  if (nsl >= 2) return 2;  // S = 4 measured slower at C3 (170 registers: 3 CTAs/SM)
-  return 1;
+// ---------------------------------------------------------------- host drivers
+static int env_int(const char *name, int dflt) {
+  const char *e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+// tuning overrides: PR_K2_PIPE=0 (no persistent kernel), PR_K2_SP (1|2), PR_K2_H (1|2), PR_K2_STAGES (2|3|4)
+struct ResConfig {
+  int enabled, sp, h, nst;
+};
+static ResConfig res_config() {
+  static const ResConfig c = [] {
+    ResConfig r;
+    r.enabled = env_int("PR_K2_PIPE", 1);
+    r.sp = env_int("PR_K2_SP", 2) == 1 ? 1 : 2;
+    r.h = env_int("PR_K2_H", 2) == 1 ? 1 : 2;
+    const int n = env_int("PR_K2_STAGES", 2);  // (SP, H, NST) = (2, 2, 2): best measured at C3
+    r.nst = n == 3 || n == 4 ? n : 2;
+    return r;
+  }();
+  return c;
 }
 
-template <int S>
-static void launch_S(int dir, bool in_il, bool next, const PassArgs &a, unsigned grid, cudaStream_t s) {
+template <int DIR, int SP, int H, int NST>
+static cudaError_t launch_res_dir(PassArgs a, cudaStream_t s) {
+  static int grid_cap = 0;
+  constexpr size_t smem = res_smem_bytes<SP, H, NST>();
+  if (grid_cap == 0) {
+    cudaError_t e =
+        cudaFuncSetAttribute(k_pass_res<DIR, SP, H, NST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int dev = 0, nsm = 0, occ = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_pass_res<DIR, SP, H, NST>, H * kSNT, smem);
+    if (e != cudaSuccess) return e;
+    grid_cap = nsm * (occ > 0 ? occ : 1);
+  }
+  a.ngroups = a.B * ((a.nsl + SP * H - 1) / (SP * H));
+  const long long nitems = (long long)a.ngroups * a.ntiles;
+  const unsigned grid = (unsigned)(nitems < grid_cap ? nitems : grid_cap);
+  k_pass_res<DIR, SP, H, NST><<<grid, H * kSNT, smem, s>>>(a);
+  return cudaGetLastError();
+}
+template <int SP, int H>
+static cudaError_t launch_res_h(int dir, const PassArgs &a, int nst, cudaStream_t s) {
+  switch (nst) {
+    case 2: return dir == 0 ? launch_res_dir<0, SP, H, 2>(a, s) : launch_res_dir<1, SP, H, 2>(a, s);
+    case 4: return dir == 0 ? launch_res_dir<0, SP, H, 4>(a, s) : launch_res_dir<1, SP, H, 4>(a, s);
+    default: return dir == 0 ? launch_res_dir<0, SP, H, 3>(a, s) : launch_res_dir<1, SP, H, 3>(a, s);
+  }
+}
+static cudaError_t launch_res(int dir, const PassArgs &a, cudaStream_t s) {
+  const ResConfig c = res_config();
+  const int sp = a.nsl >= c.sp ? c.sp : 1;
+  if (sp == 2) return c.h == 2 ? launch_res_h<2, 2>(dir, a, c.nst, s) : launch_res_h<2, 1>(dir, a, c.nst, s);
+  return c.h == 2 ? launch_res_h<1, 2>(dir, a, c.nst, s) : launch_res_h<1, 1>(dir, a, c.nst, s);
+}
+
+template <int SP>
+static void launch_tile(int dir, bool in_il, bool next, const PassArgs &a, cudaStream_t s) {
+  const unsigned grid = (unsigned)((unsigned long long)a.ngroups * a.ntiles);
   if (dir == 0) {
-    if (in_il) k_streamed_pass<0, true, true, true, S><<<grid, kSNT, 0, s>>>(a);
-    else k_streamed_pass<0, false, true, true, S><<<grid, kSNT, 0, s>>>(a);
+    if (in_il) k_streamed_pass<0, true, true, true, SP><<<grid, kSNT, 0, s>>>(a);
+    else k_streamed_pass<0, false, true, true, SP><<<grid, kSNT, 0, s>>>(a);
   } else if (a.epi == EPI_X) {
-    if (next) k_streamed_pass<1, true, true, true, S><<<grid, kSNT, 0, s>>>(a);
-    else k_streamed_pass<1, true, true, false, S><<<grid, kSNT, 0, s>>>(a);
+    if (next) k_streamed_pass<1, true, true, true, SP><<<grid, kSNT, 0, s>>>(a);
+    else k_streamed_pass<1, true, true, false, SP><<<grid, kSNT, 0, s>>>(a);
   } else {
-    k_streamed_pass<1, true, false, false, S><<<grid, kSNT, 0, s>>>(a);
+    k_streamed_pass<1, true, false, false, SP><<<grid, kSNT, 0, s>>>(a);
   }
 }
 
 // Forward passes read aggregates [0] and write [1]; backward passes read [1] and write [0].
-static cudaError_t launch_pass(StreamedState &st, int dir, bool in_il, bool next, PassArgs a, int S,
-                               cudaStream_t s) {
+static cudaError_t launch_pass(StreamedState &st, int dir, bool in_il, bool next, PassArgs a, cudaStream_t s) {
   a.ntiles = st.ntiles;
   a.aggT_cur = st.aggT[dir];
   a.aggL_cur = st.aggL[dir];
   a.aggT_next = st.aggT[1 - dir];
   a.aggL_next = st.aggL[1 - dir];
-  a.ngroups = a.B * ((a.nsl + S - 1) / S);
-  const unsigned grid = (unsigned)((unsigned long long)a.ngroups * st.ntiles);
-  if (S == 4) launch_S<4>(dir, in_il, next, a, grid, s);
-  else if (S == 2) launch_S<2>(dir, in_il, next, a, grid, s);
-  else launch_S<1>(dir, in_il, next, a, grid, s);
+  if (in_il && next && a.epi == EPI_X && res_config().enabled) return launch_res(dir, a, s);
+  const int sp = (a.epi != EPI_CHAIN && a.nsl >= 2) ? 2 : 1;
+  a.ngroups = a.B * ((a.nsl + sp - 1) / sp);
+  if (sp == 2) launch_tile<2>(dir, in_il, next, a, s);
+  else launch_tile<1>(dir, in_il, next, a, s);
   return cudaGetLastError();
 }
 
@@ -644,21 +966,20 @@ static cudaError_t streamed_steps(StreamedState &st, const PassArgs &a, const fl
     if (e != cudaSuccess) return e;
     *nl += 1;
   }
-  const int S = pick_S(a.nsl, a.epi);
   for (int m = 0; m < steps; ++m) {
     PassArgs f = a;
     f.step_m = m;
     f.in = (m == 0) ? in0 : st.X;
     f.out = st.Y;
     f.epi = EPI_X;
-    cudaError_t e = launch_pass(st, 0, m > 0, true, f, S, s);
+    cudaError_t e = launch_pass(st, 0, m > 0, true, f, s);
     if (e != cudaSuccess) return e;
     PassArgs g = a;
     g.step_m = m;
     g.in = st.Y;
     g.out = st.X;
     if (m < steps - 1) g.epi = EPI_X;
-    e = launch_pass(st, 1, true, m < steps - 1, g, S, s);
+    e = launch_pass(st, 1, true, m < steps - 1, g, s);
     if (e != cudaSuccess) return e;
     *nl += 2;
   }

@@ -91,7 +91,7 @@ struct Scheme {
   double *m = nullptr, *ip = nullptr, *cu = nullptr;  // device [nsets][Mp] (K1)
   double *iip = nullptr;                            // device [nsets][Mt] 1/p, interleaved (K2)
   double *coef = nullptr;                           // device [nsets][2] dτr/2, dτσ²/2 (K2)
-  double *thrB = nullptr;                           // device [2][nsets][Mt/kSPS] (K2 thread multipliers)
+  double *thrP = nullptr;                           // device [2][nsets][Mt/kSPS] (K2 in-tile prefix multipliers)
   double *tileB = nullptr;                          // device [2][nsets][ntiles] (K2 look-back)
   int *tileW = nullptr;
   double *bcoef = nullptr;                          // device [B]
@@ -239,7 +239,7 @@ pr_status upload_scheme(pr_ctx *c, Scheme &sc, int steps) {
   CU(cudaMemcpy(sc.ip, ip.data(), n * sizeof(double), cudaMemcpyHostToDevice));
   CU(cudaMemcpy(sc.cu, cu.data(), n * sizeof(double), cudaMemcpyHostToDevice));
   // K2: 1/p in the thread-interleaved layout (1 beyond M), the closed-form off-diagonal
-  // coefficients, and the per-thread multipliers Π(−m_j) (dir 0) / Π(−u_j/p_j) (dir 1)
+  // coefficients, and the per-thread multipliers Π(−l_j/p_j) (dir 0) / Π(−u_j/p_j) (dir 1)
   const int Mt = pr::streamed_Mt(c->M);
   const size_t nthr = (size_t)Mt / pr::kSPS;
   // K2's forward pass runs on w = y/p: multiplier m̃_j = l_j/p_j (none in row 0)
@@ -266,12 +266,25 @@ pr_status upload_scheme(pr_ctx *c, Scheme &sc, int steps) {
         thB[((size_t)dir * c->nsets + s) * nthr + q] = prod;
       }
   }
+  // → P_t: product of the multipliers of the threads preceding t in its tile, in pass order
+  std::vector<double> thP(thB.size());
+  for (int dir = 0; dir < 2; ++dir)
+    for (int s = 0; s < c->nsets; ++s)
+      for (size_t tile = 0; tile < nthr / pr::kSNT; ++tile) {
+        const size_t base = ((size_t)dir * c->nsets + s) * nthr + tile * pr::kSNT;
+        double prod = 1.0;
+        for (int k = 0; k < pr::kSNT; ++k) {
+          const int t = dir == 0 ? k : pr::kSNT - 1 - k;
+          thP[base + t] = prod;
+          prod *= thB[base + t];
+        }
+      }
   CU(cudaMalloc(&sc.iip, iip.size() * sizeof(double)));
   CU(cudaMalloc(&sc.coef, coef.size() * sizeof(double)));
-  CU(cudaMalloc(&sc.thrB, thB.size() * sizeof(double)));
+  CU(cudaMalloc(&sc.thrP, thP.size() * sizeof(double)));
   CU(cudaMemcpy(sc.iip, iip.data(), iip.size() * sizeof(double), cudaMemcpyHostToDevice));
   CU(cudaMemcpy(sc.coef, coef.data(), coef.size() * sizeof(double), cudaMemcpyHostToDevice));
-  CU(cudaMemcpy(sc.thrB, thB.data(), thB.size() * sizeof(double), cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(sc.thrP, thP.data(), thP.size() * sizeof(double), cudaMemcpyHostToDevice));
   // K2 look-back data, indexed by scan position (dir 0: tiles ascending, dir 1: descending):
   // tile multiplier B = Π(−l_j/p_j) resp. Π(−u_j/p_j) over the tile, and the window W = number of
   // predecessors whose aggregates are composed: the first W with |Π_{k≤W} B_{pos−k}| below
@@ -322,7 +335,7 @@ void free_scheme(Scheme &s) {
   cudaFree(s.tileW);
   cudaFree(s.iip);
   cudaFree(s.coef);
-  cudaFree(s.thrB);
+  cudaFree(s.thrP);
   cudaFree(s.m);
   cudaFree(s.ip);
   cudaFree(s.cu);
@@ -334,7 +347,7 @@ pr::StreamedProblem sprob(const pr_ctx *c, const Scheme &sc) {
   pr::StreamedProblem p;
   p.f.ip = sc.iip;
   p.f.coef = sc.coef;
-  p.f.thrB = sc.thrB;
+  p.f.thrP = sc.thrP;
   p.f.tileB = sc.tileB;
   p.f.tileW = sc.tileW;
   p.nsets = c->nsets;
