@@ -198,10 +198,11 @@ def roofline(p, ph, K, world, rank, pk, pk_src, clk_mhz, n_sm, synth):
                     % (n_sm, clk_mhz), "work_per_unit": "9 fp64 flop per point-step", "launch_unit": "one sweep"}
             tr = ncu_traffic("k_fine_sweep")
         else:
-            roof = {"kernel": "k_streamed_pass (K2)", "bound": "hbm", "achieved": 16.0 * pt_steps / sweep_s / 1e9,
+            roof = {"kernel": "k_pass_res (K2, persistent streamed pass)", "bound": "hbm",
+                    "achieved": 16.0 * pt_steps / sweep_s / 1e9,
                     "peak": float(pk["hbm_gbs"]), "unit": "GB/s", "peak_source": pk_src,
                     "work_per_unit": "16 B per point-step", "launch_unit": "one pass (8 B per point)"}
-            tr = ncu_traffic("k_streamed_pass")
+            tr = ncu_traffic("k_pass_res")
     else:
         evals = float(p.B) * p.M * nloc
         chain_s = ph["ms_coarse"] / (K + 1) / 1e3
@@ -242,8 +243,8 @@ def c3_fine_sweep_roofline(parareal, synth, torch, stream, pk, pk_src, flush):
         t = statistics.median(ms) / 1e3
         pt_steps = float(p.M) * p.N * p.fine_steps
         ach = 16.0 * pt_steps / t / 1e9
-        tr = ncu_traffic("k_streamed_pass")
-        return {"kernel": "k_streamed_pass (K2)", "workload": "C3 fine sweep: 64 slices x 2^20 points x 100 IE steps",
+        tr = ncu_traffic("k_pass_res")
+        return {"kernel": "k_pass_res (K2, persistent streamed pass)", "workload": "C3 fine sweep: 64 slices x 2^20 points x 100 IE steps",
                 "bound": "hbm", "achieved": ach, "peak": float(pk["hbm_gbs"]), "unit": "GB/s",
                 "frac": ach / float(pk["hbm_gbs"]), "peak_source": pk_src, "ms_per_sweep": t * 1e3,
                 "point_steps_per_s": pt_steps / t, "work_per_unit": "16 B per point-step (fp32 read+write, 2 passes)",

@@ -908,9 +908,14 @@ static cudaError_t launch_res_h(int dir, const PassArgs &a, int nst, cudaStream_
 }
 static cudaError_t launch_res(int dir, const PassArgs &a, cudaStream_t s) {
   const ResConfig c = res_config();
-  const int sp = a.nsl >= c.sp ? c.sp : 1;
-  if (sp == 2) return c.h == 2 ? launch_res_h<2, 2>(dir, a, c.nst, s) : launch_res_h<2, 1>(dir, a, c.nst, s);
-  return c.h == 2 ? launch_res_h<1, 2>(dir, a, c.nst, s) : launch_res_h<1, 1>(dir, a, c.nst, s);
+  // no more systems per item than the launch has slices (an empty slot would stream a duplicate)
+  int sp = c.sp, h = c.h;
+  while (sp * h > a.nsl) {
+    if (sp > 1) sp = 1;
+    else h = 1;
+  }
+  if (sp == 2) return h == 2 ? launch_res_h<2, 2>(dir, a, c.nst, s) : launch_res_h<2, 1>(dir, a, c.nst, s);
+  return h == 2 ? launch_res_h<1, 2>(dir, a, c.nst, s) : launch_res_h<1, 1>(dir, a, c.nst, s);
 }
 
 template <int SP>
@@ -934,7 +939,9 @@ static cudaError_t launch_pass(StreamedState &st, int dir, bool in_il, bool next
   a.aggL_cur = st.aggL[dir];
   a.aggT_next = st.aggT[1 - dir];
   a.aggL_next = st.aggL[1 - dir];
-  if (in_il && next && a.epi == EPI_X && res_config().enabled) return launch_res(dir, a, s);
+  // The persistent kernel pays off when several items share each tile's factors (C3: 16 groups
+  // of 4 slices); a lone system (the serial fine solve) runs one CTA per tile.
+  if (in_il && next && a.epi == EPI_X && res_config().enabled && a.B * a.nsl >= 16) return launch_res(dir, a, s);
   const int sp = (a.epi != EPI_CHAIN && a.nsl >= 2) ? 2 : 1;
   a.ngroups = a.B * ((a.nsl + sp - 1) / sp);
   if (sp == 2) launch_tile<2>(dir, in_il, next, a, s);
