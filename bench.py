@@ -45,6 +45,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-c3-sweep", action="store_true", help="skip the C3 fine-sweep HBM roofline leg")
+    ap.add_argument("--no-graphs", action="store_true", help="eager launches instead of the captured CUDA graph")
     return ap.parse_args()
 
 
@@ -165,6 +166,7 @@ def config_dict(args, p):
                             p.max_iter),
             "M": p.M, "N": p.N, "B": p.B, "fine_steps": p.fine_steps, "K": p.max_iter,
             "coarse": args.coarse, "parallelism": "time-slices/%d" % args.gpus,
+            "cuda_graph": (not args.no_graphs) and args.gpus == 1,
             "l2": "flushed (256 MiB write) before every timed step" if p.M * p.B * 4 * (p.N + 1) * 3 < (126 << 20)
             else "working set larger than L2"}
 
@@ -286,6 +288,8 @@ def main():
         ctx.load_weights(net)
     ws = torch.empty(ctx.workspace_bytes(), dtype=torch.uint8, device="cuda")
     ctx.bind_workspace(ws)
+    if not args.no_graphs:
+        ctx.set_option(parareal.OPT_USE_GRAPHS, 1)  # fixed-K single-GPU solves replay one CUDA graph
     out = torch.empty((p.B, p.M), dtype=torch.float32, device="cuda")
     flush = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device="cuda")
 

@@ -142,6 +142,16 @@ struct pr_ctx {
   int opt_pinn_kernel = 0;
   int opt_fine_kernel = 0;
   int opt_graphs = 0;
+  bool capturing = false;
+  // captured solve (PR_OPT_USE_GRAPHS)
+  cudaGraphExec_t g_exec = nullptr;
+  const float *g_vt = nullptr;
+  float *g_v0 = nullptr;
+  int g_K = 0;
+  int64_t g_launches = 0;
+  cudaEvent_t g_e0 = nullptr, g_e1 = nullptr;
+  std::vector<cudaEvent_t> g_events;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> g_spans;
   int64_t launches = 0;
   bool solved = false;
   // timing
@@ -623,6 +633,12 @@ pr_status store_rows(pr_ctx *c, float *dst, const float *src, bool device_ptr) {
   return PR_OK;
 }
 
+// Timing events; under stream capture they must be captured as timestamp (external) nodes.
+void record(pr_ctx *c, cudaEvent_t e) {
+  if (c->capturing) cudaEventRecordWithFlags(e, c->stream, cudaEventRecordExternal);
+  else cudaEventRecord(e, c->stream);
+}
+
 struct PhaseTimer {
   pr_ctx *c;
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> spans;
@@ -631,12 +647,12 @@ struct PhaseTimer {
   void begin(int phase) {
     a = next_event(c);
     cur = phase;
-    if (a) cudaEventRecord(a, c->stream);
+    if (a) record(c, a);
   }
   void end() {
     cudaEvent_t b = next_event(c);
     if (a && b) {
-      cudaEventRecord(b, c->stream);
+      record(c, b);
       spans.push_back({cur, {a, b}});
     }
   }
@@ -682,17 +698,70 @@ pr_plan make_plan(int N, int world, int rank, int k) {
   return P;
 }
 
+using Spans = std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>>;
+
+pr_status solve_report(pr_ctx *c, int K, int conv, cudaEvent_t e0, cudaEvent_t e1, const Spans &spans,
+                       int64_t launches, pr_report *rep) {
+  c->solved = true;
+  if (!rep) return PR_OK;
+  rep->iterations = K;
+  rep->converged = (c->tol > 0.0 && K > 0 && c->h_delta[K - 1] < c->tol) ? 1 : conv;
+  if (rep->delta)
+    for (int i = 0; i < K; ++i) rep->delta[i] = c->h_delta[i];
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  rep->ms_total = ms;
+  double ph[4] = {0, 0, 0, 0};
+  for (auto &sp : spans) {
+    float m = 0;
+    cudaEventElapsedTime(&m, sp.second.first, sp.second.second);
+    ph[sp.first] += m;
+  }
+  rep->ms_coarse = ph[PH_COARSE];
+  rep->ms_fine = ph[PH_FINE];
+  rep->ms_comm = ph[PH_COMM];
+  rep->ms_setup = ph[PH_SETUP];
+  rep->kernel_launches = launches;
+  return PR_OK;
+}
+
+void drop_graph(pr_ctx *c) {
+  if (c->g_exec) cudaGraphExecDestroy(c->g_exec);
+  c->g_exec = nullptr;
+  for (cudaEvent_t e : c->g_events) cudaEventDestroy(e);
+  c->g_events.clear();
+  c->g_vt = nullptr;
+  c->g_v0 = nullptr;
+}
+
 pr_status solve_impl(pr_ctx *c, const float *V_T, float *V_0, bool device_ptr, pr_report *rep) {
   pr_status st = check_ctx(c);
   if (st) return st;
   if (c->coarse == PR_COARSE_PINN && !c->have_pinn)
     return fail(c, PR_ERR_STATE, "coarse == PR_COARSE_PINN but no weights loaded (parareal_load_pinn_weights)");
   if ((st = ensure_ws(c))) return st;
+  // CUDA-graph replay of a fixed-K single-GPU device-pointer solve (PR_OPT_USE_GRAPHS): the whole
+  // solve (≈ 4K+4 kernels) is captured once per (V_T, V_0) pair and relaunched as one graph.
+  const bool use_graph = c->opt_graphs && c->tol == 0.0 && c->world == 1 && device_ptr;
+  if (use_graph && c->g_exec && c->g_vt == V_T && c->g_v0 == V_0) {
+    CU(cudaGraphLaunch(c->g_exec, c->stream));
+    c->launches += c->g_launches;
+    CU(cudaStreamSynchronize(c->stream));
+    return solve_report(c, c->g_K, 0, c->g_e0, c->g_e1, c->g_spans, c->g_launches, rep);
+  }
+  if (use_graph) {
+    drop_graph(c);
+    CU(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    c->capturing = true;
+  }
   c->ev_used = 0;
   const int64_t launches0 = c->launches;
   PhaseTimer pt{c};
   cudaEvent_t e0 = next_event(c), e1 = nullptr;
-  cudaEventRecord(e0, c->stream);
+  int K = 0, conv = 0;
+  st = [&]() -> pr_status {
+  pr_status st = PR_OK;
+  record(c, e0);
   const int R = c->world, r = c->rank;
   const size_t row = (size_t)c->B * c->Mp;
   // δ partials are rewritten slice by slice; clear stale chunks of earlier solves
@@ -717,7 +786,6 @@ pr_status solve_impl(pr_ctx *c, const float *V_T, float *V_0, bool device_ptr, p
       pt.end();
     }
   }
-  int K = 0, conv = 0;
   for (int k = 1; k <= c->max_iter; ++k) {
     const pr_plan P = make_plan(c->N, R, r, k);
     // (i) fine sweep F̂_n = F(U^{k−1}_n), n = k−1..N−1 (parallel across slices)
@@ -766,31 +834,39 @@ pr_status solve_impl(pr_ctx *c, const float *V_T, float *V_0, bool device_ptr, p
     if ((st = store_rows(c, V_0, src, device_ptr))) return st;
   }
   e1 = next_event(c);
-  cudaEventRecord(e1, c->stream);
+  record(c, e1);
   CU(cudaMemcpyAsync(c->h_delta, c->d_delta, K * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-  CU(cudaStreamSynchronize(c->stream));
-  c->solved = true;
-  if (rep) {
-    rep->iterations = K;
-    rep->converged = (c->tol > 0.0 && K > 0 && c->h_delta[K - 1] < c->tol) ? 1 : conv;
-    if (rep->delta)
-      for (int i = 0; i < K; ++i) rep->delta[i] = c->h_delta[i];
-    float ms = 0;
-    cudaEventElapsedTime(&ms, e0, e1);
-    rep->ms_total = ms;
-    double ph[4] = {0, 0, 0, 0};
-    for (auto &s : pt.spans) {
-      float m = 0;
-      cudaEventElapsedTime(&m, s.second.first, s.second.second);
-      ph[s.first] += m;
-    }
-    rep->ms_coarse = ph[PH_COARSE];
-    rep->ms_fine = ph[PH_FINE];
-    rep->ms_comm = ph[PH_COMM];
-    rep->ms_setup = ph[PH_SETUP];
-    rep->kernel_launches = c->launches - launches0;
-  }
   return PR_OK;
+  }();
+  if (use_graph) {
+    cudaGraph_t g = nullptr;
+    c->capturing = false;
+    const cudaError_t ce = cudaStreamEndCapture(c->stream, &g);
+    if (st) {
+      if (g) cudaGraphDestroy(g);
+      return st;
+    }
+    if (ce != cudaSuccess) return fail(c, PR_ERR_CUDA, fmt("graph capture: %s", cudaGetErrorString(ce)));
+    const cudaError_t ie = cudaGraphInstantiate(&c->g_exec, g, 0);
+    cudaGraphDestroy(g);
+    if (ie != cudaSuccess) return fail(c, PR_ERR_CUDA, fmt("graph instantiate: %s", cudaGetErrorString(ie)));
+    // the graph owns the events it records: move them out of the reusable pool
+    c->g_events.assign(c->ev.begin(), c->ev.begin() + c->ev_used);
+    c->ev.erase(c->ev.begin(), c->ev.begin() + c->ev_used);
+    c->ev_used = 0;
+    c->g_vt = V_T;
+    c->g_v0 = V_0;
+    c->g_K = K;
+    c->g_e0 = e0;
+    c->g_e1 = e1;
+    c->g_spans = pt.spans;
+    c->g_launches = c->launches - launches0;
+    CU(cudaGraphLaunch(c->g_exec, c->stream));
+  } else if (st) {
+    return st;
+  }
+  CU(cudaStreamSynchronize(c->stream));
+  return solve_report(c, K, conv, e0, e1, pt.spans, c->launches - launches0, rep);
 }
 
 pr_status serial_fine_impl(pr_ctx *c, const float *V_T, float *V_0, bool device_ptr, double *ms) {
@@ -1036,6 +1112,7 @@ pr_status parareal_load_pinn_weights(pr_ctx *c, int32_t n_linear, const int32_t 
                                      float out_scale, int32_t precision) {
   pr_status st = check_ctx(c);
   if (st) return st;
+  drop_graph(c);  // the parameter-space PINN kernels capture the weights by value
   if (n_linear < 2) return fail(c, PR_ERR_INVALID_ARGUMENT, fmt("n_linear=%d must be >= 2 (at least one hidden layer)", n_linear));
   if (!dims || !W || !b) return fail(c, PR_ERR_INVALID_ARGUMENT, "dims/W/b must be non-NULL");
   if (dims[0] != 2 && dims[0] != 4) return fail(c, PR_ERR_INVALID_ARGUMENT, fmt("dims[0]=%d must be 2 or 4", dims[0]));
@@ -1235,6 +1312,7 @@ pr_status parareal_plan_iteration(int32_t N, int32_t world, int32_t rank, int32_
 pr_status parareal_set_option(pr_ctx *c, int32_t key, int64_t value) {
   pr_status st = check_ctx(c);
   if (st) return st;
+  drop_graph(c);  // a captured solve bakes in kernel choices
   switch (key) {
     case PR_OPT_FINE_KERNEL:
       if (value < 0 || value > 2) return fail(c, PR_ERR_INVALID_ARGUMENT, "PR_OPT_FINE_KERNEL must be 0, 1 or 2");
@@ -1259,6 +1337,7 @@ pr_status parareal_set_option(pr_ctx *c, int32_t key, int64_t value) {
 void parareal_free(pr_ctx *c) {
   if (!c) return;
   if (c->stream) cudaStreamSynchronize(c->stream);
+  drop_graph(c);
   if (c->comm) {
     Nccl &n = nccl();
     if (n.ok) (c->poisoned ? n.CommAbort(c->comm) : n.CommDestroy(c->comm));

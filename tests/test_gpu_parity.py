@@ -278,6 +278,33 @@ def test_device_entry_points():
     assert np.array_equal(v0, oracle.payoff(p).astype(np.float32))
 
 
+def test_graph_replay_matches_eager():
+    """PR_OPT_USE_GRAPHS: captured + replayed solves give the eager results bitwise, replays
+    are repeatable, and new weights are picked up (the graph is re-captured)."""
+    import torch
+    p = synth.config("C2", coarse=synth.COARSE_PINN, max_iter=3, tol=0.0)
+    net0, net1 = synth.kaiming_net(synth.PINN_3x20, seed=0), synth.kaiming_net(synth.PINN_3x20, seed=3)
+    out = None
+    with ctx_for(p, net0) as c:
+        out = torch.empty((1, p.M), dtype=torch.float32, device="cuda")
+        c.solve_device(out)
+        eager = out.cpu().numpy()
+        c.set_option(parareal.OPT_USE_GRAPHS, 1)
+        reps = []
+        for _ in range(3):
+            out.zero_()
+            reps.append(c.solve_device(out))
+            assert np.array_equal(out.cpu().numpy(), eager)
+        assert all(r["iterations"] == 3 and r["ms_total"] > 0 for r in reps)
+        c.load_weights(net1)
+        out.zero_()
+        c.solve_device(out)
+        g1 = out.cpu().numpy()
+        c.set_option(parareal.OPT_USE_GRAPHS, 0)
+        c.solve_device(out)
+        assert np.array_equal(out.cpu().numpy(), g1) and not np.array_equal(g1, eager)
+
+
 def test_errors_on_gpu():
     p = synth.config("C1", coarse=synth.COARSE_PINN)
     with parareal.Context(p) as c:
