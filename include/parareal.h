@@ -81,7 +81,7 @@ typedef struct {
   int32_t upper_bc;             /* PR_BC_*                                                   */
   int32_t N;                    /* time slices ≥ 1; N % world == 0                   */
   int32_t fine_steps;           /* implicit steps per slice of F ≥ 1 (Q2)                    */
-  double fine_theta;            /* 1.0 = implicit Euler (only value supported in ABI v1)     */
+  double fine_theta;            /* θ of the fine θ-step, in [0.5, 1]: 1 implicit Euler (Q1), 0.5 Crank–Nicolson (NEXT-1) */
   int32_t coarse;               /* PR_COARSE_*                                               */
   int32_t coarse_steps;         /* implicit Euler steps per slice for numerical G ≥ 1        */
   int32_t max_iter;             /* 1 ≤ max_iter ≤ N                                          */
@@ -115,7 +115,7 @@ const char *parareal_last_error(const pr_ctx *ctx);
 pr_status parareal_get_nccl_id(uint8_t out[128]);
 
 /* Validates *prob (PR_ERR_INVALID_ARGUMENT naming the field: σ>0, T>0, r≥0, L>K≥0, M≥1,
- * N≥1, steps≥1, 1≤max_iter≤N, tol≥0, N % world == 0, fine_theta == 1), selects the device,
+ * N≥1, steps≥1, 1≤max_iter≤N, tol≥0, N % world == 0, 0.5 ≤ fine_theta ≤ 1), selects the device,
  * factorises M_f = I − dτ_f A (and M_c for numerical G) in fp64 on the host
  * (PR_ERR_NUMERICAL on a non-positive pivot), uploads factors and, for world > 1, creates
  * the NCCL communicator (collective).  Rank r owns slices [rN/world, (r+1)N/world). */

@@ -6,8 +6,10 @@
 // live in registers for all implicit steps of the slice; HBM is touched once
 // per slice (load U_n, store F̂_n or D_n = F̂_n − Ĝ_n).
 //
-// Per implicit step (implicit Euler; reading Q1) the constant-matrix
-// Thomas solve M_f x⁺ = x + dτ(a_M+b_M) g(τ⁺) e_M splits into two first-order
+// Per θ-step (implicit Euler θ=1 by reading Q1, Crank–Nicolson θ=1/2 = NEXT-1) the
+// constant-matrix solve (I − θdτA) x⁺ = (I + (1−θ)dτA) x + dτ(a_M+b_M)[θg(τ⁺) + (1−θ)g(τ)] e_M
+// first forms the explicit right-hand side (θ < 1: a 3-point stencil, neighbours across threads
+// by shuffle and across warps through shared memory) and then splits into two first-order
 // linear recurrences (forward elimination y_j = r_j − m_j y_{j−1}, back
 // substitution x_j = y_j/p_j − (u_j/p_j) x_{j+1}).  Each is evaluated as a
 // chunked scan of affine maps v ↦ A + B·v: a sequential pass over the
@@ -30,6 +32,8 @@ struct ResidentArgs {
   const double *fm, *fip, *fcu;
   const int *fset;          // [B] factor-set index per instance
   const double *bcoef;      // [B] dτ (a_M + b_M) of this scheme (boundary term of row M)
+  double theta;             // θ of the θ-step (1: implicit Euler; 1/2: Crank–Nicolson)
+  const double *ecoef;      // θ < 1: [nsets][3] (1−θ)dτσ²/2, (1−θ)dτr/2, (1−θ)dτr (explicit part)
   const double *Lb, *Kb, *rb;
   int upper_bc;             // 0 asymptotic call value, 1 zero
   double dT, dtau;          // slice length, implicit step
@@ -65,18 +69,28 @@ __device__ __forceinline__ double g_upper(const ResidentArgs &a, int b, double t
   return a.upper_bc ? 0.0 : a.Lb[b] - a.Kb[b] * exp(-a.rb[b] * tau);
 }
 
-template <int P, int NT>
+template <int P, int NT, bool CN = false>
 struct Tri {
   static constexpr int NW = NT / 32;
+  static constexpr int kShm = 6 * NW + 2;  // doubles of shared scratch per system
   double nm[P], ip[P], ncu[P], qf[P], qb[P];
   double cfL[5], cbL[5];
   double cf_exc, cb_exc;
-  int lane, w;
+  double e0, e1, er, J0;  // CN: explicit-part coefficients, J of the thread's first point
+  int lane, w, M, j0;
 
-  // shared layout per system: ctf[NW], ctb[NW], sy[2][NW]
+  // shared layout per system: ctf[NW], ctb[NW], sy[2][NW], (CN) edge values [2][NW]
   __device__ void setup(const ResidentArgs &a, int set, int t, double *sh) {
     lane = t & 31;
     w = t >> 5;
+    M = a.M;
+    j0 = t * P;
+    J0 = (double)(j0 + 1);
+    if (CN) {
+      e0 = a.ecoef[3 * set];
+      e1 = a.ecoef[3 * set + 1];
+      er = a.ecoef[3 * set + 2];
+    }
     const double *fm = a.fm + (size_t)set * a.Mp;
     const double *fip = a.fip + (size_t)set * a.Mp;
     const double *fcu = a.fcu + (size_t)set * a.Mp;
@@ -123,7 +137,39 @@ struct Tri {
 
   // One implicit step in place on x[P] (fp64).  bc_i: point index inside this thread that
   // receives the boundary term (−1 if none); bcg = dτ(a_M+b_M) g(τ⁺).
+  // Explicit part (CN): x ← (I + (1−θ)dτA) x, with V_0 = 0 below row 1; the upper boundary value
+  // is in the tabulated boundary term.  (a_j−b_j, −(2a_j+r), a_j+b_j)(1−θ)dτ = (q−p, −(2q+er), q+p)
+  // with q = e0 J², p = e1 J.  Rows beyond M (padding) stay 0.
+  __device__ __forceinline__ void explicit_part(double (&x)[P], double *sh) {
+    double xl = __shfl_up_sync(kFull, x[P - 1], 1), xr = __shfl_down_sync(kFull, x[0], 1);
+    if (NW > 1) {
+      double *xb = sh + 4 * NW + 2;
+      if (lane == 31) xb[w] = x[P - 1];
+      if (lane == 0) xb[NW + w] = x[0];
+      __syncthreads();
+      if (lane == 0) xl = (w > 0) ? xb[w - 1] : 0.0;
+      if (lane == 31) xr = (w < NW - 1) ? xb[NW + w + 1] : 0.0;
+    } else {
+      if (lane == 0) xl = 0.0;
+      if (lane == 31) xr = 0.0;
+    }
+    double prev = xl, cur = x[0];
+    const bool pad = j0 + P > M;
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      const double nxt = (i < P - 1) ? x[i + 1] : xr;
+      const double J = J0 + i;
+      const double q = e0 * J * J, pp = e1 * J;
+      double r = fma(q, (prev - 2.0 * cur) + nxt, fma(pp, nxt - prev, fma(-er, cur, cur)));
+      if (pad && j0 + i >= M) r = 0.0;
+      x[i] = r;
+      prev = cur;
+      cur = nxt;
+    }
+  }
+
   __device__ __forceinline__ void step(double (&x)[P], int bc_i, double bcg, double *sh) {
+    if (CN) explicit_part(x, sh);
 #pragma unroll
     for (int i = 0; i < P; ++i)
       if (i == bc_i) x[i] += bcg;
@@ -193,8 +239,8 @@ constexpr int kBcChunk = 128;  // boundary terms tabulated per chunk of implicit
 // All implicit steps of slice n.  The boundary term dτ(a_M+b_M)·g(τ_{m+1}) of each step needs an
 // fp64 exp; it is tabulated in shared memory for kBcChunk steps at a time (one exp per thread)
 // so no exp sits on the per-step critical path.
-template <int P, int NT>
-__device__ __forceinline__ void run_steps(Tri<P, NT> &tri, const ResidentArgs &a, int b, int n,
+template <int P, int NT, bool CN>
+__device__ __forceinline__ void run_steps(Tri<P, NT, CN> &tri, const ResidentArgs &a, int b, int n,
                                           int t, double (&x)[P], double *sh, double *bct) {
   const int bc_t = (a.M - 1) / P, bc_ip = (a.M - 1) % P;
   const int bc_i = (t == bc_t) ? bc_ip : -1;
@@ -205,7 +251,11 @@ __device__ __forceinline__ void run_steps(Tri<P, NT> &tri, const ResidentArgs &a
     __syncthreads();  // readers of the previous chunk are done
     for (int i = t; i < kBcChunk; i += NT) {
       const int m = m0 + i;
-      if (m < a.steps) bct[i] = coef * g_upper(a, b, (tau0 + m * a.dtau) + a.dtau);
+      if (m < a.steps) {
+        const double gp = g_upper(a, b, (tau0 + m * a.dtau) + a.dtau);
+        // dτ(a_M+b_M)[θ g(τ_{m+1}) + (1−θ) g(τ_m)]
+        bct[i] = CN ? coef * (a.theta * gp + (1.0 - a.theta) * g_upper(a, b, tau0 + m * a.dtau)) : coef * gp;
+      }
     }
     __syncthreads();
     const int mend = min(a.steps - m0, kBcChunk);
@@ -215,10 +265,10 @@ __device__ __forceinline__ void run_steps(Tri<P, NT> &tri, const ResidentArgs &a
 }
 
 // SWEEP: every (slice, instance) system independently; blockIdx.x = system group.
-template <int P, int NT, int SPB>
+template <int P, int NT, int SPB, bool CN>
 __global__ void __launch_bounds__(NT * SPB) k_fine_sweep(ResidentArgs a) {
   constexpr int NW = NT / 32;
-  __shared__ double shm[SPB][4 * NW + 2];
+  __shared__ double shm[SPB][Tri<P, NT, CN>::kShm];
   __shared__ double bctab[SPB][kBcChunk];
   const int sys = blockIdx.x * SPB + threadIdx.x / NT;
   const int t = threadIdx.x % NT;
@@ -227,7 +277,7 @@ __global__ void __launch_bounds__(NT * SPB) k_fine_sweep(ResidentArgs a) {
   const int s = live ? sys : nsys - 1;  // dead systems shadow a live one (barriers stay uniform)
   const int ln = a.ln0 + s / a.B, b = s % a.B;
   double *sh = shm[threadIdx.x / NT];
-  Tri<P, NT> tri;
+  Tri<P, NT, CN> tri;
   tri.setup(a, a.fset[b], t, sh);
   if (NW > 1) __syncthreads();
   const float *u = a.U + ((size_t)ln * a.B + b) * a.Mp;
@@ -237,7 +287,7 @@ __global__ void __launch_bounds__(NT * SPB) k_fine_sweep(ResidentArgs a) {
     const int j = t * P + i;
     x[i] = (j < a.M) ? (double)u[j] : 0.0;
   }
-  run_steps<P, NT>(tri, a, b, a.n_base + ln, t, x, sh, bctab[threadIdx.x / NT]);
+  run_steps<P, NT, CN>(tri, a, b, a.n_base + ln, t, x, sh, bctab[threadIdx.x / NT]);
   if (!live) return;
   const size_t row = ((size_t)ln * a.B + b) * a.Mp;
   if (a.Fout) {
@@ -267,10 +317,10 @@ __global__ void __launch_bounds__(NT * SPB) k_fine_sweep(ResidentArgs a) {
 
 // CHAIN: one system per instance walks slices c_ln0..c_ln1-1 serially (numerical coarse
 // G with the Parareal correction; or the serial fine solve, Eq. 6).
-template <int P, int NT, int SPB>
+template <int P, int NT, int SPB, bool CN>
 __global__ void __launch_bounds__(NT * SPB) k_resident_chain(ResidentArgs a) {
   constexpr int NW = NT / 32;
-  __shared__ double shm[SPB][4 * NW + 2];
+  __shared__ double shm[SPB][Tri<P, NT, CN>::kShm];
   __shared__ double red[SPB][2 * NW + 2];
   __shared__ double bctab[SPB][kBcChunk];
   const int sys = blockIdx.x * SPB + threadIdx.x / NT;
@@ -279,7 +329,7 @@ __global__ void __launch_bounds__(NT * SPB) k_resident_chain(ResidentArgs a) {
   const int b = live ? sys : a.B - 1;
   double *sh = shm[threadIdx.x / NT];
   double *rd = red[threadIdx.x / NT];
-  Tri<P, NT> tri;
+  Tri<P, NT, CN> tri;
   tri.setup(a, a.fset[b], t, sh);
   if (NW > 1) __syncthreads();
   const size_t sstride = (size_t)a.B * a.Mp;
@@ -323,7 +373,7 @@ __global__ void __launch_bounds__(NT * SPB) k_resident_chain(ResidentArgs a) {
   }
 #pragma unroll 1
   for (int ln = a.c_ln0; ln < a.c_ln1; ++ln) {
-    run_steps<P, NT>(tri, a, b, a.n_base + ln, t, x, sh, bctab[threadIdx.x / NT]);
+    run_steps<P, NT, CN>(tri, a, b, a.n_base + ln, t, x, sh, bctab[threadIdx.x / NT]);
     const size_t row = (size_t)ln * sstride + (size_t)b * a.Mp;
     float *un = a.Uw + (size_t)(ln + 1) * a.ustride + (size_t)b * a.Mp;
     double num = 0.0, den = 0.0;

@@ -75,6 +75,10 @@ struct StreamedFactors {
                                  //   preceding t in its tile, in the pass direction (dir 0: Π(−m̃), 1: Π(−c))
   const double *tileB;           // [2][nsets][ntiles] tile multiplier, indexed by scan position
   const int *tileW;              // [2][nsets][ntiles] look-back window (predecessors)
+  // θ < 1 (Crank–Nicolson, NEXT-1): explicit part and the tile-edge corrections of forward passes
+  const double *ecoef;           // [nsets][3] (1−θ)dτσ²/2, (1−θ)dτr/2, (1−θ)dτr
+  const double *PL;              // [nsets][Mt/kSPS] Π(−m̃_k), k = tile start+1 … thread start−1
+  const double *tileL;           // [nsets][ntiles] Π(−m̃_k), k = tile start+1 … tile end
 };
 
 struct StreamedState {
@@ -126,6 +130,7 @@ struct PassArgs {
   const double *bcoef, *Lb, *Kb, *rb;
   int upper_bc;
   double dT, dtau;           // τ_{m+1} = (n·dT + m·dτ) + dτ  (same association as the oracle)
+  double theta;              // θ-step (1: implicit Euler)
   int step_m;
   int n_base, ln0;           // system s ↔ local slice ln0 + s / B, instance s % B
   // epilogue (backward pass of the last step of a slice)
@@ -161,7 +166,7 @@ struct StreamedProblem {   // what every pass of one scheme shares
   const int *fset;
   const double *bcoef, *L, *K, *r;
   int upper_bc;
-  double dT, dtau;
+  double dT, dtau, theta;
   int steps, M, Mp, B;
 };
 
@@ -184,11 +189,36 @@ __device__ __forceinline__ double shfl_prev(double v, int d) {
   return DIR == 0 ? __shfl_up_sync(0xffffffffu, v, d) : __shfl_down_sync(0xffffffffu, v, d);
 }
 
-// dτ(a_M+b_M)·g(τ_{m+1}) of step m of slice n, g the upper boundary value (reading Q3)
+// dτ(a_M+b_M)·[θ g(τ_{m+1}) + (1−θ) g(τ_m)] of step m of slice n, g the upper boundary value
+// (reading Q3); θ = 1: dτ(a_M+b_M)·g(τ_{m+1}).
+__device__ __forceinline__ double g_up(const PassArgs &a, int b, double tau) {
+  return a.upper_bc ? 0.0 : a.Lb[b] - a.Kb[b] * exp(-a.rb[b] * tau);
+}
 __device__ __forceinline__ double bc_term(const PassArgs &a, int b, int n, int m) {
-  const double tau = (n * a.dT + m * a.dtau) + a.dtau;
-  const double g = a.upper_bc ? 0.0 : a.Lb[b] - a.Kb[b] * exp(-a.rb[b] * tau);
-  return a.bcoef[b] * g;
+  const double tau0 = n * a.dT + m * a.dtau;
+  const double g1 = g_up(a, b, tau0 + a.dtau);
+  if (a.theta == 1.0) return a.bcoef[b] * g1;
+  return a.bcoef[b] * (a.theta * g1 + (1.0 - a.theta) * g_up(a, b, tau0));
+}
+
+// Explicit part of a θ-step (θ < 1) at 0-based point j (J = j+1): x_j + (1−θ)dτ(A x)_j with
+// (1−θ)dτ(a_j−b_j, −(2a_j+r), a_j+b_j) = (q−p, −(2q+er), q+p), q = e0 J², p = e1 J.
+struct Expl {
+  double e0, e1, er;
+  __device__ __forceinline__ double rhs(double J, double xm, double x0, double xp) const {
+    const double q = e0 * J * J, pp = e1 * J;
+    return fma(q, (xm - 2.0 * x0) + xp, fma(pp, xp - xm, fma(-er, x0, x0)));
+  }
+  __device__ __forceinline__ double lower(double J) const { return J * fma(e0, J, -e1); }  // q − p
+  __device__ __forceinline__ double upper(double J) const { return J * fma(e0, J, e1); }   // q + p
+};
+__device__ __forceinline__ Expl load_expl(const PassArgs &a, int set) {
+  return Expl{__ldg(a.f.ecoef + 3 * set), __ldg(a.f.ecoef + 3 * set + 1), __ldg(a.f.ecoef + 3 * set + 2)};
+}
+// The pass input at 0-based point j of system s (interleaved or natural rows).
+template <bool IN_IL>
+__device__ __forceinline__ float in_at(const PassArgs &a, int s, int j) {
+  return IN_IL ? a.in[(size_t)s * a.Mt + il_index((size_t)j)] : a.in[(size_t)s * a.Mp + j];
 }
 
 // m̃_j = l_j/p_j and c_j = u_j/p_j at 0-based point j (J = j+1) from 1/p.  EDGE: apply the
@@ -260,7 +290,7 @@ __device__ __forceinline__ void compose_window(double &mA, double &mB, int lane)
 
 // The value entering the tile at scan position `pos` of system s, composing the window from
 // predecessor distance base0+1 on onto (accA, accB).  Warp-level; result in lane 0.
-template <int DIR>
+template <int DIR, bool CN = false, bool IN_IL = true>
 __device__ __forceinline__ double look_back(const PassArgs &a, int s, int pos, int set, int lane, int base0,
                                             double accA, double accB) {
   const size_t tb = ((size_t)DIR * a.nsets + set) * a.ntiles;
@@ -273,6 +303,17 @@ __device__ __forceinline__ double look_back(const PassArgs &a, int s, int pos, i
       const int p = pos - 1 - k;
       mA = agg[DIR == 0 ? p : a.ntiles - 1 - p];
       mB = __ldg(a.f.tileB + tb + p);
+      if (CN && DIR == 0) {
+        // the producer built tile p's total without the stencil terms that reach across its
+        // edges (x_{j0−1}, x_{j1+1}: other tiles' outputs); add them from this pass's input
+        const Expl ex = load_expl(a, set);
+        const double *ip = a.f.ip + (size_t)set * a.Mt;
+        const int j0 = p * kSTile, j1 = j0 + kSTile - 1;  // a predecessor tile is full (j1+1 < M)
+        double dl = 0.0;
+        if (j0 > 0) dl = __ldg(ip + il_index(j0)) * ex.lower((double)(j0 + 1)) * (double)in_at<IN_IL>(a, s, j0 - 1);
+        const double dr = __ldg(ip + il_index(j1)) * ex.upper((double)(j1 + 1)) * (double)in_at<IN_IL>(a, s, j1 + 1);
+        mA = fma(dl, __ldg(a.f.tileL + (size_t)set * a.ntiles + p), mA) + dr;
+      }
     }
     compose_window(mA, mB, lane);
     accA = fma(accB, mA, accA);
@@ -284,6 +325,9 @@ __device__ __forceinline__ double look_back(const PassArgs &a, int s, int pos, i
 // ---------------------------------------------------------------- k_agg0
 // Aggregates of the first (forward) pass of a slice, from its natural-layout input rows:
 // A_t = Σ_i r_i/p_i Π_{k>i}(−m̃_k) (w-form forward map of the thread), scanned over the tile.
+// θ < 1: r = the explicit part of step 0; its stencil terms across the tile's edges are left out
+// (the consumer adds them, see look_back), exactly as a backward pass producing these aggregates.
+template <bool CN>
 __global__ void __launch_bounds__(kSNT) k_agg0(PassArgs a) {
   __shared__ double tot[kNW][2];
   const int s = blockIdx.x % a.nsys, tile = blockIdx.x / a.nsys;
@@ -300,13 +344,26 @@ __global__ void __launch_bounds__(kSNT) k_agg0(PassArgs a) {
   const bool has_bc = j0 <= a.M - 1 && a.M - 1 < j0 + kSPS;
   const double bcv = has_bc ? bc_term(a, b, a.n_base + ln, 0) : 0.0;
   const double J0 = (double)(j0 + 1);
+  double xr = 0.0, xl = 0.0;  // neighbours across the thread's chunk (0 across the tile's edges)
+  Expl ex{0.0, 0.0, 0.0};
+  if (CN) {
+    ex = load_expl(a, set);
+    const float *row = a.in + (size_t)s * a.Mp;
+    if (t > 0 && j0 > 0) xl = row[j0 - 1];
+    if (t < kSNT - 1 && j0 + kSPS < a.M) xr = row[j0 + kSPS];
+  }
   double A[1] = {0.0}, P = 1.0;
 #pragma unroll
   for (int i = kSPS - 1; i >= 0; --i) {
     const int j = j0 + i;
     double mt, cj;
     factors<true>(c0, c1, J0 + i, ipv[i], j, a.M, mt, cj);
-    const double r = (j == a.M - 1) ? (double)x[i] + bcv : (double)x[i];
+    double r = (double)x[i];
+    if (CN) {
+      r = ex.rhs(J0 + i, i > 0 ? (double)x[i - 1] : xl, (double)x[i], i < kSPS - 1 ? (double)x[i + 1] : xr);
+      if (j >= a.M) r = 0.0;
+    }
+    if (j == a.M - 1) r += bcv;
     A[0] = fma(r * ipv[i], P, A[0]);
     P *= -mt;
   }
@@ -329,11 +386,18 @@ __global__ void __launch_bounds__(kSNT) k_agg0(PassArgs a) {
 // One CTA per tile of SP systems (the same tile of SP consecutive slices of one instance), data
 // in registers.  Used for the first pass of a slice (natural input), the last pass (epilogues)
 // and chain mode.  NEXT: also publish the next pass's aggregates.
-template <int DIR, bool IN_IL, bool OUT_IL, bool NEXT, int SP>
+// CN (θ < 1): a forward pass first forms the explicit part r = (I + (1−θ)dτA)x of its input
+// (neighbours across threads by shuffle / shared memory, across the tile's edges from memory),
+// and adds the stencil terms its producer could not see (tile-edge neighbours) to the entering
+// values; a backward pass with NEXT builds the next forward map from r of its rounded outputs,
+// leaving out the terms across the tile's edges.
+template <int DIR, bool IN_IL, bool OUT_IL, bool NEXT, int SP, bool CN>
 __global__ void __launch_bounds__(kSNT) k_streamed_pass(PassArgs a) {
   constexpr int ND = 1 - DIR;  // direction of the next pass
   static_assert(SP <= kNW, "one look-back warp per system");
   __shared__ double s_yin[SP];
+  __shared__ float s_edge[2][kNW][SP];
+  __shared__ double s_dl[SP];
   __shared__ double tot[kNW][SP + 1];
   __shared__ double red[2 * kNW];
   const int g = (int)(blockIdx.x % a.ngroups);
@@ -378,21 +442,55 @@ __global__ void __launch_bounds__(kSNT) k_streamed_pass(PassArgs a) {
     for (int i = 0; i < kSPS; ++i) ipv[i] = __ldg(ip + i * kSNT);
   }
   const double c0 = __ldg(a.f.coef + 2 * set), c1 = __ldg(a.f.coef + 2 * set + 1);
+  const double J0 = (double)(j0 + 1);
+  // ---- CN forward pass: neighbours of the thread's chunk in the input
+  Expl ex{0.0, 0.0, 0.0};
+  float xl[SP], xr[SP];
+  double PLt = 0.0;
+  if (CN) ex = load_expl(a, set);
+  if (CN && DIR == 0) {
+    PLt = __ldg(a.f.PL + (size_t)set * nthr + thr);
+#pragma unroll
+    for (int q = 0; q < SP; ++q) {
+      xl[q] = __shfl_up_sync(0xffffffffu, x[q][kSPS - 1], 1);
+      xr[q] = __shfl_down_sync(0xffffffffu, x[q][0], 1);
+      if (lane == 31) s_edge[0][w][q] = x[q][kSPS - 1];
+      if (lane == 0) s_edge[1][w][q] = x[q][0];
+      if (t == 0) {
+        xl[q] = j0 > 0 ? in_at<IN_IL>(a, sys[q], j0 - 1) : 0.0f;
+        s_dl[q] = j0 > 0 ? ipv[0] * ex.lower(J0) * (double)xl[q] : 0.0;
+      }
+      if (t == kSNT - 1) xr[q] = j0 + kSPS < a.M ? in_at<IN_IL>(a, sys[q], j0 + kSPS) : 0.0f;
+    }
+  }
   // ---- the value entering the tile (one warp per system)
   if (w >= kNW - SP) {
     const int q = kNW - 1 - w;
-    const double y = pos > 0 ? look_back<DIR>(a, sys[q], pos, set, lane, 0, 0.0, 1.0) : 0.0;
+    const double y = pos > 0 ? look_back<DIR, CN, IN_IL>(a, sys[q], pos, set, lane, 0, 0.0, 1.0) : 0.0;
     if (lane == 0) s_yin[q] = y;
   }
   __syncthreads();
+  if (CN && DIR == 0) {
+#pragma unroll
+    for (int q = 0; q < SP; ++q) {
+      if (lane == 0 && w > 0) xl[q] = s_edge[0][w - 1][q];
+      if (lane == 31 && w < kNW - 1) xr[q] = s_edge[1][w + 1][q];
+    }
+  }
   double v[SP];
 #pragma unroll
-  for (int q = 0; q < SP; ++q) v[q] = fma(P, s_yin[q], E[q]);
+  for (int q = 0; q < SP; ++q) {
+    v[q] = fma(P, s_yin[q], E[q]);
+    // the tile's left-edge stencil term, missing from its producer's prefixes
+    if (CN && DIR == 0 && t > 0) v[q] = fma(s_dl[q], PLt, v[q]);
+  }
   // ---- the recurrence, once, from the exact entering value; next pass's map on the fly
   double An[SP], Pn = 1.0;
 #pragma unroll
   for (int q = 0; q < SP; ++q) An[q] = 0.0;
-  const double J0 = (double)(j0 + 1);
+  double pv[SP];  // CN: the previous point's input value
+#pragma unroll
+  for (int q = 0; q < SP; ++q) pv[q] = CN && DIR == 0 ? (double)xl[q] : 0.0;
   auto run = [&](auto edge_tag) {
     constexpr bool EDGE = decltype(edge_tag)::value;
     double bcv[SP];
@@ -411,27 +509,70 @@ __global__ void __launch_bounds__(kSNT) k_streamed_pass(PassArgs a) {
 #pragma unroll
       for (int q = 0; q < SP; ++q) {
         if (DIR == 0) {
-          const double r = (EDGE && j == a.M - 1) ? (double)x[q][i] + bcv[q] : (double)x[q][i];
+          double r = (double)x[q][i];
+          if (CN) {
+            const double cur = r;
+            r = ex.rhs(J0 + i, pv[q], cur, i < kSPS - 1 ? (double)x[q][i + 1] : (double)xr[q]);
+            if (EDGE && j >= a.M) r = 0.0;
+            pv[q] = cur;
+          }
+          if (EDGE && j == a.M - 1) r += bcv[q];
           v[q] = fma(-mt, v[q], r * ipv[i]);
           // backward map of the thread: x_{j0} = Σ_i w_i Π_{k<i}(−c_k) + Pn·x_{j0+kSPS}
           if (NEXT) An[q] = fma(v[q], Pn, An[q]);
         } else {
           v[q] = fma(-cj, v[q], (double)x[q][i]);
           // forward map of step m+1: w_last = Σ_i r_i/p_i Π_{k>i}(−m̃_k) + Pn·w_{j0−1}
-          if (NEXT) {
+          if (NEXT && !CN) {
             const double r = (EDGE && j == a.M - 1) ? v[q] + bcv[q] : v[q];
             An[q] = fma(r * ipv[i], Pn, An[q]);
           }
         }
         x[q][i] = (float)v[q];
       }
-      if (NEXT) Pn *= DIR == 0 ? -cj : -mt;
+      if (NEXT && !(CN && DIR == 1)) Pn *= DIR == 0 ? -cj : -mt;
     }
   };
   // Aggregates use the unrounded outputs: the next pass then sees the recurrence applied to
   // inputs within fp32 rounding of the stored ones — the same perturbation storage makes.
   if (j0 == 0 || j0 + kSPS > a.M - 1) run(std::true_type{});
   else run(std::false_type{});
+  if (CN && DIR == 1 && NEXT) {
+    // next forward map from r = (I + (1−θ)dτA)x of the rounded outputs (tile-edge terms left out)
+    float ol[SP], orr[SP];
+#pragma unroll
+    for (int q = 0; q < SP; ++q) {
+      ol[q] = __shfl_up_sync(0xffffffffu, x[q][kSPS - 1], 1);
+      orr[q] = __shfl_down_sync(0xffffffffu, x[q][0], 1);
+      if (lane == 31) s_edge[0][w][q] = x[q][kSPS - 1];
+      if (lane == 0) s_edge[1][w][q] = x[q][0];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < SP; ++q) {
+      if (lane == 0) ol[q] = w > 0 ? s_edge[0][w - 1][q] : 0.0f;
+      if (lane == 31) orr[q] = w < kNW - 1 ? s_edge[1][w + 1][q] : 0.0f;
+    }
+    const bool has_bc = j0 <= a.M - 1 && a.M - 1 < j0 + kSPS;
+    double bcn[SP];
+#pragma unroll
+    for (int q = 0; q < SP; ++q) bcn[q] = has_bc ? bc_term(a, b, a.n_base + a.ln0 + ls0 + q, a.step_m + 1) : 0.0;
+#pragma unroll
+    for (int i = kSPS - 1; i >= 0; --i) {
+      const int j = j0 + i;
+      double mt, cj;
+      factors<true>(c0, c1, J0 + i, ipv[i], j, a.M, mt, cj);
+#pragma unroll
+      for (int q = 0; q < SP; ++q) {
+        double r = ex.rhs(J0 + i, i > 0 ? (double)x[q][i - 1] : (double)ol[q], (double)x[q][i],
+                          i < kSPS - 1 ? (double)x[q][i + 1] : (double)orr[q]);
+        if (j >= a.M) r = 0.0;
+        if (j == a.M - 1) r += bcn[q];
+        An[q] = fma(r * ipv[i], Pn, An[q]);
+      }
+      Pn *= -mt;
+    }
+  }
   // ---- stores / epilogues
   if (OUT_IL) {
 #pragma unroll
@@ -918,18 +1059,23 @@ static cudaError_t launch_res(int dir, const PassArgs &a, cudaStream_t s) {
   return h == 2 ? launch_res_h<1, 2>(dir, a, c.nst, s) : launch_res_h<1, 1>(dir, a, c.nst, s);
 }
 
-template <int SP>
-static void launch_tile(int dir, bool in_il, bool next, const PassArgs &a, cudaStream_t s) {
+template <int SP, bool CN>
+static void launch_tile_cn(int dir, bool in_il, bool next, const PassArgs &a, cudaStream_t s) {
   const unsigned grid = (unsigned)((unsigned long long)a.ngroups * a.ntiles);
   if (dir == 0) {
-    if (in_il) k_streamed_pass<0, true, true, true, SP><<<grid, kSNT, 0, s>>>(a);
-    else k_streamed_pass<0, false, true, true, SP><<<grid, kSNT, 0, s>>>(a);
+    if (in_il) k_streamed_pass<0, true, true, true, SP, CN><<<grid, kSNT, 0, s>>>(a);
+    else k_streamed_pass<0, false, true, true, SP, CN><<<grid, kSNT, 0, s>>>(a);
   } else if (a.epi == EPI_X) {
-    if (next) k_streamed_pass<1, true, true, true, SP><<<grid, kSNT, 0, s>>>(a);
-    else k_streamed_pass<1, true, true, false, SP><<<grid, kSNT, 0, s>>>(a);
+    if (next) k_streamed_pass<1, true, true, true, SP, CN><<<grid, kSNT, 0, s>>>(a);
+    else k_streamed_pass<1, true, true, false, SP, CN><<<grid, kSNT, 0, s>>>(a);
   } else {
-    k_streamed_pass<1, true, false, false, SP><<<grid, kSNT, 0, s>>>(a);
+    k_streamed_pass<1, true, false, false, SP, CN><<<grid, kSNT, 0, s>>>(a);
   }
+}
+template <int SP>
+static void launch_tile(int dir, bool in_il, bool next, const PassArgs &a, cudaStream_t s) {
+  if (a.theta != 1.0) launch_tile_cn<SP, true>(dir, in_il, next, a, s);
+  else launch_tile_cn<SP, false>(dir, in_il, next, a, s);
 }
 
 // Forward passes read aggregates [0] and write [1]; backward passes read [1] and write [0].
@@ -941,7 +1087,8 @@ static cudaError_t launch_pass(StreamedState &st, int dir, bool in_il, bool next
   a.aggL_next = st.aggL[1 - dir];
   // The persistent kernel pays off when several items share each tile's factors (C3: 16 groups
   // of 4 slices); a lone system (the serial fine solve) runs one CTA per tile.
-  if (in_il && next && a.epi == EPI_X && res_config().enabled && a.B * a.nsl >= 16) return launch_res(dir, a, s);
+  if (in_il && next && a.epi == EPI_X && res_config().enabled && a.B * a.nsl >= 16 && a.theta == 1.0)
+    return launch_res(dir, a, s);
   const int sp = (a.epi != EPI_CHAIN && a.nsl >= 2) ? 2 : 1;
   a.ngroups = a.B * ((a.nsl + sp - 1) / sp);
   if (sp == 2) launch_tile<2>(dir, in_il, next, a, s);
@@ -955,7 +1102,7 @@ static PassArgs pass_base(const StreamedProblem &p) {
   a.M = p.M; a.Mp = p.Mp; a.B = p.B; a.Mt = streamed_Mt(p.M); a.nsets = p.nsets;
   a.f = p.f; a.fset = p.fset;
   a.bcoef = p.bcoef; a.Lb = p.L; a.Kb = p.K; a.rb = p.r; a.upper_bc = p.upper_bc;
-  a.dT = p.dT; a.dtau = p.dtau;
+  a.dT = p.dT; a.dtau = p.dtau; a.theta = p.theta;
   return a;
 }
 
@@ -968,7 +1115,9 @@ static cudaError_t streamed_steps(StreamedState &st, const PassArgs &a, const fl
     g.in = in0;
     g.aggT_next = st.aggT[0];
     g.aggL_next = st.aggL[0];
-    k_agg0<<<(unsigned)((unsigned long long)a.nsys * st.ntiles), kSNT, 0, s>>>(g);
+    const unsigned grid = (unsigned)((unsigned long long)a.nsys * st.ntiles);
+    if (a.theta != 1.0) k_agg0<true><<<grid, kSNT, 0, s>>>(g);
+    else k_agg0<false><<<grid, kSNT, 0, s>>>(g);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     *nl += 1;

@@ -95,6 +95,9 @@ struct Scheme {
   double *tileB = nullptr;                          // device [2][nsets][ntiles] (K2 look-back)
   int *tileW = nullptr;
   double *bcoef = nullptr;                          // device [B]
+  double theta = 1.0;                               // θ-step (1: implicit Euler, 1/2: Crank–Nicolson)
+  double *ecoef = nullptr;                          // device [nsets][3] explicit part (θ < 1)
+  double *PL = nullptr, *tileL = nullptr;           // device K2 θ < 1 tile-edge correction tables
 };
 
 constexpr int kResidentMaxM = 2048;
@@ -107,6 +110,7 @@ struct pr_ctx {
   bool poisoned = false;
   // problem
   int M = 0, Mp = 0, B = 0, N = 0, nf = 0, nc = 0, coarse = 0, max_iter = 0, upper_bc = 0;
+  double fine_theta = 1.0;
   double T = 0, dT = 0, tol = 0;
   std::vector<double> K, sig, r, L;
   // placement
@@ -235,11 +239,13 @@ pr_status factorise(pr_ctx *c, double dtau, std::vector<double> &m, std::vector<
   return PR_OK;
 }
 
-pr_status upload_scheme(pr_ctx *c, Scheme &sc, int steps) {
+pr_status upload_scheme(pr_ctx *c, Scheme &sc, int steps, double theta) {
   sc.steps = steps;
   sc.dtau = c->dT / steps;
   std::vector<double> m, ip, cu;
-  pr_status st = factorise(c, sc.dtau, m, ip, cu);
+  sc.theta = theta;
+  const double dti = theta * sc.dtau;  // implicit side I − θdτA
+  pr_status st = factorise(c, dti, m, ip, cu);
   if (st) return st;
   const size_t n = m.size();
   CU(cudaMalloc(&sc.m, n * sizeof(double)));
@@ -258,13 +264,13 @@ pr_status upload_scheme(pr_ctx *c, Scheme &sc, int steps) {
     for (int i = 1; i < c->M; ++i) {
       const double sg = c->sets[s].first, rr = c->sets[s].second, j = i + 1;
       const double a = 0.5 * sg * sg * j * j, b = 0.5 * rr * j;
-      mt[(size_t)s * c->Mp + i] = -sc.dtau * (a - b) * ip[(size_t)s * c->Mp + i];
+      mt[(size_t)s * c->Mp + i] = -dti * (a - b) * ip[(size_t)s * c->Mp + i];
     }
   std::vector<double> iip((size_t)c->nsets * Mt, 1.0), coef((size_t)c->nsets * 2), thB((size_t)2 * c->nsets * nthr);
   for (int s = 0; s < c->nsets; ++s) {
     for (int j = 0; j < c->M; ++j) iip[(size_t)s * Mt + pr::il_index(j)] = ip[(size_t)s * c->Mp + j];
-    coef[2 * s] = sc.dtau * (0.5 * c->sets[s].second);
-    coef[2 * s + 1] = sc.dtau * (0.5 * c->sets[s].first * c->sets[s].first);
+    coef[2 * s] = dti * (0.5 * c->sets[s].second);
+    coef[2 * s + 1] = dti * (0.5 * c->sets[s].first * c->sets[s].first);
     for (int dir = 0; dir < 2; ++dir)
       for (size_t q = 0; q < nthr; ++q) {
         double prod = 1.0;
@@ -289,6 +295,27 @@ pr_status upload_scheme(pr_ctx *c, Scheme &sc, int steps) {
           prod *= thB[base + t];
         }
       }
+  if (theta != 1.0) {
+    // K2 tile-edge corrections (forward passes): PL_t = Π(−m̃_k), k = tile start+1 … thread start−1;
+    // tileL = Π(−m̃_k), k = tile start+1 … tile end (m̃ = 0 beyond M)
+    const int ntl = pr::streamed_ntiles(c->M);
+    std::vector<double> PL((size_t)c->nsets * nthr, 1.0), TL((size_t)c->nsets * ntl);
+    for (int s = 0; s < c->nsets; ++s)
+      for (int tile = 0; tile < ntl; ++tile) {
+        double prod = 1.0;
+        const size_t j0 = (size_t)tile * pr::kSTile;
+        for (int k = 1; k < pr::kSTile; ++k) {
+          if (k % pr::kSPS == 0) PL[(size_t)s * nthr + (size_t)tile * pr::kSNT + k / pr::kSPS] = prod;
+          const size_t j = j0 + k;
+          prod *= j < (size_t)c->M ? -mt[(size_t)s * c->Mp + j] : -0.0;
+        }
+        TL[(size_t)s * ntl + tile] = prod;
+      }
+    CU(cudaMalloc(&sc.PL, PL.size() * sizeof(double)));
+    CU(cudaMalloc(&sc.tileL, TL.size() * sizeof(double)));
+    CU(cudaMemcpy(sc.PL, PL.data(), PL.size() * sizeof(double), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(sc.tileL, TL.data(), TL.size() * sizeof(double), cudaMemcpyHostToDevice));
+  }
   CU(cudaMalloc(&sc.iip, iip.size() * sizeof(double)));
   CU(cudaMalloc(&sc.coef, coef.size() * sizeof(double)));
   CU(cudaMalloc(&sc.thrP, thP.size() * sizeof(double)));
@@ -337,6 +364,18 @@ pr_status upload_scheme(pr_ctx *c, Scheme &sc, int steps) {
   }
   CU(cudaMalloc(&sc.bcoef, c->B * sizeof(double)));
   CU(cudaMemcpy(sc.bcoef, bc.data(), c->B * sizeof(double), cudaMemcpyHostToDevice));
+  if (theta != 1.0) {  // explicit part (1−θ)dτ·(σ²/2, r/2, r) per factor set
+    std::vector<double> ec((size_t)c->nsets * 3);
+    const double dte = (1.0 - theta) * sc.dtau;
+    for (int s = 0; s < c->nsets; ++s) {
+      const double sg = c->sets[s].first, rr = c->sets[s].second;
+      ec[3 * s] = dte * (0.5 * sg * sg);
+      ec[3 * s + 1] = dte * (0.5 * rr);
+      ec[3 * s + 2] = dte * rr;
+    }
+    CU(cudaMalloc(&sc.ecoef, ec.size() * sizeof(double)));
+    CU(cudaMemcpy(sc.ecoef, ec.data(), ec.size() * sizeof(double), cudaMemcpyHostToDevice));
+  }
   return PR_OK;
 }
 
@@ -350,6 +389,9 @@ void free_scheme(Scheme &s) {
   cudaFree(s.ip);
   cudaFree(s.cu);
   cudaFree(s.bcoef);
+  cudaFree(s.ecoef);
+  cudaFree(s.PL);
+  cudaFree(s.tileL);
   s = Scheme();
 }
 
@@ -369,6 +411,10 @@ pr::StreamedProblem sprob(const pr_ctx *c, const Scheme &sc) {
   p.upper_bc = c->upper_bc;
   p.dT = c->dT;
   p.dtau = sc.dtau;
+  p.theta = sc.theta;
+  p.f.ecoef = sc.ecoef;
+  p.f.PL = sc.PL;
+  p.f.tileL = sc.tileL;
   p.steps = sc.steps;
   p.M = c->M;
   p.Mp = c->Mp;
@@ -440,6 +486,8 @@ pr::ResidentArgs base_args(pr_ctx *c, const Scheme &sc) {
   a.fcu = sc.cu;
   a.fset = c->d_fset;
   a.bcoef = sc.bcoef;
+  a.theta = sc.theta;
+  a.ecoef = sc.ecoef;
   a.Lb = c->d_L;
   a.Kb = c->d_K;
   a.rb = c->d_r;
@@ -974,8 +1022,9 @@ pr_status parareal_init(const pr_problem *p, const pr_dist *dist, pr_ctx **out) 
   if (p->max_iter < 1 || p->max_iter > p->N)
     return fail(c, PR_ERR_INVALID_ARGUMENT, fmt("problem.max_iter=%d must be in [1, N=%d]", p->max_iter, p->N));
   if (!(p->tol >= 0)) return fail(c, PR_ERR_INVALID_ARGUMENT, fmt("problem.tol=%g must be >= 0", p->tol));
-  if (p->fine_theta != 1.0)
-    return fail(c, PR_ERR_UNSUPPORTED, fmt("problem.fine_theta=%g: only implicit Euler (1.0) is implemented", p->fine_theta));
+  if (!(p->fine_theta >= 0.5 && p->fine_theta <= 1.0))
+    return fail(c, PR_ERR_INVALID_ARGUMENT,
+                fmt("problem.fine_theta=%g: must be in [0.5, 1] (1 implicit Euler, 0.5 Crank-Nicolson)", p->fine_theta));
   pr_dist dd = {0, 1, 0, nullptr, nullptr};
   if (dist) dd = *dist;
   if (dd.world < 1 || dd.rank < 0 || dd.rank >= dd.world)
@@ -998,6 +1047,7 @@ pr_status parareal_init(const pr_problem *p, const pr_dist *dist, pr_ctx **out) 
   c->B = p->B;
   c->N = p->N;
   c->nf = p->fine_steps;
+  c->fine_theta = p->fine_theta;
   c->nc = p->coarse_steps;
   c->coarse = p->coarse;
   c->max_iter = p->max_iter;
@@ -1054,8 +1104,8 @@ pr_status parareal_init(const pr_problem *p, const pr_dist *dist, pr_ctx **out) 
       return bail(PR_ERR_OUT_OF_MEMORY);
     }
   }
-  if ((st = upload_scheme(c, c->fine, c->nf))) return bail(st);
-  if (c->coarse == PR_COARSE_IMPLICIT_EULER && (st = upload_scheme(c, c->crs, c->nc))) return bail(st);
+  if ((st = upload_scheme(c, c->fine, c->nf, c->fine_theta))) return bail(st);
+  if (c->coarse == PR_COARSE_IMPLICIT_EULER && (st = upload_scheme(c, c->crs, c->nc, 1.0))) return bail(st);
   if (cudaMallocHost(&c->h_delta, std::max(c->max_iter, 1) * sizeof(double)) != cudaSuccess) {
     c->err = "cudaMallocHost(delta) failed";
     return bail(PR_ERR_OUT_OF_MEMORY);

@@ -6,10 +6,14 @@ namespace pr {
 template <int P, int NT, int SPB>
 static void launch_res(bool chain, const ResidentArgs &a, int nsys, cudaStream_t s) {
   const int grid = (nsys + SPB - 1) / SPB;
-  if (chain)
-    k_resident_chain<P, NT, SPB><<<grid, NT * SPB, 0, s>>>(a);
-  else
-    k_fine_sweep<P, NT, SPB><<<grid, NT * SPB, 0, s>>>(a);
+  const bool cn = a.theta != 1.0;  // θ-step with an explicit part (Crank–Nicolson, NEXT-1)
+  if (chain) {
+    if (cn) k_resident_chain<P, NT, SPB, true><<<grid, NT * SPB, 0, s>>>(a);
+    else k_resident_chain<P, NT, SPB, false><<<grid, NT * SPB, 0, s>>>(a);
+  } else {
+    if (cn) k_fine_sweep<P, NT, SPB, true><<<grid, NT * SPB, 0, s>>>(a);
+    else k_fine_sweep<P, NT, SPB, false><<<grid, NT * SPB, 0, s>>>(a);
+  }
 }
 
 cudaError_t launch_resident(bool chain, int M, const ResidentArgs &a, int nsys, cudaStream_t s) {

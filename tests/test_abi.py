@@ -72,10 +72,12 @@ def test_init_validation_names_the_field(field, kw, frag):
     assert ei.value.status == 1 and frag in str(ei.value), str(ei.value)
 
 
-def test_init_rejects_unsupported_theta():
+@pytest.mark.parametrize("theta", [0.3, 0.0, 1.5, float("nan")])
+def test_init_rejects_theta_outside_stable_range(theta):
+    """θ-step fine propagator: θ in [1/2, 1] (CN .. implicit Euler); others are rejected by name."""
     with pytest.raises(parareal.PararealError) as ei:
-        parareal.Context(synth.config("C1").replace(fine_theta=0.5))
-    assert ei.value.status == 7
+        parareal.Context(synth.config("C1").replace(fine_theta=theta))
+    assert ei.value.status == 1 and "fine_theta" in str(ei.value), str(ei.value)
 
 
 def test_init_rejects_bad_partition():

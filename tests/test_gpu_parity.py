@@ -37,7 +37,7 @@ def test_fine_single_slice(kernel, M, N, n):
 
 @pytest.mark.parametrize("M", [4097, 12345, 1 << 16])
 def test_fine_streamed_multi_tile(M):
-    """Several 4096-point tiles with a ragged tail: decoupled look-back across CTAs."""
+    """Several 2048-point tiles with a ragged tail: look-back across tiles."""
     p = synth.single(M, 64, fine_steps=20)
     U = synth.random_state(1, M, seed=3)
     with ctx_for(p, fine_kernel=2) as c:
@@ -63,6 +63,68 @@ def test_fine_portfolio_instances():
         with ctx_for(p, fine_kernel=kernel) as c:
             got = c.apply_fine(3, U)
         assert_close(got, oracle.fine(p, 3, U.astype(np.float64)), what="F portfolio kernel=%d" % kernel)
+
+
+# ------------------------------------------------------------------ θ-step fine propagator (NEXT-1)
+# Crank–Nicolson (θ = 1/2, the paper's F) and a θ = 3/4 scheme: explicit 3-point stencil
+# plus the implicit solve, against the oracle's θ-step (pinned in test_oracle_pins).
+
+@pytest.mark.parametrize("kernel", FINE_KERNELS)
+@pytest.mark.parametrize("M,N,n,theta", [(1, 2, 1, 0.5), (64, 4, 3, 0.5), (1000, 8, 5, 0.5), (2000, 4, 1, 0.75),
+                                         (2048, 4, 0, 0.5), (5000, 8, 2, 0.5), (12345, 16, 9, 0.5)])
+def test_fine_theta_single_slice(kernel, M, N, n, theta):
+    if kernel == 1 and M > 2048:
+        pytest.skip("resident kernel holds M <= 2048")
+    p = synth.single(M, N, fine_theta=theta, fine_steps=40)
+    U = synth.random_state(1, M, seed=M + 1)
+    with ctx_for(p, fine_kernel=kernel) as c:
+        got = c.apply_fine(n, U)
+    ref = oracle.fine(p, n, U.astype(np.float64))
+    assert_close(got, ref, what="F theta=%g M=%d n=%d kernel=%d" % (theta, M, n, kernel))
+
+
+def test_fine_cn_portfolio_and_payoff():
+    """CN on C4-style instances (several factor sets and strikes) from the payoff kink, both kernels."""
+    p = synth.portfolio(n_k=3, n_s=4, M=256, N=16, fine_theta=0.5)
+    U = oracle.payoff(p).astype(np.float32)
+    for kernel in FINE_KERNELS:
+        with ctx_for(p, fine_kernel=kernel) as c:
+            got = c.apply_fine(5, U)
+        assert_close(got, oracle.fine(p, 5, U.astype(np.float64)), what="F CN portfolio kernel=%d" % kernel)
+
+
+def test_fine_cn_c3_size_single_slice():
+    """CN at the C3 grid (2^20 points, 100 steps): dτ·a_j reaches 3e6, far outside the M-matrix
+    range of the explicit part; fp32 state between streamed passes stays within tolerance."""
+    p = synth.config("C3", fine_theta=0.5)
+    U0 = oracle.payoff(p)
+    with ctx_for(p) as c:
+        got = c.apply_fine(0, U0.astype(np.float32))
+    assert_close(got, oracle.fine(p, 0, U0), what="F CN C3")
+
+
+@pytest.mark.parametrize("kernel,M", [(1, 300), (2, 300), (2, 6000)])
+def test_serial_fine_cn(kernel, M):
+    p = synth.single(M, 8, fine_theta=0.5, fine_steps=20)
+    with ctx_for(p, fine_kernel=kernel) as c:
+        got, _ = c.serial_fine()
+    ref = oracle.serial_fine(p)[-1]
+    assert_close(got, ref, what="serial fine CN kernel=%d M=%d" % (kernel, M))
+
+
+@pytest.mark.parametrize("kernel,M,N", [(1, 64, 4), (2, 5000, 6), (2, 3000, 17)])
+def test_parareal_cn_fine_ie_coarse(kernel, M, N):
+    """Parareal with the CN fine propagator and the implicit-Euler coarse one (the paper's
+    numerical pairing): every iterate against the oracle, fixed K."""
+    p = synth.single(M, N, fine_theta=0.5, fine_steps=20, coarse=synth.COARSE_IMPLICIT_EULER, coarse_steps=2,
+                     max_iter=3, tol=0.0)
+    with ctx_for(p, fine_kernel=kernel) as c:
+        _, rep = c.solve()
+        it = c.copy_iterates(0, p.N + 1)
+    ref_U, ref_d, K, _ = oracle.parareal(p)
+    assert rep["iterations"] == K == 3
+    assert_close(it, ref_U, what="CN Parareal iterates kernel=%d M=%d" % (kernel, M))
+    assert np.allclose(rep["delta"], ref_d, rtol=2e-2)
 
 
 @pytest.mark.parametrize("dims,act", [(synth.PINN_3x20, synth.ACT_TANH), (synth.PINN_PAPER, synth.ACT_RELU),
