@@ -46,13 +46,15 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-c3-sweep", action="store_true", help="skip the C3 fine-sweep HBM roofline leg")
     ap.add_argument("--no-graphs", action="store_true", help="eager launches instead of the captured CUDA graph")
+    ap.add_argument("--fine-theta", type=float, default=1.0,
+                    help="fine theta-step: 1 implicit Euler (default, reading Q1), 0.5 Crank-Nicolson (NEXT-1)")
     return ap.parse_args()
 
 
 def problem_for(args):
     from paper_2303_03848_b200 import synth
     coarse = synth.COARSE_PINN if args.coarse == "pinn" else synth.COARSE_IMPLICIT_EULER
-    p = synth.config(args.config, coarse=coarse, coarse_steps=1, tol=0.0)
+    p = synth.config(args.config, coarse=coarse, coarse_steps=1, tol=0.0, fine_theta=args.fine_theta)
     return p.replace(max_iter=min(args.iters, p.N))
 
 
@@ -159,12 +161,13 @@ def run_reference(args):
 
 
 def config_dict(args, p):
-    return {"workload": "%s: European call, M=%d grid points x N=%d slices x B=%d instances, %d IE fine "
+    return {"workload": "%s: European call, M=%d grid points x N=%d slices x B=%d instances, %d %s fine "
                         "steps/slice, %s coarse, K=%d fixed iterations" % (
                             args.config, p.M, p.N, p.B, p.fine_steps,
+                            "IE" if p.fine_theta == 1.0 else ("CN" if p.fine_theta == 0.5 else "theta=%g" % p.fine_theta),
                             "PINN [4,20,20,20,1] tanh" if args.coarse == "pinn" else "implicit-Euler (1 step/slice)",
                             p.max_iter),
-            "M": p.M, "N": p.N, "B": p.B, "fine_steps": p.fine_steps, "K": p.max_iter,
+            "M": p.M, "N": p.N, "B": p.B, "fine_steps": p.fine_steps, "fine_theta": p.fine_theta, "K": p.max_iter,
             "coarse": args.coarse, "parallelism": "time-slices/%d" % args.gpus,
             "cuda_graph": (not args.no_graphs) and args.gpus == 1,
             "l2": "flushed (256 MiB write) before every timed step" if p.M * p.B * 4 * (p.N + 1) * 3 < (126 << 20)
@@ -200,11 +203,13 @@ def roofline(p, ph, K, world, rank, pk, pk_src, clk_mhz, n_sm, synth):
                     % (n_sm, clk_mhz), "work_per_unit": "9 fp64 flop per point-step", "launch_unit": "one sweep"}
             tr = ncu_traffic("k_fine_sweep")
         else:
-            roof = {"kernel": "k_pass_res (K2, persistent streamed pass)", "bound": "hbm",
+            kname = ("k_pass_res (K2, persistent streamed pass)" if p.fine_theta == 1.0
+                     else "k_streamed_pass (K2, Crank-Nicolson tile pass)")
+            roof = {"kernel": kname, "bound": "hbm",
                     "achieved": 16.0 * pt_steps / sweep_s / 1e9,
                     "peak": float(pk["hbm_gbs"]), "unit": "GB/s", "peak_source": pk_src,
                     "work_per_unit": "16 B per point-step", "launch_unit": "one pass (8 B per point)"}
-            tr = ncu_traffic("k_pass_res")
+            tr = ncu_traffic("k_pass_res" if p.fine_theta == 1.0 else "k_streamed_pass")
     else:
         evals = float(p.B) * p.M * nloc
         chain_s = ph["ms_coarse"] / (K + 1) / 1e3
