@@ -192,7 +192,12 @@ enum {
                                into a CUDA graph on its first call per (V_T, V_0) pair and replayed on
                                later calls (same kernels, same results); any other solve runs eagerly.
                                set_option / load_pinn_weights / free discard the captured graph.   */
-  PR_OPT_PINN_KERNEL = 3    /* 0 auto, 1 shared-memory weights, 2 latency mode (4 threads/point; B·M ≤ 65536) */
+  PR_OPT_PINN_KERNEL = 3,   /* 0 auto, 1 shared-memory weights, 2 latency mode (4 threads/point; B·M ≤ 65536) */
+  PR_OPT_PIPELINE = 4       /* 0 auto: a single-GPU fixed-K (tol == 0) solve with PINN G in latency mode and
+                               the resident fine kernel at M ≤ 1024 runs pipelined: fine
+                               solves and the coarse chain overlapped in one cooperative kernel, bitwise the
+                               blocking results; its report gives the overlapped time as both ms_fine and
+                               ms_coarse.  1: always the blocking schedule. */
 };
 pr_status parareal_set_option(pr_ctx *ctx, int32_t key, int64_t value);
 

@@ -28,6 +28,20 @@ cudaError_t launch_pinn_split(int IN, int W, int act, const PinnArgs &a, dim3 gr
 bool pinn_param_supported(int IN, int W, int LH, int act);
 cudaError_t launch_pinn_param(int IN, int W, int LH, int act, const float *pk, const PinnArgs &a, dim3 grid,
                               cudaStream_t s);
+// Pipelined Parareal on one GPU (pipe.cu, NEXT-2): PINN chain (latency mode) and K1 fine solves
+// in one cooperative kernel, synchronised per slice.
+struct PipeArgs {
+  ResidentArgs r;          // fine scheme and the U / Gh / D / Fk rows
+  PinnArgs g;              // coarse chain (same rows)
+  int N, K, C;             // slices, iterations, chain CTAs per instance
+  double *partials;        // [K+1][pstride] δ partials per iteration
+  size_t pstride;
+  double *wstage;          // [N+1][B·C][4 warps][2] per-warp δ partials of the current iteration
+  int *cnt, *floaded, *fdone;  // [B][N] counters, zero at launch
+};
+bool pipe_supported(int M, bool cn, int IN, int W, int act);
+cudaError_t launch_parareal_pipe(const PipeArgs &pa, int M, bool cn, int IN, int W, int act, size_t smem,
+                                 cudaStream_t s);
 // K6/K7 (misc.cu)
 cudaError_t launch_payoff(float *U0, int M, int Mp, int B, const double *Lb, const double *Kb, cudaStream_t s);
 cudaError_t launch_delta(const double *partials, int B, int nch, int ln_lo, int ln_hi, unsigned long long *dmax,

@@ -146,7 +146,14 @@ struct pr_ctx {
   int opt_pinn_kernel = 0;
   int opt_fine_kernel = 0;
   int opt_graphs = 0;
+  int opt_pipeline = 0;  // 0 auto, 1 off (PR_OPT_PIPELINE)
   bool capturing = false;
+  // pipelined schedule (pipe.cu): per-iteration δ partials and the slice counters
+  double *pipe_partials = nullptr;
+  int *pipe_flags = nullptr;
+  double *pipe_wstage = nullptr;
+  size_t pipe_pstride = 0;
+  int pipe_ok = -1;  // -1 unknown, 0 no, 1 yes
   // captured solve (PR_OPT_USE_GRAPHS)
   cudaGraphExec_t g_exec = nullptr;
   const float *g_vt = nullptr;
@@ -746,6 +753,75 @@ pr_plan make_plan(int N, int world, int rank, int k) {
   return P;
 }
 
+// ---------------------------------------------------------------- pipelined schedule (NEXT-2)
+// Eligible: one GPU, fixed K (tol = 0: no host decision between iterations), PINN G in latency
+// mode, resident fine kernel with M ≤ 1024, and every CTA co-resident (checked at first launch).
+bool pipe_eligible(const pr_ctx *c) {
+  if (c->opt_pipeline == 1 || c->pipe_ok == 0) return false;
+  if (c->world != 1 || c->tol != 0.0 || c->coarse != PR_COARSE_PINN || c->max_iter < 1) return false;
+  if (!use_split_pinn(c) || !use_resident(c) || c->M > 1024) return false;
+  return pr::pipe_supported(c->M, c->fine_theta != 1.0, c->IN, c->W, c->act);
+}
+
+pr_status ensure_pipe(pr_ctx *c) {
+  if (c->pipe_partials) return PR_OK;
+  c->pipe_pstride = (size_t)(c->Nloc + 1) * c->B * c->nch * 2;
+  CU(cudaMalloc(&c->pipe_partials, (size_t)(c->max_iter + 1) * c->pipe_pstride * sizeof(double)));
+  CU(cudaMalloc(&c->pipe_flags, (size_t)3 * c->B * c->N * sizeof(int)));
+  CU(cudaMalloc(&c->pipe_wstage, (size_t)(c->N + 1) * c->B * c->nch * 4 * 2 * sizeof(double)));
+  CU(cudaMemset(c->pipe_partials, 0, (size_t)(c->max_iter + 1) * c->pipe_pstride * sizeof(double)));
+  return PR_OK;
+}
+
+// All K iterations (and the k = 0 coarse sweep) in one cooperative launch, then the K δ's.
+// Returns PR_ERR_UNSUPPORTED (nothing enqueued) if the grid cannot be co-resident.
+pr_status solve_pipelined(pr_ctx *c) {
+  CU(cudaMemsetAsync(c->pipe_flags, 0, (size_t)3 * c->B * c->N * sizeof(int), c->stream));
+  pr::PipeArgs pa;
+  std::memset(&pa, 0, sizeof pa);
+  pa.r = base_args(c, c->fine);
+  pa.r.U = c->U;
+  pa.r.Gh = c->Gh;
+  pa.r.D = c->D;
+  pa.r.Fk = c->Fk;
+  pa.g = pinn_args(c);
+  pa.g.U = c->U;
+  pa.g.Gh = c->Gh;
+  pa.g.D = c->D;
+  pa.g.Fcopy = c->Fk;
+  pa.N = c->N;
+  pa.K = c->max_iter;
+  pa.C = c->nch;  // chain CTAs per instance (latency mode: 128/kPinnSplitG points each)
+  pa.partials = c->pipe_partials;
+  pa.pstride = c->pipe_pstride;
+  pa.wstage = c->pipe_wstage;
+  pa.cnt = c->pipe_flags;
+  pa.floaded = c->pipe_flags + (size_t)c->B * c->N;
+  pa.fdone = c->pipe_flags + (size_t)2 * c->B * c->N;
+  const cudaError_t e = pr::launch_parareal_pipe(pa, c->M, c->fine_theta != 1.0, c->IN, c->W, c->act,
+                                                 (size_t)c->nfloats * sizeof(float), c->stream);
+  if (e == cudaErrorCooperativeLaunchTooLarge) {
+    cudaGetLastError();
+    c->pipe_ok = 0;
+    return PR_ERR_UNSUPPORTED;
+  }
+  if (e != cudaSuccess) return fail(c, PR_ERR_CUDA, fmt("pipelined Parareal launch: %s", cudaGetErrorString(e)));
+  c->pipe_ok = 1;
+  c->launches++;
+  double *save = c->partials;
+  for (int k = 1; k <= c->max_iter; ++k) {
+    const pr_plan P = make_plan(c->N, 1, 0, k);
+    c->partials = c->pipe_partials + (size_t)k * c->pipe_pstride;
+    const pr_status st = delta_reduce(c, k, P.delta_lo, P.delta_hi, c->nch);
+    if (st) {
+      c->partials = save;
+      return st;
+    }
+  }
+  c->partials = save;
+  return PR_OK;
+}
+
 using Spans = std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>>;
 
 pr_status solve_report(pr_ctx *c, int K, int conv, cudaEvent_t e0, cudaEvent_t e1, const Spans &spans,
@@ -797,6 +873,7 @@ pr_status solve_impl(pr_ctx *c, const float *V_T, float *V_0, bool device_ptr, p
     CU(cudaStreamSynchronize(c->stream));
     return solve_report(c, c->g_K, 0, c->g_e0, c->g_e1, c->g_spans, c->g_launches, rep);
   }
+  if (pipe_eligible(c) && (st = ensure_pipe(c))) return st;  // (allocation cannot be captured)
   if (use_graph) {
     drop_graph(c);
     CU(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
@@ -818,6 +895,20 @@ pr_status solve_impl(pr_ctx *c, const float *V_T, float *V_0, bool device_ptr, p
   pt.begin(PH_SETUP);
   if (r == 0 && (st = load_initial(c, V_T, device_ptr))) return st;
   pt.end();
+  bool piped = false;
+  if (pipe_eligible(c)) {  // NEXT-2: fine solves and coarse chain overlapped in one kernel
+    pt.begin(PH_FINE);
+    st = solve_pipelined(c);
+    pt.end();
+    if (st == PR_OK) {
+      piped = true;
+      K = c->max_iter;
+      pt.spans.push_back({PH_COARSE, pt.spans.back().second});  // overlapped: same span for both
+    } else if (st != PR_ERR_UNSUPPORTED) {
+      return st;
+    }
+  }
+  if (!piped) {
   {
     const pr_plan P0 = make_plan(c->N, R, r, 0);
     if (P0.recv_first) {
@@ -870,6 +961,7 @@ pr_status solve_impl(pr_ctx *c, const float *V_T, float *V_0, bool device_ptr, p
       }
     }
   }
+  }  // !piped
   // final state U^K_N: last rank → rank 0 (→ V_0)
   if (R > 1) {
     pt.begin(PH_COMM);
@@ -1380,6 +1472,10 @@ pr_status parareal_set_option(pr_ctx *c, int32_t key, int64_t value) {
       if (value < 0 || value > 1) return fail(c, PR_ERR_INVALID_ARGUMENT, "PR_OPT_USE_GRAPHS must be 0 or 1");
       c->opt_graphs = (int)value;
       return PR_OK;
+    case PR_OPT_PIPELINE:
+      if (value < 0 || value > 1) return fail(c, PR_ERR_INVALID_ARGUMENT, "PR_OPT_PIPELINE must be 0 or 1");
+      c->opt_pipeline = (int)value;
+      return PR_OK;
   }
   return fail(c, PR_ERR_INVALID_ARGUMENT, fmt("unknown option key %d", key));
 }
@@ -1401,6 +1497,9 @@ void parareal_free(pr_ctx *c) {
   cudaFree(c->d_wts);
   if (c->own_ws) cudaFree(c->ws);
   if (c->h_delta) cudaFreeHost(c->h_delta);
+  cudaFree(c->pipe_partials);
+  cudaFree(c->pipe_flags);
+  cudaFree(c->pipe_wstage);
   for (auto e : c->ev) cudaEventDestroy(e);
   if (c->own_stream) cudaStreamDestroy(c->stream);
   delete c;

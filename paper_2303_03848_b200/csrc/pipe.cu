@@ -1,0 +1,273 @@
+// pipe.cu — pipelined Parareal on one GPU (Eq. 8).
+//
+// The blocking schedule runs, per iteration k, the fine sweep F̂^k_n = F(U^{k−1}_n) over all
+// slices and then the coarse chain U^k_{n+1} = G(U^k_n) + F̂^k_n − Ĝ^{k−1}_n (Eq. 7).
+// At small grids both are latency-bound and neither fills the GPU, so here they run at the
+// same time in one cooperative kernel and each waits only for the data it needs:
+//
+//   fine(k, n)   needs U^{k−1}_n                  (chain k−1 past slice n−1, or its copy step)
+//                and, for D_n = F̂ − Ĝ^{k−1}_n, Ĝ^{k−1}_n (chain k−1 past slice n)
+//   chain(k, n)  needs D_n                        (fine(k, n) done)
+//                and may overwrite U_{n+1} only once fine(k, n+1) has read U^{k−1}_{n+1}
+//
+// so iteration k's fine solves start slice by slice behind chain k−1 and chain k trails them,
+// approaching Eq. (8)'s pipelined cost instead of the blocking sum.  Results are bitwise those of
+// the blocking schedule (same kernels' arithmetic, same orders).  The δ partial sums of each
+// iteration go to their own buffer and are reduced after the kernel.
+//
+// Roles: CTAs [0, B·C) run the PINN chain in latency mode (kPinnSplitG threads per point,
+// 128/kPinnSplitG points per CTA, C chunks per instance), CTAs [B·C, B·C + B·N) run one K1
+// system (slice n, instance b) each for all its iterations.  Counters (per instance and slice):
+//   cnt[b][n]      += 1 by every chain warp of b after it wrote U_{n+1} (or, at its copy step, U_k)
+//   floaded[b][n]  = k after fine(k, n) loaded its input,   fdone[b][n] = k after it stored D_n / F̂
+// Waits are by one thread (ld.acquire) followed by a CTA barrier; data written by other CTAs is
+// read through L2 (ld.global.cg).  All CTAs are co-resident (cooperative launch), and the wait
+// graph is acyclic, so the kernel cannot deadlock.
+#include "launch.h"
+#include "fine_resident.cuh"
+#include "pinn_chain.cuh"
+
+namespace pr {
+
+__device__ __forceinline__ int ld_acquire(const int *p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void wait_geq(const int *p, int target) {
+  while (ld_acquire(p) < target) __nanosleep(20);
+}
+// after a CTA barrier: publish this CTA's stores
+__device__ __forceinline__ void publish_add(int *p) {
+  __threadfence();
+  atomicAdd(p, 1);
+}
+__device__ __forceinline__ void publish_set(int *p, int v) {
+  __threadfence();
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Coarse chain, warp-granular: each warp (128/(32·…) — 32/kPinnSplitG = 8 points) waits for
+// its inputs and publishes its outputs by itself (no CTA barrier per slice).  δ partial sums are
+// staged per warp and folded per CTA, warps in index order, at the end of each iteration — the
+// blocking kernel's summation order, so δ is bitwise the same.
+template <int IN, int ACT>
+__device__ void chain_role(const PipeArgs &pa, int b, int chunk, const float *sw) {
+  constexpr int G = kPinnSplitG;
+  constexpr int NWC = 128 / 32;  // warps per chain CTA
+  const PinnArgs &a = pa.g;
+  const double Lb = a.Lb[b];
+  const float gscale = (float)(Lb * (double)a.out_scale);
+  const float invL = (float)(1.0 / Lb);
+  const size_t sstride = (size_t)a.B * a.Mp;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const bool leader = threadIdx.x % G == 0;
+  const int j = chunk * (blockDim.x / G) + threadIdx.x / G;
+  const bool ok = j < a.M;
+  const double dS = Lb / (a.M + 1);
+  const float s_over_L = (float)(((j + 1) * dS) / Lb);
+  int *cnt = pa.cnt + (size_t)b * pa.N;
+  const int *floaded = pa.floaded + (size_t)b * pa.N, *fdone = pa.fdone + (size_t)b * pa.N;
+  const int cta = b * pa.C + chunk;
+  // per-warp partial of (row ln): stage[((ln·B·C) + cta)·NWC + wid]·2
+  auto stage_partial = [&](int ln, double num, double den) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      num += __shfl_xor_sync(0xffffffffu, num, o);
+      den += __shfl_xor_sync(0xffffffffu, den, o);
+    }
+    if (lane == 0) {
+      double *ps = pa.wstage + ((((size_t)ln * a.B * pa.C) + cta) * NWC + wid) * 2;
+      ps[0] = num;
+      ps[1] = den;
+    }
+  };
+  float u = ok ? __ldcg(a.U + (size_t)b * a.Mp + j) : 0.f;  // U_0 (written before the kernel)
+  for (int k = 0; k <= pa.K; ++k) {
+    int n0 = 0;
+    if (k > 0) {
+      // U^k_k := F̂^k_{k−1} (copied, reading Q12), with the δ partial of slice k
+      if (lane == 0) {
+        wait_geq(fdone + (k - 1), k);
+        if (k <= pa.N - 1) wait_geq(floaded + k, k);
+      }
+      __syncwarp();
+      float *uk = a.U + (size_t)k * sstride + (size_t)b * a.Mp;
+      double num = 0.0, den = 0.0;
+      if (ok) {
+        const float f = __ldcg(a.Fcopy + (size_t)b * a.Mp + j);
+        if (leader) {
+          const double dd = (double)f - (double)__ldcg(uk + j);
+          num = dd * dd;
+          den = (double)f * f;
+        }
+        u = f;
+      }
+      stage_partial(k, num, den);
+      __syncwarp();
+      if (ok && leader) uk[j] = u;
+      __syncwarp();
+      if (lane == 0) publish_add(cnt + (k - 1));
+      n0 = k;
+    }
+    for (int n = n0; n < pa.N; ++n) {
+      if (k > 0 && lane == 0) {
+        wait_geq(fdone + n, k);                               // D_n of this iteration
+        if (n + 1 <= pa.N - 1) wait_geq(floaded + n + 1, k);  // U^{k−1}_{n+1} has been read
+      }
+      __syncwarp();
+      const size_t row = (size_t)n * sstride + (size_t)b * a.Mp;
+      float dn = 0.f, uo = 0.f;
+      if (k > 0 && ok) {
+        dn = __ldcg(a.D + row + j);
+        uo = __ldcg(a.U + row + sstride + j);
+      }
+      const int ng = a.n_base + n;
+      const float tf = (float)((a.T - ng * a.dT) / a.T), tt = (float)((a.T - (ng + 1) * a.dT) / a.T);
+      float x[IN];
+      if (IN == 4) {
+        x[0] = tf * a.cs0;
+        x[1] = tt * a.cs1;
+        x[2] = (u * invL) * a.cs2;
+        x[3] = s_over_L * a.cs3;
+      } else {
+        x[0] = tt * a.cs0;
+        x[IN - 1] = s_over_L * a.cs1;
+      }
+      const float y = mlp_split<IN, 20, G, ACT>(sw, a.LH, x);
+      const float g = gscale * y;
+      float nv = 0.f;
+      double num = 0.0, den = 0.0;
+      if (ok) {
+        nv = k > 0 ? g + dn : g;
+        if (leader) {
+          a.Gh[row + j] = g;
+          if (k > 0) {
+            const double dd = (double)nv - (double)uo;
+            num = dd * dd;
+            den = (double)nv * nv;
+          }
+          a.U[row + sstride + j] = nv;
+        }
+      }
+      u = nv;
+      if (k > 0) stage_partial(n + 1, num, den);
+      __syncwarp();
+      if (lane == 0) publish_add(cnt + n);
+    }
+    if (k > 0) {  // fold this iteration's per-warp partials, warps in order (the blocking order)
+      __syncthreads();
+      double *part = pa.partials + (size_t)k * pa.pstride;
+      for (int ln = k + (int)threadIdx.x; ln <= pa.N; ln += blockDim.x) {
+        const double *ps = pa.wstage + (((size_t)ln * a.B * pa.C) + cta) * NWC * 2;
+        double num = 0.0, den = 0.0;
+        for (int q = 0; q < NWC; ++q) { num += ps[2 * q]; den += ps[2 * q + 1]; }
+        double *pp = part + (((size_t)ln * a.B + b) * a.nch + chunk) * 2;
+        pp[0] = num;
+        pp[1] = den;
+      }
+      __syncthreads();
+    }
+  }
+}
+
+template <int P, bool CN>
+__device__ void fine_role(const PipeArgs &pa, int n, int b) {
+  constexpr int NT = 128;
+  const ResidentArgs &a = pa.r;
+  __shared__ double sh[Tri<P, NT, CN>::kShm];
+  __shared__ double bct[kBcChunk];
+  const int t = threadIdx.x;
+  Tri<P, NT, CN> tri;
+  tri.setup(a, a.fset[b], t, sh);
+  __syncthreads();
+  const int C = pa.C * (128 / 32);  // publishing chain warps per instance
+  const int *cnt = pa.cnt + (size_t)b * pa.N;
+  int *floaded = pa.floaded + (size_t)b * pa.N, *fdone = pa.fdone + (size_t)b * pa.N;
+  const size_t row = ((size_t)n * a.B + b) * a.Mp;
+  const int kmax = min(pa.K, n + 1);
+  for (int k = 1; k <= kmax; ++k) {
+    if (n >= 1 && t == 0) wait_geq(cnt + (n - 1), k * C);  // U^{k−1}_n written
+    __syncthreads();
+    double x[P];
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      const int j = t * P + i;
+      x[i] = (j < a.M) ? (double)__ldcg(a.U + row + j) : 0.0;
+    }
+    __syncthreads();
+    if (t == 0) publish_set(floaded + n, k);
+    run_steps<P, NT, CN>(tri, a, b, a.n_base + n, t, x, sh, bct);
+    if (n == k - 1) {  // F̂_{k−1}: copied into U^k_k by chain k
+      float *o = a.Fk + (size_t)b * a.Mp;
+#pragma unroll
+      for (int i = 0; i < P; ++i) {
+        const int j = t * P + i;
+        if (j < a.M) o[j] = (float)x[i];
+      }
+    } else {  // D_n = F̂_n − Ĝ^{k−1}_n once chain k−1 has passed slice n
+      if (t == 0) wait_geq(cnt + n, k * C);
+      __syncthreads();
+#pragma unroll
+      for (int i = 0; i < P; ++i) {
+        const int j = t * P + i;
+        if (j < a.M) a.D[row + j] = (float)(x[i] - (double)__ldcg(a.Gh + row + j));
+      }
+    }
+    __syncthreads();
+    if (t == 0) publish_set(fdone + n, k);
+  }
+}
+
+template <int P, bool CN, int IN, int ACT>
+__global__ void __launch_bounds__(128) k_parareal_pipe(PipeArgs pa) {
+  extern __shared__ float sw[];
+  const int nchain = pa.g.B * pa.C;
+  if ((int)blockIdx.x < nchain) {
+    for (int i = threadIdx.x; i < pa.g.nfloats; i += blockDim.x) sw[i] = pa.g.wts[i];
+    __syncthreads();
+    chain_role<IN, ACT>(pa, blockIdx.x / pa.C, blockIdx.x % pa.C, sw);
+  } else {
+    const int f = blockIdx.x - nchain;
+    fine_role<P, CN>(pa, f / pa.g.B, f % pa.g.B);
+  }
+}
+
+typedef void (*PipeKernel)(PipeArgs);
+template <bool CN, int IN, int ACT>
+static PipeKernel pipe_kernel_p(int M) {
+  if (M <= 256) return k_parareal_pipe<2, CN, IN, ACT>;
+  if (M <= 512) return k_parareal_pipe<4, CN, IN, ACT>;
+  if (M <= 1024) return k_parareal_pipe<8, CN, IN, ACT>;
+  return nullptr;
+}
+static PipeKernel pipe_kernel(int M, bool cn, int IN, int W, int act) {
+  if (W != 20 || act != 0) return nullptr;
+  if (IN == 4) return cn ? pipe_kernel_p<true, 4, 0>(M) : pipe_kernel_p<false, 4, 0>(M);
+  if (IN == 2) return cn ? pipe_kernel_p<true, 2, 0>(M) : pipe_kernel_p<false, 2, 0>(M);
+  return nullptr;
+}
+
+bool pipe_supported(int M, bool cn, int IN, int W, int act) { return pipe_kernel(M, cn, IN, W, act) != nullptr; }
+
+// Launches the cooperative kernel; cudaErrorCooperativeLaunchTooLarge (or not supported) tells
+// the caller to use the blocking schedule.
+cudaError_t launch_parareal_pipe(const PipeArgs &pa, int M, bool cn, int IN, int W, int act, size_t smem,
+                                 cudaStream_t s) {
+  PipeKernel k = pipe_kernel(M, cn, IN, W, act);
+  if (!k) return cudaErrorInvalidValue;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, nsm = 0, occ = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 128, smem);
+  if (e != cudaSuccess) return e;
+  const int grid = pa.g.B * pa.C + pa.g.B * pa.N;
+  if (grid > occ * nsm) return cudaErrorCooperativeLaunchTooLarge;
+  PipeArgs arg = pa;
+  void *params[] = {&arg};
+  return cudaLaunchCooperativeKernel((const void *)k, dim3(grid), dim3(128), params, smem, s);
+}
+
+}  // namespace pr

@@ -340,6 +340,28 @@ def test_device_entry_points():
     assert np.array_equal(v0, oracle.payoff(p).astype(np.float32))
 
 
+@pytest.mark.parametrize("name,M,N,B,theta", [("C1", 64, 4, 1, 1.0), ("C2", 1024, 32, 1, 1.0), ("C2", 1024, 32, 1, 0.5),
+                                              ("portfolio", 256, 8, 6, 1.0), ("odd", 700, 12, 1, 1.0)])
+def test_pipelined_matches_blocking(name, M, N, B, theta):
+    """PR_OPT_PIPELINE (NEXT-2): the overlapped single-kernel schedule gives the blocking
+    schedule's iterates, output and δ bitwise (and is the one auto mode takes here)."""
+    if name == "portfolio":
+        p = synth.portfolio(n_k=2, n_s=3, M=M, N=N, coarse=synth.COARSE_PINN, max_iter=3, tol=0.0)
+    else:
+        p = synth.single(M, N, coarse=synth.COARSE_PINN, max_iter=3, tol=0.0, fine_theta=theta)
+    net = synth.kaiming_net(synth.PINN_3x20, seed=2)
+    with ctx_for(p, net) as c:
+        a, ra = c.solve()
+        it_a = c.copy_iterates(0, p.N + 1)
+        c.set_option(parareal.OPT_PIPELINE, 1)
+        b, rb = c.solve()
+        it_b = c.copy_iterates(0, p.N + 1)
+    assert ra["kernel_launches"] < rb["kernel_launches"], "auto mode did not pipeline"
+    assert ra["iterations"] == rb["iterations"] == 3
+    assert np.array_equal(a, b) and np.array_equal(it_a, it_b)
+    assert np.array_equal(ra["delta"], rb["delta"])
+
+
 def test_graph_replay_matches_eager():
     """PR_OPT_USE_GRAPHS: captured + replayed solves give the eager results bitwise, replays
     are repeatable, and new weights are picked up (the graph is re-captured)."""
