@@ -71,6 +71,39 @@ __global__ void k_delta_wide(const double *partials, int B, int nch, int ln_lo, 
   }
 }
 
+// δ^k for k = 1..K in one launch (pipelined schedule: per-iteration partial buffers of pstride
+// doubles; iteration k covers rows k..N).  Same per-row fixed-order sums as k_delta; dmax[K]
+// must be zero.
+__global__ void k_delta_multi(const double *partials, size_t pstride, int B, int nch, int N, int K,
+                              unsigned long long *dmax) {
+  const int k = blockIdx.y + 1;
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  const int total = (N - k + 1) * B;
+  double rel = 0.0;
+  if (idx < total) {
+    const int ln = k + idx / B, b = idx % B;
+    const double *p = partials + (size_t)k * pstride + (((size_t)ln * B + b) * nch) * 2;
+    double num = 0.0, den = 0.0;
+    for (int c = 0; c < nch; ++c) { num += p[2 * c]; den += p[2 * c + 1]; }
+    rel = (den > 0.0) ? sqrt(num) / sqrt(den) : sqrt(num);
+  }
+  unsigned long long v = (unsigned long long)__double_as_longlong(rel);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = w > v ? w : v;
+  }
+  if ((threadIdx.x & 31) == 0) atomicMax(dmax + (k - 1), v);
+}
+
+cudaError_t launch_delta_multi(const double *partials, size_t pstride, int B, int nch, int N, int K,
+                               unsigned long long *dmax, cudaStream_t s) {
+  if (nch > 32) return cudaErrorInvalidValue;  // (the pipelined schedule runs at most 32 chunks)
+  dim3 grid((N * B + 255) / 256, K);
+  k_delta_multi<<<grid, 256, 0, s>>>(partials, pstride, B, nch, N, K, dmax);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_delta(const double *partials, int B, int nch, int ln_lo, int ln_hi, unsigned long long *dmax,
                          cudaStream_t s) {
   const int total = (ln_hi - ln_lo + 1) * B;

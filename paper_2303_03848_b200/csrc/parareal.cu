@@ -768,7 +768,7 @@ pr_status ensure_pipe(pr_ctx *c) {
   c->pipe_pstride = (size_t)(c->Nloc + 1) * c->B * c->nch * 2;
   CU(cudaMalloc(&c->pipe_partials, (size_t)(c->max_iter + 1) * c->pipe_pstride * sizeof(double)));
   CU(cudaMalloc(&c->pipe_flags, (size_t)3 * c->B * c->N * sizeof(int)));
-  CU(cudaMalloc(&c->pipe_wstage, (size_t)(c->N + 1) * c->B * c->nch * 4 * 2 * sizeof(double)));
+  CU(cudaMalloc(&c->pipe_wstage, (size_t)(c->max_iter + 1) * (c->N + 1) * c->B * c->nch * 4 * 2 * sizeof(double)));
   CU(cudaMemset(c->pipe_partials, 0, (size_t)(c->max_iter + 1) * c->pipe_pstride * sizeof(double)));
   return PR_OK;
 }
@@ -795,6 +795,14 @@ pr_status solve_pipelined(pr_ctx *c) {
   pa.partials = c->pipe_partials;
   pa.pstride = c->pipe_pstride;
   pa.wstage = c->pipe_wstage;
+  static const char *trace_path = getenv("PR_PIPE_TRACE");  // debugging: dump the kernel's timeline
+  unsigned long long *d_trace = nullptr;
+  const size_t ntr = (size_t)(c->max_iter + 1) * c->N * 3;
+  if (trace_path && !c->capturing) {
+    CU(cudaMalloc(&d_trace, ntr * sizeof(unsigned long long)));
+    CU(cudaMemsetAsync(d_trace, 0, ntr * sizeof(unsigned long long), c->stream));
+    pa.trace = d_trace;
+  }
   pa.cnt = c->pipe_flags;
   pa.floaded = c->pipe_flags + (size_t)c->B * c->N;
   pa.fdone = c->pipe_flags + (size_t)2 * c->B * c->N;
@@ -808,17 +816,25 @@ pr_status solve_pipelined(pr_ctx *c) {
   if (e != cudaSuccess) return fail(c, PR_ERR_CUDA, fmt("pipelined Parareal launch: %s", cudaGetErrorString(e)));
   c->pipe_ok = 1;
   c->launches++;
-  double *save = c->partials;
-  for (int k = 1; k <= c->max_iter; ++k) {
-    const pr_plan P = make_plan(c->N, 1, 0, k);
-    c->partials = c->pipe_partials + (size_t)k * c->pipe_pstride;
-    const pr_status st = delta_reduce(c, k, P.delta_lo, P.delta_hi, c->nch);
-    if (st) {
-      c->partials = save;
-      return st;
+  if (d_trace) {
+    std::vector<unsigned long long> h(ntr);
+    CU(cudaMemcpyAsync(h.data(), d_trace, ntr * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    cudaFree(d_trace);
+    if (FILE *f = fopen(trace_path, "w")) {
+      for (int k = 0; k <= c->max_iter; ++k)
+        for (int n = 0; n < c->N; ++n)
+          fprintf(f, "%d %d %llu %llu %llu\n", k, n, h[((size_t)k * c->N + n) * 3], h[((size_t)k * c->N + n) * 3 + 1],
+                  h[((size_t)k * c->N + n) * 3 + 2]);
+      fclose(f);
     }
   }
-  c->partials = save;
+  // δ^1..δ^K in one launch (fixed-order sums per row, as delta_reduce)
+  CU(cudaMemsetAsync(c->d_delta, 0, (size_t)c->max_iter * sizeof(unsigned long long), c->stream));
+  const cudaError_t de = pr::launch_delta_multi(c->pipe_partials, c->pipe_pstride, c->B, c->nch, c->N, c->max_iter,
+                                                c->d_delta, c->stream);
+  if (de != cudaSuccess) return fail(c, PR_ERR_CUDA, fmt("delta: %s", cudaGetErrorString(de)));
+  c->launches++;
   return PR_OK;
 }
 
@@ -890,7 +906,8 @@ pr_status solve_impl(pr_ctx *c, const float *V_T, float *V_0, bool device_ptr, p
   const int R = c->world, r = c->rank;
   const size_t row = (size_t)c->B * c->Mp;
   // δ partials are rewritten slice by slice; clear stale chunks of earlier solves
-  CU(cudaMemsetAsync(c->partials, 0, (size_t)(c->Nloc + 1) * c->B * c->nch * 2 * sizeof(double), c->stream));
+  if (!pipe_eligible(c))
+    CU(cudaMemsetAsync(c->partials, 0, (size_t)(c->Nloc + 1) * c->B * c->nch * 2 * sizeof(double), c->stream));
   // ---- k = 0: U_0 and the initial coarse sweep U_{n+1} = G(U_n)
   pt.begin(PH_SETUP);
   if (r == 0 && (st = load_initial(c, V_T, device_ptr))) return st;
@@ -906,6 +923,8 @@ pr_status solve_impl(pr_ctx *c, const float *V_T, float *V_0, bool device_ptr, p
       pt.spans.push_back({PH_COARSE, pt.spans.back().second});  // overlapped: same span for both
     } else if (st != PR_ERR_UNSUPPORTED) {
       return st;
+    } else {  // cannot be co-resident: blocking schedule (its partials were not cleared above)
+      CU(cudaMemsetAsync(c->partials, 0, (size_t)(c->Nloc + 1) * c->B * c->nch * 2 * sizeof(double), c->stream));
     }
   }
   if (!piped) {

@@ -15,9 +15,10 @@
 // the blocking schedule (same kernels' arithmetic, same orders).  The δ partial sums of each
 // iteration go to their own buffer and are reduced after the kernel.
 //
-// Roles: CTAs [0, B·C) run the PINN chain in latency mode (kPinnSplitG threads per point,
-// 128/kPinnSplitG points per CTA, C chunks per instance), CTAs [B·C, B·C + B·N) run one K1
-// system (slice n, instance b) each for all its iterations.  Counters (per instance and slice):
+// Roles: CTAs [0, (K+1)·B·C) run the PINN chain of iteration k = CTA / (B·C) in latency mode
+// (kPinnSplitG threads per point, 128/kPinnSplitG points per CTA, C chunks per instance), the
+// next B·N CTAs one K1 system (slice n, instance b) each for all its iterations.  At each slice
+// the chains pass in iteration order (chain k+1 needs fine(k+1, n), which needs chain k past n).  Counters (per instance and slice):
 //   cnt[b][n]      += 1 by every chain warp of b after it wrote U_{n+1} (or, at its copy step, U_k)
 //   floaded[b][n]  = k after fine(k, n) loaded its input,   fdone[b][n] = k after it stored D_n / F̂
 // Waits are by one thread (ld.acquire) followed by a CTA barrier; data written by other CTAs is
@@ -29,6 +30,11 @@
 
 namespace pr {
 
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 __device__ __forceinline__ int ld_acquire(const int *p) {
   int v;
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -37,10 +43,13 @@ __device__ __forceinline__ int ld_acquire(const int *p) {
 __device__ __forceinline__ void wait_geq(const int *p, int target) {
   while (ld_acquire(p) < target) __nanosleep(20);
 }
-// after a CTA barrier: publish this CTA's stores
+// after a CTA (or warp) barrier: publish the stores of the threads that reached it
 __device__ __forceinline__ void publish_add(int *p) {
   __threadfence();
   atomicAdd(p, 1);
+}
+__device__ __forceinline__ void publish_add_release(int *p) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(p) : "memory");
 }
 __device__ __forceinline__ void publish_set(int *p, int v) {
   __threadfence();
@@ -52,7 +61,7 @@ __device__ __forceinline__ void publish_set(int *p, int v) {
 // staged per warp and folded per CTA, warps in index order, at the end of each iteration — the
 // blocking kernel's summation order, so δ is bitwise the same.
 template <int IN, int ACT>
-__device__ void chain_role(const PipeArgs &pa, int b, int chunk, const float *sw) {
+__device__ void chain_role(const PipeArgs &pa, int k, int b, int chunk, const float *sw) {
   constexpr int G = kPinnSplitG;
   constexpr int NWC = 128 / 32;  // warps per chain CTA
   const PinnArgs &a = pa.g;
@@ -69,7 +78,9 @@ __device__ void chain_role(const PipeArgs &pa, int b, int chunk, const float *sw
   int *cnt = pa.cnt + (size_t)b * pa.N;
   const int *floaded = pa.floaded + (size_t)b * pa.N, *fdone = pa.fdone + (size_t)b * pa.N;
   const int cta = b * pa.C + chunk;
-  // per-warp partial of (row ln): stage[((ln·B·C) + cta)·NWC + wid]·2
+  // per-warp partial of (row ln) in this iteration's staging block:
+  // stage[k][((ln·B·C) + cta)·NWC + wid]·2
+  double *wst = pa.wstage + (size_t)k * (pa.N + 1) * a.B * pa.C * NWC * 2;
   auto stage_partial = [&](int ln, double num, double den) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -77,13 +88,14 @@ __device__ void chain_role(const PipeArgs &pa, int b, int chunk, const float *sw
       den += __shfl_xor_sync(0xffffffffu, den, o);
     }
     if (lane == 0) {
-      double *ps = pa.wstage + ((((size_t)ln * a.B * pa.C) + cta) * NWC + wid) * 2;
+      double *ps = wst + ((((size_t)ln * a.B * pa.C) + cta) * NWC + wid) * 2;
       ps[0] = num;
       ps[1] = den;
     }
   };
-  float u = ok ? __ldcg(a.U + (size_t)b * a.Mp + j) : 0.f;  // U_0 (written before the kernel)
-  for (int k = 0; k <= pa.K; ++k) {
+  float u = 0.f;
+  if (k == 0 && ok) u = __ldcg(a.U + (size_t)b * a.Mp + j);  // U_0 (written before the kernel)
+  {
     int n0 = 0;
     if (k > 0) {
       // U^k_k := F̂^k_{k−1} (copied, reading Q12), with the δ partial of slice k
@@ -110,18 +122,36 @@ __device__ void chain_role(const PipeArgs &pa, int b, int chunk, const float *sw
       if (lane == 0) publish_add(cnt + (k - 1));
       n0 = k;
     }
-    for (int n = n0; n < pa.N; ++n) {
-      if (k > 0 && lane == 0) {
-        wait_geq(fdone + n, k);                               // D_n of this iteration
-        if (n + 1 <= pa.N - 1) wait_geq(floaded + n + 1, k);  // U^{k−1}_{n+1} has been read
+    // slice n's inputs (D_n and the old U_{n+1}) are fetched as soon as their flags are seen set:
+    // for the next slice, speculatively right after this one's stores (a non-blocking check), else
+    // at the top of the next slice (blocking wait)
+    float dn = 0.f, uo = 0.f;
+    bool have = false;
+    auto flags_ready = [&](int n) -> bool {  // lane 0's view, broadcast
+      bool r = true;
+      if (lane == 0) {
+        r = ld_acquire(fdone + n) >= k;
+        if (r && n + 1 <= pa.N - 1) r = ld_acquire(floaded + n + 1) >= k;
       }
-      __syncwarp();
+      return __shfl_sync(0xffffffffu, r ? 1 : 0, 0) != 0;
+    };
+    auto fetch = [&](int n) {
       const size_t row = (size_t)n * sstride + (size_t)b * a.Mp;
-      float dn = 0.f, uo = 0.f;
-      if (k > 0 && ok) {
+      if (ok) {
         dn = __ldcg(a.D + row + j);
         uo = __ldcg(a.U + row + sstride + j);
       }
+    };
+    for (int n = n0; n < pa.N; ++n) {
+      if (k > 0 && !have) {
+        if (lane == 0) {
+          wait_geq(fdone + n, k);                               // D_n of this iteration
+          if (n + 1 <= pa.N - 1) wait_geq(floaded + n + 1, k);  // U^{k−1}_{n+1} has been read
+        }
+        __syncwarp();
+        fetch(n);
+      }
+      const size_t row = (size_t)n * sstride + (size_t)b * a.Mp;
       const int ng = a.n_base + n;
       const float tf = (float)((a.T - ng * a.dT) / a.T), tt = (float)((a.T - (ng + 1) * a.dT) / a.T);
       float x[IN];
@@ -152,14 +182,20 @@ __device__ void chain_role(const PipeArgs &pa, int b, int chunk, const float *sw
       }
       u = nv;
       if (k > 0) stage_partial(n + 1, num, den);
+      have = false;
+      if (k > 0 && n + 1 < pa.N && flags_ready(n + 1)) {
+        fetch(n + 1);
+        have = true;
+      }
       __syncwarp();
-      if (lane == 0) publish_add(cnt + n);
+      if (lane == 0) publish_add_release(cnt + n);
+      if (pa.trace && cta == 0 && threadIdx.x == 0) pa.trace[((size_t)k * pa.N + n) * 3] = gtimer();
     }
     if (k > 0) {  // fold this iteration's per-warp partials, warps in order (the blocking order)
       __syncthreads();
       double *part = pa.partials + (size_t)k * pa.pstride;
       for (int ln = k + (int)threadIdx.x; ln <= pa.N; ln += blockDim.x) {
-        const double *ps = pa.wstage + (((size_t)ln * a.B * pa.C) + cta) * NWC * 2;
+        const double *ps = wst + (((size_t)ln * a.B * pa.C) + cta) * NWC * 2;
         double num = 0.0, den = 0.0;
         for (int q = 0; q < NWC; ++q) { num += ps[2 * q]; den += ps[2 * q + 1]; }
         double *pp = part + (((size_t)ln * a.B + b) * a.nch + chunk) * 2;
@@ -197,6 +233,7 @@ __device__ void fine_role(const PipeArgs &pa, int n, int b) {
     }
     __syncthreads();
     if (t == 0) publish_set(floaded + n, k);
+    if (pa.trace && b == 0 && t == 0) pa.trace[((size_t)k * pa.N + n) * 3 + 1] = gtimer();
     run_steps<P, NT, CN>(tri, a, b, a.n_base + n, t, x, sh, bct);
     if (n == k - 1) {  // F̂_{k−1}: copied into U^k_k by chain k
       float *o = a.Fk + (size_t)b * a.Mp;
@@ -216,17 +253,22 @@ __device__ void fine_role(const PipeArgs &pa, int n, int b) {
     }
     __syncthreads();
     if (t == 0) publish_set(fdone + n, k);
+    if (pa.trace && b == 0 && t == 0) pa.trace[((size_t)k * pa.N + n) * 3 + 2] = gtimer();
   }
 }
 
+// CTAs [0, (K+1)·B·C): the chain of iteration k = blockIdx / (B·C) (each iteration its own CTAs,
+// so chain k+1 runs behind chain k instead of after it); then one CTA per fine system.
 template <int P, bool CN, int IN, int ACT>
 __global__ void __launch_bounds__(128) k_parareal_pipe(PipeArgs pa) {
   extern __shared__ float sw[];
-  const int nchain = pa.g.B * pa.C;
+  const int per = pa.g.B * pa.C;
+  const int nchain = (pa.K + 1) * per;
   if ((int)blockIdx.x < nchain) {
     for (int i = threadIdx.x; i < pa.g.nfloats; i += blockDim.x) sw[i] = pa.g.wts[i];
     __syncthreads();
-    chain_role<IN, ACT>(pa, blockIdx.x / pa.C, blockIdx.x % pa.C, sw);
+    const int k = blockIdx.x / per, r = blockIdx.x % per;
+    chain_role<IN, ACT>(pa, k, r / pa.C, r % pa.C, sw);
   } else {
     const int f = blockIdx.x - nchain;
     fine_role<P, CN>(pa, f / pa.g.B, f % pa.g.B);
@@ -263,7 +305,7 @@ cudaError_t launch_parareal_pipe(const PipeArgs &pa, int M, bool cn, int IN, int
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 128, smem);
   if (e != cudaSuccess) return e;
-  const int grid = pa.g.B * pa.C + pa.g.B * pa.N;
+  const int grid = (pa.K + 1) * pa.g.B * pa.C + pa.g.B * pa.N;
   if (grid > occ * nsm) return cudaErrorCooperativeLaunchTooLarge;
   PipeArgs arg = pa;
   void *params[] = {&arg};
