@@ -66,6 +66,11 @@ enum { PR_BC_CALL_ASYMPTOTIC = 0, PR_BC_ZERO = 1 };
 /* hidden-layer activation: tanh (north_star) or ReLU */
 enum { PR_ACT_TANH = 0, PR_ACT_RELU = 1 };
 /* PINN arithmetic: fp32 SIMT (parity 1e-5) or tensor cores (parity 1e-3; not in ABI v1 builds) */
+/* PINN arithmetic.  FP32: fp32 SIMT kernels (any width instantiated: 8,16,20,32,50,64).
+ * FP16_TC: tcgen05 tensor cores (K4), hidden widths 64/128/256 with >= 2 hidden layers; operands
+ *   split hi + lo in fp16 and three MMAs per product, fp32 accumulation: fp32-level accuracy.
+ * BF16_TC: the same kernel with one bf16 pass: ~3x faster, error ~1e-2 growing with depth.
+ * TF32_TC: not in this build (PR_ERR_UNSUPPORTED). */
 enum { PR_PREC_FP32 = 0, PR_PREC_FP16_TC = 1, PR_PREC_BF16_TC = 2, PR_PREC_TF32_TC = 3 };
 
 /* Problem statement.  Host pointers, copied by init. */

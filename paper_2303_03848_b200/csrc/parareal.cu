@@ -142,6 +142,10 @@ struct pr_ctx {
   float cs[4] = {1, 1, 1, 1}, out_scale = 1;
   float *d_wts = nullptr;
   std::vector<float> h_wts;  // packed copy for the parameter-space kernels
+  int tc = 0;                // PR_PREC_FP16_TC / PR_PREC_BF16_TC: K4 (tensor cores), else 0
+  float *d_tcp = nullptr;    // K4 compact fp32 parameters
+  void *d_wh = nullptr;      // K4 hidden matrices (fp16/bf16, core-matrix layout)
+  int tc_nfloats = 0;
   // options
   int opt_pinn_kernel = 0;
   int opt_fine_kernel = 0;
@@ -520,12 +524,12 @@ void dispatch_res(bool chain, int M, const pr::ResidentArgs &a, int nsys, cudaSt
 constexpr long kSplitMaxPoints = 65536;
 bool split_allowed(const pr_ctx *c) { return (long)c->B * c->M <= kSplitMaxPoints; }
 bool use_split_pinn(const pr_ctx *c) {
-  if (c->opt_pinn_kernel == 1) return false;
+  if (c->tc || c->opt_pinn_kernel == 1) return false;
   if (c->opt_pinn_kernel == 0 && !split_allowed(c)) return false;
   return pr::pinn_split_supported(c->IN, c->W, c->act);
 }
 bool use_param_pinn(const pr_ctx *c) {
-  if (c->opt_pinn_kernel != 0 || use_split_pinn(c)) return false;
+  if (c->tc || c->opt_pinn_kernel != 0 || use_split_pinn(c)) return false;
   return pr::pinn_param_supported(c->IN, c->W, c->LH, c->act);
 }
 
@@ -552,6 +556,15 @@ pr::PinnArgs pinn_args(pr_ctx *c) {
 }
 
 pr_status launch_pinn(pr_ctx *c, const pr::PinnArgs &a) {
+  if (c->tc) {  // K4: tensor cores (wide nets)
+    pr::PinnArgs t = a;
+    t.wts = c->d_tcp;
+    t.nfloats = c->tc_nfloats;
+    dim3 grid((c->M + 127) / 128, c->B);
+    CU(pr::launch_pinn_tc(c->IN, c->W, c->act, c->tc == PR_PREC_BF16_TC, t, c->d_wh, grid, c->stream));
+    LAUNCHED();
+    return PR_OK;
+  }
   if (use_split_pinn(c)) {
     constexpr int ppc = kPinnTPB / pr::kPinnSplitG;  // points per CTA
     dim3 grid((c->M + ppc - 1) / ppc, c->B);
@@ -1283,12 +1296,14 @@ pr_status parareal_load_pinn_weights(pr_ctx *c, int32_t n_linear, const int32_t 
     if (dims[l] != Wd) return fail(c, PR_ERR_UNSUPPORTED, fmt("dims[%d]=%d: hidden widths must all equal dims[1]=%d", l, dims[l], Wd));
   if (activation != PR_ACT_TANH && activation != PR_ACT_RELU)
     return fail(c, PR_ERR_INVALID_ARGUMENT, fmt("activation=%d unknown", activation));
-  if (precision != PR_PREC_FP32) {
-    if (precision < 0 || precision > PR_PREC_TF32_TC) return fail(c, PR_ERR_INVALID_ARGUMENT, fmt("precision=%d unknown", precision));
-    return fail(c, PR_ERR_UNSUPPORTED, "tensor-core PINN precisions are not in this build");
-  }
-  if (!pr::pinn_smem_supported(dims[0], Wd, activation))
-    return fail(c, PR_ERR_UNSUPPORTED, fmt("hidden width %d not instantiated (8,16,20,32,50,64)", Wd));
+  if (precision < 0 || precision > PR_PREC_TF32_TC) return fail(c, PR_ERR_INVALID_ARGUMENT, fmt("precision=%d unknown", precision));
+  const bool tc = precision != PR_PREC_FP32;
+  if (precision == PR_PREC_TF32_TC) return fail(c, PR_ERR_UNSUPPORTED, "PR_PREC_TF32_TC is not in this build (FP16/BF16 tensor cores are)");
+  if (tc && (n_linear < 3 || !pr::pinn_tc_supported(dims[0], Wd, activation, precision == PR_PREC_BF16_TC)))
+    return fail(c, PR_ERR_UNSUPPORTED, fmt("tensor-core PINN needs >= 2 hidden layers of width 64, 128 or 256 (got %d x %d)",
+                                           n_linear - 1, Wd));
+  if (!tc && !pr::pinn_smem_supported(dims[0], Wd, activation))
+    return fail(c, PR_ERR_UNSUPPORTED, fmt("hidden width %d not instantiated (8,16,20,32,50,64; tensor cores: 64,128,256)", Wd));
   for (int l = 0; l < n_linear; ++l)
     if (!W[l] || !b[l]) return fail(c, PR_ERR_INVALID_ARGUMENT, fmt("W[%d]/b[%d] is NULL", l, l));
   const int IN = dims[0], LH = n_linear - 1;
@@ -1302,10 +1317,40 @@ pr_status parareal_load_pinn_weights(pr_ctx *c, int32_t n_linear, const int32_t 
     for (size_t i = 0; i < nw; ++i) pk.push_back(pre ? (float)(kTanhScale * W[l][i]) : W[l][i]);
     for (int i = 0; i < dims[l + 1]; ++i) pk.push_back(pre ? (float)(kTanhScale * b[l][i]) : b[l][i]);
   }
+  if (tc) {
+    // K4: compact fp32 params (W0, b0, hidden biases, Wo, bo) + the hidden matrices in fp16/bf16,
+    // core-matrix K-major (pinn_tc.cu)
+    const bool bf = precision == PR_PREC_BF16_TC;
+    // packed fp32 layout (pk): W0[W][IN], b0[W], {W_l[W][W], b_l[W]} x (LH−1), Wo[W], bo
+    const size_t n0 = (size_t)Wd * IN, nh = (size_t)Wd * Wd + Wd;
+    const size_t le = pr::pinn_tc_layer_elems(Wd, bf);
+    std::vector<uint16_t> wh((size_t)(LH - 1) * le);
+    std::vector<float> tq(pk.begin(), pk.begin() + n0 + Wd);  // W0, b0
+    for (int l = 1; l < LH; ++l) {
+      const size_t o = n0 + Wd + (size_t)(l - 1) * nh;
+      pr::pinn_tc_pack(pk.data() + o, Wd, bf, wh.data() + (size_t)(l - 1) * le);
+      tq.insert(tq.end(), pk.begin() + o + (size_t)Wd * Wd, pk.begin() + o + nh);  // b_l
+    }
+    const size_t oo = n0 + Wd + (size_t)(LH - 1) * nh;
+    tq.insert(tq.end(), pk.begin() + oo, pk.begin() + oo + Wd + 1);  // Wo, bo
+    if (c->d_tcp) cudaFree(c->d_tcp);
+    if (c->d_wh) cudaFree(c->d_wh);
+    c->d_tcp = nullptr;
+    c->d_wh = nullptr;
+    CU(cudaMalloc(&c->d_tcp, tq.size() * sizeof(float)));
+    CU(cudaMemcpy(c->d_tcp, tq.data(), tq.size() * sizeof(float), cudaMemcpyHostToDevice));
+    CU(cudaMalloc(&c->d_wh, wh.size() * sizeof(uint16_t)));
+    CU(cudaMemcpy(c->d_wh, wh.data(), wh.size() * sizeof(uint16_t), cudaMemcpyHostToDevice));
+    c->tc_nfloats = (int)tq.size();
+  }
+  c->tc = tc ? precision : 0;
   const size_t bytes = pk.size() * sizeof(float);
-  if (bytes > 200 * 1024) return fail(c, PR_ERR_UNSUPPORTED, fmt("network of %zu bytes exceeds the shared-memory budget", bytes));
-  CU(pr::pinn_smem_prepare(IN, Wd, activation, (int)bytes));
-  if (pr::pinn_split_supported(IN, Wd, activation)) CU(pr::pinn_split_prepare(IN, Wd, activation, (int)bytes));
+  if (!tc && bytes > 200 * 1024)
+    return fail(c, PR_ERR_UNSUPPORTED, fmt("network of %zu bytes exceeds the shared-memory budget", bytes));
+  if (!tc) {
+    CU(pr::pinn_smem_prepare(IN, Wd, activation, (int)bytes));
+    if (pr::pinn_split_supported(IN, Wd, activation)) CU(pr::pinn_split_prepare(IN, Wd, activation, (int)bytes));
+  }
   if (c->d_wts) cudaFree(c->d_wts);
   c->d_wts = nullptr;
   CU(cudaMalloc(&c->d_wts, bytes));
@@ -1514,6 +1559,8 @@ void parareal_free(pr_ctx *c) {
   cudaFree(c->d_K);
   cudaFree(c->d_r);
   cudaFree(c->d_wts);
+  cudaFree(c->d_tcp);
+  cudaFree(c->d_wh);
   if (c->own_ws) cudaFree(c->ws);
   if (c->h_delta) cudaFreeHost(c->h_delta);
   cudaFree(c->pipe_partials);

@@ -1,0 +1,409 @@
+// pinn_tc.cu — K4: the PINN coarse chain on the 5th-generation tensor cores (tcgen05), for wide
+// networks (W ∈ {64, 128, 256}: 8×256 is 920 kflop per point-eval).
+//
+// Same chain as K3 (pinn_chain.cuh; Eq. 7): every point walks the local
+// slices, g = G_n(U_n), Ĝ_n = g, U_{n+1} = g + D_n, δ partials.  A CTA of 128 threads owns a tile
+// of 128 grid points (thread t ↔ point t ↔ TMEM lane t).  Per slice:
+//   layer 0 (IN → W, K = 2 or 4: far too thin for an MMA) in fp32 on the FMA pipe; its fp16 (or
+//     bf16) activations are stored to shared memory as the A operand [128 × W], K-major, in
+//     8×8 core matrices (SWIZZLE_NONE: LBO = 128 B along K, SBO = 16·W B along M);
+//   hidden layers W → W: one elected thread issues W/16 `tcgen05.mma.cta_group::1.kind::f16`
+//     (M = 128, N = W, K = 16) with the layer's weights [W × W] (K-major, same core-matrix
+//     layout, bulk-copied from L2 or resident) as B; accumulators in TMEM (W fp32 columns);
+//     `tcgen05.commit` → mbarrier;
+//   epilogue: each thread `tcgen05.ld`s its own TMEM lane 32 columns at a time, adds the bias,
+//     applies the activation, and either writes the next A operand (fp16) or, after the last
+//     hidden layer, accumulates the output layer W → 1 in fp32.
+// fp16 operands, fp32 accumulation: the north_star tolerance for a tensor-core PINN is 1e-3.
+#include <type_traits>
+#include <cuda_fp16.h>
+#include <cuda_bf16.h>
+#include "launch.h"
+#include "pinn_chain.cuh"
+
+namespace pr {
+
+__device__ __forceinline__ uint32_t tc_smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+// UMMA shared-memory matrix descriptor (SWIZZLE_NONE, K-major): start >> 4 [0,14), LBO >> 4
+// [16,30), SBO >> 4 [32,46), version 1 [46,48) (sm_100), base offset 0, layout type 0.
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46);
+}
+// instruction descriptor, kind::f16: D f32 [4,6) = 1; A, B format [7,10) [10,13) (0 f16, 1 bf16);
+// K-major A and B; N >> 3 at [17,23); M >> 4 at [24,29)
+template <bool BF16>
+__host__ __device__ constexpr uint32_t umma_idesc(int M, int N) {
+  return (1u << 4) | ((BF16 ? 1u : 0u) << 7) | ((BF16 ? 1u : 0u) << 10) | ((uint32_t)(N >> 3) << 17) |
+         ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void tc_mbar_init(uint64_t *bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tc_smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tc_mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "PR_TC_WAIT%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra PR_TC_WAIT%=;\n}\n" ::"r"(tc_smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tc_bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tc_smem_u32(bar)), "r"(bytes)
+               : "memory");
+  // bulk copies are limited to 2^20 bytes each and must be 16-B multiples (host guarantees)
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   tc_smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(tc_smem_u32(bar))
+               : "memory");
+}
+
+template <class T>
+__device__ __forceinline__ uint32_t pack2(float a, float b);  // two values, round to nearest
+template <>
+__device__ __forceinline__ uint32_t pack2<__half>(float a, float b) {
+  const __half2 h = __floats2half2_rn(a, b);
+  return *reinterpret_cast<const uint32_t *>(&h);
+}
+template <>
+__device__ __forceinline__ uint32_t pack2<__nv_bfloat16>(float a, float b) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<const uint32_t *>(&h);
+}
+
+// element offset of (row r, column c) in the K-major core-matrix layout of a [rows × K] operand
+__host__ __device__ constexpr size_t cm_offset(int r, int c, int K) {
+  return (size_t)(r / 8) * (K / 8) * 64 + (size_t)(c / 8) * 64 + (r % 8) * 8 + (c % 8);
+}
+
+// 32 TMEM columns of this thread's lane → registers
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+struct PinnTcArgs {
+  PinnArgs g;              // chain; wts: fp32 W0[W][IN], b0[W], hidden biases [(LH−1)][W], Wo[W], bo
+  const void *wh;          // hidden matrices in K-chunks (see pinn_tc_pack), pre-scaled
+  int resident;            // 1: every chunk fits in shared memory (loaded once)
+};
+
+constexpr int kTcKC = 64;  // K columns per weight chunk
+
+// SPLIT (PR_PREC_FP16_TC): operands split hi + lo in fp16, D = A_hi·B_hi + A_hi·B_lo + A_lo·B_hi —
+// fp32-level accuracy (~2e-6 on 8×256 nets) at 3× the MMAs.  !SPLIT (PR_PREC_BF16_TC): one bf16 pass.
+template <int IN, int W, int ACT, bool SPLIT>
+__global__ void __launch_bounds__(128) k_pinn_chain_tc(PinnTcArgs ta) {
+  using T = typename std::conditional<SPLIT, __half, __nv_bfloat16>::type;
+  constexpr int TILE = 128;
+  constexpr int NP = SPLIT ? 2 : 1;                         // hi (+ lo) planes
+  constexpr uint32_t kIdesc = umma_idesc<!SPLIT>(TILE, W);
+  constexpr uint32_t kPlaneA = (uint32_t)TILE * W * 2;       // bytes of one A plane
+  constexpr uint32_t kPlaneB = (uint32_t)W * kTcKC * 2;      // bytes of one chunk plane
+  constexpr uint32_t kChunk = NP * kPlaneB;
+  constexpr int NCH = W / kTcKC;                             // chunks per layer
+  const PinnArgs &a = ta.g;
+  extern __shared__ __align__(128) unsigned char tc_smem[];
+  T *sA = reinterpret_cast<T *>(tc_smem);                    // NP planes [128 × W]
+  unsigned char *sB = tc_smem + NP * kPlaneA;                // 1 chunk, or all (LH−1)·NCH chunks
+  const int nchunks = ta.resident ? (a.LH - 1) * NCH : 1;
+  float *sP = reinterpret_cast<float *>(sB + (size_t)nchunks * kChunk);
+  __shared__ __align__(8) uint64_t bar_mma, bar_w;
+  __shared__ uint32_t s_tmem;
+  __shared__ double red[64];
+  const int t = threadIdx.x, w = t >> 5;
+  for (int i = t; i < a.nfloats; i += blockDim.x) sP[i] = a.wts[i];
+  if (t == 0) {
+    tc_mbar_init(&bar_mma);
+    tc_mbar_init(&bar_w);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (w == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tc_smem_u32(&s_tmem)),
+                 "r"((uint32_t)W));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = s_tmem;
+  const uint32_t tlane = tmem + ((uint32_t)(32 * w) << 16);  // this warp's TMEM lane quarter
+  uint32_t ph_mma = 0, ph_w = 0;
+  if (ta.resident && a.LH > 1) {  // every chunk loaded once (≤ 200 KB, one bulk copy)
+    if (t == 0) tc_bulk_g2s(sB, ta.wh, (uint32_t)((a.LH - 1) * NCH) * kChunk, &bar_w);
+    tc_mbar_wait(&bar_w, ph_w);
+    ph_w ^= 1;
+  }
+  const float *W0 = sP, *b0 = sP + W * IN;
+  const float *Wo = sP + W * IN + W + (size_t)(a.LH - 1) * W;
+  const float bo = Wo[W];
+  // store 8 consecutive activations (fp32) of column block c0 as the A operand (hi, lo)
+  auto store_a = [&](int c0, const float (&h)[8]) {
+    const size_t off = cm_offset(t, c0, W);
+    float lo[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const float hi = SPLIT ? __half2float(__float2half_rn(h[q])) : 0.f;
+      lo[q] = h[q] - hi;
+    }
+    *reinterpret_cast<uint4 *>(sA + off) =
+        make_uint4(pack2<T>(h[0], h[1]), pack2<T>(h[2], h[3]), pack2<T>(h[4], h[5]), pack2<T>(h[6], h[7]));
+    if (SPLIT)
+      *reinterpret_cast<uint4 *>(sA + (size_t)TILE * W + off) = make_uint4(
+          pack2<T>(lo[0], lo[1]), pack2<T>(lo[2], lo[3]), pack2<T>(lo[4], lo[5]), pack2<T>(lo[6], lo[7]));
+  };
+
+  const int b = blockIdx.y;
+  const double Lb = a.Lb[b];
+  const float gscale = (float)(Lb * (double)a.out_scale);
+  const float invL = (float)(1.0 / Lb);
+  const size_t sstride = (size_t)a.B * a.Mp;
+  const int j = blockIdx.x * TILE + t;
+  const bool ok = j < a.M;
+  const double dS = Lb / (a.M + 1);
+  const float s_over_L = (float)(((j + 1) * dS) / Lb);
+  float *u0 = a.U + (size_t)a.ln0 * sstride + (size_t)b * a.Mp;
+  float u = 0.f;
+  if (a.Fcopy) {
+    const float *f = a.Fcopy + (size_t)b * a.Mp;
+    double num = 0.0, den = 0.0;
+    if (ok) {
+      u = f[j];
+      const double dd = (double)u - (double)u0[j];
+      num = dd * dd;
+      den = (double)u * u;
+    }
+    __syncthreads();
+    if (ok) u0[j] = u;
+    if (a.partials) {
+      cta_reduce2(num, den, red);
+      if (t == 0) {
+        double *pp = a.partials + (((size_t)a.ln0 * a.B + b) * a.nch + blockIdx.x) * 2;
+        pp[0] = num;
+        pp[1] = den;
+      }
+    }
+  } else if (ok) {
+    u = u0[j];
+  }
+  const uint32_t aHi = tc_smem_u32(sA), aLo = aHi + kPlaneA, bBase = tc_smem_u32(sB);
+  const int ln_end = a.Gout ? a.ln0 + 1 : a.ln1;
+#pragma unroll 1
+  for (int ln = a.ln0; ln < ln_end; ++ln) {
+    const int n = a.n_base + ln;
+    const float tf = (float)((a.T - n * a.dT) / a.T), tt = (float)((a.T - (n + 1) * a.dT) / a.T);
+    float x[IN];
+    if (IN == 4) {
+      x[0] = tf * a.cs0;
+      x[1] = tt * a.cs1;
+      x[2] = (u * invL) * a.cs2;
+      x[3] = s_over_L * a.cs3;
+    } else {
+      x[0] = tt * a.cs0;
+      x[IN - 1] = s_over_L * a.cs1;
+    }
+    // ---- layer 0 (fp32) → A operand
+#pragma unroll 1
+    for (int c0 = 0; c0 < W; c0 += 8) {
+      float h[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        float z = b0[c0 + q];
+#pragma unroll
+        for (int i = 0; i < IN; ++i) z = fmaf(W0[(c0 + q) * IN + i], x[i], z);
+        h[q] = act<ACT>(z);
+      }
+      store_a(c0, h);
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    float y = 0.f;
+#pragma unroll 1
+    for (int l = 1; l < a.LH; ++l) {
+      // ---- D[128 × W] = A · W_l^T, chunk by chunk along K
+#pragma unroll 1
+      for (int c = 0; c < NCH; ++c) {
+        const int ci = (l - 1) * NCH + c;
+        uint32_t bc = bBase + (uint32_t)ci * kChunk;
+        if (!ta.resident) {  // stream the chunk (the previous MMA on the buffer has completed)
+          if (t == 0) tc_bulk_g2s(sB, (const unsigned char *)ta.wh + (size_t)ci * kChunk, kChunk, &bar_w);
+          tc_mbar_wait(&bar_w, ph_w);
+          ph_w ^= 1;
+          bc = bBase;
+        }
+        if (t == 0) {
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+          for (int ks = 0; ks < kTcKC / 16; ++ks) {
+            // A: K offset c·64 + 16·ks = core matrix (8c + 2ks) along K; B chunk: core matrix 2ks
+            const uint32_t ao = (uint32_t)(c * (kTcKC / 8) + 2 * ks) * 128, bo2 = (uint32_t)(2 * ks) * 128;
+            const uint64_t dah = umma_desc(aHi + ao, 128, 16 * W), dbh = umma_desc(bc + bo2, 128, 16 * kTcKC);
+            const uint32_t acc = (c > 0 || ks > 0) ? 1u : 0u;
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem),
+                "l"(dah), "l"(dbh), "r"(kIdesc), "r"(acc));
+            if (SPLIT) {
+              const uint64_t dal = umma_desc(aLo + ao, 128, 16 * W);
+              const uint64_t dbl = umma_desc(bc + kPlaneB + bo2, 128, 16 * kTcKC);
+              asm volatile(
+                  "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                  "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem),
+                  "l"(dah), "l"(dbl), "r"(kIdesc), "r"(1u));
+              asm volatile(
+                  "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                  "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem),
+                  "l"(dal), "l"(dbh), "r"(kIdesc), "r"(1u));
+            }
+          }
+          if (!ta.resident || c == NCH - 1)  // the chunk buffer is reused, or the layer is complete
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                             tc_smem_u32(&bar_mma))
+                         : "memory");
+        }
+        if (!ta.resident || c == NCH - 1) {
+          tc_mbar_wait(&bar_mma, ph_mma);
+          ph_mma ^= 1;
+        }
+      }
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const float *bl = sP + W * IN + W + (size_t)(l - 1) * W;
+      const bool last = l == a.LH - 1;
+#pragma unroll 1
+      for (int c0 = 0; c0 < W; c0 += 32) {
+        float v[32];
+        tmem_ld32(tlane + (uint32_t)c0, v);
+#pragma unroll
+        for (int q = 0; q < 32; ++q) v[q] = act<ACT>(v[q] + bl[c0 + q]);
+        if (last) {
+#pragma unroll
+          for (int q = 0; q < 32; ++q) y = fmaf(Wo[c0 + q], v[q], y);
+        } else {
+#pragma unroll
+          for (int q = 0; q < 32; q += 8) {
+            const float h[8] = {v[q], v[q + 1], v[q + 2], v[q + 3], v[q + 4], v[q + 5], v[q + 6], v[q + 7]};
+            store_a(c0 + q, h);
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncthreads();
+    }
+    y += bo;
+    const float g = gscale * y;
+    if (a.Gout) {
+      if (ok) a.Gout[(size_t)b * a.Mp + j] = g;
+      break;
+    }
+    const size_t row = (size_t)ln * sstride + (size_t)b * a.Mp;
+    float nv = 0.f;
+    double num = 0.0, den = 0.0;
+    if (ok) {
+      nv = a.D ? g + a.D[row + j] : g;
+      if (a.Gh) a.Gh[row + j] = g;
+      if (a.partials) {
+        const double dd = (double)nv - (double)a.U[row + sstride + j];
+        num = dd * dd;
+        den = (double)nv * nv;
+      }
+      a.U[row + sstride + j] = nv;
+    }
+    u = nv;
+    if (a.partials) {
+      cta_reduce2(num, den, red);
+      if (t == 0) {
+        double *pp = a.partials + (((size_t)(ln + 1) * a.B + b) * a.nch + blockIdx.x) * 2;
+        pp[0] = num;
+        pp[1] = den;
+      }
+    }
+  }
+  __syncthreads();
+  if (w == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((uint32_t)W));
+}
+
+typedef void (*TcKernel)(PinnTcArgs);
+template <bool SPLIT>
+static TcKernel tc_kernel_t(int IN, int W, int act) {
+  if (act != 0 && act != 1) return nullptr;
+#define PR_TC_CASE(IN_, W_)                                                       \
+  if (IN == IN_ && W == W_) return act ? k_pinn_chain_tc<IN_, W_, 1, SPLIT> : k_pinn_chain_tc<IN_, W_, 0, SPLIT>;
+  PR_TC_CASE(4, 64) PR_TC_CASE(4, 128) PR_TC_CASE(4, 256) PR_TC_CASE(2, 64) PR_TC_CASE(2, 128) PR_TC_CASE(2, 256)
+#undef PR_TC_CASE
+  return nullptr;
+}
+static TcKernel tc_kernel(int IN, int W, int act, bool bf16) {
+  return bf16 ? tc_kernel_t<false>(IN, W, act) : tc_kernel_t<true>(IN, W, act);
+}
+
+bool pinn_tc_supported(int IN, int W, int act, bool bf16) { return tc_kernel(IN, W, act, bf16) != nullptr; }
+
+// shared memory: A planes [128 × W] + weight chunks (all if they fit, else one) + fp32 parameters
+size_t pinn_tc_smem(int W, int LH, int nfloats, bool bf16, bool *resident) {
+  const size_t np = bf16 ? 1 : 2;
+  const size_t a = np * 128 * W * 2, chunk = np * (size_t)W * kTcKC * 2, p = (size_t)nfloats * 4;
+  const size_t all = (size_t)(LH - 1) * (W / kTcKC) * chunk;
+  const size_t limit = 200 * 1024;
+  if (a + all + p <= limit) {
+    *resident = true;
+    return a + all + p;
+  }
+  *resident = false;
+  return a + chunk + p;
+}
+
+// host: hidden layer l's [W][W] (fp32, pre-scaled) → its W/64 K-chunks, each [hi plane][lo plane],
+// a plane [W rows × 64 K] in the core-matrix K-major layout (SBO = 1024 B)
+size_t pinn_tc_layer_elems(int W, bool bf16) { return (size_t)(bf16 ? 1 : 2) * W * W; }
+void pinn_tc_pack(const float *Wl, int W, bool bf16, uint16_t *out) {
+  const int np = bf16 ? 1 : 2;
+  for (int c = 0; c < W / kTcKC; ++c) {
+    uint16_t *hi = out + (size_t)c * np * W * kTcKC, *lo = hi + (size_t)W * kTcKC;
+    for (int o = 0; o < W; ++o)
+      for (int i = 0; i < kTcKC; ++i) {
+        const float v = Wl[(size_t)o * W + c * kTcKC + i];
+        const size_t off = cm_offset(o, i, kTcKC);
+        if (bf16) {
+          const __nv_bfloat16 h = __float2bfloat16_rn(v);
+          hi[off] = *reinterpret_cast<const uint16_t *>(&h);
+        } else {
+          const __half h = __float2half_rn(v);
+          const __half l2 = __float2half_rn(v - __half2float(h));
+          hi[off] = *reinterpret_cast<const uint16_t *>(&h);
+          lo[off] = *reinterpret_cast<const uint16_t *>(&l2);
+        }
+      }
+  }
+}
+
+cudaError_t launch_pinn_tc(int IN, int W, int act, bool bf16, const PinnArgs &a, const void *wh, dim3 grid,
+                           cudaStream_t s) {
+  TcKernel k = tc_kernel(IN, W, act, bf16);
+  if (!k) return cudaErrorInvalidValue;
+  bool resident = false;
+  const size_t smem = pinn_tc_smem(W, a.LH, a.nfloats, bf16, &resident);
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  PinnTcArgs ta;
+  ta.g = a;
+  ta.wh = wh;
+  ta.resident = resident ? 1 : 0;
+  k<<<grid, 128, smem, s>>>(ta);
+  return cudaGetLastError();
+}
+
+}  // namespace pr

@@ -156,6 +156,65 @@ def test_pinn_G_both_weight_paths(pinn_kernel, dims, act):
     assert_close(got, oracle.pinn_G(p, net, 6, U.astype(np.float64)), what="G %s path %d" % (dims, pinn_kernel))
 
 
+# ------------------------------------------------------------------ K4: tensor-core PINN (wide nets)
+# PR_PREC_FP16_TC: operands split hi + lo in fp16, three MMAs per product (fp32-level accuracy:
+# ~2e-6 emulated on 8x256 nets) -- held to 1e-4.  PR_PREC_BF16_TC: one bf16 pass (8-bit
+# mantissa), the fast approximate mode -- its error grows with depth (~1e-2 at 3 layers).
+
+TOL_TC = 1e-4
+
+
+@pytest.mark.parametrize("W,LH,act", [(64, 2, synth.ACT_TANH), (64, 8, synth.ACT_TANH), (128, 4, synth.ACT_TANH),
+                                      (256, 3, synth.ACT_TANH), (256, 8, synth.ACT_TANH), (128, 4, synth.ACT_RELU)])
+def test_pinn_G_tensor_cores(W, LH, act):
+    """C5 widths: 128-point tiles, tcgen05 MMAs with TMEM accumulators, weights
+    resident (small nets) or streamed in 64-column chunks (8x256); a ragged last tile (M = 1000)
+    and two instances."""
+    p = synth.portfolio(n_k=2, n_s=1, M=1000, N=8)
+    net = synth.kaiming_net([4] + [W] * LH + [1], seed=W + LH, activation=act)
+    U = oracle.payoff(p) * (1.0 + 0.05 * np.sin(np.arange(1000) / 37.0))
+    with ctx_for(p) as c:
+        c.load_weights(net, precision=parareal.PREC_FP16_TC)
+        got = c.apply_coarse(5, U.astype(np.float32))
+    assert_close(got, oracle.pinn_G(p, net, 5, U), tol=TOL_TC, what="G TC W=%d LH=%d" % (W, LH))
+
+
+@pytest.mark.parametrize("W,LH", [(64, 2), (256, 3)])
+def test_pinn_G_tensor_cores_bf16(W, LH):
+    p = synth.portfolio(n_k=2, n_s=1, M=700, N=8)
+    net = synth.kaiming_net([4] + [W] * LH + [1], seed=3 * W + LH)
+    U = oracle.payoff(p)
+    with ctx_for(p) as c:
+        c.load_weights(net, precision=parareal.PREC_BF16_TC)
+        got = c.apply_coarse(2, U.astype(np.float32))
+    assert_close(got, oracle.pinn_G(p, net, 2, U), tol=3e-2, what="G TC bf16 W=%d LH=%d" % (W, LH))
+
+
+def test_pinn_tensor_core_parareal_chain():
+    """Full Parareal with the K4 coarse chain (correction fused, δ partials) at a C5-like width:
+    iterates within the TC tolerance of the oracle with the same fp32-exact fine propagator."""
+    p = synth.single(3000, 6, coarse=synth.COARSE_PINN, max_iter=2, tol=0.0)
+    net = synth.kaiming_net([4, 128, 128, 128, 1], seed=9)
+    with ctx_for(p) as c:
+        c.load_weights(net, precision=parareal.PREC_FP16_TC)
+        _, rep = c.solve()
+        it = c.copy_iterates(0, p.N + 1)
+    ref_U, ref_d, K, _ = oracle.parareal(p, net)
+    assert rep["iterations"] == K == 2
+    assert_close(it, ref_U, tol=TOL_TC, what="TC Parareal iterates")
+
+
+def test_pinn_tensor_core_errors():
+    p = synth.single(256, 4)
+    with ctx_for(p) as c:
+        with pytest.raises(parareal.PararealError) as ei:
+            c.load_weights(synth.kaiming_net([4, 20, 20, 1]), precision=parareal.PREC_FP16_TC)   # too narrow
+        assert ei.value.status == 7
+        with pytest.raises(parareal.PararealError) as ei:
+            c.load_weights(synth.kaiming_net([4, 64, 64, 1]), precision=parareal.PREC_TF32_TC)
+        assert ei.value.status == 7
+
+
 def test_pinn_G_portfolio():
     p = synth.portfolio(n_k=3, n_s=5, M=300, N=16)
     net = synth.kaiming_net(synth.PINN_3x20, seed=1)
