@@ -46,6 +46,10 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-c3-sweep", action="store_true", help="skip the C3 fine-sweep HBM roofline leg")
     ap.add_argument("--no-graphs", action="store_true", help="eager launches instead of the captured CUDA graph")
+    ap.add_argument("--pinn-width", type=int, default=20, help="PINN hidden width (C5 sweep: 20/64/256)")
+    ap.add_argument("--pinn-layers", type=int, default=3, help="PINN hidden layers")
+    ap.add_argument("--pinn-prec", default="fp32", choices=["fp32", "fp16tc", "bf16tc"],
+                    help="PINN arithmetic: fp32 SIMT, split-fp16 tensor cores (fp32-level accuracy), bf16 tensor cores")
     ap.add_argument("--fine-theta", type=float, default=1.0,
                     help="fine theta-step: 1 implicit Euler (default, reading Q1), 0.5 Crank-Nicolson (NEXT-1)")
     return ap.parse_args()
@@ -61,6 +65,13 @@ def problem_for(args):
 def work_units(p) -> float:
     """Grid-point-steps of the problem: B·M·N·n_f (the serial fine solve's point-steps)."""
     return float(p.B) * p.M * p.N * p.fine_steps
+
+
+PREC_CODE = {"fp32": 0, "fp16tc": 1, "bf16tc": 2}
+
+
+def pinn_dims(args):
+    return [4] + [args.pinn_width] * args.pinn_layers + [1]
 
 
 def pinn_flops(dims) -> float:
@@ -142,8 +153,8 @@ def run_reference(args):
         return 0
     from paper_2303_03848_b200 import synth
     p = problem_for(args)
-    net = synth.kaiming_net(synth.PINN_3x20, seed=0) if p.coarse == synth.COARSE_PINN else None
-    import oracle
+    net = synth.kaiming_net(pinn_dims(args), seed=0) if p.coarse == synth.COARSE_PINN else None
+    import oracle  # (the oracle evaluates the net in fp64 whatever --pinn-prec says)
     for _ in range(max(0, min(args.warmup, 1))):
         oracle.parareal(p, net)
     per, runs, cores = cpu_oracle_run(p, net, budget_s=1e9, max_runs=max(1, args.steps))
@@ -165,7 +176,8 @@ def config_dict(args, p):
                         "steps/slice, %s coarse, K=%d fixed iterations" % (
                             args.config, p.M, p.N, p.B, p.fine_steps,
                             "IE" if p.fine_theta == 1.0 else ("CN" if p.fine_theta == 0.5 else "theta=%g" % p.fine_theta),
-                            "PINN [4,20,20,20,1] tanh" if args.coarse == "pinn" else "implicit-Euler (1 step/slice)",
+                            ("PINN %s tanh (%s)" % (pinn_dims(args), args.pinn_prec)) if args.coarse == "pinn"
+                            else "implicit-Euler (1 step/slice)",
                             p.max_iter),
             "M": p.M, "N": p.N, "B": p.B, "fine_steps": p.fine_steps, "fine_theta": p.fine_theta, "K": p.max_iter,
             "coarse": args.coarse, "parallelism": "time-slices/%d" % args.gpus,
@@ -188,7 +200,7 @@ def ncu_traffic(kernel_prefix):
     return None
 
 
-def roofline(p, ph, K, world, rank, pk, pk_src, clk_mhz, n_sm, synth):
+def roofline(p, ph, K, world, rank, pk, pk_src, clk_mhz, n_sm, synth, dims=None, tc_prec=None):
     """Roofline of the step's dominant kernel (DESIGN.md §6 work per unit)."""
     nloc = p.N // world
     if ph["ms_fine"] >= ph["ms_coarse"]:
@@ -215,12 +227,23 @@ def roofline(p, ph, K, world, rank, pk, pk_src, clk_mhz, n_sm, synth):
     else:
         evals = float(p.B) * p.M * nloc
         chain_s = ph["ms_coarse"] / (K + 1) / 1e3
-        if p.coarse == synth.COARSE_PINN:
+        if p.coarse == synth.COARSE_PINN and tc_prec:
+            fl = pinn_flops(dims)
+            roof = {"kernel": "k_pinn_chain_tc (K4, tcgen05 %s)" % tc_prec, "bound": "tensor",
+                    "achieved": fl * evals / chain_s / 1e12,
+                    "peak": float(pk["bf16_tflops"]), "unit": "TFLOP/s",
+                    "peak_source": "measured dense bf16 (fp16 runs at the bf16 rate)",
+                    "work_per_unit": "%.0f algorithmic flop per point-eval (the split-fp16 mode issues 3x)" % fl,
+                    "launch_unit": "one coarse chain"}
+            tr = ncu_traffic("k_pinn_chain_tc")
+        elif p.coarse == synth.COARSE_PINN:
+            fl = pinn_flops(dims)
             roof = {"kernel": "k_pinn_chain* (K3, fp32 SIMT)", "bound": "alu",
-                    "achieved": pinn_flops(synth.PINN_3x20) * evals / chain_s / 1e12,
+                    "achieved": fl * evals / chain_s / 1e12,
                     "peak": n_sm * 128 * 2 * clk_mhz * 1e6 / 1e12, "unit": "TFLOP/s",
                     "peak_source": "fp32 FMA pipe: %d SMs x 128 FMA/clk x 2 x %.0f MHz (DESIGN.md)" % (n_sm, clk_mhz),
-                    "work_per_unit": "1760 flop + 60 tanh per point-eval", "launch_unit": "one coarse chain"}
+                    "work_per_unit": "%.0f flop + %d tanh per point-eval" % (fl, sum(dims[1:-1])),
+                    "launch_unit": "one coarse chain"}
             tr = ncu_traffic("k_pinn_chain")
         else:
             roof = {"kernel": "k_resident_chain (numerical G, fp64)", "bound": "alu",
@@ -283,7 +306,7 @@ def main():
     p = problem_for(args)
     if p.N % world:
         raise SystemExit("N=%d not divisible by %d GPUs" % (p.N, world))
-    net = synth.kaiming_net(synth.PINN_3x20, seed=0)
+    net = synth.kaiming_net(pinn_dims(args), seed=0)
     nccl_id = None
     if world > 1:
         obj = [parareal.get_nccl_id() if rank == 0 else None]
@@ -292,7 +315,7 @@ def main():
     stream = torch.cuda.current_stream()
     ctx = parareal.Context(p, rank=rank, world=world, device=local, nccl_id=nccl_id, stream=stream.cuda_stream)
     if p.coarse == synth.COARSE_PINN:
-        ctx.load_weights(net)
+        ctx.load_weights(net, precision=PREC_CODE[args.pinn_prec])
     ws = torch.empty(ctx.workspace_bytes(), dtype=torch.uint8, device="cuda")
     ctx.bind_workspace(ws)
     if not args.no_graphs:
@@ -347,7 +370,8 @@ def main():
     pk, pk_src = peaks()
     clk_mhz = float(pk.get("sm_max_mhz", 1965.0))
     n_sm = torch.cuda.get_device_properties(local).multi_processor_count
-    roof = roofline(p, ph, K, world, rank, pk, pk_src, clk_mhz, n_sm, synth)
+    roof = roofline(p, ph, K, world, rank, pk, pk_src, clk_mhz, n_sm, synth, dims=pinn_dims(args),
+                    tc_prec=None if args.pinn_prec == "fp32" else args.pinn_prec)
     # ---------------- north-star gate: the HBM-streamed fine sweep (K2) at the C3 grid, measured
     # live in the same run (one fine sweep over 64 slices x 2^20 points x 100 steps)
     fine_c3 = None

@@ -27,6 +27,7 @@ KEYS = [("gpu__time_duration.sum", "duration"), ("dram__bytes_read.sum", "dram_r
         ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "fp64_pipe_%"),
         ("sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active", "xu_pipe_%"),
         ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "tensor_pipe_%"),
+        ("sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed", "tensor_pipe_%"),
         ("launch__registers_per_thread", "regs"), ("launch__grid_size", "grid"), ("launch__block_size", "block")]
 UNIT_SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-9, "us": 1e-6, "usecond": 1e-6,
               "msecond": 1e-3, "ms": 1e-3, "nsecond": 1e-9, "second": 1.0}
@@ -76,15 +77,15 @@ def main():
     args = ap.parse_args()
     recs = [r for rep in args.reps for r in summarise(rep)]
     lines = ["# %s" % args.title, "",
-             "| kernel | source | time (us) | DRAM R+W (MB) | DRAM % | L2 % | issue % | warps % | fma % | fp64 % | xu % | regs | grid | top stalls |",
-             "|---|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
+             "| kernel | source | time (us) | DRAM R+W (MB) | DRAM % | L2 % | issue % | warps % | fma % | fp64 % | xu % | tensor % | regs | grid | top stalls |",
+             "|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
     for r in recs:
         f = lambda k, s=1, p=1: ("%.*f" % (p, r[k] * s)) if r.get(k) is not None else "-"
         dram = (r.get("dram_read") or 0) + (r.get("dram_write") or 0)
-        lines.append("| %s | %s | %s | %.2f | %s | %s | %s | %s | %s | %s | %s | %s | %s | %s |" % (
+        lines.append("| %s | %s | %s | %.2f | %s | %s | %s | %s | %s | %s | %s | %s | %s | %s | %s |" % (
             r["kernel"][:60], r["source"], f("duration", 1e6), dram / 1e6, f("dram_%"), f("l2_%"), f("issue_%"),
-            f("warps_active_%"), f("fma_pipe_%"), f("fp64_pipe_%"), f("xu_pipe_%"), f("regs", 1, 0), f("grid", 1, 0),
-            r["stalls"]))
+            f("warps_active_%"), f("fma_pipe_%"), f("fp64_pipe_%"), f("xu_pipe_%"), f("tensor_pipe_%"),
+            f("regs", 1, 0), f("grid", 1, 0), r["stalls"]))
     with open(args.out, "w") as fh:
         fh.write("\n".join(lines) + "\n")
     if args.traffic:
