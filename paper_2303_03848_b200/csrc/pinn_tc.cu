@@ -101,7 +101,17 @@ struct PinnTcArgs {
   int resident;            // 1: every chunk fits in shared memory (loaded once)
 };
 
-constexpr int kTcKC = 64;  // K columns per weight chunk
+constexpr int kTcKC = 32;  // K columns per weight chunk
+
+// Activation of the tensor-core epilogue.  Exact mode: the K3 tanh (ex2 + rcp, 2 MUFU ops, ~2e-7).
+// FAST (bf16 mode, itself ~1e-2): tanh.approx.f32 (1 MUFU op, ~5e-4) on the un-prescaled argument.
+template <int ACT, bool FAST>
+__device__ __forceinline__ float act_tc(float zs) {
+  if (ACT == 1 || !FAST) return act<ACT>(zs);
+  float r;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(r) : "f"(zs * 0.34657359027997264f));  // zs / (2 log2 e)
+  return r;
+}
 
 // SPLIT (PR_PREC_FP16_TC): operands split hi + lo in fp16, D = A_hi·B_hi + A_hi·B_lo + A_lo·B_hi —
 // fp32-level accuracy (~2e-6 on 8×256 nets) at 3× the MMAs.  !SPLIT (PR_PREC_BF16_TC): one bf16 pass.
@@ -119,9 +129,9 @@ __global__ void __launch_bounds__(128) k_pinn_chain_tc(PinnTcArgs ta) {
   extern __shared__ __align__(128) unsigned char tc_smem[];
   T *sA = reinterpret_cast<T *>(tc_smem);                    // NP planes [128 × W]
   unsigned char *sB = tc_smem + NP * kPlaneA;                // 1 chunk, or all (LH−1)·NCH chunks
-  const int nchunks = ta.resident ? (a.LH - 1) * NCH : 1;
+  const int nchunks = ta.resident ? (a.LH - 1) * NCH : 2;  // resident, or two streaming buffers
   float *sP = reinterpret_cast<float *>(sB + (size_t)nchunks * kChunk);
-  __shared__ __align__(8) uint64_t bar_mma, bar_w;
+  __shared__ __align__(8) uint64_t bar_mma, bar_w, bar_full[2], bar_free[2];
   __shared__ uint32_t s_tmem;
   __shared__ double red[64];
   const int t = threadIdx.x, w = t >> 5;
@@ -129,6 +139,10 @@ __global__ void __launch_bounds__(128) k_pinn_chain_tc(PinnTcArgs ta) {
   if (t == 0) {
     tc_mbar_init(&bar_mma);
     tc_mbar_init(&bar_w);
+    tc_mbar_init(&bar_full[0]);
+    tc_mbar_init(&bar_full[1]);
+    tc_mbar_init(&bar_free[0]);
+    tc_mbar_init(&bar_free[1]);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (w == 0) {
@@ -147,6 +161,16 @@ __global__ void __launch_bounds__(128) k_pinn_chain_tc(PinnTcArgs ta) {
     tc_mbar_wait(&bar_w, ph_w);
     ph_w ^= 1;
   }
+  // Streaming: chunk g of the repeating sequence (layer-major, all slices) goes to buffer g & 1;
+  // thread 0 loads chunk g+1 while the MMAs of chunk g run (after those of chunk g−1, which used
+  // that buffer, have completed).
+  const int nseq = (a.LH - 1) * NCH;
+  unsigned g_next = 0;  // next chunk of the sequence to be consumed
+  auto load_chunk = [&](unsigned g) {
+    tc_bulk_g2s(sB + (size_t)(g & 1) * kChunk, (const unsigned char *)ta.wh + (size_t)(g % nseq) * kChunk, kChunk,
+                &bar_full[g & 1]);
+  };
+  if (!ta.resident && a.LH > 1 && t == 0) load_chunk(0);
   const float *W0 = sP, *b0 = sP + W * IN;
   const float *Wo = sP + W * IN + W + (size_t)(a.LH - 1) * W;
   const float bo = Wo[W];
@@ -233,22 +257,23 @@ __global__ void __launch_bounds__(128) k_pinn_chain_tc(PinnTcArgs ta) {
     float y = 0.f;
 #pragma unroll 1
     for (int l = 1; l < a.LH; ++l) {
-      // ---- D[128 × W] = A · W_l^T, chunk by chunk along K
+      // ---- D[128 × W] = A · W_l^T, chunk by chunk along K (one thread issues)
+      if (t == 0) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll 1
-      for (int c = 0; c < NCH; ++c) {
-        const int ci = (l - 1) * NCH + c;
-        uint32_t bc = bBase + (uint32_t)ci * kChunk;
-        if (!ta.resident) {  // stream the chunk (the previous MMA on the buffer has completed)
-          if (t == 0) tc_bulk_g2s(sB, (const unsigned char *)ta.wh + (size_t)ci * kChunk, kChunk, &bar_w);
-          tc_mbar_wait(&bar_w, ph_w);
-          ph_w ^= 1;
-          bc = bBase;
-        }
-        if (t == 0) {
-          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        for (int c = 0; c < NCH; ++c) {
+          uint32_t bc;
+          unsigned g = 0;
+          if (ta.resident) {
+            bc = bBase + (uint32_t)((l - 1) * NCH + c) * kChunk;
+          } else {
+            g = g_next++;
+            tc_mbar_wait(&bar_full[g & 1], (g >> 1) & 1);
+            bc = bBase + (g & 1) * kChunk;
+          }
 #pragma unroll
           for (int ks = 0; ks < kTcKC / 16; ++ks) {
-            // A: K offset c·64 + 16·ks = core matrix (8c + 2ks) along K; B chunk: core matrix 2ks
+            // A: K offset c·KC + 16·ks = core matrix (c·KC/8 + 2ks) along K; B chunk: core matrix 2ks
             const uint32_t ao = (uint32_t)(c * (kTcKC / 8) + 2 * ks) * 128, bo2 = (uint32_t)(2 * ks) * 128;
             const uint64_t dah = umma_desc(aHi + ao, 128, 16 * W), dbh = umma_desc(bc + bo2, 128, 16 * kTcKC);
             const uint32_t acc = (c > 0 || ks > 0) ? 1u : 0u;
@@ -269,16 +294,21 @@ __global__ void __launch_bounds__(128) k_pinn_chain_tc(PinnTcArgs ta) {
                   "l"(dal), "l"(dbh), "r"(kIdesc), "r"(1u));
             }
           }
-          if (!ta.resident || c == NCH - 1)  // the chunk buffer is reused, or the layer is complete
+          if (!ta.resident) {
             asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                             tc_smem_u32(&bar_mma))
+                             tc_smem_u32(&bar_free[g & 1]))
                          : "memory");
+            // buffer (g+1)&1 held chunk g−1: reload it with chunk g+1 once chunk g−1's MMAs completed
+            if (g >= 1) tc_mbar_wait(&bar_free[(g - 1) & 1], ((g - 1) >> 1) & 1);
+            load_chunk(g + 1);
+          }
         }
-        if (!ta.resident || c == NCH - 1) {
-          tc_mbar_wait(&bar_mma, ph_mma);
-          ph_mma ^= 1;
-        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                         tc_smem_u32(&bar_mma))
+                     : "memory");
       }
+      tc_mbar_wait(&bar_mma, ph_mma);
+      ph_mma ^= 1;
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const float *bl = sP + W * IN + W + (size_t)(l - 1) * W;
       const bool last = l == a.LH - 1;
@@ -287,7 +317,7 @@ __global__ void __launch_bounds__(128) k_pinn_chain_tc(PinnTcArgs ta) {
         float v[32];
         tmem_ld32(tlane + (uint32_t)c0, v);
 #pragma unroll
-        for (int q = 0; q < 32; ++q) v[q] = act<ACT>(v[q] + bl[c0 + q]);
+        for (int q = 0; q < 32; ++q) v[q] = act_tc<ACT, !SPLIT>(v[q] + bl[c0 + q]);
         if (last) {
 #pragma unroll
           for (int q = 0; q < 32; ++q) y = fmaf(Wo[c0 + q], v[q], y);
@@ -332,6 +362,7 @@ __global__ void __launch_bounds__(128) k_pinn_chain_tc(PinnTcArgs ta) {
       }
     }
   }
+  if (!ta.resident && a.LH > 1 && t == 0) tc_mbar_wait(&bar_full[g_next & 1], (g_next >> 1) & 1);  // last prefetch
   __syncthreads();
   if (w == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((uint32_t)W));
 }
@@ -363,7 +394,7 @@ size_t pinn_tc_smem(int W, int LH, int nfloats, bool bf16, bool *resident) {
     return a + all + p;
   }
   *resident = false;
-  return a + chunk + p;
+  return a + 2 * chunk + p;
 }
 
 // host: hidden layer l's [W][W] (fp32, pre-scaled) → its W/64 K-chunks, each [hi plane][lo plane],
