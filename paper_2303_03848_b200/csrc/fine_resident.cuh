@@ -76,6 +76,10 @@ struct Tri {
   double nm[P], ip[P], ncu[P], qf[P], qb[P];
   double cfL[5], cbL[5];
   double cf_exc, cb_exc;
+  // cross-warp fold, NW ≥ 4: warp totals are combined as one weighted sum (the weights — products
+  // of the constant warp multipliers between warp q and this warp — precomputed by fold_setup)
+  static constexpr bool kParFold = NW >= 4;
+  double cfw[kParFold ? NW : 1], cbw[kParFold ? NW : 1];
   double e0, e1, er, J0;  // CN: explicit-part coefficients, J of the thread's first point
   int lane, w, M, j0;
 
@@ -134,6 +138,29 @@ struct Tri {
       if (lane == 0) sh[NW + w] = cb;   // total backward product of warp w
     }
   }
+  // after the barrier that follows setup: fold weights Π_{q<r<w} B_r (forward), Π_{w<r<q} B_r (backward)
+  __device__ void fold_setup(const double *sh) {
+    if (!kParFold) return;
+#pragma unroll
+    for (int q = 0; q < NW; ++q) {
+      double pf = 1.0, pb = 1.0;
+      for (int r = q + 1; r < w; ++r) pf *= sh[r];
+      for (int r = w + 1; r < q; ++r) pb *= sh[NW + r];
+      cfw[q] = (q < w) ? pf : 0.0;
+      cbw[q] = (q > w) ? pb : 0.0;
+    }
+  }
+  // fixed-order pairwise sum of the weighted warp totals
+  __device__ __forceinline__ double fold(const double (&c)[kParFold ? NW : 1], const double *sy) const {
+    double t[NW];
+#pragma unroll
+    for (int q = 0; q < NW; ++q) t[q] = c[q] * sy[q];
+#pragma unroll
+    for (int d = 1; d < NW; d <<= 1)
+#pragma unroll
+      for (int q = 0; q + d < NW; q += 2 * d) t[q] += t[q + d];
+    return t[0];
+  }
 
   // One implicit step in place on x[P] (fp64).  bc_i: point index inside this thread that
   // receives the boundary term (−1 if none); bcg = dτ(a_M+b_M) g(τ⁺).
@@ -186,8 +213,12 @@ struct Tri {
       double *sy = sh + 2 * NW;
       if (lane == 31) sy[w] = v;
       __syncthreads();
+      if constexpr (kParFold) {
+        in = fold(cfw, sy);
+      } else {
 #pragma unroll 1
-      for (int q = 0; q < w; ++q) in = fma(sh[q], in, sy[q]);
+        for (int q = 0; q < w; ++q) in = fma(sh[q], in, sy[q]);
+      }
     }
     const double yin = fma(cf_exc, in, ve);
 #pragma unroll
@@ -206,8 +237,12 @@ struct Tri {
       double *sy = sh + 3 * NW;
       if (lane == 0) sy[w] = v;
       __syncthreads();
+      if constexpr (kParFold) {
+        in = fold(cbw, sy);
+      } else {
 #pragma unroll 1
-      for (int q = NW - 1; q > w; --q) in = fma(sh[NW + q], in, sy[q]);
+        for (int q = NW - 1; q > w; --q) in = fma(sh[NW + q], in, sy[q]);
+      }
     }
     const double xin = fma(cb_exc, in, ve);
 #pragma unroll
@@ -280,6 +315,7 @@ __global__ void __launch_bounds__(NT * SPB) k_fine_sweep(ResidentArgs a) {
   Tri<P, NT, CN> tri;
   tri.setup(a, a.fset[b], t, sh);
   if (NW > 1) __syncthreads();
+  tri.fold_setup(sh);
   const float *u = a.U + ((size_t)ln * a.B + b) * a.Mp;
   double x[P];
 #pragma unroll
@@ -332,6 +368,7 @@ __global__ void __launch_bounds__(NT * SPB) k_resident_chain(ResidentArgs a) {
   Tri<P, NT, CN> tri;
   tri.setup(a, a.fset[b], t, sh);
   if (NW > 1) __syncthreads();
+  tri.fold_setup(sh);
   const size_t sstride = (size_t)a.B * a.Mp;
   double x[P];
   float *u0 = a.Uw + (size_t)a.c_ln0 * a.ustride + (size_t)b * a.Mp;

@@ -217,6 +217,7 @@ __device__ void fine_role(const PipeArgs &pa, int n, int b) {
   Tri<P, NT, CN> tri;
   tri.setup(a, a.fset[b], t, sh);
   __syncthreads();
+  tri.fold_setup(sh);
   const int C = pa.C * (128 / 32);  // publishing chain warps per instance
   const int *cnt = pa.cnt + (size_t)b * pa.N;
   int *floaded = pa.floaded + (size_t)b * pa.N, *fdone = pa.fdone + (size_t)b * pa.N;

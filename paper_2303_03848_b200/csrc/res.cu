@@ -1,6 +1,7 @@
 // res.cu — translation unit of K1 (fine_resident.cuh): the (P, NT, SPB) instantiations.
 #include "launch.h"
 #include "fine_resident.cuh"
+#include <stdlib.h>
 
 namespace pr {
 template <int P, int NT, int SPB>
@@ -21,7 +22,11 @@ cudaError_t launch_resident(bool chain, int M, const ResidentArgs &a, int nsys, 
   else if (M <= 128) launch_res<4, 32, 4>(chain, a, nsys, s);
   else if (M <= 256) launch_res<8, 32, 4>(chain, a, nsys, s);
   else if (M <= 512) launch_res<8, 64, 2>(chain, a, nsys, s);
-  else if (M <= 1024) launch_res<8, 128, 1>(chain, a, nsys, s);
+  else if (M <= 1024) {
+    static const bool wide = getenv("PR_K1_WIDE") && atoi(getenv("PR_K1_WIDE")) == 1;  // tuning: 8 warps x 4 points
+    if (wide) launch_res<4, 256, 1>(chain, a, nsys, s);
+    else launch_res<8, 128, 1>(chain, a, nsys, s);
+  }
   else launch_res<8, 256, 1>(chain, a, nsys, s);
   return cudaGetLastError();
 }
