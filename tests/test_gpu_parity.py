@@ -357,6 +357,25 @@ def test_streamed_determinism_and_parity():
     assert np.allclose(ra["delta"], ref_d, rtol=2e-2)
 
 
+@pytest.mark.parametrize("M,N,B", [(10000, 20, 1), (6000, 18, 1), (5000, 9, 2)])
+def test_streamed_persistent_kernel_parity(M, N, B):
+    """K2's persistent factor-resident kernel (sweeps with >= 16 systems): every iterate against
+    the oracle, including ragged item groups (18 slices in groups of 4) and two instances with
+    different factor sets sharing a launch."""
+    if B == 1:
+        p = synth.single(M, N, fine_steps=6, coarse=synth.COARSE_IMPLICIT_EULER, coarse_steps=1, max_iter=2, tol=0.0)
+    else:
+        p = synth.portfolio(n_k=1, n_s=2, M=M, N=N, fine_steps=6, coarse=synth.COARSE_IMPLICIT_EULER,
+                            coarse_steps=1, max_iter=2, tol=0.0)
+    with ctx_for(p, fine_kernel=2) as c:
+        _, rep = c.solve()
+        it = c.copy_iterates(0, p.N + 1)
+    ref_U, ref_d, K, _ = oracle.parareal(p)
+    assert rep["iterations"] == K == 2
+    assert_close(it, ref_U, what="persistent K2 M=%d N=%d B=%d" % (M, N, B))
+    assert np.allclose(rep["delta"], ref_d, rtol=2e-2)
+
+
 def test_portfolio_parareal_sampled():
     """C4 layout (many instances, 64 factor sets) at reduced instance count; fixed K."""
     p = synth.portfolio(n_k=4, n_s=16, M=256, N=16, coarse=synth.COARSE_IMPLICIT_EULER, max_iter=3, tol=0.0)
