@@ -48,9 +48,9 @@ struct PipeArgs {
   unsigned long long *trace;   // nullable: [K+1][N][3] %globaltimer (chain warp 0 of CTA 0 at each
                                // slice; fine (n, b=0) start and end), for PR_PIPE_TRACE
 };
-bool pipe_supported(int M, bool cn, int IN, int W, int act);
-cudaError_t launch_parareal_pipe(const PipeArgs &pa, int M, bool cn, int IN, int W, int act, size_t smem,
-                                 cudaStream_t s);
+bool pipe_supported(int M, bool cn, int IN, int W, int act, bool split);
+cudaError_t launch_parareal_pipe(const PipeArgs &pa, int M, bool cn, int IN, int W, int act, bool split,
+                                 size_t smem, cudaStream_t s);
 // K6/K7 (misc.cu)
 cudaError_t launch_payoff(float *U0, int M, int Mp, int B, const double *Lb, const double *Kb, cudaStream_t s);
 cudaError_t launch_delta(const double *partials, int B, int nch, int ln_lo, int ln_hi, unsigned long long *dmax,

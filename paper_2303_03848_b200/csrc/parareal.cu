@@ -771,9 +771,10 @@ pr_plan make_plan(int N, int world, int rank, int k) {
 // mode, resident fine kernel with M ≤ 1024, and every CTA co-resident (checked at first launch).
 bool pipe_eligible(const pr_ctx *c) {
   if (c->opt_pipeline == 1 || c->pipe_ok == 0) return false;
-  if (c->world != 1 || c->tol != 0.0 || c->coarse != PR_COARSE_PINN || c->max_iter < 1) return false;
-  if (!use_split_pinn(c) || !use_resident(c) || c->M > 1024) return false;
-  return pr::pipe_supported(c->M, c->fine_theta != 1.0, c->IN, c->W, c->act);
+  if (c->world != 1 || c->tol != 0.0 || c->coarse != PR_COARSE_PINN || c->max_iter < 1 || c->tc) return false;
+  if (!use_resident(c) || c->M > 1024) return false;
+  // the chain evaluates as the blocking kernel would: latency mode if it is the one chosen
+  return pr::pipe_supported(c->M, c->fine_theta != 1.0, c->IN, c->W, c->act, use_split_pinn(c));
 }
 
 pr_status ensure_pipe(pr_ctx *c) {
@@ -804,7 +805,8 @@ pr_status solve_pipelined(pr_ctx *c) {
   pa.g.Fcopy = c->Fk;
   pa.N = c->N;
   pa.K = c->max_iter;
-  pa.C = c->nch;  // chain CTAs per instance (latency mode: 128/kPinnSplitG points each)
+  const int G = use_split_pinn(c) ? pr::kPinnSplitG : 1;  // threads per point in the chain
+  pa.C = (c->M * G + 127) / 128;                         // chain CTAs per instance (≤ nch)
   pa.partials = c->pipe_partials;
   pa.pstride = c->pipe_pstride;
   pa.wstage = c->pipe_wstage;
@@ -820,7 +822,7 @@ pr_status solve_pipelined(pr_ctx *c) {
   pa.floaded = c->pipe_flags + (size_t)c->B * c->N;
   pa.fdone = c->pipe_flags + (size_t)2 * c->B * c->N;
   const cudaError_t e = pr::launch_parareal_pipe(pa, c->M, c->fine_theta != 1.0, c->IN, c->W, c->act,
-                                                 (size_t)c->nfloats * sizeof(float), c->stream);
+                                                 use_split_pinn(c), (size_t)c->nfloats * sizeof(float), c->stream);
   if (e == cudaErrorCooperativeLaunchTooLarge) {
     cudaGetLastError();
     c->pipe_ok = 0;

@@ -60,9 +60,23 @@ __device__ __forceinline__ void publish_set(int *p, int v) {
 // its inputs and publishes its outputs by itself (no CTA barrier per slice).  δ partial sums are
 // staged per warp and folded per CTA, warps in index order, at the end of each iteration — the
 // blocking kernel's summation order, so δ is bitwise the same.
-template <int IN, int ACT>
+// The network evaluator: G = kPinnSplitG threads per point (latency mode, W = 20) or one thread
+// per point (shared-memory weights, any instantiated width: the paper's 10×50 net).
+template <int IN, int W, int G, int ACT>
+__device__ __forceinline__ float chain_eval(const float *sw, int LH, const float (&x)[IN]) {
+  if constexpr (G > 1) {
+    return mlp_split<IN, W, G, ACT>(sw, LH, x);
+  } else {
+    float xx[1][IN], y[1];
+#pragma unroll
+    for (int i = 0; i < IN; ++i) xx[0][i] = x[i];
+    mlp_eval<IN, W, ACT, 1>(sw, LH, xx, y);
+    return y[0];
+  }
+}
+
+template <int IN, int W, int G, int ACT>
 __device__ void chain_role(const PipeArgs &pa, int k, int b, int chunk, const float *sw) {
-  constexpr int G = kPinnSplitG;
   constexpr int NWC = 128 / 32;  // warps per chain CTA
   const PinnArgs &a = pa.g;
   const double Lb = a.Lb[b];
@@ -164,7 +178,7 @@ __device__ void chain_role(const PipeArgs &pa, int k, int b, int chunk, const fl
         x[0] = tt * a.cs0;
         x[IN - 1] = s_over_L * a.cs1;
       }
-      const float y = mlp_split<IN, 20, G, ACT>(sw, a.LH, x);
+      const float y = chain_eval<IN, W, G, ACT>(sw, a.LH, x);
       const float g = gscale * y;
       float nv = 0.f;
       double num = 0.0, den = 0.0;
@@ -260,7 +274,7 @@ __device__ void fine_role(const PipeArgs &pa, int n, int b) {
 
 // CTAs [0, (K+1)·B·C): the chain of iteration k = blockIdx / (B·C) (each iteration its own CTAs,
 // so chain k+1 runs behind chain k instead of after it); then one CTA per fine system.
-template <int P, bool CN, int IN, int ACT>
+template <int P, bool CN, int IN, int W, int G, int ACT>
 __global__ void __launch_bounds__(128) k_parareal_pipe(PipeArgs pa) {
   extern __shared__ float sw[];
   const int per = pa.g.B * pa.C;
@@ -269,7 +283,7 @@ __global__ void __launch_bounds__(128) k_parareal_pipe(PipeArgs pa) {
     for (int i = threadIdx.x; i < pa.g.nfloats; i += blockDim.x) sw[i] = pa.g.wts[i];
     __syncthreads();
     const int k = blockIdx.x / per, r = blockIdx.x % per;
-    chain_role<IN, ACT>(pa, k, r / pa.C, r % pa.C, sw);
+    chain_role<IN, W, G, ACT>(pa, k, r / pa.C, r % pa.C, sw);
   } else {
     const int f = blockIdx.x - nchain;
     fine_role<P, CN>(pa, f / pa.g.B, f % pa.g.B);
@@ -277,27 +291,40 @@ __global__ void __launch_bounds__(128) k_parareal_pipe(PipeArgs pa) {
 }
 
 typedef void (*PipeKernel)(PipeArgs);
-template <bool CN, int IN, int ACT>
+template <bool CN, int IN, int W, int G, int ACT>
 static PipeKernel pipe_kernel_p(int M) {
-  if (M <= 256) return k_parareal_pipe<2, CN, IN, ACT>;
-  if (M <= 512) return k_parareal_pipe<4, CN, IN, ACT>;
-  if (M <= 1024) return k_parareal_pipe<8, CN, IN, ACT>;
+  if (M <= 256) return k_parareal_pipe<2, CN, IN, W, G, ACT>;
+  if (M <= 512) return k_parareal_pipe<4, CN, IN, W, G, ACT>;
+  if (M <= 1024) return k_parareal_pipe<8, CN, IN, W, G, ACT>;
   return nullptr;
 }
-static PipeKernel pipe_kernel(int M, bool cn, int IN, int W, int act) {
-  if (W != 20 || act != 0) return nullptr;
-  if (IN == 4) return cn ? pipe_kernel_p<true, 4, 0>(M) : pipe_kernel_p<false, 4, 0>(M);
-  if (IN == 2) return cn ? pipe_kernel_p<true, 2, 0>(M) : pipe_kernel_p<false, 2, 0>(M);
+template <int IN, int W, int G, int ACT>
+static PipeKernel pipe_kernel_c(int M, bool cn) {
+  return cn ? pipe_kernel_p<true, IN, W, G, ACT>(M) : pipe_kernel_p<false, IN, W, G, ACT>(M);
+}
+// instantiated: latency-mode 20-wide nets (G = 4), and one thread per point for the paper's
+// 10×50 architecture (tanh or ReLU) and 32-wide tanh nets
+static PipeKernel pipe_kernel(int M, bool cn, int IN, int W, int act, bool split) {
+  if (split) {
+    if (W != 20 || act != 0) return nullptr;
+    if (IN == 4) return pipe_kernel_c<4, 20, kPinnSplitG, 0>(M, cn);
+    if (IN == 2) return pipe_kernel_c<2, 20, kPinnSplitG, 0>(M, cn);
+    return nullptr;
+  }
+  if (IN == 4 && W == 50) return act ? pipe_kernel_c<4, 50, 1, 1>(M, cn) : pipe_kernel_c<4, 50, 1, 0>(M, cn);
+  if (IN == 4 && W == 32 && act == 0) return pipe_kernel_c<4, 32, 1, 0>(M, cn);
   return nullptr;
 }
 
-bool pipe_supported(int M, bool cn, int IN, int W, int act) { return pipe_kernel(M, cn, IN, W, act) != nullptr; }
+bool pipe_supported(int M, bool cn, int IN, int W, int act, bool split) {
+  return pipe_kernel(M, cn, IN, W, act, split) != nullptr;
+}
 
 // Launches the cooperative kernel; cudaErrorCooperativeLaunchTooLarge (or not supported) tells
 // the caller to use the blocking schedule.
-cudaError_t launch_parareal_pipe(const PipeArgs &pa, int M, bool cn, int IN, int W, int act, size_t smem,
-                                 cudaStream_t s) {
-  PipeKernel k = pipe_kernel(M, cn, IN, W, act);
+cudaError_t launch_parareal_pipe(const PipeArgs &pa, int M, bool cn, int IN, int W, int act, bool split,
+                                 size_t smem, cudaStream_t s) {
+  PipeKernel k = pipe_kernel(M, cn, IN, W, act, split);
   if (!k) return cudaErrorInvalidValue;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

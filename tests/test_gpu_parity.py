@@ -418,16 +418,22 @@ def test_device_entry_points():
     assert np.array_equal(v0, oracle.payoff(p).astype(np.float32))
 
 
-@pytest.mark.parametrize("name,M,N,B,theta", [("C1", 64, 4, 1, 1.0), ("C2", 1024, 32, 1, 1.0), ("C2", 1024, 32, 1, 0.5),
-                                              ("portfolio", 256, 8, 6, 1.0), ("odd", 700, 12, 1, 1.0)])
-def test_pipelined_matches_blocking(name, M, N, B, theta):
+@pytest.mark.parametrize("name,M,N,B,theta,dims,act", [
+    ("C1", 64, 4, 1, 1.0, synth.PINN_3x20, synth.ACT_TANH), ("C2", 1024, 32, 1, 1.0, synth.PINN_3x20, synth.ACT_TANH),
+    ("C2", 1024, 32, 1, 0.5, synth.PINN_3x20, synth.ACT_TANH), ("portfolio", 256, 8, 6, 1.0, synth.PINN_3x20, synth.ACT_TANH),
+    ("odd", 700, 12, 1, 1.0, synth.PINN_3x20, synth.ACT_TANH),
+    ("C2 paper net", 1024, 32, 1, 1.0, synth.PINN_PAPER, synth.ACT_RELU),
+    ("paper net tanh", 300, 8, 2, 1.0, synth.PINN_PAPER, synth.ACT_TANH)])
+def test_pipelined_matches_blocking(name, M, N, B, theta, dims, act):
     """PR_OPT_PIPELINE (NEXT-2): the overlapped single-kernel schedule gives the blocking
-    schedule's iterates, output and δ bitwise (and is the one auto mode takes here)."""
-    if name == "portfolio":
-        p = synth.portfolio(n_k=2, n_s=3, M=M, N=N, coarse=synth.COARSE_PINN, max_iter=3, tol=0.0)
+    schedule's iterates, output and δ bitwise (and is the one auto mode takes here), with the
+    latency-mode chain (3x20) and the one-thread-per-point chain (the paper's 10x50 net)."""
+    if B > 1:
+        p = synth.portfolio(n_k=B // 2 if B > 2 else 1, n_s=3 if B > 2 else 2, M=M, N=N, coarse=synth.COARSE_PINN,
+                            max_iter=3, tol=0.0)
     else:
         p = synth.single(M, N, coarse=synth.COARSE_PINN, max_iter=3, tol=0.0, fine_theta=theta)
-    net = synth.kaiming_net(synth.PINN_3x20, seed=2)
+    net = synth.kaiming_net(dims, seed=2, activation=act)
     with ctx_for(p, net) as c:
         a, ra = c.solve()
         it_a = c.copy_iterates(0, p.N + 1)
