@@ -265,6 +265,7 @@ def c3_fine_sweep_roofline(parareal, synth, torch, stream, pk, pk_src, flush):
     ctx = parareal.Context(p, stream=stream.cuda_stream)
     try:
         ctx.load_weights(synth.kaiming_net(synth.PINN_3x20, seed=0))
+        ctx.set_option(parareal.OPT_USE_GRAPHS, 1)  # the sweep's ~200 pass launches replay as one graph
         out = torch.empty((p.B, p.M), dtype=torch.float32, device="cuda")
         ctx.solve_device(out)
         ms = []

@@ -68,6 +68,14 @@ def summarise(rep):
     return res
 
 
+def measured_hbm_gbs():
+    try:
+        with open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"])
+    except Exception:
+        return None
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("reps", nargs="+")
@@ -77,13 +85,19 @@ def main():
     args = ap.parse_args()
     recs = [r for rep in args.reps for r in summarise(rep)]
     lines = ["# %s" % args.title, "",
-             "| kernel | source | time (us) | DRAM R+W (MB) | DRAM % | L2 % | issue % | warps % | fma % | fp64 % | xu % | tensor % | regs | grid | top stalls |",
-             "|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
+             "DRAM GB/s = dram__bytes (read+write) / gpu__time_duration of the launch under ncu; "
+             "'of meas.' divides by the measured copy bandwidth in MEASURED_PEAKS.json (%s GB/s)." % measured_hbm_gbs(), "",
+             "| kernel | source | time (us) | DRAM R+W (MB) | DRAM GB/s | of meas. | DRAM % | L2 % | issue % | warps % | fma % | fp64 % | xu % | tensor % | regs | grid | top stalls |",
+             "|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
+    hbm = measured_hbm_gbs()
     for r in recs:
         f = lambda k, s=1, p=1: ("%.*f" % (p, r[k] * s)) if r.get(k) is not None else "-"
         dram = (r.get("dram_read") or 0) + (r.get("dram_write") or 0)
-        lines.append("| %s | %s | %s | %.2f | %s | %s | %s | %s | %s | %s | %s | %s | %s | %s | %s |" % (
-            r["kernel"][:60], r["source"], f("duration", 1e6), dram / 1e6, f("dram_%"), f("l2_%"), f("issue_%"),
+        gbs = dram / r["duration"] / 1e9 if r.get("duration") else None
+        lines.append("| %s | %s | %s | %.2f | %s | %s | %s | %s | %s | %s | %s | %s | %s | %s | %s | %s | %s |" % (
+            r["kernel"][:60], r["source"], f("duration", 1e6), dram / 1e6,
+            "%.0f" % gbs if gbs is not None else "-", "%.2f" % (gbs / hbm) if (gbs and hbm) else "-",
+            f("dram_%"), f("l2_%"), f("issue_%"),
             f("warps_active_%"), f("fma_pipe_%"), f("fp64_pipe_%"), f("xu_pipe_%"), f("tensor_pipe_%"),
             f("regs", 1, 0), f("grid", 1, 0), r["stalls"]))
     with open(args.out, "w") as fh:
