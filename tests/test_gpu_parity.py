@@ -357,16 +357,19 @@ def test_streamed_determinism_and_parity():
     assert np.allclose(ra["delta"], ref_d, rtol=2e-2)
 
 
-@pytest.mark.parametrize("M,N,B", [(10000, 20, 1), (6000, 18, 1), (5000, 9, 2)])
-def test_streamed_persistent_kernel_parity(M, N, B):
+@pytest.mark.parametrize("M,N,B,theta", [(10000, 20, 1, 1.0), (6000, 18, 1, 1.0), (5000, 9, 2, 1.0),
+                                         (10000, 20, 1, 0.5), (5000, 9, 2, 0.5), (4500, 17, 1, 0.75)])
+def test_streamed_persistent_kernel_parity(M, N, B, theta):
     """K2's persistent factor-resident kernel (sweeps with >= 16 systems): every iterate against
     the oracle, including ragged item groups (18 slices in groups of 4) and two instances with
-    different factor sets sharing a launch."""
+    different factor sets sharing a launch; theta-steps run these sweeps on the tile kernel
+    (explicit stencil, tile-edge terms) and are checked the same way."""
     if B == 1:
-        p = synth.single(M, N, fine_steps=6, coarse=synth.COARSE_IMPLICIT_EULER, coarse_steps=1, max_iter=2, tol=0.0)
+        p = synth.single(M, N, fine_steps=6, coarse=synth.COARSE_IMPLICIT_EULER, coarse_steps=1, max_iter=2, tol=0.0,
+                         fine_theta=theta)
     else:
         p = synth.portfolio(n_k=1, n_s=2, M=M, N=N, fine_steps=6, coarse=synth.COARSE_IMPLICIT_EULER,
-                            coarse_steps=1, max_iter=2, tol=0.0)
+                            coarse_steps=1, max_iter=2, tol=0.0, fine_theta=theta)
     with ctx_for(p, fine_kernel=2) as c:
         _, rep = c.solve()
         it = c.copy_iterates(0, p.N + 1)
