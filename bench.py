@@ -133,18 +133,19 @@ def peaks():
 
 
 # --------------------------------------------------------------------------- reference arm
-def cpu_oracle_run(p, net, budget_s: float, max_runs: int):
-    """Time the CPU oracle (as it stands) on the full workload; returns (sec per solve, runs, cores)."""
+def cpu_oracle_run(p, net, budget_s: float, max_runs: int, threads: int = 1):
+    """Time the CPU oracle (as it stands) on the full workload; returns (sec per solve, runs, cores).
+    threads > 1: its threaded-fine variant (fine sweep slices on std::threads, bitwise the same)."""
     import oracle
     times = []
     t_start = time.perf_counter()
     while len(times) < max_runs:
         t0 = time.perf_counter()
-        oracle.parareal(p, net)
+        oracle.parareal(p, net, threads=threads)
         times.append(time.perf_counter() - t0)
         if time.perf_counter() - t_start > budget_s:
             break
-    return statistics.mean(times), len(times), 1
+    return statistics.mean(times), len(times), threads
 
 
 def run_reference(args):
@@ -401,13 +402,18 @@ def main():
         e2e = {"value": work_units(p) * args.steps / (float(et.item()) / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": 4 * p.B * p.M, "d2h_bytes_per_step": 4 * p.B * p.M}
     # ---------------- CPU oracle baseline (rank 0, N=1 only)
-    cpu = None
+    cpu = cpu_threaded = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         from paper_2303_03848_b200 import synth as S
         netc = net if p.coarse == S.COARSE_PINN else None
         per, runs, cores = cpu_oracle_run(p, netc, budget_s=10.0, max_runs=20)
         cpu = {"value": work_units(p) / per, "unit": UNIT, "cores": cores, "kind": "oracle",
                "sample": "full %s workload, %d serial fp64 oracle solves (%.3f s each)" % (args.config, runs, per)}
+        nth = max(1, min(p.N, os.cpu_count() or 1))
+        per_t, runs_t, _ = cpu_oracle_run(p, netc, budget_s=10.0, max_runs=20, threads=nth)
+        cpu_threaded = {"value": work_units(p) / per_t, "unit": UNIT, "cores": nth, "kind": "oracle, threaded fine sweep",
+                        "sample": "full %s workload, %d fp64 oracle solves with the fine sweep on %d std::threads "
+                                  "(%.3f s each; bitwise the serial result)" % (args.config, runs_t, nth, per_t)}
     if rank == 0:
         from paper_2303_03848_b200 import report
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -423,7 +429,8 @@ def main():
                 "fine_point_steps_executed_per_s": float(p.B) * p.M * p.fine_steps * sum(p.N - k + 1 for k in range(1, K + 1))
                 / (ph["ms_fine"] / 1e3) if ph["ms_fine"] > 0 else None,
                 "eq8_bound_context": None,
-                "roofline": roof, "roofline_fine_sweep_c3": fine_c3, "cpu_baseline": cpu, "e2e": e2e,
+                "roofline": roof, "roofline_fine_sweep_c3": fine_c3, "cpu_baseline": cpu,
+                "cpu_baseline_threaded": cpu_threaded, "e2e": e2e,
                 "gpu_launches": launches,
                 "clocks": clk.summary()}
         if serial_ms and ph["ms_coarse"] > 0:

@@ -32,7 +32,7 @@ def build(force: bool = False) -> str:
         os.path.getmtime(s) > os.path.getmtime(_LIB) for s in (_SRC, _HDR))
     if force or stale:
         tmp = _LIB + ".tmp%d" % os.getpid()
-        subprocess.check_call(["g++", "-O2", "-std=c++17", "-ffp-contract=off", "-fPIC", "-shared",
+        subprocess.check_call(["g++", "-O2", "-std=c++17", "-ffp-contract=off", "-fPIC", "-shared", "-pthread",
                                "-Wall", "-o", tmp, _SRC])
         os.replace(tmp, _LIB)
     return _LIB
@@ -72,6 +72,8 @@ def lib():
                 getattr(L, pre + "serial_fine").argtypes = [C.POINTER(_Problem), dp, dp]
                 getattr(L, pre + "parareal").argtypes = [C.POINTER(_Problem), C.POINTER(_Net), dp, dp, dp,
                                                          C.POINTER(C.c_int), dp]
+            L.or64_parareal_mt.argtypes = [C.POINTER(_Problem), C.POINTER(_Net), dp, dp, dp, C.POINTER(C.c_int), dp,
+                                           C.c_int]
             L.or64_theta_step.argtypes = [C.POINTER(_Problem), C.c_int, C.c_double, C.c_double, C.c_double, dp]
             L.or64_payoff.argtypes = [C.POINTER(_Problem), dp]
             L.or64_payoff.restype = None
@@ -221,8 +223,9 @@ def serial_fine(p, V_T=None, prec: int = 64) -> np.ndarray:
     return U
 
 
-def parareal(p, net=None, V_T=None, prec: int = 64, history: bool = False):
-    """Eq. (7) with schedule Q12.  Returns (U[N+1][B][M], delta[K], K, hist or None)."""
+def parareal(p, net=None, V_T=None, prec: int = 64, history: bool = False, threads: int = 1):
+    """Eq. (7) with schedule Q12.  Returns (U[N+1][B][M], delta[K], K, hist or None).
+    threads > 1 (fp64 only): the fine sweep's slices on that many std::threads, bitwise the same."""
     keep = _Keep()
     s = _problem(p, keep)
     sn = _net(net, keep)
@@ -231,8 +234,10 @@ def parareal(p, net=None, V_T=None, prec: int = 64, history: bool = False):
     delta = np.zeros(p.max_iter)
     K = C.c_int(0)
     hist = np.zeros((p.max_iter + 1, p.N + 1, p.B, p.M)) if history else None
-    _ok(getattr(lib(), "or%d_parareal" % prec)(C.byref(s), C.byref(sn) if sn is not None else None,
-                                                  _dp(vt), _dp(U), _dp(delta), C.byref(K), _dp(hist)),
-        "parareal")
+    args = (C.byref(s), C.byref(sn) if sn is not None else None, _dp(vt), _dp(U), _dp(delta), C.byref(K), _dp(hist))
+    if threads > 1 and prec == 64:
+        _ok(lib().or64_parareal_mt(*args, int(threads)), "parareal")
+    else:
+        _ok(getattr(lib(), "or%d_parareal" % prec)(*args), "parareal")
     k = K.value
     return U, delta[:k].copy(), k, (hist[:k + 1] if history else None)

@@ -15,6 +15,7 @@
 
 #include <cmath>
 #include <cstring>
+#include <thread>
 #include <vector>
 
 namespace {
@@ -242,9 +243,12 @@ int serial_fine(const or_problem *p, const double *V_T, double *Uout) {
 //           for n = k..N-1: g = G(U^k_n); U^k_{n+1} = g + (F^_n - G^_n); G^_n = g
 //           delta^k = max_{n=k..N} max_b ||U^k_n - U^{k-1}_n|| / ||U^k_n||  (Q13)
 //           stop if delta^k < tol or k = max_iter (K = k counts fine sweeps, Q14)
+// nthreads > 1: the fine sweep's slices (independent) run on std::threads, slice n on
+// thread n mod nthreads -- the CPU analog of the paper's one-process-per-slice fine propagation.
+// Every slice is computed by the same code on its own data, so results are bitwise the serial ones.
 template <class R>
 int parareal(const or_problem *p, const or_net *net, const double *V_T, double *Uout,
-             double *delta, int *iterations, double *hist) {
+             double *delta, int *iterations, double *hist, int nthreads = 1) {
   if (check_parareal(p)) return 1;
   if (p->coarse == 0 && !net) return 1;
   const int N = p->N, M = p->M, B = p->B;
@@ -261,10 +265,26 @@ int parareal(const or_problem *p, const or_net *net, const double *V_T, double *
   int K = 0;
   for (int k = 1; k <= p->max_iter; ++k) {
     Uold = U;
-    for (int n = k - 1; n < N; ++n) {
-      std::memcpy(&Fh[n * sz], &Uold[n * sz], sz * sizeof(R));
-      const int st = F<R>(p, n, &Fh[n * sz]);
-      if (st) return st;
+    if (nthreads <= 1) {
+      for (int n = k - 1; n < N; ++n) {
+        std::memcpy(&Fh[n * sz], &Uold[n * sz], sz * sizeof(R));
+        const int st = F<R>(p, n, &Fh[n * sz]);
+        if (st) return st;
+      }
+    } else {
+      std::vector<int> sts(nthreads, 0);
+      std::vector<std::thread> pool;
+      for (int t = 0; t < nthreads; ++t)
+        pool.emplace_back([&, t]() {
+          for (int n = k - 1 + t; n < N; n += nthreads) {
+            std::memcpy(&Fh[n * sz], &Uold[n * sz], sz * sizeof(R));
+            const int st = F<R>(p, n, &Fh[n * sz]);
+            if (st) { sts[t] = st; return; }
+          }
+        });
+      for (auto &th : pool) th.join();
+      for (int st : sts)
+        if (st) return st;
     }
     std::memcpy(&U[k * sz], &Fh[(k - 1) * sz], sz * sizeof(R));
     for (int n = k; n < N; ++n) {
@@ -394,6 +414,10 @@ int or64_parareal(const or_problem *p, const or_net *net, const double *V_T, dou
 int or32_parareal(const or_problem *p, const or_net *net, const double *V_T, double *U,
                   double *delta, int *iterations, double *hist) {
   return parareal<float>(p, net, V_T, U, delta, iterations, hist);
+}
+int or64_parareal_mt(const or_problem *p, const or_net *net, const double *V_T, double *U,
+                     double *delta, int *iterations, double *hist, int nthreads) {
+  return parareal<double>(p, net, V_T, U, delta, iterations, hist, nthreads);
 }
 
 }  // extern "C"

@@ -87,6 +87,9 @@ int or64_parareal(const or_problem *p, const or_net *net, const double *V_T,
                   double *U, double *delta, int *iterations, double *hist);
 int or32_parareal(const or_problem *p, const or_net *net, const double *V_T,
                   double *U, double *delta, int *iterations, double *hist);
+/* or64_parareal with the fine sweep's slices on nthreads std::threads (bitwise the serial result) */
+int or64_parareal_mt(const or_problem *p, const or_net *net, const double *V_T, double *U,
+                     double *delta, int *iterations, double *hist, int nthreads);
 
 #ifdef __cplusplus
 }

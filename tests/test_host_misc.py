@@ -51,3 +51,15 @@ def test_configs_match_baseline():
     assert (c["C5"].M, c["C5"].N) == (1 << 18, 64)
     for p in c.values():
         assert p.fine_steps == 100 and p.fine_theta == 1.0 and p.T == 1.0
+
+
+def test_oracle_threaded_fine_is_bitwise_serial():
+    """The threaded-fine CPU baseline (SURVEY 8(d)): slices of each fine sweep on std::threads give
+    exactly the serial oracle's iterates and deltas (each slice is the same code on its own data)."""
+    import oracle
+    for cfg in (dict(coarse=synth.COARSE_PINN), dict(coarse=synth.COARSE_IMPLICIT_EULER, coarse_steps=2)):
+        p = synth.single(64, 7, max_iter=3, tol=0.0, **cfg)
+        net = synth.kaiming_net(synth.PINN_3x20, seed=4) if cfg["coarse"] == synth.COARSE_PINN else None
+        a = oracle.parareal(p, net, history=True)
+        b = oracle.parareal(p, net, history=True, threads=3)
+        assert a[2] == b[2] and np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and np.array_equal(a[3], b[3])
