@@ -213,6 +213,9 @@ def roofline(p, ph, K, world, rank, pk, pk_src, clk_mhz, n_sm, synth, dims=None,
             piped = ph["ms_fine"] == ph["ms_coarse"]  # the pipelined schedule reports its overlapped time in both
             roof = {"kernel": "k_parareal_pipe (pipelined schedule; fine role = K1, fp64)" if piped
                     else "k_fine_sweep (resident K1, fp64)", "bound": "alu",
+                    "note": "latency-bound at this size: each implicit step is two dependent scans over "
+                            "one system per CTA (0.5 us/step), one CTA per slice on 148 SMs; the fraction "
+                            "of the fp64 pipe is small by construction (DESIGN.md 6, 11)",
                     "achieved": 9.0 * pt_steps / sweep_s / 1e12, "peak": n_sm * 64 * 2 * clk_mhz * 1e6 / 1e12,
                     "unit": "TFLOP/s", "peak_source": "fp64 pipe: %d SMs x 64 FMA/clk x 2 x %.0f MHz (DESIGN.md)"
                     % (n_sm, clk_mhz), "work_per_unit": "9 fp64 flop per point-step", "launch_unit": "one sweep"}
