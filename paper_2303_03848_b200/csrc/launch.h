@@ -19,8 +19,13 @@ bool pinn_smem_supported(int IN, int W, int act);
 int pinn_smem_pts(int W);
 cudaError_t pinn_smem_prepare(int IN, int W, int act, int smem_bytes);
 cudaError_t launch_pinn_smem(int IN, int W, int act, const PinnArgs &a, dim3 grid, size_t smem, cudaStream_t s);
-// K3 latency mode: kPinnSplitG threads per point (pinn_smem.cu)
+// K3 latency mode (pinn_smem.cu): kPinnSplitG threads per point for 20-wide nets (shuffle
+// exchange); pinn_split_G(W) threads per point (group kernels, shared-memory exchange) for
+// 32-, 50- and 64-wide nets; pinn_split_ppc(W) points per 128-thread CTA
 constexpr int kPinnSplitG = 4;
+constexpr int kPinnSplitMinPPC = 4;  // the fewest points per CTA of any latency-mode kernel
+int pinn_split_G(int W);
+int pinn_split_ppc(int W);
 bool pinn_split_supported(int IN, int W, int act);
 cudaError_t pinn_split_prepare(int IN, int W, int act, int smem_bytes);
 cudaError_t launch_pinn_split(int IN, int W, int act, const PinnArgs &a, dim3 grid, size_t smem, cudaStream_t s);

@@ -96,9 +96,13 @@ __global__ void k_delta_multi(const double *partials, size_t pstride, int B, int
   if ((threadIdx.x & 31) == 0) atomicMax(dmax + (k - 1), v);
 }
 
+// Up to kDeltaSeqMax chunks a thread sums a row's chunks in index order (k_delta, k_delta_multi:
+// the same order in the blocking and pipelined schedules; unused chunks are zero and leave the
+// sums bitwise unchanged), beyond that a CTA per row does (k_delta_wide).
+constexpr int kDeltaSeqMax = 256;
 cudaError_t launch_delta_multi(const double *partials, size_t pstride, int B, int nch, int N, int K,
                                unsigned long long *dmax, cudaStream_t s) {
-  if (nch > 32) return cudaErrorInvalidValue;  // (the pipelined schedule runs at most 32 chunks)
+  if (nch > kDeltaSeqMax) return cudaErrorInvalidValue;  // (the pipelined schedule runs small grids)
   dim3 grid((N * B + 255) / 256, K);
   k_delta_multi<<<grid, 256, 0, s>>>(partials, pstride, B, nch, N, K, dmax);
   return cudaGetLastError();
@@ -107,7 +111,7 @@ cudaError_t launch_delta_multi(const double *partials, size_t pstride, int B, in
 cudaError_t launch_delta(const double *partials, int B, int nch, int ln_lo, int ln_hi, unsigned long long *dmax,
                          cudaStream_t s) {
   const int total = (ln_hi - ln_lo + 1) * B;
-  if (nch > 32)
+  if (nch > kDeltaSeqMax)
     k_delta_wide<<<total, 128, 0, s>>>(partials, B, nch, ln_lo, dmax);
   else
     k_delta<<<(total + 255) / 256, 256, 0, s>>>(partials, B, nch, ln_lo, ln_hi, dmax);

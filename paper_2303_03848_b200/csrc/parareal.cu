@@ -141,6 +141,7 @@ struct pr_ctx {
   int IN = 4, W = 0, LH = 0, act = 0, nfloats = 0;
   float cs[4] = {1, 1, 1, 1}, out_scale = 1;
   float *d_wts = nullptr;
+  float *d_wgrp = nullptr;   // the packed weights with the hidden matrices in the group-kernel order
   std::vector<float> h_wts;  // packed copy for the parameter-space kernels
   int tc = 0;                // PR_PREC_FP16_TC / PR_PREC_BF16_TC: K4 (tensor cores), else 0
   float *d_tcp = nullptr;    // K4 compact fp32 parameters
@@ -519,13 +520,17 @@ void dispatch_res(bool chain, int M, const pr::ResidentArgs &a, int nsys, cudaSt
 
 // ---------------------------------------------------------------- PINN launches
 // Few grid points (B·M ≤ kSplitMaxPoints): the coarse chain is latency-bound, so the latency
-// mode (kPinnSplitG threads per point) runs it; otherwise constant-bank weights when instantiated,
-// else shared-memory weights.  PR_OPT_PINN_KERNEL: 0 auto, 1 shared memory, 2 latency mode.
+// mode (kPinnSplitG threads per point for 20-wide nets; pinn_split_G(W) for the group kernels,
+// auto only while B·M ≤ kGroupMaxPoints, where one thread per point leaves most SMs idle) runs
+// it; otherwise constant-bank weights when instantiated, else shared-memory weights.
+// PR_OPT_PINN_KERNEL: 0 auto, 1 shared memory, 2 latency mode.
 constexpr long kSplitMaxPoints = 65536;
+constexpr long kGroupMaxPoints = 16384;
 bool split_allowed(const pr_ctx *c) { return (long)c->B * c->M <= kSplitMaxPoints; }
 bool use_split_pinn(const pr_ctx *c) {
   if (c->tc || c->opt_pinn_kernel == 1) return false;
   if (c->opt_pinn_kernel == 0 && !split_allowed(c)) return false;
+  if (c->opt_pinn_kernel == 0 && c->W != 20 && (long)c->B * c->M > kGroupMaxPoints) return false;
   return pr::pinn_split_supported(c->IN, c->W, c->act);
 }
 bool use_param_pinn(const pr_ctx *c) {
@@ -566,9 +571,11 @@ pr_status launch_pinn(pr_ctx *c, const pr::PinnArgs &a) {
     return PR_OK;
   }
   if (use_split_pinn(c)) {
-    constexpr int ppc = kPinnTPB / pr::kPinnSplitG;  // points per CTA
+    const int ppc = pr::pinn_split_ppc(c->W);  // points per CTA
     dim3 grid((c->M + ppc - 1) / ppc, c->B);
-    pr::launch_pinn_split(c->IN, c->W, c->act, a, grid, (size_t)c->nfloats * sizeof(float), c->stream);
+    pr::PinnArgs t = a;
+    if (c->W != 20) t.wts = c->d_wgrp;  // group kernels: hidden matrices in the group order
+    pr::launch_pinn_split(c->IN, c->W, c->act, t, grid, (size_t)c->nfloats * sizeof(float), c->stream);
     LAUNCHED();
     return PR_OK;
   }
@@ -799,14 +806,15 @@ pr_status solve_pipelined(pr_ctx *c) {
   pa.r.D = c->D;
   pa.r.Fk = c->Fk;
   pa.g = pinn_args(c);
+  if (use_split_pinn(c) && c->W != 20) pa.g.wts = c->d_wgrp;  // group chain: group-order weights
   pa.g.U = c->U;
   pa.g.Gh = c->Gh;
   pa.g.D = c->D;
   pa.g.Fcopy = c->Fk;
   pa.N = c->N;
   pa.K = c->max_iter;
-  const int G = use_split_pinn(c) ? pr::kPinnSplitG : 1;  // threads per point in the chain
-  pa.C = (c->M * G + 127) / 128;                         // chain CTAs per instance (≤ nch)
+  const int ppc = use_split_pinn(c) ? pr::pinn_split_ppc(c->W) : 128;  // chain points per CTA
+  pa.C = (c->M + ppc - 1) / ppc;                                        // chain CTAs per instance (≤ nch)
   pa.partials = c->pipe_partials;
   pa.pstride = c->pipe_pstride;
   pa.wstage = c->pipe_wstage;
@@ -1239,7 +1247,7 @@ pr_status parareal_init(const pr_problem *p, const pr_dist *dist, pr_ctx **out) 
   // δ partial chunks per (slice, instance): upper bound over every producer (PINN CTAs with one
   // point per thread, 256-wide copy blocks, streamed tiles, one resident system)
   c->nch = std::max(1, (c->M + kPinnTPB - 1) / kPinnTPB);
-  if (split_allowed(c)) c->nch = std::max(1, (c->M * pr::kPinnSplitG + kPinnTPB - 1) / kPinnTPB);
+  if (split_allowed(c)) c->nch = std::max(1, (c->M + pr::kPinnSplitMinPPC - 1) / pr::kPinnSplitMinPPC);
   if (dd.world > 1) {
     Nccl &n = nccl();
     if (!n.ok) {
@@ -1357,6 +1365,23 @@ pr_status parareal_load_pinn_weights(pr_ctx *c, int32_t n_linear, const int32_t 
   c->d_wts = nullptr;
   CU(cudaMalloc(&c->d_wts, bytes));
   CU(cudaMemcpy(c->d_wts, pk.data(), bytes, cudaMemcpyHostToDevice));
+  if (c->d_wgrp) cudaFree(c->d_wgrp);
+  c->d_wgrp = nullptr;
+  if (!tc && Wd != 20 && pr::pinn_split_supported(IN, Wd, activation)) {
+    // group kernels (pinn_chain.cuh, mlp_group): hidden matrix l stored as [i][q][k] =
+    // W_l[q·NPT + k][i], so the G threads of a group read consecutive addresses for input i
+    const int G = pr::pinn_split_G(Wd), NPT = Wd / G;
+    std::vector<float> pg(pk);
+    for (int l = 1; l < LH; ++l) {
+      const size_t o = (size_t)Wd * IN + Wd + (size_t)(l - 1) * ((size_t)Wd * Wd + Wd);
+      for (int i = 0; i < Wd; ++i)
+        for (int q = 0; q < G; ++q)
+          for (int k = 0; k < NPT; ++k)
+            pg[o + ((size_t)i * G + q) * NPT + k] = pk[o + (size_t)(q * NPT + k) * Wd + i];
+    }
+    CU(cudaMalloc(&c->d_wgrp, bytes));
+    CU(cudaMemcpy(c->d_wgrp, pg.data(), bytes, cudaMemcpyHostToDevice));
+  }
   c->h_wts = pk;
   c->IN = IN;
   c->W = Wd;
@@ -1561,6 +1586,7 @@ void parareal_free(pr_ctx *c) {
   cudaFree(c->d_K);
   cudaFree(c->d_r);
   cudaFree(c->d_wts);
+  cudaFree(c->d_wgrp);
   cudaFree(c->d_tcp);
   cudaFree(c->d_wh);
   if (c->own_ws) cudaFree(c->ws);

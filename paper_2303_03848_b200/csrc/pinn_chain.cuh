@@ -138,15 +138,19 @@ __device__ __forceinline__ void pinn_chain_body(const PinnArgs &a, Eval ev) {
   const float gscale = (float)(Lb * (double)a.out_scale);
   const float invL = (float)(1.0 / Lb);
   const size_t sstride = (size_t)a.B * a.Mp;
-  const bool leader = (G == 1) || (threadIdx.x % G == 0);
+  // G > 1: 32/G groups per warp (lanes beyond them idle when G does not divide 32)
+  constexpr int GPW = 32 / G;
+  const int lane_ = threadIdx.x & 31;
+  const bool active = (G == 1) || lane_ < GPW * G;
+  const bool leader = (G == 1) || (active && lane_ % G == 0);
   int j[PTS];
   bool ok[PTS];
   float s_over_L[PTS], u[PTS];
 #pragma unroll
   for (int p = 0; p < PTS; ++p) {
     j[p] = (G == 1) ? blockIdx.x * (blockDim.x * PTS) + p * blockDim.x + threadIdx.x
-                    : blockIdx.x * (blockDim.x / G) + threadIdx.x / G;
-    ok[p] = j[p] < a.M;
+                    : blockIdx.x * ((blockDim.x >> 5) * GPW) + (threadIdx.x >> 5) * GPW + lane_ / G;
+    ok[p] = active && j[p] < a.M;
     // S_j / L_b = j dS / L_b with dS = L_b / (M+1)  (reading Q4, Q8)
     const double dS = Lb / (a.M + 1);
     s_over_L[p] = (float)(((j[p] + 1) * dS) / Lb);
@@ -324,6 +328,113 @@ __global__ void __launch_bounds__(128) k_pinn_chain_split(PinnArgs a) {
   __syncthreads();
   static_assert(W % G == 0 && (G & (G - 1)) == 0, "G must be a power of two dividing W");
   auto ev = [&](const float (&x)[1][IN], float (&y)[1]) { y[0] = mlp_split<IN, W, G, ACT>(sw, a.LH, x[0]); };
+  pinn_chain_body<IN, 1, decltype(ev), G>(a, ev);
+}
+
+// Latency mode for wider nets (the paper's 10×50): G threads per point (GPW = 32/G groups
+// per warp; W % G == 0), thread q owning the NPT = W/G consecutive neurons q·NPT … of every
+// layer.  After each layer the group's activations are exchanged through a per-group row of
+// shared memory (one store per owned neuron, W/4 broadcast float4 loads) instead of W shuffles;
+// weights are read from global memory through L1, the hidden matrices host-permuted to
+// [i][q][k] so a group's loads for input i are one coalesced segment (row-major rows would put
+// each lane on its own cache line: G lines per load), so the kernel needs no dynamic shared
+// memory and many chain CTAs can be co-resident (pipe.cu).
+// Two accumulators per neuron halve the FMA dependency chain.  The output layer's G partial
+// sums are added in lane order (deterministic).
+template <int W>
+struct GroupRow {
+  static constexpr int kPad = (W + 3) / 4 * 4;  // floats per group row (16-B aligned)
+};
+template <int IN, int W, int G, int ACT>
+__device__ __forceinline__ float mlp_group(const float *__restrict__ gw, int LH, const float (&x)[IN],
+                                           float *__restrict__ row, bool active) {
+  static_assert(W % G == 0 && G <= 32, "G must divide W");
+  constexpr int NPT = W / G;
+  constexpr int KP = GroupRow<W>::kPad;
+  const int q = (threadIdx.x & 31) % G;
+  float own[NPT];
+#pragma unroll
+  for (int k = 0; k < NPT; ++k) {
+    const int o = q * NPT + k;
+    float z = __ldg(gw + W * IN + o);
+#pragma unroll
+    for (int i = 0; i < IN; ++i) z = fmaf(__ldg(gw + o * IN + i), x[i], z);
+    own[k] = act<ACT>(z);
+  }
+  const float *lw = gw + W * IN + W;
+#pragma unroll 1
+  for (int l = 1; l < LH; ++l) {
+    __syncwarp();
+    if (active) {
+#pragma unroll
+      for (int k = 0; k < NPT; ++k) row[q * NPT + k] = own[k];
+    }
+    __syncwarp();
+    float h[KP];
+#pragma unroll
+    for (int i = 0; i < KP; i += 4) {
+      const float4 v = *reinterpret_cast<const float4 *>(row + i);
+      h[i] = v.x; h[i + 1] = v.y; h[i + 2] = v.z; h[i + 3] = v.w;
+    }
+    // hidden matrix in the group order [i][q][k] (host-packed): for each input i the group's
+    // lanes read consecutive addresses (coalesced), NPT weights per lane
+    float z0[NPT], z1[NPT];
+#pragma unroll
+    for (int k = 0; k < NPT; ++k) {
+      z0[k] = __ldg(lw + W * W + q * NPT + k);
+      z1[k] = 0.f;
+    }
+    const float *wq = lw + q * NPT;
+#pragma unroll
+    for (int i = 0; i < W; ++i) {
+      float wv[NPT];
+      if constexpr (NPT % 4 == 0) {
+#pragma unroll
+        for (int k = 0; k < NPT; k += 4) {
+          const float4 t = __ldg(reinterpret_cast<const float4 *>(wq + i * W + k));
+          wv[k] = t.x; wv[k + 1] = t.y; wv[k + 2] = t.z; wv[k + 3] = t.w;
+        }
+      } else if constexpr (NPT % 2 == 0) {
+#pragma unroll
+        for (int k = 0; k < NPT; k += 2) {
+          const float2 t = __ldg(reinterpret_cast<const float2 *>(wq + i * W + k));
+          wv[k] = t.x; wv[k + 1] = t.y;
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < NPT; ++k) wv[k] = __ldg(wq + i * W + k);
+      }
+#pragma unroll
+      for (int k = 0; k < NPT; ++k) {
+        if (i & 1) z1[k] = fmaf(wv[k], h[i], z1[k]);
+        else z0[k] = fmaf(wv[k], h[i], z0[k]);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < NPT; ++k) own[k] = act<ACT>(z0[k] + z1[k]);
+    lw += W * W + W;
+  }
+  float y = 0.f;
+#pragma unroll
+  for (int k = 0; k < NPT; ++k) y = fmaf(__ldg(lw + q * NPT + k), own[k], y);
+  __syncwarp();
+  if (active) row[q] = y;
+  __syncwarp();
+  float s = __ldg(lw + W);
+#pragma unroll
+  for (int r = 0; r < G; ++r) s += row[r];
+  return s;
+}
+
+template <int IN, int W, int G, int ACT>
+__global__ void __launch_bounds__(128) k_pinn_chain_group(PinnArgs a) {
+  constexpr int GPW = 32 / G, KP = GroupRow<W>::kPad;
+  __shared__ __align__(16) float xrow[4][GPW][KP];
+  const int lane = threadIdx.x & 31;
+  const int grp = lane / G < GPW ? lane / G : GPW - 1;  // idle lanes read (never write) the last row
+  const bool active = lane < GPW * G;
+  float *row = &xrow[threadIdx.x >> 5][grp][0];
+  auto ev = [&](const float (&x)[1][IN], float (&y)[1]) { y[0] = mlp_group<IN, W, G, ACT>(a.wts, a.LH, x[0], row, active); };
   pinn_chain_body<IN, 1, decltype(ev), G>(a, ev);
 }
 

@@ -1,6 +1,7 @@
 // pinn_smem.cu — K3 with shared-memory weights (any instantiated width, runtime depth).
 #include "launch.h"
 #include "pinn_chain.cuh"
+#include <stdlib.h>
 
 namespace pr {
 typedef void (*SmemKernel)(PinnArgs);
@@ -40,21 +41,35 @@ namespace pr {
 // latency mode (G = 4 threads per point), shared-memory weights
 typedef void (*SplitKernel)(PinnArgs);
 static SplitKernel split_kernel(int IN, int W, int act) {
+  if (IN == 4 && W == 50 && pinn_split_G(50) == 25)
+    return act ? k_pinn_chain_group<4, 50, 25, 1> : k_pinn_chain_group<4, 50, 25, 0>;
+  if (IN == 4 && W == 50) return act ? k_pinn_chain_group<4, 50, 10, 1> : k_pinn_chain_group<4, 50, 10, 0>;
+  if (IN == 4 && W == 64 && act == 0) return k_pinn_chain_group<4, 64, 16, 0>;
+  if (IN == 4 && W == 32 && act == 0) return k_pinn_chain_group<4, 32, 8, 0>;
   if (W != 20) return nullptr;
   if (IN == 4) return act ? k_pinn_chain_split<4, 20, 4, 1> : k_pinn_chain_split<4, 20, 4, 0>;
   if (IN == 2 && act == 0) return k_pinn_chain_split<2, 20, 4, 0>;
   return nullptr;
 }
 bool pinn_split_supported(int IN, int W, int act) { return split_kernel(IN, W, act) != nullptr; }
+int pinn_split_G(int W) {
+  static const int g50 = getenv("PR_PINN_G50") && atoi(getenv("PR_PINN_G50")) == 25 ? 25 : 10;
+  return W == 20 ? 4 : W == 32 ? 8 : W == 50 ? g50 : W == 64 ? 16 : 0;
+}
+int pinn_split_ppc(int W) {
+  const int G = pinn_split_G(W);
+  return G ? 4 * (32 / G) : 0;
+}
 cudaError_t pinn_split_prepare(int IN, int W, int act, int smem_bytes) {
   SplitKernel k = split_kernel(IN, W, act);
   if (!k) return cudaErrorInvalidValue;
+  if (W != 20) return cudaSuccess;  // group kernels: weights through L1, no dynamic shared memory
   return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
 }
 cudaError_t launch_pinn_split(int IN, int W, int act, const PinnArgs &a, dim3 grid, size_t smem, cudaStream_t s) {
   SplitKernel k = split_kernel(IN, W, act);
   if (!k) return cudaErrorInvalidValue;
-  k<<<grid, 128, smem, s>>>(a);
+  k<<<grid, 128, W == 20 ? smem : 0, s>>>(a);
   return cudaGetLastError();
 }
 }  // namespace pr

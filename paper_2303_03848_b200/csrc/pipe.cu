@@ -35,13 +35,19 @@ __device__ __forceinline__ unsigned long long gtimer() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
-__device__ __forceinline__ int ld_acquire(const int *p) {
+// Flags are polled with relaxed gpu-scope loads: an ld.acquire.gpu compiles to LDG.STRONG.GPU +
+// CCTL.IVALL, i.e. every poll would invalidate the SM's L1 -- and with it the weights the group
+// chains read through L1 (measured: chain 5.6x slower per slice).  Every datum guarded by a flag
+// is read through L2 (ld.global.cg) after the polling loop has observed the flag (the loads are
+// issued only once the flag value has returned), and the producers publish with a release
+// (fence + st.release / red.release), so L1 never has to be invalidated.
+__device__ __forceinline__ int ld_flag(const int *p) {
   int v;
-  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
 __device__ __forceinline__ void wait_geq(const int *p, int target) {
-  while (ld_acquire(p) < target) __nanosleep(20);
+  while (ld_flag(p) < target) __nanosleep(20);
 }
 // after a CTA (or warp) barrier: publish the stores of the threads that reached it
 __device__ __forceinline__ void publish_add(int *p) {
@@ -63,8 +69,10 @@ __device__ __forceinline__ void publish_set(int *p, int v) {
 // The network evaluator: G = kPinnSplitG threads per point (latency mode, W = 20) or one thread
 // per point (shared-memory weights, any instantiated width: the paper's 10×50 net).
 template <int IN, int W, int G, int ACT>
-__device__ __forceinline__ float chain_eval(const float *sw, int LH, const float (&x)[IN]) {
-  if constexpr (G > 1) {
+__device__ __forceinline__ float chain_eval(const float *sw, int LH, const float (&x)[IN], float *row, bool active) {
+  if constexpr (G > 1 && W != 20) {
+    return mlp_group<IN, W, G, ACT>(sw, LH, x, row, active);  // sw = the global weights here
+  } else if constexpr (G > 1) {
     return mlp_split<IN, W, G, ACT>(sw, LH, x);
   } else {
     float xx[1][IN], y[1];
@@ -84,9 +92,14 @@ __device__ void chain_role(const PipeArgs &pa, int k, int b, int chunk, const fl
   const float invL = (float)(1.0 / Lb);
   const size_t sstride = (size_t)a.B * a.Mp;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const bool leader = threadIdx.x % G == 0;
-  const int j = chunk * (blockDim.x / G) + threadIdx.x / G;
-  const bool ok = j < a.M;
+  constexpr int GPW = 32 / G;  // point groups per warp (lanes beyond them idle)
+  const bool active = lane < GPW * G;
+  const bool leader = active && lane % G == 0;
+  const int j = chunk * (NWC * GPW) + wid * GPW + lane / G;
+  const bool ok = active && j < a.M;
+  constexpr bool kGroup = G > 1 && W != 20;
+  __shared__ __align__(16) float xrow[NWC][kGroup ? GPW : 1][kGroup ? GroupRow<W>::kPad : 4];  // group exchange rows
+  float *xr = &xrow[wid][kGroup && lane / G < GPW ? lane / G : (kGroup ? GPW - 1 : 0)][0];
   const double dS = Lb / (a.M + 1);
   const float s_over_L = (float)(((j + 1) * dS) / Lb);
   int *cnt = pa.cnt + (size_t)b * pa.N;
@@ -144,8 +157,8 @@ __device__ void chain_role(const PipeArgs &pa, int k, int b, int chunk, const fl
     auto flags_ready = [&](int n) -> bool {  // lane 0's view, broadcast
       bool r = true;
       if (lane == 0) {
-        r = ld_acquire(fdone + n) >= k;
-        if (r && n + 1 <= pa.N - 1) r = ld_acquire(floaded + n + 1) >= k;
+        r = ld_flag(fdone + n) >= k;
+        if (r && n + 1 <= pa.N - 1) r = ld_flag(floaded + n + 1) >= k;
       }
       return __shfl_sync(0xffffffffu, r ? 1 : 0, 0) != 0;
     };
@@ -178,7 +191,7 @@ __device__ void chain_role(const PipeArgs &pa, int k, int b, int chunk, const fl
         x[0] = tt * a.cs0;
         x[IN - 1] = s_over_L * a.cs1;
       }
-      const float y = chain_eval<IN, W, G, ACT>(sw, a.LH, x);
+      const float y = chain_eval<IN, W, G, ACT>(sw, a.LH, x, xr, active);
       const float g = gscale * y;
       float nv = 0.f;
       double num = 0.0, den = 0.0;
@@ -280,10 +293,14 @@ __global__ void __launch_bounds__(128) k_parareal_pipe(PipeArgs pa) {
   const int per = pa.g.B * pa.C;
   const int nchain = (pa.K + 1) * per;
   if ((int)blockIdx.x < nchain) {
-    for (int i = threadIdx.x; i < pa.g.nfloats; i += blockDim.x) sw[i] = pa.g.wts[i];
-    __syncthreads();
+    const float *w = pa.g.wts;  // group kernels read the weights through L1
+    if (G == 1 || W == 20) {
+      for (int i = threadIdx.x; i < pa.g.nfloats; i += blockDim.x) sw[i] = pa.g.wts[i];
+      __syncthreads();
+      w = sw;
+    }
     const int k = blockIdx.x / per, r = blockIdx.x % per;
-    chain_role<IN, W, G, ACT>(pa, k, r / pa.C, r % pa.C, sw);
+    chain_role<IN, W, G, ACT>(pa, k, r / pa.C, r % pa.C, w);
   } else {
     const int f = blockIdx.x - nchain;
     fine_role<P, CN>(pa, f / pa.g.B, f % pa.g.B);
@@ -306,6 +323,8 @@ static PipeKernel pipe_kernel_c(int M, bool cn) {
 // 10×50 architecture (tanh or ReLU) and 32-wide tanh nets
 static PipeKernel pipe_kernel(int M, bool cn, int IN, int W, int act, bool split) {
   if (split) {
+    if (IN == 4 && W == 50 && pinn_split_G(50) != 10) return nullptr;
+    if (IN == 4 && W == 50) return act ? pipe_kernel_c<4, 50, 10, 1>(M, cn) : pipe_kernel_c<4, 50, 10, 0>(M, cn);
     if (W != 20 || act != 0) return nullptr;
     if (IN == 4) return pipe_kernel_c<4, 20, kPinnSplitG, 0>(M, cn);
     if (IN == 2) return pipe_kernel_c<2, 20, kPinnSplitG, 0>(M, cn);
@@ -326,6 +345,7 @@ cudaError_t launch_parareal_pipe(const PipeArgs &pa, int M, bool cn, int IN, int
                                  size_t smem, cudaStream_t s) {
   PipeKernel k = pipe_kernel(M, cn, IN, W, act, split);
   if (!k) return cudaErrorInvalidValue;
+  if (split && W != 20) smem = 0;  // group chains read the weights through L1
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int dev = 0, nsm = 0, occ = 0;

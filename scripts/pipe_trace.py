@@ -4,9 +4,10 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 os.environ["PR_PIPE_TRACE"] = os.environ.get("PR_PIPE_TRACE", "gpurun_out/pipe_trace.txt")
 from paper_2303_03848_b200 import parareal, synth  # noqa: E402
 theta = float(sys.argv[1]) if len(sys.argv) > 1 else 1.0
+net = synth.PINN_PAPER if "paper" in sys.argv else synth.PINN_3x20
 p = synth.config("C2", coarse=synth.COARSE_PINN, max_iter=3, tol=0.0, fine_theta=theta)
 with parareal.Context(p) as c:
-    c.load_weights(synth.kaiming_net(synth.PINN_3x20, seed=0))
+    c.load_weights(synth.kaiming_net(net, seed=0))
     for _ in range(3):
         U, rep = c.solve()
     print(rep)

@@ -144,9 +144,15 @@ def test_pinn_G_single_slice(dims, act):
 
 @pytest.mark.parametrize("pinn_kernel", [0, 1, 2])
 @pytest.mark.parametrize("dims,act", [(synth.PINN_3x20, synth.ACT_TANH), (synth.PINN_3x20, synth.ACT_RELU),
-                                      ([2, 20, 20, 20, 1], synth.ACT_TANH)])
+                                      ([2, 20, 20, 20, 1], synth.ACT_TANH), (synth.PINN_PAPER, synth.ACT_TANH),
+                                      (synth.PINN_PAPER, synth.ACT_RELU), ([4, 64, 64, 64, 1], synth.ACT_TANH),
+                                      ([4, 32, 32, 32, 1], synth.ACT_TANH)])
 def test_pinn_G_both_weight_paths(pinn_kernel, dims, act):
-    """Constant-bank weights (auto for these shapes) and shared-memory weights agree with the oracle."""
+    """Every evaluator agrees with the oracle: constant-bank weights (auto for small nets at this
+    size), shared-memory weights (one thread per point), and the latency modes (4 threads per
+    point with shuffles for 20-wide nets; groups of W/NPT threads with a shared-memory exchange
+    for 32/50/64-wide nets, including the paper's 10x50 architecture).  M = 3000 gives a
+    ragged last CTA in every mode."""
     p = synth.single(3000, 8)
     net = synth.kaiming_net(dims, seed=11, activation=act)
     U = synth.random_state(1, 3000, seed=12) * 3.0
