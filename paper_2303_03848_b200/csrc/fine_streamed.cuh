@@ -966,6 +966,281 @@ __global__ void __launch_bounds__(H *kSNT) k_pass_res(PassArgs a) {
   if (n > 0) finish((n - 1) & 1);
 }
 
+// ---------------------------------------------------------------- k_pass_res2 (persistent, paired)
+// As k_pass_res, but each thread runs two adjacent 16-point chunks ("virtual threads" v0 = 2t',
+// v1 = 2t'+1 of the tile's kSNT) of each of its systems.  Both chunks' entering values are known
+// up front (E_v + P_v·y_tile), so they are two independent recurrences (twice the ILP per
+// thread); their inputs, outputs and factors are adjacent in the interleaved layout (float2 /
+// double2 accesses: half the load/store instructions); and the per-item work (prefetch, scans,
+// folds, cursors) is paid once per 32 points instead of 16.  The next pass's maps of the two
+// chunks are composed in-thread (in the next pass's order) before the warp scan, and expanded
+// back to per-chunk prefixes after it, so the aggregates keep the per-16-point format every
+// other K2 kernel reads.
+constexpr int kHT = kSNT / 2;   // threads per half (one tile of SP systems)
+constexpr int kNW2 = kHT / 32;  // warps per half
+
+template <int DIR, int SP, int H, int NST>
+__global__ void __launch_bounds__(H *kHT) k_pass_res2(PassArgs a) {
+  constexpr int ND = 1 - DIR;
+  constexpr int SG = SP * H;  // systems per item
+  constexpr int CF = ND == 0 ? 0 : 1;  // the chunk the next pass visits first
+  static_assert(SP <= kNW2, "one look-back warp per system");
+  extern __shared__ __align__(128) unsigned char res_smem_raw[];
+  ResSmem<SP, H, NST> &sm = *reinterpret_cast<ResSmem<SP, H, NST> *>(res_smem_raw);
+  __shared__ __align__(8) uint64_t full[NST];
+  __shared__ double s_yin[2][H][SP];
+  __shared__ double tot[2][H][kNW2][SP + 1];
+  const int t = threadIdx.x, h = t / kHT, tt = t % kHT, lane = t & 31, wl = tt >> 5;
+  const int v0 = 2 * tt;  // this thread's first chunk (index among the tile's kSNT chunks)
+  const unsigned nitems = (unsigned)a.ngroups * (unsigned)a.ntiles;
+  const unsigned lo = (unsigned)(((unsigned long long)blockIdx.x * nitems) / gridDim.x);
+  const unsigned hi = (unsigned)(((unsigned long long)(blockIdx.x + 1) * nitems) / gridDim.x);
+  const size_t nthr = (size_t)a.Mt / kSPS;
+  const int swN = ND == 0 ? wl : kNW2 - 1 - wl;
+  const int slN = ND == 0 ? lane : 31 - lane;
+  const uint64_t pol_stream = policy_evict_first();
+  using Cur = ResCursor<SG>;
+
+  Cur cur, nxt, iss, prev;
+  auto issue = [&](int stage) {
+    mbar_expect_tx(&full[stage], (uint32_t)(SG * kSTile * sizeof(float)));
+    const int tile = iss.template tile<DIR>(a);
+#pragma unroll
+    for (int hh = 0; hh < H; ++hh)
+#pragma unroll
+      for (int q = 0; q < SP; ++q)
+        bulk_g2s(sm.x[stage][hh][q], a.in + (size_t)iss.sys(a, hh * SP + q) * a.Mt + (size_t)tile * kSTile,
+                 kSTile * sizeof(float), &full[stage], pol_stream);
+    iss.step(a);
+  };
+  if (t == 0) {
+    for (int i = 0; i < NST; ++i) mbar_init(&full[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  cur.init(a, lo);
+  nxt = cur;
+  iss = cur;
+  prev = cur;
+  if (t == 0)
+    for (int i = 0; i < NST && lo + i < hi; ++i) issue(i);
+  struct Pre {
+    double E[2][SP], P[2], LA, LB;
+    int W, set;
+  };
+  Pre pre[2];
+  int cb = -1, cset = 0;
+  auto prefetch = [&](const Cur &c, Pre &r) {
+    const int tile = c.template tile<DIR>(a);
+    if (c.b != cb) {
+      cb = c.b;
+      cset = a.fset[cb];
+    }
+    const int set = cset;
+    r.set = set;
+    const size_t thr = (size_t)tile * kSNT + v0;
+#pragma unroll
+    for (int q = 0; q < SP; ++q) {
+      const double2 e = *reinterpret_cast<const double2 *>(a.aggT_cur + (size_t)c.sys(a, h * SP + q) * nthr + thr);
+      r.E[0][q] = e.x;
+      r.E[1][q] = e.y;
+    }
+    const double2 pp = __ldg(reinterpret_cast<const double2 *>(a.f.thrP + ((size_t)DIR * a.nsets + set) * nthr + thr));
+    r.P[0] = pp.x;
+    r.P[1] = pp.y;
+    r.LA = 0.0;
+    r.LB = 1.0;
+    r.W = 0;
+    if (wl >= kNW2 - SP && c.pos > 0) {
+      const int q = kNW2 - 1 - wl;
+      const size_t tb = ((size_t)DIR * a.nsets + set) * a.ntiles;
+      r.W = __ldg(a.f.tileW + tb + c.pos);
+      const int p = c.pos - 1 - lane;
+      if (p >= 0) {
+        r.LA = a.aggL_cur[(size_t)c.sys(a, h * SP + q) * a.ntiles + (DIR == 0 ? p : a.ntiles - 1 - p)];
+        r.LB = __ldg(a.f.tileB + tb + p);
+      }
+    }
+  };
+  // the previous item's exclusive pair prefixes (next-pass order) and its first chunks' maps
+  double qA[SP], qB = 1.0, fA[SP], fB = 1.0;
+  auto finish = [&](int pb) {
+    const int tile = prev.template tile<DIR>(a);
+#pragma unroll
+    for (int q = 0; q < SP; ++q) {
+      double wA = 0.0;
+      for (int k = 0; k < swN; ++k) wA = fma(tot[pb][h][k][SP], wA, tot[pb][h][k][q]);
+      const double eF = fma(qB, wA, qA[q]);  // entering the pair = entering its first chunk
+      const double eS = fma(fB, eF, fA[q]);  // entering the second chunk
+      const int slot = h * SP + q;
+      if (prev.ok(a, slot))
+        *reinterpret_cast<double2 *>(a.aggT_next + (size_t)prev.sys(a, slot) * nthr + (size_t)tile * kSNT + v0) =
+            CF == 0 ? make_double2(eF, eS) : make_double2(eS, eF);
+    }
+    if (tt < SP) {
+      const int q = tt;
+      double T = 0.0;
+      for (int k = 0; k < kNW2; ++k) T = fma(tot[pb][h][k][SP], T, tot[pb][h][k][q]);
+      const int slot = h * SP + q;
+      if (prev.ok(a, slot)) a.aggL_next[(size_t)prev.sys(a, slot) * a.ntiles + tile] = T;
+    }
+  };
+  if (lo < hi) prefetch(nxt, pre[0]);
+  nxt.step(a);
+  if (lo + 1 < hi) prefetch(nxt, pre[1]);
+  nxt.step(a);
+  int fac_tile = -1, fac_set = -1;
+  int n = 0;
+  for (unsigned k = lo; k < hi; ++k, ++n) {
+    const int stage = n % NST;
+    const int pb = n & 1;
+    const uint32_t parity = (uint32_t)(n / NST) & 1u;
+    double E[2][SP], P[2], LA, LB;
+    int W, set;
+    if (n & 1) {
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        P[c] = pre[1].P[c];
+#pragma unroll
+        for (int q = 0; q < SP; ++q) E[c][q] = pre[1].E[c][q];
+      }
+      LA = pre[1].LA; LB = pre[1].LB; W = pre[1].W; set = pre[1].set;
+      if (k + 2 < hi) prefetch(nxt, pre[1]);
+    } else {
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        P[c] = pre[0].P[c];
+#pragma unroll
+        for (int q = 0; q < SP; ++q) E[c][q] = pre[0].E[c][q];
+      }
+      LA = pre[0].LA; LB = pre[0].LB; W = pre[0].W; set = pre[0].set;
+      if (k + 2 < hi) prefetch(nxt, pre[0]);
+    }
+    if (k + 2 < hi) nxt.step(a);
+    const int tile = cur.template tile<DIR>(a);
+    if (wl >= kNW2 - SP) {
+      const int q = kNW2 - 1 - wl;
+      double mA = lane < W ? LA : 0.0, mB = lane < W ? LB : 1.0;
+      compose_window(mA, mB, lane);
+      double y = mA;
+      if (W > 32) y = look_back<DIR>(a, cur.sys(a, h * SP + q), cur.pos, set, lane, 32, mA, mB);  // rare
+      if (lane == 0) s_yin[pb][h][q] = y;
+    }
+    __syncthreads();  // the barrier of the item
+    if (n > 0) {
+      finish(pb ^ 1);
+      if (t == 0 && k - 1 + NST < hi) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue((n - 1) % NST);
+      }
+    }
+    if (tile != fac_tile || set != fac_set) {
+      const double *ipg = a.f.ip + (size_t)set * a.Mt + (size_t)tile * kSTile;
+      const double c0 = __ldg(a.f.coef + 2 * set), c1 = __ldg(a.f.coef + 2 * set + 1);
+      constexpr int kPer = kSTile / (H * kHT);
+      double ipl[kPer];
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) ipl[u] = __ldg(ipg + t + u * H * kHT);
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) {
+        const int e = t + u * H * kHT;
+        const int j = tile * kSTile + (e % kSNT) * kSPS + e / kSNT;
+        double mtj, cjj;
+        factors<true>(c0, c1, (double)(j + 1), ipl[u], j, a.M, mtj, cjj);
+        sm.ip[e] = ipl[u];
+        sm.mt[e] = mtj;
+        sm.cj[e] = cjj;
+      }
+      fac_tile = tile;
+      fac_set = set;
+      __syncthreads();
+    }
+    double v[2][SP];
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+#pragma unroll
+      for (int q = 0; q < SP; ++q) v[c][q] = fma(P[c], s_yin[pb][h][q], E[c][q]);
+    mbar_wait(&full[stage], parity);
+    const int j0 = tile * kSTile + v0 * kSPS;  // chunk 1 starts at j0 + kSPS
+    const double *ips = sm.ip + v0, *mts = sm.mt + v0, *cjs = sm.cj + v0;
+    double An[2][SP], Pn[2] = {1.0, 1.0};
+    float *op[SP];
+    const float *xs[SP];
+    bool okq[SP];
+#pragma unroll
+    for (int q = 0; q < SP; ++q) {
+      An[0][q] = 0.0;
+      An[1][q] = 0.0;
+      okq[q] = cur.ok(a, h * SP + q);
+      op[q] = a.out + (size_t)cur.sys(a, h * SP + q) * a.Mt + (size_t)tile * kSTile + v0;
+      xs[q] = sm.x[stage][h][q] + v0;
+    }
+    auto run = [&](auto bc_tag) {
+      constexpr bool BC = decltype(bc_tag)::value;
+      double bcv[SP];
+      const int ibc0 = a.M - 1 - j0, ibc1 = ibc0 - kSPS;
+#pragma unroll
+      for (int q = 0; q < SP; ++q)
+        bcv[q] = BC ? bc_term(a, cur.b, a.n_base + a.ln0 + cur.lg * SG + h * SP + q, a.step_m + DIR) : 0.0;
+#pragma unroll
+      for (int ii = 0; ii < kSPS; ++ii) {
+        const int i = DIR == 0 ? ii : kSPS - 1 - ii;
+        const double2 ipj = *reinterpret_cast<const double2 *>(ips + i * kSNT);
+        const double2 mtj = *reinterpret_cast<const double2 *>(mts + i * kSNT);
+        const double2 cjj = *reinterpret_cast<const double2 *>(cjs + i * kSNT);
+        const double ipc[2] = {ipj.x, ipj.y};
+        const double f1[2] = {DIR == 0 ? mtj.x : cjj.x, DIR == 0 ? mtj.y : cjj.y};  // this pass's multiplier
+        const double f2[2] = {DIR == 0 ? cjj.x : mtj.x, DIR == 0 ? cjj.y : mtj.y};  // the next pass's
+#pragma unroll
+        for (int q = 0; q < SP; ++q) {
+          const float2 xin2 = *reinterpret_cast<const float2 *>(xs[q] + i * kSNT);
+          const double xin[2] = {(double)xin2.x, (double)xin2.y};
+          float o[2];
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            const bool isbc = BC && i == (c == 0 ? ibc0 : ibc1);
+            if (DIR == 0) {
+              const double r = isbc ? xin[c] + bcv[q] : xin[c];
+              v[c][q] = fma(-f1[c], v[c][q], r * ipc[c]);
+              An[c][q] = fma(v[c][q], Pn[c], An[c][q]);
+            } else {
+              v[c][q] = fma(-f1[c], v[c][q], xin[c]);
+              const double r = isbc ? v[c][q] + bcv[q] : v[c][q];
+              An[c][q] = fma(r * ipc[c], Pn[c], An[c][q]);
+            }
+            o[c] = (float)v[c][q];
+          }
+          if (okq[q]) __stcs(reinterpret_cast<float2 *>(op[q] + i * kSNT), make_float2(o[0], o[1]));
+        }
+        Pn[0] *= -f2[0];
+        Pn[1] *= -f2[1];
+      }
+    };
+    if (j0 <= a.M - 1 && a.M - 1 < j0 + 2 * kSPS) run(std::true_type{});
+    else run(std::false_type{});
+    // next-pass map of the pair (first chunk CF, then the other), in-warp scan now
+    constexpr int CS = 1 - CF;
+    double pA[SP];
+#pragma unroll
+    for (int q = 0; q < SP; ++q) {
+      pA[q] = fma(Pn[CS], An[CF][q], An[CS][q]);
+      fA[q] = An[CF][q];
+    }
+    double pB = Pn[CS] * Pn[CF];
+    fB = Pn[CF];
+    warp_scan<ND, SP>(pA, pB, qA, qB, lane);
+    if (slN == 31) {
+#pragma unroll
+      for (int q = 0; q < SP; ++q) tot[pb][h][swN][q] = pA[q];
+      tot[pb][h][swN][SP] = pB;
+    }
+    prev = cur;
+    cur.step(a);
+  }
+  __syncthreads();
+  if (n > 0) finish((n - 1) & 1);
+}
+
 // U_k := F̂_{k−1} with the δ partial of slice k (reading Q12), elementwise.
 __global__ void k_copy_delta(float *Uk, const float *F, int M, int Mp, double *partials, int B, int nch) {
   __shared__ double red[64];
@@ -1003,49 +1278,57 @@ static int env_int(const char *name, int dflt) {
 }
 // tuning overrides: PR_K2_PIPE=0 (no persistent kernel), PR_K2_SP (1|2), PR_K2_H (1|2), PR_K2_STAGES (2|3|4)
 struct ResConfig {
-  int enabled, sp, h, nst;
+  int enabled, sp, h, nst, pair;
 };
 static ResConfig res_config() {
   static const ResConfig c = [] {
     ResConfig r;
     r.enabled = env_int("PR_K2_PIPE", 1);
     r.sp = env_int("PR_K2_SP", 2) == 1 ? 1 : 2;
-    r.h = env_int("PR_K2_H", 2) == 1 ? 1 : 2;
+    r.h = env_int("PR_K2_H", 2);
+    r.h = r.h == 1 ? 1 : r.h == 4 ? 4 : 2;
     const int n = env_int("PR_K2_STAGES", 2);  // (SP, H, NST) = (2, 2, 2): best measured at C3
     r.nst = n == 3 || n == 4 ? n : 2;
+    r.pair = env_int("PR_K2_PAIR", 1);  // k_pass_res2 (two chunks per thread); 0: k_pass_res
+    if (r.pair && r.sp == 2 && r.h == 4) r.h = 2;
     return r;
   }();
   return c;
 }
 
-template <int DIR, int SP, int H, int NST>
+template <int DIR, int SP, int H, int NST, bool PAIR>
 static cudaError_t launch_res_dir(PassArgs a, cudaStream_t s) {
   static int grid_cap = 0;
   constexpr size_t smem = res_smem_bytes<SP, H, NST>();
+  constexpr int nthreads = PAIR ? H * kHT : H * kSNT;
+  auto kern = PAIR ? k_pass_res2<DIR, SP, H, NST> : k_pass_res<DIR, SP, H, NST>;
   if (grid_cap == 0) {
-    cudaError_t e =
-        cudaFuncSetAttribute(k_pass_res<DIR, SP, H, NST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int dev = 0, nsm = 0, occ = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_pass_res<DIR, SP, H, NST>, H * kSNT, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, nthreads, smem);
     if (e != cudaSuccess) return e;
     grid_cap = nsm * (occ > 0 ? occ : 1);
   }
   a.ngroups = a.B * ((a.nsl + SP * H - 1) / (SP * H));
   const long long nitems = (long long)a.ngroups * a.ntiles;
   const unsigned grid = (unsigned)(nitems < grid_cap ? nitems : grid_cap);
-  k_pass_res<DIR, SP, H, NST><<<grid, H * kSNT, smem, s>>>(a);
+  kern<<<grid, nthreads, smem, s>>>(a);
   return cudaGetLastError();
+}
+template <int SP, int H, bool PAIR>
+static cudaError_t launch_res_hp(int dir, const PassArgs &a, int nst, cudaStream_t s) {
+  switch (nst) {
+    case 2: return dir == 0 ? launch_res_dir<0, SP, H, 2, PAIR>(a, s) : launch_res_dir<1, SP, H, 2, PAIR>(a, s);
+    case 4: return dir == 0 ? launch_res_dir<0, SP, H, 4, PAIR>(a, s) : launch_res_dir<1, SP, H, 4, PAIR>(a, s);
+    default: return dir == 0 ? launch_res_dir<0, SP, H, 3, PAIR>(a, s) : launch_res_dir<1, SP, H, 3, PAIR>(a, s);
+  }
 }
 template <int SP, int H>
 static cudaError_t launch_res_h(int dir, const PassArgs &a, int nst, cudaStream_t s) {
-  switch (nst) {
-    case 2: return dir == 0 ? launch_res_dir<0, SP, H, 2>(a, s) : launch_res_dir<1, SP, H, 2>(a, s);
-    case 4: return dir == 0 ? launch_res_dir<0, SP, H, 4>(a, s) : launch_res_dir<1, SP, H, 4>(a, s);
-    default: return dir == 0 ? launch_res_dir<0, SP, H, 3>(a, s) : launch_res_dir<1, SP, H, 3>(a, s);
-  }
+  return res_config().pair ? launch_res_hp<SP, H, true>(dir, a, nst, s) : launch_res_hp<SP, H, false>(dir, a, nst, s);
 }
 static cudaError_t launch_res(int dir, const PassArgs &a, cudaStream_t s) {
   const ResConfig c = res_config();
@@ -1056,7 +1339,8 @@ static cudaError_t launch_res(int dir, const PassArgs &a, cudaStream_t s) {
     else h = 1;
   }
   if (sp == 2) return h == 2 ? launch_res_h<2, 2>(dir, a, c.nst, s) : launch_res_h<2, 1>(dir, a, c.nst, s);
-  return h == 2 ? launch_res_h<1, 2>(dir, a, c.nst, s) : launch_res_h<1, 1>(dir, a, c.nst, s);
+  if (h == 4 && c.pair) return launch_res_hp<1, 4, true>(dir, a, c.nst, s);
+  return h >= 2 ? launch_res_h<1, 2>(dir, a, c.nst, s) : launch_res_h<1, 1>(dir, a, c.nst, s);
 }
 
 template <int SP, bool CN>

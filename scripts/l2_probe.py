@@ -9,7 +9,7 @@ import torch  # noqa: E402
 from paper_2303_03848_b200 import parareal, synth  # noqa: E402
 
 flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
-for M, N in [(1 << 20, 64), (1 << 20, 16), (1 << 19, 16), (1 << 18, 32), (1 << 18, 16), (1 << 17, 32)]:
+for M, N in [(1 << 20, 64)] if os.environ.get("PR_PROBE_ONE") else [(1 << 20, 64), (1 << 20, 16), (1 << 19, 16), (1 << 18, 32), (1 << 18, 16), (1 << 17, 32)]:
     p = synth.single(M, N, coarse=synth.COARSE_PINN, max_iter=1, tol=0.0)
     with parareal.Context(p) as ctx:
         ctx.load_weights(synth.kaiming_net(synth.PINN_3x20, seed=0))
