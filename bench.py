@@ -219,15 +219,15 @@ def roofline(p, ph, K, world, rank, pk, pk_src, clk_mhz, n_sm, synth, dims=None,
                     "achieved": 9.0 * pt_steps / sweep_s / 1e12, "peak": n_sm * 64 * 2 * clk_mhz * 1e6 / 1e12,
                     "unit": "TFLOP/s", "peak_source": "fp64 pipe: %d SMs x 64 FMA/clk x 2 x %.0f MHz (DESIGN.md)"
                     % (n_sm, clk_mhz), "work_per_unit": "9 fp64 flop per point-step", "launch_unit": "one sweep"}
-            tr = ncu_traffic("k_fine_sweep")
+            tr = ncu_traffic("k_parareal_pipe" if piped else "k_fine_sweep")
         else:
-            kname = ("k_pass_res (K2, persistent streamed pass)" if p.fine_theta == 1.0
+            kname = ("k_pass_res2 (K2, persistent paired streamed pass)" if p.fine_theta == 1.0
                      else "k_streamed_pass (K2, Crank-Nicolson tile pass)")
             roof = {"kernel": kname, "bound": "hbm",
                     "achieved": 16.0 * pt_steps / sweep_s / 1e9,
                     "peak": float(pk["hbm_gbs"]), "unit": "GB/s", "peak_source": pk_src,
                     "work_per_unit": "16 B per point-step", "launch_unit": "one pass (8 B per point)"}
-            tr = ncu_traffic("k_pass_res" if p.fine_theta == 1.0 else "k_streamed_pass")
+            tr = ncu_traffic("k_pass_res2" if p.fine_theta == 1.0 else "k_streamed_pass")
     else:
         evals = float(p.B) * p.M * nloc
         chain_s = ph["ms_coarse"] / (K + 1) / 1e3
@@ -280,8 +280,8 @@ def c3_fine_sweep_roofline(parareal, synth, torch, stream, pk, pk_src, flush):
         t = statistics.median(ms) / 1e3
         pt_steps = float(p.M) * p.N * p.fine_steps
         ach = 16.0 * pt_steps / t / 1e9
-        tr = ncu_traffic("k_pass_res")
-        return {"kernel": "k_pass_res (K2, persistent streamed pass)", "workload": "C3 fine sweep: 64 slices x 2^20 points x 100 IE steps",
+        tr = ncu_traffic("k_pass_res2")
+        return {"kernel": "k_pass_res2 (K2, persistent paired streamed pass)", "workload": "C3 fine sweep: 64 slices x 2^20 points x 100 IE steps",
                 "bound": "hbm", "achieved": ach, "peak": float(pk["hbm_gbs"]), "unit": "GB/s",
                 "frac": ach / float(pk["hbm_gbs"]), "peak_source": pk_src, "ms_per_sweep": t * 1e3,
                 "point_steps_per_s": pt_steps / t, "work_per_unit": "16 B per point-step (fp32 read+write, 2 passes)",
