@@ -23,7 +23,7 @@ cudaError_t launch_pinn_smem(int IN, int W, int act, const PinnArgs &a, dim3 gri
 // exchange); pinn_split_G(W) threads per point (group kernels, shared-memory exchange) for
 // 32-, 50- and 64-wide nets; pinn_split_ppc(W) points per 128-thread CTA
 constexpr int kPinnSplitG = 4;
-constexpr int kPinnSplitMinPPC = 4;  // the fewest points per CTA of any latency-mode kernel
+constexpr int kPinnSplitMinPPC = 8;  // the fewest points per CTA of any latency-mode kernel
 int pinn_split_G(int W);
 int pinn_split_ppc(int W);
 bool pinn_split_supported(int IN, int W, int act);

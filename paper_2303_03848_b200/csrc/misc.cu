@@ -19,26 +19,29 @@ __global__ void k_payoff(float *U0, int M, int Mp, int B, const double *Lb, cons
 // Partials hold (Σ d², Σ u²) per (local slice, instance, chunk); chunks are summed in a
 // fixed order, the max is order-free, so δ is bitwise reproducible and independent of
 // how slices are sharded across ranks.
-__global__ void k_delta(const double *partials, int B, int nch, int ln_lo, int ln_hi,
-                        unsigned long long *dmax) {
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  const int total = (ln_hi - ln_lo + 1) * B;
-  double rel = 0.0;
-  if (idx < total) {
-    const int ln = ln_lo + idx / B, b = idx % B;
-    const double *p = partials + (((size_t)ln * B + b) * nch) * 2;
-    double num = 0.0, den = 0.0;
-    for (int c = 0; c < nch; ++c) { num += p[2 * c]; den += p[2 * c + 1]; }
-    rel = (den > 0.0) ? sqrt(num) / sqrt(den) : sqrt(num);
-  }
-  // warp max then one atomic per warp; non-negative doubles order like their bit patterns
-  unsigned long long v = (unsigned long long)__double_as_longlong(rel);
+// One row's chunks summed by one warp in a fixed order: lane l adds chunks l, l+32, … in index
+// order, then a fixed xor-shuffle tree; lane 0's result is the one used (deterministic).
+__device__ __forceinline__ double row_rel(const double *p, int nch, int lane) {
+  double num = 0.0, den = 0.0;
+  for (int c = lane; c < nch; c += 32) { num += p[2 * c]; den += p[2 * c + 1]; }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
-    const unsigned long long w = __shfl_xor_sync(0xffffffffu, v, o);
-    v = w > v ? w : v;
+    num += __shfl_xor_sync(0xffffffffu, num, o);
+    den += __shfl_xor_sync(0xffffffffu, den, o);
   }
-  if ((threadIdx.x & 31) == 0) atomicMax(dmax, v);
+  return (den > 0.0) ? sqrt(num) / sqrt(den) : sqrt(num);
+}
+
+// one warp per (slice, instance) row; rows ln_lo..ln_hi
+__global__ void k_delta(const double *partials, int B, int nch, int ln_lo, int ln_hi,
+                        unsigned long long *dmax) {
+  const int row = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+  const int total = (ln_hi - ln_lo + 1) * B;
+  if (row >= total) return;
+  const int ln = ln_lo + row / B, b = row % B;
+  const double rel = row_rel(partials + (((size_t)ln * B + b) * nch) * 2, nch, lane);
+  // non-negative doubles order like their bit patterns
+  if (lane == 0) atomicMax(dmax, (unsigned long long)__double_as_longlong(rel));
 }
 
 cudaError_t launch_payoff(float *U0, int M, int Mp, int B, const double *Lb, const double *Kb, cudaStream_t s) {
@@ -77,33 +80,22 @@ __global__ void k_delta_wide(const double *partials, int B, int nch, int ln_lo, 
 __global__ void k_delta_multi(const double *partials, size_t pstride, int B, int nch, int N, int K,
                               unsigned long long *dmax) {
   const int k = blockIdx.y + 1;
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  const int row = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
   const int total = (N - k + 1) * B;
-  double rel = 0.0;
-  if (idx < total) {
-    const int ln = k + idx / B, b = idx % B;
-    const double *p = partials + (size_t)k * pstride + (((size_t)ln * B + b) * nch) * 2;
-    double num = 0.0, den = 0.0;
-    for (int c = 0; c < nch; ++c) { num += p[2 * c]; den += p[2 * c + 1]; }
-    rel = (den > 0.0) ? sqrt(num) / sqrt(den) : sqrt(num);
-  }
-  unsigned long long v = (unsigned long long)__double_as_longlong(rel);
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const unsigned long long w = __shfl_xor_sync(0xffffffffu, v, o);
-    v = w > v ? w : v;
-  }
-  if ((threadIdx.x & 31) == 0) atomicMax(dmax + (k - 1), v);
+  if (row >= total) return;
+  const int ln = k + row / B, b = row % B;
+  const double rel = row_rel(partials + (size_t)k * pstride + (((size_t)ln * B + b) * nch) * 2, nch, lane);
+  if (lane == 0) atomicMax(dmax + (k - 1), (unsigned long long)__double_as_longlong(rel));
 }
 
-// Up to kDeltaSeqMax chunks a thread sums a row's chunks in index order (k_delta, k_delta_multi:
-// the same order in the blocking and pipelined schedules; unused chunks are zero and leave the
-// sums bitwise unchanged), beyond that a CTA per row does (k_delta_wide).
-constexpr int kDeltaSeqMax = 256;
+// Up to kDeltaWarpMax chunks a warp sums a row (k_delta, k_delta_multi: the same order in the
+// blocking and pipelined schedules; unused chunks are zero), beyond that a CTA per row does
+// (k_delta_wide).
+constexpr int kDeltaWarpMax = 1024;
 cudaError_t launch_delta_multi(const double *partials, size_t pstride, int B, int nch, int N, int K,
                                unsigned long long *dmax, cudaStream_t s) {
-  if (nch > kDeltaSeqMax) return cudaErrorInvalidValue;  // (the pipelined schedule runs small grids)
-  dim3 grid((N * B + 255) / 256, K);
+  if (nch > kDeltaWarpMax) return cudaErrorInvalidValue;  // (the pipelined schedule runs small grids)
+  dim3 grid((N * B * 32 + 255) / 256, K);
   k_delta_multi<<<grid, 256, 0, s>>>(partials, pstride, B, nch, N, K, dmax);
   return cudaGetLastError();
 }
@@ -111,10 +103,10 @@ cudaError_t launch_delta_multi(const double *partials, size_t pstride, int B, in
 cudaError_t launch_delta(const double *partials, int B, int nch, int ln_lo, int ln_hi, unsigned long long *dmax,
                          cudaStream_t s) {
   const int total = (ln_hi - ln_lo + 1) * B;
-  if (nch > kDeltaSeqMax)
+  if (nch > kDeltaWarpMax)
     k_delta_wide<<<total, 128, 0, s>>>(partials, B, nch, ln_lo, dmax);
   else
-    k_delta<<<(total + 255) / 256, 256, 0, s>>>(partials, B, nch, ln_lo, ln_hi, dmax);
+    k_delta<<<(total * 32 + 255) / 256, 256, 0, s>>>(partials, B, nch, ln_lo, ln_hi, dmax);
   return cudaGetLastError();
 }
 

@@ -41,8 +41,6 @@ namespace pr {
 // latency mode (G = 4 threads per point), shared-memory weights
 typedef void (*SplitKernel)(PinnArgs);
 static SplitKernel split_kernel(int IN, int W, int act) {
-  if (IN == 4 && W == 50 && pinn_split_G(50) == 25)
-    return act ? k_pinn_chain_group<4, 50, 25, 1> : k_pinn_chain_group<4, 50, 25, 0>;
   if (IN == 4 && W == 50) return act ? k_pinn_chain_group<4, 50, 10, 1> : k_pinn_chain_group<4, 50, 10, 0>;
   if (IN == 4 && W == 64 && act == 0) return k_pinn_chain_group<4, 64, 16, 0>;
   if (IN == 4 && W == 32 && act == 0) return k_pinn_chain_group<4, 32, 8, 0>;
@@ -52,10 +50,9 @@ static SplitKernel split_kernel(int IN, int W, int act) {
   return nullptr;
 }
 bool pinn_split_supported(int IN, int W, int act) { return split_kernel(IN, W, act) != nullptr; }
-int pinn_split_G(int W) {
-  static const int g50 = getenv("PR_PINN_G50") && atoi(getenv("PR_PINN_G50")) == 25 ? 25 : 10;
-  return W == 20 ? 4 : W == 32 ? 8 : W == 50 ? g50 : W == 64 ? 16 : 0;
-}
+// (W = 50 with G = 25 -- two neurons per thread, one point per warp -- measured slower: every
+// warp re-reads the whole weight matrix, so L1 traffic per layer triples)
+int pinn_split_G(int W) { return W == 20 ? 4 : W == 32 ? 8 : W == 50 ? 10 : W == 64 ? 16 : 0; }
 int pinn_split_ppc(int W) {
   const int G = pinn_split_G(W);
   return G ? 4 * (32 / G) : 0;

@@ -323,7 +323,6 @@ static PipeKernel pipe_kernel_c(int M, bool cn) {
 // 10×50 architecture (tanh or ReLU) and 32-wide tanh nets
 static PipeKernel pipe_kernel(int M, bool cn, int IN, int W, int act, bool split) {
   if (split) {
-    if (IN == 4 && W == 50 && pinn_split_G(50) != 10) return nullptr;
     if (IN == 4 && W == 50) return act ? pipe_kernel_c<4, 50, 10, 1>(M, cn) : pipe_kernel_c<4, 50, 10, 0>(M, cn);
     if (W != 20 || act != 0) return nullptr;
     if (IN == 4) return pipe_kernel_c<4, 20, kPinnSplitG, 0>(M, cn);
