@@ -196,7 +196,11 @@ enum {
   PR_OPT_USE_GRAPHS = 2,    /* 0/1: a fixed-K (tol == 0), single-GPU, device-pointer solve is captured
                                into a CUDA graph on its first call per (V_T, V_0) pair and replayed on
                                later calls (same kernels, same results); any other solve runs eagerly.
-                               set_option / load_pinn_weights / free discard the captured graph.   */
+                               set_option / load_pinn_weights / free discard the captured graph.
+                               2: the same, but the graph is captured without the phase-timing events
+                               and a replay returns as soon as it is enqueued on the context stream
+                               (stream-ordered, like a library call: the caller synchronises; rep, if
+                               given, receives iterations and kernel_launches, zero times, no δ).  */
   PR_OPT_PINN_KERNEL = 3,   /* 0 auto, 1 shared-memory weights, 2 latency mode (4 threads/point; B·M ≤ 65536) */
   PR_OPT_PIPELINE = 4       /* 0 auto: a single-GPU fixed-K (tol == 0) solve with PINN G in latency mode and
                                the resident fine kernel at M ≤ 1024 runs pipelined: fine

@@ -710,6 +710,7 @@ pr_status store_rows(pr_ctx *c, float *dst, const float *src, bool device_ptr) {
 
 // Timing events; under stream capture they must be captured as timestamp (external) nodes.
 void record(pr_ctx *c, cudaEvent_t e) {
+  if (c->capturing && c->opt_graphs == 2) return;  // lean graph: no timing nodes
   if (c->capturing) cudaEventRecordWithFlags(e, c->stream, cudaEventRecordExternal);
   else cudaEventRecord(e, c->stream);
 }
@@ -871,6 +872,11 @@ pr_status solve_report(pr_ctx *c, int K, int conv, cudaEvent_t e0, cudaEvent_t e
   rep->converged = (c->tol > 0.0 && K > 0 && c->h_delta[K - 1] < c->tol) ? 1 : conv;
   if (rep->delta)
     for (int i = 0; i < K; ++i) rep->delta[i] = c->h_delta[i];
+  rep->kernel_launches = launches;
+  if (c->opt_graphs == 2 && c->g_exec) {  // lean graph: no timing events were captured
+    rep->ms_total = rep->ms_coarse = rep->ms_fine = rep->ms_comm = rep->ms_setup = 0.0;
+    return PR_OK;
+  }
   float ms = 0;
   cudaEventElapsedTime(&ms, e0, e1);
   rep->ms_total = ms;
@@ -909,6 +915,16 @@ pr_status solve_impl(pr_ctx *c, const float *V_T, float *V_0, bool device_ptr, p
   if (use_graph && c->g_exec && c->g_vt == V_T && c->g_v0 == V_0) {
     CU(cudaGraphLaunch(c->g_exec, c->stream));
     c->launches += c->g_launches;
+    if (c->opt_graphs == 2) {  // stream-ordered replay: return once enqueued (no δ, no times)
+      c->solved = true;
+      if (rep) {
+        rep->iterations = c->g_K;
+        rep->converged = 0;
+        rep->kernel_launches = c->g_launches;
+        rep->ms_total = rep->ms_coarse = rep->ms_fine = rep->ms_comm = rep->ms_setup = 0.0;
+      }
+      return PR_OK;
+    }
     CU(cudaStreamSynchronize(c->stream));
     return solve_report(c, c->g_K, 0, c->g_e0, c->g_e1, c->g_spans, c->g_launches, rep);
   }
@@ -1560,7 +1576,8 @@ pr_status parareal_set_option(pr_ctx *c, int32_t key, int64_t value) {
       c->opt_pinn_kernel = (int)value;
       return PR_OK;
     case PR_OPT_USE_GRAPHS:
-      if (value < 0 || value > 1) return fail(c, PR_ERR_INVALID_ARGUMENT, "PR_OPT_USE_GRAPHS must be 0 or 1");
+      if (value < 0 || value > 2) return fail(c, PR_ERR_INVALID_ARGUMENT, "PR_OPT_USE_GRAPHS must be 0, 1 or 2");
+      if (value != c->opt_graphs) drop_graph(c);
       c->opt_graphs = (int)value;
       return PR_OK;
     case PR_OPT_PIPELINE:

@@ -480,6 +480,14 @@ def test_graph_replay_matches_eager():
         c.set_option(parareal.OPT_USE_GRAPHS, 0)
         c.solve_device(out)
         assert np.array_equal(out.cpu().numpy(), g1) and not np.array_equal(g1, eager)
+        # lean stream-ordered replays (no timing nodes; the call returns once enqueued)
+        c.set_option(parareal.OPT_USE_GRAPHS, 2)
+        for _ in range(3):
+            out.zero_()
+            r = c.solve_device(out)
+            torch.cuda.synchronize()
+            assert r["iterations"] == 3 and r["kernel_launches"] > 0
+            assert np.array_equal(out.cpu().numpy(), g1)
 
 
 def test_errors_on_gpu():
