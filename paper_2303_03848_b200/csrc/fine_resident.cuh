@@ -63,6 +63,11 @@ struct ResidentArgs {
 
 #if !defined(PR_ARGS_ONLY) && !defined(PR_FINE_RESIDENT_IMPL)
 #define PR_FINE_RESIDENT_IMPL
+// The barrier of one system's threads: the whole CTA by default; a translation unit whose CTAs
+// hold other work besides the system (pipe.cu) defines it as a named barrier first.
+#ifndef PR_TRI_SYNC
+#define PR_TRI_SYNC() __syncthreads()
+#endif
 namespace pr {
 __device__ __forceinline__ double g_upper(const ResidentArgs &a, int b, double tau) {
   // Reading Q3: V(L, τ) = L − K e^{−rτ} (default) or 0 (paper-literal P:161)
@@ -173,7 +178,7 @@ struct Tri {
       double *xb = sh + 4 * NW + 2;
       if (lane == 31) xb[w] = x[P - 1];
       if (lane == 0) xb[NW + w] = x[0];
-      __syncthreads();
+      PR_TRI_SYNC();
       if (lane == 0) xl = (w > 0) ? xb[w - 1] : 0.0;
       if (lane == 31) xr = (w < NW - 1) ? xb[NW + w + 1] : 0.0;
     } else {
@@ -212,7 +217,7 @@ struct Tri {
     if (NW > 1) {
       double *sy = sh + 2 * NW;
       if (lane == 31) sy[w] = v;
-      __syncthreads();
+      PR_TRI_SYNC();
       if constexpr (kParFold) {
         in = fold(cfw, sy);
       } else {
@@ -236,7 +241,7 @@ struct Tri {
     if (NW > 1) {
       double *sy = sh + 3 * NW;
       if (lane == 0) sy[w] = v;
-      __syncthreads();
+      PR_TRI_SYNC();
       if constexpr (kParFold) {
         in = fold(cbw, sy);
       } else {
@@ -260,9 +265,9 @@ __device__ __forceinline__ void sys_reduce2(double &a, double &b, int t, double 
   }
   if (NT > 32) {
     constexpr int NW = NT / 32;
-    __syncthreads();
+    PR_TRI_SYNC();
     if ((t & 31) == 0) { red[2 * (t >> 5)] = a; red[2 * (t >> 5) + 1] = b; }
-    __syncthreads();
+    PR_TRI_SYNC();
     a = 0.0; b = 0.0;
 #pragma unroll 1
     for (int q = 0; q < NW; ++q) { a += red[2 * q]; b += red[2 * q + 1]; }
@@ -283,7 +288,7 @@ __device__ __forceinline__ void run_steps(Tri<P, NT, CN> &tri, const ResidentArg
   const double tau0 = n * a.dT;
 #pragma unroll 1
   for (int m0 = 0; m0 < a.steps; m0 += kBcChunk) {
-    __syncthreads();  // readers of the previous chunk are done
+    PR_TRI_SYNC();  // readers of the previous chunk are done
     for (int i = t; i < kBcChunk; i += NT) {
       const int m = m0 + i;
       if (m < a.steps) {
@@ -292,7 +297,7 @@ __device__ __forceinline__ void run_steps(Tri<P, NT, CN> &tri, const ResidentArg
         bct[i] = CN ? coef * (a.theta * gp + (1.0 - a.theta) * g_upper(a, b, tau0 + m * a.dtau)) : coef * gp;
       }
     }
-    __syncthreads();
+    PR_TRI_SYNC();
     const int mend = min(a.steps - m0, kBcChunk);
 #pragma unroll 1
     for (int mm = 0; mm < mend; ++mm) tri.step(x, bc_i, bc_i >= 0 ? bct[mm] : 0.0, sh);
@@ -314,7 +319,7 @@ __global__ void __launch_bounds__(NT * SPB) k_fine_sweep(ResidentArgs a) {
   double *sh = shm[threadIdx.x / NT];
   Tri<P, NT, CN> tri;
   tri.setup(a, a.fset[b], t, sh);
-  if (NW > 1) __syncthreads();
+  if (NW > 1) PR_TRI_SYNC();
   tri.fold_setup(sh);
   const float *u = a.U + ((size_t)ln * a.B + b) * a.Mp;
   double x[P];
@@ -367,7 +372,7 @@ __global__ void __launch_bounds__(NT * SPB) k_resident_chain(ResidentArgs a) {
   double *rd = red[threadIdx.x / NT];
   Tri<P, NT, CN> tri;
   tri.setup(a, a.fset[b], t, sh);
-  if (NW > 1) __syncthreads();
+  if (NW > 1) PR_TRI_SYNC();
   tri.fold_setup(sh);
   const size_t sstride = (size_t)a.B * a.Mp;
   double x[P];

@@ -54,6 +54,7 @@ struct PipeArgs {
                                // slice; fine (n, b=0) start and end), for PR_PIPE_TRACE
 };
 bool pipe_supported(int M, bool cn, int IN, int W, int act, bool split);
+int pipe_chain_warps(int W, bool split);  // warps per chain CTA (the chain's points per CTA = warps · 32/G)
 cudaError_t launch_parareal_pipe(const PipeArgs &pa, int M, bool cn, int IN, int W, int act, bool split,
                                  size_t smem, cudaStream_t s);
 // K6/K7 (misc.cu)

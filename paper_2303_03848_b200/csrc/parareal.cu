@@ -814,8 +814,15 @@ pr_status solve_pipelined(pr_ctx *c) {
   pa.g.Fcopy = c->Fk;
   pa.N = c->N;
   pa.K = c->max_iter;
-  const int ppc = use_split_pinn(c) ? pr::pinn_split_ppc(c->W) : 128;  // chain points per CTA
-  pa.C = (c->M + ppc - 1) / ppc;                                        // chain CTAs per instance (≤ nch)
+  // chain points per CTA: the blocking chain's CTA (4 warps) times the chain-CTA width in warps / 4
+  const int nwc = pr::pipe_chain_warps(c->W, use_split_pinn(c));
+  const int ppc = (use_split_pinn(c) ? pr::pinn_split_ppc(c->W) : 128) * (nwc / 4);
+  pa.C = (c->M + ppc - 1) / ppc;  // chain CTAs per instance
+  if ((size_t)pa.C * (nwc / 4) > (size_t)c->nch || (size_t)pa.C * nwc > (size_t)c->nch * 4)
+  {
+    c->pipe_ok = 0;
+    return PR_ERR_UNSUPPORTED;  // δ chunks / warp staging would not fit: blocking schedule
+  }
   pa.partials = c->pipe_partials;
   pa.pstride = c->pipe_pstride;
   pa.wstage = c->pipe_wstage;

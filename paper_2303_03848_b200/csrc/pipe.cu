@@ -25,6 +25,9 @@
 // read through L2 (ld.global.cg).  All CTAs are co-resident (cooperative launch), and the wait
 // graph is acyclic, so the kernel cannot deadlock.
 #include "launch.h"
+// fine-role CTAs run one K1 system on their first 128 threads (the rest exit at once when the
+// chain CTAs are wider): every K1 barrier is the named barrier 1 over those 128 threads
+#define PR_TRI_SYNC() asm volatile("bar.sync 1, 128;" ::: "memory")
 #include "fine_resident.cuh"
 #include "pinn_chain.cuh"
 
@@ -83,9 +86,11 @@ __device__ __forceinline__ float chain_eval(const float *sw, int LH, const float
   }
 }
 
-template <int IN, int W, int G, int ACT>
+constexpr int kChunkWarps = 4;  // warps per δ chunk: the blocking chain kernel's CTA (128 threads)
+
+template <int IN, int W, int G, int ACT, int NWC>
 __device__ void chain_role(const PipeArgs &pa, int k, int b, int chunk, const float *sw) {
-  constexpr int NWC = 128 / 32;  // warps per chain CTA
+  static_assert(NWC % kChunkWarps == 0, "a chain CTA holds whole δ chunks");
   const PinnArgs &a = pa.g;
   const double Lb = a.Lb[b];
   const float gscale = (float)(Lb * (double)a.out_scale);
@@ -218,14 +223,17 @@ __device__ void chain_role(const PipeArgs &pa, int k, int b, int chunk, const fl
       if (lane == 0) publish_add_release(cnt + n);
       if (pa.trace && cta == 0 && threadIdx.x == 0) pa.trace[((size_t)k * pa.N + n) * 3] = gtimer();
     }
-    if (k > 0) {  // fold this iteration's per-warp partials, warps in order (the blocking order)
+    if (k > 0) {  // fold this iteration's per-warp partials, warps in order (the blocking order):
+      // every kChunkWarps warps form the δ chunk the blocking kernel's CTA over the same points writes
       __syncthreads();
       double *part = pa.partials + (size_t)k * pa.pstride;
-      for (int ln = k + (int)threadIdx.x; ln <= pa.N; ln += blockDim.x) {
-        const double *ps = wst + (((size_t)ln * a.B * pa.C) + cta) * NWC * 2;
+      constexpr int SUBS = NWC / kChunkWarps;
+      for (int it = (int)threadIdx.x; it < (pa.N + 1 - k) * SUBS; it += blockDim.x) {
+        const int ln = k + it / SUBS, sub = it % SUBS;
+        const double *ps = wst + ((((size_t)ln * a.B * pa.C) + cta) * NWC + sub * kChunkWarps) * 2;
         double num = 0.0, den = 0.0;
-        for (int q = 0; q < NWC; ++q) { num += ps[2 * q]; den += ps[2 * q + 1]; }
-        double *pp = part + (((size_t)ln * a.B + b) * a.nch + chunk) * 2;
+        for (int q = 0; q < kChunkWarps; ++q) { num += ps[2 * q]; den += ps[2 * q + 1]; }
+        double *pp = part + (((size_t)ln * a.B + b) * a.nch + chunk * SUBS + sub) * 2;
         pp[0] = num;
         pp[1] = den;
       }
@@ -234,7 +242,7 @@ __device__ void chain_role(const PipeArgs &pa, int k, int b, int chunk, const fl
   }
 }
 
-template <int P, bool CN>
+template <int P, bool CN, int NWC>
 __device__ void fine_role(const PipeArgs &pa, int n, int b) {
   constexpr int NT = 128;
   const ResidentArgs &a = pa.r;
@@ -243,23 +251,23 @@ __device__ void fine_role(const PipeArgs &pa, int n, int b) {
   const int t = threadIdx.x;
   Tri<P, NT, CN> tri;
   tri.setup(a, a.fset[b], t, sh);
-  __syncthreads();
+  PR_TRI_SYNC();
   tri.fold_setup(sh);
-  const int C = pa.C * (128 / 32);  // publishing chain warps per instance
+  const int C = pa.C * NWC;  // publishing chain warps per instance
   const int *cnt = pa.cnt + (size_t)b * pa.N;
   int *floaded = pa.floaded + (size_t)b * pa.N, *fdone = pa.fdone + (size_t)b * pa.N;
   const size_t row = ((size_t)n * a.B + b) * a.Mp;
   const int kmax = min(pa.K, n + 1);
   for (int k = 1; k <= kmax; ++k) {
     if (n >= 1 && t == 0) wait_geq(cnt + (n - 1), k * C);  // U^{k−1}_n written
-    __syncthreads();
+    PR_TRI_SYNC();
     double x[P];
 #pragma unroll
     for (int i = 0; i < P; ++i) {
       const int j = t * P + i;
       x[i] = (j < a.M) ? (double)__ldcg(a.U + row + j) : 0.0;
     }
-    __syncthreads();
+    PR_TRI_SYNC();
     if (t == 0) publish_set(floaded + n, k);
     if (pa.trace && b == 0 && t == 0) pa.trace[((size_t)k * pa.N + n) * 3 + 1] = gtimer();
     run_steps<P, NT, CN>(tri, a, b, a.n_base + n, t, x, sh, bct);
@@ -272,14 +280,14 @@ __device__ void fine_role(const PipeArgs &pa, int n, int b) {
       }
     } else {  // D_n = F̂_n − Ĝ^{k−1}_n once chain k−1 has passed slice n
       if (t == 0) wait_geq(cnt + n, k * C);
-      __syncthreads();
+      PR_TRI_SYNC();
 #pragma unroll
       for (int i = 0; i < P; ++i) {
         const int j = t * P + i;
         if (j < a.M) a.D[row + j] = (float)(x[i] - (double)__ldcg(a.Gh + row + j));
       }
     }
-    __syncthreads();
+    PR_TRI_SYNC();
     if (t == 0) publish_set(fdone + n, k);
     if (pa.trace && b == 0 && t == 0) pa.trace[((size_t)k * pa.N + n) * 3 + 2] = gtimer();
   }
@@ -287,8 +295,8 @@ __device__ void fine_role(const PipeArgs &pa, int n, int b) {
 
 // CTAs [0, (K+1)·B·C): the chain of iteration k = blockIdx / (B·C) (each iteration its own CTAs,
 // so chain k+1 runs behind chain k instead of after it); then one CTA per fine system.
-template <int P, bool CN, int IN, int W, int G, int ACT>
-__global__ void __launch_bounds__(128) k_parareal_pipe(PipeArgs pa) {
+template <int P, bool CN, int IN, int W, int G, int ACT, int NWC>
+__global__ void __launch_bounds__(NWC * 32) k_parareal_pipe(PipeArgs pa) {
   extern __shared__ float sw[];
   const int per = pa.g.B * pa.C;
   const int nchain = (pa.K + 1) * per;
@@ -300,19 +308,29 @@ __global__ void __launch_bounds__(128) k_parareal_pipe(PipeArgs pa) {
       w = sw;
     }
     const int k = blockIdx.x / per, r = blockIdx.x % per;
-    chain_role<IN, W, G, ACT>(pa, k, r / pa.C, r % pa.C, w);
+    chain_role<IN, W, G, ACT, NWC>(pa, k, r / pa.C, r % pa.C, w);
   } else {
+    if (threadIdx.x >= 128) return;  // one K1 system per fine CTA (128 threads)
     const int f = blockIdx.x - nchain;
-    fine_role<P, CN>(pa, f / pa.g.B, f % pa.g.B);
+    fine_role<P, CN, NWC>(pa, f / pa.g.B, f % pa.g.B);
   }
 }
 
 typedef void (*PipeKernel)(PipeArgs);
+// Chain CTAs of the group chains (the paper's 10×50 net) are 12 warps wide: with one K1 system
+// per 128 threads of a fine CTA and ~168 registers per thread, a 384-thread CTA fills an SM, so
+// (K+1)·C chain CTAs + N fine CTAs ≤ 148 run one per SM and the chains do not share SMs with the
+// fine solves (measured: 3× slower chain slices when they did).
+template <int IN, int W, int G>
+constexpr int pipe_nwc() { return (G > 1 && W != 20) ? 12 : 4; }
+int pipe_chain_warps(int W, bool split) { return split && W != 20 ? 12 : 4; }
+
 template <bool CN, int IN, int W, int G, int ACT>
 static PipeKernel pipe_kernel_p(int M) {
-  if (M <= 256) return k_parareal_pipe<2, CN, IN, W, G, ACT>;
-  if (M <= 512) return k_parareal_pipe<4, CN, IN, W, G, ACT>;
-  if (M <= 1024) return k_parareal_pipe<8, CN, IN, W, G, ACT>;
+  constexpr int NWC = pipe_nwc<IN, W, G>();
+  if (M <= 256) return k_parareal_pipe<2, CN, IN, W, G, ACT, NWC>;
+  if (M <= 512) return k_parareal_pipe<4, CN, IN, W, G, ACT, NWC>;
+  if (M <= 1024) return k_parareal_pipe<8, CN, IN, W, G, ACT, NWC>;
   return nullptr;
 }
 template <int IN, int W, int G, int ACT>
@@ -350,13 +368,14 @@ cudaError_t launch_parareal_pipe(const PipeArgs &pa, int M, bool cn, int IN, int
   int dev = 0, nsm = 0, occ = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 128, smem);
+  const int nthreads = 32 * pipe_chain_warps(W, split);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, nthreads, smem);
   if (e != cudaSuccess) return e;
   const int grid = (pa.K + 1) * pa.g.B * pa.C + pa.g.B * pa.N;
   if (grid > occ * nsm) return cudaErrorCooperativeLaunchTooLarge;
   PipeArgs arg = pa;
   void *params[] = {&arg};
-  return cudaLaunchCooperativeKernel((const void *)k, dim3(grid), dim3(128), params, smem, s);
+  return cudaLaunchCooperativeKernel((const void *)k, dim3(grid), dim3(nthreads), params, smem, s);
 }
 
 }  // namespace pr
