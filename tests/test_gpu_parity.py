@@ -503,3 +503,18 @@ def test_errors_on_gpu():
         assert ei.value.status == 7
         with pytest.raises(parareal.PararealError):
             c.apply_fine(99, np.zeros((1, 64), np.float32))
+
+
+def test_pipeline_falls_back_when_not_co_resident():
+    """The pipelined kernel needs every CTA co-resident: the paper's 10x50 net at C2 with K = 8
+    needs 9 chains x 29 twelve-warp CTAs + 32 fine CTAs > 148 SMs, so auto mode must run the
+    blocking schedule (same launches as PR_OPT_PIPELINE=1) and give its results bitwise."""
+    p = synth.single(1024, 32, coarse=synth.COARSE_PINN, max_iter=8, tol=0.0)
+    net = synth.kaiming_net(synth.PINN_PAPER, seed=4)
+    with ctx_for(p, net) as c:
+        a, ra = c.solve()
+        c.set_option(parareal.OPT_PIPELINE, 1)
+        b, rb = c.solve()
+    assert ra["kernel_launches"] == rb["kernel_launches"], "auto mode should have fallen back"
+    assert ra["iterations"] == rb["iterations"] == 8
+    assert np.array_equal(a, b) and np.array_equal(ra["delta"], rb["delta"])
