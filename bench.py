@@ -212,7 +212,10 @@ def roofline(p, ph, K, world, rank, pk, pk_src, clk_mhz, n_sm, synth, dims=None,
         sweep_s = ph["ms_fine"] / K / 1e3
         if p.M <= 2048:
             piped = ph["ms_fine"] == ph["ms_coarse"]  # the pipelined schedule reports its overlapped time in both
-            roof = {"kernel": "k_parareal_pipe (pipelined schedule; fine role = K1, fp64)" if piped
+            pipe_name = ("k_parareal_pipe_num (pipelined schedule, numerical G; fine role = K1, fp64)"
+                         if p.coarse == synth.COARSE_IMPLICIT_EULER
+                         else "k_parareal_pipe (pipelined schedule; fine role = K1, fp64)")
+            roof = {"kernel": pipe_name if piped
                     else "k_fine_sweep (resident K1, fp64)", "bound": "alu",
                     "note": "latency-bound at this size: each implicit step is two dependent scans over "
                             "one system per CTA (0.5 us/step), one CTA per slice on 148 SMs; the fraction "

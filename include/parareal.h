@@ -202,8 +202,9 @@ enum {
                                (stream-ordered, like a library call: the caller synchronises; rep, if
                                given, receives iterations and kernel_launches, zero times, no δ).  */
   PR_OPT_PINN_KERNEL = 3,   /* 0 auto, 1 shared-memory weights, 2 latency mode (4 threads/point; B·M ≤ 65536) */
-  PR_OPT_PIPELINE = 4       /* 0 auto: a single-GPU fixed-K (tol == 0) solve with PINN G in latency mode and
-                               the resident fine kernel at M ≤ 1024 runs pipelined: fine
+  PR_OPT_PIPELINE = 4       /* 0 auto: a single-GPU fixed-K (tol == 0) solve with PINN G in latency mode (or
+                               the numerical G) and the resident fine kernel at M ≤ 1024 runs pipelined
+                               (SURVEY NEXT-2): fine
                                solves and the coarse chain overlapped in one cooperative kernel, bitwise the
                                blocking results; its report gives the overlapped time as both ms_fine and
                                ms_coarse.  1: always the blocking schedule. */

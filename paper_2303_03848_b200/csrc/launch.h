@@ -45,7 +45,9 @@ cudaError_t launch_pinn_tc(int IN, int W, int act, bool bf16, const PinnArgs &a,
 struct PipeArgs {
   ResidentArgs r;          // fine scheme and the U / Gh / D / Fk rows
   PinnArgs g;              // coarse chain (same rows)
+  ResidentArgs rc;         // numerical coarse G (PR_COARSE_IMPLICIT_EULER): its scheme (n_c steps)
   int N, K, C;             // slices, iterations, chain CTAs per instance
+  int cpub;                // chain publications per (instance, slice): chain warps (PINN) or 1 (numerical)
   double *partials;        // [K+1][pstride] δ partials per iteration
   size_t pstride;
   double *wstage;          // [N+1][B·C][4 warps][2] per-warp δ partials of the current iteration
@@ -54,6 +56,8 @@ struct PipeArgs {
                                // slice; fine (n, b=0) start and end), for PR_PIPE_TRACE
 };
 bool pipe_supported(int M, bool cn, int IN, int W, int act, bool split);
+bool pipe_num_supported(int M, bool cn);  // numerical coarse G (one K1 chain CTA per iteration and instance)
+cudaError_t launch_parareal_pipe_num(const PipeArgs &pa, int M, bool cn, cudaStream_t s);
 int pipe_chain_warps(int W, bool split);  // warps per chain CTA (the chain's points per CTA = warps · 32/G)
 cudaError_t launch_parareal_pipe(const PipeArgs &pa, int M, bool cn, int IN, int W, int act, bool split,
                                  size_t smem, cudaStream_t s);

@@ -779,8 +779,9 @@ pr_plan make_plan(int N, int world, int rank, int k) {
 // mode, resident fine kernel with M ≤ 1024, and every CTA co-resident (checked at first launch).
 bool pipe_eligible(const pr_ctx *c) {
   if (c->opt_pipeline == 1 || c->pipe_ok == 0) return false;
-  if (c->world != 1 || c->tol != 0.0 || c->coarse != PR_COARSE_PINN || c->max_iter < 1 || c->tc) return false;
+  if (c->world != 1 || c->tol != 0.0 || c->max_iter < 1 || c->tc) return false;
   if (!use_resident(c) || c->M > 1024) return false;
+  if (c->coarse == PR_COARSE_IMPLICIT_EULER) return pr::pipe_num_supported(c->M, c->fine_theta != 1.0);
   // the chain evaluates as the blocking kernel would: latency mode if it is the one chosen
   return pr::pipe_supported(c->M, c->fine_theta != 1.0, c->IN, c->W, c->act, use_split_pinn(c));
 }
@@ -814,14 +815,22 @@ pr_status solve_pipelined(pr_ctx *c) {
   pa.g.Fcopy = c->Fk;
   pa.N = c->N;
   pa.K = c->max_iter;
-  // chain points per CTA: the blocking chain's CTA (4 warps) times the chain-CTA width in warps / 4
-  const int nwc = pr::pipe_chain_warps(c->W, use_split_pinn(c));
-  const int ppc = (use_split_pinn(c) ? pr::pinn_split_ppc(c->W) : 128) * (nwc / 4);
-  pa.C = (c->M + ppc - 1) / ppc;  // chain CTAs per instance
-  if ((size_t)pa.C * (nwc / 4) > (size_t)c->nch || (size_t)pa.C * nwc > (size_t)c->nch * 4)
-  {
-    c->pipe_ok = 0;
-    return PR_ERR_UNSUPPORTED;  // δ chunks / warp staging would not fit: blocking schedule
+  const bool num = c->coarse == PR_COARSE_IMPLICIT_EULER;
+  if (num) {  // one K1 chain system per (iteration, instance), one publication per slice
+    pa.rc = base_args(c, c->crs);
+    pa.g.B = c->B;
+    pa.C = 1;
+    pa.cpub = 1;
+  } else {
+    // chain points per CTA: the blocking chain's CTA (4 warps) times the chain-CTA width in warps / 4
+    const int nwc = pr::pipe_chain_warps(c->W, use_split_pinn(c));
+    const int ppc = (use_split_pinn(c) ? pr::pinn_split_ppc(c->W) : 128) * (nwc / 4);
+    pa.C = (c->M + ppc - 1) / ppc;  // chain CTAs per instance
+    pa.cpub = pa.C * nwc;           // every chain warp publishes
+    if ((size_t)pa.C * (nwc / 4) > (size_t)c->nch || (size_t)pa.C * nwc > (size_t)c->nch * 4) {
+      c->pipe_ok = 0;
+      return PR_ERR_UNSUPPORTED;  // δ chunks / warp staging would not fit: blocking schedule
+    }
   }
   pa.partials = c->pipe_partials;
   pa.pstride = c->pipe_pstride;
@@ -837,8 +846,10 @@ pr_status solve_pipelined(pr_ctx *c) {
   pa.cnt = c->pipe_flags;
   pa.floaded = c->pipe_flags + (size_t)c->B * c->N;
   pa.fdone = c->pipe_flags + (size_t)2 * c->B * c->N;
-  const cudaError_t e = pr::launch_parareal_pipe(pa, c->M, c->fine_theta != 1.0, c->IN, c->W, c->act,
-                                                 use_split_pinn(c), (size_t)c->nfloats * sizeof(float), c->stream);
+  const cudaError_t e =
+      num ? pr::launch_parareal_pipe_num(pa, c->M, c->fine_theta != 1.0, c->stream)
+          : pr::launch_parareal_pipe(pa, c->M, c->fine_theta != 1.0, c->IN, c->W, c->act, use_split_pinn(c),
+                                     (size_t)c->nfloats * sizeof(float), c->stream);
   if (e == cudaErrorCooperativeLaunchTooLarge) {
     cudaGetLastError();
     c->pipe_ok = 0;

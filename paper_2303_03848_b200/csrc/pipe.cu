@@ -253,7 +253,7 @@ __device__ void fine_role(const PipeArgs &pa, int n, int b) {
   tri.setup(a, a.fset[b], t, sh);
   PR_TRI_SYNC();
   tri.fold_setup(sh);
-  const int C = pa.C * NWC;  // publishing chain warps per instance
+  const int C = pa.cpub;  // chain publications per (instance, slice)
   const int *cnt = pa.cnt + (size_t)b * pa.N;
   int *floaded = pa.floaded + (size_t)b * pa.N, *fdone = pa.fdone + (size_t)b * pa.N;
   const size_t row = ((size_t)n * a.B + b) * a.Mp;
@@ -290,6 +290,129 @@ __device__ void fine_role(const PipeArgs &pa, int n, int b) {
     PR_TRI_SYNC();
     if (t == 0) publish_set(fdone + n, k);
     if (pa.trace && b == 0 && t == 0) pa.trace[((size_t)k * pa.N + n) * 3 + 2] = gtimer();
+  }
+}
+
+// Numerical coarse G (implicit Euler, n_c steps per slice) as the chain of iteration k
+// for instance b: one K1 system (128 threads, the coarse scheme's factors) walking the slices —
+// k_resident_chain's arithmetic and δ partials (chunk 0, sys_reduce2) with the flag protocol of
+// the PINN chain: it reads D_n once fine(k, n) is done and overwrites U_{n+1} once fine(k, n+1)
+// has read it; one publication per slice.
+template <int P>
+__device__ void chain_role_num(const PipeArgs &pa, int k, int b) {
+  constexpr int NT = 128, NW = NT / 32;
+  const ResidentArgs &a = pa.rc;
+  __shared__ double shc[Tri<P, NT, false>::kShm];
+  __shared__ double bcc[kBcChunk];
+  __shared__ double rdc[2 * NW + 2];
+  const int t = threadIdx.x;
+  Tri<P, NT, false> tri;
+  tri.setup(a, a.fset[b], t, shc);
+  PR_TRI_SYNC();
+  tri.fold_setup(shc);
+  const size_t sstride = (size_t)a.B * a.Mp;
+  int *cnt = pa.cnt + (size_t)b * pa.N;
+  const int *floaded = pa.floaded + (size_t)b * pa.N, *fdone = pa.fdone + (size_t)b * pa.N;
+  double *part = pa.partials + (size_t)k * pa.pstride;
+  float *U = pa.g.U;  // the writable view of the boundary rows
+  double x[P];
+  int n0 = 0;
+  if (k == 0) {
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      const int j = t * P + i;
+      x[i] = (j < a.M) ? (double)__ldcg(U + (size_t)b * a.Mp + j) : 0.0;
+    }
+  } else {
+    // U^k_k := F̂^k_{k−1} (copied, reading Q12) with the δ partial of slice k
+    if (t == 0) {
+      wait_geq(fdone + (k - 1), k);
+      if (k <= pa.N - 1) wait_geq(floaded + k, k);
+    }
+    PR_TRI_SYNC();
+    float *uk = U + (size_t)k * sstride + (size_t)b * a.Mp;
+    const float *f = pa.r.Fk + (size_t)b * a.Mp;
+    double num = 0.0, den = 0.0;
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      const int j = t * P + i;
+      float nv = 0.f;
+      if (j < a.M) {
+        nv = __ldcg(f + j);
+        const double dd = (double)nv - (double)__ldcg(uk + j);
+        num += dd * dd;
+        den += (double)nv * nv;
+      }
+      x[i] = (double)nv;
+    }
+    sys_reduce2<NT>(num, den, t, rdc);
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      const int j = t * P + i;
+      if (j < a.M) uk[j] = (float)x[i];
+    }
+    if (t == 0) {
+      double *pp = part + (((size_t)k * a.B + b) * a.nch) * 2;
+      pp[0] = num;
+      pp[1] = den;
+    }
+    PR_TRI_SYNC();
+    if (t == 0) publish_add(cnt + (k - 1));
+    n0 = k;
+  }
+#pragma unroll 1
+  for (int n = n0; n < pa.N; ++n) {
+    run_steps<P, NT, false>(tri, a, b, a.n_base + n, t, x, shc, bcc);  // g = G(U_n)
+    if (k > 0) {
+      if (t == 0) {
+        wait_geq(fdone + n, k);                               // D_n of this iteration
+        if (n + 1 <= pa.N - 1) wait_geq(floaded + n + 1, k);  // U^{k−1}_{n+1} has been read
+      }
+      PR_TRI_SYNC();
+    }
+    const size_t row = (size_t)n * sstride + (size_t)b * a.Mp;
+    float *un = U + row + sstride;
+    double num = 0.0, den = 0.0;
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      const int j = t * P + i;
+      float nv = 0.f;
+      if (j < a.M) {
+        pa.g.Gh[row + j] = (float)x[i];
+        nv = k > 0 ? (float)(x[i] + (double)__ldcg(pa.r.D + row + j)) : (float)x[i];
+        if (k > 0) {
+          const double dd = (double)nv - (double)__ldcg(un + j);
+          num += dd * dd;
+          den += (double)nv * nv;
+        }
+      }
+      x[i] = (double)nv;  // continue from the stored fp32 value (as k_resident_chain)
+    }
+    if (k > 0) sys_reduce2<NT>(num, den, t, rdc);
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      const int j = t * P + i;
+      if (j < a.M) un[j] = (float)x[i];
+    }
+    if (k > 0 && t == 0) {
+      double *pp = part + (((size_t)(n + 1) * a.B + b) * a.nch) * 2;
+      pp[0] = num;
+      pp[1] = den;
+    }
+    PR_TRI_SYNC();
+    if (t == 0) publish_add(cnt + n);
+    if (pa.trace && b == 0 && t == 0) pa.trace[((size_t)k * pa.N + n) * 3] = gtimer();
+  }
+}
+
+template <int P, bool CN>
+__global__ void __launch_bounds__(128) k_parareal_pipe_num(PipeArgs pa) {
+  const int nchain = (pa.K + 1) * pa.g.B;
+  if ((int)blockIdx.x < nchain) {
+    chain_role_num<P>(pa, blockIdx.x / pa.g.B, blockIdx.x % pa.g.B);
+  } else {
+    const int f = blockIdx.x - nchain;
+    fine_role<P, CN, 4>(pa, f / pa.g.B, f % pa.g.B);
   }
 }
 
@@ -350,6 +473,29 @@ static PipeKernel pipe_kernel(int M, bool cn, int IN, int W, int act, bool split
   if (IN == 4 && W == 50) return act ? pipe_kernel_c<4, 50, 1, 1>(M, cn) : pipe_kernel_c<4, 50, 1, 0>(M, cn);
   if (IN == 4 && W == 32 && act == 0) return pipe_kernel_c<4, 32, 1, 0>(M, cn);
   return nullptr;
+}
+
+typedef void (*PipeNumKernel)(PipeArgs);
+static PipeNumKernel pipe_num_kernel(int M, bool cn) {
+  if (M <= 256) return cn ? k_parareal_pipe_num<2, true> : k_parareal_pipe_num<2, false>;
+  if (M <= 512) return cn ? k_parareal_pipe_num<4, true> : k_parareal_pipe_num<4, false>;
+  if (M <= 1024) return cn ? k_parareal_pipe_num<8, true> : k_parareal_pipe_num<8, false>;
+  return nullptr;
+}
+bool pipe_num_supported(int M, bool cn) { return pipe_num_kernel(M, cn) != nullptr; }
+cudaError_t launch_parareal_pipe_num(const PipeArgs &pa, int M, bool cn, cudaStream_t s) {
+  PipeNumKernel k = pipe_num_kernel(M, cn);
+  if (!k) return cudaErrorInvalidValue;
+  int dev = 0, nsm = 0, occ = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 128, 0);
+  if (e != cudaSuccess) return e;
+  const int grid = (pa.K + 1) * pa.g.B + pa.g.B * pa.N;
+  if (grid > occ * nsm) return cudaErrorCooperativeLaunchTooLarge;
+  PipeArgs arg = pa;
+  void *params[] = {&arg};
+  return cudaLaunchCooperativeKernel((const void *)k, dim3(grid), dim3(128), params, 0, s);
 }
 
 bool pipe_supported(int M, bool cn, int IN, int W, int act, bool split) {

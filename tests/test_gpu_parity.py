@@ -518,3 +518,30 @@ def test_pipeline_falls_back_when_not_co_resident():
     assert ra["kernel_launches"] == rb["kernel_launches"], "auto mode should have fallen back"
     assert ra["iterations"] == rb["iterations"] == 8
     assert np.array_equal(a, b) and np.array_equal(ra["delta"], rb["delta"])
+
+
+@pytest.mark.parametrize("M,N,B,theta,nc", [(1024, 32, 1, 1.0, 1), (1024, 32, 1, 1.0, 50), (1024, 32, 1, 0.5, 1),
+                                           (700, 12, 1, 1.0, 3), (256, 8, 6, 1.0, 1), (64, 4, 1, 1.0, 1)])
+def test_pipelined_numerical_G_matches_blocking(M, N, B, theta, nc):
+    """NEXT-2 with the numerical coarse propagator (implicit Euler, n_c steps): one K1
+    chain system per iteration runs beside the fine solves in the cooperative kernel; iterates,
+    output and δ are bitwise the blocking schedule's, which the oracle check of the blocking
+    path (test_parareal_*) covers; here also the final state against the oracle."""
+    if B > 1:
+        p = synth.portfolio(n_k=B // 2, n_s=2, M=M, N=N, coarse=synth.COARSE_IMPLICIT_EULER, coarse_steps=nc,
+                            max_iter=3, tol=0.0)
+    else:
+        p = synth.single(M, N, coarse=synth.COARSE_IMPLICIT_EULER, coarse_steps=nc, max_iter=min(3, N), tol=0.0,
+                         fine_theta=theta)
+    with ctx_for(p) as c:
+        a, ra = c.solve()
+        it_a = c.copy_iterates(0, p.N + 1)
+        c.set_option(parareal.OPT_PIPELINE, 1)
+        b, rb = c.solve()
+        it_b = c.copy_iterates(0, p.N + 1)
+    assert ra["kernel_launches"] < rb["kernel_launches"], "auto mode did not pipeline"
+    assert ra["iterations"] == rb["iterations"] == p.max_iter
+    assert np.array_equal(a, b) and np.array_equal(it_a, it_b)
+    assert np.array_equal(ra["delta"], rb["delta"])
+    U_ref = oracle.parareal(p)[0]
+    assert_close(a, U_ref[-1], what="pipelined numerical-G Parareal M=%d" % M)
