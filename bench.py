@@ -42,6 +42,8 @@ def parse():
     ap.add_argument("--config", default="C2")
     ap.add_argument("--coarse", default="pinn", choices=["pinn", "ie"])
     ap.add_argument("--iters", type=int, default=3, help="fixed Parareal iterations K (tol = 0)")
+    ap.add_argument("--coarse-steps", type=int, default=1,
+                    help="implicit-Euler steps per slice of the numerical coarse G (--coarse ie; paper ratio n_f/2 = 50)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-c3-sweep", action="store_true", help="skip the C3 fine-sweep HBM roofline leg")
@@ -58,7 +60,7 @@ def parse():
 def problem_for(args):
     from paper_2303_03848_b200 import synth
     coarse = synth.COARSE_PINN if args.coarse == "pinn" else synth.COARSE_IMPLICIT_EULER
-    p = synth.config(args.config, coarse=coarse, coarse_steps=1, tol=0.0, fine_theta=args.fine_theta)
+    p = synth.config(args.config, coarse=coarse, coarse_steps=args.coarse_steps, tol=0.0, fine_theta=args.fine_theta)
     return p.replace(max_iter=min(args.iters, p.N))
 
 
