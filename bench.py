@@ -180,7 +180,7 @@ def config_dict(args, p):
                             args.config, p.M, p.N, p.B, p.fine_steps,
                             "IE" if p.fine_theta == 1.0 else ("CN" if p.fine_theta == 0.5 else "theta=%g" % p.fine_theta),
                             ("PINN %s tanh (%s)" % (pinn_dims(args), args.pinn_prec)) if args.coarse == "pinn"
-                            else "implicit-Euler (1 step/slice)",
+                            else "implicit-Euler (%d step%s/slice)" % (p.coarse_steps, "" if p.coarse_steps == 1 else "s"),
                             p.max_iter),
             "M": p.M, "N": p.N, "B": p.B, "fine_steps": p.fine_steps, "fine_theta": p.fine_theta, "K": p.max_iter,
             "coarse": args.coarse, "parallelism": "time-slices/%d" % args.gpus,
