@@ -19,16 +19,19 @@ bool pinn_smem_supported(int IN, int W, int act);
 int pinn_smem_pts(int W);
 cudaError_t pinn_smem_prepare(int IN, int W, int act, int smem_bytes);
 cudaError_t launch_pinn_smem(int IN, int W, int act, const PinnArgs &a, dim3 grid, size_t smem, cudaStream_t s);
-// K3 latency mode (pinn_smem.cu): kPinnSplitG threads per point for 20-wide nets (shuffle
-// exchange); pinn_split_G(W) threads per point (group kernels, shared-memory exchange) for
-// 32-, 50- and 64-wide nets; pinn_split_ppc(W) points per 128-thread CTA
+// K3 latency mode (pinn_smem.cu): G threads per point; G = kPinnSplitG with 20-wide nets is the
+// shuffle kernel, any other G a group kernel (shared-memory exchange, group-ordered weights:
+// pinn_group_G(W) = 10 for 20/50-wide, 8 for 32-wide, 16 for 64-wide nets); pinn_split_ppc(G)
+// points per 128-thread CTA
 constexpr int kPinnSplitG = 4;
 constexpr int kPinnSplitMinPPC = 8;  // the fewest points per CTA of any latency-mode kernel
-int pinn_split_G(int W);
-int pinn_split_ppc(int W);
-bool pinn_split_supported(int IN, int W, int act);
-cudaError_t pinn_split_prepare(int IN, int W, int act, int smem_bytes);
-cudaError_t launch_pinn_split(int IN, int W, int act, const PinnArgs &a, dim3 grid, size_t smem, cudaStream_t s);
+int pinn_group_G(int W);
+bool pinn_split_is_group(int W, int G);
+int pinn_split_ppc(int G);
+bool pinn_split_supported(int IN, int W, int act, int G);
+cudaError_t pinn_split_prepare(int IN, int W, int act, int G, int smem_bytes);
+cudaError_t launch_pinn_split(int IN, int W, int act, int G, const PinnArgs &a, dim3 grid, size_t smem,
+                              cudaStream_t s);
 // K3, constant-bank weights (pinn_param.cu)
 bool pinn_param_supported(int IN, int W, int LH, int act);
 cudaError_t launch_pinn_param(int IN, int W, int LH, int act, const float *pk, const PinnArgs &a, dim3 grid,
@@ -55,11 +58,11 @@ struct PipeArgs {
   unsigned long long *trace;   // nullable: [K+1][N][3] %globaltimer (chain warp 0 of CTA 0 at each
                                // slice; fine (n, b=0) start and end), for PR_PIPE_TRACE
 };
-bool pipe_supported(int M, bool cn, int IN, int W, int act, bool split);
+bool pipe_supported(int M, bool cn, int IN, int W, int act, int G);  // G: chain threads per point (1: one)
 bool pipe_num_supported(int M, bool cn);  // numerical coarse G (one K1 chain CTA per iteration and instance)
 cudaError_t launch_parareal_pipe_num(const PipeArgs &pa, int M, bool cn, cudaStream_t s);
-int pipe_chain_warps(int W, bool split);  // warps per chain CTA (the chain's points per CTA = warps · 32/G)
-cudaError_t launch_parareal_pipe(const PipeArgs &pa, int M, bool cn, int IN, int W, int act, bool split,
+int pipe_chain_warps(int W, int G);  // warps per chain CTA (the chain's points per CTA = warps · 32/G)
+cudaError_t launch_parareal_pipe(const PipeArgs &pa, int M, bool cn, int IN, int W, int act, int G,
                                  size_t smem, cudaStream_t s);
 // K6/K7 (misc.cu)
 cudaError_t launch_payoff(float *U0, int M, int Mp, int B, const double *Lb, const double *Kb, cudaStream_t s);

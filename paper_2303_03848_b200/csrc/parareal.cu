@@ -519,19 +519,35 @@ void dispatch_res(bool chain, int M, const pr::ResidentArgs &a, int nsys, cudaSt
 }
 
 // ---------------------------------------------------------------- PINN launches
-// Few grid points (B·M ≤ kSplitMaxPoints): the coarse chain is latency-bound, so the latency
-// mode (kPinnSplitG threads per point for 20-wide nets; pinn_split_G(W) for the group kernels,
-// auto only while B·M ≤ kGroupMaxPoints, where one thread per point leaves most SMs idle) runs
-// it; otherwise constant-bank weights when instantiated, else shared-memory weights.
+// Few grid points (B·M ≤ kSplitMaxPoints): the coarse chain is latency-bound, so a latency mode
+// runs it with G threads per point (split_G): the group kernels (pinn_group_G(W) threads, shared-
+// memory exchange, group-ordered weights) while B·M ≤ kGroupMaxPoints, where one thread per
+// point leaves most SMs idle; 20-wide nets beyond that use the 4-thread shuffle kernel.  Otherwise
+// constant-bank weights when instantiated, else shared-memory weights.
 // PR_OPT_PINN_KERNEL: 0 auto, 1 shared memory, 2 latency mode.
 constexpr long kSplitMaxPoints = 65536;
 constexpr long kGroupMaxPoints = 16384;
 bool split_allowed(const pr_ctx *c) { return (long)c->B * c->M <= kSplitMaxPoints; }
+// 20-wide nets: in a problem the pipelined schedule can run (one GPU, fixed K, resident fine
+// kernel, M ≤ 1024) the 4-thread shuffle chain, whose 4-warp chain CTAs pack several per SM
+// beside the fine CTAs (measured 0.281 vs 0.287 ms per C2 solve with the group chain); elsewhere
+// the group kernel (blocking C2: 0.38 vs 0.43 ms).  The choice depends on the problem only, not on
+// PR_OPT_PIPELINE, so both schedules of one context use the same evaluator (bitwise-equal results).
+bool pipe_shape(const pr_ctx *c) {
+  return c->world == 1 && c->tol == 0.0 && c->max_iter >= 1 && !c->tc && c->coarse == PR_COARSE_PINN &&
+         use_resident(c) && c->M <= 1024;
+}
+int split_G(const pr_ctx *c) {
+  const bool small = (long)c->B * c->M <= kGroupMaxPoints;
+  if (c->W == 20) return small && !pipe_shape(c) ? pr::pinn_group_G(20) : pr::kPinnSplitG;
+  if (pr::pinn_group_G(c->W) > 0 && (small || c->opt_pinn_kernel == 2)) return pr::pinn_group_G(c->W);
+  return 0;
+}
 bool use_split_pinn(const pr_ctx *c) {
   if (c->tc || c->opt_pinn_kernel == 1) return false;
   if (c->opt_pinn_kernel == 0 && !split_allowed(c)) return false;
-  if (c->opt_pinn_kernel == 0 && c->W != 20 && (long)c->B * c->M > kGroupMaxPoints) return false;
-  return pr::pinn_split_supported(c->IN, c->W, c->act);
+  const int G = split_G(c);
+  return G > 0 && pr::pinn_split_supported(c->IN, c->W, c->act, G);
 }
 bool use_param_pinn(const pr_ctx *c) {
   if (c->tc || c->opt_pinn_kernel != 0 || use_split_pinn(c)) return false;
@@ -571,11 +587,11 @@ pr_status launch_pinn(pr_ctx *c, const pr::PinnArgs &a) {
     return PR_OK;
   }
   if (use_split_pinn(c)) {
-    const int ppc = pr::pinn_split_ppc(c->W);  // points per CTA
+    const int G = split_G(c), ppc = pr::pinn_split_ppc(G);  // points per CTA
     dim3 grid((c->M + ppc - 1) / ppc, c->B);
     pr::PinnArgs t = a;
-    if (c->W != 20) t.wts = c->d_wgrp;  // group kernels: hidden matrices in the group order
-    pr::launch_pinn_split(c->IN, c->W, c->act, t, grid, (size_t)c->nfloats * sizeof(float), c->stream);
+    if (pr::pinn_split_is_group(c->W, G)) t.wts = c->d_wgrp;  // group kernels: hidden matrices in the group order
+    pr::launch_pinn_split(c->IN, c->W, c->act, G, t, grid, (size_t)c->nfloats * sizeof(float), c->stream);
     LAUNCHED();
     return PR_OK;
   }
@@ -783,7 +799,7 @@ bool pipe_eligible(const pr_ctx *c) {
   if (!use_resident(c) || c->M > 1024) return false;
   if (c->coarse == PR_COARSE_IMPLICIT_EULER) return pr::pipe_num_supported(c->M, c->fine_theta != 1.0);
   // the chain evaluates as the blocking kernel would: latency mode if it is the one chosen
-  return pr::pipe_supported(c->M, c->fine_theta != 1.0, c->IN, c->W, c->act, use_split_pinn(c));
+  return pr::pipe_supported(c->M, c->fine_theta != 1.0, c->IN, c->W, c->act, use_split_pinn(c) ? split_G(c) : 1);
 }
 
 pr_status ensure_pipe(pr_ctx *c) {
@@ -808,7 +824,8 @@ pr_status solve_pipelined(pr_ctx *c) {
   pa.r.D = c->D;
   pa.r.Fk = c->Fk;
   pa.g = pinn_args(c);
-  if (use_split_pinn(c) && c->W != 20) pa.g.wts = c->d_wgrp;  // group chain: group-order weights
+  const int G = use_split_pinn(c) ? split_G(c) : 1;  // chain threads per point
+  if (pr::pinn_split_is_group(c->W, G)) pa.g.wts = c->d_wgrp;  // group chain: group-order weights
   pa.g.U = c->U;
   pa.g.Gh = c->Gh;
   pa.g.D = c->D;
@@ -823,8 +840,8 @@ pr_status solve_pipelined(pr_ctx *c) {
     pa.cpub = 1;
   } else {
     // chain points per CTA: the blocking chain's CTA (4 warps) times the chain-CTA width in warps / 4
-    const int nwc = pr::pipe_chain_warps(c->W, use_split_pinn(c));
-    const int ppc = (use_split_pinn(c) ? pr::pinn_split_ppc(c->W) : 128) * (nwc / 4);
+    const int nwc = pr::pipe_chain_warps(c->W, G);
+    const int ppc = (G > 1 ? pr::pinn_split_ppc(G) : 128) * (nwc / 4);
     pa.C = (c->M + ppc - 1) / ppc;  // chain CTAs per instance
     pa.cpub = pa.C * nwc;           // every chain warp publishes
     if ((size_t)pa.C * (nwc / 4) > (size_t)c->nch || (size_t)pa.C * nwc > (size_t)c->nch * 4) {
@@ -848,7 +865,7 @@ pr_status solve_pipelined(pr_ctx *c) {
   pa.fdone = c->pipe_flags + (size_t)2 * c->B * c->N;
   const cudaError_t e =
       num ? pr::launch_parareal_pipe_num(pa, c->M, c->fine_theta != 1.0, c->stream)
-          : pr::launch_parareal_pipe(pa, c->M, c->fine_theta != 1.0, c->IN, c->W, c->act, use_split_pinn(c),
+          : pr::launch_parareal_pipe(pa, c->M, c->fine_theta != 1.0, c->IN, c->W, c->act, G,
                                      (size_t)c->nfloats * sizeof(float), c->stream);
   if (e == cudaErrorCooperativeLaunchTooLarge) {
     cudaGetLastError();
@@ -1393,7 +1410,8 @@ pr_status parareal_load_pinn_weights(pr_ctx *c, int32_t n_linear, const int32_t 
     return fail(c, PR_ERR_UNSUPPORTED, fmt("network of %zu bytes exceeds the shared-memory budget", bytes));
   if (!tc) {
     CU(pr::pinn_smem_prepare(IN, Wd, activation, (int)bytes));
-    if (pr::pinn_split_supported(IN, Wd, activation)) CU(pr::pinn_split_prepare(IN, Wd, activation, (int)bytes));
+    if (pr::pinn_split_supported(IN, Wd, activation, pr::kPinnSplitG))
+      CU(pr::pinn_split_prepare(IN, Wd, activation, pr::kPinnSplitG, (int)bytes));
   }
   if (c->d_wts) cudaFree(c->d_wts);
   c->d_wts = nullptr;
@@ -1401,10 +1419,10 @@ pr_status parareal_load_pinn_weights(pr_ctx *c, int32_t n_linear, const int32_t 
   CU(cudaMemcpy(c->d_wts, pk.data(), bytes, cudaMemcpyHostToDevice));
   if (c->d_wgrp) cudaFree(c->d_wgrp);
   c->d_wgrp = nullptr;
-  if (!tc && Wd != 20 && pr::pinn_split_supported(IN, Wd, activation)) {
+  if (!tc && pr::pinn_group_G(Wd) > 0 && pr::pinn_split_supported(IN, Wd, activation, pr::pinn_group_G(Wd))) {
     // group kernels (pinn_chain.cuh, mlp_group): hidden matrix l stored as [i][q][k] =
     // W_l[q·NPT + k][i], so the G threads of a group read consecutive addresses for input i
-    const int G = pr::pinn_split_G(Wd), NPT = Wd / G;
+    const int G = pr::pinn_group_G(Wd), NPT = Wd / G;
     std::vector<float> pg(pk);
     for (int l = 1; l < LH; ++l) {
       const size_t o = (size_t)Wd * IN + Wd + (size_t)(l - 1) * ((size_t)Wd * Wd + Wd);

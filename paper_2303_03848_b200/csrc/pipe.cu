@@ -73,7 +73,7 @@ __device__ __forceinline__ void publish_set(int *p, int v) {
 // per point (shared-memory weights, any instantiated width: the paper's 10×50 net).
 template <int IN, int W, int G, int ACT>
 __device__ __forceinline__ float chain_eval(const float *sw, int LH, const float (&x)[IN], float *row, bool active) {
-  if constexpr (G > 1 && W != 20) {
+  if constexpr (G > 1 && !(W == 20 && G == kPinnSplitG)) {
     return mlp_group<IN, W, G, ACT>(sw, LH, x, row, active);  // sw = the global weights here
   } else if constexpr (G > 1) {
     return mlp_split<IN, W, G, ACT>(sw, LH, x);
@@ -102,7 +102,7 @@ __device__ void chain_role(const PipeArgs &pa, int k, int b, int chunk, const fl
   const bool leader = active && lane % G == 0;
   const int j = chunk * (NWC * GPW) + wid * GPW + lane / G;
   const bool ok = active && j < a.M;
-  constexpr bool kGroup = G > 1 && W != 20;
+  constexpr bool kGroup = G > 1 && !(W == 20 && G == kPinnSplitG);
   __shared__ __align__(16) float xrow[NWC][kGroup ? GPW : 1][kGroup ? GroupRow<W>::kPad : 4];  // group exchange rows
   float *xr = &xrow[wid][kGroup && lane / G < GPW ? lane / G : (kGroup ? GPW - 1 : 0)][0];
   const double dS = Lb / (a.M + 1);
@@ -425,7 +425,7 @@ __global__ void __launch_bounds__(NWC * 32) k_parareal_pipe(PipeArgs pa) {
   const int nchain = (pa.K + 1) * per;
   if ((int)blockIdx.x < nchain) {
     const float *w = pa.g.wts;  // group kernels read the weights through L1
-    if (G == 1 || W == 20) {
+    if (G == 1 || (W == 20 && G == kPinnSplitG)) {  // smem weights (group chains read them through L1)
       for (int i = threadIdx.x; i < pa.g.nfloats; i += blockDim.x) sw[i] = pa.g.wts[i];
       __syncthreads();
       w = sw;
@@ -445,8 +445,8 @@ typedef void (*PipeKernel)(PipeArgs);
 // (K+1)·C chain CTAs + N fine CTAs ≤ 148 run one per SM and the chains do not share SMs with the
 // fine solves (measured: 3× slower chain slices when they did).
 template <int IN, int W, int G>
-constexpr int pipe_nwc() { return (G > 1 && W != 20) ? 12 : 4; }
-int pipe_chain_warps(int W, bool split) { return split && W != 20 ? 12 : 4; }
+constexpr int pipe_nwc() { return (G > 1 && !(W == 20 && G == kPinnSplitG)) ? 12 : 4; }
+int pipe_chain_warps(int W, int G) { return pinn_split_is_group(W, G) ? 12 : 4; }
 
 template <bool CN, int IN, int W, int G, int ACT>
 static PipeKernel pipe_kernel_p(int M) {
@@ -462,14 +462,18 @@ static PipeKernel pipe_kernel_c(int M, bool cn) {
 }
 // instantiated: latency-mode 20-wide nets (G = 4), and one thread per point for the paper's
 // 10×50 architecture (tanh or ReLU) and 32-wide tanh nets
-static PipeKernel pipe_kernel(int M, bool cn, int IN, int W, int act, bool split) {
-  if (split) {
+static PipeKernel pipe_kernel(int M, bool cn, int IN, int W, int act, int G) {
+  if (G == 10) {  // group chains (12-warp CTAs)
     if (IN == 4 && W == 50) return act ? pipe_kernel_c<4, 50, 10, 1>(M, cn) : pipe_kernel_c<4, 50, 10, 0>(M, cn);
+    return nullptr;
+  }
+  if (G == kPinnSplitG) {  // shuffle chain
     if (W != 20 || act != 0) return nullptr;
     if (IN == 4) return pipe_kernel_c<4, 20, kPinnSplitG, 0>(M, cn);
     if (IN == 2) return pipe_kernel_c<2, 20, kPinnSplitG, 0>(M, cn);
     return nullptr;
   }
+  if (G != 1) return nullptr;
   if (IN == 4 && W == 50) return act ? pipe_kernel_c<4, 50, 1, 1>(M, cn) : pipe_kernel_c<4, 50, 1, 0>(M, cn);
   if (IN == 4 && W == 32 && act == 0) return pipe_kernel_c<4, 32, 1, 0>(M, cn);
   return nullptr;
@@ -498,23 +502,23 @@ cudaError_t launch_parareal_pipe_num(const PipeArgs &pa, int M, bool cn, cudaStr
   return cudaLaunchCooperativeKernel((const void *)k, dim3(grid), dim3(128), params, 0, s);
 }
 
-bool pipe_supported(int M, bool cn, int IN, int W, int act, bool split) {
-  return pipe_kernel(M, cn, IN, W, act, split) != nullptr;
+bool pipe_supported(int M, bool cn, int IN, int W, int act, int G) {
+  return pipe_kernel(M, cn, IN, W, act, G) != nullptr;
 }
 
 // Launches the cooperative kernel; cudaErrorCooperativeLaunchTooLarge (or not supported) tells
 // the caller to use the blocking schedule.
-cudaError_t launch_parareal_pipe(const PipeArgs &pa, int M, bool cn, int IN, int W, int act, bool split,
+cudaError_t launch_parareal_pipe(const PipeArgs &pa, int M, bool cn, int IN, int W, int act, int G,
                                  size_t smem, cudaStream_t s) {
-  PipeKernel k = pipe_kernel(M, cn, IN, W, act, split);
+  PipeKernel k = pipe_kernel(M, cn, IN, W, act, G);
   if (!k) return cudaErrorInvalidValue;
-  if (split && W != 20) smem = 0;  // group chains read the weights through L1
+  if (pinn_split_is_group(W, G)) smem = 0;  // group chains read the weights through L1
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int dev = 0, nsm = 0, occ = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  const int nthreads = 32 * pipe_chain_warps(W, split);
+  const int nthreads = 32 * pipe_chain_warps(W, G);
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, nthreads, smem);
   if (e != cudaSuccess) return e;
   const int grid = (pa.K + 1) * pa.g.B * pa.C + pa.g.B * pa.N;
