@@ -315,11 +315,21 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     p = problem_for(args)
-    if p.N % world:
-        raise SystemExit("N=%d not divisible by %d GPUs" % (p.N, world))
+    # C4 (the batched portfolio) shards its independent instances across the GPUs (SURVEY §8(e):
+    # no data-path collective; fixed K, so no δ all-reduce either): each rank solves its B/R
+    # instances as a one-GPU problem.  The other configs shard the time slices (NCCL chain).
+    shard_inst = args.config.upper() == "C4" and world > 1
+    if shard_inst:
+        if p.B % world:
+            raise SystemExit("B=%d not divisible by %d GPUs" % (p.B, world))
+        p_run, ctx_world, ctx_rank = synth.shard_instances(p, rank, world), 1, 0
+    else:
+        if p.N % world:
+            raise SystemExit("N=%d not divisible by %d GPUs" % (p.N, world))
+        p_run, ctx_world, ctx_rank = p, world, rank
     net = synth.kaiming_net(pinn_dims(args), seed=0)
     nccl_id = None
-    if world > 1:
+    if ctx_world > 1:
         obj = [parareal.get_nccl_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
@@ -328,7 +338,8 @@ def main():
     # its own non-blocking stream, which the events on the NULL stream would not order with)
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
-    ctx = parareal.Context(p, rank=rank, world=world, device=local, nccl_id=nccl_id, stream=stream.cuda_stream)
+    ctx = parareal.Context(p_run, rank=ctx_rank, world=ctx_world, device=local, nccl_id=nccl_id,
+                           stream=stream.cuda_stream)
     if p.coarse == synth.COARSE_PINN:
         ctx.load_weights(net, precision=PREC_CODE[args.pinn_prec])
     ws = torch.empty(ctx.workspace_bytes(), dtype=torch.uint8, device="cuda")
@@ -338,7 +349,7 @@ def main():
     # only; the phase times come from a few instrumented replays afterwards
     graph_timed, graph_phases = (0, 0) if args.no_graphs else (2, 1)
     ctx.set_option(parareal.OPT_USE_GRAPHS, graph_timed)
-    out = torch.empty((p.B, p.M), dtype=torch.float32, device="cuda")
+    out = torch.empty((p_run.B, p.M), dtype=torch.float32, device="cuda")
     flush = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device="cuda")
 
     def barrier():
@@ -395,7 +406,7 @@ def main():
     # pipelined schedule: its phases overlap (reported as one span); the blocking schedule's phase
     # times (a few solves) give Eq. (8)'s c_c, c_f and the pipelining gain
     ph_block, block_ms = ph, None
-    if ph["ms_fine"] == ph["ms_coarse"] and world == 1:
+    if ph["ms_fine"] == ph["ms_coarse"] and ctx_world == 1:
         ctx.set_option(parareal.OPT_PIPELINE, 1)
         ctx.solve_device(out)
         breps = []
@@ -410,7 +421,7 @@ def main():
     pk, pk_src = peaks()
     clk_mhz = float(pk.get("sm_max_mhz", 1965.0))
     n_sm = torch.cuda.get_device_properties(local).multi_processor_count
-    roof = roofline(p, ph, K, world, rank, pk, pk_src, clk_mhz, n_sm, synth, dims=pinn_dims(args),
+    roof = roofline(p_run, ph, K, ctx_world, ctx_rank, pk, pk_src, clk_mhz, n_sm, synth, dims=pinn_dims(args),
                     tc_prec=None if args.pinn_prec == "fp32" else args.pinn_prec)
     # ---------------- north-star gate: the HBM-streamed fine sweep (K2) at the C3 grid, measured
     # live in the same run (one fine sweep over 64 slices x 2^20 points x 100 steps)
@@ -420,9 +431,10 @@ def main():
     # ---------------- e2e through the host-buffer ABI call (pinned H2D of V_T, D2H of V_0)
     e2e = None
     if not args.no_e2e:
-        vt_host = torch.from_numpy(ctx.initial_state()).pin_memory() if rank == 0 else None
-        v0_host = torch.empty((p.B, p.M), dtype=torch.float32).pin_memory()
-        ctx.solve_host_ptrs(vt_host.data_ptr() if rank == 0 else None, v0_host.data_ptr())
+        has_vt = ctx_rank == 0  # (slice sharding: rank 0 owns U_0; instance sharding: every rank)
+        vt_host = torch.from_numpy(ctx.initial_state()).pin_memory() if has_vt else None
+        v0_host = torch.empty((p_run.B, p.M), dtype=torch.float32).pin_memory()
+        ctx.solve_host_ptrs(vt_host.data_ptr() if has_vt else None, v0_host.data_ptr())
         barrier()
         torch.cuda.synchronize()
         ems = []
@@ -430,7 +442,7 @@ def main():
             flush.zero_()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            ctx.solve_host_ptrs(vt_host.data_ptr() if rank == 0 else None, v0_host.data_ptr())
+            ctx.solve_host_ptrs(vt_host.data_ptr() if has_vt else None, v0_host.data_ptr())
             e1.record(stream)
             e1.synchronize()
             ems.append(e0.elapsed_time(e1))
@@ -458,7 +470,8 @@ def main():
                 "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f32 state / f64 implicit solves / f32 PINN",
                 "data": "synthetic (payoff initial state, Kaiming-random PINN weights seed 0)",
-                "config": config_dict(args, p),
+                "config": dict(config_dict(args, p), **({"parallelism": "instances/%d (B/R per GPU, no exchange)" % world}
+                                                        if shard_inst else {})),
                 "speedup_vs_serial_fine": (serial_ms / ms_step) if serial_ms else None,
                 "serial_fine_ms": serial_ms,
                 "phases_ms": ph,
@@ -471,6 +484,9 @@ def main():
                 "cpu_baseline_threaded": cpu_threaded, "e2e": e2e,
                 "gpu_launches": launches,
                 "clocks": clk.summary()}
+        if shard_inst:
+            line["speedup_basis"] = ("per GPU: the serial fine solve of one rank's B/R instances vs the Parareal "
+                                     "step (every rank solves its own instances)")
         line["schedule"] = "pipelined" if block_ms is not None else "blocking"
         if block_ms is not None:
             line["blocking_schedule_ms_per_solve"] = block_ms

@@ -116,6 +116,17 @@ def config(name: str, **kw) -> Problem:
     raise KeyError(name)
 
 
+def shard_instances(p: Problem, rank: int, world: int) -> Problem:
+    """Instances [rank·B/world, (rank+1)·B/world) of p: the C4 multi-GPU layout (SURVEY.md §8(e):
+    independent problems, no data-path exchange; with a fixed K there is no collective at all)."""
+    if world < 1 or not 0 <= rank < world or p.B % world:
+        raise ValueError("B=%d instances cannot be split over %d ranks" % (p.B, world))
+    n = p.B // world
+    sl = slice(rank * n, (rank + 1) * n)
+    return p.replace(strike=p.strike[sl].copy(), sigma=p.sigma[sl].copy(), rate=p.rate[sl].copy(),
+                     L=p.L[sl].copy())
+
+
 PINN_3x20 = [4, 20, 20, 20, 1]          # BASELINE configs "PINN 3x20 tanh"
 PINN_PAPER = [4] + [50] * 10 + [1]      # PAPER.md:203 "10 fully connected layers with 50 neurons"
 

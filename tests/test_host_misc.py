@@ -63,3 +63,23 @@ def test_oracle_threaded_fine_is_bitwise_serial():
         a = oracle.parareal(p, net, history=True)
         b = oracle.parareal(p, net, history=True, threads=3)
         assert a[2] == b[2] and np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and np.array_equal(a[3], b[3])
+
+
+def test_instance_sharding_covers_and_matches_the_oracle():
+    """C4's multi-GPU layout: every rank solves B/R instances as its own
+    problem; the shards cover the instances in order, and (instances being independent, K fixed)
+    the oracle's output per shard is bitwise the full problem's rows."""
+    import numpy as np
+    import oracle
+    from paper_2303_03848_b200 import synth
+    p = synth.portfolio(n_k=2, n_s=2, M=32, N=4, coarse=synth.COARSE_IMPLICIT_EULER, max_iter=2, tol=0.0)
+    full = oracle.parareal(p)[0][-1]
+    for world in (1, 2, 4):
+        shards = [synth.shard_instances(p, r, world) for r in range(world)]
+        assert [s.B for s in shards] == [p.B // world] * world
+        assert np.array_equal(np.concatenate([s.strike for s in shards]), p.strike)
+        assert np.array_equal(np.concatenate([s.sigma for s in shards]), p.sigma)
+        got = np.concatenate([oracle.parareal(s)[0][-1] for s in shards])
+        assert np.array_equal(got, full)
+    with pytest.raises(ValueError):
+        synth.shard_instances(p, 0, 3)
