@@ -16,6 +16,7 @@
 //     hidden layer, accumulates the output layer W → 1 in fp32.
 // fp16 operands, fp32 accumulation: the north_star tolerance for a tensor-core PINN is 1e-3.
 #include <type_traits>
+#include <stdlib.h>
 #include <cuda_fp16.h>
 #include <cuda_bf16.h>
 #include "launch.h"
@@ -367,6 +368,299 @@ __global__ void __launch_bounds__(128) k_pinn_chain_tc(PinnTcArgs ta) {
   if (w == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((uint32_t)W));
 }
 
+// ---------------------------------------------------------------- K4 ping-pong (bf16)
+constexpr int kTc2Ring = 4;  // weight-chunk ring of the ping-pong kernel (one CTA per SM: a deeper ring)
+// Two 128-point tiles per CTA and a warp-specialised schedule, so one tile's epilogue overlaps
+// the other tile's MMAs: warpgroups 0 and 1 (threads 0-255) each own a tile (thread ↔ point ↔
+// TMEM lane of its tile's W accumulator columns), warp 8 allocates TMEM (2W columns) and its lane 0
+// issues every MMA and weight load.  Per hidden layer and tile: the issuer waits for the tile's A
+// operand (bar_a[w], 128 arrivals after the tile's previous epilogue, which also means its TMEM
+// columns have been read), issues the K-chunked MMAs and commits to bar_mma[w]; the warpgroup
+// waits on bar_mma[w], runs the epilogue and arrives on bar_a[w].  With tile 0's epilogue running
+// while tile 1's MMAs do (and vice versa) the tensor pipe no longer idles through every epilogue
+// (k_pinn_chain_tc: 20-25 % tensor-pipe activity).  Weights stream through the same 2-chunk ring,
+// in the order (slice, layer, tile, chunk) — each tile re-reads its layer's chunks — or stay
+// resident when they fit.  Same arithmetic per point as k_pinn_chain_tc<…, SPLIT = false>.
+__device__ __forceinline__ void tc_mbar_init_n(uint64_t *bar, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(tc_smem_u32(bar)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void tc_mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc_smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+
+template <int IN, int W, int ACT>
+__global__ void __launch_bounds__(288, 1) k_pinn_chain_tc2(PinnTcArgs ta) {
+  using T = __nv_bfloat16;
+  constexpr int TILE = 128;
+  constexpr uint32_t kIdesc = umma_idesc<true>(TILE, W);
+  constexpr uint32_t kPlaneA = (uint32_t)TILE * W * 2;
+  constexpr uint32_t kChunk = (uint32_t)W * kTcKC * 2;
+  constexpr int NCH = W / kTcKC;
+  const PinnArgs &a = ta.g;
+  extern __shared__ __align__(128) unsigned char tc_smem[];
+  T *sA = reinterpret_cast<T *>(tc_smem);  // [2 tiles][128 × W]
+  unsigned char *sB = tc_smem + 2 * kPlaneA;
+  constexpr int NB = kTc2Ring;  // streaming ring depth (NB − 1 chunks in flight)
+  const int nchunks = ta.resident ? (a.LH - 1) * NCH : NB;
+  float *sP = reinterpret_cast<float *>(sB + (size_t)nchunks * kChunk);
+  __shared__ __align__(8) uint64_t bar_mma[2], bar_a[2], bar_w, bar_full[NB], bar_free[NB];
+  __shared__ uint32_t s_tmem;
+  __shared__ double red[16];
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const int wg = t >> 7;  // 0, 1: epilogue warpgroups; 2: the issuer warp
+  for (int i = t; i < a.nfloats; i += blockDim.x) sP[i] = a.wts[i];
+  if (t == 0) {
+    for (int i = 0; i < 2; ++i) {
+      tc_mbar_init_n(&bar_mma[i], 1);
+      tc_mbar_init_n(&bar_a[i], TILE);
+    }
+    for (int i = 0; i < NB; ++i) {
+      tc_mbar_init_n(&bar_full[i], 1);
+      tc_mbar_init_n(&bar_free[i], 1);
+    }
+    tc_mbar_init_n(&bar_w, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 8) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tc_smem_u32(&s_tmem)),
+                 "r"((uint32_t)(2 * W)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = s_tmem;
+  const int ln_end = a.Gout ? a.ln0 + 1 : a.ln1;
+  const int nslices = ln_end - a.ln0;
+
+  if (wg == 2) {  // ---------------- the issuer (lane 0 of warp 8)
+    if (lane == 0 && a.LH > 1) {
+      const uint32_t aBase = tc_smem_u32(sA), bBase = tc_smem_u32(sB);
+      const int nseq = (a.LH - 1) * NCH;  // chunks of one tile's pass over the hidden layers
+      auto wchunk = [&](unsigned g) {      // sequence g → weight chunk (order: slice, layer, tile, chunk)
+        const unsigned q = g % (unsigned)(2 * nseq);
+        return (q / (2 * NCH)) * NCH + q % NCH;
+      };
+      auto load_chunk = [&](unsigned g) {
+        tc_bulk_g2s(sB + (size_t)(g % NB) * kChunk, (const unsigned char *)ta.wh + (size_t)wchunk(g) * kChunk, kChunk,
+                    &bar_full[g % NB]);
+      };
+      if (ta.resident) {
+        tc_bulk_g2s(sB, ta.wh, (uint32_t)((a.LH - 1) * NCH) * kChunk, &bar_w);
+        tc_mbar_wait(&bar_w, 0);
+      } else {
+        for (unsigned d = 0; d + 1 < (unsigned)NB; ++d) load_chunk(d);
+      }
+      unsigned g = 0;
+      uint32_t ph_a[2] = {0, 0};
+#pragma unroll 1
+      for (int sl = 0; sl < nslices; ++sl) {
+#pragma unroll 1
+        for (int l = 1; l < a.LH; ++l) {
+#pragma unroll 1
+          for (int w = 0; w < 2; ++w) {
+            tc_mbar_wait(&bar_a[w], ph_a[w]);
+            ph_a[w] ^= 1;
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t aw = aBase + (uint32_t)w * kPlaneA, dw = tmem + (uint32_t)(w * W);
+#pragma unroll 1
+            for (int c = 0; c < NCH; ++c) {
+              uint32_t bc;
+              if (ta.resident) {
+                bc = bBase + (uint32_t)((l - 1) * NCH + c) * kChunk;
+              } else {
+                tc_mbar_wait(&bar_full[g % NB], (g / NB) & 1);
+                bc = bBase + (g % NB) * kChunk;
+              }
+#pragma unroll
+              for (int ks = 0; ks < kTcKC / 16; ++ks) {
+                const uint32_t ao = (uint32_t)(c * (kTcKC / 8) + 2 * ks) * 128, bo2 = (uint32_t)(2 * ks) * 128;
+                const uint64_t da = umma_desc(aw + ao, 128, 16 * W), db = umma_desc(bc + bo2, 128, 16 * kTcKC);
+                const uint32_t acc = (c > 0 || ks > 0) ? 1u : 0u;
+                asm volatile(
+                    "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                    "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(dw),
+                    "l"(da), "l"(db), "r"(kIdesc), "r"(acc));
+              }
+              if (!ta.resident) {
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                                 tc_smem_u32(&bar_free[g % NB]))
+                             : "memory");
+                // the buffer of chunk g−1 takes chunk g + NB − 1 once chunk g−1's MMAs completed
+                if (g >= 1) tc_mbar_wait(&bar_free[(g - 1) % NB], ((g - 1) / NB) & 1);
+                load_chunk(g + NB - 1);
+                ++g;
+              }
+            }
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                             tc_smem_u32(&bar_mma[w]))
+                         : "memory");
+          }
+        }
+      }
+      if (!ta.resident)  // the prefetches still in flight
+        for (unsigned q = g; q + 1 < g + (unsigned)NB; ++q) tc_mbar_wait(&bar_full[q % NB], (q / NB) & 1);
+    }
+    __syncwarp();
+  } else {  // ---------------- epilogue warpgroup wg: tile wg of this CTA
+    const int tw = t & 127;
+    T *sAw = sA + (size_t)wg * TILE * W;
+    const uint32_t tlane = tmem + (uint32_t)(wg * W) + ((uint32_t)(32 * (warp & 3)) << 16);
+    const float *W0 = sP, *b0 = sP + W * IN;
+    const float *Wo = sP + W * IN + W + (size_t)(a.LH - 1) * W;
+    const float bo = Wo[W];
+    auto store_a = [&](int c0, const float (&h)[8]) {
+      const size_t off = cm_offset(tw, c0, W);
+      *reinterpret_cast<uint4 *>(sAw + off) =
+          make_uint4(pack2<T>(h[0], h[1]), pack2<T>(h[2], h[3]), pack2<T>(h[4], h[5]), pack2<T>(h[6], h[7]));
+    };
+    // fixed-order sum of (num, den) over the 256 epilogue threads; valid in thread 0
+    auto reduce256 = [&](double &num, double &den) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        num += __shfl_xor_sync(0xffffffffu, num, o);
+        den += __shfl_xor_sync(0xffffffffu, den, o);
+      }
+      epi_sync();
+      if (lane == 0) { red[2 * warp] = num; red[2 * warp + 1] = den; }
+      epi_sync();
+      if (t == 0) {
+        num = 0.0; den = 0.0;
+        for (int q = 0; q < 8; ++q) { num += red[2 * q]; den += red[2 * q + 1]; }
+      }
+    };
+    const int b = blockIdx.y;
+    const double Lb = a.Lb[b];
+    const float gscale = (float)(Lb * (double)a.out_scale);
+    const float invL = (float)(1.0 / Lb);
+    const size_t sstride = (size_t)a.B * a.Mp;
+    const int j = blockIdx.x * (2 * TILE) + wg * TILE + tw;
+    const bool ok = j < a.M;
+    const double dS = Lb / (a.M + 1);
+    const float s_over_L = (float)(((j + 1) * dS) / Lb);
+    float *u0 = a.U + (size_t)a.ln0 * sstride + (size_t)b * a.Mp;
+    float u = 0.f;
+    if (a.Fcopy) {
+      const float *f = a.Fcopy + (size_t)b * a.Mp;
+      double num = 0.0, den = 0.0;
+      if (ok) {
+        u = f[j];
+        const double dd = (double)u - (double)u0[j];
+        num = dd * dd;
+        den = (double)u * u;
+      }
+      epi_sync();
+      if (ok) u0[j] = u;
+      if (a.partials) {
+        reduce256(num, den);
+        if (t == 0) {
+          double *pp = a.partials + (((size_t)a.ln0 * a.B + b) * a.nch + blockIdx.x) * 2;
+          pp[0] = num;
+          pp[1] = den;
+        }
+      }
+    } else if (ok) {
+      u = u0[j];
+    }
+    uint32_t ph_m = 0;
+#pragma unroll 1
+    for (int ln = a.ln0; ln < ln_end; ++ln) {
+      const int n = a.n_base + ln;
+      const float tf = (float)((a.T - n * a.dT) / a.T), tt = (float)((a.T - (n + 1) * a.dT) / a.T);
+      float x[IN];
+      if (IN == 4) {
+        x[0] = tf * a.cs0;
+        x[1] = tt * a.cs1;
+        x[2] = (u * invL) * a.cs2;
+        x[3] = s_over_L * a.cs3;
+      } else {
+        x[0] = tt * a.cs0;
+        x[IN - 1] = s_over_L * a.cs1;
+      }
+#pragma unroll 1
+      for (int c0 = 0; c0 < W; c0 += 8) {
+        float h[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          float z = b0[c0 + q];
+#pragma unroll
+          for (int i = 0; i < IN; ++i) z = fmaf(W0[(c0 + q) * IN + i], x[i], z);
+          h[q] = act<ACT>(z);
+        }
+        store_a(c0, h);
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      tc_mbar_arrive(&bar_a[wg]);
+      float y = 0.f;
+#pragma unroll 1
+      for (int l = 1; l < a.LH; ++l) {
+        tc_mbar_wait(&bar_mma[wg], ph_m);
+        ph_m ^= 1;
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const float *bl = sP + W * IN + W + (size_t)(l - 1) * W;
+        const bool last = l == a.LH - 1;
+#pragma unroll 1
+        for (int c0 = 0; c0 < W; c0 += 32) {
+          float v[32];
+          tmem_ld32(tlane + (uint32_t)c0, v);
+#pragma unroll
+          for (int q = 0; q < 32; ++q) v[q] = act_tc<ACT, true>(v[q] + bl[c0 + q]);
+          if (last) {
+#pragma unroll
+            for (int q = 0; q < 32; ++q) y = fmaf(Wo[c0 + q], v[q], y);
+          } else {
+#pragma unroll
+            for (int q = 0; q < 32; q += 8) {
+              const float h[8] = {v[q], v[q + 1], v[q + 2], v[q + 3], v[q + 4], v[q + 5], v[q + 6], v[q + 7]};
+              store_a(c0 + q, h);
+            }
+          }
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        if (!last) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          tc_mbar_arrive(&bar_a[wg]);
+        }
+      }
+      y += bo;
+      const float g = gscale * y;
+      if (a.Gout) {
+        if (ok) a.Gout[(size_t)b * a.Mp + j] = g;
+        continue;  // (ln_end = ln0 + 1)
+      }
+      const size_t row = (size_t)ln * sstride + (size_t)b * a.Mp;
+      float nv = 0.f;
+      double num = 0.0, den = 0.0;
+      if (ok) {
+        nv = a.D ? g + a.D[row + j] : g;
+        if (a.Gh) a.Gh[row + j] = g;
+        if (a.partials) {
+          const double dd = (double)nv - (double)a.U[row + sstride + j];
+          num = dd * dd;
+          den = (double)nv * nv;
+        }
+        a.U[row + sstride + j] = nv;
+      }
+      u = nv;
+      if (a.partials) {
+        reduce256(num, den);
+        if (t == 0) {
+          double *pp = a.partials + (((size_t)(ln + 1) * a.B + b) * a.nch + blockIdx.x) * 2;
+          pp[0] = num;
+          pp[1] = den;
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 8) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((uint32_t)(2 * W)));
+  }
+}
+
 typedef void (*TcKernel)(PinnTcArgs);
 template <bool SPLIT>
 static TcKernel tc_kernel_t(int IN, int W, int act) {
@@ -421,8 +715,50 @@ void pinn_tc_pack(const float *Wl, int W, bool bf16, uint16_t *out) {
   }
 }
 
+// ping-pong kernel (bf16): two A planes; weights resident when they fit, else the 2-chunk ring
+static TcKernel tc2_kernel(int IN, int W, int act) {
+#define PR_TC2_CASE(IN_, W_) \
+  if (IN == IN_ && W == W_) return act ? k_pinn_chain_tc2<IN_, W_, 1> : k_pinn_chain_tc2<IN_, W_, 0>;
+  PR_TC2_CASE(4, 64) PR_TC2_CASE(4, 128) PR_TC2_CASE(4, 256) PR_TC2_CASE(2, 64) PR_TC2_CASE(2, 128) PR_TC2_CASE(2, 256)
+#undef PR_TC2_CASE
+  return nullptr;
+}
+static size_t pinn_tc2_smem(int W, int LH, int nfloats, bool *resident) {
+  const size_t a = 2 * 128 * (size_t)W * 2, chunk = (size_t)W * kTcKC * 2, p = (size_t)nfloats * 4;
+  const size_t all = (size_t)(LH - 1) * (W / kTcKC) * chunk;
+  *resident = a + all + p <= 200 * 1024;
+  return *resident ? a + all + p : a + kTc2Ring * chunk + p;
+}
+static bool use_pingpong(bool bf16) {
+  static const int on = getenv("PR_TC_PINGPONG") ? atoi(getenv("PR_TC_PINGPONG")) : 1;
+  return bf16 && on != 0;
+}
+
 cudaError_t launch_pinn_tc(int IN, int W, int act, bool bf16, const PinnArgs &a, const void *wh, dim3 grid,
                            cudaStream_t s) {
+  bool resident2 = false;
+  const size_t smem2 = pinn_tc2_smem(W, a.LH, a.nfloats, &resident2);
+  // The ping-pong kernel when the weights stay resident (its two A planes leave room for a short
+  // ring only): with streamed weights (8×256: 128 KB per layer and tile) both kernels are bound by
+  // the weight traffic from L2 and the one-tile kernel, two CTAs per SM, is as fast (measured
+  // 631 vs 610 M evals/s); with resident weights the ping-pong kernel is 1.86× faster (4×128)
+  // (and only for nets with enough MMA work per slice to hide the second tile's epilogue: 4×64
+  // measured 8.3 vs 9.3 G evals/s, 8×64 4.9 vs 3.5)
+  if (use_pingpong(bf16) && resident2 && (long)(a.LH - 1) * W * W >= 24576) {
+    TcKernel k2 = tc2_kernel(IN, W, act);
+    if (!k2) return cudaErrorInvalidValue;
+    const bool resident = resident2;
+    const size_t smem = smem2;
+    cudaError_t e = cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    PinnTcArgs ta;
+    ta.g = a;
+    ta.wh = wh;
+    ta.resident = resident ? 1 : 0;
+    dim3 g2((a.M + 255) / 256, grid.y);  // two 128-point tiles per CTA
+    k2<<<g2, 288, smem, s>>>(ta);
+    return cudaGetLastError();
+  }
   TcKernel k = tc_kernel(IN, W, act, bf16);
   if (!k) return cudaErrorInvalidValue;
   bool resident = false;
