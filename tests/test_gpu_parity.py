@@ -185,7 +185,7 @@ def test_pinn_G_tensor_cores(W, LH, act):
     assert_close(got, oracle.pinn_G(p, net, 5, U), tol=TOL_TC, what="G TC W=%d LH=%d" % (W, LH))
 
 
-@pytest.mark.parametrize("W,LH", [(64, 2), (256, 3)])
+@pytest.mark.parametrize("W,LH", [(64, 2), (256, 3), (128, 4), (64, 8)])
 def test_pinn_G_tensor_cores_bf16(W, LH):
     p = synth.portfolio(n_k=2, n_s=1, M=700, N=8)
     net = synth.kaiming_net([4] + [W] * LH + [1], seed=3 * W + LH)
@@ -196,18 +196,21 @@ def test_pinn_G_tensor_cores_bf16(W, LH):
     assert_close(got, oracle.pinn_G(p, net, 2, U), tol=3e-2, what="G TC bf16 W=%d LH=%d" % (W, LH))
 
 
-def test_pinn_tensor_core_parareal_chain():
-    """Full Parareal with the K4 coarse chain (correction fused, δ partials) at a C5-like width:
-    iterates within the TC tolerance of the oracle with the same fp32-exact fine propagator."""
+@pytest.mark.parametrize("prec,dims,tol", [(1, [4, 128, 128, 128, 1], TOL_TC), (2, [4, 128, 128, 128, 1], 5e-2)])
+def test_pinn_tensor_core_parareal_chain(prec, dims, tol):
+    """Full Parareal with the K4 coarse chain (correction fused, δ partials, the copy step) at a
+    C5-like width: iterates within the TC tolerance of the oracle with the same fp32-exact fine
+    propagator.  prec 1: split fp16 (one-tile kernel); prec 2: bf16 with resident weights, i.e.
+    the ping-pong kernel (two tiles per CTA, 256-point δ chunks); M = 3000 leaves a ragged CTA."""
     p = synth.single(3000, 6, coarse=synth.COARSE_PINN, max_iter=2, tol=0.0)
-    net = synth.kaiming_net([4, 128, 128, 128, 1], seed=9)
+    net = synth.kaiming_net(dims, seed=9)
     with ctx_for(p) as c:
-        c.load_weights(net, precision=parareal.PREC_FP16_TC)
+        c.load_weights(net, precision=prec)
         _, rep = c.solve()
         it = c.copy_iterates(0, p.N + 1)
     ref_U, ref_d, K, _ = oracle.parareal(p, net)
     assert rep["iterations"] == K == 2
-    assert_close(it, ref_U, tol=TOL_TC, what="TC Parareal iterates")
+    assert_close(it, ref_U, tol=tol, what="TC Parareal iterates (precision %d)" % prec)
 
 
 def test_pinn_tensor_core_errors():
