@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <condition_variable>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -102,6 +103,7 @@ struct Scheme {
 
 constexpr int kResidentMaxM = 2048;
 constexpr int kPinnTPB = 128;
+struct LoopGroup;  // in-process loopback transport (defined with the transport calls below)
 }  // namespace
 
 // ============================================================================ context
@@ -118,6 +120,7 @@ struct pr_ctx {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   ncclComm_t comm = nullptr;
+  LoopGroup *loop = nullptr;  // in-process loopback transport (test only), else NCCL
   // constants on device
   int nsets = 0;
   int *d_fset = nullptr;
@@ -533,9 +536,10 @@ bool split_allowed(const pr_ctx *c) { return (long)c->B * c->M <= kSplitMaxPoint
 // beside the fine CTAs (measured 0.281 vs 0.287 ms per C2 solve with the group chain); elsewhere
 // the group kernel (blocking C2: 0.38 vs 0.43 ms).  The choice depends on the problem only, not on
 // PR_OPT_PIPELINE, so both schedules of one context use the same evaluator (bitwise-equal results).
+// (independent of the rank count, so a problem's evaluator — and its results — are the same on any R)
 bool pipe_shape(const pr_ctx *c) {
-  return c->world == 1 && c->tol == 0.0 && c->max_iter >= 1 && !c->tc && c->coarse == PR_COARSE_PINN &&
-         use_resident(c) && c->M <= 1024;
+  return c->tol == 0.0 && c->max_iter >= 1 && !c->tc && c->coarse == PR_COARSE_PINN && use_resident(c) &&
+         c->M <= 1024;
 }
 int split_G(const pr_ctx *c) {
   const bool small = (long)c->B * c->M <= kGroupMaxPoints;
@@ -681,6 +685,123 @@ pr_status coarse_chain(pr_ctx *c, int k, int ln0, bool copy) {
   return PR_OK;
 }
 
+// ---------------------------------------------------------------- rank transport
+// NCCL between processes (one per GPU), or — for tests on a single GPU — an in-process loopback:
+// contexts whose 128-byte id starts with "PRLOOPBK" and shares the rest form a group whose ranks
+// (each driven by its own host thread) hand the same rows through device mailboxes, fully
+// synchronously.  The schedule, kernels and buffers are those of the NCCL path; only the three
+// transport calls below differ.
+struct LoopGroup {
+  int world = 0, refs = 0;
+  std::mutex mu;
+  std::condition_variable cv;
+  std::vector<void *> box;  // [src·world + dst] device mailbox
+  std::vector<size_t> box_bytes;
+  std::vector<int> full;
+  std::vector<unsigned long long> vals;  // all-reduce contributions (bit patterns of doubles ≥ 0)
+  unsigned long long result = 0;
+  int arrived = 0, gen = 0;
+};
+std::mutex g_loop_mu;
+std::map<std::string, LoopGroup *> g_loops;
+const char kLoopMagic[8] = {'P', 'R', 'L', 'O', 'O', 'P', 'B', 'K'};
+
+bool loop_id(const uint8_t *id) { return id && std::memcmp(id, kLoopMagic, 8) == 0; }
+LoopGroup *loop_join(const uint8_t *id, int world) {
+  std::lock_guard<std::mutex> lk(g_loop_mu);
+  const std::string key((const char *)id + 8, 120);
+  LoopGroup *&g = g_loops[key];
+  if (!g) {
+    g = new LoopGroup;
+    g->world = world;
+    g->box.assign((size_t)world * world, nullptr);
+    g->box_bytes.assign((size_t)world * world, 0);
+    g->full.assign((size_t)world * world, 0);
+    g->vals.assign(world, 0);
+  }
+  if (g->world != world) return nullptr;
+  g->refs++;
+  return g;
+}
+void loop_leave(LoopGroup *g) {
+  std::lock_guard<std::mutex> lk(g_loop_mu);
+  if (--g->refs > 0) return;
+  for (void *b : g->box) cudaFree(b);
+  for (auto it = g_loops.begin(); it != g_loops.end(); ++it)
+    if (it->second == g) {
+      g_loops.erase(it);
+      break;
+    }
+  delete g;
+}
+
+pr_status comm_send(pr_ctx *c, const float *buf, size_t count, int peer) {
+  if (!c->loop) {
+    NC(nccl().Send(buf, count, kNcclFloat32, peer, c->comm, c->stream));
+    return PR_OK;
+  }
+  LoopGroup *g = c->loop;
+  const size_t bytes = count * sizeof(float), idx = (size_t)c->rank * g->world + peer;
+  CU(cudaStreamSynchronize(c->stream));  // the row is complete
+  std::unique_lock<std::mutex> lk(g->mu);
+  g->cv.wait(lk, [&] { return !g->full[idx]; });
+  if (g->box_bytes[idx] < bytes) {
+    cudaFree(g->box[idx]);
+    g->box[idx] = nullptr;
+    CU(cudaMalloc(&g->box[idx], bytes));
+    g->box_bytes[idx] = bytes;
+  }
+  CU(cudaMemcpy(g->box[idx], buf, bytes, cudaMemcpyDeviceToDevice));
+  g->full[idx] = 1;
+  g->cv.notify_all();
+  return PR_OK;
+}
+pr_status comm_recv(pr_ctx *c, float *buf, size_t count, int peer) {
+  if (!c->loop) {
+    NC(nccl().Recv(buf, count, kNcclFloat32, peer, c->comm, c->stream));
+    return PR_OK;
+  }
+  LoopGroup *g = c->loop;
+  const size_t bytes = count * sizeof(float), idx = (size_t)peer * g->world + c->rank;
+  CU(cudaStreamSynchronize(c->stream));  // earlier work reading buf is done
+  std::unique_lock<std::mutex> lk(g->mu);
+  g->cv.wait(lk, [&] { return g->full[idx] != 0; });
+  CU(cudaMemcpy(buf, g->box[idx], bytes, cudaMemcpyDeviceToDevice));
+  g->full[idx] = 0;
+  g->cv.notify_all();
+  return PR_OK;
+}
+// MAX over ranks of one non-negative double held as its bit pattern (δ, reading Q13)
+pr_status comm_allreduce_max(pr_ctx *c, unsigned long long *slot) {
+  if (!c->loop) {
+    NC(nccl().AllReduce(slot, slot, 1, kNcclFloat64, kNcclMax, c->comm, c->stream));
+    return PR_OK;
+  }
+  LoopGroup *g = c->loop;
+  unsigned long long v = 0;
+  CU(cudaStreamSynchronize(c->stream));
+  CU(cudaMemcpy(&v, slot, sizeof v, cudaMemcpyDeviceToHost));
+  unsigned long long res;
+  {
+    std::unique_lock<std::mutex> lk(g->mu);
+    const int my_gen = g->gen;
+    g->vals[c->rank] = v;
+    if (++g->arrived == g->world) {
+      unsigned long long m = 0;
+      for (unsigned long long x : g->vals) m = x > m ? x : m;
+      g->result = m;
+      g->arrived = 0;
+      g->gen++;
+      g->cv.notify_all();
+    } else {
+      g->cv.wait(lk, [&] { return g->gen != my_gen; });
+    }
+    res = g->result;  // (the next generation needs this rank's arrival first)
+  }
+  CU(cudaMemcpy(slot, &res, sizeof res, cudaMemcpyHostToDevice));
+  return PR_OK;
+}
+
 pr_status delta_reduce(pr_ctx *c, int k, int ln_lo, int ln_hi, int nch) {
   unsigned long long *slot = c->d_delta + (k - 1);
   CU(cudaMemsetAsync(slot, 0, sizeof(unsigned long long), c->stream));
@@ -690,9 +811,7 @@ pr_status delta_reduce(pr_ctx *c, int k, int ln_lo, int ln_hi, int nch) {
     pr::launch_delta(c->partials, c->B, nch, ln_lo, ln_hi, slot, c->stream);
     LAUNCHED();
   }
-  if (c->world > 1) {
-    NC(nccl().AllReduce(slot, slot, 1, kNcclFloat64, kNcclMax, c->comm, c->stream));
-  }
+  if (c->world > 1) return comm_allreduce_max(c, slot);
   return PR_OK;
 }
 
@@ -1006,7 +1125,7 @@ pr_status solve_impl(pr_ctx *c, const float *V_T, float *V_0, bool device_ptr, p
     const pr_plan P0 = make_plan(c->N, R, r, 0);
     if (P0.recv_first) {
       pt.begin(PH_COMM);
-      NC(nccl().Recv(c->U, row, kNcclFloat32, r - 1, c->comm, c->stream));
+      if ((st = comm_recv(c, c->U, row, r - 1))) return st;
       pt.end();
     }
     pt.begin(PH_COARSE);
@@ -1014,7 +1133,7 @@ pr_status solve_impl(pr_ctx *c, const float *V_T, float *V_0, bool device_ptr, p
     pt.end();
     if (P0.send_last) {
       pt.begin(PH_COMM);
-      NC(nccl().Send(c->U + (size_t)c->Nloc * row, row, kNcclFloat32, r + 1, c->comm, c->stream));
+      if ((st = comm_send(c, c->U + (size_t)c->Nloc * row, row, r + 1))) return st;
       pt.end();
     }
   }
@@ -1027,7 +1146,7 @@ pr_status solve_impl(pr_ctx *c, const float *V_T, float *V_0, bool device_ptr, p
     // (ii) coarse chain with correction, serial in n across ranks
     if (P.recv_first) {
       pt.begin(PH_COMM);
-      NC(nccl().Recv(c->U, row, kNcclFloat32, r - 1, c->comm, c->stream));
+      if ((st = comm_recv(c, c->U, row, r - 1))) return st;
       pt.end();
     }
     if (P.copy || P.recv_first) {
@@ -1037,7 +1156,7 @@ pr_status solve_impl(pr_ctx *c, const float *V_T, float *V_0, bool device_ptr, p
     }
     if (P.send_last) {
       pt.begin(PH_COMM);
-      NC(nccl().Send(c->U + (size_t)c->Nloc * row, row, kNcclFloat32, r + 1, c->comm, c->stream));
+      if ((st = comm_send(c, c->U + (size_t)c->Nloc * row, row, r + 1))) return st;
       pt.end();
     }
     const int dlo = P.delta_lo, dhi = P.delta_hi;
@@ -1058,8 +1177,8 @@ pr_status solve_impl(pr_ctx *c, const float *V_T, float *V_0, bool device_ptr, p
   // final state U^K_N: last rank → rank 0 (→ V_0)
   if (R > 1) {
     pt.begin(PH_COMM);
-    if (r == R - 1) NC(nccl().Send(c->U + (size_t)c->Nloc * row, row, kNcclFloat32, 0, c->comm, c->stream));
-    if (r == 0) NC(nccl().Recv(c->tmp, row, kNcclFloat32, R - 1, c->comm, c->stream));
+    if (r == R - 1 && (st = comm_send(c, c->U + (size_t)c->Nloc * row, row, 0))) return st;
+    if (r == 0 && (st = comm_recv(c, c->tmp, row, R - 1))) return st;
     pt.end();
   }
   if (r == 0 && V_0) {
@@ -1299,7 +1418,13 @@ pr_status parareal_init(const pr_problem *p, const pr_dist *dist, pr_ctx **out) 
   // point per thread, 256-wide copy blocks, streamed tiles, one resident system)
   c->nch = std::max(1, (c->M + kPinnTPB - 1) / kPinnTPB);
   if (split_allowed(c)) c->nch = std::max(1, (c->M + pr::kPinnSplitMinPPC - 1) / pr::kPinnSplitMinPPC);
-  if (dd.world > 1) {
+  if (dd.world > 1 && loop_id(dd.nccl_id)) {  // test transport (one process, one GPU)
+    c->loop = loop_join(dd.nccl_id, dd.world);
+    if (!c->loop) {
+      c->err = "loopback group joined with a different world size";
+      return bail(PR_ERR_INVALID_ARGUMENT);
+    }
+  } else if (dd.world > 1) {
     Nccl &n = nccl();
     if (!n.ok) {
       c->err = n.why;
@@ -1628,6 +1753,7 @@ void parareal_free(pr_ctx *c) {
   if (!c) return;
   if (c->stream) cudaStreamSynchronize(c->stream);
   drop_graph(c);
+  if (c->loop) loop_leave(c->loop);
   if (c->comm) {
     Nccl &n = nccl();
     if (n.ok) (c->poisoned ? n.CommAbort(c->comm) : n.CommDestroy(c->comm));

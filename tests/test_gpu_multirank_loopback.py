@@ -1,0 +1,76 @@
+"""The multi-rank schedule on one GPU: R contexts in one process, one host
+thread each, exchanging through the library's in-process loopback transport (a 128-byte id
+starting "PRLOOPBK") instead of NCCL.  Everything else is the multi-GPU path — per-rank plan,
+kernels, the U_{n0} receive / U_{n1} send around each coarse chain, the MAX all-reduce of δ that
+decides the stop, the gather of U_N to rank 0 — so this executes it on real kernels.  The results
+must be bitwise the one-rank solve's: every slice's arithmetic is independent of R and MAX is
+order-free."""
+import threading
+
+import numpy as np
+import pytest
+
+from paper_2303_03848_b200 import parareal, synth
+
+pytestmark = pytest.mark.gpu
+
+
+def solve_ranks(p, net, world, key):
+    nid = b"PRLOOPBK" + key.ljust(120, b"\0")
+    ctxs = [parareal.Context(p, rank=r, world=world, device=0, nccl_id=nid) for r in range(world)]
+    try:
+        for c in ctxs:
+            if net is not None:
+                c.load_weights(net)
+        outs, reps, its, errs = [None] * world, [None] * world, [None] * world, []
+
+        def work(r):
+            try:
+                outs[r], reps[r] = ctxs[r].solve()
+                n0 = r * (p.N // world)
+                its[r] = ctxs[r].copy_iterates(n0, p.N // world + 1)
+            except Exception as e:  # pragma: no cover - reported below
+                errs.append((r, e))
+
+        th = [threading.Thread(target=work, args=(r,)) for r in range(world)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join(timeout=120)
+        assert not any(t.is_alive() for t in th), "loopback ranks deadlocked"
+        assert not errs, errs
+        return outs[0], reps, its
+    finally:
+        for c in ctxs:
+            c.close()
+
+
+@pytest.mark.parametrize("name,world", [("pinn", 2), ("pinn", 4), ("ie", 2), ("ie_tol", 2), ("ie_tol", 4),
+                                        ("streamed", 2), ("portfolio", 2)])
+def test_multirank_matches_one_rank(name, world):
+    net = None
+    if name == "pinn":
+        p = synth.single(1024, 32, coarse=synth.COARSE_PINN, max_iter=3, tol=0.0)
+        net = synth.kaiming_net(synth.PINN_3x20, seed=1)
+    elif name == "ie":
+        p = synth.single(700, 8, coarse=synth.COARSE_IMPLICIT_EULER, max_iter=3, tol=0.0)
+    elif name == "ie_tol":  # C1 with numerical G: K = 3 at tol = 3e-5, decided by the all-reduced δ
+        p = synth.config("C1", coarse=synth.COARSE_IMPLICIT_EULER, max_iter=4, tol=3e-5)
+    elif name == "streamed":  # K2 fine sweeps and the streamed numerical chain
+        p = synth.single(5000, 4, coarse=synth.COARSE_IMPLICIT_EULER, max_iter=2, tol=0.0, fine_steps=20)
+    else:
+        p = synth.portfolio(n_k=2, n_s=2, M=256, N=8, coarse=synth.COARSE_PINN, max_iter=3, tol=0.0)
+        net = synth.kaiming_net(synth.PINN_3x20, seed=2)
+    with parareal.Context(p) as c:
+        if net is not None:
+            c.load_weights(net)
+        c.set_option(parareal.OPT_PIPELINE, 1)  # the blocking schedule (multi-rank runs blocking)
+        ref, rref = c.solve()
+        it_ref = c.copy_iterates(0, p.N + 1)
+    out, reps, its = solve_ranks(p, net, world, ("%s-%d" % (name, world)).encode())
+    assert all(r["iterations"] == rref["iterations"] for r in reps)
+    assert np.array_equal(reps[0]["delta"], rref["delta"])
+    assert np.array_equal(out, ref)
+    per = p.N // world
+    for r in range(world):
+        assert np.array_equal(its[r], it_ref[r * per:(r + 1) * per + 1]), "rank %d iterates" % r
