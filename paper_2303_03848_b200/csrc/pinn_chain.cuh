@@ -316,13 +316,13 @@ __device__ __forceinline__ float mlp_split(const float *__restrict__ sw, int LH,
   float y = 0.f;
 #pragma unroll
   for (int k = 0; k < NPT; ++k) y = fmaf(lw[q * NPT + k], own[k], y);
-  // the group's partial sums added in lane order by every thread: all G threads hold the same
-  // value (a butterfly would leave each lane its own rounding, so a thread's next-slice feature
-  // U/L_b could differ from the stored U that another rank or schedule reads back)
-  float s = 0.f;
+  // butterfly sum, then every thread takes the group leader's value: a butterfly alone leaves
+  // each lane its own rounding, so a thread's next-slice feature U/L_b could differ from the
+  // stored U that another rank or schedule reads back
 #pragma unroll
-  for (int r = 0; r < G; ++r) s += __shfl_sync(0xffffffffu, y, gbase + r);
-  return s + lw[W];
+  for (int d = 1; d < G; d <<= 1) y += __shfl_xor_sync(0xffffffffu, y, d);
+  y = __shfl_sync(0xffffffffu, y, gbase);
+  return y + lw[W];
 }
 
 template <int IN, int W, int G, int ACT>
