@@ -1025,7 +1025,7 @@ __global__ void __launch_bounds__(H *kHT) k_pass_res2(PassArgs a) {
   if (t == 0)
     for (int i = 0; i < NST && lo + i < hi; ++i) issue(i);
   struct Pre {
-    double E[2][SP], P[2], LA, LB;
+    double E[2][SP], P[2], LA, LB, LA2, LB2;  // look-back operands: predecessors 1-32 and 33-64
     int W, set;
   };
   Pre pre[2];
@@ -1050,15 +1050,26 @@ __global__ void __launch_bounds__(H *kHT) k_pass_res2(PassArgs a) {
     r.P[1] = pp.y;
     r.LA = 0.0;
     r.LB = 1.0;
+    r.LA2 = 0.0;
+    r.LB2 = 1.0;
     r.W = 0;
     if (wl >= kNW2 - SP && c.pos > 0) {
       const int q = kNW2 - 1 - wl;
       const size_t tb = ((size_t)DIR * a.nsets + set) * a.ntiles;
       r.W = __ldg(a.f.tileW + tb + c.pos);
+      const double *aggl = a.aggL_cur + (size_t)c.sys(a, h * SP + q) * a.ntiles;
       const int p = c.pos - 1 - lane;
       if (p >= 0) {
-        r.LA = a.aggL_cur[(size_t)c.sys(a, h * SP + q) * a.ntiles + (DIR == 0 ? p : a.ntiles - 1 - p)];
+        r.LA = aggl[DIR == 0 ? p : a.ntiles - 1 - p];
         r.LB = __ldg(a.f.tileB + tb + p);
+      }
+      // the second window too: a third of the C3 tiles look back 33-48 tiles (multipliers
+      // within 5e-4 of 1 at the top of the grid), which otherwise costs a synchronous load
+      // round trip in front of the item's barrier
+      const int p2 = p - 32;
+      if (p2 >= 0) {
+        r.LA2 = aggl[DIR == 0 ? p2 : a.ntiles - 1 - p2];
+        r.LB2 = __ldg(a.f.tileB + tb + p2);
       }
     }
   };
@@ -1095,7 +1106,7 @@ __global__ void __launch_bounds__(H *kHT) k_pass_res2(PassArgs a) {
     const int stage = n % NST;
     const int pb = n & 1;
     const uint32_t parity = (uint32_t)(n / NST) & 1u;
-    double E[2][SP], P[2], LA, LB;
+    double E[2][SP], P[2], LA, LB, LA2, LB2;
     int W, set;
     if (n & 1) {
 #pragma unroll
@@ -1104,7 +1115,7 @@ __global__ void __launch_bounds__(H *kHT) k_pass_res2(PassArgs a) {
 #pragma unroll
         for (int q = 0; q < SP; ++q) E[c][q] = pre[1].E[c][q];
       }
-      LA = pre[1].LA; LB = pre[1].LB; W = pre[1].W; set = pre[1].set;
+      LA = pre[1].LA; LB = pre[1].LB; LA2 = pre[1].LA2; LB2 = pre[1].LB2; W = pre[1].W; set = pre[1].set;
       if (k + 2 < hi) prefetch(nxt, pre[1]);
     } else {
 #pragma unroll
@@ -1113,7 +1124,7 @@ __global__ void __launch_bounds__(H *kHT) k_pass_res2(PassArgs a) {
 #pragma unroll
         for (int q = 0; q < SP; ++q) E[c][q] = pre[0].E[c][q];
       }
-      LA = pre[0].LA; LB = pre[0].LB; W = pre[0].W; set = pre[0].set;
+      LA = pre[0].LA; LB = pre[0].LB; LA2 = pre[0].LA2; LB2 = pre[0].LB2; W = pre[0].W; set = pre[0].set;
       if (k + 2 < hi) prefetch(nxt, pre[0]);
     }
     if (k + 2 < hi) nxt.step(a);
@@ -1123,7 +1134,12 @@ __global__ void __launch_bounds__(H *kHT) k_pass_res2(PassArgs a) {
       double mA = lane < W ? LA : 0.0, mB = lane < W ? LB : 1.0;
       compose_window(mA, mB, lane);
       double y = mA;
-      if (W > 32) y = look_back<DIR>(a, cur.sys(a, h * SP + q), cur.pos, set, lane, 32, mA, mB);  // rare
+      if (W > 32) {  // (warp-uniform) predecessors 33-64 from the prefetched second window
+        double mA2 = lane + 32 < W ? LA2 : 0.0, mB2 = lane + 32 < W ? LB2 : 1.0;
+        compose_window(mA2, mB2, lane);
+        y = fma(mB, mA2, mA);
+        if (W > 64) y = look_back<DIR>(a, cur.sys(a, h * SP + q), cur.pos, set, lane, 64, y, mB * mB2);  // rare
+      }
       if (lane == 0) s_yin[pb][h][q] = y;
     }
     __syncthreads();  // the barrier of the item
