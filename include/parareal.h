@@ -93,7 +93,11 @@ typedef struct {
   double tol;                   /* stop at the first k with δ^k < tol; 0 → run max_iter     */
 } pr_problem;
 
-/* Process placement.  world == 1: single GPU, nccl_id must be NULL. */
+/* Process placement.  world == 1: single GPU, nccl_id must be NULL.
+ * Test transport: an id whose first 8 bytes are "PRLOOPBK" makes the world contexts created
+ * with the same id in ONE process (one host thread per rank, any device) exchange through
+ * device mailboxes instead of NCCL (send / receive / MAX all-reduce, fully synchronous); every
+ * other step is the multi-process path.  For tests on a single GPU only. */
 typedef struct {
   int32_t rank, world;          /* this process / all processes (one GPU each)               */
   int32_t device;               /* CUDA device ordinal                                       */
