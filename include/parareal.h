@@ -197,12 +197,13 @@ pr_status parareal_plan_iteration(int32_t N, int32_t world, int32_t rank, int32_
 /* Tuning/test options (values are validated; unknown keys → PR_ERR_INVALID_ARGUMENT). */
 enum {
   PR_OPT_FINE_KERNEL = 1,   /* 0 auto, 1 resident (M ≤ 4096), 2 streamed            */
-  PR_OPT_USE_GRAPHS = 2,    /* 0/1: a fixed-K (tol == 0), single-GPU, device-pointer solve is captured
+  PR_OPT_USE_GRAPHS = 2,    /* 0/1: a fixed-K (tol == 0), single-GPU solve with device pointers (or pinned
+                               host buffers, whose copies become graph nodes) is captured
                                into a CUDA graph on its first call per (V_T, V_0) pair and replayed on
                                later calls (same kernels, same results); any other solve runs eagerly.
                                set_option / load_pinn_weights / free discard the captured graph.
                                2: the same, but the graph is captured without the phase-timing events
-                               and a replay returns as soon as it is enqueued on the context stream
+                               and a device-pointer replay returns as soon as it is enqueued on the context stream
                                (stream-ordered, like a library call: the caller synchronises; rep, if
                                given, receives iterations and kernel_launches, zero times, no δ).  */
   PR_OPT_PINN_KERNEL = 3,   /* 0 auto, 1 shared-memory weights, 2 latency mode (4 threads/point; B·M ≤ 65536) */

@@ -1065,11 +1065,23 @@ pr_status solve_impl(pr_ctx *c, const float *V_T, float *V_0, bool device_ptr, p
   if ((st = ensure_ws(c))) return st;
   // CUDA-graph replay of a fixed-K single-GPU device-pointer solve (PR_OPT_USE_GRAPHS): the whole
   // solve (≈ 4K+4 kernels) is captured once per (V_T, V_0) pair and relaunched as one graph.
-  const bool use_graph = c->opt_graphs && c->tol == 0.0 && c->world == 1 && device_ptr;
+  // (host buffers qualify when they are pinned: the graph's copy nodes then stay valid; a replay
+  // with host buffers always returns with V_0 written)
+  auto pinned = [](const void *h) {
+    if (!h) return true;
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, h) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+  };
+  const bool use_graph = c->opt_graphs && c->tol == 0.0 && c->world == 1 &&
+                         (device_ptr || (pinned(V_T) && pinned(V_0)));
   if (use_graph && c->g_exec && c->g_vt == V_T && c->g_v0 == V_0) {
     CU(cudaGraphLaunch(c->g_exec, c->stream));
     c->launches += c->g_launches;
-    if (c->opt_graphs == 2) {  // stream-ordered replay: return once enqueued (no δ, no times)
+    if (c->opt_graphs == 2 && device_ptr) {  // stream-ordered replay: return once enqueued (no δ, no times)
       c->solved = true;
       if (rep) {
         rep->iterations = c->g_K;

@@ -548,3 +548,27 @@ def test_pipelined_numerical_G_matches_blocking(M, N, B, theta, nc):
     assert np.array_equal(ra["delta"], rb["delta"])
     U_ref = oracle.parareal(p)[0]
     assert_close(a, U_ref[-1], what="pipelined numerical-G Parareal M=%d" % M)
+
+
+def test_graph_replay_with_pinned_host_buffers():
+    """PR_OPT_USE_GRAPHS with host buffers: pinned ones are captured as graph copy nodes (the
+    bench's e2e path), pageable ones run eagerly; every result is the eager solve's, bitwise."""
+    import torch
+    p = synth.config("C2", coarse=synth.COARSE_PINN, max_iter=3, tol=0.0)
+    net = synth.kaiming_net(synth.PINN_3x20, seed=5)
+    with ctx_for(p, net) as c:
+        eager, _ = c.solve()
+        vt = torch.from_numpy(c.initial_state()).pin_memory()
+        v0 = torch.zeros((p.B, p.M), dtype=torch.float32).pin_memory()
+        for mode in (1, 2):
+            c.set_option(parareal.OPT_USE_GRAPHS, mode)
+            launches = []
+            for _ in range(3):
+                v0.zero_()
+                r = c.solve_host_ptrs(vt.data_ptr(), v0.data_ptr())   # returns with V_0 written
+                launches.append(r["kernel_launches"])
+                assert np.array_equal(v0.numpy(), eager)
+            assert r["iterations"] == 3 and launches[0] == launches[-1] > 0
+        c.set_option(parareal.OPT_USE_GRAPHS, 1)
+        again, _ = c.solve()   # pageable buffers: eager
+        assert np.array_equal(again, eager)
