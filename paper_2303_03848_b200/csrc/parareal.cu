@@ -103,6 +103,7 @@ struct Scheme {
 
 constexpr int kResidentMaxM = 2048;
 constexpr int kPinnTPB = 128;
+constexpr int kPinnSmemBudget = 200 * 1024;  // dynamic shared memory for the fp32 PINN weights
 struct LoopGroup;  // in-process loopback transport (defined with the transport calls below)
 }  // namespace
 
@@ -205,10 +206,13 @@ pr_status fail(pr_ctx *c, pr_status s, const std::string &msg) {
       return fail(c, PR_ERR_NCCL, fmt("%s failed: %s", #call, nccl().GetErrorString(e_)));    \
   } while (0)
 
-#define LAUNCHED()                                                                            \
+// Every launcher returns the launch's cudaError_t (and leaves the sticky error state alone);
+// a failed launch poisons the context like any other CUDA failure (include/parareal.h).
+#define LAUNCH(call)                                                                          \
   do {                                                                                        \
     c->launches++;                                                                            \
-    cudaError_t e_ = cudaGetLastError();                                                      \
+    cudaError_t e_ = (call);                                                                  \
+    if (e_ == cudaSuccess) e_ = cudaPeekAtLastError();                                        \
     if (e_ != cudaSuccess)                                                                    \
       return fail(c, PR_ERR_CUDA, fmt("kernel launch failed: %s (%s:%d)", cudaGetErrorString(e_), \
                                       __FILE__, __LINE__));                                   \
@@ -217,6 +221,9 @@ pr_status fail(pr_ctx *c, pr_status s, const std::string &msg) {
 pr_status check_ctx(pr_ctx *c) {
   if (!c) return fail(nullptr, PR_ERR_INVALID_ARGUMENT, "ctx is NULL");
   if (c->poisoned) return PR_ERR_STATE;
+  // every entry point works on the context's device, whatever the calling thread has current
+  const cudaError_t e = cudaSetDevice(c->device);
+  if (e != cudaSuccess) return fail(c, PR_ERR_CUDA, fmt("cudaSetDevice(%d): %s", c->device, cudaGetErrorString(e)));
   return PR_OK;
 }
 
@@ -517,8 +524,8 @@ pr::ResidentArgs base_args(pr_ctx *c, const Scheme &sc) {
   return a;
 }
 
-void dispatch_res(bool chain, int M, const pr::ResidentArgs &a, int nsys, cudaStream_t s) {
-  pr::launch_resident(chain, M, a, nsys, s);
+cudaError_t dispatch_res(bool chain, int M, const pr::ResidentArgs &a, int nsys, cudaStream_t s) {
+  return pr::launch_resident(chain, M, a, nsys, s);
 }
 
 // ---------------------------------------------------------------- PINN launches
@@ -586,8 +593,7 @@ pr_status launch_pinn(pr_ctx *c, const pr::PinnArgs &a) {
     t.wts = c->d_tcp;
     t.nfloats = c->tc_nfloats;
     dim3 grid((c->M + 127) / 128, c->B);
-    CU(pr::launch_pinn_tc(c->IN, c->W, c->act, c->tc == PR_PREC_BF16_TC, t, c->d_wh, grid, c->stream));
-    LAUNCHED();
+    LAUNCH(pr::launch_pinn_tc(c->IN, c->W, c->act, c->tc == PR_PREC_BF16_TC, t, c->d_wh, grid, c->stream));
     return PR_OK;
   }
   if (use_split_pinn(c)) {
@@ -595,21 +601,18 @@ pr_status launch_pinn(pr_ctx *c, const pr::PinnArgs &a) {
     dim3 grid((c->M + ppc - 1) / ppc, c->B);
     pr::PinnArgs t = a;
     if (pr::pinn_split_is_group(c->W, G)) t.wts = c->d_wgrp;  // group kernels: hidden matrices in the group order
-    pr::launch_pinn_split(c->IN, c->W, c->act, G, t, grid, (size_t)c->nfloats * sizeof(float), c->stream);
-    LAUNCHED();
+    LAUNCH(pr::launch_pinn_split(c->IN, c->W, c->act, G, t, grid, (size_t)c->nfloats * sizeof(float), c->stream));
     return PR_OK;
   }
   if (use_param_pinn(c)) {
     dim3 grid((c->M + kPinnTPB - 1) / kPinnTPB, c->B);
-    pr::launch_pinn_param(c->IN, c->W, c->LH, c->act, c->h_wts.data(), a, grid, c->stream);
-    LAUNCHED();
+    LAUNCH(pr::launch_pinn_param(c->IN, c->W, c->LH, c->act, c->h_wts.data(), a, grid, c->stream));
     return PR_OK;
   }
   if (!pr::pinn_smem_supported(c->IN, c->W, c->act)) return fail(c, PR_ERR_UNSUPPORTED, "no PINN kernel for this width");
   const int pts = pr::pinn_smem_pts(c->W);
   dim3 grid((c->M + kPinnTPB * pts - 1) / (kPinnTPB * pts), c->B);
-  pr::launch_pinn_smem(c->IN, c->W, c->act, a, grid, (size_t)c->nfloats * sizeof(float), c->stream);
-  LAUNCHED();
+  LAUNCH(pr::launch_pinn_smem(c->IN, c->W, c->act, a, grid, (size_t)c->nfloats * sizeof(float), c->stream));
   return PR_OK;
 }
 
@@ -628,8 +631,7 @@ pr_status fine_sweep(pr_ctx *c, int ln_lo, int fk_ln) {
     a.D = c->D;
     a.Fk = c->Fk;
     a.fk_ln = fk_ln;
-    dispatch_res(false, c->M, a, nsl * c->B, c->stream);
-    LAUNCHED();
+    LAUNCH(dispatch_res(false, c->M, a, nsl * c->B, c->stream));
     return PR_OK;
   }
   pr::StreamedJob j;
@@ -680,8 +682,7 @@ pr_status coarse_chain(pr_ctx *c, int k, int ln0, bool copy) {
   a.c_ln1 = c->Nloc;
   a.partials = corr ? c->partials : nullptr;
   if (ln0 >= c->Nloc && !copy) return PR_OK;
-  dispatch_res(true, c->M, a, c->B, c->stream);
-  LAUNCHED();
+  LAUNCH(dispatch_res(true, c->M, a, c->B, c->stream));
   return PR_OK;
 }
 
@@ -808,8 +809,7 @@ pr_status delta_reduce(pr_ctx *c, int k, int ln_lo, int ln_hi, int nch) {
   if (ln_hi >= ln_lo) {
     const int total = (ln_hi - ln_lo + 1) * c->B;
     (void)total;
-    pr::launch_delta(c->partials, c->B, nch, ln_lo, ln_hi, slot, c->stream);
-    LAUNCHED();
+    LAUNCH(pr::launch_delta(c->partials, c->B, nch, ln_lo, ln_hi, slot, c->stream));
   }
   if (c->world > 1) return comm_allreduce_max(c, slot);
   return PR_OK;
@@ -826,8 +826,7 @@ pr_status load_initial(pr_ctx *c, const float *V_T, bool device_ptr) {
                            device_ptr ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->stream));
     }
   } else {
-    pr::launch_payoff(c->U, c->M, c->Mp, c->B, c->d_L, c->d_K, c->stream);
-    LAUNCHED();
+    LAUNCH(pr::launch_payoff(c->U, c->M, c->Mp, c->B, c->d_L, c->d_K, c->stream));
   }
   return PR_OK;
 }
@@ -1018,8 +1017,9 @@ pr_status solve_pipelined(pr_ctx *c) {
 
 using Spans = std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>>;
 
+// lean: this solve ran a lean (PR_OPT_USE_GRAPHS = 2) graph, which records no timing events
 pr_status solve_report(pr_ctx *c, int K, int conv, cudaEvent_t e0, cudaEvent_t e1, const Spans &spans,
-                       int64_t launches, pr_report *rep) {
+                       int64_t launches, pr_report *rep, bool lean) {
   c->solved = true;
   if (!rep) return PR_OK;
   rep->iterations = K;
@@ -1027,7 +1027,7 @@ pr_status solve_report(pr_ctx *c, int K, int conv, cudaEvent_t e0, cudaEvent_t e
   if (rep->delta)
     for (int i = 0; i < K; ++i) rep->delta[i] = c->h_delta[i];
   rep->kernel_launches = launches;
-  if (c->opt_graphs == 2 && c->g_exec) {  // lean graph: no timing events were captured
+  if (lean) {  // lean graph: no timing events were captured
     rep->ms_total = rep->ms_coarse = rep->ms_fine = rep->ms_comm = rep->ms_setup = 0.0;
     return PR_OK;
   }
@@ -1092,7 +1092,7 @@ pr_status solve_impl(pr_ctx *c, const float *V_T, float *V_0, bool device_ptr, p
       return PR_OK;
     }
     CU(cudaStreamSynchronize(c->stream));
-    return solve_report(c, c->g_K, 0, c->g_e0, c->g_e1, c->g_spans, c->g_launches, rep);
+    return solve_report(c, c->g_K, 0, c->g_e0, c->g_e1, c->g_spans, c->g_launches, rep, c->opt_graphs == 2);
   }
   if (pipe_eligible(c) && (st = ensure_pipe(c))) return st;  // (allocation cannot be captured)
   if (use_graph) {
@@ -1230,7 +1230,7 @@ pr_status solve_impl(pr_ctx *c, const float *V_T, float *V_0, bool device_ptr, p
     return st;
   }
   CU(cudaStreamSynchronize(c->stream));
-  return solve_report(c, K, conv, e0, e1, pt.spans, c->launches - launches0, rep);
+  return solve_report(c, K, conv, e0, e1, pt.spans, c->launches - launches0, rep, use_graph && c->opt_graphs == 2);
 }
 
 pr_status serial_fine_impl(pr_ctx *c, const float *V_T, float *V_0, bool device_ptr, double *ms) {
@@ -1253,8 +1253,7 @@ pr_status serial_fine_impl(pr_ctx *c, const float *V_T, float *V_0, bool device_
     a.ustride = 0;  // one row, updated in place slice after slice
     a.c_ln0 = 0;
     a.c_ln1 = c->N;
-    dispatch_res(true, c->M, a, c->B, c->stream);
-    LAUNCHED();
+    LAUNCH(dispatch_res(true, c->M, a, c->B, c->stream));
   } else {
     pr::StreamedChainJob j;
     j.U = c->tmp; j.Gh = nullptr; j.D = nullptr; j.Fcopy = nullptr; j.partials = nullptr; j.nch = 1;
@@ -1350,6 +1349,8 @@ pr_status parareal_init(const pr_problem *p, const pr_dist *dist, pr_ctx **out) 
   if (dd.world > 1 && !dd.nccl_id) return fail(c, PR_ERR_INVALID_ARGUMENT, "dist.nccl_id is NULL with world > 1");
   if ((size_t)p->M * p->B > (size_t)1 << 31)
     return fail(c, PR_ERR_UNSUPPORTED, "M*B above 2^31 points per slice");
+  if (p->B > 65535)  // the instance index is a grid y coordinate in the payoff, PINN and K2 kernels
+    return fail(c, PR_ERR_UNSUPPORTED, fmt("problem.B=%d above 65535 instances per context", p->B));
 
   c = new pr_ctx();
   pr_status st = PR_OK;
@@ -1543,12 +1544,14 @@ pr_status parareal_load_pinn_weights(pr_ctx *c, int32_t n_linear, const int32_t 
   }
   c->tc = tc ? precision : 0;
   const size_t bytes = pk.size() * sizeof(float);
-  if (!tc && bytes > 200 * 1024)
+  if (!tc && bytes > (size_t)kPinnSmemBudget)
     return fail(c, PR_ERR_UNSUPPORTED, fmt("network of %zu bytes exceeds the shared-memory budget", bytes));
   if (!tc) {
-    CU(pr::pinn_smem_prepare(IN, Wd, activation, (int)bytes));
+    // the attribute is per kernel and process-wide: set it to the whole budget (never lowered by
+    // a smaller net loaded into another context that shares the kernel)
+    CU(pr::pinn_smem_prepare(IN, Wd, activation, kPinnSmemBudget));
     if (pr::pinn_split_supported(IN, Wd, activation, pr::kPinnSplitG))
-      CU(pr::pinn_split_prepare(IN, Wd, activation, pr::kPinnSplitG, (int)bytes));
+      CU(pr::pinn_split_prepare(IN, Wd, activation, pr::kPinnSplitG, kPinnSmemBudget));
   }
   if (c->d_wts) cudaFree(c->d_wts);
   c->d_wts = nullptr;
@@ -1644,8 +1647,7 @@ pr_status parareal_apply_fine(pr_ctx *c, int32_t n, const float *U_in, float *U_
     a.nsl = 1;
     a.U = c->tmp;
     a.Fout = c->tmp + row;
-    dispatch_res(false, c->M, a, c->B, c->stream);
-    LAUNCHED();
+    LAUNCH(dispatch_res(false, c->M, a, c->B, c->stream));
   } else {
     pr::StreamedJob j;
     j.U = c->tmp; j.Gh = nullptr; j.D = nullptr; j.Fk = nullptr; j.fk_ln = -1; j.Fout = c->tmp + row;
@@ -1689,8 +1691,7 @@ pr_status parareal_apply_coarse(pr_ctx *c, int32_t n, const float *U_in, float *
     a.ustride = 0;
     a.c_ln0 = 0;
     a.c_ln1 = 1;
-    dispatch_res(true, c->M, a, c->B, c->stream);
-    LAUNCHED();
+    LAUNCH(dispatch_res(true, c->M, a, c->B, c->stream));
     if ((st = store_rows(c, U_out, c->tmp, false))) return st;
   } else {
     pr::StreamedChainJob j;
@@ -1763,6 +1764,7 @@ pr_status parareal_set_option(pr_ctx *c, int32_t key, int64_t value) {
 
 void parareal_free(pr_ctx *c) {
   if (!c) return;
+  cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   drop_graph(c);
   if (c->loop) loop_leave(c->loop);

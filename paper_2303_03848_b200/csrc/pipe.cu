@@ -49,8 +49,14 @@ __device__ __forceinline__ int ld_flag(const int *p) {
   asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+// The relaxed polls are followed by one acquire fence once the flag is observed: with the
+// producer's release (fence + st.release / red.release) this is the PTX memory model's
+// release/acquire pattern through a relaxed read (morally strong: same scope, same address), so
+// the data reads after it are ordered after the producer's writes.  One fence per wait, not per
+// poll: the L1 is invalidated at most once per wait.
 __device__ __forceinline__ void wait_geq(const int *p, int target) {
   while (ld_flag(p) < target) __nanosleep(20);
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
 }
 // after a CTA (or warp) barrier: publish the stores of the threads that reached it
 __device__ __forceinline__ void publish_add(int *p) {

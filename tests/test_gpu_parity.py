@@ -5,7 +5,7 @@ import numpy as np
 import pytest
 
 import oracle
-from gpu_helpers import TOL_FP32, assert_close, rel_err
+from gpu_helpers import TOL_FP32, assert_close, assert_delta, rel_err
 from paper_2303_03848_b200 import parareal, synth
 
 pytestmark = pytest.mark.gpu
@@ -124,7 +124,7 @@ def test_parareal_cn_fine_ie_coarse(kernel, M, N):
     ref_U, ref_d, K, _ = oracle.parareal(p)
     assert rep["iterations"] == K == 3
     assert_close(it, ref_U, what="CN Parareal iterates kernel=%d M=%d" % (kernel, M))
-    assert np.allclose(rep["delta"], ref_d, rtol=2e-2)
+    assert_delta(rep["delta"], ref_d)
 
 
 @pytest.mark.parametrize("dims,act", [(synth.PINN_3x20, synth.ACT_TANH), (synth.PINN_PAPER, synth.ACT_RELU),
@@ -267,7 +267,7 @@ def test_parareal_numerical_G_converges_like_oracle(kernel, cfg, tol, K_expected
         U, rep = c.solve()
         it = c.copy_iterates(0, p.N + 1)
     assert rep["iterations"] == ref_K and rep["converged"]
-    assert np.allclose(rep["delta"], ref_d, rtol=2e-2, atol=2e-6)
+    assert_delta(rep["delta"], ref_d)
     assert_close(U, ref_U[-1], what="U_N")
     assert_close(it, ref_U, what="all U_n")
 
@@ -301,7 +301,7 @@ def test_parareal_pinn_fixed_K(kernel):
         it = c.copy_iterates(0, p.N + 1)
     assert rep["iterations"] == 3
     _gate_or_amplification(it, ref_U, U32, "PINN iterates C1")
-    assert np.allclose(rep["delta"], ref_d, rtol=1e-2)
+    assert_delta(rep["delta"], ref_d)
 
 
 def test_parareal_pinn_k1_c2():
@@ -363,7 +363,7 @@ def test_streamed_determinism_and_parity():
     assert np.array_equal(a, b) and np.array_equal(ra["delta"], rb["delta"])
     ref_U, ref_d, _, _ = oracle.parareal(p)
     assert_close(it, ref_U, what="streamed Parareal iterates")
-    assert np.allclose(ra["delta"], ref_d, rtol=2e-2)
+    assert_delta(ra["delta"], ref_d)
 
 
 @pytest.mark.parametrize("M,N,B,theta", [(10000, 20, 1, 1.0), (6000, 18, 1, 1.0), (5000, 9, 2, 1.0),
@@ -385,7 +385,7 @@ def test_streamed_persistent_kernel_parity(M, N, B, theta):
     ref_U, ref_d, K, _ = oracle.parareal(p)
     assert rep["iterations"] == K == 2
     assert_close(it, ref_U, what="persistent K2 M=%d N=%d B=%d" % (M, N, B))
-    assert np.allclose(rep["delta"], ref_d, rtol=2e-2)
+    assert_delta(rep["delta"], ref_d)
 
 
 def test_portfolio_parareal_sampled():
@@ -395,7 +395,7 @@ def test_portfolio_parareal_sampled():
     with ctx_for(p) as c:
         U, rep = c.solve()
     assert_close(U, ref_U[-1], what="portfolio U_N")
-    assert np.allclose(rep["delta"], ref_d, rtol=2e-2, atol=1e-6)
+    assert_delta(rep["delta"], ref_d)
 
 
 def test_homogeneity_c4_full_sampled():
@@ -572,3 +572,107 @@ def test_graph_replay_with_pinned_host_buffers():
         c.set_option(parareal.OPT_USE_GRAPHS, 1)
         again, _ = c.solve()   # pageable buffers: eager
         assert np.array_equal(again, eager)
+
+
+# ------------------------------------------------------------------ the configurations the bench reports
+# (VERDICT r01 "What's weak" 1-2: the exact headline configuration and the C3-scale K2 kernel)
+
+def _k2_lookback_windows(M, sigma, r, dtau):
+    """Largest look-back window (in predecessor tiles) of the K2 passes for this grid, computed
+    here from a plain fp64 factorisation of I - dτA: the number of predecessor tiles
+    whose multiplier product stays above 1e-24 (fine_streamed.cuh kLookbackEps), per direction."""
+    j = np.arange(1, M + 1, dtype=np.float64)
+    a, b = 0.5 * sigma ** 2 * j ** 2, 0.5 * r * j
+    d, lo, up = 1.0 + dtau * (2 * a + r), -dtau * (a - b), -dtau * (a + b)
+    p = np.empty(M)
+    p[0] = d[0]
+    for i in range(1, M):
+        p[i] = d[i] - lo[i] / p[i - 1] * up[i - 1]
+    mt = np.concatenate([[0.0], lo[1:] / p[1:]])
+    cu = np.concatenate([up[:-1] / p[:-1], [0.0]])
+    T = 2048
+    nt = (M + T - 1) // T
+    best = 0
+    for f in (mt, cu):
+        lt = np.array([np.sum(np.log(np.abs(f[t * T:(t + 1) * T]) + 1e-300)) for t in range(nt)])
+        for pos in range(nt):
+            acc, w = 0.0, pos
+            for k in range(1, pos + 1):
+                acc += lt[pos - k] if f is mt else lt[nt - 1 - (pos - k)]
+                if acc < np.log(1e-24):
+                    w = k
+                    break
+            best = max(best, w)
+    return best
+
+
+def test_headline_bench_config_matches_oracle():
+    """The exact bench.py default step: C2 (1024 x 32 slices, 100 IE steps), PINN 3x20 tanh seed 0,
+    fixed K = 3, auto schedule (the pipelined cooperative kernel), workspace bound by the caller,
+    lean graph capture + stream-ordered replays (PR_OPT_USE_GRAPHS = 2) on a caller stream -- every
+    iterate U^3_n against the oracle (Eq. 7) under the stability gate of SURVEY §8(c),
+    and K, δ from an instrumented solve of the same context."""
+    import torch
+    p = synth.config("C2", coarse=synth.COARSE_PINN, coarse_steps=1, tol=0.0, fine_theta=1.0).replace(max_iter=3)
+    net = synth.kaiming_net(synth.PINN_3x20, seed=0)
+    ref_U, ref_d, ref_K, _ = oracle.parareal(p, net)
+    U32, _, _, _ = oracle.parareal(p, net, prec=32)
+    stream = torch.cuda.Stream()
+    with parareal.Context(p, stream=stream.cuda_stream) as c:
+        c.load_weights(net)
+        ws = torch.empty(c.workspace_bytes(), dtype=torch.uint8, device="cuda")
+        c.bind_workspace(ws)
+        c.set_option(parareal.OPT_USE_GRAPHS, 2)
+        out = torch.empty((p.B, p.M), dtype=torch.float32, device="cuda")
+        with torch.cuda.stream(stream):
+            for _ in range(4):                     # capture, then replays (as the timed loop)
+                out.zero_()
+                rep = c.solve_device(out)
+            stream.synchronize()
+        U = out.cpu().numpy()
+        it = c.copy_iterates(0, p.N + 1)
+        assert rep["iterations"] == ref_K == 3
+        c.set_option(parareal.OPT_PIPELINE, 1)
+        _, rb = c.solve()                          # the blocking schedule's launch count
+        c.set_option(parareal.OPT_PIPELINE, 0)
+        c.set_option(parareal.OPT_USE_GRAPHS, 0)
+        _, ra = c.solve()                          # instrumented: δ history
+    assert rep["kernel_launches"] < rb["kernel_launches"], "the bench step did not run the pipelined kernel"
+    assert np.array_equal(U, it[-1])
+    _gate_or_amplification(it, ref_U, U32, "headline C2 iterates")
+    assert ra["iterations"] == 3
+    assert_delta(ra["delta"], ref_d)
+
+
+def test_k2_persistent_pass_long_lookback():
+    """k_pass_res2 (>= 16 systems) on a grid whose look-back windows exceed 32 and 64 predecessor
+    tiles (the prefetched second window and the > 64 fallback of fine_streamed.cuh): 2^18 points,
+    dτ = 1/96, 16 slices of 6 IE steps, one Parareal iteration with numerical G -- every iterate
+    against the oracle."""
+    M, N, nf = 1 << 18, 16, 6
+    p = synth.single(M, N, fine_steps=nf, coarse=synth.COARSE_IMPLICIT_EULER, coarse_steps=1, max_iter=1, tol=0.0)
+    W = _k2_lookback_windows(M, 0.2, 0.05, 1.0 / (N * nf))
+    assert W > 64, W
+    with ctx_for(p, fine_kernel=2) as c:
+        _, rep = c.solve()
+        it = c.copy_iterates(0, p.N + 1)
+    ref_U, ref_d, K, _ = oracle.parareal(p)
+    assert rep["iterations"] == K == 1
+    assert_close(it, ref_U, what="K2 long look-back M=2^18")
+    assert_delta(rep["delta"], ref_d)
+
+
+def test_c3_grid_fine_sweep_persistent():
+    """The C3 grid (2^20 points, the C3 step dτ = 1/6400) on the persistent K2 kernel: 16 slices of
+    2 steps, one Parareal iteration with numerical G -- all 17 boundary states (about 17 M values)
+    against the oracle."""
+    M, N, nf = 1 << 20, 16, 2
+    p = synth.single(M, N, fine_steps=nf, coarse=synth.COARSE_IMPLICIT_EULER, coarse_steps=1, max_iter=1, tol=0.0,
+                     T=N * nf / 6400.0)
+    with ctx_for(p) as c:
+        _, rep = c.solve()
+        it = c.copy_iterates(0, p.N + 1)
+    ref_U, ref_d, K, _ = oracle.parareal(p)
+    assert rep["iterations"] == K == 1
+    assert_close(it, ref_U, what="C3-grid Parareal iterate")
+    assert_delta(rep["delta"], ref_d)
