@@ -9,7 +9,7 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r02/
 timeout 900 python bench.py > gpurun_out/r02/bench_default.json 2> gpurun_out/r02/bench_default.err; tail -c 600 gpurun_out/r02/bench_default.err
 for c in c1pipe c2num k2res k4 c4; do
   for t in memcheck racecheck synccheck; do
-    timeout 600 compute-sanitizer --tool $t --print-limit 20 python scripts/sanitize_target.py $c > gpurun_out/r02/san_${c}_${t}.txt 2>&1
+    timeout 300 compute-sanitizer --tool $t --print-limit 20 python scripts/sanitize_target.py $c > gpurun_out/r02/san_${c}_${t}.txt 2>&1
     echo "$c $t rc=$? $(grep -E 'ERROR SUMMARY|RACECHECK SUMMARY' gpurun_out/r02/san_${c}_${t}.txt | tail -1)"
   done
 done
