@@ -193,3 +193,30 @@ def load_blob(path: str) -> Net:
     if off != len(data):
         raise ValueError("trailing bytes in blob")
     return Net(dims, W, b, act, ins, float(outs))
+
+
+# ---- PINN training inputs ("randomly generate N_f=100,000 collocation
+# points within the domain ..., N_b=10,000 at the boundary and N_exp=10,000 ... over [0,5000]")
+PAPER_COLLOCATION = (100000, 10000, 10000)   # N_f, N_b, N_exp
+
+
+def collocation(market: dict, n_f: int, n_b: int, n_exp: int, seed: int = 0):
+    """Seeded collocation sets (float32) for the market dict(K, sigma, r, T, L): interior (t, S)
+    uniform over [0,T]x[0,L]; boundary (t, S) with t uniform and S alternating 0, L (SPEC S:236:
+    both ends in equal proportion); expiry S uniform over [0,L].  Returns (t_f, S_f, t_b, S_b, S_e)."""
+    rng = np.random.Generator(np.random.PCG64(seed + 104729))
+    T, L = float(market["T"]), float(market["L"])
+    t_f = rng.uniform(0.0, T, n_f).astype(np.float32)
+    S_f = rng.uniform(0.0, L, n_f).astype(np.float32)
+    t_b = rng.uniform(0.0, T, n_b).astype(np.float32)
+    S_b = np.where(np.arange(n_b) % 2 == 0, 0.0, L).astype(np.float32)
+    S_e = rng.uniform(0.0, L, n_exp).astype(np.float32)
+    return t_f, S_f, t_b, S_b, S_e
+
+
+def pinn2_net(dims: Sequence[int], seed: int = 0, activation: int = ACT_TANH) -> Net:
+    """A 2-input (t, S) network for training (dims[0] = 2): Kaiming-normal weights, zero biases
+    (SPEC S:197)."""
+    net = kaiming_net(dims, seed=seed, activation=activation)
+    net.b = [np.zeros_like(b) for b in net.b]
+    return net
