@@ -207,12 +207,17 @@ enum {
                                (stream-ordered, like a library call: the caller synchronises; rep, if
                                given, receives iterations and kernel_launches, zero times, no δ).  */
   PR_OPT_PINN_KERNEL = 3,   /* 0 auto, 1 shared-memory weights, 2 latency mode (4 threads/point; B·M ≤ 65536) */
-  PR_OPT_PIPELINE = 4       /* 0 auto: a single-GPU fixed-K (tol == 0) solve with PINN G in latency mode (or
+  PR_OPT_PIPELINE = 4,      /* 0 auto: a single-GPU fixed-K (tol == 0) solve with PINN G in latency mode (or
                                the numerical G) and the resident fine kernel at M ≤ 1024 runs pipelined
                                (SURVEY NEXT-2): fine
                                solves and the coarse chain overlapped in one cooperative kernel, bitwise the
                                blocking results; its report gives the overlapped time as both ms_fine and
                                ms_coarse.  1: always the blocking schedule. */
+  PR_OPT_COMM_TIMEOUT_MS = 5 /* world > 1 with NCCL: every host wait on the context stream polls
+                               ncclCommGetAsyncError; an asynchronous NCCL error, or a wait longer than
+                               this many milliseconds (a peer rank that died or hangs), aborts the
+                               communicator and poisons the context (PR_ERR_NCCL) instead of hanging.
+                               Default 600000; 0 waits forever.  No effect with world == 1. */
 };
 pr_status parareal_set_option(pr_ctx *ctx, int32_t key, int64_t value);
 

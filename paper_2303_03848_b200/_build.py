@@ -9,10 +9,11 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libparareal.so")
-UNITS = ["parareal.cu", "res.cu", "streamed.cu", "pinn_smem.cu", "pinn_param.cu", "misc.cu", "pipe.cu", "pinn_tc.cu"]
+UNITS = ["parareal.cu", "res.cu", "streamed.cu", "pinn_smem.cu", "pinn_param.cu", "misc.cu", "pipe.cu", "pinn_tc.cu", "pinn_train.cu"]
 HEADERS = ["launch.h", "fine_resident.cuh", "fine_streamed.cuh", "pinn_chain.cuh"]
 SOURCES = UNITS + HEADERS
 HEADER = os.path.join(ROOT, "include", "parareal.h")
+HEADERS_ABI = [HEADER, os.path.join(ROOT, "include", "pinn_train.h")]
 
 NVCC_FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
               "-Xcompiler", "-fPIC"]
@@ -31,7 +32,7 @@ def stale() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = [os.path.join(CSRC, s) for s in SOURCES] + [HEADER]
+    deps = [os.path.join(CSRC, s) for s in SOURCES] + HEADERS_ABI
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
@@ -44,7 +45,7 @@ def build_cuda(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(BUILD_DIR, exist_ok=True)
     nv = _nvcc()
     hdr_t = max(os.path.getmtime(os.path.join(CSRC, h)) for h in HEADERS + []) if HEADERS else 0
-    hdr_t = max(hdr_t, os.path.getmtime(HEADER))
+    hdr_t = max([hdr_t] + [os.path.getmtime(h) for h in HEADERS_ABI])
 
     def compile_unit(u):
         src = os.path.join(CSRC, u)

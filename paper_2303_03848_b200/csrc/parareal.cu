@@ -8,6 +8,8 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <chrono>
+#include <thread>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -28,7 +30,7 @@ namespace {
 typedef struct ncclComm *ncclComm_t;
 typedef struct { char internal[128]; } ncclUniqueId;
 typedef int ncclResult_t;
-enum { kNcclFloat32 = 7, kNcclFloat64 = 8, kNcclMax = 2 };
+enum { kNcclFloat32 = 7, kNcclFloat64 = 8, kNcclMax = 2, kNcclInProgress = 7 /* ncclResult_t */ };
 
 struct Nccl {
   bool tried = false, ok = false;
@@ -43,6 +45,7 @@ struct Nccl {
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
   const char *(*GetErrorString)(ncclResult_t) = nullptr;
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t *) = nullptr;
 };
 std::mutex g_nccl_mu;
 Nccl g_nccl;
@@ -69,6 +72,7 @@ Nccl &nccl() {
   PR_SYM(GroupStart, "ncclGroupStart");
   PR_SYM(GroupEnd, "ncclGroupEnd");
   PR_SYM(GetErrorString, "ncclGetErrorString");
+  PR_SYM(CommGetAsyncError, "ncclCommGetAsyncError");
 #undef PR_SYM
   g_nccl.ok = true;
   return g_nccl;
@@ -156,6 +160,7 @@ struct pr_ctx {
   int opt_fine_kernel = 0;
   int opt_graphs = 0;
   int opt_pipeline = 0;  // 0 auto, 1 off (PR_OPT_PIPELINE)
+  int64_t comm_timeout_ms = 600000;  // PR_OPT_COMM_TIMEOUT_MS (0: wait forever)
   bool capturing = false;
   // pipelined schedule (pipe.cu): per-iteration δ partials and the slice counters
   double *pipe_partials = nullptr;
@@ -216,6 +221,44 @@ pr_status fail(pr_ctx *c, pr_status s, const std::string &msg) {
     if (e_ != cudaSuccess)                                                                    \
       return fail(c, PR_ERR_CUDA, fmt("kernel launch failed: %s (%s:%d)", cudaGetErrorString(e_), \
                                       __FILE__, __LINE__));                                   \
+  } while (0)
+
+// Waits for the context stream.  With an NCCL communicator the wait polls instead of blocking:
+// ncclCommGetAsyncError reports a failed collective (a peer that died, a network error), and a
+// wait longer than PR_OPT_COMM_TIMEOUT_MS (a hung peer that reports nothing) aborts the
+// communicator; both poison the context with PR_ERR_NCCL instead of hanging every rank
+// (failures are reported, per slice and iteration, not waited on forever).
+pr_status sync_stream(pr_ctx *c) {
+  if (!c->comm) {
+    CU(cudaStreamSynchronize(c->stream));
+    return PR_OK;
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  for (unsigned spin = 0;; ++spin) {
+    const cudaError_t q = cudaStreamQuery(c->stream);
+    if (q == cudaSuccess) return PR_OK;
+    if (q != cudaErrorNotReady) CU(q);
+    ncclResult_t ae = 0;
+    NC(nccl().CommGetAsyncError(c->comm, &ae));
+    if (ae != 0 && ae != kNcclInProgress) {
+      nccl().CommAbort(c->comm);
+      c->comm = nullptr;
+      return fail(c, PR_ERR_NCCL, fmt("NCCL asynchronous error on rank %d: %s", c->rank, nccl().GetErrorString(ae)));
+    }
+    const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    if (c->comm_timeout_ms > 0 && ms > (double)c->comm_timeout_ms) {
+      nccl().CommAbort(c->comm);
+      c->comm = nullptr;
+      return fail(c, PR_ERR_NCCL, fmt("rank %d: stream wait exceeded PR_OPT_COMM_TIMEOUT_MS = %lld ms (a peer rank "
+                                      "stalled or died); communicator aborted", c->rank, (long long)c->comm_timeout_ms));
+    }
+    if (spin > 64) std::this_thread::sleep_for(std::chrono::microseconds(50));
+  }
+}
+#define SYNC()                          \
+  do {                                  \
+    pr_status s_ = sync_stream(c);      \
+    if (s_ != PR_OK) return s_;         \
   } while (0)
 
 pr_status check_ctx(pr_ctx *c) {
@@ -743,7 +786,7 @@ pr_status comm_send(pr_ctx *c, const float *buf, size_t count, int peer) {
   }
   LoopGroup *g = c->loop;
   const size_t bytes = count * sizeof(float), idx = (size_t)c->rank * g->world + peer;
-  CU(cudaStreamSynchronize(c->stream));  // the row is complete
+  SYNC();  // the row is complete
   std::unique_lock<std::mutex> lk(g->mu);
   g->cv.wait(lk, [&] { return !g->full[idx]; });
   if (g->box_bytes[idx] < bytes) {
@@ -764,7 +807,7 @@ pr_status comm_recv(pr_ctx *c, float *buf, size_t count, int peer) {
   }
   LoopGroup *g = c->loop;
   const size_t bytes = count * sizeof(float), idx = (size_t)peer * g->world + c->rank;
-  CU(cudaStreamSynchronize(c->stream));  // earlier work reading buf is done
+  SYNC();  // earlier work reading buf is done
   std::unique_lock<std::mutex> lk(g->mu);
   g->cv.wait(lk, [&] { return g->full[idx] != 0; });
   CU(cudaMemcpy(buf, g->box[idx], bytes, cudaMemcpyDeviceToDevice));
@@ -780,7 +823,7 @@ pr_status comm_allreduce_max(pr_ctx *c, unsigned long long *slot) {
   }
   LoopGroup *g = c->loop;
   unsigned long long v = 0;
-  CU(cudaStreamSynchronize(c->stream));
+  SYNC();
   CU(cudaMemcpy(&v, slot, sizeof v, cudaMemcpyDeviceToHost));
   unsigned long long res;
   {
@@ -996,7 +1039,7 @@ pr_status solve_pipelined(pr_ctx *c) {
   if (d_trace) {
     std::vector<unsigned long long> h(ntr);
     CU(cudaMemcpyAsync(h.data(), d_trace, ntr * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
-    CU(cudaStreamSynchronize(c->stream));
+    SYNC();
     cudaFree(d_trace);
     if (FILE *f = fopen(trace_path, "w")) {
       for (int k = 0; k <= c->max_iter; ++k)
@@ -1091,7 +1134,7 @@ pr_status solve_impl(pr_ctx *c, const float *V_T, float *V_0, bool device_ptr, p
       }
       return PR_OK;
     }
-    CU(cudaStreamSynchronize(c->stream));
+    SYNC();
     return solve_report(c, c->g_K, 0, c->g_e0, c->g_e1, c->g_spans, c->g_launches, rep, c->opt_graphs == 2);
   }
   if (pipe_eligible(c) && (st = ensure_pipe(c))) return st;  // (allocation cannot be captured)
@@ -1178,7 +1221,7 @@ pr_status solve_impl(pr_ctx *c, const float *V_T, float *V_0, bool device_ptr, p
     if (c->tol > 0.0) {
       CU(cudaMemcpyAsync(c->h_delta + (k - 1), c->d_delta + (k - 1), sizeof(double), cudaMemcpyDeviceToHost,
                          c->stream));
-      CU(cudaStreamSynchronize(c->stream));
+      SYNC();
       if (c->h_delta[k - 1] < c->tol) {
         conv = 1;
         break;
@@ -1229,7 +1272,7 @@ pr_status solve_impl(pr_ctx *c, const float *V_T, float *V_0, bool device_ptr, p
   } else if (st) {
     return st;
   }
-  CU(cudaStreamSynchronize(c->stream));
+  SYNC();
   return solve_report(c, K, conv, e0, e1, pt.spans, c->launches - launches0, rep, use_graph && c->opt_graphs == 2);
 }
 
@@ -1265,7 +1308,7 @@ pr_status serial_fine_impl(pr_ctx *c, const float *V_T, float *V_0, bool device_
   }
   cudaEventRecord(e1, c->stream);
   if (V_0 && (st = store_rows(c, V_0, c->tmp, device_ptr))) return st;
-  CU(cudaStreamSynchronize(c->stream));
+  SYNC();
   if (ms) {
     float m = 0;
     cudaEventElapsedTime(&m, e0, e1);
@@ -1624,7 +1667,7 @@ pr_status parareal_initial_state(pr_ctx *c, float *V_T) {
   c->U = save;
   if (st) return st;
   if ((st = store_rows(c, V_T, c->tmp, false))) return st;
-  CU(cudaStreamSynchronize(c->stream));
+  SYNC();
   return PR_OK;
 }
 
@@ -1658,7 +1701,7 @@ pr_status parareal_apply_fine(pr_ctx *c, int32_t n, const float *U_in, float *U_
     if (e != cudaSuccess) return fail(c, PR_ERR_CUDA, fmt("streamed apply: %s", cudaGetErrorString(e)));
   }
   if ((st = store_rows(c, U_out, c->tmp + row, false))) return st;
-  CU(cudaStreamSynchronize(c->stream));
+  SYNC();
   return PR_OK;
 }
 
@@ -1703,7 +1746,7 @@ pr_status parareal_apply_coarse(pr_ctx *c, int32_t n, const float *U_in, float *
     if (e != cudaSuccess) return fail(c, PR_ERR_CUDA, fmt("streamed coarse apply: %s", cudaGetErrorString(e)));
     if ((st = store_rows(c, U_out, c->tmp, false))) return st;
   }
-  CU(cudaStreamSynchronize(c->stream));
+  SYNC();
   return PR_OK;
 }
 
@@ -1719,7 +1762,7 @@ pr_status parareal_copy_iterates(pr_ctx *c, int32_t n_first, int32_t n_count, fl
     if ((st = store_rows(c, host + (size_t)i * c->B * c->M, c->U + (size_t)(n_first - c->n0 + i) * row, false)))
       return st;
   }
-  CU(cudaStreamSynchronize(c->stream));
+  SYNC();
   return PR_OK;
 }
 
@@ -1757,6 +1800,10 @@ pr_status parareal_set_option(pr_ctx *c, int32_t key, int64_t value) {
     case PR_OPT_PIPELINE:
       if (value < 0 || value > 1) return fail(c, PR_ERR_INVALID_ARGUMENT, "PR_OPT_PIPELINE must be 0 or 1");
       c->opt_pipeline = (int)value;
+      return PR_OK;
+    case PR_OPT_COMM_TIMEOUT_MS:
+      if (value < 0) return fail(c, PR_ERR_INVALID_ARGUMENT, "PR_OPT_COMM_TIMEOUT_MS must be >= 0");
+      c->comm_timeout_ms = value;
       return PR_OK;
   }
   return fail(c, PR_ERR_INVALID_ARGUMENT, fmt("unknown option key %d", key));

@@ -6,24 +6,29 @@ import re
 import numpy as np
 import pytest
 
-from paper_2303_03848_b200 import parareal, synth
+from paper_2303_03848_b200 import parareal, pinn_train, synth
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def _header_functions():
-    src = open(os.path.join(ROOT, "include", "parareal.h")).read()
+def _header_functions(header="parareal.h", prefix="parareal_"):
+    src = open(os.path.join(ROOT, "include", header)).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(parareal_\w+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(%s\w+)\s*\(" % prefix, src)))
+
+
+def _all_declared():
+    return _header_functions() + _header_functions("pinn_train.h", "pinn_train_")
 
 
 def test_header_matches_binding_list():
     assert _header_functions() == sorted(parareal.EXPORTS)
+    assert _header_functions("pinn_train.h", "pinn_train_") == sorted(pinn_train.EXPORTS)
 
 
 def test_library_exports_every_declared_symbol():
     L = parareal.lib()
-    for name in _header_functions():
+    for name in _all_declared():
         assert hasattr(L, name), name
 
 
@@ -32,7 +37,7 @@ def test_exports_are_c_symbols():
     import subprocess
     out = subprocess.check_output(["nm", "-D", "--defined-only", parareal.LIB_PATH]).decode()
     syms = {l.split()[-1] for l in out.splitlines() if " T " in l}
-    for name in _header_functions():
+    for name in _all_declared():
         assert name in syms, name
 
 
@@ -94,3 +99,29 @@ def test_no_cpu_fallback_without_gpu():
     with pytest.raises(parareal.PararealError) as ei:
         parareal.Context(synth.config("C1"))
     assert ei.value.status == 3
+
+
+# ---------------------------------------------------------------- pinn_train.h validation (no device call)
+
+_MK = dict(K=1.0, sigma=0.2, r=0.05, T=1.0, L=4.0)
+
+
+@pytest.mark.parametrize("change,frag", [
+    (dict(market=dict(_MK, sigma=0.0)), "cfg.sigma"),
+    (dict(market=dict(_MK, L=-1.0)), "cfg.L"),
+    (dict(dims=[3, 20, 1]), "cfg.dims"),
+    (dict(dims=[2, 20, 16, 1]), "hidden widths"),
+    (dict(dims=[2, 24, 24, 1]), "hidden width 24"),
+    (dict(batches=0), "cfg.batches"),
+    (dict(batches=1000), "cfg.batches"),
+    (dict(beta1=1.0), "cfg.beta1"),
+])
+def test_pinn_train_init_validates_before_touching_the_device(change, frag):
+    dims = change.get("dims", [2, 20, 20, 1])
+    net = synth.pinn2_net([2 if i == 0 and dims[0] == 2 else d for i, d in enumerate(dims)], seed=0) \
+        if dims[0] == 2 else synth.kaiming_net(dims, seed=0)
+    sets = synth.collocation(_MK, 500, 50, 50, seed=0)
+    with pytest.raises(parareal.PararealError) as ei:
+        pinn_train.Trainer(net, change.get("market", _MK), sets, batches=change.get("batches", 5),
+                           beta1=change.get("beta1", 0.9))
+    assert frag in str(ei.value)
