@@ -111,7 +111,9 @@ typedef struct {
   int32_t converged;            /* 1 iff δ^K < tol                                           */
   double *delta;                /* caller buffer [max_iter] or NULL: δ^k, k = 1..K            */
   double ms_total;              /* device time of the solve on this rank                      */
-  double ms_coarse, ms_fine, ms_comm, ms_setup;  /* per-phase device time on this rank        */
+  double ms_coarse, ms_fine, ms_comm, ms_setup;  /* per-phase device time on this rank; with world > 1
+                                   ms_coarse includes the chain's hand-offs of U_{n0}/U_{n1} (they
+                                   overlap the chain in the wavefront) and ms_comm is the gather of U_N */
   int64_t kernel_launches;      /* this library's kernels launched during the solve          */
 } pr_report;
 
@@ -213,11 +215,18 @@ enum {
                                solves and the coarse chain overlapped in one cooperative kernel, bitwise the
                                blocking results; its report gives the overlapped time as both ms_fine and
                                ms_coarse.  1: always the blocking schedule. */
-  PR_OPT_COMM_TIMEOUT_MS = 5 /* world > 1 with NCCL: every host wait on the context stream polls
+  PR_OPT_COMM_TIMEOUT_MS = 5, /* world > 1 with NCCL: every host wait on the context stream polls
                                ncclCommGetAsyncError; an asynchronous NCCL error, or a wait longer than
                                this many milliseconds (a peer rank that died or hangs), aborts the
                                communicator and poisons the context (PR_ERR_NCCL) instead of hanging.
                                Default 600000; 0 waits forever.  No effect with world == 1. */
+  PR_OPT_WAVEFRONT = 6       /* world > 1, PINN G, B == 1: the coarse chain runs as a wavefront of j-chunks
+                               across ranks (G is pointwise in S): each chunk of U_{n1} goes
+                               to the next rank as soon as it is chained, so the ranks chain concurrently.
+                               Results are bitwise those of the blocking chain (the chunks are CTA ranges
+                               of the same kernel).  0 auto (8 chunks when M ≥ 65536, else blocking),
+                               1 blocking, n ≥ 2: n chunks (at most one per CTA).  Numerical G (coupled in
+                               S) and B > 1 always chain blocking. */
 };
 pr_status parareal_set_option(pr_ctx *ctx, int32_t key, int64_t value);
 

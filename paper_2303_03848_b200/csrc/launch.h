@@ -41,6 +41,7 @@ bool pinn_tc_supported(int IN, int W, int act, bool bf16);
 size_t pinn_tc_smem(int W, int LH, int nfloats, bool bf16, bool *resident);
 size_t pinn_tc_layer_elems(int W, bool bf16);
 void pinn_tc_pack(const float *Wl, int W, bool bf16, uint16_t *out);
+int pinn_tc_points_per_cta(int W, int LH, int nfloats, bool bf16);  // 256 (ping-pong kernel) or 128
 cudaError_t launch_pinn_tc(int IN, int W, int act, bool bf16, const PinnArgs &a, const void *wh, dim3 grid,
                            cudaStream_t s);
 // Pipelined Parareal on one GPU (pipe.cu, NEXT-2): PINN chain (latency mode) and K1 fine solves

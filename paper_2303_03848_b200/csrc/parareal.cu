@@ -161,6 +161,7 @@ struct pr_ctx {
   int opt_graphs = 0;
   int opt_pipeline = 0;  // 0 auto, 1 off (PR_OPT_PIPELINE)
   int64_t comm_timeout_ms = 600000;  // PR_OPT_COMM_TIMEOUT_MS (0: wait forever)
+  int opt_wavefront = 0;             // PR_OPT_WAVEFRONT: 0 auto, 1 blocking chain, n ≥ 2 chunks
   bool capturing = false;
   // pipelined schedule (pipe.cu): per-iteration δ partials and the slice counters
   double *pipe_partials = nullptr;
@@ -630,31 +631,47 @@ pr::PinnArgs pinn_args(pr_ctx *c) {
   return a;
 }
 
-pr_status launch_pinn(pr_ctx *c, const pr::PinnArgs &a) {
+// CTA geometry of the PINN chain along j: points per CTA and CTAs per instance row of the
+// evaluator launch_pinn picks (a j-chunk of the chain is a CTA range, so a chunked chain does the
+// arithmetic of the whole one, δ partial slots included).
+void pinn_geometry(const pr_ctx *c, int *ppc, int *gx) {
+  int p;
+  if (c->tc) p = pr::pinn_tc_points_per_cta(c->W, c->LH, c->tc_nfloats, c->tc == PR_PREC_BF16_TC);
+  else if (use_split_pinn(c)) p = pr::pinn_split_ppc(split_G(c));
+  else if (use_param_pinn(c)) p = kPinnTPB;
+  else p = kPinnTPB * pr::pinn_smem_pts(c->W);
+  *ppc = p;
+  *gx = (c->M + p - 1) / p;
+}
+
+// The PINN chain over the CTAs [cta_lo, cta_hi) along j (cta_hi < 0: all of them).
+pr_status launch_pinn(pr_ctx *c, const pr::PinnArgs &a0, int cta_lo = 0, int cta_hi = -1) {
+  int ppc, gx;
+  pinn_geometry(c, &ppc, &gx);
+  if (cta_hi < 0) cta_hi = gx;
+  if (cta_hi <= cta_lo) return PR_OK;
+  pr::PinnArgs a = a0;
+  a.cta0 = cta_lo;
+  const dim3 grid(cta_hi - cta_lo, c->B);
   if (c->tc) {  // K4: tensor cores (wide nets)
     pr::PinnArgs t = a;
     t.wts = c->d_tcp;
     t.nfloats = c->tc_nfloats;
-    dim3 grid((c->M + 127) / 128, c->B);
     LAUNCH(pr::launch_pinn_tc(c->IN, c->W, c->act, c->tc == PR_PREC_BF16_TC, t, c->d_wh, grid, c->stream));
     return PR_OK;
   }
   if (use_split_pinn(c)) {
-    const int G = split_G(c), ppc = pr::pinn_split_ppc(G);  // points per CTA
-    dim3 grid((c->M + ppc - 1) / ppc, c->B);
+    const int G = split_G(c);
     pr::PinnArgs t = a;
     if (pr::pinn_split_is_group(c->W, G)) t.wts = c->d_wgrp;  // group kernels: hidden matrices in the group order
     LAUNCH(pr::launch_pinn_split(c->IN, c->W, c->act, G, t, grid, (size_t)c->nfloats * sizeof(float), c->stream));
     return PR_OK;
   }
   if (use_param_pinn(c)) {
-    dim3 grid((c->M + kPinnTPB - 1) / kPinnTPB, c->B);
     LAUNCH(pr::launch_pinn_param(c->IN, c->W, c->LH, c->act, c->h_wts.data(), a, grid, c->stream));
     return PR_OK;
   }
   if (!pr::pinn_smem_supported(c->IN, c->W, c->act)) return fail(c, PR_ERR_UNSUPPORTED, "no PINN kernel for this width");
-  const int pts = pr::pinn_smem_pts(c->W);
-  dim3 grid((c->M + kPinnTPB * pts - 1) / (kPinnTPB * pts), c->B);
   LAUNCH(pr::launch_pinn_smem(c->IN, c->W, c->act, a, grid, (size_t)c->nfloats * sizeof(float), c->stream));
   return PR_OK;
 }
@@ -688,7 +705,8 @@ pr_status fine_sweep(pr_ctx *c, int ln_lo, int fk_ln) {
 }
 
 // Coarse chain with correction over local slices [ln0, Nloc).  k == 0: no correction, no δ.
-pr_status coarse_chain(pr_ctx *c, int k, int ln0, bool copy) {
+// PINN G: only the CTAs [cta_lo, cta_hi) along j (a wavefront chunk; cta_hi < 0: all).
+pr_status coarse_chain(pr_ctx *c, int k, int ln0, bool copy, int cta_lo = 0, int cta_hi = -1) {
   const bool corr = k > 0;
   if (c->coarse == PR_COARSE_PINN) {
     pr::PinnArgs a = pinn_args(c);
@@ -703,7 +721,7 @@ pr_status coarse_chain(pr_ctx *c, int k, int ln0, bool copy) {
     if (ln0 >= c->Nloc) {  // copy only (chain empty): still need U_k := F̂_{k−1} and its δ
       a.ln1 = ln0;
     }
-    return launch_pinn(c, a);
+    return launch_pinn(c, a, cta_lo, cta_hi);
   }
   if (!use_resident(c)) {
     pr::StreamedChainJob j;
@@ -843,6 +861,71 @@ pr_status comm_allreduce_max(pr_ctx *c, unsigned long long *slot) {
     res = g->result;  // (the next generation needs this rank's arrival first)
   }
   CU(cudaMemcpy(slot, &res, sizeof res, cudaMemcpyHostToDevice));
+  return PR_OK;
+}
+
+// One wavefront hand-off: send `scount` values to `speer` and receive `rcount` from `rpeer` (either
+// may be absent: count 0).  NCCL: one group, so the send of chunk c−1 and the receive of chunk c
+// progress together; loopback: the send, then the receive.
+pr_status comm_sendrecv(pr_ctx *c, const float *sbuf, size_t scount, int speer, float *rbuf, size_t rcount, int rpeer) {
+  if (!c->loop) {
+    NC(nccl().GroupStart());
+    if (scount) NC(nccl().Send(sbuf, scount, kNcclFloat32, speer, c->comm, c->stream));
+    if (rcount) NC(nccl().Recv(rbuf, rcount, kNcclFloat32, rpeer, c->comm, c->stream));
+    NC(nccl().GroupEnd());
+    return PR_OK;
+  }
+  pr_status st;
+  if (scount && (st = comm_send(c, sbuf, scount, speer))) return st;
+  if (rcount && (st = comm_recv(c, rbuf, rcount, rpeer))) return st;
+  return PR_OK;
+}
+
+// Chunks of the PINN chain's wavefront across ranks: G is pointwise in S, so the
+// chain of grid-point chunk q needs only chunk q of U_{n0} from the previous rank; a rank hands on
+// each chunk of U_{n1} as soon as its chain has finished it and the next rank starts on it while
+// this one chains the next chunk.  Coarse time per iteration ≈ (1 + (R−1)/C)·t_rank instead of
+// R·t_rank.  Pointwise G and one instance row (contiguous chunks) only; 1 = the blocking chain.
+int wavefront_chunks(const pr_ctx *c) {
+  if (c->world == 1 || c->coarse != PR_COARSE_PINN || c->B != 1 || c->opt_wavefront == 1) return 1;
+  int ppc, gx;
+  pinn_geometry(c, &ppc, &gx);
+  const int want = c->opt_wavefront >= 2 ? c->opt_wavefront : (c->M >= (1 << 16) ? 8 : 1);
+  return std::max(1, std::min(want, gx));
+}
+
+// The chain of iteration k on this rank with the receive of U_{n0} before it and the send of
+// U_{n1} after it (plan P), as one blocking exchange or as a chunk wavefront.
+pr_status chain_exchange(pr_ctx *c, int k, const pr_plan &P, bool run_chain, double *ms_comm_unused) {
+  (void)ms_comm_unused;
+  const size_t row = (size_t)c->B * c->Mp;
+  float *u_in = c->U, *u_out = c->U + (size_t)c->Nloc * row;
+  const int r = c->rank, C = wavefront_chunks(c);
+  pr_status st;
+  if (C <= 1) {
+    if (P.recv_first && (st = comm_recv(c, u_in, row, r - 1))) return st;
+    if (run_chain && (st = coarse_chain(c, k, P.chain_lo, P.copy != 0))) return st;
+    if (P.send_last && (st = comm_send(c, u_out, row, r + 1))) return st;
+    return PR_OK;
+  }
+  int ppc, gx;
+  pinn_geometry(c, &ppc, &gx);
+  auto jr = [&](int q, int *lo, int *hi) {  // grid points of chunk q (CTA-aligned)
+    const int c0 = (int)((long)q * gx / C), c1 = (int)((long)(q + 1) * gx / C);
+    *lo = std::min(c0 * ppc, c->M);
+    *hi = std::min(c1 * ppc, c->M);
+    return std::make_pair(c0, c1);
+  };
+  int plo = 0, phi = 0;  // previous chunk (to send)
+  for (int q = 0; q < C; ++q) {
+    int lo, hi;
+    const auto ctas = jr(q, &lo, &hi);
+    const size_t sc = (q > 0 && P.send_last) ? (size_t)(phi - plo) : 0, rc = P.recv_first ? (size_t)(hi - lo) : 0;
+    if ((sc || rc) && (st = comm_sendrecv(c, u_out + plo, sc, r + 1, u_in + lo, rc, r - 1))) return st;
+    if (run_chain && (st = coarse_chain(c, k, P.chain_lo, P.copy != 0, ctas.first, ctas.second))) return st;
+    plo = lo, phi = hi;
+  }
+  if (P.send_last && (st = comm_send(c, u_out + plo, (size_t)(phi - plo), r + 1))) return st;
   return PR_OK;
 }
 
@@ -1178,19 +1261,9 @@ pr_status solve_impl(pr_ctx *c, const float *V_T, float *V_0, bool device_ptr, p
   if (!piped) {
   {
     const pr_plan P0 = make_plan(c->N, R, r, 0);
-    if (P0.recv_first) {
-      pt.begin(PH_COMM);
-      if ((st = comm_recv(c, c->U, row, r - 1))) return st;
-      pt.end();
-    }
-    pt.begin(PH_COARSE);
-    if ((st = coarse_chain(c, 0, P0.chain_lo, false))) return st;
+    pt.begin(PH_COARSE);  // (with R > 1 this span includes the hand-offs of U_{n0} / U_{n1})
+    if ((st = chain_exchange(c, 0, P0, true, nullptr))) return st;
     pt.end();
-    if (P0.send_last) {
-      pt.begin(PH_COMM);
-      if ((st = comm_send(c, c->U + (size_t)c->Nloc * row, row, r + 1))) return st;
-      pt.end();
-    }
   }
   for (int k = 1; k <= c->max_iter; ++k) {
     const pr_plan P = make_plan(c->N, R, r, k);
@@ -1198,22 +1271,10 @@ pr_status solve_impl(pr_ctx *c, const float *V_T, float *V_0, bool device_ptr, p
     pt.begin(PH_FINE);
     if (P.fine_hi > P.fine_lo && (st = fine_sweep(c, P.fine_lo, P.fk_local))) return st;
     pt.end();
-    // (ii) coarse chain with correction, serial in n across ranks
-    if (P.recv_first) {
-      pt.begin(PH_COMM);
-      if ((st = comm_recv(c, c->U, row, r - 1))) return st;
-      pt.end();
-    }
-    if (P.copy || P.recv_first) {
-      pt.begin(PH_COARSE);
-      if ((st = coarse_chain(c, k, P.chain_lo, P.copy != 0))) return st;
-      pt.end();
-    }
-    if (P.send_last) {
-      pt.begin(PH_COMM);
-      if ((st = comm_send(c, c->U + (size_t)c->Nloc * row, row, r + 1))) return st;
-      pt.end();
-    }
+    // (ii) coarse chain with correction, serial in n across ranks (blocking or chunk wavefront)
+    pt.begin(PH_COARSE);
+    if ((st = chain_exchange(c, k, P, P.copy || P.recv_first, nullptr))) return st;
+    pt.end();
     const int dlo = P.delta_lo, dhi = P.delta_hi;
     // (iii) δ^k and the stop rule (Q13)
     if ((st = delta_reduce(c, k, dlo, dhi, c->nch))) return st;
@@ -1800,6 +1861,10 @@ pr_status parareal_set_option(pr_ctx *c, int32_t key, int64_t value) {
     case PR_OPT_PIPELINE:
       if (value < 0 || value > 1) return fail(c, PR_ERR_INVALID_ARGUMENT, "PR_OPT_PIPELINE must be 0 or 1");
       c->opt_pipeline = (int)value;
+      return PR_OK;
+    case PR_OPT_WAVEFRONT:
+      if (value < 0 || value > 4096) return fail(c, PR_ERR_INVALID_ARGUMENT, "PR_OPT_WAVEFRONT must be in [0, 4096]");
+      c->opt_wavefront = (int)value;
       return PR_OK;
     case PR_OPT_COMM_TIMEOUT_MS:
       if (value < 0) return fail(c, PR_ERR_INVALID_ARGUMENT, "PR_OPT_COMM_TIMEOUT_MS must be >= 0");

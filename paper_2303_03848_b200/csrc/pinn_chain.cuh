@@ -34,6 +34,7 @@ struct PinnArgs {
   double *partials;        // nullable [(ln·B + b)·nch + chunk]·2
   int nch;
   float *Gout;             // test hook: non-null → write G_{ln0}(U[ln0]) only, no chain
+  int cta0;                // first CTA (along j) of this launch: a j-chunk of the chain (NEXT-2 wavefront)
 };
 
 }  // namespace pr
@@ -143,13 +144,14 @@ __device__ __forceinline__ void pinn_chain_body(const PinnArgs &a, Eval ev) {
   const int lane_ = threadIdx.x & 31;
   const bool active = (G == 1) || lane_ < GPW * G;
   const bool leader = (G == 1) || (active && lane_ % G == 0);
+  const int cta = blockIdx.x + a.cta0;  // CTA index along j (δ partial slot)
   int j[PTS];
   bool ok[PTS];
   float s_over_L[PTS], u[PTS];
 #pragma unroll
   for (int p = 0; p < PTS; ++p) {
-    j[p] = (G == 1) ? blockIdx.x * (blockDim.x * PTS) + p * blockDim.x + threadIdx.x
-                    : blockIdx.x * ((blockDim.x >> 5) * GPW) + (threadIdx.x >> 5) * GPW + lane_ / G;
+    j[p] = (G == 1) ? cta * (blockDim.x * PTS) + p * blockDim.x + threadIdx.x
+                    : cta * ((blockDim.x >> 5) * GPW) + (threadIdx.x >> 5) * GPW + lane_ / G;
     ok[p] = active && j[p] < a.M;
     // S_j / L_b = j dS / L_b with dS = L_b / (M+1)  (reading Q4, Q8)
     const double dS = Lb / (a.M + 1);
@@ -179,7 +181,7 @@ __device__ __forceinline__ void pinn_chain_body(const PinnArgs &a, Eval ev) {
     if (a.partials) {
       cta_reduce2(num, den, red);
       if (threadIdx.x == 0) {
-        double *pp = a.partials + (((size_t)a.ln0 * a.B + b) * a.nch + blockIdx.x) * 2;
+        double *pp = a.partials + (((size_t)a.ln0 * a.B + b) * a.nch + cta) * 2;
         pp[0] = num;
         pp[1] = den;
       }
@@ -199,7 +201,7 @@ __device__ __forceinline__ void pinn_chain_body(const PinnArgs &a, Eval ev) {
     if (threadIdx.x < count) {
       double num = 0.0, den = 0.0;
       for (int q = 0; q < nwarp; ++q) { num += wpart[threadIdx.x][q][0]; den += wpart[threadIdx.x][q][1]; }
-      double *pp = a.partials + (((size_t)(ln_first + threadIdx.x + 1) * a.B + b) * a.nch + blockIdx.x) * 2;
+      double *pp = a.partials + (((size_t)(ln_first + threadIdx.x + 1) * a.B + b) * a.nch + cta) * 2;
       pp[0] = num;
       pp[1] = den;
     }

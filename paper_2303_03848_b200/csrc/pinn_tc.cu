@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(128) k_pinn_chain_tc(PinnTcArgs ta) {
   const float gscale = (float)(Lb * (double)a.out_scale);
   const float invL = (float)(1.0 / Lb);
   const size_t sstride = (size_t)a.B * a.Mp;
-  const int j = blockIdx.x * TILE + t;
+  const int j = (blockIdx.x + a.cta0) * TILE + t;
   const bool ok = j < a.M;
   const double dS = Lb / (a.M + 1);
   const float s_over_L = (float)(((j + 1) * dS) / Lb);
@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(128) k_pinn_chain_tc(PinnTcArgs ta) {
     if (a.partials) {
       cta_reduce2(num, den, red);
       if (t == 0) {
-        double *pp = a.partials + (((size_t)a.ln0 * a.B + b) * a.nch + blockIdx.x) * 2;
+        double *pp = a.partials + (((size_t)a.ln0 * a.B + b) * a.nch + blockIdx.x + a.cta0) * 2;
         pp[0] = num;
         pp[1] = den;
       }
@@ -357,7 +357,7 @@ __global__ void __launch_bounds__(128) k_pinn_chain_tc(PinnTcArgs ta) {
     if (a.partials) {
       cta_reduce2(num, den, red);
       if (t == 0) {
-        double *pp = a.partials + (((size_t)(ln + 1) * a.B + b) * a.nch + blockIdx.x) * 2;
+        double *pp = a.partials + (((size_t)(ln + 1) * a.B + b) * a.nch + blockIdx.x + a.cta0) * 2;
         pp[0] = num;
         pp[1] = den;
       }
@@ -535,7 +535,7 @@ __global__ void __launch_bounds__(288, 1) k_pinn_chain_tc2(PinnTcArgs ta) {
     const float gscale = (float)(Lb * (double)a.out_scale);
     const float invL = (float)(1.0 / Lb);
     const size_t sstride = (size_t)a.B * a.Mp;
-    const int j = blockIdx.x * (2 * TILE) + wg * TILE + tw;
+    const int j = (blockIdx.x + a.cta0) * (2 * TILE) + wg * TILE + tw;
     const bool ok = j < a.M;
     const double dS = Lb / (a.M + 1);
     const float s_over_L = (float)(((j + 1) * dS) / Lb);
@@ -555,7 +555,7 @@ __global__ void __launch_bounds__(288, 1) k_pinn_chain_tc2(PinnTcArgs ta) {
       if (a.partials) {
         reduce256(num, den);
         if (t == 0) {
-          double *pp = a.partials + (((size_t)a.ln0 * a.B + b) * a.nch + blockIdx.x) * 2;
+          double *pp = a.partials + (((size_t)a.ln0 * a.B + b) * a.nch + blockIdx.x + a.cta0) * 2;
           pp[0] = num;
           pp[1] = den;
         }
@@ -646,7 +646,7 @@ __global__ void __launch_bounds__(288, 1) k_pinn_chain_tc2(PinnTcArgs ta) {
       if (a.partials) {
         reduce256(num, den);
         if (t == 0) {
-          double *pp = a.partials + (((size_t)(ln + 1) * a.B + b) * a.nch + blockIdx.x) * 2;
+          double *pp = a.partials + (((size_t)(ln + 1) * a.B + b) * a.nch + blockIdx.x + a.cta0) * 2;
           pp[0] = num;
           pp[1] = den;
         }
@@ -734,17 +734,29 @@ static bool use_pingpong(bool bf16) {
   return bf16 && on != 0;
 }
 
+static bool tc_uses_pingpong(int W, int LH, int nfloats, bool bf16, bool *resident2, size_t *smem2) {
+  *smem2 = pinn_tc2_smem(W, LH, nfloats, resident2);
+  return use_pingpong(bf16) && *resident2 && (long)(LH - 1) * W * W >= 24576;
+}
+int pinn_tc_points_per_cta(int W, int LH, int nfloats, bool bf16) {
+  bool r2 = false;
+  size_t sm2 = 0;
+  return tc_uses_pingpong(W, LH, nfloats, bf16, &r2, &sm2) ? 256 : 128;
+}
+
+// grid.x: CTAs along j in units of pinn_tc_points_per_cta points (from CTA a.cta0 on)
 cudaError_t launch_pinn_tc(int IN, int W, int act, bool bf16, const PinnArgs &a, const void *wh, dim3 grid,
                            cudaStream_t s) {
   bool resident2 = false;
-  const size_t smem2 = pinn_tc2_smem(W, a.LH, a.nfloats, &resident2);
+  size_t smem2 = 0;
+  const bool pingpong = tc_uses_pingpong(W, a.LH, a.nfloats, bf16, &resident2, &smem2);
   // The ping-pong kernel when the weights stay resident (its two A planes leave room for a short
   // ring only): with streamed weights (8×256: 128 KB per layer and tile) both kernels are bound by
   // the weight traffic from L2 and the one-tile kernel, two CTAs per SM, is as fast (measured
   // 631 vs 610 M evals/s); with resident weights the ping-pong kernel is 1.86× faster (4×128)
   // (and only for nets with enough MMA work per slice to hide the second tile's epilogue: 4×64
   // measured 8.3 vs 9.3 G evals/s, 8×64 4.9 vs 3.5)
-  if (use_pingpong(bf16) && resident2 && (long)(a.LH - 1) * W * W >= 24576) {
+  if (pingpong) {
     TcKernel k2 = tc2_kernel(IN, W, act);
     if (!k2) return cudaErrorInvalidValue;
     const bool resident = resident2;
@@ -755,8 +767,7 @@ cudaError_t launch_pinn_tc(int IN, int W, int act, bool bf16, const PinnArgs &a,
     ta.g = a;
     ta.wh = wh;
     ta.resident = resident ? 1 : 0;
-    dim3 g2((a.M + 255) / 256, grid.y);  // two 128-point tiles per CTA
-    k2<<<g2, 288, smem, s>>>(ta);
+    k2<<<grid, 288, smem, s>>>(ta);  // two 128-point tiles per CTA
     return cudaGetLastError();
   }
   TcKernel k = tc_kernel(IN, W, act, bf16);

@@ -60,7 +60,7 @@ def _free_port():
     return port
 
 
-def _rank_main(rank, world, port, cfg, coarse, K, out_q):
+def _rank_main(rank, world, port, cfg, coarse, K, out_q, chunks=1):
     import torch
     import torch.distributed as dist
 
@@ -92,14 +92,49 @@ def _rank_main(rank, world, port, cfg, coarse, K, out_q):
         def send_last():
             dist.send(torch.from_numpy(U[per].reshape(-1).copy()), dst=rank + 1)
 
+        def chain(P, k, lo=0, hi=None):
+            """G chain over local slices, grid points [lo, hi) only (G is pointwise in S)."""
+            hi = M if hi is None else hi
+            if k > 0 and P["copy"]:
+                U[P["chain_lo"], :, lo:hi] = Fk[:, lo:hi]
+            for l in range(P["chain_lo"], P["chain_hi"]):
+                g = G(n0 + l, U[l])[:, lo:hi]
+                U[l + 1, :, lo:hi] = g + D[l, :, lo:hi] if k > 0 else g
+                Gh[l, :, lo:hi] = g
+
+        def exchange(P, k, run):
+            """The chain with its hand-offs: blocking, or the NEXT-2 wavefront of j-chunks (the
+            product's PR_OPT_WAVEFRONT schedule: per chunk q, send chunk q-1 of U_{n1} and receive
+            chunk q of U_{n0} as one group, chain chunk q; finally send the last chunk)."""
+            if chunks <= 1:
+                if P["recv_first"]:
+                    recv0()
+                if run:
+                    chain(P, k)
+                if P["send_last"]:
+                    send_last()
+                return
+            bnd = [q * M // chunks for q in range(chunks + 1)]
+            for q in range(chunks):
+                reqs = []
+                if q > 0 and P["send_last"]:
+                    reqs.append(dist.isend(torch.from_numpy(U[per, :, bnd[q - 1]:bnd[q]].copy().reshape(-1)),
+                                           dst=rank + 1))
+                if P["recv_first"]:
+                    t = torch.zeros(B * (bnd[q + 1] - bnd[q]), dtype=torch.float64)
+                    reqs.append(dist.irecv(t, src=rank - 1))
+                for rq in reqs:
+                    rq.wait()
+                if P["recv_first"]:
+                    U[0, :, bnd[q]:bnd[q + 1]] = t.numpy().reshape(B, -1)
+                if run:
+                    chain(P, k, bnd[q], bnd[q + 1])
+            if P["send_last"]:
+                dist.send(torch.from_numpy(U[per, :, bnd[-2]:bnd[-1]].copy().reshape(-1)), dst=rank + 1)
+
+        Fk = None
         P0 = parareal.plan_iteration(N, world, rank, 0)
-        if P0["recv_first"]:
-            recv0()
-        for l in range(P0["chain_lo"], P0["chain_hi"]):
-            Gh[l] = G(n0 + l, U[l])
-            U[l + 1] = Gh[l]
-        if P0["send_last"]:
-            send_last()
+        exchange(P0, 0, True)
         deltas = []
         for k in range(1, K + 1):
             P = parareal.plan_iteration(N, world, rank, k)
@@ -111,17 +146,7 @@ def _rank_main(rank, world, port, cfg, coarse, K, out_q):
                     Fk = Fh
                 else:
                     D[l] = Fh - Gh[l]
-            if P["recv_first"]:
-                recv0()
-            if P["copy"]:
-                U[P["chain_lo"]] = Fk
-            if P["copy"] or P["recv_first"]:
-                for l in range(P["chain_lo"], P["chain_hi"]):
-                    g = G(n0 + l, U[l])
-                    U[l + 1] = g + D[l]
-                    Gh[l] = g
-            if P["send_last"]:
-                send_last()
+            exchange(P, k, P["copy"] or P["recv_first"])
             dk = 0.0
             for l in range(P["delta_lo"], P["delta_hi"] + 1):
                 for b in range(B):
@@ -147,9 +172,10 @@ def _rank_main(rank, world, port, cfg, coarse, K, out_q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,coarse", [(2, synth.COARSE_IMPLICIT_EULER), (2, synth.COARSE_PINN),
-                                          (4, synth.COARSE_IMPLICIT_EULER)])
-def test_sharded_schedule_matches_serial_oracle(world, coarse):
+@pytest.mark.parametrize("world,coarse,chunks", [(2, synth.COARSE_IMPLICIT_EULER, 1), (2, synth.COARSE_PINN, 1),
+                                                 (4, synth.COARSE_IMPLICIT_EULER, 1), (2, synth.COARSE_PINN, 3),
+                                                 (4, synth.COARSE_PINN, 5)])
+def test_sharded_schedule_matches_serial_oracle(world, coarse, chunks):
     import torch.multiprocessing as mp
 
     import oracle
@@ -157,7 +183,7 @@ def test_sharded_schedule_matches_serial_oracle(world, coarse):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_rank_main, args=(r, world, port, cfg, coarse, K, q)) for r in range(world)]
+    procs = [ctx.Process(target=_rank_main, args=(r, world, port, cfg, coarse, K, q, chunks)) for r in range(world)]
     for pr in procs:
         pr.start()
     final, deltas = q.get(timeout=300)

@@ -15,13 +15,15 @@ from paper_2303_03848_b200 import parareal, synth
 pytestmark = pytest.mark.gpu
 
 
-def solve_ranks(p, net, world, key):
+def solve_ranks(p, net, world, key, opts=None, precision=parareal.PREC_FP32):
     nid = b"PRLOOPBK" + key.ljust(120, b"\0")
     ctxs = [parareal.Context(p, rank=r, world=world, device=0, nccl_id=nid) for r in range(world)]
     try:
         for c in ctxs:
             if net is not None:
-                c.load_weights(net)
+                c.load_weights(net, precision=precision)
+            for k, v in (opts or {}).items():
+                c.set_option(k, v)
         outs, reps, its, errs = [None] * world, [None] * world, [None] * world, []
 
         def work(r):
@@ -74,3 +76,36 @@ def test_multirank_matches_one_rank(name, world):
     per = p.N // world
     for r in range(world):
         assert np.array_equal(its[r], it_ref[r * per:(r + 1) * per + 1]), "rank %d iterates" % r
+
+
+@pytest.mark.parametrize("case,world,chunks", [("c2", 2, 3), ("c2", 4, 5), ("c2", 4, 64), ("big", 2, 0), ("big", 4, 0),
+                                               ("tc", 2, 3)])
+def test_chain_wavefront_matches_one_rank(case, world, chunks):
+    """NEXT-2 across ranks: the PINN chain as a wavefront of j-chunks (PR_OPT_WAVEFRONT; 0 = auto,
+    8 chunks at M >= 65536).  Every chunk is a CTA range of the same kernel, so output, every
+    rank's iterates and δ are bitwise the one-rank (and the blocking multi-rank) solve's."""
+    prec = parareal.PREC_FP32
+    if case == "c2":
+        p = synth.single(1024, 32, coarse=synth.COARSE_PINN, max_iter=3, tol=0.0)
+        net = synth.kaiming_net(synth.PINN_3x20, seed=1)
+    elif case == "big":
+        p = synth.single(1 << 16, 8, coarse=synth.COARSE_PINN, max_iter=2, tol=0.0, fine_steps=4)
+        net = synth.kaiming_net(synth.PINN_3x20, seed=3)
+    else:  # tensor-core chain (K4, split fp16)
+        p = synth.single(3000, 8, coarse=synth.COARSE_PINN, max_iter=2, tol=0.0, fine_steps=10)
+        net, prec = synth.kaiming_net([4, 64, 64, 64, 1], seed=4), parareal.PREC_FP16_TC
+    with parareal.Context(p) as c:
+        c.load_weights(net, precision=prec)
+        c.set_option(parareal.OPT_PIPELINE, 1)
+        ref, rref = c.solve()
+        it_ref = c.copy_iterates(0, p.N + 1)
+    key = ("wave-%s-%d-%d" % (case, world, chunks)).encode()
+    out, reps, its = solve_ranks(p, net, world, key, {parareal.OPT_WAVEFRONT: chunks}, prec)
+    _, breps, _ = solve_ranks(p, net, world, key + b"b", {parareal.OPT_WAVEFRONT: 1}, prec)
+    assert np.array_equal(out, ref)
+    assert np.array_equal(reps[0]["delta"], rref["delta"])
+    per = p.N // world
+    for r in range(world):
+        assert np.array_equal(its[r], it_ref[r * per:(r + 1) * per + 1]), "rank %d iterates" % r
+    # the wavefront really ran: more (chunked) chain launches than the blocking schedule
+    assert reps[-1]["kernel_launches"] > breps[-1]["kernel_launches"]
