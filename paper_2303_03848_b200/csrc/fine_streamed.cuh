@@ -256,13 +256,14 @@ __device__ __forceinline__ void warp_scan(double (&A)[SP], double &B, double (&e
   const int sl = D == 0 ? lane : 31 - lane;
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
+    // lanes without a predecessor at distance d keep their map: coefficient 0 / factor 1 instead
+    // of a select per value (fma(0, finite, A) = A exactly)
+    const bool has = sl >= d;
     const double pB = shfl_prev<D>(B, d);
+    const double Bm = has ? B : 0.0;
 #pragma unroll
-    for (int q = 0; q < SP; ++q) {
-      const double pA = shfl_prev<D>(A[q], d);
-      if (sl >= d) A[q] = fma(B, pA, A[q]);
-    }
-    if (sl >= d) B *= pB;
+    for (int q = 0; q < SP; ++q) A[q] = fma(Bm, shfl_prev<D>(A[q], d), A[q]);
+    B *= has ? pB : 1.0;
   }
   eB = shfl_prev<D>(B, 1);
 #pragma unroll
@@ -281,10 +282,9 @@ __device__ __forceinline__ void compose_window(double &mA, double &mB, int lane)
   for (int d = 1; d < 32; d <<= 1) {
     const double oA = __shfl_down_sync(0xffffffffu, mA, d);
     const double oB = __shfl_down_sync(0xffffffffu, mB, d);
-    if ((lane & (2 * d - 1)) == 0) {
-      mA = fma(mB, oA, mA);
-      mB *= oB;
-    }
+    const bool take = (lane & (2 * d - 1)) == 0;  // masked as in warp_scan (bitwise the same)
+    mA = fma(take ? mB : 0.0, oA, mA);
+    mB *= take ? oB : 1.0;
   }
 }
 

@@ -17,7 +17,7 @@ import numpy as np
 from . import synth
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libparareal.so")
+LIB_PATH = os.environ.get("PR_LIB_VARIANT") or os.path.join(_HERE, "libparareal.so")  # variant: A/B experiments only
 
 PR_OK = 0
 STATUS = {0: "PR_OK", 1: "PR_ERR_INVALID_ARGUMENT", 2: "PR_ERR_OUT_OF_MEMORY", 3: "PR_ERR_CUDA",
