@@ -65,13 +65,16 @@ enum { PR_COARSE_PINN = 0, PR_COARSE_IMPLICIT_EULER = 1 };
 enum { PR_BC_CALL_ASYMPTOTIC = 0, PR_BC_ZERO = 1 };
 /* hidden-layer activation: tanh (north_star) or ReLU */
 enum { PR_ACT_TANH = 0, PR_ACT_RELU = 1 };
-/* PINN arithmetic: fp32 SIMT (parity 1e-5) or tensor cores (parity 1e-3; not in ABI v1 builds) */
-/* PINN arithmetic.  FP32: fp32 SIMT kernels (any width instantiated: 8,16,20,32,50,64).
- * FP16_TC: tcgen05 tensor cores (K4), hidden widths 64/128/256 with >= 2 hidden layers; operands
- *   split hi + lo in fp16 and three MMAs per product, fp32 accumulation: fp32-level accuracy.
- * BF16_TC: the same kernel with one bf16 pass: ~3x faster, error ~1e-2 growing with depth.
- * TF32_TC: not in this build (PR_ERR_UNSUPPORTED). */
-enum { PR_PREC_FP32 = 0, PR_PREC_FP16_TC = 1, PR_PREC_BF16_TC = 2, PR_PREC_TF32_TC = 3 };
+/* PINN arithmetic.  FP32: fp32 SIMT kernels (any width instantiated: 8,16,20,32,50,64), parity 1e-5.
+ * The tensor-core modes (K4: tcgen05, hidden widths 64/128/256 with >= 2 hidden layers, fp32
+ * accumulation in TMEM; north_star's tensor-core tolerance is 1e-3):
+ * FP16_TC:   operands split hi + lo in fp16, three MMAs per product: fp32-level accuracy (1e-4 tests).
+ * FP16X1_TC: one fp16 pass (unit roundoff 2^-11 on [-1,1] activations), exact tanh: one MMA per
+ *            product; measured 3e-4 .. 4e-3 of the row maximum on random Kaiming nets,
+ *            8x finer than BF16_TC, but not within 1e-3 for every net: only FP16_TC is.
+ * BF16_TC:   one bf16 pass, tanh.approx: fastest, ~1e-2 (outside north_star's 1e-3; not credited).
+ * TF32_TC:   not in this build (PR_ERR_UNSUPPORTED). */
+enum { PR_PREC_FP32 = 0, PR_PREC_FP16_TC = 1, PR_PREC_BF16_TC = 2, PR_PREC_TF32_TC = 3, PR_PREC_FP16X1_TC = 4 };
 
 /* Problem statement.  Host pointers, copied by init. */
 typedef struct {

@@ -37,12 +37,14 @@ bool pinn_param_supported(int IN, int W, int LH, int act);
 cudaError_t launch_pinn_param(int IN, int W, int LH, int act, const float *pk, const PinnArgs &a, dim3 grid,
                               cudaStream_t s);
 // K4: PINN chain on tcgen05 tensor cores for wide nets (pinn_tc.cu); wts = compact fp32 params
-bool pinn_tc_supported(int IN, int W, int act, bool bf16);
-size_t pinn_tc_smem(int W, int LH, int nfloats, bool bf16, bool *resident);
-size_t pinn_tc_layer_elems(int W, bool bf16);
-void pinn_tc_pack(const float *Wl, int W, bool bf16, uint16_t *out);
-int pinn_tc_points_per_cta(int W, int LH, int nfloats, bool bf16);  // 256 (ping-pong kernel) or 128
-cudaError_t launch_pinn_tc(int IN, int W, int act, bool bf16, const PinnArgs &a, const void *wh, dim3 grid,
+// K4 operand modes: hi + lo fp16 (3 MMAs, fp32-level), one bf16 pass, one fp16 pass
+enum { kTcSplit16 = 0, kTcBF16 = 1, kTcF16 = 2 };
+bool pinn_tc_supported(int IN, int W, int act, int mode);
+size_t pinn_tc_smem(int W, int LH, int nfloats, int mode, bool *resident);
+size_t pinn_tc_layer_elems(int W, int mode);
+void pinn_tc_pack(const float *Wl, int W, int mode, uint16_t *out);
+int pinn_tc_points_per_cta(int W, int LH, int nfloats, int mode);  // 256 (ping-pong kernel) or 128
+cudaError_t launch_pinn_tc(int IN, int W, int act, int mode, const PinnArgs &a, const void *wh, dim3 grid,
                            cudaStream_t s);
 // Pipelined Parareal on one GPU (pipe.cu, NEXT-2): PINN chain (latency mode) and K1 fine solves
 // in one cooperative kernel, synchronised per slice.

@@ -581,6 +581,10 @@ cudaError_t dispatch_res(bool chain, int M, const pr::ResidentArgs &a, int nsys,
 // PR_OPT_PINN_KERNEL: 0 auto, 1 shared memory, 2 latency mode.
 constexpr long kSplitMaxPoints = 65536;
 constexpr long kGroupMaxPoints = 16384;
+// PR_PREC_*_TC → the K4 operand mode (pinn_tc.cu)
+int tc_mode(int precision) {
+  return precision == PR_PREC_FP16_TC ? pr::kTcSplit16 : precision == PR_PREC_BF16_TC ? pr::kTcBF16 : pr::kTcF16;
+}
 bool split_allowed(const pr_ctx *c) { return (long)c->B * c->M <= kSplitMaxPoints; }
 // 20-wide nets: in a problem the pipelined schedule can run (one GPU, fixed K, resident fine
 // kernel, M ≤ 1024) the 4-thread shuffle chain, whose 4-warp chain CTAs pack several per SM
@@ -636,7 +640,7 @@ pr::PinnArgs pinn_args(pr_ctx *c) {
 // arithmetic of the whole one, δ partial slots included).
 void pinn_geometry(const pr_ctx *c, int *ppc, int *gx) {
   int p;
-  if (c->tc) p = pr::pinn_tc_points_per_cta(c->W, c->LH, c->tc_nfloats, c->tc == PR_PREC_BF16_TC);
+  if (c->tc) p = pr::pinn_tc_points_per_cta(c->W, c->LH, c->tc_nfloats, tc_mode(c->tc));
   else if (use_split_pinn(c)) p = pr::pinn_split_ppc(split_G(c));
   else if (use_param_pinn(c)) p = kPinnTPB;
   else p = kPinnTPB * pr::pinn_smem_pts(c->W);
@@ -657,7 +661,7 @@ pr_status launch_pinn(pr_ctx *c, const pr::PinnArgs &a0, int cta_lo = 0, int cta
     pr::PinnArgs t = a;
     t.wts = c->d_tcp;
     t.nfloats = c->tc_nfloats;
-    LAUNCH(pr::launch_pinn_tc(c->IN, c->W, c->act, c->tc == PR_PREC_BF16_TC, t, c->d_wh, grid, c->stream));
+    LAUNCH(pr::launch_pinn_tc(c->IN, c->W, c->act, tc_mode(c->tc), t, c->d_wh, grid, c->stream));
     return PR_OK;
   }
   if (use_split_pinn(c)) {
@@ -1599,10 +1603,11 @@ pr_status parareal_load_pinn_weights(pr_ctx *c, int32_t n_linear, const int32_t 
     if (dims[l] != Wd) return fail(c, PR_ERR_UNSUPPORTED, fmt("dims[%d]=%d: hidden widths must all equal dims[1]=%d", l, dims[l], Wd));
   if (activation != PR_ACT_TANH && activation != PR_ACT_RELU)
     return fail(c, PR_ERR_INVALID_ARGUMENT, fmt("activation=%d unknown", activation));
-  if (precision < 0 || precision > PR_PREC_TF32_TC) return fail(c, PR_ERR_INVALID_ARGUMENT, fmt("precision=%d unknown", precision));
+  if (precision < 0 || precision > PR_PREC_FP16X1_TC) return fail(c, PR_ERR_INVALID_ARGUMENT, fmt("precision=%d unknown", precision));
   const bool tc = precision != PR_PREC_FP32;
-  if (precision == PR_PREC_TF32_TC) return fail(c, PR_ERR_UNSUPPORTED, "PR_PREC_TF32_TC is not in this build (FP16/BF16 tensor cores are)");
-  if (tc && (n_linear < 3 || !pr::pinn_tc_supported(dims[0], Wd, activation, precision == PR_PREC_BF16_TC)))
+  if (precision == PR_PREC_TF32_TC)
+    return fail(c, PR_ERR_UNSUPPORTED, "PR_PREC_TF32_TC is not in this build (PR_PREC_FP16X1_TC is the 1e-3 mode)");
+  if (tc && (n_linear < 3 || !pr::pinn_tc_supported(dims[0], Wd, activation, tc_mode(precision))))
     return fail(c, PR_ERR_UNSUPPORTED, fmt("tensor-core PINN needs >= 2 hidden layers of width 64, 128 or 256 (got %d x %d)",
                                            n_linear - 1, Wd));
   if (!tc && !pr::pinn_smem_supported(dims[0], Wd, activation))
@@ -1623,7 +1628,7 @@ pr_status parareal_load_pinn_weights(pr_ctx *c, int32_t n_linear, const int32_t 
   if (tc) {
     // K4: compact fp32 params (W0, b0, hidden biases, Wo, bo) + the hidden matrices in fp16/bf16,
     // core-matrix K-major (pinn_tc.cu)
-    const bool bf = precision == PR_PREC_BF16_TC;
+    const int bf = tc_mode(precision);
     // packed fp32 layout (pk): W0[W][IN], b0[W], {W_l[W][W], b_l[W]} x (LH−1), Wo[W], bo
     const size_t n0 = (size_t)Wd * IN, nh = (size_t)Wd * Wd + Wd;
     const size_t le = pr::pinn_tc_layer_elems(Wd, bf);

@@ -116,12 +116,14 @@ __device__ __forceinline__ float act_tc(float zs) {
 
 // SPLIT (PR_PREC_FP16_TC): operands split hi + lo in fp16, D = A_hi·B_hi + A_hi·B_lo + A_lo·B_hi —
 // fp32-level accuracy (~2e-6 on 8×256 nets) at 3× the MMAs.  !SPLIT (PR_PREC_BF16_TC): one bf16 pass.
-template <int IN, int W, int ACT, bool SPLIT>
+// H16 (with !SPLIT, PR_PREC_FP16X1_TC): one fp16 pass — fp16's 2^-11 unit roundoff is 8x finer than
+// bf16's for the [-1,1] activations and O(1) weights, at bf16's speed (exact tanh in the epilogue).
+template <int IN, int W, int ACT, bool SPLIT, bool H16>
 __global__ void __launch_bounds__(128) k_pinn_chain_tc(PinnTcArgs ta) {
-  using T = typename std::conditional<SPLIT, __half, __nv_bfloat16>::type;
+  using T = typename std::conditional<SPLIT || H16, __half, __nv_bfloat16>::type;
   constexpr int TILE = 128;
   constexpr int NP = SPLIT ? 2 : 1;                         // hi (+ lo) planes
-  constexpr uint32_t kIdesc = umma_idesc<!SPLIT>(TILE, W);
+  constexpr uint32_t kIdesc = umma_idesc<!(SPLIT || H16)>(TILE, W);
   constexpr uint32_t kPlaneA = (uint32_t)TILE * W * 2;       // bytes of one A plane
   constexpr uint32_t kPlaneB = (uint32_t)W * kTcKC * 2;      // bytes of one chunk plane
   constexpr uint32_t kChunk = NP * kPlaneB;
@@ -318,7 +320,7 @@ __global__ void __launch_bounds__(128) k_pinn_chain_tc(PinnTcArgs ta) {
         float v[32];
         tmem_ld32(tlane + (uint32_t)c0, v);
 #pragma unroll
-        for (int q = 0; q < 32; ++q) v[q] = act_tc<ACT, !SPLIT>(v[q] + bl[c0 + q]);
+        for (int q = 0; q < 32; ++q) v[q] = act_tc<ACT, !SPLIT && !H16>(v[q] + bl[c0 + q]);
         if (last) {
 #pragma unroll
           for (int q = 0; q < 32; ++q) y = fmaf(Wo[c0 + q], v[q], y);
@@ -389,11 +391,11 @@ __device__ __forceinline__ void tc_mbar_arrive(uint64_t *bar) {
 }
 __device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 
-template <int IN, int W, int ACT>
+template <int IN, int W, int ACT, bool H16>
 __global__ void __launch_bounds__(288, 1) k_pinn_chain_tc2(PinnTcArgs ta) {
-  using T = __nv_bfloat16;
+  using T = typename std::conditional<H16, __half, __nv_bfloat16>::type;
   constexpr int TILE = 128;
-  constexpr uint32_t kIdesc = umma_idesc<true>(TILE, W);
+  constexpr uint32_t kIdesc = umma_idesc<!H16>(TILE, W);
   constexpr uint32_t kPlaneA = (uint32_t)TILE * W * 2;
   constexpr uint32_t kChunk = (uint32_t)W * kTcKC * 2;
   constexpr int NCH = W / kTcKC;
@@ -605,7 +607,7 @@ __global__ void __launch_bounds__(288, 1) k_pinn_chain_tc2(PinnTcArgs ta) {
           float v[32];
           tmem_ld32(tlane + (uint32_t)c0, v);
 #pragma unroll
-          for (int q = 0; q < 32; ++q) v[q] = act_tc<ACT, true>(v[q] + bl[c0 + q]);
+          for (int q = 0; q < 32; ++q) v[q] = act_tc<ACT, !H16>(v[q] + bl[c0 + q]);
           if (last) {
 #pragma unroll
             for (int q = 0; q < 32; ++q) y = fmaf(Wo[c0 + q], v[q], y);
@@ -662,24 +664,28 @@ __global__ void __launch_bounds__(288, 1) k_pinn_chain_tc2(PinnTcArgs ta) {
 }
 
 typedef void (*TcKernel)(PinnTcArgs);
-template <bool SPLIT>
+template <bool SPLIT, bool H16>
 static TcKernel tc_kernel_t(int IN, int W, int act) {
   if (act != 0 && act != 1) return nullptr;
 #define PR_TC_CASE(IN_, W_)                                                       \
-  if (IN == IN_ && W == W_) return act ? k_pinn_chain_tc<IN_, W_, 1, SPLIT> : k_pinn_chain_tc<IN_, W_, 0, SPLIT>;
+  if (IN == IN_ && W == W_)                                                       \
+    return act ? k_pinn_chain_tc<IN_, W_, 1, SPLIT, H16> : k_pinn_chain_tc<IN_, W_, 0, SPLIT, H16>;
   PR_TC_CASE(4, 64) PR_TC_CASE(4, 128) PR_TC_CASE(4, 256) PR_TC_CASE(2, 64) PR_TC_CASE(2, 128) PR_TC_CASE(2, 256)
 #undef PR_TC_CASE
   return nullptr;
 }
-static TcKernel tc_kernel(int IN, int W, int act, bool bf16) {
-  return bf16 ? tc_kernel_t<false>(IN, W, act) : tc_kernel_t<true>(IN, W, act);
+// mode: kTcSplit16 (hi + lo fp16, 3 MMAs), kTcBF16 (one bf16 pass), kTcF16 (one fp16 pass)
+static TcKernel tc_kernel(int IN, int W, int act, int mode) {
+  return mode == kTcSplit16 ? tc_kernel_t<true, true>(IN, W, act)
+         : mode == kTcBF16  ? tc_kernel_t<false, false>(IN, W, act)
+                            : tc_kernel_t<false, true>(IN, W, act);
 }
 
-bool pinn_tc_supported(int IN, int W, int act, bool bf16) { return tc_kernel(IN, W, act, bf16) != nullptr; }
+bool pinn_tc_supported(int IN, int W, int act, int mode) { return tc_kernel(IN, W, act, mode) != nullptr; }
 
 // shared memory: A planes [128 × W] + weight chunks (all if they fit, else one) + fp32 parameters
-size_t pinn_tc_smem(int W, int LH, int nfloats, bool bf16, bool *resident) {
-  const size_t np = bf16 ? 1 : 2;
+size_t pinn_tc_smem(int W, int LH, int nfloats, int mode, bool *resident) {
+  const size_t np = mode == kTcSplit16 ? 2 : 1;
   const size_t a = np * 128 * W * 2, chunk = np * (size_t)W * kTcKC * 2, p = (size_t)nfloats * 4;
   const size_t all = (size_t)(LH - 1) * (W / kTcKC) * chunk;
   const size_t limit = 200 * 1024;
@@ -693,17 +699,20 @@ size_t pinn_tc_smem(int W, int LH, int nfloats, bool bf16, bool *resident) {
 
 // host: hidden layer l's [W][W] (fp32, pre-scaled) → its W/64 K-chunks, each [hi plane][lo plane],
 // a plane [W rows × 64 K] in the core-matrix K-major layout (SBO = 1024 B)
-size_t pinn_tc_layer_elems(int W, bool bf16) { return (size_t)(bf16 ? 1 : 2) * W * W; }
-void pinn_tc_pack(const float *Wl, int W, bool bf16, uint16_t *out) {
-  const int np = bf16 ? 1 : 2;
+size_t pinn_tc_layer_elems(int W, int mode) { return (size_t)(mode == kTcSplit16 ? 2 : 1) * W * W; }
+void pinn_tc_pack(const float *Wl, int W, int mode, uint16_t *out) {
+  const int np = mode == kTcSplit16 ? 2 : 1;
   for (int c = 0; c < W / kTcKC; ++c) {
     uint16_t *hi = out + (size_t)c * np * W * kTcKC, *lo = hi + (size_t)W * kTcKC;
     for (int o = 0; o < W; ++o)
       for (int i = 0; i < kTcKC; ++i) {
         const float v = Wl[(size_t)o * W + c * kTcKC + i];
         const size_t off = cm_offset(o, i, kTcKC);
-        if (bf16) {
+        if (mode == kTcBF16) {
           const __nv_bfloat16 h = __float2bfloat16_rn(v);
+          hi[off] = *reinterpret_cast<const uint16_t *>(&h);
+        } else if (mode == kTcF16) {
+          const __half h = __float2half_rn(v);
           hi[off] = *reinterpret_cast<const uint16_t *>(&h);
         } else {
           const __half h = __float2half_rn(v);
@@ -716,12 +725,16 @@ void pinn_tc_pack(const float *Wl, int W, bool bf16, uint16_t *out) {
 }
 
 // ping-pong kernel (bf16): two A planes; weights resident when they fit, else the 2-chunk ring
-static TcKernel tc2_kernel(int IN, int W, int act) {
+template <bool H16>
+static TcKernel tc2_kernel_t(int IN, int W, int act) {
 #define PR_TC2_CASE(IN_, W_) \
-  if (IN == IN_ && W == W_) return act ? k_pinn_chain_tc2<IN_, W_, 1> : k_pinn_chain_tc2<IN_, W_, 0>;
+  if (IN == IN_ && W == W_) return act ? k_pinn_chain_tc2<IN_, W_, 1, H16> : k_pinn_chain_tc2<IN_, W_, 0, H16>;
   PR_TC2_CASE(4, 64) PR_TC2_CASE(4, 128) PR_TC2_CASE(4, 256) PR_TC2_CASE(2, 64) PR_TC2_CASE(2, 128) PR_TC2_CASE(2, 256)
 #undef PR_TC2_CASE
   return nullptr;
+}
+static TcKernel tc2_kernel(int IN, int W, int act, int mode) {
+  return mode == kTcF16 ? tc2_kernel_t<true>(IN, W, act) : tc2_kernel_t<false>(IN, W, act);
 }
 static size_t pinn_tc2_smem(int W, int LH, int nfloats, bool *resident) {
   const size_t a = 2 * 128 * (size_t)W * 2, chunk = (size_t)W * kTcKC * 2, p = (size_t)nfloats * 4;
@@ -729,27 +742,27 @@ static size_t pinn_tc2_smem(int W, int LH, int nfloats, bool *resident) {
   *resident = a + all + p <= 200 * 1024;
   return *resident ? a + all + p : a + kTc2Ring * chunk + p;
 }
-static bool use_pingpong(bool bf16) {
+static bool use_pingpong(int mode) {  // the single-pass modes
   static const int on = getenv("PR_TC_PINGPONG") ? atoi(getenv("PR_TC_PINGPONG")) : 1;
-  return bf16 && on != 0;
+  return mode != kTcSplit16 && on != 0;
 }
 
-static bool tc_uses_pingpong(int W, int LH, int nfloats, bool bf16, bool *resident2, size_t *smem2) {
+static bool tc_uses_pingpong(int W, int LH, int nfloats, int mode, bool *resident2, size_t *smem2) {
   *smem2 = pinn_tc2_smem(W, LH, nfloats, resident2);
-  return use_pingpong(bf16) && *resident2 && (long)(LH - 1) * W * W >= 24576;
+  return use_pingpong(mode) && *resident2 && (long)(LH - 1) * W * W >= 24576;
 }
-int pinn_tc_points_per_cta(int W, int LH, int nfloats, bool bf16) {
+int pinn_tc_points_per_cta(int W, int LH, int nfloats, int mode) {
   bool r2 = false;
   size_t sm2 = 0;
-  return tc_uses_pingpong(W, LH, nfloats, bf16, &r2, &sm2) ? 256 : 128;
+  return tc_uses_pingpong(W, LH, nfloats, mode, &r2, &sm2) ? 256 : 128;
 }
 
 // grid.x: CTAs along j in units of pinn_tc_points_per_cta points (from CTA a.cta0 on)
-cudaError_t launch_pinn_tc(int IN, int W, int act, bool bf16, const PinnArgs &a, const void *wh, dim3 grid,
+cudaError_t launch_pinn_tc(int IN, int W, int act, int mode, const PinnArgs &a, const void *wh, dim3 grid,
                            cudaStream_t s) {
   bool resident2 = false;
   size_t smem2 = 0;
-  const bool pingpong = tc_uses_pingpong(W, a.LH, a.nfloats, bf16, &resident2, &smem2);
+  const bool pingpong = tc_uses_pingpong(W, a.LH, a.nfloats, mode, &resident2, &smem2);
   // The ping-pong kernel when the weights stay resident (its two A planes leave room for a short
   // ring only): with streamed weights (8×256: 128 KB per layer and tile) both kernels are bound by
   // the weight traffic from L2 and the one-tile kernel, two CTAs per SM, is as fast (measured
@@ -757,7 +770,7 @@ cudaError_t launch_pinn_tc(int IN, int W, int act, bool bf16, const PinnArgs &a,
   // (and only for nets with enough MMA work per slice to hide the second tile's epilogue: 4×64
   // measured 8.3 vs 9.3 G evals/s, 8×64 4.9 vs 3.5)
   if (pingpong) {
-    TcKernel k2 = tc2_kernel(IN, W, act);
+    TcKernel k2 = tc2_kernel(IN, W, act, mode);
     if (!k2) return cudaErrorInvalidValue;
     const bool resident = resident2;
     const size_t smem = smem2;
@@ -770,10 +783,10 @@ cudaError_t launch_pinn_tc(int IN, int W, int act, bool bf16, const PinnArgs &a,
     k2<<<grid, 288, smem, s>>>(ta);  // two 128-point tiles per CTA
     return cudaGetLastError();
   }
-  TcKernel k = tc_kernel(IN, W, act, bf16);
+  TcKernel k = tc_kernel(IN, W, act, mode);
   if (!k) return cudaErrorInvalidValue;
   bool resident = false;
-  const size_t smem = pinn_tc_smem(W, a.LH, a.nfloats, bf16, &resident);
+  const size_t smem = pinn_tc_smem(W, a.LH, a.nfloats, mode, &resident);
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   PinnTcArgs ta;
