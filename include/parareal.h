@@ -223,13 +223,19 @@ enum {
                                this many milliseconds (a peer rank that died or hangs), aborts the
                                communicator and poisons the context (PR_ERR_NCCL) instead of hanging.
                                Default 600000; 0 waits forever.  No effect with world == 1. */
-  PR_OPT_WAVEFRONT = 6       /* world > 1, PINN G, B == 1: the coarse chain runs as a wavefront of j-chunks
+  PR_OPT_WAVEFRONT = 6,      /* world > 1, PINN G, B == 1: the coarse chain runs as a wavefront of j-chunks
                                across ranks (G is pointwise in S): each chunk of U_{n1} goes
                                to the next rank as soon as it is chained, so the ranks chain concurrently.
                                Results are bitwise those of the blocking chain (the chunks are CTA ranges
                                of the same kernel).  0 auto (8 chunks when M ≥ 65536, else blocking),
                                1 blocking, n ≥ 2: n chunks (at most one per CTA).  Numerical G (coupled in
                                S) and B > 1 always chain blocking. */
+  PR_OPT_SPATIAL_CHAIN = 7   /* world > 1, PINN G, B == 1: every rank chains ALL slices over
+                               its own range of grid points (G is pointwise in S) while the fine sweep
+                               stays sharded by slices; per iteration U/Ĝ rows go to the slice owners and
+                               D rows (+ F̂_{k−1}) back, δ's partial slots are summed over ranks.  Bitwise
+                               the one-rank results.  0 auto (on for tensor-core nets, whose chain
+                               dominates), 1 off (slice-sharded chain / wavefront), 2 on. */
 };
 pr_status parareal_set_option(pr_ctx *ctx, int32_t key, int64_t value);
 

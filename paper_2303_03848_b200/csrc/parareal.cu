@@ -15,6 +15,8 @@
 #include <cstdio>
 #include <condition_variable>
 #include <cstring>
+#include <deque>
+#include <functional>
 #include <map>
 #include <mutex>
 #include <string>
@@ -30,7 +32,7 @@ namespace {
 typedef struct ncclComm *ncclComm_t;
 typedef struct { char internal[128]; } ncclUniqueId;
 typedef int ncclResult_t;
-enum { kNcclFloat32 = 7, kNcclFloat64 = 8, kNcclMax = 2, kNcclInProgress = 7 /* ncclResult_t */ };
+enum { kNcclFloat32 = 7, kNcclFloat64 = 8, kNcclSum = 0, kNcclMax = 2, kNcclInProgress = 7 /* ncclResult_t */ };
 
 struct Nccl {
   bool tried = false, ok = false;
@@ -162,6 +164,10 @@ struct pr_ctx {
   int opt_pipeline = 0;  // 0 auto, 1 off (PR_OPT_PIPELINE)
   int64_t comm_timeout_ms = 600000;  // PR_OPT_COMM_TIMEOUT_MS (0: wait forever)
   int opt_wavefront = 0;             // PR_OPT_WAVEFRONT: 0 auto, 1 blocking chain, n ≥ 2 chunks
+  int opt_spatial = 0;               // PR_OPT_SPATIAL_CHAIN: 0 auto, 1 off, 2 on
+  // spatially sharded chain (NEXT-4): every slice's rows, this rank's j-range meaningful
+  float *sp_U = nullptr, *sp_Gh = nullptr, *sp_D = nullptr, *sp_F = nullptr;
+  double *sp_part = nullptr;
   bool capturing = false;
   // pipelined schedule (pipe.cu): per-iteration δ partials and the slice counters
   double *pipe_partials = nullptr;
@@ -761,11 +767,13 @@ struct LoopGroup {
   int world = 0, refs = 0;
   std::mutex mu;
   std::condition_variable cv;
-  std::vector<void *> box;  // [src·world + dst] device mailbox
-  std::vector<size_t> box_bytes;
-  std::vector<int> full;
+  // [src·world + dst] FIFO of device messages: a send never blocks (like NCCL's grouped p2p, any
+  // number of messages may be in flight per pair), a receive takes the oldest
+  std::vector<std::deque<std::pair<void *, size_t>>> box;
   std::vector<unsigned long long> vals;  // all-reduce contributions (bit patterns of doubles ≥ 0)
   unsigned long long result = 0;
+  std::vector<std::vector<double>> sums;  // SUM all-reduce contributions
+  std::vector<double> sum_result;
   int arrived = 0, gen = 0;
 };
 std::mutex g_loop_mu;
@@ -780,10 +788,9 @@ LoopGroup *loop_join(const uint8_t *id, int world) {
   if (!g) {
     g = new LoopGroup;
     g->world = world;
-    g->box.assign((size_t)world * world, nullptr);
-    g->box_bytes.assign((size_t)world * world, 0);
-    g->full.assign((size_t)world * world, 0);
+    g->box.assign((size_t)world * world, {});
     g->vals.assign(world, 0);
+    g->sums.assign(world, {});
   }
   if (g->world != world) return nullptr;
   g->refs++;
@@ -792,7 +799,8 @@ LoopGroup *loop_join(const uint8_t *id, int world) {
 void loop_leave(LoopGroup *g) {
   std::lock_guard<std::mutex> lk(g_loop_mu);
   if (--g->refs > 0) return;
-  for (void *b : g->box) cudaFree(b);
+  for (auto &q : g->box)
+    for (auto &m : q) cudaFree(m.first);
   for (auto it = g_loops.begin(); it != g_loops.end(); ++it)
     if (it->second == g) {
       g_loops.erase(it);
@@ -809,16 +817,11 @@ pr_status comm_send(pr_ctx *c, const float *buf, size_t count, int peer) {
   LoopGroup *g = c->loop;
   const size_t bytes = count * sizeof(float), idx = (size_t)c->rank * g->world + peer;
   SYNC();  // the row is complete
-  std::unique_lock<std::mutex> lk(g->mu);
-  g->cv.wait(lk, [&] { return !g->full[idx]; });
-  if (g->box_bytes[idx] < bytes) {
-    cudaFree(g->box[idx]);
-    g->box[idx] = nullptr;
-    CU(cudaMalloc(&g->box[idx], bytes));
-    g->box_bytes[idx] = bytes;
-  }
-  CU(cudaMemcpy(g->box[idx], buf, bytes, cudaMemcpyDeviceToDevice));
-  g->full[idx] = 1;
+  void *m = nullptr;
+  CU(cudaMalloc(&m, bytes ? bytes : 4));
+  CU(cudaMemcpy(m, buf, bytes, cudaMemcpyDeviceToDevice));
+  std::lock_guard<std::mutex> lk(g->mu);
+  g->box[idx].push_back({m, bytes});
   g->cv.notify_all();
   return PR_OK;
 }
@@ -830,11 +833,49 @@ pr_status comm_recv(pr_ctx *c, float *buf, size_t count, int peer) {
   LoopGroup *g = c->loop;
   const size_t bytes = count * sizeof(float), idx = (size_t)peer * g->world + c->rank;
   SYNC();  // earlier work reading buf is done
-  std::unique_lock<std::mutex> lk(g->mu);
-  g->cv.wait(lk, [&] { return g->full[idx] != 0; });
-  CU(cudaMemcpy(buf, g->box[idx], bytes, cudaMemcpyDeviceToDevice));
-  g->full[idx] = 0;
-  g->cv.notify_all();
+  std::pair<void *, size_t> m;
+  {
+    std::unique_lock<std::mutex> lk(g->mu);
+    g->cv.wait(lk, [&] { return !g->box[idx].empty(); });
+    m = g->box[idx].front();
+    g->box[idx].pop_front();
+  }
+  if (m.second != bytes) {
+    cudaFree(m.first);
+    return fail(c, PR_ERR_STATE, fmt("loopback message from rank %d has %zu bytes, expected %zu", peer, m.second, bytes));
+  }
+  CU(cudaMemcpy(buf, m.first, bytes, cudaMemcpyDeviceToDevice));
+  CU(cudaFree(m.first));
+  return PR_OK;
+}
+// SUM over ranks of `count` doubles in place (loopback: summed in rank order on the host)
+pr_status comm_allreduce_sum(pr_ctx *c, double *buf, size_t count) {
+  if (!c->loop) {
+    NC(nccl().AllReduce(buf, buf, count, kNcclFloat64, kNcclSum, c->comm, c->stream));
+    return PR_OK;
+  }
+  LoopGroup *g = c->loop;
+  std::vector<double> mine(count);
+  SYNC();
+  CU(cudaMemcpy(mine.data(), buf, count * sizeof(double), cudaMemcpyDeviceToHost));
+  std::vector<double> res;
+  {
+    std::unique_lock<std::mutex> lk(g->mu);
+    const int my_gen = g->gen;
+    g->sums[c->rank] = std::move(mine);
+    if (++g->arrived == g->world) {
+      g->sum_result.assign(count, 0.0);
+      for (int q = 0; q < g->world; ++q)
+        for (size_t i = 0; i < count; ++i) g->sum_result[i] += g->sums[q][i];
+      g->arrived = 0;
+      g->gen++;
+      g->cv.notify_all();
+    } else {
+      g->cv.wait(lk, [&] { return g->gen != my_gen; });
+    }
+    res = g->sum_result;
+  }
+  CU(cudaMemcpy(buf, res.data(), count * sizeof(double), cudaMemcpyHostToDevice));
   return PR_OK;
 }
 // MAX over ranks of one non-negative double held as its bit pattern (δ, reading Q13)
@@ -1187,6 +1228,215 @@ void drop_graph(pr_ctx *c) {
   c->g_v0 = nullptr;
 }
 
+// ---------------------------------------------------------------- NEXT-4: spatially sharded chain
+// PINN G is pointwise in S, so the coarse chain of iteration k can run on every rank at once, each
+// over ALL slices but only its own range of grid points (a CTA range of the same kernel), while the
+// fine sweep stays sharded by slices (it couples every point of a slice).  Per iteration two
+// exchanges convert between the layouts: the boundary states U^{k−1}_n and Ĝ_n of the active
+// slices go from the point owners to the slice owners (the fine epilogue forms D_n = F̂_n − Ĝ_n in
+// fp64, as on one rank), and D_n and F̂_{k−1} go back.  The δ partial slots (one per chain CTA)
+// are summed over ranks (each slot has one non-zero contributor: exact) and reduced as on one
+// rank.  Every rank's chain then takes t_chain/R instead of the wavefront's ≈ (1 + (R−1)/C)·t_chain/R
+// and the exchanges cost ≈ 2·N·M·4 B·(R−1)/R² per rank; results are bitwise the one-rank solve's.
+bool spatial_chain(const pr_ctx *c) {
+  if (c->world == 1 || c->coarse != PR_COARSE_PINN || c->B != 1 || c->opt_spatial == 1) return false;
+  return c->opt_spatial == 2 || c->tc != 0;  // auto: the tensor-core (wide) nets, whose chain dominates
+}
+
+struct SpGeom {
+  int ppc, gx;
+  std::vector<int> jlo, jhi, clo, chi;  // per rank: grid points and chain CTAs
+};
+SpGeom sp_geom(const pr_ctx *c) {
+  SpGeom g;
+  pinn_geometry(c, &g.ppc, &g.gx);
+  const int R = c->world;
+  for (int q = 0; q < R; ++q) {
+    const int a = (int)((long)q * g.gx / R), b = (int)((long)(q + 1) * g.gx / R);
+    g.clo.push_back(a);
+    g.chi.push_back(b);
+    g.jlo.push_back(std::min(a * g.ppc, c->M));
+    g.jhi.push_back(std::min(b * g.ppc, c->M));
+  }
+  return g;
+}
+
+// Rows [a, b] of the sharded buffers (sp_U / sp_Gh, this rank's point range) → the slice owners'
+// local rows (U / Gh), every owner receiving every rank's piece.  The owner of slices [n0, n1) holds
+// U rows n0..n1 and Gh rows n0..n1−1.  NCCL: one group; messages between a pair in ascending n.
+pr_status sp_to_owners(pr_ctx *c, const SpGeom &g, int a, int b, bool with_gh) {
+  const int R = c->world, r = c->rank, per = c->Nloc;
+  const size_t row = (size_t)c->Mp;
+  std::vector<std::function<pr_status()>> ops;  // sends first (loopback: non-blocking), then receives
+  std::vector<std::function<pr_status()>> rcv;
+  for (int n = a; n <= b; ++n) {
+    for (int o = 0; o < R; ++o) {  // owners holding row n of U: o = n / per (row n − n0) and o = n/per − 1 (row per)
+      const int n0 = o * per;
+      if (n < n0 || n > n0 + per) continue;
+      const int ln = n - n0;
+      for (int part = 0; part < (with_gh && n < n0 + per ? 2 : 1); ++part) {
+        const float *src = (part == 0 ? c->sp_U : c->sp_Gh) + (size_t)n * row;
+        float *dst = (part == 0 ? c->U : c->Gh) + (size_t)ln * row;
+        if (o == r) {
+          for (int q = 0; q < R; ++q) {
+            const size_t cnt = (size_t)(g.jhi[q] - g.jlo[q]);
+            if (!cnt) continue;
+            if (q == r)
+              ops.push_back([=]() -> pr_status {
+                CU(cudaMemcpyAsync(dst + g.jlo[q], src + g.jlo[q], cnt * sizeof(float), cudaMemcpyDeviceToDevice, c->stream));
+                return PR_OK;
+              });
+            else
+              rcv.push_back([=]() { return comm_recv(c, dst + g.jlo[q], cnt, q); });
+          }
+        } else {
+          const size_t cnt = (size_t)(g.jhi[r] - g.jlo[r]);
+          if (cnt) ops.push_back([=]() { return comm_send(c, src + g.jlo[r], cnt, o); });
+        }
+      }
+    }
+  }
+  if (!c->loop) NC(nccl().GroupStart());
+  pr_status st = PR_OK;
+  for (auto &f : ops)
+    if ((st = f())) break;
+  if (!st)
+    for (auto &f : rcv)
+      if ((st = f())) break;
+  if (!c->loop) NC(nccl().GroupEnd());
+  return st;
+}
+
+// This rank's fine outputs → the point owners: D_n (local rows of slices [lo, n1)) into sp_D, and
+// F̂_{k−1} (if this rank owns slice k−1) into sp_F on every rank.
+pr_status sp_from_owners(pr_ctx *c, const SpGeom &g, int k) {
+  const int R = c->world, r = c->rank, per = c->Nloc;
+  const size_t row = (size_t)c->Mp;
+  std::vector<std::function<pr_status()>> ops, rcv;
+  auto piece = [&](const float *src_row, float *dst_row, int owner) {  // every rank's range of one row
+    if (owner == r) {
+      for (int q = 0; q < R; ++q) {
+        const size_t cnt = (size_t)(g.jhi[q] - g.jlo[q]);
+        if (!cnt) continue;
+        if (q == r)
+          ops.push_back([=]() -> pr_status {
+            CU(cudaMemcpyAsync(dst_row + g.jlo[q], src_row + g.jlo[q], cnt * sizeof(float), cudaMemcpyDeviceToDevice, c->stream));
+            return PR_OK;
+          });
+        else
+          ops.push_back([=]() { return comm_send(c, src_row + g.jlo[q], cnt, q); });
+      }
+    } else {
+      const size_t cnt = (size_t)(g.jhi[r] - g.jlo[r]);
+      if (cnt) rcv.push_back([=]() { return comm_recv(c, dst_row + g.jlo[r], cnt, owner); });
+    }
+  };
+  for (int n = k - 1; n < c->N; ++n) {
+    const int o = n / per;
+    if (n == k - 1) piece(c->Fk, c->sp_F, o);
+    else piece(c->D + (size_t)(n - o * per) * row, c->sp_D + (size_t)n * row, o);
+  }
+  if (!c->loop) NC(nccl().GroupStart());
+  pr_status st = PR_OK;
+  for (auto &f : ops)
+    if ((st = f())) break;
+  if (!st)
+    for (auto &f : rcv)
+      if ((st = f())) break;
+  if (!c->loop) NC(nccl().GroupEnd());
+  return st;
+}
+
+pr_status sp_chain(pr_ctx *c, const SpGeom &g, int k) {
+  pr::PinnArgs a = pinn_args(c);
+  a.n_base = 0;  // global slice indices
+  a.ln0 = k;
+  a.ln1 = c->N;
+  a.U = c->sp_U;
+  a.Gh = c->sp_Gh;
+  a.D = k > 0 ? c->sp_D : nullptr;
+  a.Fcopy = k > 0 ? c->sp_F : nullptr;
+  a.partials = k > 0 ? c->sp_part : nullptr;
+  return launch_pinn(c, a, g.clo[c->rank], g.chi[c->rank]);
+}
+
+// Parareal with the spatially sharded chain (R > 1, B == 1).  Leaves U (local rows) and δ exactly
+// as the slice-sharded schedule does, so the gather of U_N and copy_iterates work unchanged.
+pr_status solve_spatial(pr_ctx *c, const float *V_T, bool device_ptr, PhaseTimer &pt, int &K, int &conv) {
+  const int N = c->N, r = c->rank;
+  const size_t row = (size_t)c->Mp, rows = (size_t)(N + 1) * row;
+  pr_status st;
+  if (!c->sp_U) {
+    CU(cudaMalloc(&c->sp_U, rows * sizeof(float)));
+    CU(cudaMalloc(&c->sp_Gh, rows * sizeof(float)));
+    CU(cudaMalloc(&c->sp_D, rows * sizeof(float)));
+    CU(cudaMalloc(&c->sp_F, row * sizeof(float)));
+    CU(cudaMalloc(&c->sp_part, (size_t)(N + 1) * c->nch * 2 * sizeof(double)));
+    CU(cudaMemsetAsync(c->sp_U, 0, rows * sizeof(float), c->stream));
+    CU(cudaMemsetAsync(c->sp_Gh, 0, rows * sizeof(float), c->stream));
+    CU(cudaMemsetAsync(c->sp_D, 0, rows * sizeof(float), c->stream));
+  }
+  const size_t npart = (size_t)(N + 1) * c->nch * 2;
+  const SpGeom g = sp_geom(c);
+  // U_0 from rank 0 (V_T or the payoff) to every rank's point range
+  pt.begin(PH_SETUP);
+  if (r == 0 && (st = load_initial(c, V_T, device_ptr))) return st;
+  {
+    std::vector<std::function<pr_status()>> ops, rcv;
+    for (int q = 0; q < c->world; ++q) {
+      const size_t cnt = (size_t)(g.jhi[q] - g.jlo[q]);
+      if (!cnt) continue;
+      if (r == 0 && q == 0) {
+        CU(cudaMemcpyAsync(c->sp_U + g.jlo[0], c->U + g.jlo[0], cnt * sizeof(float), cudaMemcpyDeviceToDevice, c->stream));
+      } else if (r == 0) {
+        if ((st = comm_send(c, c->U + g.jlo[q], cnt, q))) return st;
+      } else if (q == r) {
+        if ((st = comm_recv(c, c->sp_U + g.jlo[r], cnt, 0))) return st;
+      }
+    }
+  }
+  pt.end();
+  pt.begin(PH_COARSE);
+  if ((st = sp_chain(c, g, 0))) return st;  // k = 0: U_{n+1} = G(U_n), all slices, own points
+  pt.end();
+  for (int k = 1; k <= c->max_iter; ++k) {
+    const pr_plan P = make_plan(N, c->world, r, k);
+    pt.begin(PH_COMM);
+    if ((st = sp_to_owners(c, g, k - 1, N, true))) return st;  // U^{k−1}_n, Ĝ_n of the active slices
+    pt.end();
+    pt.begin(PH_FINE);
+    if (P.fine_hi > P.fine_lo && (st = fine_sweep(c, P.fine_lo, P.fk_local))) return st;
+    pt.end();
+    pt.begin(PH_COMM);
+    if ((st = sp_from_owners(c, g, k))) return st;  // D_n, F̂_{k−1} → point owners
+    pt.end();
+    pt.begin(PH_COARSE);
+    CU(cudaMemsetAsync(c->sp_part, 0, npart * sizeof(double), c->stream));
+    if ((st = sp_chain(c, g, k))) return st;
+    pt.end();
+    pt.begin(PH_COMM);
+    if ((st = comm_allreduce_sum(c, c->sp_part + (size_t)k * c->nch * 2, (size_t)(N + 1 - k) * c->nch * 2))) return st;
+    pt.end();
+    unsigned long long *slot = c->d_delta + (k - 1);
+    CU(cudaMemsetAsync(slot, 0, sizeof(unsigned long long), c->stream));
+    LAUNCH(pr::launch_delta(c->sp_part, c->B, c->nch, k, N, slot, c->stream));
+    K = k;
+    if (c->tol > 0.0) {
+      CU(cudaMemcpyAsync(c->h_delta + (k - 1), slot, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+      SYNC();
+      if (c->h_delta[k - 1] < c->tol) {
+        conv = 1;
+        break;
+      }
+    }
+  }
+  // the final iterate back into the slice owners' rows (U_N then reaches rank 0 as usual)
+  pt.begin(PH_COMM);
+  st = sp_to_owners(c, g, 0, N, false);
+  pt.end();
+  return st;
+}
+
 pr_status solve_impl(pr_ctx *c, const float *V_T, float *V_0, bool device_ptr, pr_report *rep) {
   pr_status st = check_ctx(c);
   if (st) return st;
@@ -1262,7 +1512,9 @@ pr_status solve_impl(pr_ctx *c, const float *V_T, float *V_0, bool device_ptr, p
       CU(cudaMemsetAsync(c->partials, 0, (size_t)(c->Nloc + 1) * c->B * c->nch * 2 * sizeof(double), c->stream));
     }
   }
-  if (!piped) {
+  if (!piped && spatial_chain(c)) {
+    if ((st = solve_spatial(c, V_T, device_ptr, pt, K, conv))) return st;
+  } else if (!piped) {
   {
     const pr_plan P0 = make_plan(c->N, R, r, 0);
     pt.begin(PH_COARSE);  // (with R > 1 this span includes the hand-offs of U_{n0} / U_{n1})
@@ -1871,6 +2123,10 @@ pr_status parareal_set_option(pr_ctx *c, int32_t key, int64_t value) {
       if (value < 0 || value > 4096) return fail(c, PR_ERR_INVALID_ARGUMENT, "PR_OPT_WAVEFRONT must be in [0, 4096]");
       c->opt_wavefront = (int)value;
       return PR_OK;
+    case PR_OPT_SPATIAL_CHAIN:
+      if (value < 0 || value > 2) return fail(c, PR_ERR_INVALID_ARGUMENT, "PR_OPT_SPATIAL_CHAIN must be 0, 1 or 2");
+      c->opt_spatial = (int)value;
+      return PR_OK;
     case PR_OPT_COMM_TIMEOUT_MS:
       if (value < 0) return fail(c, PR_ERR_INVALID_ARGUMENT, "PR_OPT_COMM_TIMEOUT_MS must be >= 0");
       c->comm_timeout_ms = value;
@@ -1902,6 +2158,11 @@ void parareal_free(pr_ctx *c) {
   if (c->own_ws) cudaFree(c->ws);
   if (c->h_delta) cudaFreeHost(c->h_delta);
   cudaFree(c->pipe_partials);
+  cudaFree(c->sp_U);
+  cudaFree(c->sp_Gh);
+  cudaFree(c->sp_D);
+  cudaFree(c->sp_F);
+  cudaFree(c->sp_part);
   cudaFree(c->pipe_flags);
   cudaFree(c->pipe_wstage);
   for (auto e : c->ev) cudaEventDestroy(e);

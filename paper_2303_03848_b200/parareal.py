@@ -23,7 +23,7 @@ PR_OK = 0
 STATUS = {0: "PR_OK", 1: "PR_ERR_INVALID_ARGUMENT", 2: "PR_ERR_OUT_OF_MEMORY", 3: "PR_ERR_CUDA",
           4: "PR_ERR_NCCL", 5: "PR_ERR_STATE", 6: "PR_ERR_NUMERICAL", 7: "PR_ERR_UNSUPPORTED"}
 PREC_FP32, PREC_FP16_TC, PREC_BF16_TC, PREC_TF32_TC, PREC_FP16X1_TC = 0, 1, 2, 3, 4
-OPT_FINE_KERNEL, OPT_USE_GRAPHS, OPT_PINN_KERNEL, OPT_PIPELINE, OPT_COMM_TIMEOUT_MS, OPT_WAVEFRONT = 1, 2, 3, 4, 5, 6
+OPT_FINE_KERNEL, OPT_USE_GRAPHS, OPT_PINN_KERNEL, OPT_PIPELINE, OPT_COMM_TIMEOUT_MS, OPT_WAVEFRONT, OPT_SPATIAL_CHAIN = 1, 2, 3, 4, 5, 6, 7
 
 # every symbol include/parareal.h declares (checked by tests/test_abi.py)
 EXPORTS = ["parareal_status_string", "parareal_last_error", "parareal_get_nccl_id", "parareal_init",

@@ -228,3 +228,114 @@ def test_nccl_id_broadcast():
     for pr in procs:
         pr.join(timeout=60)
     assert len(got[0]) == 128 and got[0] == got[1]
+
+
+def _spatial_main(rank, world, port, K, out_q):
+    """The NEXT-4 schedule (PR_OPT_SPATIAL_CHAIN) with the oracle's propagators: fine sweep sharded
+    by slices, the PINN chain of every slice sharded by grid points, rows changing owner twice per
+    iteration (gloo point-to-point), δ's per-slice sums added over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    import oracle
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        p = synth.config("C1", coarse=synth.COARSE_PINN, max_iter=K, tol=0.0)
+        net = synth.kaiming_net(synth.PINN_3x20, seed=0)
+        N, M = p.N, p.M
+        per = N // world
+        jb = [q * M // world for q in range(world + 1)]
+        lo, hi = jb[rank], jb[rank + 1]
+        owner = lambda n: n // per
+        Us = np.zeros((N + 1, M)); Ghs = np.zeros((N, M)); Ds = np.zeros((N, M)); Fs = np.zeros(M)
+        U = np.zeros((N + 1, M)); Gh = np.zeros((N, M)); D = np.zeros((N, M)); Fk = None
+        Us[0, lo:hi] = oracle.payoff(p)[0, lo:hi]
+
+        def move(rows, src, dst, frm_owner):
+            """rows: list of n.  frm_owner False: point owners → slice owner(n) (src sharded by
+            points); True: slice owner(n) → point owners."""
+            reqs, pend = [], []
+            for n in rows:
+                o = owner(min(n, N - 1))
+                for q in range(world):
+                    a, b = jb[q], jb[q + 1]
+                    s_, d_ = (o, q) if frm_owner else (q, o)
+                    if s_ == d_ == rank:
+                        dst[n, a:b] = src[n, a:b]
+                    elif s_ == rank:
+                        reqs.append(dist.isend(torch.from_numpy(src[n, a:b].copy()), dst=d_))
+                    elif d_ == rank:
+                        t = torch.zeros(b - a, dtype=torch.float64)
+                        reqs.append(dist.irecv(t, src=s_))
+                        pend.append((n, a, b, t))
+            for rq in reqs:
+                rq.wait()
+            for n, a, b, t in pend:
+                dst[n, a:b] = t.numpy()
+
+        def chain(k):
+            if k > 0:
+                Us[k, lo:hi] = Fs[lo:hi]
+            for n in range(k, N):
+                g = oracle.pinn_G(p, net, n, Us[n][None])[0, lo:hi]
+                Us[n + 1, lo:hi] = g + Ds[n, lo:hi] if k > 0 else g
+                Ghs[n, lo:hi] = g
+
+        chain(0)
+        deltas = []
+        for k in range(1, K + 1):
+            Uold = Us.copy()
+            move(range(k - 1, N), Us, U, False)
+            move(range(k - 1, N), Ghs, Gh, False)
+            for n in range(max(k - 1, rank * per), (rank + 1) * per):
+                Fh = oracle.fine(p, n, U[n][None])[0]
+                if n == k - 1:
+                    Fk = Fh
+                else:
+                    D[n] = Fh - Gh[n]
+            if Fk is not None and owner(k - 1) == rank:
+                Ftmp = np.zeros((N + 1, M)); Ftmp[k - 1] = Fk
+            else:
+                Ftmp = np.zeros((N + 1, M))
+            move([k - 1], Ftmp, Ftmp, True)
+            Fs[:] = Ftmp[k - 1]
+            move(range(k, N), D, Ds, True)
+            chain(k)
+            num = np.array([np.sum((Us[n, lo:hi] - Uold[n, lo:hi]) ** 2) for n in range(k, N + 1)])
+            den = np.array([np.sum(Us[n, lo:hi] ** 2) for n in range(k, N + 1)])
+            t = torch.from_numpy(np.concatenate([num, den]))
+            dist.all_reduce(t, op=dist.ReduceOp.SUM)
+            nn, dd = t.numpy()[:N + 1 - k], t.numpy()[N + 1 - k:]
+            deltas.append(float(np.max(np.sqrt(nn) / np.sqrt(dd))))
+        # U_N: every rank's point range (zeros elsewhere), summed = gathered
+        t = torch.from_numpy(np.where((np.arange(M) >= lo) & (np.arange(M) < hi), Us[N], 0.0))
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        final = t.numpy()
+        if rank == 0:
+            out_q.put((final, deltas))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_spatial_chain_schedule_matches_serial_oracle(world):
+    import torch.multiprocessing as mp
+
+    import oracle
+    K = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_spatial_main, args=(r, world, port, K, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    final, deltas = q.get(timeout=300)
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    p = synth.config("C1", coarse=synth.COARSE_PINN, max_iter=K, tol=0.0)
+    U, d, _, _ = oracle.parareal(p, synth.kaiming_net(synth.PINN_3x20, seed=0))
+    assert np.array_equal(final, U[-1][0])               # G pointwise: sharding points changes no arithmetic
+    assert np.allclose(deltas, d, rtol=1e-12, atol=0)    # (δ's sums are split over ranks: rounding only)

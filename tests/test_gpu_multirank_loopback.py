@@ -100,8 +100,9 @@ def test_chain_wavefront_matches_one_rank(case, world, chunks):
         ref, rref = c.solve()
         it_ref = c.copy_iterates(0, p.N + 1)
     key = ("wave-%s-%d-%d" % (case, world, chunks)).encode()
-    out, reps, its = solve_ranks(p, net, world, key, {parareal.OPT_WAVEFRONT: chunks}, prec)
-    _, breps, _ = solve_ranks(p, net, world, key + b"b", {parareal.OPT_WAVEFRONT: 1}, prec)
+    off = {parareal.OPT_SPATIAL_CHAIN: 1}  # (auto would shard the TC chain spatially instead)
+    out, reps, its = solve_ranks(p, net, world, key, {**off, parareal.OPT_WAVEFRONT: chunks}, prec)
+    _, breps, _ = solve_ranks(p, net, world, key + b"b", {**off, parareal.OPT_WAVEFRONT: 1}, prec)
     assert np.array_equal(out, ref)
     assert np.array_equal(reps[0]["delta"], rref["delta"])
     per = p.N // world
@@ -109,3 +110,34 @@ def test_chain_wavefront_matches_one_rank(case, world, chunks):
         assert np.array_equal(its[r], it_ref[r * per:(r + 1) * per + 1]), "rank %d iterates" % r
     # the wavefront really ran: more (chunked) chain launches than the blocking schedule
     assert reps[-1]["kernel_launches"] > breps[-1]["kernel_launches"]
+
+
+@pytest.mark.parametrize("case,world", [("c2", 2), ("c2", 4), ("tc", 2), ("tc", 4), ("tol", 2)])
+def test_spatial_chain_matches_one_rank(case, world):
+    """NEXT-4: the spatially sharded coarse chain (PR_OPT_SPATIAL_CHAIN; every rank chains all
+    slices over its own point range, the fine sweep stays slice-sharded, rows change owner twice
+    per iteration, δ slots summed over ranks).  Output, every rank's iterates, δ and K are bitwise
+    the one-rank solve's; "tc" runs the auto choice (on for tensor-core nets)."""
+    prec, opts = parareal.PREC_FP32, {parareal.OPT_SPATIAL_CHAIN: 2}
+    if case == "c2":
+        p = synth.single(1024, 32, coarse=synth.COARSE_PINN, max_iter=3, tol=0.0)
+        net = synth.kaiming_net(synth.PINN_3x20, seed=1)
+    elif case == "tc":
+        p = synth.single(3000, 8, coarse=synth.COARSE_PINN, max_iter=3, tol=0.0, fine_steps=10)
+        net, prec, opts = synth.kaiming_net([4, 128, 128, 128, 1], seed=4), parareal.PREC_FP16_TC, {}
+    else:  # a tolerance: the stop is decided from the δ every rank reduces from the summed slots
+        p = synth.single(256, 8, coarse=synth.COARSE_PINN, max_iter=8, tol=1e-3, fine_steps=10)
+        net = synth.kaiming_net([4, 16, 16, 1], seed=7)
+    with parareal.Context(p) as c:
+        c.load_weights(net, precision=prec)
+        c.set_option(parareal.OPT_PIPELINE, 1)
+        ref, rref = c.solve()
+        it_ref = c.copy_iterates(0, p.N + 1)
+    out, reps, its = solve_ranks(p, net, world, ("spatial-%s-%d" % (case, world)).encode(), opts, prec)
+    assert all(r["iterations"] == rref["iterations"] for r in reps)
+    assert np.array_equal(out, ref)
+    for r in reps:
+        assert np.array_equal(r["delta"], rref["delta"])
+    per = p.N // world
+    for r in range(world):
+        assert np.array_equal(its[r], it_ref[r * per:(r + 1) * per + 1]), "rank %d iterates" % r
