@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-c3-sweep", action="store_true", help="skip the C3 fine-sweep HBM roofline leg")
+    ap.add_argument("--no-training", action="store_true", help="skip the PINN-training leg (NEXT-3)")
     ap.add_argument("--no-graphs", action="store_true", help="eager launches instead of the captured CUDA graph")
     ap.add_argument("--pinn-width", type=int, default=20, help="PINN hidden width (C5 sweep: 20/64/256)")
     ap.add_argument("--pinn-layers", type=int, default=3, help="PINN hidden layers")
@@ -123,6 +124,21 @@ class Clocks:
         reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
                 "reasons": reasons, "samples": len(self.rows)}
+
+
+ALU = None
+
+
+def alu_peaks():
+    """fp64 / fp32 FMA peaks measured on this pool's B200 by scripts/peaks_microbench.cu
+    (profiles/r02/peaks.json); the nominal unit-count figure only if that file is missing."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02", "peaks.json")) as f:
+            d = json.load(f)
+        return {"fp64": float(d["fp64_fma_tflops"]), "fp32": float(d["fp32_fma_tflops"]),
+                "src": "measured (scripts/peaks_microbench.cu, profiles/r02/peaks.json)"}
+    except Exception:
+        return None
 
 
 def peaks():
@@ -239,17 +255,20 @@ def roofline(p, ph, K, world, rank, pk, pk_src, clk_mhz, n_sm, synth, dims=None,
                     "note": "latency-bound at this size: each implicit step is two dependent scans over "
                             "one system per CTA (0.5 us/step), one CTA per slice on 148 SMs; the fraction "
                             "of the fp64 pipe is small by construction (DESIGN.md 6, 11)",
-                    "achieved": 9.0 * pt_steps / sweep_s / 1e12, "peak": n_sm * 64 * 2 * clk_mhz * 1e6 / 1e12,
-                    "unit": "TFLOP/s", "peak_source": "fp64 pipe: %d SMs x 64 FMA/clk x 2 x %.0f MHz (DESIGN.md)"
-                    % (n_sm, clk_mhz), "work_per_unit": "9 fp64 flop per point-step", "launch_unit": "one sweep"}
+                    "achieved": 9.0 * pt_steps / sweep_s / 1e12,
+                    "peak": ALU["fp64"] if ALU else n_sm * 64 * 2 * clk_mhz * 1e6 / 1e12,
+                    "unit": "TFLOP/s", "peak_source": ALU["src"] if ALU else
+                    "fp64 pipe: %d SMs x 64 FMA/clk x 2 x %.0f MHz (nominal)" % (n_sm, clk_mhz),
+                    "work_per_unit": "9 fp64 flop per point-step", "launch_unit": "one sweep"}
             tr = ncu_traffic("k_parareal_pipe" if piped else "k_fine_sweep")
         else:
             kname = ("k_pass_res2 (K2, persistent paired streamed pass)" if p.fine_theta == 1.0
                      else "k_streamed_pass (K2, Crank-Nicolson tile pass)")
             roof = {"kernel": kname, "bound": "hbm",
-                    "achieved": 16.0 * pt_steps / sweep_s / 1e9,
+                    "achieved": 8.0 * pt_steps / sweep_s / 1e9,
                     "peak": float(pk["hbm_gbs"]), "unit": "GB/s", "peak_source": pk_src,
-                    "work_per_unit": "16 B per point-step", "launch_unit": "one pass (8 B per point)"}
+                    "work_per_unit": "8 B per point-step (SURVEY 8(d) algorithmic: one fp32 read + write; "
+                                     "the two-pass kernel moves 16)", "launch_unit": "one sweep"}
             tr = ncu_traffic("k_pass_res2" if p.fine_theta == 1.0 else "k_streamed_pass")
     else:
         evals = float(p.B) * p.M * nloc
@@ -267,15 +286,17 @@ def roofline(p, ph, K, world, rank, pk, pk_src, clk_mhz, n_sm, synth, dims=None,
             fl = pinn_flops(dims)
             roof = {"kernel": "k_pinn_chain* (K3, fp32 SIMT)", "bound": "alu",
                     "achieved": fl * evals / chain_s / 1e12,
-                    "peak": n_sm * 128 * 2 * clk_mhz * 1e6 / 1e12, "unit": "TFLOP/s",
-                    "peak_source": "fp32 FMA pipe: %d SMs x 128 FMA/clk x 2 x %.0f MHz (DESIGN.md)" % (n_sm, clk_mhz),
+                    "peak": ALU["fp32"] if ALU else n_sm * 128 * 2 * clk_mhz * 1e6 / 1e12, "unit": "TFLOP/s",
+                    "peak_source": ALU["src"] if ALU else
+                    "fp32 FMA pipe: %d SMs x 128 FMA/clk x 2 x %.0f MHz (nominal)" % (n_sm, clk_mhz),
                     "work_per_unit": "%.0f flop + %d tanh per point-eval" % (fl, sum(dims[1:-1])),
                     "launch_unit": "one coarse chain"}
             tr = ncu_traffic("k_pinn_chain")
         else:
             roof = {"kernel": "k_resident_chain (numerical G, fp64)", "bound": "alu",
                     "achieved": 9.0 * evals * p.coarse_steps / chain_s / 1e12,
-                    "peak": n_sm * 64 * 2 * clk_mhz * 1e6 / 1e12, "unit": "TFLOP/s", "peak_source": "fp64 pipe",
+                    "peak": ALU["fp64"] if ALU else n_sm * 64 * 2 * clk_mhz * 1e6 / 1e12, "unit": "TFLOP/s",
+                    "peak_source": ALU["src"] if ALU else "fp64 pipe (nominal)",
                     "work_per_unit": "9 fp64 flop per point-step", "launch_unit": "one coarse chain"}
             tr = ncu_traffic("k_resident_chain")
     roof["frac"] = roof["achieved"] / roof["peak"]
@@ -302,15 +323,65 @@ def c3_fine_sweep_roofline(parareal, synth, torch, stream, pk, pk_src, flush):
             ms.append(ctx.solve_device(out)["ms_fine"])
         t = statistics.median(ms) / 1e3
         pt_steps = float(p.M) * p.N * p.fine_steps
-        ach = 16.0 * pt_steps / t / 1e9
+        ach = 8.0 * pt_steps / t / 1e9
         tr = ncu_traffic("k_pass_res2")
         return {"kernel": "k_pass_res2 (K2, persistent paired streamed pass)", "workload": "C3 fine sweep: 64 slices x 2^20 points x 100 IE steps",
                 "bound": "hbm", "achieved": ach, "peak": float(pk["hbm_gbs"]), "unit": "GB/s",
                 "frac": ach / float(pk["hbm_gbs"]), "peak_source": pk_src, "ms_per_sweep": t * 1e3,
-                "point_steps_per_s": pt_steps / t, "work_per_unit": "16 B per point-step (fp32 read+write, 2 passes)",
-                "traffic": tr["dram_bytes_per_launch"] if tr else None}
+                "point_steps_per_s": pt_steps / t,
+                "work_per_unit": "8 B per point-step (SURVEY 8(d) algorithmic, single-pass design)",
+                "moved_bytes_frac": 2.0 * ach / float(pk["hbm_gbs"]),
+                "moved_bytes_basis": "16 B per point-step: the two-pass kernel reads and writes fp32 state in both passes",
+                "traffic": tr["dram_bytes_per_launch"] if tr else None,
+                "traffic_unit": "bytes per pass launch (ncu dram read+write; one pass = 8 B per point)"}
     finally:
         ctx.close()
+
+
+def training_run(synth):
+    """The paper's PINN training (P:190 collocation counts: 5000 epochs at 1e-2 then 800
+    at 1e-3, shuffled batches of 10 per epoch) of the 3x20 tanh net for the C2 market on this GPU,
+    timed with CUDA events around the two pinn_train_epochs calls; plus the CPU oracle's time per
+    Adam step on the same batch size (a bounded sample of 5 steps, numpy fp64, 1 process)."""
+    import torch
+    from paper_2303_03848_b200 import pinn_train
+    mk = dict(K=1.0, sigma=0.2, r=0.05, T=1.0, L=4.0)
+    sets = synth.collocation(mk, *synth.PAPER_COLLOCATION, seed=0)
+    net0 = synth.pinn2_net([2, 20, 20, 20, 1], seed=0)
+    st = torch.cuda.Stream()
+    with pinn_train.Trainer(net0, mk, sets, batches=10, seed=0, stream=st.cuda_stream) as tr:
+        l0 = tr.loss()
+        tr.epochs(5, 1e-2, history=False)  # warm-up (graph capture, caches)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(st)                      # events on the trainer's stream (pinn_train_epochs syncs it)
+        tr.epochs(5000, 1e-2, history=False)
+        tr.epochs(800, 1e-3, history=False)
+        e1.record(st)
+        e1.synchronize()
+        wall = e0.elapsed_time(e1) / 1e3
+        l1 = tr.loss()
+    steps = 5800 * 10
+    pts = sum(synth.PAPER_COLLOCATION) / 10
+    cpu_step = None
+    try:
+        from oracle import pinn_train as opt
+        o = opt.Trainer(net0, mk, sets, batches=10, seed=0)
+        o.gradient(0)
+        t1 = time.perf_counter()
+        for st in range(1, 6):
+            o.gradient(st)
+        cpu_step = (time.perf_counter() - t1) / 5
+    except Exception:
+        pass
+    return {"workload": "paper schedule: 5000 epochs lr 1e-2 + 800 epochs lr 1e-3, 10 shuffled batches/epoch, "
+                        "N_f/N_b/N_exp = 100000/10000/10000 (P:190, P:210-211), 3x20 tanh, C2 market",
+            "seconds": wall, "steps": steps, "us_per_step": 1e6 * wall / steps,
+            "point_evals_per_s": steps * pts / wall, "loss_initial": list(map(float, l0)),
+            "loss_final": list(map(float, l1)),
+            "paper_context": "P:212: 'around 30 minutes' for the paper's 10x50 ReLU net (other hardware)",
+            "cpu_oracle_s_per_step": cpu_step,
+            "cpu_oracle_sample": "5 gradient evaluations of the numpy fp64 training oracle on the same batch (1 process)"}
 
 
 CONVERGED_TOL = {"C1": 3e-5, "C2": 1e-5, "C3": 3e-5}  # Q18-valid tolerances (SURVEY §8(d) C1-C3 rows)
@@ -476,6 +547,8 @@ def main():
         ctx.set_option(parareal.OPT_PIPELINE, 0)
     # ---------------- roofline of the dominant kernel (per-launch average, events per phase)
     pk, pk_src = peaks()
+    global ALU
+    ALU = alu_peaks()
     clk_mhz = float(pk.get("sm_max_mhz", 1965.0))
     n_sm = torch.cuda.get_device_properties(local).multi_processor_count
     roof = roofline(p_run, ph, K, ctx_world, ctx_rank, pk, pk_src, clk_mhz, n_sm, synth, dims=pinn_dims(args),
@@ -490,6 +563,10 @@ def main():
     converged = None
     if rank == 0 and world == 1 and args.config.upper() in CONVERGED_TOL:
         converged = converged_run(args, parareal, synth, torch, stream, flush)
+    # ---------------- NEXT-3: PINN training on the GPU (the paper's sets and schedule)
+    training = None
+    if rank == 0 and world == 1 and not args.no_training:
+        training = training_run(synth)
     # ---------------- e2e through the host-buffer ABI call (pinned H2D of V_T, D2H of V_0)
     e2e = None
     if not args.no_e2e:
@@ -551,6 +628,7 @@ def main():
                 "step_ms_stats": step_stats(step_ms),
                 "eq8_bound_context": None,
                 "roofline": roof, "roofline_fine_sweep_c3": fine_c3, "converged_K_run": converged,
+                "pinn_training": training,
                 "cpu_baseline": cpu,
                 "cpu_baseline_threaded": cpu_threaded, "e2e": e2e,
                 "gpu_launches": launches,
