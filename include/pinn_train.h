@@ -4,7 +4,8 @@
  *
  *   network     Ṽ(t, S) = L · y(t/T, S/L): a fully connected net, 2 inputs (t, S) — the
  *               function the losses are written over (reading Q28) — hidden layers
- *               of equal width W ≤ 32 with tanh (north_star) or ReLU, linear output.
+ *               of equal width W ∈ {8,16,20,32,50,64} with tanh (north_star) or ReLU,
+ *               linear output (the paper's 10×50 ReLU net included; shared memory bounds the depth).
  *               The trained weights plug into parareal_load_pinn_weights unchanged as a 2-input
  *               G (dims[0] = 2, features (t_to/T, S/L_b), output × L_b; reading Q8).
  *   loss        MSE_total = MSE_f + MSE_exp + MSE_b (Eq. 11) over three collocation
@@ -48,7 +49,7 @@ typedef struct {
   int32_t upper_bc;              /* PR_BC_*: the boundary target at S = L (reading Q3)            */
   int32_t n_linear;              /* linear layers ≥ 2                                             */
   const int32_t *dims;           /* [n_linear+1]: dims[0] = 2, hidden widths equal and in
-                                    {8, 16, 20, 32}, dims[n_linear] = 1                           */
+                                    {8, 16, 20, 32, 50, 64}, dims[n_linear] = 1                   */
   int32_t activation;            /* PR_ACT_TANH / PR_ACT_RELU                                     */
   const float *const *W;         /* [n_linear] initial weights, row-major [out][in] (copied)      */
   const float *const *b;         /* [n_linear] initial biases (copied)                            */
@@ -64,7 +65,8 @@ typedef struct {
 } pt_config;
 
 /* Validates the config (PR_ERR_INVALID_ARGUMENT naming the field; PR_ERR_UNSUPPORTED for a
- * hidden width outside {8,16,20,32} or unequal widths), copies weights and points to the
+ * hidden width outside {8,16,20,32,50,64}, unequal widths, or a net whose weights and forward
+ * stash exceed the shared memory of one CTA), copies weights and points to the
  * device, zeroes Adam's moments and the step counter. */
 pr_status pinn_train_init(const pt_config *cfg, pt_trainer **out);
 

@@ -2,17 +2,18 @@
 // PAPER.md §3.3; C ABI in include/pinn_train.h).
 //
 // One Adam step is two kernels:
-//  k_train_grad  one thread per collocation point of the step's batch (its epoch's shuffle of
-//                each set): forward jets (Ṽ, Ṽ_t, Ṽ_S, Ṽ_SS) through the net with the
-//                weights in shared memory, the point's loss term (Eqs. 12-14) and its adjoint,
-//                then reverse accumulation layer by layer.  Each layer's weight
-//                gradient Σ_points Σ_jet z̄_c ⊗ h_c is contracted per CTA from shared-memory
-//                tiles of the 128 points' adjoints and inputs and written as the CTA's partial
-//                (no atomics: fixed summation order, run-to-run bitwise).  The forward
-//                pre-activation jets are stashed per thread (coalesced, L2-resident) for the
-//                reverse pass.
-//  k_adam        one CTA: the fp64 sum of the CTA partials in CTA order, Adam, the
-//                batch's loss terms into the history, the step counter.
+//  k_train_grad  G threads per collocation point of the step's batch (its epoch's shuffle of
+//                each set), each owning W/G neurons of every layer: forward jets (Ṽ, Ṽ_t,
+//                Ṽ_S, Ṽ_SS) through the net with the weights in shared memory and the layer
+//                activations exchanged through a shared row per point, the point's loss term
+//                (Eqs. 12-14) and its adjoint, then reverse accumulation layer by layer.
+//                Each layer's weight gradient Σ_points Σ_jet z̄_c ⊗ h_c is contracted per CTA from
+//                the points' shared rows and written as the CTA's partial (no atomics: fixed
+//                summation order, run-to-run bitwise).  The forward pre-activation jets are
+//                stashed in shared memory for the reverse pass.
+//  k_adam        32 parameters per CTA: the fp64 sum of the CTA partials (fixed tree), Adam
+//                (P:210); the last CTA (completion ticket) writes the batch's loss terms into the
+//                history and advances the step counter.
 // One epoch (batches × the two kernels) is captured as a CUDA graph and replayed; both kernels
 // read the step counter from device memory, so the same graph serves every epoch.
 #include "../../include/pinn_train.h"
@@ -28,7 +29,7 @@
 
 namespace {
 
-constexpr int kTPB = 128;          // points per CTA of the gradient kernel (one per thread)
+constexpr int kTPB = 128;          // threads per CTA of the gradient kernel
 constexpr int kAdamThreads = 1024;
 constexpr int kActTanh = PR_ACT_TANH;
 
@@ -42,7 +43,6 @@ struct GradArgs {
   int np, LH;
   float *gpart;     // [nblk][np] CTA partial gradients
   double *lpart;    // [nblk][3] CTA partial loss terms
-  float *stash;     // [nblk][LH][4][W][kTPB] forward pre-activation jets (h, z_t, z_S, z_SS)
   const float *t_f, *S_f, *t_b, *S_b, *S_e;
   int n_f, n_b, n_e, batches;
   const long long *d_step;  // the global step counter (device)
@@ -110,144 +110,189 @@ __device__ __forceinline__ double block_sum3(double v, int c, double *sl) {
   return v;
 }
 
-// Contracts one layer's gradient over the CTA's points: entry (i, j) of the [Wo][Wi] weight block
-// = Σ_p Σ_c A[c][p][i]·B[c][p][j]; bias i = Σ_p A[0][p][i].  A, B in shared memory, p-major rows.
+// Geometry of the gradient kernel: G threads per collocation point, each owning NPT = W/G neurons
+// of every layer (groups of G consecutive lanes; 32/G groups per warp, lanes beyond them idle).
+template <int W> struct TrainGeom;
+template <> struct TrainGeom<8> { static constexpr int G = 2; };
+template <> struct TrainGeom<16> { static constexpr int G = 4; };
+template <> struct TrainGeom<20> { static constexpr int G = 4; };
+template <> struct TrainGeom<32> { static constexpr int G = 4; };
+template <> struct TrainGeom<50> { static constexpr int G = 10; };
+template <> struct TrainGeom<64> { static constexpr int G = 8; };
 template <int W>
-__device__ __forceinline__ void contract(const float *sA, int Wo, const float *sB, int Wi, float *gout) {
-  const int nW = Wo * Wi;
-  for (int e = threadIdx.x; e < nW + Wo; e += kTPB) {
-    float acc = 0.0f;
-    if (e < nW) {
-      const int i = e / Wi, j = e - (e / Wi) * Wi;
-#pragma unroll 4
-      for (int p = 0; p < kTPB; ++p) {
-#pragma unroll
-        for (int c = 0; c < 4; ++c) acc = fmaf(sA[(c * kTPB + p) * W + i], sB[(c * kTPB + p) * W + j], acc);
-      }
-    } else {
-      const int i = e - nW;
-#pragma unroll 8
-      for (int p = 0; p < kTPB; ++p) acc += sA[p * W + i];
-    }
-    gout[e] = acc;
-  }
+struct TG {
+  static constexpr int G = TrainGeom<W>::G, NPT = W / G, GPW = 32 / G;
+  static constexpr int PP = (kTPB / 32) * GPW;  // collocation points per CTA
+  static constexpr int RS = 4 * W + 1;          // shared row stride of one point's 4 jet rows (odd: no conflicts)
+};
+// shared memory of the gradient kernel (floats after the 128-B loss scratch): weights, the
+// forward stash [LH][PP][4W], two exchange rows [PP][RS] (z̄ / activations, and h_prev jets), ȳ [PP][4]
+template <int W>
+size_t train_smem_floats(int np, int LH) {
+  using T = TG<W>;
+  return (size_t)np + (size_t)LH * T::PP * 4 * W + 2 * (size_t)T::PP * T::RS + 4 * T::PP + 4;
 }
 
+// Gradient of the batch loss (GRAD) or the loss terms only (!GRAD) over this CTA's PP points.
+//  forward   lane q of point p computes the jets (z, z_t, z_S, z_SS) of its NPT neurons of each
+//            layer from the whole previous layer (read from the point's shared row), stashes
+//            (h, z_t, z_S, z_SS) in shared memory and writes its activation jets back to the row;
+//  loss      the group's output-layer partials are summed by the leader in lane order; it forms the
+//            loss term and the output adjoints (Eqs. 12-14, Eq. 11) and shares them;
+//  backward  per layer, top down: z-bar of its own neurons from h-bar (jet chain rules, up to the
+//            third derivative of the activation), written to the shared row; the CTA contracts the
+//            layer's weight gradient sum_p sum_c zbar_c (x) h_c over its points (fixed order); h-bar
+//            of the layer below for its own neurons = sum_i W_ij zbar_i.
 template <int W, int ACT, bool GRAD>
 __global__ void __launch_bounds__(kTPB) k_train_grad(GradArgs a) {
+  using T = TG<W>;
+  constexpr int G = T::G, NPT = T::NPT, GPW = T::GPW, PP = T::PP, RS = T::RS;
   extern __shared__ __align__(16) unsigned char smraw[];
-  double *sl = reinterpret_cast<double *>(smraw);                  // [kTPB/32][3]
-  float *sA = reinterpret_cast<float *>(smraw + 128);              // [4][kTPB][W]
-  float *sB = sA + 4 * kTPB * W;                                   // [4][kTPB][W]
-  float *sw = sB + 4 * kTPB * W;                                   // [np]
-  const int tid = threadIdx.x, blk = blockIdx.x, LH = a.LH;
+  double *sl = reinterpret_cast<double *>(smraw);  // [kTPB/32][3]
+  float *sw = reinterpret_cast<float *>(smraw + 128);
+  const int LH = a.LH;
+  float *sst = sw + a.np;                           // [LH][PP][4W]
+  float *sZ = sst + (size_t)LH * PP * 4 * W;        // [PP][RS]
+  float *sH = sZ + PP * RS;                         // [PP][RS]
+  float *sY = sH + PP * RS;                         // [PP][4]
+  const int tid = threadIdx.x, blk = blockIdx.x, lane = tid & 31;
   for (int i = tid; i < a.np; i += kTPB) sw[i] = a.theta[i];
+  const int grp = lane / G, q = lane - (lane / G) * G;
+  const bool act_lane = grp < GPW;
+  const int pidx = (tid >> 5) * GPW + (act_lane ? grp : 0);  // (idle lanes shadow group 0)
+  const int i0 = q * NPT;                                     // this lane's first neuron
 
-  // ---- the point this thread owns (batch part ib of each set's shuffle)
+  // ---- the point (batch part ib of each set's shuffle)
   const long long step = a.step_override >= 0 ? a.step_override : *a.d_step;
   const long long epoch = step / a.batches;
   const int ib = (int)(step - epoch * a.batches);
-  long long lo[3], cnt[3];
-  const long long n[3] = {a.n_f, a.n_b, a.n_e};
-  for (int c = 0; c < 3; ++c) {
-    lo[c] = a.full ? 0 : ib * n[c] / a.batches;
-    cnt[c] = a.full ? n[c] : (ib + 1) * n[c] / a.batches - lo[c];
+  long long lo0, lo1, lo2, c0, c1, c2;
+  {
+    const long long n0 = a.n_f, n1 = a.n_b, n2 = a.n_e;
+    lo0 = a.full ? 0 : ib * n0 / a.batches, c0 = a.full ? n0 : (ib + 1) * n0 / a.batches - lo0;
+    lo1 = a.full ? 0 : ib * n1 / a.batches, c1 = a.full ? n1 : (ib + 1) * n1 / a.batches - lo1;
+    lo2 = a.full ? 0 : ib * n2 / a.batches, c2 = a.full ? n2 : (ib + 1) * n2 / a.batches - lo2;
   }
-  const long long g = (long long)blk * kTPB + tid;
+  const long long gpt = (long long)blk * PP + pidx;
   int kind = -1;
-  long long pos = 0;
-  if (g < cnt[0]) kind = 0, pos = g;
-  else if (g < cnt[0] + cnt[1]) kind = 1, pos = g - cnt[0];
-  else if (g < cnt[0] + cnt[1] + cnt[2]) kind = 2, pos = g - cnt[0] - cnt[1];
+  if (act_lane) {
+    if (gpt < c0) kind = 0;
+    else if (gpt < c0 + c1) kind = 1;
+    else if (gpt < c0 + c1 + c2) kind = 2;
+  }
   const Market mk = a.mk;
   float t = 0.0f, S = 0.0f;
-  if (kind >= 0) {
-    const long long idx = a.full ? pos : perm_at(a.seed, epoch, kind, n[kind], lo[kind] + pos);
-    if (kind == 0) t = a.t_f[idx], S = a.S_f[idx];
-    else if (kind == 1) t = a.t_b[idx], S = a.S_b[idx];
-    else t = mk.T, S = a.S_e[idx];
+  if (kind == 0) {
+    const long long idx = a.full ? gpt : perm_at(a.seed, epoch, 0, a.n_f, lo0 + gpt);
+    t = a.t_f[idx], S = a.S_f[idx];
+  } else if (kind == 1) {
+    const long long pos = gpt - c0, idx = a.full ? pos : perm_at(a.seed, epoch, 1, a.n_b, lo1 + pos);
+    t = a.t_b[idx], S = a.S_b[idx];
+  } else if (kind == 2) {
+    const long long pos = gpt - c0 - c1, idx = a.full ? pos : perm_at(a.seed, epoch, 2, a.n_e, lo2 + pos);
+    t = mk.T, S = a.S_e[idx];
   }
   __syncthreads();
 
-  // ---- forward jets (value, ∂t, ∂S, ∂SS) through the hidden layers; features (t/T, S/L)
+  // ---- forward jets; features x = (t/T, S/L): x_t = (1/T, 0), x_S = (0, 1/L)
   const float iT = 1.0f / mk.T, iL = 1.0f / mk.L;
   const float x0 = t * iT, x1 = S * iL;
-  float h[W], ht[W], hS[W], hSS[W];
-  float *st = a.stash + (size_t)blk * LH * 4 * W * kTPB + tid;
+  float *rowZ = sZ + pidx * RS, *rowH = sH + pidx * RS;
   {
     const float *W0 = sw, *b0 = sw + 2 * W;
+    float *st = sst + (size_t)pidx * 4 * W;
 #pragma unroll
-    for (int i = 0; i < W; ++i) {
+    for (int ii = 0; ii < NPT; ++ii) {
+      const int i = i0 + ii;
       const float z = fmaf(W0[2 * i], x0, fmaf(W0[2 * i + 1], x1, b0[i]));
       const float zt = W0[2 * i] * iT, zS = W0[2 * i + 1] * iL;
       const float hv = act<ACT>(z);
       float s1, s2, s3;
       act_derivs<ACT>(hv, s1, s2, s3);
-      if (GRAD) {
-        st[(0 * W + i) * kTPB] = hv;
-        st[(1 * W + i) * kTPB] = zt;
-        st[(2 * W + i) * kTPB] = zS;
-        st[(3 * W + i) * kTPB] = 0.0f;
+      if (act_lane) {
+        if (GRAD) st[i] = hv, st[W + i] = zt, st[2 * W + i] = zS, st[3 * W + i] = 0.0f;
+        rowZ[i] = hv, rowZ[W + i] = s1 * zt, rowZ[2 * W + i] = s1 * zS, rowZ[3 * W + i] = s2 * zS * zS;
       }
-      h[i] = hv, ht[i] = s1 * zt, hS[i] = s1 * zS, hSS[i] = s2 * zS * zS;
     }
   }
-  int off = 3 * W;  // start of layer 1's parameters
+  __syncthreads();
+  int off = 3 * W;
   for (int l = 1; l < LH; ++l) {
     const float *Wl = sw + off, *bl = sw + off + W * W;
-    float z[W], zt[W], zS[W], zSS[W];
+    float z[NPT], zt[NPT], zS[NPT], zSS[NPT];
 #pragma unroll
-    for (int i = 0; i < W; ++i) {
-      float a0 = bl[i], a1 = 0.0f, a2 = 0.0f, a3 = 0.0f;
+    for (int ii = 0; ii < NPT; ++ii) z[ii] = bl[i0 + ii], zt[ii] = 0.0f, zS[ii] = 0.0f, zSS[ii] = 0.0f;
+#pragma unroll 4
+    for (int j = 0; j < W; ++j) {
+      const float h0 = rowZ[j], h1 = rowZ[W + j], h2 = rowZ[2 * W + j], h3 = rowZ[3 * W + j];
 #pragma unroll
-      for (int j = 0; j < W; ++j) {
-        const float w = Wl[i * W + j];
-        a0 = fmaf(w, h[j], a0), a1 = fmaf(w, ht[j], a1), a2 = fmaf(w, hS[j], a2), a3 = fmaf(w, hSS[j], a3);
+      for (int ii = 0; ii < NPT; ++ii) {
+        const float w = Wl[(i0 + ii) * W + j];
+        z[ii] = fmaf(w, h0, z[ii]), zt[ii] = fmaf(w, h1, zt[ii]), zS[ii] = fmaf(w, h2, zS[ii]),
+        zSS[ii] = fmaf(w, h3, zSS[ii]);
       }
-      z[i] = a0, zt[i] = a1, zS[i] = a2, zSS[i] = a3;
     }
-    float *sl_ = st + (size_t)l * 4 * W * kTPB;
+    __syncthreads();  // every lane has read the previous layer's row
+    float *st = sst + ((size_t)l * PP + pidx) * 4 * W;
 #pragma unroll
-    for (int i = 0; i < W; ++i) {
-      const float hv = act<ACT>(z[i]);
+    for (int ii = 0; ii < NPT; ++ii) {
+      const int i = i0 + ii;
+      const float hv = act<ACT>(z[ii]);
       float s1, s2, s3;
       act_derivs<ACT>(hv, s1, s2, s3);
-      if (GRAD) {
-        sl_[(0 * W + i) * kTPB] = hv;
-        sl_[(1 * W + i) * kTPB] = zt[i];
-        sl_[(2 * W + i) * kTPB] = zS[i];
-        sl_[(3 * W + i) * kTPB] = zSS[i];
+      if (act_lane) {
+        if (GRAD) st[i] = hv, st[W + i] = zt[ii], st[2 * W + i] = zS[ii], st[3 * W + i] = zSS[ii];
+        rowZ[i] = hv, rowZ[W + i] = s1 * zt[ii], rowZ[2 * W + i] = s1 * zS[ii],
+        rowZ[3 * W + i] = fmaf(s2 * zS[ii], zS[ii], s1 * zSS[ii]);
       }
-      h[i] = hv, ht[i] = s1 * zt[i], hS[i] = s1 * zS[i], hSS[i] = fmaf(s2 * zS[i], zS[i], s1 * zSS[i]);
     }
+    __syncthreads();
     off += W * W + W;
   }
   const int off_o = off;  // output layer: wo [W], bo
   const float *wo = sw + off_o;
-  float y = sw[off_o + W], yt = 0.0f, yS = 0.0f, ySS = 0.0f;
+  {  // group partials of y_c over this lane's neurons -> the leader (lane order, fixed)
+    float y[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
-  for (int j = 0; j < W; ++j) y = fmaf(wo[j], h[j], y), yt = fmaf(wo[j], ht[j], yt), yS = fmaf(wo[j], hS[j], yS),
-                              ySS = fmaf(wo[j], hSS[j], ySS);
-  const float V = mk.L * y, Vt = mk.L * yt, VS = mk.L * yS, VSS = mk.L * ySS;
-
-  // ---- loss term and output adjoints (Eqs. 12-14; MSE_total Eq. 11)
-  float Vb = 0.0f, Vtb = 0.0f, VSb = 0.0f, VSSb = 0.0f;
+    for (int ii = 0; ii < NPT; ++ii) {
+      const int i = i0 + ii;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) y[c] = fmaf(wo[i], rowZ[c * W + i], y[c]);
+    }
+    if (act_lane)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) rowH[c * G + q] = y[c];
+  }
+  __syncthreads();
   double ell[3] = {0.0, 0.0, 0.0};
-  if (kind == 0) {
-    const float hs2 = 0.5f * mk.sig * mk.sig * S * S;
-    const float f = Vt + hs2 * VSS + mk.r * S * VS - mk.r * V;  // Eq. (1) applied to Ṽ
-    ell[0] = (double)f * (double)f / (double)cnt[0];
-    const float fb = 2.0f * f / (float)cnt[0];
-    Vb = -mk.r * fb, Vtb = fb, VSb = mk.r * S * fb, VSSb = hs2 * fb;
-  } else if (kind == 1) {
-    const float tgt = S > 0.5f * mk.L ? (mk.asym ? mk.L - mk.K * expf(-mk.r * (mk.T - t)) : 0.0f) : 0.0f;
-    const float e = V - tgt;
-    ell[1] = (double)e * (double)e / (double)cnt[1];
-    Vb = 2.0f * e / (float)cnt[1];
-  } else if (kind == 2) {
-    const float e = V - fmaxf(S - mk.K, 0.0f);
-    ell[2] = (double)e * (double)e / (double)cnt[2];
-    Vb = 2.0f * e / (float)cnt[2];
+  if (act_lane && q == 0) {
+    float y[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      float acc = c == 0 ? sw[off_o + W] : 0.0f;
+      for (int r = 0; r < G; ++r) acc += rowH[c * G + r];
+      y[c] = acc;
+    }
+    const float V = mk.L * y[0], Vt = mk.L * y[1], VS = mk.L * y[2], VSS = mk.L * y[3];
+    float Vb = 0.0f, Vtb = 0.0f, VSb = 0.0f, VSSb = 0.0f;
+    if (kind == 0) {
+      const float hs2 = 0.5f * mk.sig * mk.sig * S * S;
+      const float f = Vt + hs2 * VSS + mk.r * S * VS - mk.r * V;  // Eq. (1) applied to the network
+      ell[0] = (double)f * (double)f / (double)c0;
+      const float fb = 2.0f * f / (float)c0;
+      Vb = -mk.r * fb, Vtb = fb, VSb = mk.r * S * fb, VSSb = hs2 * fb;
+    } else if (kind == 1) {
+      const float tgt = S > 0.5f * mk.L ? (mk.asym ? mk.L - mk.K * expf(-mk.r * (mk.T - t)) : 0.0f) : 0.0f;
+      const float e = V - tgt;
+      ell[1] = (double)e * (double)e / (double)c1;
+      Vb = 2.0f * e / (float)c1;
+    } else if (kind == 2) {
+      const float e = V - fmaxf(S - mk.K, 0.0f);
+      ell[2] = (double)e * (double)e / (double)c2;
+      Vb = 2.0f * e / (float)c2;
+    }
+    float *yb = sY + pidx * 4;
+    yb[0] = mk.L * Vb, yb[1] = mk.L * Vtb, yb[2] = mk.L * VSb, yb[3] = mk.L * VSSb;
   }
   for (int c = 0; c < 3; ++c) block_sum3(ell[c], c, sl);
   __syncthreads();
@@ -260,117 +305,171 @@ __global__ void __launch_bounds__(kTPB) k_train_grad(GradArgs a) {
 
   // ---- reverse accumulation
   float *gout = a.gpart + (size_t)blk * a.np;
-  const float yb[4] = {mk.L * Vb, mk.L * Vtb, mk.L * VSb, mk.L * VSSb};
-  // output layer: A = ȳ (one "neuron"), B = last hidden jets
+  // output layer: grad wo_i = sum_p sum_c ybar_c h_c,i (h rows still in sZ), grad bo = sum_p ybar_0
+  for (int e = tid; e <= W; e += kTPB) {
+    float acc = 0.0f;
+    if (e < W) {
+      for (int p = 0; p < PP; ++p)
 #pragma unroll
-  for (int c = 0; c < 4; ++c) sA[(c * kTPB + tid) * W] = yb[c];
-#pragma unroll
-  for (int j = 0; j < W; ++j) {
-    sB[(0 * kTPB + tid) * W + j] = h[j];
-    sB[(1 * kTPB + tid) * W + j] = ht[j];
-    sB[(2 * kTPB + tid) * W + j] = hS[j];
-    sB[(3 * kTPB + tid) * W + j] = hSS[j];
+        for (int c = 0; c < 4; ++c) acc = fmaf(sY[p * 4 + c], sZ[p * RS + c * W + e], acc);
+    } else {
+      for (int p = 0; p < PP; ++p) acc += sY[p * 4];
+    }
+    gout[off_o + e] = acc;
   }
-  __syncthreads();
-  contract<W>(sA, 1, sB, W, gout + off_o);
-  float hb[W], hbt[W], hbS[W], hbSS[W];
+  float hb[4][NPT];
+  {
+    const float *yb = sY + pidx * 4;
 #pragma unroll
-  for (int j = 0; j < W; ++j) hb[j] = wo[j] * yb[0], hbt[j] = wo[j] * yb[1], hbS[j] = wo[j] * yb[2], hbSS[j] = wo[j] * yb[3];
-  __syncthreads();
-
+    for (int ii = 0; ii < NPT; ++ii)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) hb[c][ii] = wo[i0 + ii] * yb[c];
+  }
+  __syncthreads();  // sZ is rewritten below
   for (int l = LH - 1; l >= 0; --l) {
-    const float *sl_ = st + (size_t)l * 4 * W * kTPB;
-    // z̄ from h̄ through the activation's jet rules (in place)
+    const float *st = sst + ((size_t)l * PP + pidx) * 4 * W;
+    // z-bar of this lane's neurons through the activation's jet rules -> the point's row
 #pragma unroll
-    for (int i = 0; i < W; ++i) {
-      const float hv = sl_[(0 * W + i) * kTPB], zt = sl_[(1 * W + i) * kTPB], zS = sl_[(2 * W + i) * kTPB],
-                  zSS = sl_[(3 * W + i) * kTPB];
+    for (int ii = 0; ii < NPT; ++ii) {
+      const int i = i0 + ii;
+      const float hv = st[i], zt = st[W + i], zS = st[2 * W + i], zSS = st[3 * W + i];
       float s1, s2, s3;
       act_derivs<ACT>(hv, s1, s2, s3);
-      const float zb = hb[i] * s1 + hbt[i] * s2 * zt + hbS[i] * s2 * zS + hbSS[i] * fmaf(s3 * zS, zS, s2 * zSS);
-      const float zbS = fmaf(hbSS[i] * 2.0f * s2, zS, hbS[i] * s1);
-      hb[i] = zb, hbt[i] = hbt[i] * s1, hbS[i] = zbS, hbSS[i] = hbSS[i] * s1;
-      sA[(0 * kTPB + tid) * W + i] = hb[i];
-      sA[(1 * kTPB + tid) * W + i] = hbt[i];
-      sA[(2 * kTPB + tid) * W + i] = hbS[i];
-      sA[(3 * kTPB + tid) * W + i] = hbSS[i];
+      const float zb = hb[0][ii] * s1 + hb[1][ii] * s2 * zt + hb[2][ii] * s2 * zS + hb[3][ii] * fmaf(s3 * zS, zS, s2 * zSS);
+      const float zbS = fmaf(hb[3][ii] * 2.0f * s2, zS, hb[2][ii] * s1);
+      hb[0][ii] = zb, hb[1][ii] = hb[1][ii] * s1, hb[2][ii] = zbS, hb[3][ii] = hb[3][ii] * s1;
+      if (act_lane)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) rowZ[c * W + i] = hb[c][ii];
     }
+    // activation jets of the layer below (this layer's input): from the stash, or the features
     int Wi, offl;
     if (l > 0) {
       Wi = W;
       offl = 3 * W + (l - 1) * (W * W + W);
-      const float *sp = st + (size_t)(l - 1) * 4 * W * kTPB;
+      const float *sp = sst + ((size_t)(l - 1) * PP + pidx) * 4 * W;
 #pragma unroll
-      for (int j = 0; j < W; ++j) {
-        const float hv = sp[(0 * W + j) * kTPB], zt = sp[(1 * W + j) * kTPB], zS = sp[(2 * W + j) * kTPB],
-                    zSS = sp[(3 * W + j) * kTPB];
+      for (int ii = 0; ii < NPT; ++ii) {
+        const int j = i0 + ii;
+        const float hv = sp[j], zt = sp[W + j], zS = sp[2 * W + j], zSS = sp[3 * W + j];
         float s1, s2, s3;
         act_derivs<ACT>(hv, s1, s2, s3);
-        sB[(0 * kTPB + tid) * W + j] = hv;
-        sB[(1 * kTPB + tid) * W + j] = s1 * zt;
-        sB[(2 * kTPB + tid) * W + j] = s1 * zS;
-        sB[(3 * kTPB + tid) * W + j] = fmaf(s2 * zS, zS, s1 * zSS);
+        if (act_lane)
+          rowH[j] = hv, rowH[W + j] = s1 * zt, rowH[2 * W + j] = s1 * zS, rowH[3 * W + j] = fmaf(s2 * zS, zS, s1 * zSS);
       }
     } else {
       Wi = 2;
       offl = 0;
-      sB[(0 * kTPB + tid) * W + 0] = x0, sB[(0 * kTPB + tid) * W + 1] = x1;
-      sB[(1 * kTPB + tid) * W + 0] = iT, sB[(1 * kTPB + tid) * W + 1] = 0.0f;
-      sB[(2 * kTPB + tid) * W + 0] = 0.0f, sB[(2 * kTPB + tid) * W + 1] = iL;
-      sB[(3 * kTPB + tid) * W + 0] = 0.0f, sB[(3 * kTPB + tid) * W + 1] = 0.0f;
+      if (act_lane && q == 0) {
+        rowH[0] = x0, rowH[1] = x1, rowH[W] = iT, rowH[W + 1] = 0.0f;
+        rowH[2 * W] = 0.0f, rowH[2 * W + 1] = iL, rowH[3 * W] = 0.0f, rowH[3 * W + 1] = 0.0f;
+      }
     }
     __syncthreads();
-    contract<W>(sA, W, sB, Wi, gout + offl);
-    if (l > 0) {  // h̄_prev = W_lᵀ z̄ for every jet component
+    // the layer's weight block [W][Wi] and bias over the CTA's points, fixed order
+    const int nW = W * Wi;
+    for (int e = tid; e < nW + W; e += kTPB) {
+      float acc = 0.0f;
+      if (e < nW) {
+        const int i = e / Wi, j = e - (e / Wi) * Wi;
+        for (int p = 0; p < PP; ++p) {
+          const float *zr = sZ + p * RS, *hr = sH + p * RS;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) acc = fmaf(zr[c * W + i], hr[c * W + j], acc);
+        }
+      } else {
+        const int i = e - nW;
+        for (int p = 0; p < PP; ++p) acc += sZ[p * RS + i];
+      }
+      gout[offl + e] = acc;
+    }
+    if (l > 0) {  // h-bar of the layer below, this lane's neurons: sum_i W_l[i][j] zbar_c,i
       const float *Wl = sw + offl;
-      float nb[W], nbt[W], nbS[W], nbSS[W];
+      float nb[4][NPT];
 #pragma unroll
-      for (int j = 0; j < W; ++j) nb[j] = nbt[j] = nbS[j] = nbSS[j] = 0.0f;
+      for (int ii = 0; ii < NPT; ++ii)
 #pragma unroll
+        for (int c = 0; c < 4; ++c) nb[c][ii] = 0.0f;
+#pragma unroll 4
       for (int i = 0; i < W; ++i) {
+        const float z0 = rowZ[i], z1 = rowZ[W + i], z2 = rowZ[2 * W + i], z3 = rowZ[3 * W + i];
 #pragma unroll
-        for (int j = 0; j < W; ++j) {
-          const float w = Wl[i * W + j];
-          nb[j] = fmaf(w, hb[i], nb[j]), nbt[j] = fmaf(w, hbt[i], nbt[j]), nbS[j] = fmaf(w, hbS[i], nbS[j]),
-          nbSS[j] = fmaf(w, hbSS[i], nbSS[j]);
+        for (int ii = 0; ii < NPT; ++ii) {
+          const float w = Wl[i * W + i0 + ii];
+          nb[0][ii] = fmaf(w, z0, nb[0][ii]), nb[1][ii] = fmaf(w, z1, nb[1][ii]), nb[2][ii] = fmaf(w, z2, nb[2][ii]),
+          nb[3][ii] = fmaf(w, z3, nb[3][ii]);
         }
       }
 #pragma unroll
-      for (int j = 0; j < W; ++j) hb[j] = nb[j], hbt[j] = nbt[j], hbS[j] = nbS[j], hbSS[j] = nbSS[j];
+      for (int ii = 0; ii < NPT; ++ii)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) hb[c][ii] = nb[c][ii];
     }
     __syncthreads();
   }
 }
 
-// One CTA: g = Σ_blk partial (fp64, CTA order); Adam (Kingma & Ba, Alg. 1) unless update == 0;
-// the batch's loss terms into hist[step − step0]; the step counter.
+// Adam over the CTA partials.  A CTA owns 32 parameters (lanes) and sums their partials with its
+// 32 warps (warp w: partials w, w+32, …), then the 32 warp sums in warp order (a fixed tree: the
+// result is run-to-run bitwise); Adam (Kingma & Ba, Alg. 1) unless update == 0.  d_ctr[0] is the
+// step counter, d_ctr[1] a completion ticket: the CTA that finishes last (every CTA has read the
+// step by then) sums the loss partials, writes them into hist[step − step0] and advances the step.
+constexpr int kAdamWarps = kAdamThreads / 32;
 __global__ void __launch_bounds__(kAdamThreads)
     k_adam(float *theta, float *m, float *v, const float *gpart, const double *lpart, int nblk, int np,
-           long long *d_step, long long step0, double *hist, double lr, double b1, double b2, double eps,
+           long long *d_ctr, long long step0, double *hist, double lr, double b1, double b2, double eps,
            int update, float *gout, double *lout) {
-  const long long step = *d_step;
-  const double t = (double)(step + 1);
-  const double bc1 = 1.0 - pow(b1, t), bc2 = 1.0 - pow(b2, t);
-  for (int p = threadIdx.x; p < np && (update || gout); p += kAdamThreads) {
+  __shared__ double red[kAdamWarps][33];
+  __shared__ bool last;
+  const long long step = d_ctr[0];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int p = blockIdx.x * 32 + lane;
+  if (update || gout) {
     double g = 0.0;
-    for (int k = 0; k < nblk; ++k) g += (double)gpart[(size_t)k * np + p];
-    if (gout) gout[p] = (float)g;
-    if (update) {
-      const double mm = b1 * (double)m[p] + (1.0 - b1) * g;
-      const double vv = b2 * (double)v[p] + (1.0 - b2) * g * g;
-      m[p] = (float)mm;
-      v[p] = (float)vv;
-      theta[p] = (float)((double)theta[p] - lr * (mm / bc1) / (sqrt(vv / bc2) + eps));
+    if (p < np)
+      for (int k = w; k < nblk; k += kAdamWarps) g += (double)gpart[(size_t)k * np + p];
+    red[w][lane] = g;
+    __syncthreads();
+    if (w == 0 && p < np) {
+      double s = 0.0;
+      for (int q = 0; q < kAdamWarps; ++q) s += red[q][lane];
+      if (gout) gout[p] = (float)s;
+      if (update) {
+        const double t = (double)(step + 1);
+        const double bc1 = 1.0 - pow(b1, t), bc2 = 1.0 - pow(b2, t);
+        const double mm = b1 * (double)m[p] + (1.0 - b1) * s;
+        const double vv = b2 * (double)v[p] + (1.0 - b2) * s * s;
+        m[p] = (float)mm;
+        v[p] = (float)vv;
+        theta[p] = (float)((double)theta[p] - lr * (mm / bc1) / (sqrt(vv / bc2) + eps));
+      }
     }
   }
-  if (threadIdx.x < 3) {
-    double s = 0.0;
-    for (int k = 0; k < nblk; ++k) s += lpart[(size_t)k * 3 + threadIdx.x];
-    if (hist) hist[(step - step0) * 3 + threadIdx.x] = s;
-    if (lout) lout[threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(reinterpret_cast<unsigned long long *>(d_ctr + 1), 1ull) == gridDim.x - 1;
   }
   __syncthreads();
-  if (threadIdx.x == 0 && update) *d_step = step + 1;
+  if (!last) return;
+  for (int c = 0; c < 3; ++c) {  // loss terms: the same fixed tree over the CTA partials
+    double s = 0.0;
+    for (int k = threadIdx.x; k < nblk; k += kAdamThreads) s += lpart[(size_t)k * 3 + c];
+    red[w][lane] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double tot = 0.0;
+      for (int q = 0; q < kAdamWarps; ++q)
+        for (int l = 0; l < 32; ++l) tot += red[q][l];
+      if (hist) hist[(step - step0) * 3 + c] = tot;
+      if (lout) lout[c] = tot;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    d_ctr[1] = 0;
+    if (update) d_ctr[0] = step + 1;
+  }
 }
 
 // ---------------------------------------------------------------- dispatch on (W, ACT)
@@ -383,10 +482,24 @@ GradFn grad_kernel(int W, int act) {
   PT_CASE(16)
   PT_CASE(20)
   PT_CASE(32)
+  PT_CASE(50)
+  PT_CASE(64)
 #undef PT_CASE
   return nullptr;
 }
-size_t grad_smem(int W, int np) { return 128 + 2 * (size_t)4 * kTPB * W * sizeof(float) + (size_t)np * sizeof(float); }
+// collocation points per CTA and shared memory of the gradient kernel
+void grad_geometry(int W, int np, int LH, int *pp, size_t *smem) {
+#define PT_G(w)                                                        \
+  if (W == w) {                                                        \
+    *pp = TG<w>::PP;                                                   \
+    *smem = 128 + train_smem_floats<w>(np, LH) * sizeof(float);        \
+    return;                                                            \
+  }
+  PT_G(8) PT_G(16) PT_G(20) PT_G(32) PT_G(50) PT_G(64)
+#undef PT_G
+  *pp = 0;
+  *smem = 0;
+}
 
 std::string g_init_err = "no error";
 
@@ -412,7 +525,9 @@ struct pt_trainer {
   Market mk{};
   unsigned long long seed = 0;
   double b1 = 0.9, b2 = 0.999, eps = 1e-8;
-  float *theta = nullptr, *m = nullptr, *v = nullptr, *gpart = nullptr, *stash = nullptr, *gout = nullptr;
+  float *theta = nullptr, *m = nullptr, *v = nullptr, *gpart = nullptr, *gout = nullptr;
+  int pp = 0;       // collocation points per CTA of the gradient kernel
+  size_t smem = 0;  // its dynamic shared memory
   float *pts = nullptr;  // t_f, S_f, t_b, S_b, S_e
   double *lpart = nullptr, *lout = nullptr, *hist = nullptr;
   size_t hist_cap = 0;
@@ -452,7 +567,6 @@ GradArgs grad_args(pt_trainer *tr, bool full, long long step_override) {
   a.LH = tr->LH;
   a.gpart = tr->gpart;
   a.lpart = tr->lpart;
-  a.stash = tr->stash;
   a.t_f = tr->pts;
   a.S_f = tr->pts + tr->n_f;
   a.t_b = tr->pts + 2 * (size_t)tr->n_f;
@@ -473,13 +587,13 @@ pr_status launch_grad(pt_trainer *tr, bool grad, bool full, long long step_overr
   GradFn fn = grad ? grad_kernel<true>(tr->W, tr->act) : grad_kernel<false>(tr->W, tr->act);
   const int nblk = full ? tr->nblk_full : tr->nblk;
   void *args[] = {(void *)&a};
-  TCU(cudaLaunchKernel((const void *)fn, dim3(nblk), dim3(kTPB), args, grad_smem(tr->W, tr->np), tr->stream));
+  TCU(cudaLaunchKernel((const void *)fn, dim3(nblk), dim3(kTPB), args, tr->smem, tr->stream));
   return PR_OK;
 }
 
 pr_status launch_adam(pt_trainer *tr, int nblk, long long step0, double *hist, double lr, int update, float *gout,
                       double *lout) {
-  k_adam<<<1, kAdamThreads, 0, tr->stream>>>(tr->theta, tr->m, tr->v, tr->gpart, tr->lpart, nblk, tr->np, tr->d_step,
+  k_adam<<<(tr->np + 31) / 32, kAdamThreads, 0, tr->stream>>>(tr->theta, tr->m, tr->v, tr->gpart, tr->lpart, nblk, tr->np, tr->d_step,
                                              step0, hist, lr, tr->b1, tr->b2, tr->eps, update, gout, lout);
   TCU(cudaPeekAtLastError());
   return PR_OK;
@@ -515,7 +629,7 @@ pr_status pinn_train_init(const pt_config *cfg, pt_trainer **out) {
   for (int l = 1; l < c.n_linear; ++l)
     if (c.dims[l] != W) return tfail(nullptr, PR_ERR_UNSUPPORTED, "cfg.dims: hidden widths must be equal");
   if (!grad_kernel<true>(W, c.activation))
-    return tfail(nullptr, PR_ERR_UNSUPPORTED, fmt("cfg.dims: hidden width %d not in {8, 16, 20, 32}", W));
+    return tfail(nullptr, PR_ERR_UNSUPPORTED, fmt("cfg.dims: hidden width %d not in {8, 16, 20, 32, 50, 64}", W));
   if (c.n_f < 1 || c.n_b < 1 || c.n_exp < 1 || !c.t_f || !c.S_f || !c.t_b || !c.S_b || !c.S_exp)
     return tfail(nullptr, PR_ERR_INVALID_ARGUMENT, "cfg: every collocation set needs >= 1 point (n_f, n_b, n_exp)");
   if (c.batches < 1 || c.batches > c.n_f || c.batches > c.n_b || c.batches > c.n_exp)
@@ -550,8 +664,9 @@ pr_status pinn_train_init(const pt_config *cfg, pt_trainer **out) {
       s += (ib + 1) * n / c.batches - ib * n / c.batches;
     maxb = s > maxb ? s : maxb;
   }
-  tr->nblk = (int)((maxb + kTPB - 1) / kTPB);
-  tr->nblk_full = (int)(((long long)c.n_f + c.n_b + c.n_exp + kTPB - 1) / kTPB);
+  grad_geometry(W, tr->np, tr->LH, &tr->pp, &tr->smem);
+  tr->nblk = (int)((maxb + tr->pp - 1) / tr->pp);
+  tr->nblk_full = (int)(((long long)c.n_f + c.n_b + c.n_exp + tr->pp - 1) / tr->pp);
   auto bail = [&](pr_status s) {
     g_init_err = tr->err;
     pinn_train_free(tr);
@@ -572,7 +687,7 @@ pr_status pinn_train_init(const pt_config *cfg, pt_trainer **out) {
     ICU(cudaStreamCreateWithFlags(&tr->stream, cudaStreamNonBlocking));
     tr->own_stream = true;
   }
-  const size_t smem = grad_smem(W, tr->np);
+  const size_t smem = tr->smem;
   int max_optin = 0;
   ICU(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, tr->device));
   if (smem > (size_t)max_optin) {
@@ -590,13 +705,12 @@ pr_status pinn_train_init(const pt_config *cfg, pt_trainer **out) {
   ICU(cudaMalloc(&tr->gpart, (size_t)tr->nblk * np * sizeof(float)));
   ICU(cudaMalloc(&tr->lpart, (size_t)nb_max * 3 * sizeof(double)));
   ICU(cudaMalloc(&tr->lout, 3 * sizeof(double)));
-  ICU(cudaMalloc(&tr->stash, (size_t)tr->nblk * tr->LH * 4 * W * kTPB * sizeof(float)));
   ICU(cudaMalloc(&tr->pts, npts * sizeof(float)));
-  ICU(cudaMalloc(&tr->d_step, sizeof(long long)));
+  ICU(cudaMalloc(&tr->d_step, 2 * sizeof(long long)));  // step counter, k_adam's completion ticket
   ICU(cudaMemcpyAsync(tr->theta, packed.data(), np * sizeof(float), cudaMemcpyHostToDevice, tr->stream));
   ICU(cudaMemsetAsync(tr->m, 0, np * sizeof(float), tr->stream));
   ICU(cudaMemsetAsync(tr->v, 0, np * sizeof(float), tr->stream));
-  ICU(cudaMemsetAsync(tr->d_step, 0, sizeof(long long), tr->stream));
+  ICU(cudaMemsetAsync(tr->d_step, 0, 2 * sizeof(long long), tr->stream));
   float *p = tr->pts;
   const std::pair<const float *, int> parts[] = {{c.t_f, c.n_f}, {c.S_f, c.n_f}, {c.t_b, c.n_b}, {c.S_b, c.n_b},
                                                  {c.S_exp, c.n_exp}};
@@ -739,7 +853,6 @@ void pinn_train_free(pt_trainer *tr) {
   cudaFree(tr->gpart);
   cudaFree(tr->lpart);
   cudaFree(tr->lout);
-  cudaFree(tr->stash);
   cudaFree(tr->pts);
   cudaFree(tr->d_step);
   cudaFree(tr->hist);

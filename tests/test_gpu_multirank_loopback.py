@@ -112,7 +112,7 @@ def test_chain_wavefront_matches_one_rank(case, world, chunks):
     assert reps[-1]["kernel_launches"] > breps[-1]["kernel_launches"]
 
 
-@pytest.mark.parametrize("case,world", [("c2", 2), ("c2", 4), ("tc", 2), ("tc", 4), ("tol", 2)])
+@pytest.mark.parametrize("case,world", [("c2", 2), ("c2", 4), ("tc", 2), ("tc", 4), ("tol", 2), ("kN", 4)])
 def test_spatial_chain_matches_one_rank(case, world):
     """NEXT-4: the spatially sharded coarse chain (PR_OPT_SPATIAL_CHAIN; every rank chains all
     slices over its own point range, the fine sweep stays slice-sharded, rows change owner twice
@@ -125,9 +125,12 @@ def test_spatial_chain_matches_one_rank(case, world):
     elif case == "tc":
         p = synth.single(3000, 8, coarse=synth.COARSE_PINN, max_iter=3, tol=0.0, fine_steps=10)
         net, prec, opts = synth.kaiming_net([4, 128, 128, 128, 1], seed=4), parareal.PREC_FP16_TC, {}
-    else:  # a tolerance: the stop is decided from the δ every rank reduces from the summed slots
+    elif case == "tol":  # a tolerance: the stop is decided from the δ every rank reduces from the summed slots
         p = synth.single(256, 8, coarse=synth.COARSE_PINN, max_iter=8, tol=1e-3, fine_steps=10)
         net = synth.kaiming_net([4, 16, 16, 1], seed=7)
+    else:  # K = N: the last iteration's chain is the copy step alone (finite termination)
+        p = synth.single(200, 4, coarse=synth.COARSE_PINN, max_iter=4, tol=0.0, fine_steps=7)
+        net = synth.kaiming_net([4, 8, 8, 1], seed=8)
     with parareal.Context(p) as c:
         c.load_weights(net, precision=prec)
         c.set_option(parareal.OPT_PIPELINE, 1)

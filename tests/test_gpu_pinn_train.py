@@ -27,7 +27,9 @@ def _grad_close(g, ref, what):
 
 @pytest.mark.parametrize("dims,act", [([2, 20, 20, 20, 1], synth.ACT_TANH), ([2, 8, 8, 1], synth.ACT_TANH),
                                       ([2, 16, 16, 16, 16, 1], synth.ACT_TANH), ([2, 32, 32, 1], synth.ACT_TANH),
-                                      ([2, 20, 20, 1], synth.ACT_RELU)])
+                                      ([2, 20, 20, 1], synth.ACT_RELU), ([2, 64, 64, 64, 1], synth.ACT_TANH),
+                                      ([2] + [50] * 10 + [1], synth.ACT_RELU),   # the paper's net
+                                      ([2] + [50] * 4 + [1], synth.ACT_TANH)])
 def test_full_loss_and_batch_gradient_match_oracle(dims, act):
     net = synth.pinn2_net(dims, seed=1, activation=act)
     sets = synth.collocation(MK, 3000, 300, 300, seed=2)   # 3600 points: 28 CTAs, ragged tail
