@@ -374,6 +374,16 @@ def training_run(synth):
         cpu_step = (time.perf_counter() - t1) / 5
     except Exception:
         pass
+    # algorithmic flops per point and step: forward jets 4 components x W^2 FMA per hidden layer,
+    # the same again for h-bar and for the weight gradient (2 flop per FMA), plus the thin layers
+    W, LHh = 20, 3
+    flop_pt = 3 * 8 * W * W * (LHh - 1) + 3 * 8 * W * 3
+    alu = alu_peaks()
+    roof = {"kernel": "k_train_grad + k_adam (fp32 SIMT)", "bound": "alu",
+            "achieved": flop_pt * pts / (wall / steps) / 1e12, "unit": "TFLOP/s",
+            "peak": alu["fp32"] if alu else None, "peak_source": alu["src"] if alu else None,
+            "work_per_unit": "%d flop per collocation point per step (3x20 net)" % flop_pt}
+    roof["frac"] = roof["achieved"] / roof["peak"] if roof["peak"] else None
     return {"workload": "paper schedule: 5000 epochs lr 1e-2 + 800 epochs lr 1e-3, 10 shuffled batches/epoch, "
                         "N_f/N_b/N_exp = 100000/10000/10000 (P:190, P:210-211), 3x20 tanh, C2 market",
             "seconds": wall, "steps": steps, "us_per_step": 1e6 * wall / steps,
@@ -381,7 +391,8 @@ def training_run(synth):
             "loss_final": list(map(float, l1)),
             "paper_context": "P:212: 'around 30 minutes' for the paper's 10x50 ReLU net (other hardware)",
             "cpu_oracle_s_per_step": cpu_step,
-            "cpu_oracle_sample": "5 gradient evaluations of the numpy fp64 training oracle on the same batch (1 process)"}
+            "cpu_oracle_sample": "5 gradient evaluations of the numpy fp64 training oracle on the same batch (1 process)",
+            "roofline": roof}
 
 
 CONVERGED_TOL = {"C1": 3e-5, "C2": 1e-5, "C3": 3e-5}  # Q18-valid tolerances
