@@ -24,6 +24,7 @@
 #include <vector>
 
 #include "launch.h"
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX: phase ranges for nsys/ncu --nvtx (no-ops untraced)
 
 // ============================================================================ NCCL (dlopen)
 // NCCL is resolved at run time so the library loads without it (world == 1 never touches
@@ -1025,7 +1026,10 @@ struct PhaseTimer {
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> spans;
   cudaEvent_t a = nullptr;
   int cur = -1;
+  nvtxRangeId_t rid = 0;
   void begin(int phase) {
+    static const char *const names[] = {"pr: coarse chain", "pr: fine sweep", "pr: exchange", "pr: setup"};
+    rid = nvtxRangeStartA(names[phase & 3]);  // host-side phase range (nsys / ncu --nvtx)
     a = next_event(c);
     cur = phase;
     if (a) record(c, a);
@@ -1036,6 +1040,7 @@ struct PhaseTimer {
       record(c, b);
       spans.push_back({cur, {a, b}});
     }
+    nvtxRangeEnd(rid);
   }
 };
 enum { PH_COARSE = 0, PH_FINE = 1, PH_COMM = 2, PH_SETUP = 3 };
@@ -1437,7 +1442,14 @@ pr_status solve_spatial(pr_ctx *c, const float *V_T, bool device_ptr, PhaseTimer
   return st;
 }
 
+pr_status solve_impl_(pr_ctx *c, const float *V_T, float *V_0, bool device_ptr, pr_report *rep);
 pr_status solve_impl(pr_ctx *c, const float *V_T, float *V_0, bool device_ptr, pr_report *rep) {
+  const nvtxRangeId_t r = nvtxRangeStartA("parareal_solve");
+  const pr_status st = solve_impl_(c, V_T, V_0, device_ptr, rep);
+  nvtxRangeEnd(r);
+  return st;
+}
+pr_status solve_impl_(pr_ctx *c, const float *V_T, float *V_0, bool device_ptr, pr_report *rep) {
   pr_status st = check_ctx(c);
   if (st) return st;
   if (c->coarse == PR_COARSE_PINN && !c->have_pinn)

@@ -19,6 +19,7 @@
 #include "../../include/pinn_train.h"
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <cmath>
 #include <cstdarg>
@@ -724,7 +725,14 @@ pr_status pinn_train_init(const pt_config *cfg, pt_trainer **out) {
   return PR_OK;
 }
 
+static pr_status pinn_train_epochs_(pt_trainer *tr, int32_t epochs, double lr, double *loss_hist);
 pr_status pinn_train_epochs(pt_trainer *tr, int32_t epochs, double lr, double *loss_hist) {
+  const nvtxRangeId_t r = nvtxRangeStartA("pinn_train_epochs");
+  const pr_status st = pinn_train_epochs_(tr, epochs, lr, loss_hist);
+  nvtxRangeEnd(r);
+  return st;
+}
+static pr_status pinn_train_epochs_(pt_trainer *tr, int32_t epochs, double lr, double *loss_hist) {
   pr_status st = check(tr);
   if (st) return st;
   if (epochs < 1) return tfail(tr, PR_ERR_INVALID_ARGUMENT, "epochs must be >= 1");
