@@ -391,18 +391,22 @@ __device__ __forceinline__ void tc_mbar_arrive(uint64_t *bar) {
 }
 __device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 
-template <int IN, int W, int ACT, bool H16>
+// SPLIT (PR_PREC_FP16_TC, W ≤ 128): hi + lo fp16 planes for every A tile and weight chunk and the
+// three MMAs of k_pinn_chain_tc<…, SPLIT> per K step — the accurate mode with the ping-pong overlap.
+template <int IN, int W, int ACT, bool H16, bool SPLIT>
 __global__ void __launch_bounds__(288, 1) k_pinn_chain_tc2(PinnTcArgs ta) {
-  using T = typename std::conditional<H16, __half, __nv_bfloat16>::type;
+  using T = typename std::conditional<H16 || SPLIT, __half, __nv_bfloat16>::type;
   constexpr int TILE = 128;
-  constexpr uint32_t kIdesc = umma_idesc<!H16>(TILE, W);
+  constexpr int NP = SPLIT ? 2 : 1;  // operand planes (hi, lo)
+  constexpr uint32_t kIdesc = umma_idesc<!(H16 || SPLIT)>(TILE, W);
   constexpr uint32_t kPlaneA = (uint32_t)TILE * W * 2;
-  constexpr uint32_t kChunk = (uint32_t)W * kTcKC * 2;
+  constexpr uint32_t kPlaneB = (uint32_t)W * kTcKC * 2;
+  constexpr uint32_t kChunk = NP * kPlaneB;
   constexpr int NCH = W / kTcKC;
   const PinnArgs &a = ta.g;
   extern __shared__ __align__(128) unsigned char tc_smem[];
-  T *sA = reinterpret_cast<T *>(tc_smem);  // [2 tiles][128 × W]
-  unsigned char *sB = tc_smem + 2 * kPlaneA;
+  T *sA = reinterpret_cast<T *>(tc_smem);  // [2 tiles][NP planes][128 × W]
+  unsigned char *sB = tc_smem + 2 * NP * kPlaneA;
   constexpr int NB = kTc2Ring;  // streaming ring depth (NB − 1 chunks in flight)
   const int nchunks = ta.resident ? (a.LH - 1) * NCH : NB;
   float *sP = reinterpret_cast<float *>(sB + (size_t)nchunks * kChunk);
@@ -465,7 +469,7 @@ __global__ void __launch_bounds__(288, 1) k_pinn_chain_tc2(PinnTcArgs ta) {
             tc_mbar_wait(&bar_a[w], ph_a[w]);
             ph_a[w] ^= 1;
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const uint32_t aw = aBase + (uint32_t)w * kPlaneA, dw = tmem + (uint32_t)(w * W);
+            const uint32_t aw = aBase + (uint32_t)(w * NP) * kPlaneA, dw = tmem + (uint32_t)(w * W);
 #pragma unroll 1
             for (int c = 0; c < NCH; ++c) {
               uint32_t bc;
@@ -484,6 +488,18 @@ __global__ void __launch_bounds__(288, 1) k_pinn_chain_tc2(PinnTcArgs ta) {
                     "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                     "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(dw),
                     "l"(da), "l"(db), "r"(kIdesc), "r"(acc));
+                if (SPLIT) {  // + A_hi·B_lo + A_lo·B_hi
+                  const uint64_t dbl = umma_desc(bc + kPlaneB + bo2, 128, 16 * kTcKC);
+                  const uint64_t dal = umma_desc(aw + kPlaneA + ao, 128, 16 * W);
+                  asm volatile(
+                      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(dw),
+                      "l"(da), "l"(dbl), "r"(kIdesc), "r"(1u));
+                  asm volatile(
+                      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(dw),
+                      "l"(dal), "l"(db), "r"(kIdesc), "r"(1u));
+                }
               }
               if (!ta.resident) {
                 asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -507,7 +523,7 @@ __global__ void __launch_bounds__(288, 1) k_pinn_chain_tc2(PinnTcArgs ta) {
     __syncwarp();
   } else {  // ---------------- epilogue warpgroup wg: tile wg of this CTA
     const int tw = t & 127;
-    T *sAw = sA + (size_t)wg * TILE * W;
+    T *sAw = sA + (size_t)(wg * NP) * TILE * W;
     const uint32_t tlane = tmem + (uint32_t)(wg * W) + ((uint32_t)(32 * (warp & 3)) << 16);
     const float *W0 = sP, *b0 = sP + W * IN;
     const float *Wo = sP + W * IN + W + (size_t)(a.LH - 1) * W;
@@ -516,6 +532,13 @@ __global__ void __launch_bounds__(288, 1) k_pinn_chain_tc2(PinnTcArgs ta) {
       const size_t off = cm_offset(tw, c0, W);
       *reinterpret_cast<uint4 *>(sAw + off) =
           make_uint4(pack2<T>(h[0], h[1]), pack2<T>(h[2], h[3]), pack2<T>(h[4], h[5]), pack2<T>(h[6], h[7]));
+      if (SPLIT) {
+        float lo[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) lo[q] = h[q] - __half2float(__float2half_rn(h[q]));
+        *reinterpret_cast<uint4 *>(sAw + (size_t)TILE * W + off) = make_uint4(
+            pack2<T>(lo[0], lo[1]), pack2<T>(lo[2], lo[3]), pack2<T>(lo[4], lo[5]), pack2<T>(lo[6], lo[7]));
+      }
     };
     // fixed-order sum of (num, den) over the 256 epilogue threads; valid in thread 0
     auto reduce256 = [&](double &num, double &den) {
@@ -607,7 +630,7 @@ __global__ void __launch_bounds__(288, 1) k_pinn_chain_tc2(PinnTcArgs ta) {
           float v[32];
           tmem_ld32(tlane + (uint32_t)c0, v);
 #pragma unroll
-          for (int q = 0; q < 32; ++q) v[q] = act_tc<ACT, !H16>(v[q] + bl[c0 + q]);
+          for (int q = 0; q < 32; ++q) v[q] = act_tc<ACT, !H16 && !SPLIT>(v[q] + bl[c0 + q]);
           if (last) {
 #pragma unroll
             for (int q = 0; q < 32; ++q) y = fmaf(Wo[c0 + q], v[q], y);
@@ -725,31 +748,44 @@ void pinn_tc_pack(const float *Wl, int W, int mode, uint16_t *out) {
 }
 
 // ping-pong kernel (bf16): two A planes; weights resident when they fit, else the 2-chunk ring
-template <bool H16>
+template <bool H16, bool SPLIT>
 static TcKernel tc2_kernel_t(int IN, int W, int act) {
 #define PR_TC2_CASE(IN_, W_) \
-  if (IN == IN_ && W == W_) return act ? k_pinn_chain_tc2<IN_, W_, 1, H16> : k_pinn_chain_tc2<IN_, W_, 0, H16>;
+  if (IN == IN_ && W == W_) return act ? k_pinn_chain_tc2<IN_, W_, 1, H16, SPLIT> : k_pinn_chain_tc2<IN_, W_, 0, H16, SPLIT>;
   PR_TC2_CASE(4, 64) PR_TC2_CASE(4, 128) PR_TC2_CASE(4, 256) PR_TC2_CASE(2, 64) PR_TC2_CASE(2, 128) PR_TC2_CASE(2, 256)
 #undef PR_TC2_CASE
   return nullptr;
 }
 static TcKernel tc2_kernel(int IN, int W, int act, int mode) {
-  return mode == kTcF16 ? tc2_kernel_t<true>(IN, W, act) : tc2_kernel_t<false>(IN, W, act);
+  if (mode == kTcSplit16) return W <= 128 ? tc2_kernel_t<true, true>(IN, W, act) : nullptr;
+  return mode == kTcF16 ? tc2_kernel_t<true, false>(IN, W, act) : tc2_kernel_t<false, false>(IN, W, act);
 }
-static size_t pinn_tc2_smem(int W, int LH, int nfloats, bool *resident) {
-  const size_t a = 2 * 128 * (size_t)W * 2, chunk = (size_t)W * kTcKC * 2, p = (size_t)nfloats * 4;
+static size_t pinn_tc2_smem(int W, int LH, int nfloats, int np, bool *resident) {
+  const size_t a = 2 * (size_t)np * 128 * W * 2, chunk = (size_t)np * W * kTcKC * 2, p = (size_t)nfloats * 4;
   const size_t all = (size_t)(LH - 1) * (W / kTcKC) * chunk;
   *resident = a + all + p <= 200 * 1024;
   return *resident ? a + all + p : a + kTc2Ring * chunk + p;
 }
-static bool use_pingpong(int mode) {  // the single-pass modes
+// PR_TC_PINGPONG (tuning): 1 (default) every mode, 0 none, 2 the single-pass modes only
+static int pingpong_env() {
   static const int on = getenv("PR_TC_PINGPONG") ? atoi(getenv("PR_TC_PINGPONG")) : 1;
-  return mode != kTcSplit16 && on != 0;
+  return on;
 }
 
+// The ping-pong kernel for nets with enough MMA work per slice to hide the other tile's epilogue
+// ((LH−1)·W² ≥ 24576: 4×64 measured 8.3 vs 9.3 G evals/s, 8×64 4.9 vs 3.5).  Single-pass modes:
+// with resident weights only (with streamed weights — 8×256: 128 KB per layer and tile — both
+// kernels are bound by the weight traffic from L2 and the one-tile kernel, two CTAs per SM, is as
+// fast: 631 vs 610 M evals/s).  Split mode: W ≤ 128 (four A planes).
 static bool tc_uses_pingpong(int W, int LH, int nfloats, int mode, bool *resident2, size_t *smem2) {
-  *smem2 = pinn_tc2_smem(W, LH, nfloats, resident2);
-  return use_pingpong(mode) && *resident2 && (long)(LH - 1) * W * W >= 24576;
+  const int on = pingpong_env();
+  const bool split = mode == kTcSplit16;
+  *smem2 = pinn_tc2_smem(W, LH, nfloats, split ? 2 : 1, resident2);
+  if (on == 0 || (split && on == 2) || (long)(LH - 1) * W * W < 24576) return false;
+  // split: measured at C5 (scripts/tc_split_ab.py) 8×64 resident 24.9 → 14.8 ms, 3×128 streamed
+  // 17.6 → 13.8, but 4×128 / 8×128 streamed 17.8 → 18.6 / 36.6 → 38.0: resident, or ≤ 2 hidden MMA layers
+  if (split) return W <= 128 && *smem2 <= 220 * 1024 && (*resident2 || LH <= 3);
+  return *resident2;
 }
 int pinn_tc_points_per_cta(int W, int LH, int nfloats, int mode) {
   bool r2 = false;
