@@ -30,6 +30,9 @@ struct ResidentArgs {
   int M, Mp, B;
   // factors of the scheme used by this launch: [nsets][Mp] each (fp64)
   const double *fm, *fip, *fcu;
+  const double *zz;         // θ = 1: zig-zag factors [6][nsets][Mp] (ip, nml, ncu, iq, ncl, nmu)
+  int nsets;
+  int use_zz;               // 1: the kernels run the zig-zag form (host choice, pipe.cu consistent)
   const int *fset;          // [B] factor-set index per instance
   const double *bcoef;      // [B] dτ (a_M + b_M) of this scheme (boundary term of row M)
   double theta;             // θ of the θ-step (1: implicit Euler; 1/2: Crank–Nicolson)
@@ -74,7 +77,7 @@ __device__ __forceinline__ double g_upper(const ResidentArgs &a, int b, double t
   return a.upper_bc ? 0.0 : a.Lb[b] - a.Kb[b] * exp(-a.rb[b] * tau);
 }
 
-template <int P, int NT, bool CN = false>
+template <int P, int NT, bool CN = false, bool ZZ = false>
 struct Tri {
   static constexpr int NW = NT / 32;
   static constexpr int kShm = 6 * NW + 2;  // doubles of shared scratch per system
@@ -255,6 +258,232 @@ struct Tri {
   }
 };
 
+// ---------------------------------------------------------------- zig-zag implicit Euler (θ = 1)
+// Implicit steps alternate between the LU and the UL factorisation of the same constant matrix
+// M_f = I − dτA (both exact in fp64; constant coefficients).  Step m (LU when m is even)
+// is an elimination sweep and a substitution sweep in opposite directions; the UL step runs them
+// reversed.  So the substitution of step m and the elimination of step m+1 run in the SAME
+// direction and are evaluated as one pass of a 2-state recurrence s_j = A_j s_{j∓1} + a_j (A_j
+// lower triangular: the elimination consumes the substituted value of the same point):
+//   ↓↓ (after an LU step):  x_j = w_j + ncu_j x_{j+1},   w̃_j = iq_j (x_j + bc_j) + nmu_j w̃_{j+1}
+//   ↑↑ (after a UL step):   x_j = w̃_j + ncl_j x_{j−1},   w_j = ip_j (x_j + bc_j) + nml_j w_{j−1}
+// (w = y/p, w̃ = ỹ/q: eliminations in divided form).  An n-step slice is n+1 passes: a lone
+// elimination ↑, n−1 merged passes, a lone substitution — one chunked scan per implicit step
+// instead of two (one barrier instead of two).  Each pass: the thread's P points from a zero
+// entering state (chunk total), a Hillis–Steele warp scan of the 2-vector affine parts whose
+// level coefficients (the lane's composite chunk maps, constant) are precomputed once per kernel,
+// a serial fold over the ≤ NW preceding warp totals (warp maps constant, in shared memory), then
+// the P points again from the exact entering state.  The lone passes use the same scan with one
+// component zero (lower-triangular maps compose their diagonal entries independently).
+template <int P, int NT>
+struct Tri<P, NT, false, true> {
+  static constexpr int NW = NT / 32;
+  // shared per system: per direction [NW][2] pass totals + [NW][3] constant warp maps
+  static constexpr int kShm = 10 * NW + 2;
+  double ip[P], nml[P], ncu[P], iq[P], ncl[P], nmu[P];
+  double uC[5][3], dC[5][3];  // level coefficients (lane's composite at the level, 0 without predecessor)
+  double uX[3], dX[3];        // exclusive maps (identity for the first lane in pass order)
+  double uA11, uA21, uA22, dA11, dA21, dA22;  // the thread's chunk maps
+  int lane, w;
+
+  __device__ void setup(const ResidentArgs &a, int set, int t, double *sh) {
+    lane = t & 31;
+    w = t >> 5;
+    const size_t ks = (size_t)a.nsets * a.Mp;
+    const double *z = a.zz + (size_t)set * a.Mp;
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      const int j = t * P + i;
+      const bool in = j < a.Mp;  // rows M..Mp−1 are identity in the table; beyond Mp too
+      ip[i] = in ? z[j] : 1.0;
+      nml[i] = in ? z[ks + j] : 0.0;
+      ncu[i] = in ? z[2 * ks + j] : 0.0;
+      iq[i] = in ? z[3 * ks + j] : 1.0;
+      ncl[i] = in ? z[4 * ks + j] : 0.0;
+      nmu[i] = in ? z[5 * ks + j] : 0.0;
+    }
+    // chunk maps, composed in pass order: M ← A_i · M
+    double m11 = 1.0, m21 = 0.0, m22 = 1.0;
+#pragma unroll
+    for (int i = P - 1; i >= 0; --i) {  // ↓↓: A = [[ncu, 0], [iq·ncu, nmu]]
+      const double a21 = iq[i] * ncu[i];
+      m21 = a21 * m11 + nmu[i] * m21;
+      m11 *= ncu[i];
+      m22 *= nmu[i];
+    }
+    dA11 = m11, dA21 = m21, dA22 = m22;
+    m11 = 1.0, m21 = 0.0, m22 = 1.0;
+#pragma unroll
+    for (int i = 0; i < P; ++i) {  // ↑↑: A = [[ncl, 0], [ip·ncl, nml]]
+      const double a21 = ip[i] * ncl[i];
+      m21 = a21 * m11 + nml[i] * m21;
+      m11 *= ncl[i];
+      m22 *= nml[i];
+    }
+    uA11 = m11, uA21 = m21, uA22 = m22;
+    levels<true>(uA11, uA21, uA22, uC, uX, sh);
+    levels<false>(dA11, dA21, dA22, dC, dX, sh);
+  }
+  // the warp scan of the (constant) chunk maps: per level the lane's composite before combining
+  // (0 if it has no predecessor at that distance), the exclusive map, and the warp total
+  template <bool UP>
+  __device__ __forceinline__ void levels(double m11, double m21, double m22, double (&C)[5][3], double (&X)[3],
+                                         double *sh) {
+#pragma unroll
+    for (int l = 0; l < 5; ++l) {
+      const int d = 1 << l;
+      const double p11 = UP ? __shfl_up_sync(kFull, m11, d) : __shfl_down_sync(kFull, m11, d);
+      const double p21 = UP ? __shfl_up_sync(kFull, m21, d) : __shfl_down_sync(kFull, m21, d);
+      const double p22 = UP ? __shfl_up_sync(kFull, m22, d) : __shfl_down_sync(kFull, m22, d);
+      const bool has = UP ? lane >= d : lane + d <= 31;
+      C[l][0] = has ? m11 : 0.0;
+      C[l][1] = has ? m21 : 0.0;
+      C[l][2] = has ? m22 : 0.0;
+      if (has) {
+        m21 = fma(m21, p11, m22 * p21);
+        m11 *= p11;
+        m22 *= p22;
+      }
+    }
+    X[0] = UP ? __shfl_up_sync(kFull, m11, 1) : __shfl_down_sync(kFull, m11, 1);
+    X[1] = UP ? __shfl_up_sync(kFull, m21, 1) : __shfl_down_sync(kFull, m21, 1);
+    X[2] = UP ? __shfl_up_sync(kFull, m22, 1) : __shfl_down_sync(kFull, m22, 1);
+    if (lane == (UP ? 0 : 31)) X[0] = 1.0, X[1] = 0.0, X[2] = 1.0;
+    if (NW > 1 && lane == (UP ? 31 : 0)) {
+      double *o = sh + (UP ? 0 : 5 * NW) + 2 * NW + 3 * w;  // constant warp map of this direction
+      o[0] = m11, o[1] = m21, o[2] = m22;
+    }
+  }
+  __device__ void fold_setup(const double *) {}
+
+  // entering state of this thread's chunk for a pass in direction UP from the chunk totals (s1, s2)
+  template <bool UP>
+  __device__ __forceinline__ void enter(double s1, double s2, double *sh, double &e1, double &e2) const {
+    const double(&C)[5][3] = UP ? uC : dC;
+    const double(&X)[3] = UP ? uX : dX;
+#pragma unroll
+    for (int l = 0; l < 5; ++l) {
+      const int d = 1 << l;
+      const double q1 = UP ? __shfl_up_sync(kFull, s1, d) : __shfl_down_sync(kFull, s1, d);
+      const double q2 = UP ? __shfl_up_sync(kFull, s2, d) : __shfl_down_sync(kFull, s2, d);
+      s2 = fma(C[l][1], q1, fma(C[l][2], q2, s2));  // coefficient 0 without predecessor: s unchanged
+      s1 = fma(C[l][0], q1, s1);
+    }
+    double xs1 = UP ? __shfl_up_sync(kFull, s1, 1) : __shfl_down_sync(kFull, s1, 1);
+    double xs2 = UP ? __shfl_up_sync(kFull, s2, 1) : __shfl_down_sync(kFull, s2, 1);
+    if (lane == (UP ? 0 : 31)) xs1 = 0.0, xs2 = 0.0;
+    double i1 = 0.0, i2 = 0.0;
+    if (NW > 1) {
+      double *tot = sh + (UP ? 0 : 5 * NW);  // [NW][2] pass totals, then [NW][3] warp maps
+      if (lane == (UP ? 31 : 0)) tot[2 * w] = s1, tot[2 * w + 1] = s2;
+      PR_TRI_SYNC();
+      const double *mp = tot + 2 * NW;
+      // every warp's total and map loaded at once, then the serial composition over the
+      // predecessors in pass order (predicated: the same fixed order for every warp)
+      double t1[NW], t2[NW], a11[NW], a21[NW], a22[NW];
+#pragma unroll
+      for (int q = 0; q < NW; ++q) {
+        t1[q] = tot[2 * q], t2[q] = tot[2 * q + 1];
+        a11[q] = mp[3 * q], a21[q] = mp[3 * q + 1], a22[q] = mp[3 * q + 2];
+      }
+#pragma unroll
+      for (int k = 0; k < NW; ++k) {
+        const int q = UP ? k : NW - 1 - k;
+        if (UP ? q < w : q > w) {
+          i2 = fma(a21[q], i1, fma(a22[q], i2, t2[q]));
+          i1 = fma(a11[q], i1, t1[q]);
+        }
+      }
+    }
+    e2 = fma(X[1], i1, fma(X[2], i2, xs2));
+    e1 = fma(X[0], i1, xs1);
+  }
+
+  // ↓↓: x (LU substitution of the previous step) and w̃ (UL elimination of this step, bc at bc_i)
+  __device__ __forceinline__ void pass_down2(double (&v)[P], int bc_i, double bcg, double *sh) const {
+    double x = 0.0, z = 0.0;
+#pragma unroll
+    for (int i = P - 1; i >= 0; --i) {
+      x = fma(ncu[i], x, v[i]);
+      z = fma(nmu[i], z, iq[i] * (i == bc_i ? x + bcg : x));
+    }
+    double e1, e2;
+    enter<false>(x, z, sh, e1, e2);
+    x = e1, z = e2;
+#pragma unroll
+    for (int i = P - 1; i >= 0; --i) {
+      x = fma(ncu[i], x, v[i]);
+      z = fma(nmu[i], z, iq[i] * (i == bc_i ? x + bcg : x));
+      v[i] = z;
+    }
+  }
+  // ↑↑: x (UL substitution of the previous step) and w (LU elimination of this step)
+  __device__ __forceinline__ void pass_up2(double (&v)[P], int bc_i, double bcg, double *sh) const {
+    double x = 0.0, z = 0.0;
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      x = fma(ncl[i], x, v[i]);
+      z = fma(nml[i], z, ip[i] * (i == bc_i ? x + bcg : x));
+    }
+    double e1, e2;
+    enter<true>(x, z, sh, e1, e2);
+    x = e1, z = e2;
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      x = fma(ncl[i], x, v[i]);
+      z = fma(nml[i], z, ip[i] * (i == bc_i ? x + bcg : x));
+      v[i] = z;
+    }
+  }
+  // lone LU elimination ↑ (first step of a slice): w_j = ip_j (x_j + bc_j) + nml_j w_{j−1}
+  __device__ __forceinline__ void pass_up_elim(double (&v)[P], int bc_i, double bcg, double *sh) const {
+    double z = 0.0;
+#pragma unroll
+    for (int i = 0; i < P; ++i) z = fma(nml[i], z, ip[i] * (i == bc_i ? v[i] + bcg : v[i]));
+    double e1, e2;
+    enter<true>(0.0, z, sh, e1, e2);  // first component 0: the (2,2) entries carry the scan
+    z = e2;
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      z = fma(nml[i], z, ip[i] * (i == bc_i ? v[i] + bcg : v[i]));
+      v[i] = z;
+    }
+  }
+  // lone substitution of the last step: LU (↓, x_j = w_j + ncu_j x_{j+1}) or UL (↑)
+  template <bool UP>
+  __device__ __forceinline__ void pass_sub(double (&v)[P], double *sh) const {
+    double x = 0.0;
+    if (UP) {
+#pragma unroll
+      for (int i = 0; i < P; ++i) x = fma(ncl[i], x, v[i]);
+    } else {
+#pragma unroll
+      for (int i = P - 1; i >= 0; --i) x = fma(ncu[i], x, v[i]);
+    }
+    double e1, e2;
+    enter<UP>(x, 0.0, sh, e1, e2);  // the (1,1) entries carry the scan; component 2 is ignored
+    x = e1;
+    if (UP) {
+#pragma unroll
+      for (int i = 0; i < P; ++i) v[i] = x = fma(ncl[i], x, v[i]);
+    } else {
+#pragma unroll
+      for (int i = P - 1; i >= 0; --i) v[i] = x = fma(ncu[i], x, v[i]);
+    }
+  }
+  // implicit step m of the slice (its elimination merged with the substitution of step m−1)
+  __device__ __forceinline__ void zz_step(int m, double (&v)[P], int bc_i, double bcg, double *sh) const {
+    if (m == 0) pass_up_elim(v, bc_i, bcg, sh);
+    else if (m & 1) pass_down2(v, bc_i, bcg, sh);
+    else pass_up2(v, bc_i, bcg, sh);
+  }
+  // after the last step n−1: its substitution (LU ↓ when n−1 is even, UL ↑ when odd)
+  __device__ __forceinline__ void zz_finish(int n, double (&v)[P], double *sh) const {
+    if ((n - 1) & 1) pass_sub<true>(v, sh);
+    else pass_sub<false>(v, sh);
+  }
+};
+
 // Fixed-order block reduction of two doubles over the threads of one system (NT threads).
 template <int NT>
 __device__ __forceinline__ void sys_reduce2(double &a, double &b, int t, double *red) {
@@ -279,8 +508,8 @@ constexpr int kBcChunk = 128;  // boundary terms tabulated per chunk of implicit
 // All implicit steps of slice n.  The boundary term dτ(a_M+b_M)·g(τ_{m+1}) of each step needs an
 // fp64 exp; it is tabulated in shared memory for kBcChunk steps at a time (one exp per thread)
 // so no exp sits on the per-step critical path.
-template <int P, int NT, bool CN>
-__device__ __forceinline__ void run_steps(Tri<P, NT, CN> &tri, const ResidentArgs &a, int b, int n,
+template <int P, int NT, bool CN, bool ZZ = false>
+__device__ __forceinline__ void run_steps(Tri<P, NT, CN, ZZ> &tri, const ResidentArgs &a, int b, int n,
                                           int t, double (&x)[P], double *sh, double *bct) {
   const int bc_t = (a.M - 1) / P, bc_ip = (a.M - 1) % P;
   const int bc_i = (t == bc_t) ? bc_ip : -1;
@@ -300,15 +529,20 @@ __device__ __forceinline__ void run_steps(Tri<P, NT, CN> &tri, const ResidentArg
     PR_TRI_SYNC();
     const int mend = min(a.steps - m0, kBcChunk);
 #pragma unroll 1
-    for (int mm = 0; mm < mend; ++mm) tri.step(x, bc_i, bc_i >= 0 ? bct[mm] : 0.0, sh);
+    if constexpr (ZZ) {
+      for (int mm = 0; mm < mend; ++mm) tri.zz_step(m0 + mm, x, bc_i, bc_i >= 0 ? bct[mm] : 0.0, sh);
+    } else {
+      for (int mm = 0; mm < mend; ++mm) tri.step(x, bc_i, bc_i >= 0 ? bct[mm] : 0.0, sh);
+    }
   }
+  if constexpr (ZZ) tri.zz_finish(a.steps, x, sh);
 }
 
 // SWEEP: every (slice, instance) system independently; blockIdx.x = system group.
-template <int P, int NT, int SPB, bool CN>
+template <int P, int NT, int SPB, bool CN, bool ZZ = false>
 __global__ void __launch_bounds__(NT * SPB) k_fine_sweep(ResidentArgs a) {
   constexpr int NW = NT / 32;
-  __shared__ double shm[SPB][Tri<P, NT, CN>::kShm];
+  __shared__ double shm[SPB][Tri<P, NT, CN, ZZ>::kShm];
   __shared__ double bctab[SPB][kBcChunk];
   const int sys = blockIdx.x * SPB + threadIdx.x / NT;
   const int t = threadIdx.x % NT;
@@ -317,7 +551,7 @@ __global__ void __launch_bounds__(NT * SPB) k_fine_sweep(ResidentArgs a) {
   const int s = live ? sys : nsys - 1;  // dead systems shadow a live one (barriers stay uniform)
   const int ln = a.ln0 + s / a.B, b = s % a.B;
   double *sh = shm[threadIdx.x / NT];
-  Tri<P, NT, CN> tri;
+  Tri<P, NT, CN, ZZ> tri;
   tri.setup(a, a.fset[b], t, sh);
   if (NW > 1) PR_TRI_SYNC();
   tri.fold_setup(sh);
@@ -328,7 +562,7 @@ __global__ void __launch_bounds__(NT * SPB) k_fine_sweep(ResidentArgs a) {
     const int j = t * P + i;
     x[i] = (j < a.M) ? (double)u[j] : 0.0;
   }
-  run_steps<P, NT, CN>(tri, a, b, a.n_base + ln, t, x, sh, bctab[threadIdx.x / NT]);
+  run_steps<P, NT, CN, ZZ>(tri, a, b, a.n_base + ln, t, x, sh, bctab[threadIdx.x / NT]);
   if (!live) return;
   const size_t row = ((size_t)ln * a.B + b) * a.Mp;
   if (a.Fout) {
@@ -358,10 +592,10 @@ __global__ void __launch_bounds__(NT * SPB) k_fine_sweep(ResidentArgs a) {
 
 // CHAIN: one system per instance walks slices c_ln0..c_ln1-1 serially (numerical coarse
 // G with the Parareal correction; or the serial fine solve, Eq. 6).
-template <int P, int NT, int SPB, bool CN>
+template <int P, int NT, int SPB, bool CN, bool ZZ = false>
 __global__ void __launch_bounds__(NT * SPB) k_resident_chain(ResidentArgs a) {
   constexpr int NW = NT / 32;
-  __shared__ double shm[SPB][Tri<P, NT, CN>::kShm];
+  __shared__ double shm[SPB][Tri<P, NT, CN, ZZ>::kShm];
   __shared__ double red[SPB][2 * NW + 2];
   __shared__ double bctab[SPB][kBcChunk];
   const int sys = blockIdx.x * SPB + threadIdx.x / NT;
@@ -370,7 +604,7 @@ __global__ void __launch_bounds__(NT * SPB) k_resident_chain(ResidentArgs a) {
   const int b = live ? sys : a.B - 1;
   double *sh = shm[threadIdx.x / NT];
   double *rd = red[threadIdx.x / NT];
-  Tri<P, NT, CN> tri;
+  Tri<P, NT, CN, ZZ> tri;
   tri.setup(a, a.fset[b], t, sh);
   if (NW > 1) PR_TRI_SYNC();
   tri.fold_setup(sh);
@@ -415,7 +649,7 @@ __global__ void __launch_bounds__(NT * SPB) k_resident_chain(ResidentArgs a) {
   }
 #pragma unroll 1
   for (int ln = a.c_ln0; ln < a.c_ln1; ++ln) {
-    run_steps<P, NT, CN>(tri, a, b, a.n_base + ln, t, x, sh, bctab[threadIdx.x / NT]);
+    run_steps<P, NT, CN, ZZ>(tri, a, b, a.n_base + ln, t, x, sh, bctab[threadIdx.x / NT]);
     const size_t row = (size_t)ln * sstride + (size_t)b * a.Mp;
     float *un = a.Uw + (size_t)(ln + 1) * a.ustride + (size_t)b * a.Mp;
     double num = 0.0, den = 0.0;

@@ -97,6 +97,7 @@ struct Scheme {
   double dtau = 0;
   int steps = 0;
   double *m = nullptr, *ip = nullptr, *cu = nullptr;  // device [nsets][Mp] (K1)
+  double *zz = nullptr;  // device [6][nsets][Mp] K1 zig-zag factors (θ = 1): ip, nml, ncu (LU), iq, ncl, nmu (UL)
   double *iip = nullptr;                            // device [nsets][Mt] 1/p, interleaved (K2)
   double *coef = nullptr;                           // device [nsets][2] dτr/2, dτσ²/2 (K2)
   double *thrP = nullptr;                           // device [2][nsets][Mt/kSPS] (K2 in-tile prefix multipliers)
@@ -312,6 +313,44 @@ pr_status factorise(pr_ctx *c, double dtau, std::vector<double> &m, std::vector<
   return PR_OK;
 }
 
+// K1 zig-zag factors of I − dτA (θ = 1; fine_resident.cuh "zig-zag"): the LU factorisation in
+// w = y/p form (w_j = ip_j r_j + nml_j w_{j−1}; back substitution x_j = w_j + ncu_j x_{j+1}) and the
+// UL factorisation (pivots q_j from the bottom row up) in w̃ = ỹ/q form (w̃_j = iq_j r_j + nmu_j w̃_{j+1};
+// forward substitution x_j = w̃_j + ncl_j x_{j−1}).  Layout [6][nsets][Mp], padding rows identity.
+pr_status factorise_zz(pr_ctx *c, double dtau, std::vector<double> &zz) {
+  const int M = c->M, Mp = c->Mp, ns = c->nsets;
+  zz.assign((size_t)6 * ns * Mp, 0.0);
+  auto at = [&](int k, int s, int i) -> double & { return zz[((size_t)k * ns + s) * Mp + i]; };
+  std::vector<double> d(M), l(M), u(M), q(M);
+  for (int s = 0; s < ns; ++s) {
+    const double sg = c->sets[s].first, rr = c->sets[s].second;
+    for (int i = 0; i < M; ++i) {
+      const double j = i + 1, a = 0.5 * sg * sg * j * j, b = 0.5 * rr * j;
+      d[i] = 1.0 + dtau * (2.0 * a + rr);
+      l[i] = i > 0 ? -dtau * (a - b) : 0.0;       // coupling to V_{j−1} (none in row 1: V_0 = 0)
+      u[i] = i < M - 1 ? -dtau * (a + b) : 0.0;   // coupling to V_{j+1} (row M: the boundary term)
+    }
+    double p = 0.0;
+    for (int i = 0; i < M; ++i) {
+      p = i > 0 ? d[i] - l[i] / p * u[i - 1] : d[i];
+      if (!(p > 0.0)) return fail(c, PR_ERR_NUMERICAL, fmt("non-positive LU pivot %g at j=%d", p, i + 1));
+      at(0, s, i) = 1.0 / p;
+      at(1, s, i) = -l[i] / p;
+      at(2, s, i) = -u[i] / p;
+    }
+    q[M - 1] = d[M - 1];
+    for (int i = M - 2; i >= 0; --i) q[i] = d[i] - u[i] / q[i + 1] * l[i + 1];
+    for (int i = 0; i < M; ++i) {
+      if (!(q[i] > 0.0)) return fail(c, PR_ERR_NUMERICAL, fmt("non-positive UL pivot %g at j=%d", q[i], i + 1));
+      at(3, s, i) = 1.0 / q[i];
+      at(4, s, i) = -l[i] / q[i];
+      at(5, s, i) = -u[i] / q[i];
+    }
+    for (int i = M; i < Mp; ++i) at(0, s, i) = at(3, s, i) = 1.0;
+  }
+  return PR_OK;
+}
+
 pr_status upload_scheme(pr_ctx *c, Scheme &sc, int steps, double theta) {
   sc.steps = steps;
   sc.dtau = c->dT / steps;
@@ -327,6 +366,13 @@ pr_status upload_scheme(pr_ctx *c, Scheme &sc, int steps, double theta) {
   CU(cudaMemcpy(sc.m, m.data(), n * sizeof(double), cudaMemcpyHostToDevice));
   CU(cudaMemcpy(sc.ip, ip.data(), n * sizeof(double), cudaMemcpyHostToDevice));
   CU(cudaMemcpy(sc.cu, cu.data(), n * sizeof(double), cudaMemcpyHostToDevice));
+  if (theta == 1.0 && c->M <= kResidentMaxM) {
+    std::vector<double> zz;
+    st = factorise_zz(c, dti, zz);
+    if (st) return st;
+    CU(cudaMalloc(&sc.zz, zz.size() * sizeof(double)));
+    CU(cudaMemcpy(sc.zz, zz.data(), zz.size() * sizeof(double), cudaMemcpyHostToDevice));
+  }
   // K2: 1/p in the thread-interleaved layout (1 beyond M), the closed-form off-diagonal
   // coefficients, and the per-thread multipliers Π(−l_j/p_j) (dir 0) / Π(−u_j/p_j) (dir 1)
   const int Mt = pr::streamed_Mt(c->M);
@@ -461,6 +507,7 @@ void free_scheme(Scheme &s) {
   cudaFree(s.m);
   cudaFree(s.ip);
   cudaFree(s.cu);
+  cudaFree(s.zz);
   cudaFree(s.bcoef);
   cudaFree(s.ecoef);
   cudaFree(s.PL);
@@ -548,6 +595,19 @@ cudaEvent_t next_event(pr_ctx *c) {
 }
 
 // ---------------------------------------------------------------- resident launches
+bool use_split_pinn(const pr_ctx *c);
+int split_G(const pr_ctx *c);
+// The K1 kernels run the zig-zag form (fine_resident.cuh) for implicit Euler schemes, except in
+// problems whose PINN chain is a group kernel: the pipelined kernel of those has 384-thread CTAs
+// (168 registers per thread), too few for the zig-zag solver, and the blocking kernels of a
+// problem must do the pipelined kernel's arithmetic (bitwise-equal schedules).
+bool use_zz(const pr_ctx *c, const Scheme &sc) {
+  if (sc.theta != 1.0 || !sc.zz) return false;
+  if (c->coarse == PR_COARSE_PINN && c->have_pinn && !c->tc && use_split_pinn(c) &&
+      pr::pinn_split_is_group(c->W, split_G(c)))
+    return false;
+  return true;
+}
 pr::ResidentArgs base_args(pr_ctx *c, const Scheme &sc) {
   pr::ResidentArgs a;
   std::memset(&a, 0, sizeof a);
@@ -557,6 +617,9 @@ pr::ResidentArgs base_args(pr_ctx *c, const Scheme &sc) {
   a.fm = sc.m;
   a.fip = sc.ip;
   a.fcu = sc.cu;
+  a.zz = sc.zz;
+  a.nsets = c->nsets;
+  a.use_zz = use_zz(c, sc) ? 1 : 0;
   a.fset = c->d_fset;
   a.bcoef = sc.bcoef;
   a.theta = sc.theta;

@@ -252,10 +252,13 @@ template <int P, bool CN, int NWC>
 __device__ void fine_role(const PipeArgs &pa, int n, int b) {
   constexpr int NT = 128;
   const ResidentArgs &a = pa.r;
-  __shared__ double sh[Tri<P, NT, CN>::kShm];
+  // the zig-zag form where the 128-thread chain CTAs leave the registers for it (NWC = 4); the
+  // host sets ResidentArgs::use_zz for the blocking kernels of the same problem identically
+  constexpr bool ZZ = !CN && NWC == 4;
+  __shared__ double sh[Tri<P, NT, CN, ZZ>::kShm];
   __shared__ double bct[kBcChunk];
   const int t = threadIdx.x;
-  Tri<P, NT, CN> tri;
+  Tri<P, NT, CN, ZZ> tri;
   tri.setup(a, a.fset[b], t, sh);
   PR_TRI_SYNC();
   tri.fold_setup(sh);
@@ -276,7 +279,7 @@ __device__ void fine_role(const PipeArgs &pa, int n, int b) {
     PR_TRI_SYNC();
     if (t == 0) publish_set(floaded + n, k);
     if (pa.trace && b == 0 && t == 0) pa.trace[((size_t)k * pa.N + n) * 3 + 1] = gtimer();
-    run_steps<P, NT, CN>(tri, a, b, a.n_base + n, t, x, sh, bct);
+    run_steps<P, NT, CN, ZZ>(tri, a, b, a.n_base + n, t, x, sh, bct);
     if (n == k - 1) {  // F̂_{k−1}: copied into U^k_k by chain k
       float *o = a.Fk + (size_t)b * a.Mp;
 #pragma unroll
@@ -308,11 +311,11 @@ template <int P>
 __device__ void chain_role_num(const PipeArgs &pa, int k, int b) {
   constexpr int NT = 128, NW = NT / 32;
   const ResidentArgs &a = pa.rc;
-  __shared__ double shc[Tri<P, NT, false>::kShm];
+  __shared__ double shc[Tri<P, NT, false, true>::kShm];
   __shared__ double bcc[kBcChunk];
   __shared__ double rdc[2 * NW + 2];
   const int t = threadIdx.x;
-  Tri<P, NT, false> tri;
+  Tri<P, NT, false, true> tri;  // the coarse scheme is implicit Euler: zig-zag (use_zz on the host too)
   tri.setup(a, a.fset[b], t, shc);
   PR_TRI_SYNC();
   tri.fold_setup(shc);
@@ -368,7 +371,7 @@ __device__ void chain_role_num(const PipeArgs &pa, int k, int b) {
   }
 #pragma unroll 1
   for (int n = n0; n < pa.N; ++n) {
-    run_steps<P, NT, false>(tri, a, b, a.n_base + n, t, x, shc, bcc);  // g = G(U_n)
+    run_steps<P, NT, false, true>(tri, a, b, a.n_base + n, t, x, shc, bcc);  // g = G(U_n)
     if (k > 0) {
       if (t == 0) {
         wait_geq(fdone + n, k);                               // D_n of this iteration

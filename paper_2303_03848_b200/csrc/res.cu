@@ -8,11 +8,14 @@ template <int P, int NT, int SPB>
 static void launch_res(bool chain, const ResidentArgs &a, int nsys, cudaStream_t s) {
   const int grid = (nsys + SPB - 1) / SPB;
   const bool cn = a.theta != 1.0;  // θ-step with an explicit part (Crank–Nicolson, NEXT-1)
+  const bool zz = !cn && a.use_zz;  // zig-zag LU/UL form (θ = 1; fine_resident.cuh)
   if (chain) {
     if (cn) k_resident_chain<P, NT, SPB, true><<<grid, NT * SPB, 0, s>>>(a);
+    else if (zz) k_resident_chain<P, NT, SPB, false, true><<<grid, NT * SPB, 0, s>>>(a);
     else k_resident_chain<P, NT, SPB, false><<<grid, NT * SPB, 0, s>>>(a);
   } else {
     if (cn) k_fine_sweep<P, NT, SPB, true><<<grid, NT * SPB, 0, s>>>(a);
+    else if (zz) k_fine_sweep<P, NT, SPB, false, true><<<grid, NT * SPB, 0, s>>>(a);
     else k_fine_sweep<P, NT, SPB, false><<<grid, NT * SPB, 0, s>>>(a);
   }
 }
