@@ -36,6 +36,13 @@ elif case == "k4pp":
 elif case == "c4":
     p = synth.portfolio(n_k=4, n_s=4, M=256, N=16, coarse=synth.COARSE_IMPLICIT_EULER, max_iter=2, tol=0.0,
                         fine_steps=10)
+elif case == "train":  # PINN trainer: k_train_grad (shared rows, stash) and k_adam (completion ticket)
+    from paper_2303_03848_b200 import pinn_train
+    mk = dict(K=1.0, sigma=0.2, r=0.05, T=1.0, L=4.0)
+    with pinn_train.Trainer(synth.pinn2_net([2, 20, 20, 20, 1]), mk, synth.collocation(mk, 2000, 200, 200), batches=3) as tr:
+        tr.epochs(2, 1e-2)
+        print("train loss", tr.loss(), tr.batch_gradient(1)[0])
+    raise SystemExit(0)
 else:
     raise SystemExit("unknown case " + case)
 with parareal.Context(p) as c:
