@@ -9,7 +9,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libparareal.so")
-UNITS = ["parareal.cu", "res.cu", "streamed.cu", "pinn_smem.cu", "pinn_param.cu", "misc.cu", "pipe.cu", "pinn_tc.cu", "pinn_train.cu"]
+UNITS = ["parareal.cu", "res.cu", "streamed.cu", "pinn_smem.cu", "pinn_param.cu", "misc.cu", "pipe.cu", "pinn_tc.cu", "pinn_train.cu", "fine_grid.cu"]
 HEADERS = ["launch.h", "fine_resident.cuh", "fine_streamed.cuh", "pinn_chain.cuh"]
 SOURCES = UNITS + HEADERS
 HEADER = os.path.join(ROOT, "include", "parareal.h")

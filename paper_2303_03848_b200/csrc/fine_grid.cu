@@ -1,0 +1,477 @@
+// fine_grid.cu — K2R: the grid-resident fine sweep for large grids (SURVEY NEXT-4 "whole-GPU
+// resident fine solver"; the large-M counterpart of K1).
+//
+// Same mathematics as K1's zig-zag form (fine_resident.cuh): implicit Euler steps of slice n
+// alternate between the LU and the UL factorisation of the constant matrix
+// M_f = I − dτA, so the substitution of step m and the elimination of step m+1 form one pass of a
+// 2-state recurrence; an n-step slice is n+1 passes.  Here one system (2^20 points at C3) spans
+// the whole GPU: CTA c (one per SM, cooperative launch) owns a contiguous range of 256·PT points,
+// thread t of it PT consecutive points, and NS systems (slices) are solved together.  The state
+// stays in registers (fp64) for all passes of a slice group — HBM is touched once per slice (load
+// U_n, store D_n) instead of 16 B per point and step — and the factors 1/p_j, 1/q_j of the CTA's
+// points sit in shared memory; the off-diagonals come from the closed forms
+// l_j = −J(c1·J − c0), u_j = −J(c1·J + c0) (J = j+1, c0 = dτr/2, c1 = dτσ²/2).
+//
+// One pass: each thread runs its points from a zero entering state (chunk totals), a warp scan
+// of the 2-vector affine parts with per-lane level coefficients precomputed at kernel start, a
+// fold over the warps (constant warp maps in shared memory), the CTA total is published
+// (per-pass slot + release flag) and the entering state of the CTA is composed from the totals of
+// its W predecessors in pass direction (decoupled look-back: every CTA publishes before it waits,
+// so the wait is one flag propagation; W from the host, where the product of the predecessors'
+// maps falls below 1e-24 — the same truncation as K2; the weights Π of the CTA maps in between
+// are host tables), then each thread reruns its points from its exact entering state.
+#include "launch.h"
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <type_traits>
+
+namespace pr {
+namespace {
+
+
+constexpr int kGT = 256;        // threads per CTA
+constexpr int kGW = kGT / 32;   // warps per CTA
+constexpr long long kSpinMax = 1ll << 28;  // look-back wait bound (then the solve fails, no hang)
+
+__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned *p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long v;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned *p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <int PT, int NS>
+struct GridSolver {
+  // per-lane level coefficients (the lane's composite map at each level, 0 without predecessor)
+  // and exclusive maps, for ↑↑ (index 0) and ↓↓ (index 1)
+  double C[2][5][3], X[2][3];
+  int t, lane, w, c, j0;
+
+  // closed-form off-diagonals and factors of point j (padding beyond M: identity, no coupling)
+  __device__ __forceinline__ void mults(const GridArgs &a, const double *sip, const double *siq, int i, double &ip,
+                                        double &iq, double &l, double &u) const {
+    const int j = j0 + i;
+    const double J = (double)(j + 1);
+    ip = sip[t * PT + i];
+    iq = siq[t * PT + i];
+    l = (j >= 1 && j < a.M) ? -J * fma(a.c1, J, -a.c0) : 0.0;
+    u = (j < a.M - 1) ? -J * fma(a.c1, J, a.c0) : 0.0;
+  }
+};
+
+}  // namespace
+
+template <int PT, int NS>
+__global__ void __launch_bounds__(kGT, 1) k_fine_grid(GridArgs a) {
+  extern __shared__ __align__(16) double gsm[];
+  double *sip = gsm, *siq = gsm + kGT * PT;          // this CTA's 1/p, 1/q
+  double *swm = siq + kGT * PT;                        // [2][kGW][3] constant warp maps
+  double *swt = swm + 2 * kGW * 3;                     // [kGW][NS][2] warp totals of the pass
+  double *sE = swt + kGW * NS * 2;                     // [NS][2] CTA entering state
+  double *sbc = sE + NS * 2;                           // [NS][steps] boundary terms
+  GridSolver<PT, NS> g;
+  g.t = threadIdx.x;
+  g.lane = g.t & 31;
+  g.w = g.t >> 5;
+  g.c = blockIdx.x;
+  g.j0 = (g.c * kGT + g.t) * PT;
+  const int nCTA = gridDim.x;
+  const int t = g.t, lane = g.lane, w = g.w, c = g.c;
+  for (int i = t; i < kGT * PT; i += kGT) {
+    const int j = c * kGT * PT + i;
+    sip[i] = j < a.M ? a.ip[j] : 1.0;
+    siq[i] = j < a.M ? a.iq[j] : 1.0;
+  }
+  __syncthreads();
+  // thread chunk maps in pass order: ↑↑ A = [[ncl, 0], [ip·ncl, nml]], ↓↓ A = [[ncu, 0], [iq·ncu, nmu]]
+  {
+    double m[2][3] = {{1.0, 0.0, 1.0}, {1.0, 0.0, 1.0}};
+#pragma unroll
+    for (int i = 0; i < PT; ++i) {  // ↑↑: ascending
+      double ip, iq, l, u;
+      g.mults(a, sip, siq, i, ip, iq, l, u);
+      const double ncl = -l * iq, nml = -l * ip;
+      m[0][1] = fma(ip * ncl, m[0][0], nml * m[0][1]);
+      m[0][0] *= ncl;
+      m[0][2] *= nml;
+    }
+#pragma unroll
+    for (int i = PT - 1; i >= 0; --i) {  // ↓↓: descending
+      double ip, iq, l, u;
+      g.mults(a, sip, siq, i, ip, iq, l, u);
+      const double ncu = -u * ip, nmu = -u * iq;
+      m[1][1] = fma(iq * ncu, m[1][0], nmu * m[1][1]);
+      m[1][0] *= ncu;
+      m[1][2] *= nmu;
+    }
+    // level coefficients, exclusive maps and warp totals (constant) per direction
+#pragma unroll
+    for (int dir = 0; dir < 2; ++dir) {
+      const bool up = dir == 0;
+      double m11 = m[dir][0], m21 = m[dir][1], m22 = m[dir][2];
+#pragma unroll
+      for (int l = 0; l < 5; ++l) {
+        const int d = 1 << l;
+        const double p11 = up ? __shfl_up_sync(kFull, m11, d) : __shfl_down_sync(kFull, m11, d);
+        const double p21 = up ? __shfl_up_sync(kFull, m21, d) : __shfl_down_sync(kFull, m21, d);
+        const double p22 = up ? __shfl_up_sync(kFull, m22, d) : __shfl_down_sync(kFull, m22, d);
+        const bool has = up ? lane >= d : lane + d <= 31;
+        g.C[dir][l][0] = has ? m11 : 0.0;
+        g.C[dir][l][1] = has ? m21 : 0.0;
+        g.C[dir][l][2] = has ? m22 : 0.0;
+        if (has) {
+          m21 = fma(m21, p11, m22 * p21);
+          m11 *= p11;
+          m22 *= p22;
+        }
+      }
+      g.X[dir][0] = up ? __shfl_up_sync(kFull, m11, 1) : __shfl_down_sync(kFull, m11, 1);
+      g.X[dir][1] = up ? __shfl_up_sync(kFull, m21, 1) : __shfl_down_sync(kFull, m21, 1);
+      g.X[dir][2] = up ? __shfl_up_sync(kFull, m22, 1) : __shfl_down_sync(kFull, m22, 1);
+      if (lane == (up ? 0 : 31)) g.X[dir][0] = 1.0, g.X[dir][1] = 0.0, g.X[dir][2] = 1.0;
+      if (lane == (up ? 31 : 0)) {
+        double *o = swm + (dir * kGW + w) * 3;
+        o[0] = m11, o[1] = m21, o[2] = m22;
+      }
+    }
+  }
+  __syncthreads();
+
+  const int ngroups = (a.nsys + NS - 1) / NS;
+  const int bc_t = (a.M - 1) / PT - c * kGT, bc_ip = (a.M - 1) % PT;  // thread / point of row M
+  const int bc_i = (t == bc_t && (a.M - 1) / (kGT * PT) == c) ? bc_ip : -1;
+  unsigned pid = 0;  // passes published so far (flag values)
+  // The closed-form path serves every warp except the one holding row M (the boundary term):
+  // at j = 0 and j = M−1 the closed-form off-diagonal only ever multiplies a zero entering state
+  // (nothing precedes row 1 upward; above row M sit padding points, whose inputs are 0, so they
+  // pass zeros downward), and padding points' maps only ever multiply zeros.  Warp-uniform.
+  const bool fast = !__any_sync(kFull, bc_i >= 0);
+  const double J0 = (double)(g.j0 + 1);
+  for (int grp = 0; grp < ngroups; ++grp) {
+    // ---- inputs and boundary terms of the NS systems (slices ln0 + grp·NS + k)
+    double x[NS][PT];
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+      const int s = grp * NS + k;
+      const float *u = s < a.nsys ? a.U + (size_t)(a.ln0 + s) * a.row : nullptr;
+#pragma unroll
+      for (int i = 0; i < PT; ++i) {
+        const int j = g.j0 + i;
+        x[k][i] = (u && j < a.M) ? (double)u[j] : 0.0;
+      }
+    }
+    for (int q = t; q < NS * a.steps; q += kGT) {
+      const int k = q / a.steps, m = q - k * a.steps;
+      const int n = a.n_base + a.ln0 + grp * NS + k;
+      const double tau1 = (n * a.dT + m * a.dtau) + a.dtau;  // τ_{m+1} of slice n (the oracle's association)
+      sbc[q] = a.upper_bc ? 0.0 : a.bcoef * (a.Lb - a.Kb * exp(-a.rb * tau1));
+    }
+    __syncthreads();
+    // ---- the steps+1 passes
+    for (int m = 0; m <= a.steps; ++m) {
+      // direction and kind: m = 0 lone ↑ elimination; 0 < m < steps merged (odd ↓↓, even ↑↑);
+      // m = steps lone substitution (↓ after an LU step, ↑ after a UL step)
+      const bool last = m == a.steps;
+      // the pass body with direction and kind as compile-time constants (register-resident
+      // coefficients, no per-point selects): kind 0 lone elimination, 1 merged, 2 lone substitution
+      auto pass = [&](auto up_tag, auto kind_tag) {
+      constexpr bool up = decltype(up_tag)::value;
+      constexpr int dir = up ? 0 : 1;
+      constexpr int kind = decltype(kind_tag)::value;
+      constexpr bool elim = kind != 2, subst = kind != 0;
+      double bcg[NS];
+#pragma unroll
+      for (int k = 0; k < NS; ++k) bcg[k] = (bc_i >= 0 && elim) ? sbc[k * a.steps + (m < a.steps ? m : 0)] : 0.0;
+      unsigned long long *tr = a.trace ? a.trace + ((size_t)(pid) * gridDim.x + c) * 5 : nullptr;
+      if (tr && t == 0) tr[0] = gtime();
+      // (1) local totals from a zero entering state
+      double s1[NS], s2[NS];
+#pragma unroll
+      for (int k = 0; k < NS; ++k) s1[k] = 0.0, s2[k] = 0.0;
+      // general point: boundary rows (no l at j = 0, no u at j = M−1), padding, the boundary term
+      auto point = [&](int i, double(&xs)[NS], double(&zs)[NS], bool write) {
+        double ip, iq, l, u;
+        g.mults(a, sip, siq, i, ip, iq, l, u);
+#pragma unroll
+        for (int k = 0; k < NS; ++k) {
+          const double v = x[k][i];
+          double xn, zn = 0.0;
+          if (up) {  // x: UL forward substitution (ncl = −l·iq); z: LU elimination (nml = −l·ip)
+            xn = subst ? fma(-l * iq, xs[k], v) : v;
+            const double r = i == bc_i ? xn + bcg[k] : xn;
+            if (elim) zn = fma(-l * ip, zs[k], ip * r);
+          } else {   // x: LU back substitution (ncu = −u·ip); z: UL elimination (nmu = −u·iq)
+            xn = subst ? fma(-u * ip, xs[k], v) : v;
+            const double r = i == bc_i ? xn + bcg[k] : xn;
+            if (elim) zn = fma(-u * iq, zs[k], iq * r);
+          }
+          if (subst) xs[k] = xn;
+          if (elim) zs[k] = zn;
+          if (write) x[k][i] = elim ? zn : xn;
+        }
+      };
+      // interior point (every point of the thread strictly inside 1 … M−2, no boundary term):
+      // J = J0 + i exactly, only the off-diagonal of this direction, no selects
+      auto point_fast = [&](int i, double(&xs)[NS], double(&zs)[NS], bool write) {
+        const double J = J0 + (double)i;
+        const double ip = sip[t * PT + i], iq = siq[t * PT + i];
+        const double nl = up ? J * fma(a.c1, J, -a.c0) : J * fma(a.c1, J, a.c0);  // −l or −u
+        const double mx = nl * (up ? iq : ip), mz = nl * (up ? ip : iq), fz = up ? ip : iq;
+#pragma unroll
+        for (int k = 0; k < NS; ++k) {
+          const double xn = subst ? fma(mx, xs[k], x[k][i]) : x[k][i];
+          double zn = 0.0;
+          if (elim) zn = fma(mz, zs[k], fz * xn);
+          if (subst) xs[k] = xn;
+          if (elim) zs[k] = zn;
+          if (write) x[k][i] = elim ? zn : xn;
+        }
+      };
+      auto run = [&](double(&xs)[NS], double(&zs)[NS], bool write) {
+        if (fast) {
+          if (up) {
+#pragma unroll
+            for (int i = 0; i < PT; ++i) point_fast(i, xs, zs, write);
+          } else {
+#pragma unroll
+            for (int i = PT - 1; i >= 0; --i) point_fast(i, xs, zs, write);
+          }
+        } else {
+          if (up) {
+#pragma unroll
+            for (int i = 0; i < PT; ++i) point(i, xs, zs, write);
+          } else {
+#pragma unroll
+            for (int i = PT - 1; i >= 0; --i) point(i, xs, zs, write);
+          }
+        }
+      };
+      run(s1, s2, false);
+      // (2) warp scan of the NS 2-vectors with the precomputed level coefficients
+#pragma unroll
+      for (int l = 0; l < 5; ++l) {
+        const int d = 1 << l;
+        const double *Cl = g.C[dir][l];
+#pragma unroll
+        for (int k = 0; k < NS; ++k) {
+          const double q1 = up ? __shfl_up_sync(kFull, s1[k], d) : __shfl_down_sync(kFull, s1[k], d);
+          const double q2 = up ? __shfl_up_sync(kFull, s2[k], d) : __shfl_down_sync(kFull, s2[k], d);
+          s2[k] = fma(Cl[1], q1, fma(Cl[2], q2, s2[k]));
+          s1[k] = fma(Cl[0], q1, s1[k]);
+        }
+      }
+      double xs1[NS], xs2[NS];
+#pragma unroll
+      for (int k = 0; k < NS; ++k) {
+        xs1[k] = up ? __shfl_up_sync(kFull, s1[k], 1) : __shfl_down_sync(kFull, s1[k], 1);
+        xs2[k] = up ? __shfl_up_sync(kFull, s2[k], 1) : __shfl_down_sync(kFull, s2[k], 1);
+        if (lane == (up ? 0 : 31)) xs1[k] = 0.0, xs2[k] = 0.0;
+        if (lane == (up ? 31 : 0)) swt[(w * NS + k) * 2] = s1[k], swt[(w * NS + k) * 2 + 1] = s2[k];
+      }
+      __syncthreads();
+      // (3) this warp's entering within the CTA (fold of the preceding warps' totals), and the
+      //     CTA total (thread 0) → published with the pass id
+      const double *wm = swm + dir * kGW * 3;
+      double f1[NS], f2[NS];
+#pragma unroll
+      for (int k = 0; k < NS; ++k) f1[k] = 0.0, f2[k] = 0.0;
+#pragma unroll
+      for (int kk = 0; kk < kGW; ++kk) {
+        const int q = up ? kk : kGW - 1 - kk;
+        if (up ? q < w : q > w) {
+#pragma unroll
+          for (int k = 0; k < NS; ++k) {
+            const double t1 = swt[(q * NS + k) * 2], t2 = swt[(q * NS + k) * 2 + 1];
+            f2[k] = fma(wm[q * 3 + 1], f1[k], fma(wm[q * 3 + 2], f2[k], t2));
+            f1[k] = fma(wm[q * 3], f1[k], t1);
+          }
+        }
+      }
+      ++pid;
+      // four pass slots: a CTA publishes pass pid+2 before its successors may have read pass pid
+      // when two passes in a row run upward (a group ending on a UL substitution, then the next
+      // group's first elimination); it cannot publish pid+4 before they finished pid (pass pid+2
+      // or pid+3 runs downward and waits for them)
+      const int par = pid & 3;
+      double *slot = a.tot + ((size_t)par * nCTA) * NS * 2;
+      if (t == 0) {  // the CTA total: all warps composed in pass order
+        double T1[NS], T2[NS];
+#pragma unroll
+        for (int k = 0; k < NS; ++k) T1[k] = 0.0, T2[k] = 0.0;
+        for (int kk = 0; kk < kGW; ++kk) {
+          const int q = up ? kk : kGW - 1 - kk;
+#pragma unroll
+          for (int k = 0; k < NS; ++k) {
+            const double t1 = swt[(q * NS + k) * 2], t2 = swt[(q * NS + k) * 2 + 1];
+            T2[k] = fma(wm[q * 3 + 1], T1[k], fma(wm[q * 3 + 2], T2[k], t2));
+            T1[k] = fma(wm[q * 3], T1[k], t1);
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < NS; ++k) slot[(c * NS + k) * 2] = T1[k], slot[(c * NS + k) * 2 + 1] = T2[k];
+        st_release_u32(a.flag + c, pid);
+        if (tr) tr[1] = gtime();
+      }
+      // (4) look-back (warp 0): the totals of the W predecessors in pass direction
+      if (w == 0) {
+        const int W = a.lbW[dir * nCTA + c];
+        double e1[NS], e2[NS];
+#pragma unroll
+        for (int k = 0; k < NS; ++k) e1[k] = 0.0, e2[k] = 0.0;
+        for (int base = 0; base < W; base += 32) {
+          const int kq = base + lane + 1;  // predecessor distance
+          if (kq <= W) {
+            const int p = up ? c - kq : c + kq;
+            long long spins = 0;
+            // relaxed polls (an ld.acquire per poll would invalidate L1 every time), one acquire
+            // fence once the flag is seen; the totals are then read from L2
+            while (ld_relaxed_u32(a.flag + p) < pid) {
+              if (++spins > kSpinMax) {
+                a.err[0] = 1;  // the host reports the solve as failed
+                break;
+              }
+            }
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");
+            const double *P = a.lbP + (((size_t)dir * nCTA + c) * a.KW + (kq - 1)) * 3;
+#pragma unroll
+            for (int k = 0; k < NS; ++k) {
+              const double t1 = __ldcg(slot + (p * NS + k) * 2), t2 = __ldcg(slot + (p * NS + k) * 2 + 1);
+              e2[k] += fma(P[1], t1, P[2] * t2);
+              e1[k] += P[0] * t1;
+            }
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < NS; ++k)
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {  // fixed-order tree (deterministic)
+            e1[k] += __shfl_down_sync(kFull, e1[k], o);
+            e2[k] += __shfl_down_sync(kFull, e2[k], o);
+          }
+        if (lane == 0)
+#pragma unroll
+          for (int k = 0; k < NS; ++k) sE[k * 2] = e1[k], sE[k * 2 + 1] = e2[k];
+        if (tr && lane == 0) tr[2] = gtime();
+      }
+      __syncthreads();
+      if (tr && t == 0) tr[3] = gtime();
+      // (5) this thread's entering state: warp map of the preceding warps applied to the CTA
+      //     entering state, plus their fold, then the lane's exclusive prefix; rerun
+      double i1[NS], i2[NS];
+      {
+        // composite map of the preceding warps in pass order (constant, recomputed: ≤ 7 products)
+        double M11 = 1.0, M21 = 0.0, M22 = 1.0;
+#pragma unroll
+        for (int kk = 0; kk < kGW; ++kk) {
+          const int q = up ? kk : kGW - 1 - kk;
+          if (up ? q < w : q > w) {
+            M21 = fma(wm[q * 3 + 1], M11, wm[q * 3 + 2] * M21);
+            M11 *= wm[q * 3];
+            M22 *= wm[q * 3 + 2];
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < NS; ++k) {
+          const double E1 = sE[k * 2], E2 = sE[k * 2 + 1];
+          const double w1 = fma(M11, E1, f1[k]), w2 = fma(M21, E1, fma(M22, E2, f2[k]));
+          i2[k] = fma(g.X[dir][1], w1, fma(g.X[dir][2], w2, xs2[k]));
+          i1[k] = fma(g.X[dir][0], w1, xs1[k]);
+        }
+      }
+      run(i1, i2, true);
+      if (tr && t == 0) tr[4] = gtime();
+      };
+      const bool up = last ? ((a.steps - 1) & 1) != 0 : (m & 1) == 0;
+      using K0 = std::integral_constant<int, 0>;
+      using K1 = std::integral_constant<int, 1>;
+      using K2 = std::integral_constant<int, 2>;
+      if (m == 0) pass(std::true_type{}, K0{});
+      else if (last) {
+        if (up) pass(std::true_type{}, K2{});
+        else pass(std::false_type{}, K2{});
+      } else if (up) pass(std::true_type{}, K1{});
+      else pass(std::false_type{}, K1{});
+    }
+    // ---- epilogue of the group: F̂ (test hook / F̂_{k−1}) or D = F̂ − Ĝ, fp32 rows
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+      const int s = grp * NS + k;
+      if (s >= a.nsys) continue;
+      const int ln = a.ln0 + s;
+      float *dst;
+      const float *gh = nullptr;
+      if (a.Fout) dst = a.Fout + (size_t)s * a.row;
+      else if (ln == a.fk_ln) dst = a.Fk;
+      else dst = a.D + (size_t)ln * a.row, gh = a.Gh + (size_t)ln * a.row;
+#pragma unroll
+      for (int i = 0; i < PT; ++i) {
+        const int j = g.j0 + i;
+        if (j < a.M) dst[j] = gh ? (float)(x[k][i] - (double)gh[j]) : (float)x[k][i];
+      }
+    }
+    __syncthreads();  // sbc is rewritten by the next group
+  }
+}
+
+namespace {
+using GridKernel = void (*)(GridArgs);
+template <int NS>
+GridKernel grid_kernel(int PT) {
+  switch (PT) {
+    case 4: return k_fine_grid<4, NS>;
+    case 8: return k_fine_grid<8, NS>;
+    case 16: return k_fine_grid<16, NS>;
+    case 28: return k_fine_grid<28, NS>;
+  }
+  return nullptr;
+}
+constexpr int kPTs[] = {4, 8, 16, 28};
+constexpr int kNS = 2;
+}  // namespace
+
+size_t fine_grid_smem(int PT, int steps) {
+  return ((size_t)2 * kGT * PT + 2 * kGW * 3 + kGW * kNS * 2 + kNS * 2 + (size_t)kNS * steps) * sizeof(double);
+}
+
+// Points per thread and CTAs for M grid points on nsm SMs (one CTA per SM): the smallest PT with
+// ⌈M / (256·PT)⌉ ≤ nsm.  0 if none.
+int fine_grid_pt(int M, int nsm, int *nblocks) {
+  for (int PT : kPTs) {
+    const long long per = (long long)kGT * PT;
+    const long long nb = (M + per - 1) / per;
+    if (nb <= nsm) {
+      *nblocks = (int)nb;
+      return PT;
+    }
+  }
+  return 0;
+}
+int fine_grid_ns() { return kNS; }
+
+cudaError_t launch_fine_grid(const GridArgs &a, int PT, int nblocks, cudaStream_t s) {
+  GridKernel k = grid_kernel<kNS>(PT);
+  if (!k) return cudaErrorInvalidValue;
+  const size_t smem = fine_grid_smem(PT, a.steps);
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, occ = 0, nsm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kGT, smem);
+  if (e != cudaSuccess) return e;
+  if ((long long)occ * nsm < nblocks) return cudaErrorCooperativeLaunchTooLarge;
+  GridArgs arg = a;
+  void *params[] = {&arg};
+  return cudaLaunchCooperativeKernel((const void *)k, dim3(nblocks), dim3(kGT), params, smem, s);
+}
+
+}  // namespace pr

@@ -46,6 +46,30 @@ void pinn_tc_pack(const float *Wl, int W, int mode, uint16_t *out);
 int pinn_tc_points_per_cta(int W, int LH, int nfloats, int mode);  // 256 (ping-pong kernel) or 128
 cudaError_t launch_pinn_tc(int IN, int W, int act, int mode, const PinnArgs &a, const void *wh, dim3 grid,
                            cudaStream_t s);
+// K2R grid-resident fine sweep (fine_grid.cu): one system per GPU, NS systems at a time, state in
+// registers for all passes; θ = 1, one instance (B = 1).
+struct GridArgs {
+  int M, nsys, ln0, n_base, steps;  // systems = local slices ln0 … ln0 + nsys − 1 of instance 0
+  size_t row;                        // floats between slice rows (B·Mp)
+  double dT, dtau, c0, c1;           // c0 = dτr/2, c1 = dτσ²/2 (closed-form off-diagonals)
+  const double *ip, *iq;             // [M] 1/p_j (LU), 1/q_j (UL), natural layout
+  double bcoef, Lb, Kb, rb;          // boundary term dτ(a_M+b_M)·g(τ) of instance 0
+  int upper_bc;
+  const double *lbP;                 // [2][nCTA][KW][3] look-back weights (maps between predecessor and CTA)
+  const int *lbW;                    // [2][nCTA] look-back windows
+  int KW;
+  double *tot;                       // [4][nCTA][NS][2] published CTA totals per pass slot
+  unsigned *flag;                    // [nCTA] last pass published (zeroed before the launch)
+  int *err;                          // set when a look-back wait times out
+  const float *U, *Gh;               // [.][row] inputs U_n, Ĝ_n
+  float *D, *Fk, *Fout;              // outputs: D_n = F̂_n − Ĝ_n, F̂ of local slice fk_ln, or F̂ rows (test hook)
+  int fk_ln;
+  unsigned long long *trace;         // nullable: per (pass, CTA) %globaltimer stamps (PR_GRID_TRACE)
+};
+size_t fine_grid_smem(int PT, int steps);
+int fine_grid_pt(int M, int nsm, int *nblocks);  // points per thread for M points (0: too large)
+int fine_grid_ns();                               // systems per group
+cudaError_t launch_fine_grid(const GridArgs &a, int PT, int nblocks, cudaStream_t s);
 // Pipelined Parareal on one GPU (pipe.cu, NEXT-2): PINN chain (latency mode) and K1 fine solves
 // in one cooperative kernel, synchronised per slice.
 struct PipeArgs {

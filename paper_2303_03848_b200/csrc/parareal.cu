@@ -107,6 +107,12 @@ struct Scheme {
   double theta = 1.0;                               // θ-step (1: implicit Euler, 1/2: Crank–Nicolson)
   double *ecoef = nullptr;                          // device [nsets][3] explicit part (θ < 1)
   double *PL = nullptr, *tileL = nullptr;           // device K2 θ < 1 tile-edge correction tables
+  // K2R grid-resident solver (fine_grid.cu; θ = 1, one factor set, M > kResidentMaxM)
+  double *giq = nullptr;                            // device [M] 1/q_j (UL pivots)
+  double *lbP = nullptr;                            // device [2][nb][KW][3] look-back weights
+  int *lbW = nullptr;                               // device [2][nb] windows
+  int g_pt = 0, g_nb = 0, g_kw = 0;                 // points per thread, CTAs, table stride (0: no grid solver)
+  double g_c0 = 0, g_c1 = 0, g_bcoef = 0;         // closed-form coefficients; dτ(a_M+b_M) of instance 0
 };
 
 constexpr int kResidentMaxM = 2048;
@@ -167,6 +173,10 @@ struct pr_ctx {
   int64_t comm_timeout_ms = 600000;  // PR_OPT_COMM_TIMEOUT_MS (0: wait forever)
   int opt_wavefront = 0;             // PR_OPT_WAVEFRONT: 0 auto, 1 blocking chain, n ≥ 2 chunks
   int opt_spatial = 0;               // PR_OPT_SPATIAL_CHAIN: 0 auto, 1 off, 2 on
+  // K2R grid-resident fine solver: published totals, flags, timeout flag (mapped host memory)
+  double *g_tot = nullptr;
+  unsigned *g_flag = nullptr;
+  int *g_err_h = nullptr, *g_err_d = nullptr;
   // spatially sharded chain (NEXT-4): every slice's rows, this rank's j-range meaningful
   float *sp_U = nullptr, *sp_Gh = nullptr, *sp_D = nullptr, *sp_F = nullptr;
   double *sp_part = nullptr;
@@ -351,6 +361,93 @@ pr_status factorise_zz(pr_ctx *c, double dtau, std::vector<double> &zz) {
   return PR_OK;
 }
 
+// K2R tables (fine_grid.cu): the UL inverse pivots 1/q_j, and per CTA of the grid partition its
+// composite maps (↑↑ and ↓↓, from the same closed-form multipliers the kernel uses) and the
+// look-back weights P_k = M_{c∓1}·…·M_{c∓(k−1)} up to the window W where max|P| < 1e-24 (K2's
+// truncation).  ip: the LU inverse pivots of factorise (row 0 of [nsets][Mp]).
+pr_status grid_tables(pr_ctx *c, Scheme &sc, double dtau, const std::vector<double> &ip) {
+  int dev = 0, nsm = 0;
+  CU(cudaGetDevice(&dev));
+  CU(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  int nb = 0;
+  const int PT = pr::fine_grid_pt(c->M, nsm, &nb);
+  if (!PT) return PR_OK;  // too large for one pass over the GPU: K2 only
+  const int M = c->M;
+  const double sg = c->sets[0].first, rr = c->sets[0].second;
+  const double c0 = dtau * (0.5 * rr), c1 = dtau * (0.5 * sg * sg);
+  std::vector<double> iq(M), q(M), d(M), l(M), u(M);
+  for (int i = 0; i < M; ++i) {
+    const double J = i + 1, a = 0.5 * sg * sg * J * J, b = 0.5 * rr * J;
+    d[i] = 1.0 + dtau * (2.0 * a + rr);
+    l[i] = i > 0 ? -dtau * (a - b) : 0.0;
+    u[i] = i < M - 1 ? -dtau * (a + b) : 0.0;
+  }
+  q[M - 1] = d[M - 1];
+  for (int i = M - 2; i >= 0; --i) q[i] = d[i] - u[i] / q[i + 1] * l[i + 1];
+  for (int i = 0; i < M; ++i) {
+    if (!(q[i] > 0.0)) return fail(c, PR_ERR_NUMERICAL, fmt("non-positive UL pivot %g at j=%d", q[i], i + 1));
+    iq[i] = 1.0 / q[i];
+  }
+  // per-CTA maps in pass order (the kernel's multipliers: closed forms, identity padding)
+  const int per = 256 * PT;
+  std::vector<double> cm((size_t)2 * nb * 3);
+  for (int cb = 0; cb < nb; ++cb) {
+    for (int dir = 0; dir < 2; ++dir) {
+      double m11 = 1.0, m21 = 0.0, m22 = 1.0;
+      for (int k = 0; k < per; ++k) {
+        const int j = dir == 0 ? cb * per + k : cb * per + per - 1 - k;
+        double a11 = 0.0, a21 = 0.0, a22 = 0.0;
+        if (j < M) {
+          const double J = j + 1;
+          const double lj = (j >= 1) ? -J * std::fma(c1, J, -c0) : 0.0;
+          const double uj = (j < M - 1) ? -J * std::fma(c1, J, c0) : 0.0;
+          const double pj = ip[j], qj = iq[j];
+          if (dir == 0) a11 = -lj * qj, a21 = pj * a11, a22 = -lj * pj;   // ↑↑
+          else a11 = -uj * pj, a21 = qj * a11, a22 = -uj * qj;            // ↓↓
+        }
+        m21 = a21 * m11 + a22 * m21;
+        m11 *= a11;
+        m22 *= a22;
+      }
+      double *o = &cm[((size_t)dir * nb + cb) * 3];
+      o[0] = m11, o[1] = m21, o[2] = m22;
+    }
+  }
+  // look-back weights
+  std::vector<std::vector<double>> P((size_t)2 * nb);
+  std::vector<int> W((size_t)2 * nb, 0);
+  int KW = 1;
+  for (int dir = 0; dir < 2; ++dir)
+    for (int cb = 0; cb < nb; ++cb) {
+      std::vector<double> &pv = P[(size_t)dir * nb + cb];
+      double p11 = 1.0, p21 = 0.0, p22 = 1.0;
+      const int maxk = dir == 0 ? cb : nb - 1 - cb;
+      int k = 1;
+      for (; k <= maxk; ++k) {
+        if (std::max(std::fabs(p11), std::max(std::fabs(p21), std::fabs(p22))) < pr::kLookbackEps) break;
+        pv.push_back(p11), pv.push_back(p21), pv.push_back(p22);
+        const int pc = dir == 0 ? cb - k : cb + k;  // the k-th predecessor: its map joins the product
+        const double *mm = &cm[((size_t)dir * nb + pc) * 3];
+        p21 = p21 * mm[0] + p22 * mm[1];  // P ← P · M_pc
+        p11 *= mm[0];
+        p22 *= mm[2];
+      }
+      W[(size_t)dir * nb + cb] = k - 1;
+      KW = std::max(KW, k - 1);
+    }
+  std::vector<double> lb((size_t)2 * nb * KW * 3, 0.0);
+  for (int i = 0; i < 2 * nb; ++i)
+    for (size_t e = 0; e < P[i].size(); ++e) lb[(size_t)i * KW * 3 + e] = P[i][e];
+  CU(cudaMalloc(&sc.giq, (size_t)M * sizeof(double)));
+  CU(cudaMalloc(&sc.lbP, lb.size() * sizeof(double)));
+  CU(cudaMalloc(&sc.lbW, W.size() * sizeof(int)));
+  CU(cudaMemcpy(sc.giq, iq.data(), (size_t)M * sizeof(double), cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(sc.lbP, lb.data(), lb.size() * sizeof(double), cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(sc.lbW, W.data(), W.size() * sizeof(int), cudaMemcpyHostToDevice));
+  sc.g_pt = PT, sc.g_nb = nb, sc.g_kw = KW, sc.g_c0 = c0, sc.g_c1 = c1;
+  return PR_OK;
+}
+
 pr_status upload_scheme(pr_ctx *c, Scheme &sc, int steps, double theta) {
   sc.steps = steps;
   sc.dtau = c->dT / steps;
@@ -373,6 +470,8 @@ pr_status upload_scheme(pr_ctx *c, Scheme &sc, int steps, double theta) {
     CU(cudaMalloc(&sc.zz, zz.size() * sizeof(double)));
     CU(cudaMemcpy(sc.zz, zz.data(), zz.size() * sizeof(double), cudaMemcpyHostToDevice));
   }
+  if (theta == 1.0 && c->M > kResidentMaxM && c->nsets == 1 && c->B == 1 && (st = grid_tables(c, sc, dti, ip)))
+    return st;
   // K2: 1/p in the thread-interleaved layout (1 beyond M), the closed-form off-diagonal
   // coefficients, and the per-thread multipliers Π(−l_j/p_j) (dir 0) / Π(−u_j/p_j) (dir 1)
   const int Mt = pr::streamed_Mt(c->M);
@@ -483,6 +582,7 @@ pr_status upload_scheme(pr_ctx *c, Scheme &sc, int steps, double theta) {
   }
   CU(cudaMalloc(&sc.bcoef, c->B * sizeof(double)));
   CU(cudaMemcpy(sc.bcoef, bc.data(), c->B * sizeof(double), cudaMemcpyHostToDevice));
+  sc.g_bcoef = bc[0];
   if (theta != 1.0) {  // explicit part (1−θ)dτ·(σ²/2, r/2, r) per factor set
     std::vector<double> ec((size_t)c->nsets * 3);
     const double dte = (1.0 - theta) * sc.dtau;
@@ -508,6 +608,9 @@ void free_scheme(Scheme &s) {
   cudaFree(s.ip);
   cudaFree(s.cu);
   cudaFree(s.zz);
+  cudaFree(s.giq);
+  cudaFree(s.lbP);
+  cudaFree(s.lbW);
   cudaFree(s.bcoef);
   cudaFree(s.ecoef);
   cudaFree(s.PL);
@@ -750,12 +853,107 @@ pr_status launch_pinn(pr_ctx *c, const pr::PinnArgs &a0, int cta_lo = 0, int cta
   return PR_OK;
 }
 
+// ---------------------------------------------------------------- K2R grid-resident fine sweep
+// Used for θ = 1, one instance, M > kResidentMaxM when the partition fits the GPU, for sweeps of
+// at most kGridMaxSys systems (auto; measured at 2^20 points: 1.74× K2 for 1 system, 2.05× for 2,
+// 1.19× for 8, equal at 16, K2 ahead at 64 — the grid solver's pass is latency-bound and solves
+// 2 systems at a time, K2 streams all of them), or forced with PR_OPT_FINE_KERNEL = 3.
+constexpr int kGridMaxSys = 16;
+bool use_grid(const pr_ctx *c, int nsys) {
+  // (not with the in-process loopback transport: its ranks share one GPU, and the cooperative
+  // grid of one rank cannot be co-resident with another's)
+  if (!c->fine.g_pt || c->loop || c->opt_fine_kernel == 1 || c->opt_fine_kernel == 2) return false;
+  return c->opt_fine_kernel == 3 || (c->M > kResidentMaxM && nsys <= kGridMaxSys);
+}
+pr_status ensure_grid(pr_ctx *c) {
+  if (c->g_tot) return PR_OK;
+  const int nb = c->fine.g_nb;
+  CU(cudaMalloc(&c->g_tot, (size_t)4 * nb * pr::fine_grid_ns() * 2 * sizeof(double)));
+  CU(cudaMalloc(&c->g_flag, (size_t)nb * sizeof(unsigned)));
+  CU(cudaHostAlloc((void **)&c->g_err_h, sizeof(int), cudaHostAllocMapped));
+  *c->g_err_h = 0;
+  CU(cudaHostGetDevicePointer((void **)&c->g_err_d, c->g_err_h, 0));
+  return PR_OK;
+}
+// One grid sweep over the local slices [ln0, ln0+nsl): D (or F̂ into Fk / Fout)
+pr_status grid_sweep(pr_ctx *c, int ln0, int nsl, int n_base, const float *U, float *Fout, int fk_ln) {
+  pr_status st = ensure_grid(c);
+  if (st) return st;
+  const Scheme &sc = c->fine;
+  pr::GridArgs g;
+  std::memset(&g, 0, sizeof g);
+  g.M = c->M;
+  g.nsys = nsl;
+  g.ln0 = ln0;
+  g.n_base = n_base;
+  g.steps = sc.steps;
+  g.row = (size_t)c->B * c->Mp;
+  g.dT = c->dT;
+  g.dtau = sc.dtau;
+  g.c0 = sc.g_c0;
+  g.c1 = sc.g_c1;
+  g.ip = sc.ip;
+  g.iq = sc.giq;
+  g.bcoef = sc.g_bcoef;
+  g.Lb = c->L[0];
+  g.Kb = c->K[0];
+  g.rb = c->r[0];
+  g.upper_bc = c->upper_bc;
+  g.lbP = sc.lbP;
+  g.lbW = sc.lbW;
+  g.KW = sc.g_kw;
+  g.tot = c->g_tot;
+  g.flag = c->g_flag;
+  g.err = c->g_err_d;
+  g.U = U;
+  g.Gh = c->Gh;
+  g.D = c->D;
+  g.Fk = c->Fk;
+  g.Fout = Fout;
+  g.fk_ln = fk_ln;
+  CU(cudaMemsetAsync(c->g_flag, 0, (size_t)sc.g_nb * sizeof(unsigned), c->stream));
+  // PR_GRID_TRACE=file (tuning): %globaltimer stamps per pass and CTA, written after the launch
+  static const char *trace_path = getenv("PR_GRID_TRACE");
+  const size_t npass = (size_t)((nsl + pr::fine_grid_ns() - 1) / pr::fine_grid_ns()) * (sc.steps + 1);
+  unsigned long long *trace = nullptr;
+  if (trace_path && !c->capturing) {
+    CU(cudaMalloc(&trace, npass * sc.g_nb * 5 * sizeof(unsigned long long)));
+    CU(cudaMemsetAsync(trace, 0, npass * sc.g_nb * 5 * sizeof(unsigned long long), c->stream));
+    g.trace = trace;
+  }
+  LAUNCH(pr::launch_fine_grid(g, sc.g_pt, sc.g_nb, c->stream));
+  if (trace) {
+    std::vector<unsigned long long> h(npass * sc.g_nb * 5);
+    CU(cudaMemcpyAsync(h.data(), trace, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
+    SYNC();
+    cudaFree(trace);
+    if (FILE *f = fopen(trace_path, "w")) {
+      for (size_t ps = 0; ps < npass; ++ps)
+        for (int cb = 0; cb < sc.g_nb; ++cb) {
+          const unsigned long long *r = &h[(ps * sc.g_nb + cb) * 5];
+          fprintf(f, "%zu %d %llu %llu %llu %llu %llu\n", ps, cb, r[0], r[1], r[2], r[3], r[4]);
+        }
+      fclose(f);
+    }
+  }
+  return PR_OK;
+}
+// after a sync: a look-back wait that timed out (a failed launch or a lost CTA) fails the solve
+pr_status grid_check(pr_ctx *c) {
+  if (c->g_err_h && *c->g_err_h) {
+    *c->g_err_h = 0;
+    return fail(c, PR_ERR_CUDA, "grid-resident fine sweep: look-back wait timed out");
+  }
+  return PR_OK;
+}
+
 // ---------------------------------------------------------------- phases of one iteration
 // Fine sweep over local slices [ln_lo, Nloc) reading U^{k−1}: D_n = F̂_n − Ĝ_n, and
 // F̂ of local slice fk_ln (= k−1 when owned here) into Fk.
 pr_status fine_sweep(pr_ctx *c, int ln_lo, int fk_ln) {
   const int nsl = c->Nloc - ln_lo;
   if (nsl <= 0) return PR_OK;
+  if (use_grid(c, nsl)) return grid_sweep(c, ln_lo, nsl, c->n0, c->U, nullptr, fk_ln);
   if (use_resident(c)) {
     pr::ResidentArgs a = base_args(c, c->fine);
     a.ln0 = ln_lo;
@@ -1550,6 +1748,7 @@ pr_status solve_impl_(pr_ctx *c, const float *V_T, float *V_0, bool device_ptr, 
     return solve_report(c, c->g_K, 0, c->g_e0, c->g_e1, c->g_spans, c->g_launches, rep, c->opt_graphs == 2);
   }
   if (pipe_eligible(c) && (st = ensure_pipe(c))) return st;  // (allocation cannot be captured)
+  if (c->fine.g_pt && (st = ensure_grid(c))) return st;
   if (use_graph) {
     drop_graph(c);
     CU(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
@@ -1665,6 +1864,7 @@ pr_status solve_impl_(pr_ctx *c, const float *V_T, float *V_0, bool device_ptr, 
     return st;
   }
   SYNC();
+  if ((st = grid_check(c))) return st;
   return solve_report(c, K, conv, e0, e1, pt.spans, c->launches - launches0, rep, use_graph && c->opt_graphs == 2);
 }
 
@@ -1689,6 +1889,9 @@ pr_status serial_fine_impl(pr_ctx *c, const float *V_T, float *V_0, bool device_
     a.c_ln0 = 0;
     a.c_ln1 = c->N;
     LAUNCH(dispatch_res(true, c->M, a, c->B, c->stream));
+  } else if (use_grid(c, 1)) {  // one grid-resident slice solve per slice, in place (each CTA owns its points)
+    for (int n = 0; n < c->N; ++n)
+      if ((st = grid_sweep(c, 0, 1, n, c->tmp, c->tmp, -1))) return st;
   } else {
     pr::StreamedChainJob j;
     j.U = c->tmp; j.Gh = nullptr; j.D = nullptr; j.Fcopy = nullptr; j.partials = nullptr; j.nch = 1;
@@ -1701,6 +1904,7 @@ pr_status serial_fine_impl(pr_ctx *c, const float *V_T, float *V_0, bool device_
   cudaEventRecord(e1, c->stream);
   if (V_0 && (st = store_rows(c, V_0, c->tmp, device_ptr))) return st;
   SYNC();
+  if ((st = grid_check(c))) return st;
   if (ms) {
     float m = 0;
     cudaEventElapsedTime(&m, e0, e1);
@@ -2076,7 +2280,9 @@ pr_status parareal_apply_fine(pr_ctx *c, int32_t n, const float *U_in, float *U_
   c->U = save;
   if (st) return st;
   const size_t row = (size_t)c->B * c->Mp;
-  if (use_resident(c)) {
+  if (use_grid(c, 1)) {
+    if ((st = grid_sweep(c, 0, 1, n, c->tmp, c->tmp + row, -1))) return st;
+  } else if (use_resident(c)) {
     pr::ResidentArgs a = base_args(c, c->fine);
     a.n_base = n;
     a.ln0 = 0;
@@ -2095,7 +2301,7 @@ pr_status parareal_apply_fine(pr_ctx *c, int32_t n, const float *U_in, float *U_
   }
   if ((st = store_rows(c, U_out, c->tmp + row, false))) return st;
   SYNC();
-  return PR_OK;
+  return grid_check(c);
 }
 
 pr_status parareal_apply_coarse(pr_ctx *c, int32_t n, const float *U_in, float *U_out) {
@@ -2174,7 +2380,9 @@ pr_status parareal_set_option(pr_ctx *c, int32_t key, int64_t value) {
   drop_graph(c);  // a captured solve bakes in kernel choices
   switch (key) {
     case PR_OPT_FINE_KERNEL:
-      if (value < 0 || value > 2) return fail(c, PR_ERR_INVALID_ARGUMENT, "PR_OPT_FINE_KERNEL must be 0, 1 or 2");
+      if (value < 0 || value > 3) return fail(c, PR_ERR_INVALID_ARGUMENT, "PR_OPT_FINE_KERNEL must be 0, 1, 2 or 3");
+      if (value == 3 && !c->fine.g_pt)
+        return fail(c, PR_ERR_UNSUPPORTED, "grid-resident fine kernel needs theta = 1, B = 1, M > 2048 and a grid that fits the GPU");
       if (value == 1 && c->M > kResidentMaxM)
         return fail(c, PR_ERR_UNSUPPORTED, fmt("resident fine kernel needs M <= %d", kResidentMaxM));
       c->opt_fine_kernel = (int)value;
@@ -2233,6 +2441,9 @@ void parareal_free(pr_ctx *c) {
   if (c->own_ws) cudaFree(c->ws);
   if (c->h_delta) cudaFreeHost(c->h_delta);
   cudaFree(c->pipe_partials);
+  cudaFree(c->g_tot);
+  cudaFree(c->g_flag);
+  if (c->g_err_h) cudaFreeHost(c->g_err_h);
   cudaFree(c->sp_U);
   cudaFree(c->sp_Gh);
   cudaFree(c->sp_D);

@@ -10,6 +10,8 @@ flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 with parareal.Context(p, stream=s.cuda_stream) as c:
     c.load_weights(synth.kaiming_net(synth.PINN_3x20, seed=0))
     c.set_option(parareal.OPT_USE_GRAPHS, 1)
+    if os.environ.get("FINE_KERNEL"):
+        c.set_option(parareal.OPT_FINE_KERNEL, int(os.environ["FINE_KERNEL"]))
     out = torch.empty((1, p.M), dtype=torch.float32, device="cuda")
     c.solve_device(out)
     ms = []

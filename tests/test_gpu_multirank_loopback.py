@@ -50,7 +50,9 @@ def solve_ranks(p, net, world, key, opts=None, precision=parareal.PREC_FP32):
 @pytest.mark.parametrize("name,world", [("pinn", 2), ("pinn", 4), ("ie", 2), ("ie_tol", 2), ("ie_tol", 4),
                                         ("streamed", 2), ("portfolio", 2)])
 def test_multirank_matches_one_rank(name, world):
-    net = None
+    # (the loopback ranks share one GPU and never run the cooperative grid-resident fine kernel:
+    # problems that would use it pin K2 on every side)
+    net, opts = None, {}
     if name == "pinn":
         p = synth.single(1024, 32, coarse=synth.COARSE_PINN, max_iter=3, tol=0.0)
         net = synth.kaiming_net(synth.PINN_3x20, seed=1)
@@ -60,6 +62,7 @@ def test_multirank_matches_one_rank(name, world):
         p = synth.config("C1", coarse=synth.COARSE_IMPLICIT_EULER, max_iter=4, tol=3e-5)
     elif name == "streamed":  # K2 fine sweeps and the streamed numerical chain
         p = synth.single(5000, 4, coarse=synth.COARSE_IMPLICIT_EULER, max_iter=2, tol=0.0, fine_steps=20)
+        opts = {parareal.OPT_FINE_KERNEL: 2}
     else:
         p = synth.portfolio(n_k=2, n_s=2, M=256, N=8, coarse=synth.COARSE_PINN, max_iter=3, tol=0.0)
         net = synth.kaiming_net(synth.PINN_3x20, seed=2)
@@ -67,9 +70,11 @@ def test_multirank_matches_one_rank(name, world):
         if net is not None:
             c.load_weights(net)
         c.set_option(parareal.OPT_PIPELINE, 1)  # the blocking schedule (multi-rank runs blocking)
+        for k, v in opts.items():
+            c.set_option(k, v)
         ref, rref = c.solve()
         it_ref = c.copy_iterates(0, p.N + 1)
-    out, reps, its = solve_ranks(p, net, world, ("%s-%d" % (name, world)).encode())
+    out, reps, its = solve_ranks(p, net, world, ("%s-%d" % (name, world)).encode(), opts)
     assert all(r["iterations"] == rref["iterations"] for r in reps)
     assert np.array_equal(reps[0]["delta"], rref["delta"])
     assert np.array_equal(out, ref)
@@ -94,13 +99,16 @@ def test_chain_wavefront_matches_one_rank(case, world, chunks):
     else:  # tensor-core chain (K4, split fp16)
         p = synth.single(3000, 8, coarse=synth.COARSE_PINN, max_iter=2, tol=0.0, fine_steps=10)
         net, prec = synth.kaiming_net([4, 64, 64, 64, 1], seed=4), parareal.PREC_FP16_TC
+    fk = {parareal.OPT_FINE_KERNEL: 2} if p.M > 2048 else {}  # (no grid-resident kernel in loopback)
     with parareal.Context(p) as c:
         c.load_weights(net, precision=prec)
         c.set_option(parareal.OPT_PIPELINE, 1)
+        for k, v in fk.items():
+            c.set_option(k, v)
         ref, rref = c.solve()
         it_ref = c.copy_iterates(0, p.N + 1)
     key = ("wave-%s-%d-%d" % (case, world, chunks)).encode()
-    off = {parareal.OPT_SPATIAL_CHAIN: 1}  # (auto would shard the TC chain spatially instead)
+    off = {parareal.OPT_SPATIAL_CHAIN: 1, **fk}  # (auto would shard the TC chain spatially instead)
     out, reps, its = solve_ranks(p, net, world, key, {**off, parareal.OPT_WAVEFRONT: chunks}, prec)
     _, breps, _ = solve_ranks(p, net, world, key + b"b", {**off, parareal.OPT_WAVEFRONT: 1}, prec)
     assert np.array_equal(out, ref)
@@ -131,9 +139,14 @@ def test_spatial_chain_matches_one_rank(case, world):
     else:  # K = N: the last iteration's chain is the copy step alone (finite termination)
         p = synth.single(200, 4, coarse=synth.COARSE_PINN, max_iter=4, tol=0.0, fine_steps=7)
         net = synth.kaiming_net([4, 8, 8, 1], seed=8)
+    if p.M > 2048:
+        opts = {**opts, parareal.OPT_FINE_KERNEL: 2}  # (no grid-resident kernel in loopback)
     with parareal.Context(p) as c:
         c.load_weights(net, precision=prec)
         c.set_option(parareal.OPT_PIPELINE, 1)
+        for k, v in opts.items():
+            if k == parareal.OPT_FINE_KERNEL:
+                c.set_option(k, v)
         ref, rref = c.solve()
         it_ref = c.copy_iterates(0, p.N + 1)
     out, reps, its = solve_ranks(p, net, world, ("spatial-%s-%d" % (case, world)).encode(), opts, prec)

@@ -10,7 +10,7 @@ from paper_2303_03848_b200 import parareal, synth
 
 pytestmark = pytest.mark.gpu
 
-FINE_KERNELS = [1, 2]   # resident, streamed (PR_OPT_FINE_KERNEL)
+FINE_KERNELS = [1, 2]   # resident, streamed (PR_OPT_FINE_KERNEL); the grid-resident kernel (3) has its own tests
 
 
 def ctx_for(p, net=None, fine_kernel=0):
@@ -680,17 +680,60 @@ def test_k2_persistent_pass_long_lookback():
     assert_delta(rep["delta"], ref_d)
 
 
-def test_c3_grid_fine_sweep_persistent():
-    """The C3 grid (2^20 points, the C3 step dτ = 1/6400) on the persistent K2 kernel: 16 slices of
-    2 steps, one Parareal iteration with numerical G -- all 17 boundary states (about 17 M values)
-    against the oracle."""
+@pytest.mark.parametrize("kernel", [2, 3])
+def test_c3_grid_fine_sweep_persistent(kernel):
+    """The C3 grid (2^20 points, the C3 step dτ = 1/6400) on the persistent K2 kernel (2) and on
+    the grid-resident kernel (3): 16 slices of 2 steps, one Parareal iteration with numerical G --
+    all 17 boundary states (about 17 M values) against the oracle."""
     M, N, nf = 1 << 20, 16, 2
     p = synth.single(M, N, fine_steps=nf, coarse=synth.COARSE_IMPLICIT_EULER, coarse_steps=1, max_iter=1, tol=0.0,
                      T=N * nf / 6400.0)
-    with ctx_for(p) as c:
+    with ctx_for(p, fine_kernel=kernel) as c:
         _, rep = c.solve()
         it = c.copy_iterates(0, p.N + 1)
     ref_U, ref_d, K, _ = oracle.parareal(p)
     assert rep["iterations"] == K == 1
     assert_close(it, ref_U, what="C3-grid Parareal iterate")
     assert_delta(rep["delta"], ref_d)
+
+
+
+# ------------------------------------------------------------------ K2R grid-resident fine solver
+# (fine_grid.cu: one system spans the GPU, state in registers for all passes, LU/UL zig-zag)
+
+@pytest.mark.parametrize("M,N,n,nf", [(2049, 4, 0, 3), (3000, 4, 1, 10), (5000, 8, 3, 7), (70000, 4, 2, 5),
+                                      (1 << 18, 4, 1, 6)])
+def test_grid_fine_single_slice(M, N, n, nf):
+    """One F application (n_f IE steps) on the grid-resident kernel against the oracle: ragged last
+    CTA (2049, 3000, 70000), several CTAs and look-back windows, the 2^18 C5 grid."""
+    p = synth.single(M, N, fine_steps=nf)
+    U = synth.random_state(1, M, seed=M + n)
+    with ctx_for(p, fine_kernel=3) as c:
+        got = c.apply_fine(n, U)
+    assert_close(got, oracle.fine(p, n, U.astype(np.float64)), what="grid F M=%d" % M)
+
+
+@pytest.mark.parametrize("M,N,K", [(3000, 6, 3), (5000, 9, 2), (40000, 4, 4)])
+def test_grid_parareal_iterates(M, N, K):
+    """Parareal with numerical G on the grid-resident fine kernel: every iterate against the
+    oracle; odd slice counts leave a group with one live system; K = N (finite termination)."""
+    p = synth.single(M, N, fine_steps=8, coarse=synth.COARSE_IMPLICIT_EULER, max_iter=K, tol=0.0)
+    with ctx_for(p, fine_kernel=3) as c:
+        _, rep = c.solve()
+        it = c.copy_iterates(0, p.N + 1)
+        again, _ = c.solve()
+        it2 = c.copy_iterates(0, p.N + 1)
+    ref_U, ref_d, Kr, _ = oracle.parareal(p)
+    assert rep["iterations"] == Kr == K
+    assert_close(it, ref_U, what="grid Parareal M=%d" % M)
+    assert_delta(rep["delta"], ref_d)
+    assert np.array_equal(it, it2)  # run-to-run bitwise (fixed composition orders)
+
+
+def test_grid_serial_fine_matches_oracle():
+    """The serial fine solve (the speedup baseline) runs one grid-resident solve per slice for
+    M > 2048: against the oracle's serial fine solution."""
+    p = synth.single(6000, 8, fine_steps=12)
+    with ctx_for(p) as c:
+        got, _ = c.serial_fine()
+    assert_close(got, oracle.serial_fine(p)[-1], what="grid serial fine")
