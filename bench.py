@@ -265,14 +265,15 @@ def roofline(p, ph, K, world, rank, pk, pk_src, clk_mhz, n_sm, synth, dims=None,
                     "work_per_unit": "9 fp64 flop per point-step", "launch_unit": "one sweep"}
             tr = ncu_traffic("k_parareal_pipe" if piped else "k_fine_sweep")
         else:
-            kname = ("k_pass_res2 (K2, persistent paired streamed pass)" if p.fine_theta == 1.0
-                     else "k_streamed_pass (K2, Crank-Nicolson tile pass)")
+            grid = p.fine_theta == 1.0 and p.B == 1
+            kname = ("k_fine_grid / k_pass_res2 (K2R grid-resident solver where its cost model wins, else K2)"
+                     if grid else "k_streamed_pass (K2, Crank-Nicolson tile pass)")
             roof = {"kernel": kname, "bound": "hbm",
                     "achieved": 8.0 * pt_steps / sweep_s / 1e9,
                     "peak": float(pk["hbm_gbs"]), "unit": "GB/s", "peak_source": pk_src,
                     "work_per_unit": "8 B per point-step (SURVEY 8(d) algorithmic: one fp32 read + write; "
                                      "the two-pass kernel moves 16)", "launch_unit": "one sweep"}
-            tr = ncu_traffic("k_pass_res2" if p.fine_theta == 1.0 else "k_streamed_pass")
+            tr = ncu_traffic("k_fine_grid" if grid else "k_streamed_pass")
     else:
         evals = float(p.B) * p.M * nloc
         chain_s = ph["ms_coarse"] / (K + 1) / 1e3
@@ -310,35 +311,55 @@ def roofline(p, ph, K, world, rank, pk, pk_src, clk_mhz, n_sm, synth, dims=None,
 
 
 def c3_fine_sweep_roofline(parareal, synth, torch, stream, pk, pk_src, flush):
-    """One Parareal iteration at C3 (2^20 points x 64 slices): its fine sweep runs the streamed
-    kernel over all 64 slices x 100 steps; HBM roofline from the CUDA-event phase time."""
+    """One Parareal iteration at C3 (2^20 points x 64 slices): its fine sweep (all 64 slices x 100
+    steps) through the kernel the library picks (K2R, the grid-resident solver) and,
+    beside it, forced through K2 (the HBM-streamed pass).  Roofline on SURVEY 8(d)'s algorithmic
+    8 B per point-step from the CUDA-event phase time (median of 3, L2 flushed before each)."""
     p = synth.config("C3", coarse=synth.COARSE_PINN, max_iter=1, tol=0.0)
-    ctx = parareal.Context(p, stream=stream.cuda_stream)
-    try:
-        ctx.load_weights(synth.kaiming_net(synth.PINN_3x20, seed=0))
-        ctx.set_option(parareal.OPT_USE_GRAPHS, 1)  # the sweep's ~200 pass launches replay as one graph
-        out = torch.empty((p.B, p.M), dtype=torch.float32, device="cuda")
-        ctx.solve_device(out)
-        ms = []
-        for _ in range(3):
-            flush.zero_()
-            torch.cuda.synchronize()
-            ms.append(ctx.solve_device(out)["ms_fine"])
-        t = statistics.median(ms) / 1e3
-        pt_steps = float(p.M) * p.N * p.fine_steps
-        ach = 8.0 * pt_steps / t / 1e9
-        tr = ncu_traffic("k_pass_res2")
-        return {"kernel": "k_pass_res2 (K2, persistent paired streamed pass)", "workload": "C3 fine sweep: 64 slices x 2^20 points x 100 IE steps",
-                "bound": "hbm", "achieved": ach, "peak": float(pk["hbm_gbs"]), "unit": "GB/s",
-                "frac": ach / float(pk["hbm_gbs"]), "peak_source": pk_src, "ms_per_sweep": t * 1e3,
-                "point_steps_per_s": pt_steps / t,
-                "work_per_unit": "8 B per point-step (SURVEY 8(d) algorithmic, single-pass design)",
-                "moved_bytes_frac": 2.0 * ach / float(pk["hbm_gbs"]),
-                "moved_bytes_basis": "16 B per point-step: the two-pass kernel reads and writes fp32 state in both passes",
-                "traffic": tr["dram_bytes_per_launch"] if tr else None,
-                "traffic_unit": "bytes per pass launch (ncu dram read+write; one pass = 8 B per point)"}
-    finally:
-        ctx.close()
+
+    def sweep_ms(fine_kernel):
+        ctx = parareal.Context(p, stream=stream.cuda_stream)
+        try:
+            ctx.load_weights(synth.kaiming_net(synth.PINN_3x20, seed=0))
+            ctx.set_option(parareal.OPT_USE_GRAPHS, 1)  # K2's ~200 pass launches replay as one graph
+            ctx.set_option(parareal.OPT_FINE_KERNEL, fine_kernel)
+            out = torch.empty((p.B, p.M), dtype=torch.float32, device="cuda")
+            ctx.solve_device(out)
+            ms = []
+            for _ in range(3):
+                flush.zero_()
+                torch.cuda.synchronize()
+                ms.append(ctx.solve_device(out)["ms_fine"])
+            return statistics.median(ms)
+        finally:
+            ctx.close()
+
+    t = sweep_ms(0) / 1e3          # auto: the grid-resident K2R at this size
+    t_k2 = sweep_ms(2) / 1e3       # K2 forced
+    pt_steps = float(p.M) * p.N * p.fine_steps
+    ach = 8.0 * pt_steps / t / 1e9
+    tr = ncu_traffic("k_fine_grid")
+    tr2 = ncu_traffic("k_pass_res2")
+    out = {"kernel": "k_fine_grid (K2R, grid-resident fine solver; state in registers, HBM once per slice)",
+           "workload": "C3 fine sweep: 64 slices x 2^20 points x 100 IE steps",
+           "bound": "hbm", "achieved": ach, "peak": float(pk["hbm_gbs"]), "unit": "GB/s",
+           "frac": ach / float(pk["hbm_gbs"]), "peak_source": pk_src, "ms_per_sweep": t * 1e3,
+           "point_steps_per_s": pt_steps / t,
+           "work_per_unit": "8 B per point-step (SURVEY 8(d) algorithmic, single-pass design); K2R keeps the "
+                            "state on chip, so this is the HBM-equivalent rate",
+           "traffic": tr["dram_bytes_per_launch"] if tr else None,
+           "traffic_unit": "bytes per sweep launch (ncu dram read+write; the whole sweep is one launch)",
+           "k2": {"kernel": "k_pass_res2 (K2, persistent paired streamed pass)", "ms_per_sweep": t_k2 * 1e3,
+                  "frac": 8.0 * pt_steps / t_k2 / 1e9 / float(pk["hbm_gbs"]),
+                  "moved_bytes_frac": 16.0 * pt_steps / t_k2 / 1e9 / float(pk["hbm_gbs"]),
+                  "moved_bytes_basis": "16 B per point-step: the two-pass kernel reads and writes fp32 state in both passes",
+                  "traffic": tr2["dram_bytes_per_launch"] if tr2 else None,
+                  "traffic_unit": "bytes per pass launch (one pass = 8 B per point)"}}
+    if ALU:
+        out["alu"] = {"achieved": 9.0 * pt_steps / t / 1e12, "peak": ALU["fp64"], "unit": "TFLOP/s",
+                      "frac": 9.0 * pt_steps / t / 1e12 / ALU["fp64"],
+                      "work_per_unit": "9 fp64 flop per point-step (the kernel issues ~2x: local run + rerun)"}
+    return out
 
 
 def training_run(synth):

@@ -15,9 +15,9 @@
 // One pass: each thread runs its points from a zero entering state (chunk totals), a warp scan
 // of the 2-vector affine parts with per-lane level coefficients precomputed at kernel start, a
 // fold over the warps (constant warp maps in shared memory), the CTA total is published
-// (per-pass slot + release flag) and the entering state of the CTA is composed from the totals of
+// (per-pass slot, tagged words) and the entering state of the CTA is composed from the totals of
 // its W predecessors in pass direction (decoupled look-back: every CTA publishes before it waits,
-// so the wait is one flag propagation; W from the host, where the product of the predecessors'
+// so the wait is one store-to-load propagation; W from the host, where the product of the predecessors'
 // maps falls below 1e-24 — the same truncation as K2; the weights Π of the CTA maps in between
 // are host tables), then each thread reruns its points from its exact entering state.
 #include "launch.h"
@@ -35,34 +35,37 @@ constexpr int kGT = 256;        // threads per CTA
 constexpr int kGW = kGT / 32;   // warps per CTA
 constexpr long long kSpinMax = 1ll << 28;  // look-back wait bound (then the solve fails, no hang)
 
-__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned *p) {
-  unsigned v;
-  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long *p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
+}
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long *p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 __device__ __forceinline__ unsigned long long gtime() {
   unsigned long long v;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
   return v;
 }
-__device__ __forceinline__ void st_release_u32(unsigned *p, unsigned v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
 
 template <int PT, int NS>
 struct GridSolver {
   // per-lane level coefficients (the lane's composite map at each level, 0 without predecessor)
-  // and exclusive maps, for ↑↑ (index 0) and ↓↓ (index 1)
-  double C[2][5][3], X[2][3];
+  // and exclusive maps, for ↑↑ (index 0) and ↓↓ (index 1), in shared memory [..][kGT] (the
+  // registers hold the NS systems' state)
+  double *sC, *sX;
   int t, lane, w, c, j0;
+  __device__ __forceinline__ double &C(int dir, int l, int e) const { return sC[((dir * 5 + l) * 3 + e) * kGT + t]; }
+  __device__ __forceinline__ double &X(int dir, int e) const { return sX[(dir * 3 + e) * kGT + t]; }
 
   // closed-form off-diagonals and factors of point j (padding beyond M: identity, no coupling)
   __device__ __forceinline__ void mults(const GridArgs &a, const double *sip, const double *siq, int i, double &ip,
                                         double &iq, double &l, double &u) const {
     const int j = j0 + i;
     const double J = (double)(j + 1);
-    ip = sip[t * PT + i];
-    iq = siq[t * PT + i];
+    ip = sip[i * kGT + t];
+    iq = siq[i * kGT + t];
     l = (j >= 1 && j < a.M) ? -J * fma(a.c1, J, -a.c0) : 0.0;
     u = (j < a.M - 1) ? -J * fma(a.c1, J, a.c0) : 0.0;
   }
@@ -70,15 +73,23 @@ struct GridSolver {
 
 }  // namespace
 
-template <int PT, int NS>
+// St: the storage type of the state between passes — fp64 where NS·PT values fit the registers,
+// else fp32 (the precision K2 stores between its passes in HBM; the arithmetic stays fp64)
+template <int PT, int NS, typename St>
 __global__ void __launch_bounds__(kGT, 1) k_fine_grid(GridArgs a) {
   extern __shared__ __align__(16) double gsm[];
-  double *sip = gsm, *siq = gsm + kGT * PT;          // this CTA's 1/p, 1/q
+  double *sip = gsm, *siq = gsm + kGT * PT;          // this CTA's 1/p, 1/q, [PT][kGT]
   double *swm = siq + kGT * PT;                        // [2][kGW][3] constant warp maps
   double *swt = swm + 2 * kGW * 3;                     // [kGW][NS][2] warp totals of the pass
   double *sE = swt + kGW * NS * 2;                     // [NS][2] CTA entering state
-  double *sbc = sE + NS * 2;                           // [NS][steps] boundary terms
+  double *sT = sE + NS * 2;                            // [NS][2] CTA total of the pass
+  double *sred = sT + NS * 2;                          // [32][2] look-back partial sums (warp 0)
+  double *sC = sred + 64;                              // [2][5][3][kGT] level coefficients
+  double *sX = sC + 2 * 5 * 3 * kGT;                   // [2][3][kGT] exclusive maps
+  double *sbc = sX + 2 * 3 * kGT;                      // [NS][steps] boundary terms
   GridSolver<PT, NS> g;
+  g.sC = sC;
+  g.sX = sX;
   g.t = threadIdx.x;
   g.lane = g.t & 31;
   g.w = g.t >> 5;
@@ -88,8 +99,9 @@ __global__ void __launch_bounds__(kGT, 1) k_fine_grid(GridArgs a) {
   const int t = g.t, lane = g.lane, w = g.w, c = g.c;
   for (int i = t; i < kGT * PT; i += kGT) {
     const int j = c * kGT * PT + i;
-    sip[i] = j < a.M ? a.ip[j] : 1.0;
-    siq[i] = j < a.M ? a.iq[j] : 1.0;
+    const int o = (i % PT) * kGT + i / PT;  // point-major: thread t's point i at [i][t] (no bank conflicts)
+    sip[o] = j < a.M ? a.ip[j] : 1.0;
+    siq[o] = j < a.M ? a.iq[j] : 1.0;
   }
   __syncthreads();
   // thread chunk maps in pass order: ↑↑ A = [[ncl, 0], [ip·ncl, nml]], ↓↓ A = [[ncu, 0], [iq·ncu, nmu]]
@@ -125,19 +137,20 @@ __global__ void __launch_bounds__(kGT, 1) k_fine_grid(GridArgs a) {
         const double p21 = up ? __shfl_up_sync(kFull, m21, d) : __shfl_down_sync(kFull, m21, d);
         const double p22 = up ? __shfl_up_sync(kFull, m22, d) : __shfl_down_sync(kFull, m22, d);
         const bool has = up ? lane >= d : lane + d <= 31;
-        g.C[dir][l][0] = has ? m11 : 0.0;
-        g.C[dir][l][1] = has ? m21 : 0.0;
-        g.C[dir][l][2] = has ? m22 : 0.0;
+        g.C(dir, l, 0) = has ? m11 : 0.0;
+        g.C(dir, l, 1) = has ? m21 : 0.0;
+        g.C(dir, l, 2) = has ? m22 : 0.0;
         if (has) {
           m21 = fma(m21, p11, m22 * p21);
           m11 *= p11;
           m22 *= p22;
         }
       }
-      g.X[dir][0] = up ? __shfl_up_sync(kFull, m11, 1) : __shfl_down_sync(kFull, m11, 1);
-      g.X[dir][1] = up ? __shfl_up_sync(kFull, m21, 1) : __shfl_down_sync(kFull, m21, 1);
-      g.X[dir][2] = up ? __shfl_up_sync(kFull, m22, 1) : __shfl_down_sync(kFull, m22, 1);
-      if (lane == (up ? 0 : 31)) g.X[dir][0] = 1.0, g.X[dir][1] = 0.0, g.X[dir][2] = 1.0;
+      double x0 = up ? __shfl_up_sync(kFull, m11, 1) : __shfl_down_sync(kFull, m11, 1);
+      double x1 = up ? __shfl_up_sync(kFull, m21, 1) : __shfl_down_sync(kFull, m21, 1);
+      double x2 = up ? __shfl_up_sync(kFull, m22, 1) : __shfl_down_sync(kFull, m22, 1);
+      if (lane == (up ? 0 : 31)) x0 = 1.0, x1 = 0.0, x2 = 1.0;
+      g.X(dir, 0) = x0, g.X(dir, 1) = x1, g.X(dir, 2) = x2;
       if (lane == (up ? 31 : 0)) {
         double *o = swm + (dir * kGW + w) * 3;
         o[0] = m11, o[1] = m21, o[2] = m22;
@@ -149,7 +162,7 @@ __global__ void __launch_bounds__(kGT, 1) k_fine_grid(GridArgs a) {
   const int ngroups = (a.nsys + NS - 1) / NS;
   const int bc_t = (a.M - 1) / PT - c * kGT, bc_ip = (a.M - 1) % PT;  // thread / point of row M
   const int bc_i = (t == bc_t && (a.M - 1) / (kGT * PT) == c) ? bc_ip : -1;
-  unsigned pid = 0;  // passes published so far (flag values)
+  unsigned pid = 0;  // passes published so far (the tags)
   // The closed-form path serves every warp except the one holding row M (the boundary term):
   // at j = 0 and j = M−1 the closed-form off-diagonal only ever multiplies a zero entering state
   // (nothing precedes row 1 upward; above row M sit padding points, whose inputs are 0, so they
@@ -158,7 +171,7 @@ __global__ void __launch_bounds__(kGT, 1) k_fine_grid(GridArgs a) {
   const double J0 = (double)(g.j0 + 1);
   for (int grp = 0; grp < ngroups; ++grp) {
     // ---- inputs and boundary terms of the NS systems (slices ln0 + grp·NS + k)
-    double x[NS][PT];
+    St x[NS][PT];
 #pragma unroll
     for (int k = 0; k < NS; ++k) {
       const int s = grp * NS + k;
@@ -166,7 +179,7 @@ __global__ void __launch_bounds__(kGT, 1) k_fine_grid(GridArgs a) {
 #pragma unroll
       for (int i = 0; i < PT; ++i) {
         const int j = g.j0 + i;
-        x[k][i] = (u && j < a.M) ? (double)u[j] : 0.0;
+        x[k][i] = (u && j < a.M) ? (St)u[j] : (St)0;
       }
     }
     for (int q = t; q < NS * a.steps; q += kGT) {
@@ -203,7 +216,7 @@ __global__ void __launch_bounds__(kGT, 1) k_fine_grid(GridArgs a) {
         g.mults(a, sip, siq, i, ip, iq, l, u);
 #pragma unroll
         for (int k = 0; k < NS; ++k) {
-          const double v = x[k][i];
+          const double v = (double)x[k][i];
           double xn, zn = 0.0;
           if (up) {  // x: UL forward substitution (ncl = −l·iq); z: LU elimination (nml = −l·ip)
             xn = subst ? fma(-l * iq, xs[k], v) : v;
@@ -216,24 +229,25 @@ __global__ void __launch_bounds__(kGT, 1) k_fine_grid(GridArgs a) {
           }
           if (subst) xs[k] = xn;
           if (elim) zs[k] = zn;
-          if (write) x[k][i] = elim ? zn : xn;
+          if (write) x[k][i] = (St)(elim ? zn : xn);
         }
       };
       // interior point (every point of the thread strictly inside 1 … M−2, no boundary term):
       // J = J0 + i exactly, only the off-diagonal of this direction, no selects
       auto point_fast = [&](int i, double(&xs)[NS], double(&zs)[NS], bool write) {
         const double J = J0 + (double)i;
-        const double ip = sip[t * PT + i], iq = siq[t * PT + i];
+        const double ip = sip[i * kGT + t], iq = siq[i * kGT + t];
         const double nl = up ? J * fma(a.c1, J, -a.c0) : J * fma(a.c1, J, a.c0);  // −l or −u
         const double mx = nl * (up ? iq : ip), mz = nl * (up ? ip : iq), fz = up ? ip : iq;
 #pragma unroll
         for (int k = 0; k < NS; ++k) {
-          const double xn = subst ? fma(mx, xs[k], x[k][i]) : x[k][i];
+          const double xv = (double)x[k][i];
+          const double xn = subst ? fma(mx, xs[k], xv) : xv;
           double zn = 0.0;
           if (elim) zn = fma(mz, zs[k], fz * xn);
           if (subst) xs[k] = xn;
           if (elim) zs[k] = zn;
-          if (write) x[k][i] = elim ? zn : xn;
+          if (write) x[k][i] = (St)(elim ? zn : xn);
         }
       };
       auto run = [&](double(&xs)[NS], double(&zs)[NS], bool write) {
@@ -260,13 +274,13 @@ __global__ void __launch_bounds__(kGT, 1) k_fine_grid(GridArgs a) {
 #pragma unroll
       for (int l = 0; l < 5; ++l) {
         const int d = 1 << l;
-        const double *Cl = g.C[dir][l];
+        const double C0 = g.C(dir, l, 0), C1 = g.C(dir, l, 1), C2 = g.C(dir, l, 2);
 #pragma unroll
         for (int k = 0; k < NS; ++k) {
           const double q1 = up ? __shfl_up_sync(kFull, s1[k], d) : __shfl_down_sync(kFull, s1[k], d);
           const double q2 = up ? __shfl_up_sync(kFull, s2[k], d) : __shfl_down_sync(kFull, s2[k], d);
-          s2[k] = fma(Cl[1], q1, fma(Cl[2], q2, s2[k]));
-          s1[k] = fma(Cl[0], q1, s1[k]);
+          s2[k] = fma(C1, q1, fma(C2, q2, s2[k]));
+          s1[k] = fma(C0, q1, s1[k]);
         }
       }
       double xs1[NS], xs2[NS];
@@ -297,14 +311,19 @@ __global__ void __launch_bounds__(kGT, 1) k_fine_grid(GridArgs a) {
         }
       }
       ++pid;
-      // four pass slots: a CTA publishes pass pid+2 before its successors may have read pass pid
-      // when two passes in a row run upward (a group ending on a UL substitution, then the next
-      // group's first elimination); it cannot publish pid+4 before they finished pid (pass pid+2
-      // or pid+3 runs downward and waits for them)
-      const int par = pid & 3;
-      double *slot = a.tot + ((size_t)par * nCTA) * NS * 2;
-      if (t == 0) {  // the CTA total: all warps composed in pass order
-        double T1[NS], T2[NS];
+      // (4) publish and look-back, warp 0.  A CTA total is NS 2-vectors of fp64, published as
+      //     4·NS words (one 32-bit half | pass id << 32): 64-bit relaxed stores and loads are
+      //     single-copy atomic, so a word carries its own validity — no flag, no release/acquire
+      //     fences, and the poll that sees the tag has already read the data.  Four pass slots:
+      //     a CTA publishes pass pid+2 before its successors may have read pass pid when two
+      //     passes in a row run upward (a group ending on a UL substitution, then the next
+      //     group's first elimination); it cannot publish pid+4 before they finished pid (pass
+      //     pid+2 or pid+3 runs downward and waits for them)
+      constexpr int WPC = NS * 4;     // words per CTA total
+      constexpr int G = 32 / WPC;     // predecessors polled per round
+      unsigned long long *slot = a.tot + (size_t)(pid & 3) * nCTA * WPC;
+      if (w == 0) {
+        double T1[NS], T2[NS];  // the CTA total: all warps composed in pass order (every lane)
 #pragma unroll
         for (int k = 0; k < NS; ++k) T1[k] = 0.0, T2[k] = 0.0;
         for (int kk = 0; kk < kGW; ++kk) {
@@ -316,50 +335,64 @@ __global__ void __launch_bounds__(kGT, 1) k_fine_grid(GridArgs a) {
             T1[k] = fma(wm[q * 3], T1[k], t1);
           }
         }
+        if (lane == 0)
 #pragma unroll
-        for (int k = 0; k < NS; ++k) slot[(c * NS + k) * 2] = T1[k], slot[(c * NS + k) * 2 + 1] = T2[k];
-        st_release_u32(a.flag + c, pid);
-        if (tr) tr[1] = gtime();
-      }
-      // (4) look-back (warp 0): the totals of the W predecessors in pass direction
-      if (w == 0) {
+          for (int k = 0; k < NS; ++k) sT[k * 2] = T1[k], sT[k * 2 + 1] = T2[k];
+        __syncwarp();
+        if (lane < WPC) {  // word lane: value v = lane/2 (system v/2, component v&1), half lane&1
+          const double val = sT[lane >> 1];
+          const unsigned long long bits = (unsigned long long)__double_as_longlong(val);
+          const unsigned half = (lane & 1) ? (unsigned)(bits >> 32) : (unsigned)bits;
+          st_relaxed_u64(slot + (size_t)c * WPC + lane, ((unsigned long long)pid << 32) | half);
+        }
+        if (tr && lane == 0) tr[1] = gtime();
+        // look-back: the totals of the W predecessors in pass direction, G per round
+        // (lane = g·WPC + word), weighted by the host maps Π between predecessor and CTA
         const int W = a.lbW[dir * nCTA + c];
-        double e1[NS], e2[NS];
-#pragma unroll
-        for (int k = 0; k < NS; ++k) e1[k] = 0.0, e2[k] = 0.0;
-        for (int base = 0; base < W; base += 32) {
-          const int kq = base + lane + 1;  // predecessor distance
-          if (kq <= W) {
-            const int p = up ? c - kq : c + kq;
+        const int gi = lane / WPC, q = lane - gi * WPC;
+        // an even word lane holds value v = q/2 = (system v/2, component v&1) of its predecessor;
+        // its contributions to the entering state e = Σ Π·T: component 0 (T1) → e1 += Π11·T1,
+        // e2 += Π21·T1; component 1 (T2) → e2 += Π22·T2
+        double c1 = 0.0, c2 = 0.0;
+        for (int base = 0; base < W; base += G) {
+          const int kq = base + gi + 1;  // predecessor distance
+          const bool act = gi < G && kq <= W;
+          unsigned half = 0;
+          if (act) {
+            const unsigned long long *src = slot + (size_t)(up ? c - kq : c + kq) * WPC + q;
+            unsigned long long wd;
             long long spins = 0;
-            // relaxed polls (an ld.acquire per poll would invalidate L1 every time), one acquire
-            // fence once the flag is seen; the totals are then read from L2
-            while (ld_relaxed_u32(a.flag + p) < pid) {
+            while (((wd = ld_relaxed_u64(src)) >> 32) != pid) {
               if (++spins > kSpinMax) {
                 a.err[0] = 1;  // the host reports the solve as failed
                 break;
               }
             }
-            asm volatile("fence.acq_rel.gpu;" ::: "memory");
+            half = (unsigned)wd;
+          }
+          const unsigned hi = __shfl_down_sync(kFull, half, 1);
+          if (act && (q & 1) == 0) {
+            const double val = __longlong_as_double((long long)(((unsigned long long)hi << 32) | half));
             const double *P = a.lbP + (((size_t)dir * nCTA + c) * a.KW + (kq - 1)) * 3;
-#pragma unroll
-            for (int k = 0; k < NS; ++k) {
-              const double t1 = __ldcg(slot + (p * NS + k) * 2), t2 = __ldcg(slot + (p * NS + k) * 2 + 1);
-              e2[k] += fma(P[1], t1, P[2] * t2);
-              e1[k] += P[0] * t1;
+            if ((q >> 1) & 1) {
+              c2 = fma(P[2], val, c2);
+            } else {
+              c1 = fma(P[0], val, c1);
+              c2 = fma(P[1], val, c2);
             }
           }
         }
-#pragma unroll
-        for (int k = 0; k < NS; ++k)
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) {  // fixed-order tree (deterministic)
-            e1[k] += __shfl_down_sync(kFull, e1[k], o);
-            e2[k] += __shfl_down_sync(kFull, e2[k], o);
+        sred[lane * 2] = c1, sred[lane * 2 + 1] = c2;
+        __syncwarp();
+        if (lane < NS * 2) {  // lane 2k: e1 of system k, lane 2k+1: e2 (fixed order: deterministic)
+          const int k = lane >> 1;
+          double e = 0.0;
+          for (int g2 = 0; g2 < G; ++g2) {
+            const double *r = sred + (g2 * WPC + 4 * k) * 2;
+            e += (lane & 1) ? r[1] + r[5] : r[0];
           }
-        if (lane == 0)
-#pragma unroll
-          for (int k = 0; k < NS; ++k) sE[k * 2] = e1[k], sE[k * 2 + 1] = e2[k];
+          sE[lane] = e;
+        }
         if (tr && lane == 0) tr[2] = gtime();
       }
       __syncthreads();
@@ -383,8 +416,8 @@ __global__ void __launch_bounds__(kGT, 1) k_fine_grid(GridArgs a) {
         for (int k = 0; k < NS; ++k) {
           const double E1 = sE[k * 2], E2 = sE[k * 2 + 1];
           const double w1 = fma(M11, E1, f1[k]), w2 = fma(M21, E1, fma(M22, E2, f2[k]));
-          i2[k] = fma(g.X[dir][1], w1, fma(g.X[dir][2], w2, xs2[k]));
-          i1[k] = fma(g.X[dir][0], w1, xs1[k]);
+          i2[k] = fma(g.X(dir, 1), w1, fma(g.X(dir, 2), w2, xs2[k]));
+          i1[k] = fma(g.X(dir, 0), w1, xs1[k]);
         }
       }
       run(i1, i2, true);
@@ -415,7 +448,7 @@ __global__ void __launch_bounds__(kGT, 1) k_fine_grid(GridArgs a) {
 #pragma unroll
       for (int i = 0; i < PT; ++i) {
         const int j = g.j0 + i;
-        if (j < a.M) dst[j] = gh ? (float)(x[k][i] - (double)gh[j]) : (float)x[k][i];
+        if (j < a.M) dst[j] = gh ? (float)((double)x[k][i] - (double)gh[j]) : (float)x[k][i];
       }
     }
     __syncthreads();  // sbc is rewritten by the next group
@@ -424,22 +457,27 @@ __global__ void __launch_bounds__(kGT, 1) k_fine_grid(GridArgs a) {
 
 namespace {
 using GridKernel = void (*)(GridArgs);
-template <int NS>
+// systems per group for PT points per thread: the state NS·PT fp64 values must fit the registers
+// (fp32 storage of 3 systems at PT = 28 was measured slower: the F2F conversions per point and
+// pass cost more than the third system saves)
+constexpr int ns_for(int PT) { return PT >= 28 ? 2 : 4; }
 GridKernel grid_kernel(int PT) {
   switch (PT) {
-    case 4: return k_fine_grid<4, NS>;
-    case 8: return k_fine_grid<8, NS>;
-    case 16: return k_fine_grid<16, NS>;
-    case 28: return k_fine_grid<28, NS>;
+    case 4: return k_fine_grid<4, ns_for(4), double>;
+    case 8: return k_fine_grid<8, ns_for(8), double>;
+    case 16: return k_fine_grid<16, ns_for(16), double>;
+    case 28: return k_fine_grid<28, ns_for(28), double>;
   }
   return nullptr;
 }
 constexpr int kPTs[] = {4, 8, 16, 28};
-constexpr int kNS = 2;
 }  // namespace
 
+int fine_grid_ns(int PT) { return ns_for(PT); }
 size_t fine_grid_smem(int PT, int steps) {
-  return ((size_t)2 * kGT * PT + 2 * kGW * 3 + kGW * kNS * 2 + kNS * 2 + (size_t)kNS * steps) * sizeof(double);
+  const int NS = ns_for(PT);
+  return ((size_t)2 * kGT * PT + 2 * kGW * 3 + kGW * NS * 2 + NS * 4 + 64 + (size_t)(30 + 6) * kGT + (size_t)NS * steps) *
+         sizeof(double);
 }
 
 // Points per thread and CTAs for M grid points on nsm SMs (one CTA per SM): the smallest PT with
@@ -455,10 +493,9 @@ int fine_grid_pt(int M, int nsm, int *nblocks) {
   }
   return 0;
 }
-int fine_grid_ns() { return kNS; }
 
 cudaError_t launch_fine_grid(const GridArgs &a, int PT, int nblocks, cudaStream_t s) {
-  GridKernel k = grid_kernel<kNS>(PT);
+  GridKernel k = grid_kernel(PT);
   if (!k) return cudaErrorInvalidValue;
   const size_t smem = fine_grid_smem(PT, a.steps);
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -58,8 +58,9 @@ struct GridArgs {
   const double *lbP;                 // [2][nCTA][KW][3] look-back weights (maps between predecessor and CTA)
   const int *lbW;                    // [2][nCTA] look-back windows
   int KW;
-  double *tot;                       // [4][nCTA][NS][2] published CTA totals per pass slot
-  unsigned *flag;                    // [nCTA] last pass published (zeroed before the launch)
+  unsigned long long *tot;           // [4][nCTA][NS·2][2] published CTA totals per pass slot: each
+                                     // fp64 total as two words (32-bit half | pass id << 32), zeroed
+                                     // before the launch
   int *err;                          // set when a look-back wait times out
   const float *U, *Gh;               // [.][row] inputs U_n, Ĝ_n
   float *D, *Fk, *Fout;              // outputs: D_n = F̂_n − Ĝ_n, F̂ of local slice fk_ln, or F̂ rows (test hook)
@@ -68,7 +69,7 @@ struct GridArgs {
 };
 size_t fine_grid_smem(int PT, int steps);
 int fine_grid_pt(int M, int nsm, int *nblocks);  // points per thread for M points (0: too large)
-int fine_grid_ns();                               // systems per group
+int fine_grid_ns(int PT);                         // systems per group for PT points per thread
 cudaError_t launch_fine_grid(const GridArgs &a, int PT, int nblocks, cudaStream_t s);
 // Pipelined Parareal on one GPU (pipe.cu, NEXT-2): PINN chain (latency mode) and K1 fine solves
 // in one cooperative kernel, synchronised per slice.

@@ -174,8 +174,8 @@ struct pr_ctx {
   int opt_wavefront = 0;             // PR_OPT_WAVEFRONT: 0 auto, 1 blocking chain, n ≥ 2 chunks
   int opt_spatial = 0;               // PR_OPT_SPATIAL_CHAIN: 0 auto, 1 off, 2 on
   // K2R grid-resident fine solver: published totals, flags, timeout flag (mapped host memory)
-  double *g_tot = nullptr;
-  unsigned *g_flag = nullptr;
+  unsigned long long *g_tot = nullptr;  // K2R published totals (tagged 32-bit halves)
+  size_t g_tot_words = 0;
   int *g_err_h = nullptr, *g_err_d = nullptr;
   // spatially sharded chain (NEXT-4): every slice's rows, this rank's j-range meaningful
   float *sp_U = nullptr, *sp_Gh = nullptr, *sp_D = nullptr, *sp_F = nullptr;
@@ -854,22 +854,30 @@ pr_status launch_pinn(pr_ctx *c, const pr::PinnArgs &a0, int cta_lo = 0, int cta
 }
 
 // ---------------------------------------------------------------- K2R grid-resident fine sweep
-// Used for θ = 1, one instance, M > kResidentMaxM when the partition fits the GPU, for sweeps of
-// at most kGridMaxSys systems (auto; measured at 2^20 points: 1.74× K2 for 1 system, 2.05× for 2,
-// 1.19× for 8, equal at 16, K2 ahead at 64 — the grid solver's pass is latency-bound and solves
-// 2 systems at a time, K2 streams all of them), or forced with PR_OPT_FINE_KERNEL = 3.
-constexpr int kGridMaxSys = 16;
+// Used for θ = 1, one instance, M > kResidentMaxM when the partition fits the GPU and the cost
+// model below predicts it ahead of K2 (auto), or forced with PR_OPT_FINE_KERNEL = 3.  The model
+// (µs per fine step of the sweep; constants fitted to scripts/grid_vs_k2.py on B200,
+// profiles/r02/grid_vs_k2.txt, M = 2^12 … 2^20, 4 … 64 systems, within ~15 %):
+//   K2    12 + 16 B · M · nsys / 4.4 TB/s         (launch/look-back floor + HBM streaming)
+//   grid  ⌈nsys / NS⌉ · (2.7 + 1.9 · min(nCTA, 100) / 100)  (one latency-bound pass per group)
+// e.g. 2^20 points: grid ahead at every count (1.7× at 64 systems); 2^12 … 2^18 points: grid
+// up to ~16 systems, K2 beyond (its cost stays near the floor while the grid's grows per group).
 bool use_grid(const pr_ctx *c, int nsys) {
   // (not with the in-process loopback transport: its ranks share one GPU, and the cooperative
   // grid of one rank cannot be co-resident with another's)
   if (!c->fine.g_pt || c->loop || c->opt_fine_kernel == 1 || c->opt_fine_kernel == 2) return false;
-  return c->opt_fine_kernel == 3 || (c->M > kResidentMaxM && nsys <= kGridMaxSys);
+  if (c->opt_fine_kernel == 3) return true;
+  if (c->M <= kResidentMaxM) return false;
+  const double k2 = 12.0 + 16.0 * (double)c->M * nsys / 4.4e6;
+  const int ns = pr::fine_grid_ns(c->fine.g_pt);
+  const double grid = (double)((nsys + ns - 1) / ns) * (2.7 + 1.9 * std::min(c->fine.g_nb, 100) / 100.0);
+  return grid < k2;
 }
 pr_status ensure_grid(pr_ctx *c) {
   if (c->g_tot) return PR_OK;
   const int nb = c->fine.g_nb;
-  CU(cudaMalloc(&c->g_tot, (size_t)4 * nb * pr::fine_grid_ns() * 2 * sizeof(double)));
-  CU(cudaMalloc(&c->g_flag, (size_t)nb * sizeof(unsigned)));
+  c->g_tot_words = (size_t)4 * nb * pr::fine_grid_ns(c->fine.g_pt) * 4;
+  CU(cudaMalloc(&c->g_tot, c->g_tot_words * sizeof(unsigned long long)));
   CU(cudaHostAlloc((void **)&c->g_err_h, sizeof(int), cudaHostAllocMapped));
   *c->g_err_h = 0;
   CU(cudaHostGetDevicePointer((void **)&c->g_err_d, c->g_err_h, 0));
@@ -903,7 +911,6 @@ pr_status grid_sweep(pr_ctx *c, int ln0, int nsl, int n_base, const float *U, fl
   g.lbW = sc.lbW;
   g.KW = sc.g_kw;
   g.tot = c->g_tot;
-  g.flag = c->g_flag;
   g.err = c->g_err_d;
   g.U = U;
   g.Gh = c->Gh;
@@ -911,10 +918,10 @@ pr_status grid_sweep(pr_ctx *c, int ln0, int nsl, int n_base, const float *U, fl
   g.Fk = c->Fk;
   g.Fout = Fout;
   g.fk_ln = fk_ln;
-  CU(cudaMemsetAsync(c->g_flag, 0, (size_t)sc.g_nb * sizeof(unsigned), c->stream));
+  CU(cudaMemsetAsync(c->g_tot, 0, c->g_tot_words * sizeof(unsigned long long), c->stream));  // tags 0
   // PR_GRID_TRACE=file (tuning): %globaltimer stamps per pass and CTA, written after the launch
   static const char *trace_path = getenv("PR_GRID_TRACE");
-  const size_t npass = (size_t)((nsl + pr::fine_grid_ns() - 1) / pr::fine_grid_ns()) * (sc.steps + 1);
+  const size_t npass = (size_t)((nsl + pr::fine_grid_ns(sc.g_pt) - 1) / pr::fine_grid_ns(sc.g_pt)) * (sc.steps + 1);
   unsigned long long *trace = nullptr;
   if (trace_path && !c->capturing) {
     CU(cudaMalloc(&trace, npass * sc.g_nb * 5 * sizeof(unsigned long long)));
@@ -2442,7 +2449,6 @@ void parareal_free(pr_ctx *c) {
   if (c->h_delta) cudaFreeHost(c->h_delta);
   cudaFree(c->pipe_partials);
   cudaFree(c->g_tot);
-  cudaFree(c->g_flag);
   if (c->g_err_h) cudaFreeHost(c->g_err_h);
   cudaFree(c->sp_U);
   cudaFree(c->sp_Gh);
