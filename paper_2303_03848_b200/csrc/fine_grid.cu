@@ -25,6 +25,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <type_traits>
 
 namespace pr {
@@ -80,13 +81,14 @@ __global__ void __launch_bounds__(kGT, 1) k_fine_grid(GridArgs a) {
   extern __shared__ __align__(16) double gsm[];
   double *sip = gsm, *siq = gsm + kGT * PT;          // this CTA's 1/p, 1/q, [PT][kGT]
   double *swm = siq + kGT * PT;                        // [2][kGW][3] constant warp maps
-  double *swt = swm + 2 * kGW * 3;                     // [kGW][NS][2] warp totals of the pass
-  double *sE = swt + kGW * NS * 2;                     // [NS][2] CTA entering state
+  double *swt = swm + 2 * kGW * 3;                     // [2][kGW][NS][2] warp totals (by pass parity)
+  double *sE = swt + 2 * kGW * NS * 2;                 // [NS][2] CTA entering state
   double *sT = sE + NS * 2;                            // [NS][2] CTA total of the pass
   double *sred = sT + NS * 2;                          // [32][2] look-back partial sums (warp 0)
   double *sC = sred + 64;                              // [2][5][3][kGT] level coefficients
   double *sX = sC + 2 * 5 * 3 * kGT;                   // [2][3][kGT] exclusive maps
-  double *sbc = sX + 2 * 3 * kGT;                      // [NS][steps] boundary terms
+  double *sxs = sX + 2 * 3 * kGT;                      // [NS][2][kGT] lanes' exclusive warp prefixes
+  double *sbc = sxs + NS * 2 * kGT;                    // [NS][steps] boundary terms
   GridSolver<PT, NS> g;
   g.sC = sC;
   g.sX = sX;
@@ -210,6 +212,9 @@ __global__ void __launch_bounds__(kGT, 1) k_fine_grid(GridArgs a) {
       double s1[NS], s2[NS];
 #pragma unroll
       for (int k = 0; k < NS; ++k) s1[k] = 0.0, s2[k] = 0.0;
+      // this pass's warp totals (double-buffered: a warp may write the next pass's while another
+      // still folds this pass's in step 5)
+      double *swtb = swt + (pid & 1) * (kGW * NS * 2);
       // general point: boundary rows (no l at j = 0, no u at j = M−1), padding, the boundary term
       auto point = [&](int i, double(&xs)[NS], double(&zs)[NS], bool write) {
         double ip, iq, l, u;
@@ -283,33 +288,18 @@ __global__ void __launch_bounds__(kGT, 1) k_fine_grid(GridArgs a) {
           s1[k] = fma(C0, q1, s1[k]);
         }
       }
-      double xs1[NS], xs2[NS];
+      // the lane's exclusive prefix, parked in shared memory until step 5 (register pressure)
 #pragma unroll
       for (int k = 0; k < NS; ++k) {
-        xs1[k] = up ? __shfl_up_sync(kFull, s1[k], 1) : __shfl_down_sync(kFull, s1[k], 1);
-        xs2[k] = up ? __shfl_up_sync(kFull, s2[k], 1) : __shfl_down_sync(kFull, s2[k], 1);
-        if (lane == (up ? 0 : 31)) xs1[k] = 0.0, xs2[k] = 0.0;
-        if (lane == (up ? 31 : 0)) swt[(w * NS + k) * 2] = s1[k], swt[(w * NS + k) * 2 + 1] = s2[k];
+        double xs1 = up ? __shfl_up_sync(kFull, s1[k], 1) : __shfl_down_sync(kFull, s1[k], 1);
+        double xs2 = up ? __shfl_up_sync(kFull, s2[k], 1) : __shfl_down_sync(kFull, s2[k], 1);
+        if (lane == (up ? 0 : 31)) xs1 = 0.0, xs2 = 0.0;
+        sxs[(k * 2) * kGT + t] = xs1;
+        sxs[(k * 2 + 1) * kGT + t] = xs2;
+        if (lane == (up ? 31 : 0)) swtb[(w * NS + k) * 2] = s1[k], swtb[(w * NS + k) * 2 + 1] = s2[k];
       }
       __syncthreads();
-      // (3) this warp's entering within the CTA (fold of the preceding warps' totals), and the
-      //     CTA total (thread 0) → published with the pass id
-      const double *wm = swm + dir * kGW * 3;
-      double f1[NS], f2[NS];
-#pragma unroll
-      for (int k = 0; k < NS; ++k) f1[k] = 0.0, f2[k] = 0.0;
-#pragma unroll
-      for (int kk = 0; kk < kGW; ++kk) {
-        const int q = up ? kk : kGW - 1 - kk;
-        if (up ? q < w : q > w) {
-#pragma unroll
-          for (int k = 0; k < NS; ++k) {
-            const double t1 = swt[(q * NS + k) * 2], t2 = swt[(q * NS + k) * 2 + 1];
-            f2[k] = fma(wm[q * 3 + 1], f1[k], fma(wm[q * 3 + 2], f2[k], t2));
-            f1[k] = fma(wm[q * 3], f1[k], t1);
-          }
-        }
-      }
+      const double *wm = swm + dir * kGW * 3;  // constant warp maps of this direction
       ++pid;
       // (4) publish and look-back, warp 0.  A CTA total is NS 2-vectors of fp64, published as
       //     4·NS words (one 32-bit half | pass id << 32): 64-bit relaxed stores and loads are
@@ -326,11 +316,12 @@ __global__ void __launch_bounds__(kGT, 1) k_fine_grid(GridArgs a) {
         double T1[NS], T2[NS];  // the CTA total: all warps composed in pass order (every lane)
 #pragma unroll
         for (int k = 0; k < NS; ++k) T1[k] = 0.0, T2[k] = 0.0;
+#pragma unroll 1
         for (int kk = 0; kk < kGW; ++kk) {
           const int q = up ? kk : kGW - 1 - kk;
 #pragma unroll
           for (int k = 0; k < NS; ++k) {
-            const double t1 = swt[(q * NS + k) * 2], t2 = swt[(q * NS + k) * 2 + 1];
+            const double t1 = swtb[(q * NS + k) * 2], t2 = swtb[(q * NS + k) * 2 + 1];
             T2[k] = fma(wm[q * 3 + 1], T1[k], fma(wm[q * 3 + 2], T2[k], t2));
             T1[k] = fma(wm[q * 3], T1[k], t1);
           }
@@ -397,27 +388,29 @@ __global__ void __launch_bounds__(kGT, 1) k_fine_grid(GridArgs a) {
       }
       __syncthreads();
       if (tr && t == 0) tr[3] = gtime();
-      // (5) this thread's entering state: warp map of the preceding warps applied to the CTA
-      //     entering state, plus their fold, then the lane's exclusive prefix; rerun
+      // (5) this thread's entering state: the CTA entering state carried through the preceding
+      //     warps (their maps and totals, in pass order), then the lane's exclusive prefix; rerun
       double i1[NS], i2[NS];
       {
-        // composite map of the preceding warps in pass order (constant, recomputed: ≤ 7 products)
-        double M11 = 1.0, M21 = 0.0, M22 = 1.0;
+        double w1[NS], w2[NS];
 #pragma unroll
+        for (int k = 0; k < NS; ++k) w1[k] = sE[k * 2], w2[k] = sE[k * 2 + 1];
+#pragma unroll 1
         for (int kk = 0; kk < kGW; ++kk) {
           const int q = up ? kk : kGW - 1 - kk;
           if (up ? q < w : q > w) {
-            M21 = fma(wm[q * 3 + 1], M11, wm[q * 3 + 2] * M21);
-            M11 *= wm[q * 3];
-            M22 *= wm[q * 3 + 2];
+#pragma unroll
+            for (int k = 0; k < NS; ++k) {
+              const double t1 = swtb[(q * NS + k) * 2], t2 = swtb[(q * NS + k) * 2 + 1];
+              w2[k] = fma(wm[q * 3 + 1], w1[k], fma(wm[q * 3 + 2], w2[k], t2));
+              w1[k] = fma(wm[q * 3], w1[k], t1);
+            }
           }
         }
 #pragma unroll
         for (int k = 0; k < NS; ++k) {
-          const double E1 = sE[k * 2], E2 = sE[k * 2 + 1];
-          const double w1 = fma(M11, E1, f1[k]), w2 = fma(M21, E1, fma(M22, E2, f2[k]));
-          i2[k] = fma(g.X(dir, 1), w1, fma(g.X(dir, 2), w2, xs2[k]));
-          i1[k] = fma(g.X(dir, 0), w1, xs1[k]);
+          i2[k] = fma(g.X(dir, 1), w1[k], fma(g.X(dir, 2), w2[k], sxs[(k * 2 + 1) * kGT + t]));
+          i1[k] = fma(g.X(dir, 0), w1[k], sxs[(k * 2) * kGT + t]);
         }
       }
       run(i1, i2, true);
@@ -458,25 +451,38 @@ __global__ void __launch_bounds__(kGT, 1) k_fine_grid(GridArgs a) {
 namespace {
 using GridKernel = void (*)(GridArgs);
 // systems per group for PT points per thread: the state NS·PT fp64 values must fit the registers
-// (fp32 storage of 3 systems at PT = 28 was measured slower: the F2F conversions per point and
-// pass cost more than the third system saves)
-constexpr int ns_for(int PT) { return PT >= 28 ? 2 : 4; }
-GridKernel grid_kernel(int PT) {
-  switch (PT) {
-    case 4: return k_fine_grid<4, ns_for(4), double>;
-    case 8: return k_fine_grid<8, ns_for(8), double>;
-    case 16: return k_fine_grid<16, ns_for(16), double>;
-    case 28: return k_fine_grid<28, ns_for(28), double>;
+// Systems per group: the state NS·PT fp64 values live in registers, so NS is bounded by PT (PT =
+// 28: 2; 16: 4; ≤ 8: 8) and chosen per launch as the smallest of {2, 4, 8} covering the sweep's
+// systems (a group computes all NS systems whether used or not).  Measured: 3 systems at PT = 28
+// (fp64 with 52 B of spills, or fp32 storage — the F2F conversions per point and pass) were
+// slower per system than 2.
+constexpr int ns_max(int PT) { return PT >= 28 ? 2 : PT >= 16 ? 4 : 8; }
+int ns_pick(int PT, int nsys) {
+  const int mx = ns_max(PT);
+  return nsys <= 2 ? 2 : (nsys <= 4 || mx == 4) ? std::min(4, mx) : mx;
+}
+GridKernel grid_kernel(int PT, int NS) {
+  switch (PT * 16 + NS) {
+    case 4 * 16 + 2: return k_fine_grid<4, 2, double>;
+    case 4 * 16 + 4: return k_fine_grid<4, 4, double>;
+    case 4 * 16 + 8: return k_fine_grid<4, 8, double>;
+    case 8 * 16 + 2: return k_fine_grid<8, 2, double>;
+    case 8 * 16 + 4: return k_fine_grid<8, 4, double>;
+    case 8 * 16 + 8: return k_fine_grid<8, 8, double>;
+    case 16 * 16 + 2: return k_fine_grid<16, 2, double>;
+    case 16 * 16 + 4: return k_fine_grid<16, 4, double>;
+    case 28 * 16 + 2: return k_fine_grid<28, 2, double>;
   }
   return nullptr;
 }
 constexpr int kPTs[] = {4, 8, 16, 28};
 }  // namespace
 
-int fine_grid_ns(int PT) { return ns_for(PT); }
-size_t fine_grid_smem(int PT, int steps) {
-  const int NS = ns_for(PT);
-  return ((size_t)2 * kGT * PT + 2 * kGW * 3 + kGW * NS * 2 + NS * 4 + 64 + (size_t)(30 + 6) * kGT + (size_t)NS * steps) *
+int fine_grid_ns(int PT, int nsys) { return ns_pick(PT, nsys); }
+size_t fine_grid_smem(int PT, int steps) {  // at the largest NS of PT (every launch fits)
+  const int NS = ns_max(PT);
+  return ((size_t)2 * kGT * PT + 2 * kGW * 3 + 2 * kGW * NS * 2 + NS * 4 + 64 + (size_t)(30 + 6 + NS * 2) * kGT +
+          (size_t)NS * steps) *
          sizeof(double);
 }
 
@@ -495,7 +501,7 @@ int fine_grid_pt(int M, int nsm, int *nblocks) {
 }
 
 cudaError_t launch_fine_grid(const GridArgs &a, int PT, int nblocks, cudaStream_t s) {
-  GridKernel k = grid_kernel(PT);
+  GridKernel k = grid_kernel(PT, ns_pick(PT, a.nsys));
   if (!k) return cudaErrorInvalidValue;
   const size_t smem = fine_grid_smem(PT, a.steps);
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -69,7 +69,7 @@ struct GridArgs {
 };
 size_t fine_grid_smem(int PT, int steps);
 int fine_grid_pt(int M, int nsm, int *nblocks);  // points per thread for M points (0: too large)
-int fine_grid_ns(int PT);                         // systems per group for PT points per thread
+int fine_grid_ns(int PT, int nsys);               // systems per group of a launch over nsys systems
 cudaError_t launch_fine_grid(const GridArgs &a, int PT, int nblocks, cudaStream_t s);
 // Pipelined Parareal on one GPU (pipe.cu, NEXT-2): PINN chain (latency mode) and K1 fine solves
 // in one cooperative kernel, synchronised per slice.

@@ -372,6 +372,9 @@ pr_status grid_tables(pr_ctx *c, Scheme &sc, double dtau, const std::vector<doub
   int nb = 0;
   const int PT = pr::fine_grid_pt(c->M, nsm, &nb);
   if (!PT) return PR_OK;  // too large for one pass over the GPU: K2 only
+  int smem_max = 0;
+  CU(cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  if (pr::fine_grid_smem(PT, sc.steps) > (size_t)smem_max) return PR_OK;  // boundary terms of very long slices: K2
   const int M = c->M;
   const double sg = c->sets[0].first, rr = c->sets[0].second;
   const double c0 = dtau * (0.5 * rr), c1 = dtau * (0.5 * sg * sg);
@@ -858,10 +861,11 @@ pr_status launch_pinn(pr_ctx *c, const pr::PinnArgs &a0, int cta_lo = 0, int cta
 // model below predicts it ahead of K2 (auto), or forced with PR_OPT_FINE_KERNEL = 3.  The model
 // (µs per fine step of the sweep; constants fitted to scripts/grid_vs_k2.py on B200,
 // profiles/r02/grid_vs_k2.txt, M = 2^12 … 2^20, 4 … 64 systems, within ~15 %):
-//   K2    12 + 16 B · M · nsys / 4.4 TB/s         (launch/look-back floor + HBM streaming)
-//   grid  ⌈nsys / NS⌉ · (2.7 + 1.9 · min(nCTA, 100) / 100)  (one latency-bound pass per group)
-// e.g. 2^20 points: grid ahead at every count (1.7× at 64 systems); 2^12 … 2^18 points: grid
-// up to ~16 systems, K2 beyond (its cost stays near the floor while the grid's grows per group).
+//   K2    12 + 16 B · M · nsys / 4.4 TB/s             (launch/look-back floor + HBM streaming)
+//   grid  ⌈nsys / NS⌉ · (0.4 + 3.5 · nCTA/148 + 0.5 · NS)  (one latency-bound pass per group)
+// e.g. 2^18 … 2^20 points: grid ahead at every count (1.7× at 64 systems of 2^20); 2^12 … 2^16
+// points: grid up to ~16 systems, K2 beyond (its cost stays near the floor, the grid's grows
+// per group).
 bool use_grid(const pr_ctx *c, int nsys) {
   // (not with the in-process loopback transport: its ranks share one GPU, and the cooperative
   // grid of one rank cannot be co-resident with another's)
@@ -869,14 +873,14 @@ bool use_grid(const pr_ctx *c, int nsys) {
   if (c->opt_fine_kernel == 3) return true;
   if (c->M <= kResidentMaxM) return false;
   const double k2 = 12.0 + 16.0 * (double)c->M * nsys / 4.4e6;
-  const int ns = pr::fine_grid_ns(c->fine.g_pt);
-  const double grid = (double)((nsys + ns - 1) / ns) * (2.7 + 1.9 * std::min(c->fine.g_nb, 100) / 100.0);
+  const int ns = pr::fine_grid_ns(c->fine.g_pt, nsys);
+  const double grid = (double)((nsys + ns - 1) / ns) * (0.4 + 3.5 * c->fine.g_nb / 148.0 + 0.5 * ns);
   return grid < k2;
 }
 pr_status ensure_grid(pr_ctx *c) {
   if (c->g_tot) return PR_OK;
   const int nb = c->fine.g_nb;
-  c->g_tot_words = (size_t)4 * nb * pr::fine_grid_ns(c->fine.g_pt) * 4;
+  c->g_tot_words = (size_t)4 * nb * pr::fine_grid_ns(c->fine.g_pt, 1 << 30) * 4;
   CU(cudaMalloc(&c->g_tot, c->g_tot_words * sizeof(unsigned long long)));
   CU(cudaHostAlloc((void **)&c->g_err_h, sizeof(int), cudaHostAllocMapped));
   *c->g_err_h = 0;
@@ -921,7 +925,8 @@ pr_status grid_sweep(pr_ctx *c, int ln0, int nsl, int n_base, const float *U, fl
   CU(cudaMemsetAsync(c->g_tot, 0, c->g_tot_words * sizeof(unsigned long long), c->stream));  // tags 0
   // PR_GRID_TRACE=file (tuning): %globaltimer stamps per pass and CTA, written after the launch
   static const char *trace_path = getenv("PR_GRID_TRACE");
-  const size_t npass = (size_t)((nsl + pr::fine_grid_ns(sc.g_pt) - 1) / pr::fine_grid_ns(sc.g_pt)) * (sc.steps + 1);
+  const int ns = pr::fine_grid_ns(sc.g_pt, nsl);
+  const size_t npass = (size_t)((nsl + ns - 1) / ns) * (sc.steps + 1);
   unsigned long long *trace = nullptr;
   if (trace_path && !c->capturing) {
     CU(cudaMalloc(&trace, npass * sc.g_nb * 5 * sizeof(unsigned long long)));
