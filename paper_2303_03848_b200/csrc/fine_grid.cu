@@ -35,6 +35,7 @@ namespace {
 constexpr int kGT = 256;        // threads per CTA
 constexpr int kGW = kGT / 32;   // warps per CTA
 constexpr long long kSpinMax = 1ll << 28;  // look-back wait bound (then the solve fails, no hang)
+constexpr int kPollRounds = 4;             // look-back rounds whose loads are in flight together
 
 __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long *p) {
   unsigned long long v;
@@ -344,32 +345,43 @@ __global__ void __launch_bounds__(kGT, 1) k_fine_grid(GridArgs a) {
         // an even word lane holds value v = q/2 = (system v/2, component v&1) of its predecessor;
         // its contributions to the entering state e = Σ Π·T: component 0 (T1) → e1 += Π11·T1,
         // e2 += Π21·T1; component 1 (T2) → e2 += Π22·T2
+        // the loads of up to kPollRounds rounds are issued together (one L2 round trip for the
+        // whole window instead of one per round; the summation order is the rounds' order)
         double c1 = 0.0, c2 = 0.0;
-        for (int base = 0; base < W; base += G) {
-          const int kq = base + gi + 1;  // predecessor distance
-          const bool act = gi < G && kq <= W;
-          unsigned half = 0;
-          if (act) {
-            const unsigned long long *src = slot + (size_t)(up ? c - kq : c + kq) * WPC + q;
-            unsigned long long wd;
-            long long spins = 0;
-            while (((wd = ld_relaxed_u64(src)) >> 32) != pid) {
-              if (++spins > kSpinMax) {
-                a.err[0] = 1;  // the host reports the solve as failed
-                break;
-              }
-            }
-            half = (unsigned)wd;
+        for (int base0 = 0; base0 < W; base0 += kPollRounds * G) {
+          unsigned long long wd[kPollRounds];
+#pragma unroll
+          for (int r = 0; r < kPollRounds; ++r) {
+            const int kq = base0 + r * G + gi + 1;  // predecessor distance
+            wd[r] = (gi < G && kq <= W) ? ld_relaxed_u64(slot + (size_t)(up ? c - kq : c + kq) * WPC + q) : 0ull;
           }
-          const unsigned hi = __shfl_down_sync(kFull, half, 1);
-          if (act && (q & 1) == 0) {
-            const double val = __longlong_as_double((long long)(((unsigned long long)hi << 32) | half));
-            const double *P = a.lbP + (((size_t)dir * nCTA + c) * a.KW + (kq - 1)) * 3;
-            if ((q >> 1) & 1) {
-              c2 = fma(P[2], val, c2);
-            } else {
-              c1 = fma(P[0], val, c1);
-              c2 = fma(P[1], val, c2);
+#pragma unroll
+          for (int r = 0; r < kPollRounds; ++r) {
+            const int kq = base0 + r * G + gi + 1;
+            const bool act = gi < G && kq <= W;
+            unsigned half = 0;
+            if (act) {
+              const unsigned long long *src = slot + (size_t)(up ? c - kq : c + kq) * WPC + q;
+              long long spins = 0;
+              while ((wd[r] >> 32) != pid) {
+                wd[r] = ld_relaxed_u64(src);
+                if (++spins > kSpinMax) {
+                  a.err[0] = 1;  // the host reports the solve as failed
+                  break;
+                }
+              }
+              half = (unsigned)wd[r];
+            }
+            const unsigned hi = __shfl_down_sync(kFull, half, 1);
+            if (act && (q & 1) == 0) {
+              const double val = __longlong_as_double((long long)(((unsigned long long)hi << 32) | half));
+              const double *P = a.lbP + (((size_t)dir * nCTA + c) * a.KW + (kq - 1)) * 3;
+              if ((q >> 1) & 1) {
+                c2 = fma(P[2], val, c2);
+              } else {
+                c1 = fma(P[0], val, c1);
+                c2 = fma(P[1], val, c2);
+              }
             }
           }
         }
