@@ -275,7 +275,39 @@ __global__ void __launch_bounds__(kGT, 1) k_fine_grid(GridArgs a) {
           }
         }
       };
-      run(s1, s2, false);
+      if (kind == 1 && fast) {
+        // local run of a merged pass over interior points from a zero entering state, with the
+        // elimination chain in scaled form t = z/f (f = ip upward, iq downward):
+        //   t_i = x̂_i + (−l_i or −u_i)·f_{i∓1}·t_{i∓1},   z_last = f_last·t_last
+        // (one FMA per point and system instead of a multiply and an FMA; only the totals are
+        // needed here — the rerun produces the outputs in the unscaled form)
+        double fprev = 0.0;
+#pragma unroll
+        for (int ii = 0; ii < PT; ++ii) {
+          const int i = up ? ii : PT - 1 - ii;
+          const double J = J0 + (double)i;
+          const double ip = sip[i * kGT + t], iq = siq[i * kGT + t];
+          const double nl = up ? J * fma(a.c1, J, -a.c0) : J * fma(a.c1, J, a.c0);  // −l or −u
+          const double mx = nl * (up ? iq : ip), f = up ? ip : iq;
+          const double cz = nl * fprev;  // (ii = 0: the entering state is zero, cz unused)
+#pragma unroll
+          for (int k = 0; k < NS; ++k) {
+            const double xv = (double)x[k][i];
+            if (ii == 0) {
+              s1[k] = xv;
+              s2[k] = xv;
+            } else {
+              s1[k] = fma(mx, s1[k], xv);
+              s2[k] = fma(cz, s2[k], s1[k]);
+            }
+          }
+          fprev = f;
+        }
+#pragma unroll
+        for (int k = 0; k < NS; ++k) s2[k] *= fprev;
+      } else {
+        run(s1, s2, false);
+      }
       // (2) warp scan of the NS 2-vectors with the precomputed level coefficients
 #pragma unroll
       for (int l = 0; l < 5; ++l) {
