@@ -201,7 +201,10 @@ pr_status parareal_plan_iteration(int32_t N, int32_t world, int32_t rank, int32_
 
 /* Tuning/test options (values are validated; unknown keys → PR_ERR_INVALID_ARGUMENT). */
 enum {
-  PR_OPT_FINE_KERNEL = 1,   /* 0 auto, 1 resident (M ≤ 4096), 2 streamed            */
+  PR_OPT_FINE_KERNEL = 1,   /* 0 auto, 1 resident K1 (M ≤ 2048), 2 streamed K2, 3 grid-resident K2R
+                               (θ = 1, B = 1, M > 2048, partition fits the GPU; else PR_ERR_UNSUPPORTED).
+                               Auto: K1 for M ≤ 2048, else K2R or K2 by a fitted cost model (K2R for
+                               every sweep at 2^18 … 2^20 points, K2 for many small systems).  */
   PR_OPT_USE_GRAPHS = 2,    /* 0/1: a fixed-K (tol == 0), single-GPU solve with device pointers (or pinned
                                host buffers, whose copies become graph nodes) is captured
                                into a CUDA graph on its first call per (V_T, V_0) pair and replayed on

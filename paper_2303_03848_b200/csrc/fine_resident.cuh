@@ -1,4 +1,4 @@
-// fine_resident.cuh — K1: on-chip implicit-Euler propagator for M ≤ 4096.
+// fine_resident.cuh — K1: on-chip implicit-Euler propagator for M ≤ 2048 (kResidentMaxM).
 //
 // One "system" = one (instance, slice) state vector of M interior points
 // (§3.2), owned by NT threads with P consecutive points each.
