@@ -399,13 +399,23 @@ struct Tri<P, NT, false, true> {
     e1 = fma(X[0], i1, xs1);
   }
 
+  // the boundary term dτ(a_M+b_M)g of row M enters the elimination at one point of one thread.
+  // BCL (M a multiple of P): row M is the last point of its thread, and bcg is passed as 0 to every
+  // other thread, so the term is one add at point P−1 (no per-point compare and select); else
+  // the general point test.
+  template <bool BCL>
+  __device__ __forceinline__ static double bc_add(int i, double x, int bc_i, double bcg) {
+    if (BCL) return i == P - 1 ? x + bcg : x;
+    return i == bc_i ? x + bcg : x;
+  }
   // ↓↓: x (LU substitution of the previous step) and w̃ (UL elimination of this step, bc at bc_i)
+  template <bool BCL>
   __device__ __forceinline__ void pass_down2(double (&v)[P], int bc_i, double bcg, double *sh) const {
     double x = 0.0, z = 0.0;
 #pragma unroll
     for (int i = P - 1; i >= 0; --i) {
       x = fma(ncu[i], x, v[i]);
-      z = fma(nmu[i], z, iq[i] * (i == bc_i ? x + bcg : x));
+      z = fma(nmu[i], z, iq[i] * bc_add<BCL>(i, x, bc_i, bcg));
     }
     double e1, e2;
     enter<false>(x, z, sh, e1, e2);
@@ -413,17 +423,18 @@ struct Tri<P, NT, false, true> {
 #pragma unroll
     for (int i = P - 1; i >= 0; --i) {
       x = fma(ncu[i], x, v[i]);
-      z = fma(nmu[i], z, iq[i] * (i == bc_i ? x + bcg : x));
+      z = fma(nmu[i], z, iq[i] * bc_add<BCL>(i, x, bc_i, bcg));
       v[i] = z;
     }
   }
   // ↑↑: x (UL substitution of the previous step) and w (LU elimination of this step)
+  template <bool BCL>
   __device__ __forceinline__ void pass_up2(double (&v)[P], int bc_i, double bcg, double *sh) const {
     double x = 0.0, z = 0.0;
 #pragma unroll
     for (int i = 0; i < P; ++i) {
       x = fma(ncl[i], x, v[i]);
-      z = fma(nml[i], z, ip[i] * (i == bc_i ? x + bcg : x));
+      z = fma(nml[i], z, ip[i] * bc_add<BCL>(i, x, bc_i, bcg));
     }
     double e1, e2;
     enter<true>(x, z, sh, e1, e2);
@@ -431,21 +442,22 @@ struct Tri<P, NT, false, true> {
 #pragma unroll
     for (int i = 0; i < P; ++i) {
       x = fma(ncl[i], x, v[i]);
-      z = fma(nml[i], z, ip[i] * (i == bc_i ? x + bcg : x));
+      z = fma(nml[i], z, ip[i] * bc_add<BCL>(i, x, bc_i, bcg));
       v[i] = z;
     }
   }
   // lone LU elimination ↑ (first step of a slice): w_j = ip_j (x_j + bc_j) + nml_j w_{j−1}
+  template <bool BCL>
   __device__ __forceinline__ void pass_up_elim(double (&v)[P], int bc_i, double bcg, double *sh) const {
     double z = 0.0;
 #pragma unroll
-    for (int i = 0; i < P; ++i) z = fma(nml[i], z, ip[i] * (i == bc_i ? v[i] + bcg : v[i]));
+    for (int i = 0; i < P; ++i) z = fma(nml[i], z, ip[i] * bc_add<BCL>(i, v[i], bc_i, bcg));
     double e1, e2;
     enter<true>(0.0, z, sh, e1, e2);  // first component 0: the (2,2) entries carry the scan
     z = e2;
 #pragma unroll
     for (int i = 0; i < P; ++i) {
-      z = fma(nml[i], z, ip[i] * (i == bc_i ? v[i] + bcg : v[i]));
+      z = fma(nml[i], z, ip[i] * bc_add<BCL>(i, v[i], bc_i, bcg));
       v[i] = z;
     }
   }
@@ -472,10 +484,11 @@ struct Tri<P, NT, false, true> {
     }
   }
   // implicit step m of the slice (its elimination merged with the substitution of step m−1)
+  template <bool BCL = false>
   __device__ __forceinline__ void zz_step(int m, double (&v)[P], int bc_i, double bcg, double *sh) const {
-    if (m == 0) pass_up_elim(v, bc_i, bcg, sh);
-    else if (m & 1) pass_down2(v, bc_i, bcg, sh);
-    else pass_up2(v, bc_i, bcg, sh);
+    if (m == 0) pass_up_elim<BCL>(v, bc_i, bcg, sh);
+    else if (m & 1) pass_down2<BCL>(v, bc_i, bcg, sh);
+    else pass_up2<BCL>(v, bc_i, bcg, sh);
   }
   // after the last step n−1: its substitution (LU ↓ when n−1 is even, UL ↑ when odd)
   __device__ __forceinline__ void zz_finish(int n, double (&v)[P], double *sh) const {
@@ -513,6 +526,7 @@ __device__ __forceinline__ void run_steps(Tri<P, NT, CN, ZZ> &tri, const Residen
                                           int t, double (&x)[P], double *sh, double *bct) {
   const int bc_t = (a.M - 1) / P, bc_ip = (a.M - 1) % P;
   const int bc_i = (t == bc_t) ? bc_ip : -1;
+  const bool bcl = bc_ip == P - 1;  // M a multiple of P (C1, C2, C4)
   const double coef = a.bcoef[b];
   const double tau0 = n * a.dT;
 #pragma unroll 1
@@ -530,7 +544,11 @@ __device__ __forceinline__ void run_steps(Tri<P, NT, CN, ZZ> &tri, const Residen
     const int mend = min(a.steps - m0, kBcChunk);
 #pragma unroll 1
     if constexpr (ZZ) {
-      for (int mm = 0; mm < mend; ++mm) tri.zz_step(m0 + mm, x, bc_i, bc_i >= 0 ? bct[mm] : 0.0, sh);
+      if (bcl) {  // row M is the last point of thread bc_t: bcg is 0 for every other thread
+        for (int mm = 0; mm < mend; ++mm) tri.template zz_step<true>(m0 + mm, x, bc_i, bc_i >= 0 ? bct[mm] : 0.0, sh);
+      } else {
+        for (int mm = 0; mm < mend; ++mm) tri.zz_step(m0 + mm, x, bc_i, bc_i >= 0 ? bct[mm] : 0.0, sh);
+      }
     } else {
       for (int mm = 0; mm < mend; ++mm) tri.step(x, bc_i, bc_i >= 0 ? bct[mm] : 0.0, sh);
     }
