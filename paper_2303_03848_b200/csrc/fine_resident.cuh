@@ -203,11 +203,17 @@ struct Tri {
     }
   }
 
+  // BCL: row M is the thread's last point and bcg is 0 on every other thread (run_steps)
+  template <bool BCL = false>
   __device__ __forceinline__ void step(double (&x)[P], int bc_i, double bcg, double *sh) {
     if (CN) explicit_part(x, sh);
+    if (BCL) {
+      x[P - 1] += bcg;
+    } else {
 #pragma unroll
-    for (int i = 0; i < P; ++i)
-      if (i == bc_i) x[i] += bcg;
+      for (int i = 0; i < P; ++i)
+        if (i == bc_i) x[i] += bcg;
+    }
     // ---- forward elimination y_j = r_j − m_j y_{j−1}
 #pragma unroll
     for (int i = 1; i < P; ++i) x[i] = fma(nm[i], x[i - 1], x[i]);
@@ -550,7 +556,11 @@ __device__ __forceinline__ void run_steps(Tri<P, NT, CN, ZZ> &tri, const Residen
         for (int mm = 0; mm < mend; ++mm) tri.zz_step(m0 + mm, x, bc_i, bc_i >= 0 ? bct[mm] : 0.0, sh);
       }
     } else {
-      for (int mm = 0; mm < mend; ++mm) tri.step(x, bc_i, bc_i >= 0 ? bct[mm] : 0.0, sh);
+      if (bcl) {
+        for (int mm = 0; mm < mend; ++mm) tri.template step<true>(x, bc_i, bc_i >= 0 ? bct[mm] : 0.0, sh);
+      } else {
+        for (int mm = 0; mm < mend; ++mm) tri.step(x, bc_i, bc_i >= 0 ? bct[mm] : 0.0, sh);
+      }
     }
   }
   if constexpr (ZZ) tri.zz_finish(a.steps, x, sh);
