@@ -86,8 +86,16 @@ __global__ void __launch_bounds__(kGT, 1) k_fine_grid(GridArgs a) {
   double *sE = swt + 2 * kGW * NS * 2;                 // [NS][2] CTA entering state
   double *sT = sE + NS * 2;                            // [NS][2] CTA total of the pass
   double *sred = sT + NS * 2;                          // [32][2] look-back partial sums (warp 0)
-  double *sC = sred + 64;                              // [2][5][3][kGT] level coefficients
-  double *sX = sC + 2 * 5 * 3 * kGT;                   // [2][3][kGT] exclusive maps
+  // NS = 3 (PT = 28): two systems in registers, the third in shared memory (fp64, point-major);
+  // the room is the per-lane level coefficients', which are then recomputed in every scan from
+  // the thread's constant chunk maps (sA) — the same operations in the same order as at setup
+  constexpr int NSM = NS == 3 ? 1 : 0;  // systems whose state lives in shared memory
+  constexpr int NR = NS - NSM;          // systems whose state lives in registers
+  constexpr bool LVL = NSM > 0;         // level coefficients recomputed per scan
+  double *sC = sred + 64;                              // [2][5][3][kGT] level coefficients (!LVL)
+  double *sA = sC;                                     // [2][3][kGT] thread chunk maps (LVL)
+  double *sxm = sA + 2 * 3 * kGT;                      // [NSM][PT][kGT] state of the smem systems (LVL)
+  double *sX = LVL ? sxm + NSM * PT * kGT : sC + 2 * 5 * 3 * kGT;  // [2][3][kGT] exclusive maps
   double *sxs = sX + 2 * 3 * kGT;                      // [NS][2][kGT] lanes' exclusive warp prefixes
   double *sbc = sxs + NS * 2 * kGT;                    // [NS][steps] boundary terms
   GridSolver<PT, NS> g;
@@ -99,6 +107,13 @@ __global__ void __launch_bounds__(kGT, 1) k_fine_grid(GridArgs a) {
   g.c = blockIdx.x;
   g.j0 = (g.c * kGT + g.t) * PT;
   const int nCTA = gridDim.x;
+  // state of system k at the thread's point i (registers for k < NR, else shared memory)
+#define PR_XR(k, i) ((k) < NR ? (double)x[(k) < NR ? (k) : 0][i] : sxm[(((k) - NR) * PT + (i)) * kGT + t])
+#define PR_XW(k, i, v)                                          \
+  do {                                                          \
+    if ((k) < NR) x[(k) < NR ? (k) : 0][i] = (St)(v);           \
+    else sxm[(((k) - NR) * PT + (i)) * kGT + t] = (v);          \
+  } while (0)
   const int t = g.t, lane = g.lane, w = g.w, c = g.c;
   for (int i = t; i < kGT * PT; i += kGT) {
     const int j = c * kGT * PT + i;
@@ -133,6 +148,7 @@ __global__ void __launch_bounds__(kGT, 1) k_fine_grid(GridArgs a) {
     for (int dir = 0; dir < 2; ++dir) {
       const bool up = dir == 0;
       double m11 = m[dir][0], m21 = m[dir][1], m22 = m[dir][2];
+      if (LVL) sA[(dir * 3) * kGT + t] = m11, sA[(dir * 3 + 1) * kGT + t] = m21, sA[(dir * 3 + 2) * kGT + t] = m22;
 #pragma unroll
       for (int l = 0; l < 5; ++l) {
         const int d = 1 << l;
@@ -140,9 +156,11 @@ __global__ void __launch_bounds__(kGT, 1) k_fine_grid(GridArgs a) {
         const double p21 = up ? __shfl_up_sync(kFull, m21, d) : __shfl_down_sync(kFull, m21, d);
         const double p22 = up ? __shfl_up_sync(kFull, m22, d) : __shfl_down_sync(kFull, m22, d);
         const bool has = up ? lane >= d : lane + d <= 31;
-        g.C(dir, l, 0) = has ? m11 : 0.0;
-        g.C(dir, l, 1) = has ? m21 : 0.0;
-        g.C(dir, l, 2) = has ? m22 : 0.0;
+        if (!LVL) {
+          g.C(dir, l, 0) = has ? m11 : 0.0;
+          g.C(dir, l, 1) = has ? m21 : 0.0;
+          g.C(dir, l, 2) = has ? m22 : 0.0;
+        }
         if (has) {
           m21 = fma(m21, p11, m22 * p21);
           m11 *= p11;
@@ -174,7 +192,7 @@ __global__ void __launch_bounds__(kGT, 1) k_fine_grid(GridArgs a) {
   const double J0 = (double)(g.j0 + 1);
   for (int grp = 0; grp < ngroups; ++grp) {
     // ---- inputs and boundary terms of the NS systems (slices ln0 + grp·NS + k)
-    St x[NS][PT];
+    St x[NR][PT];
 #pragma unroll
     for (int k = 0; k < NS; ++k) {
       const int s = grp * NS + k;
@@ -182,7 +200,7 @@ __global__ void __launch_bounds__(kGT, 1) k_fine_grid(GridArgs a) {
 #pragma unroll
       for (int i = 0; i < PT; ++i) {
         const int j = g.j0 + i;
-        x[k][i] = (u && j < a.M) ? (St)u[j] : (St)0;
+        PR_XW(k, i, (u && j < a.M) ? (double)u[j] : 0.0);
       }
     }
     for (int q = t; q < NS * a.steps; q += kGT) {
@@ -222,7 +240,7 @@ __global__ void __launch_bounds__(kGT, 1) k_fine_grid(GridArgs a) {
         g.mults(a, sip, siq, i, ip, iq, l, u);
 #pragma unroll
         for (int k = 0; k < NS; ++k) {
-          const double v = (double)x[k][i];
+          const double v = PR_XR(k, i);
           double xn, zn = 0.0;
           if (up) {  // x: UL forward substitution (ncl = −l·iq); z: LU elimination (nml = −l·ip)
             xn = subst ? fma(-l * iq, xs[k], v) : v;
@@ -235,7 +253,7 @@ __global__ void __launch_bounds__(kGT, 1) k_fine_grid(GridArgs a) {
           }
           if (subst) xs[k] = xn;
           if (elim) zs[k] = zn;
-          if (write) x[k][i] = (St)(elim ? zn : xn);
+          if (write) PR_XW(k, i, elim ? zn : xn);
         }
       };
       // interior point (every point of the thread strictly inside 1 … M−2, no boundary term):
@@ -247,13 +265,13 @@ __global__ void __launch_bounds__(kGT, 1) k_fine_grid(GridArgs a) {
         const double mx = nl * (up ? iq : ip), mz = nl * (up ? ip : iq), fz = up ? ip : iq;
 #pragma unroll
         for (int k = 0; k < NS; ++k) {
-          const double xv = (double)x[k][i];
+          const double xv = PR_XR(k, i);
           const double xn = subst ? fma(mx, xs[k], xv) : xv;
           double zn = 0.0;
           if (elim) zn = fma(mz, zs[k], fz * xn);
           if (subst) xs[k] = xn;
           if (elim) zs[k] = zn;
-          if (write) x[k][i] = (St)(elim ? zn : xn);
+          if (write) PR_XW(k, i, elim ? zn : xn);
         }
       };
       auto run = [&](double(&xs)[NS], double(&zs)[NS], bool write) {
@@ -292,7 +310,7 @@ __global__ void __launch_bounds__(kGT, 1) k_fine_grid(GridArgs a) {
           const double cz = nl * fprev;  // (ii = 0: the entering state is zero, cz unused)
 #pragma unroll
           for (int k = 0; k < NS; ++k) {
-            const double xv = (double)x[k][i];
+            const double xv = PR_XR(k, i);
             if (ii == 0) {
               s1[k] = xv;
               s2[k] = xv;
@@ -308,11 +326,28 @@ __global__ void __launch_bounds__(kGT, 1) k_fine_grid(GridArgs a) {
       } else {
         run(s1, s2, false);
       }
-      // (2) warp scan of the NS 2-vectors with the precomputed level coefficients
+      // (2) warp scan of the NS 2-vectors with the level coefficients (precomputed, or recomputed
+      //     alongside from the chunk maps when LVL)
+      double lm11 = 0.0, lm21 = 0.0, lm22 = 0.0;  // LVL: the lane's composite chunk map so far
+      if (LVL) lm11 = sA[(dir * 3) * kGT + t], lm21 = sA[(dir * 3 + 1) * kGT + t], lm22 = sA[(dir * 3 + 2) * kGT + t];
 #pragma unroll
       for (int l = 0; l < 5; ++l) {
         const int d = 1 << l;
-        const double C0 = g.C(dir, l, 0), C1 = g.C(dir, l, 1), C2 = g.C(dir, l, 2);
+        double C0, C1, C2;
+        if (LVL) {  // the setup's level recurrence (bitwise the same coefficients)
+          const bool has = up ? lane >= d : lane + d <= 31;
+          C0 = has ? lm11 : 0.0, C1 = has ? lm21 : 0.0, C2 = has ? lm22 : 0.0;
+          const double p11 = up ? __shfl_up_sync(kFull, lm11, d) : __shfl_down_sync(kFull, lm11, d);
+          const double p21 = up ? __shfl_up_sync(kFull, lm21, d) : __shfl_down_sync(kFull, lm21, d);
+          const double p22 = up ? __shfl_up_sync(kFull, lm22, d) : __shfl_down_sync(kFull, lm22, d);
+          if (has) {
+            lm21 = fma(lm21, p11, lm22 * p21);
+            lm11 *= p11;
+            lm22 *= p22;
+          }
+        } else {
+          C0 = g.C(dir, l, 0), C1 = g.C(dir, l, 1), C2 = g.C(dir, l, 2);
+        }
 #pragma unroll
         for (int k = 0; k < NS; ++k) {
           const double q1 = up ? __shfl_up_sync(kFull, s1[k], d) : __shfl_down_sync(kFull, s1[k], d);
@@ -485,11 +520,13 @@ __global__ void __launch_bounds__(kGT, 1) k_fine_grid(GridArgs a) {
 #pragma unroll
       for (int i = 0; i < PT; ++i) {
         const int j = g.j0 + i;
-        if (j < a.M) dst[j] = gh ? (float)((double)x[k][i] - (double)gh[j]) : (float)x[k][i];
+        if (j < a.M) dst[j] = gh ? (float)(PR_XR(k, i) - (double)gh[j]) : (float)PR_XR(k, i);
       }
     }
     __syncthreads();  // sbc is rewritten by the next group
   }
+#undef PR_XR
+#undef PR_XW
 }
 
 namespace {
@@ -500,9 +537,10 @@ using GridKernel = void (*)(GridArgs);
 // systems (a group computes all NS systems whether used or not).  Measured: 3 systems at PT = 28
 // (fp64 with 52 B of spills, or fp32 storage — the F2F conversions per point and pass) were
 // slower per system than 2.
-constexpr int ns_max(int PT) { return PT >= 28 ? 2 : PT >= 16 ? 4 : 8; }
+constexpr int ns_max(int PT) { return PT >= 28 ? 3 : PT >= 16 ? 4 : 8; }
 int ns_pick(int PT, int nsys) {
   const int mx = ns_max(PT);
+  if (mx == 3) return nsys <= 2 ? 2 : 3;
   return nsys <= 2 ? 2 : (nsys <= 4 || mx == 4) ? std::min(4, mx) : mx;
 }
 GridKernel grid_kernel(int PT, int NS) {
@@ -516,6 +554,7 @@ GridKernel grid_kernel(int PT, int NS) {
     case 16 * 16 + 2: return k_fine_grid<16, 2, double>;
     case 16 * 16 + 4: return k_fine_grid<16, 4, double>;
     case 28 * 16 + 2: return k_fine_grid<28, 2, double>;
+    case 28 * 16 + 3: return k_fine_grid<28, 3, double>;
   }
   return nullptr;
 }
@@ -525,7 +564,8 @@ constexpr int kPTs[] = {4, 8, 16, 28};
 int fine_grid_ns(int PT, int nsys) { return ns_pick(PT, nsys); }
 size_t fine_grid_smem(int PT, int steps) {  // at the largest NS of PT (every launch fits)
   const int NS = ns_max(PT);
-  return ((size_t)2 * kGT * PT + 2 * kGW * 3 + 2 * kGW * NS * 2 + NS * 4 + 64 + (size_t)(30 + 6 + NS * 2) * kGT +
+  const size_t lvl = NS == 3 ? (size_t)(6 + PT) : 30;  // chunk maps + smem state (NS = 3), else level coefficients
+  return ((size_t)2 * kGT * PT + 2 * kGW * 3 + 2 * kGW * NS * 2 + NS * 4 + 64 + (lvl + 6 + NS * 2) * kGT +
           (size_t)NS * steps) *
          sizeof(double);
 }
