@@ -334,7 +334,8 @@ def c3_fine_sweep_roofline(parareal, synth, torch, stream, pk, pk_src, flush):
         finally:
             ctx.close()
 
-    t = sweep_ms(0) / 1e3          # auto: the grid-resident K2R at this size
+    with Clocks(torch.cuda.current_device()) as clk:
+        t = sweep_ms(0) / 1e3      # auto: the grid-resident K2R at this size
     t_k2 = sweep_ms(2) / 1e3       # K2 forced
     pt_steps = float(p.M) * p.N * p.fine_steps
     ach = 8.0 * pt_steps / t / 1e9
@@ -347,6 +348,7 @@ def c3_fine_sweep_roofline(parareal, synth, torch, stream, pk, pk_src, flush):
            "point_steps_per_s": pt_steps / t,
            "work_per_unit": "8 B per point-step (SURVEY 8(d) algorithmic, single-pass design); K2R keeps the "
                             "state on chip, so this is the HBM-equivalent rate",
+           "clocks": clk.summary(),
            "traffic": tr["dram_bytes_per_launch"] if tr else None,
            "traffic_unit": "bytes per sweep launch (ncu dram read+write; the whole sweep is one launch)",
            "k2": {"kernel": "k_pass_res2 (K2, persistent paired streamed pass)", "ms_per_sweep": t_k2 * 1e3,
