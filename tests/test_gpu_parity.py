@@ -231,6 +231,26 @@ def test_pinn_tensor_core_parareal_chain(prec, dims, tol):
     assert_close(it, ref_U, tol=tol, what="TC Parareal iterates (precision %d)" % prec)
 
 
+@pytest.mark.parametrize("W,LH", [(64, 4), (128, 3), (256, 2)])
+def test_pinn_tensor_core_two_input_nets(W, LH):
+    """2-input (t_to, S) networks -- the form the GPU trainer produces (reading Q28) and the C5
+    study runs on the split-fp16 tensor-core chain (profiles/r02/c5_study.md): one G application
+    (ragged last tile) and a K = 2 Parareal solve against the oracle at the TC tolerance."""
+    net = synth.kaiming_net([2] + [W] * LH + [1], seed=7 * W + LH)
+    p = synth.single(1000, 6, coarse=synth.COARSE_PINN, max_iter=2, tol=0.0)
+    U = oracle.payoff(p) * (1.0 + 0.05 * np.sin(np.arange(1000) / 23.0))
+    with ctx_for(p) as c:
+        c.load_weights(net, precision=parareal.PREC_FP16_TC)
+        got = c.apply_coarse(4, U.astype(np.float32))
+        _, rep = c.solve()
+        it = c.copy_iterates(0, p.N + 1)
+    assert_close(got, oracle.pinn_G(p, net, 4, U), tol=TOL_TC, what="2-input G TC W=%d LH=%d" % (W, LH))
+    ref_U, ref_d, K, _ = oracle.parareal(p, net)
+    assert rep["iterations"] == K == 2
+    assert_close(it, ref_U, tol=TOL_TC, what="2-input TC Parareal W=%d LH=%d" % (W, LH))
+    assert_delta(rep["delta"], ref_d)
+
+
 def test_pinn_tensor_core_errors():
     p = synth.single(256, 4)
     with ctx_for(p) as c:
