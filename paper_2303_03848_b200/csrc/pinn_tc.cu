@@ -118,8 +118,12 @@ __device__ __forceinline__ float act_tc(float zs) {
 // fp32-level accuracy (~2e-6 on 8×256 nets) at 3× the MMAs.  !SPLIT (PR_PREC_BF16_TC): one bf16 pass.
 // H16 (with !SPLIT, PR_PREC_FP16X1_TC): one fp16 pass — fp16's 2^-11 unit roundoff is 8x finer than
 // bf16's for the [-1,1] activations and O(1) weights, at bf16's speed (exact tanh in the epilogue).
-template <int IN, int W, int ACT, bool SPLIT, bool H16>
-__global__ void __launch_bounds__(128) k_pinn_chain_tc(PinnTcArgs ta) {
+// NT = 256: two threads per row of the tile (thread t: row t & 127, columns of half t >> 7), so
+// the epilogue (TMEM loads, bias, tanh, operand stores) has two warps per sub-partition instead of
+// one; the per-point chain state and outputs stay with the first half, the output layer's two
+// column halves are added in a fixed order.
+template <int IN, int W, int ACT, bool SPLIT, bool H16, int NT = 128>
+__global__ void __launch_bounds__(NT) k_pinn_chain_tc(PinnTcArgs ta) {
   using T = typename std::conditional<SPLIT || H16, __half, __nv_bfloat16>::type;
   constexpr int TILE = 128;
   constexpr int NP = SPLIT ? 2 : 1;                         // hi (+ lo) planes
@@ -128,6 +132,8 @@ __global__ void __launch_bounds__(128) k_pinn_chain_tc(PinnTcArgs ta) {
   constexpr uint32_t kPlaneB = (uint32_t)W * kTcKC * 2;      // bytes of one chunk plane
   constexpr uint32_t kChunk = NP * kPlaneB;
   constexpr int NCH = W / kTcKC;                             // chunks per layer
+  constexpr int HALVES = NT / 128, WH = W / HALVES;           // column halves per row
+  static_assert(WH >= 32 && WH % 32 == 0, "a half holds whole 32-column TMEM loads");
   const PinnArgs &a = ta.g;
   extern __shared__ __align__(128) unsigned char tc_smem[];
   T *sA = reinterpret_cast<T *>(tc_smem);                    // NP planes [128 × W]
@@ -137,7 +143,8 @@ __global__ void __launch_bounds__(128) k_pinn_chain_tc(PinnTcArgs ta) {
   __shared__ __align__(8) uint64_t bar_mma, bar_w, bar_full[2], bar_free[2];
   __shared__ uint32_t s_tmem;
   __shared__ double red[64];
-  const int t = threadIdx.x, w = t >> 5;
+  __shared__ float s_y[HALVES > 1 ? 128 : 1], s_u[HALVES > 1 ? 128 : 1];
+  const int t = threadIdx.x, w = t >> 5, r = t & 127, hh = t >> 7, col0 = hh * WH;
   for (int i = t; i < a.nfloats; i += blockDim.x) sP[i] = a.wts[i];
   if (t == 0) {
     tc_mbar_init(&bar_mma);
@@ -157,7 +164,7 @@ __global__ void __launch_bounds__(128) k_pinn_chain_tc(PinnTcArgs ta) {
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = s_tmem;
-  const uint32_t tlane = tmem + ((uint32_t)(32 * w) << 16);  // this warp's TMEM lane quarter
+  const uint32_t tlane = tmem + ((uint32_t)(32 * (w & 3)) << 16);  // this warp's TMEM lane quarter
   uint32_t ph_mma = 0, ph_w = 0;
   if (ta.resident && a.LH > 1) {  // every chunk loaded once (≤ 200 KB, one bulk copy)
     if (t == 0) tc_bulk_g2s(sB, ta.wh, (uint32_t)((a.LH - 1) * NCH) * kChunk, &bar_w);
@@ -179,7 +186,7 @@ __global__ void __launch_bounds__(128) k_pinn_chain_tc(PinnTcArgs ta) {
   const float bo = Wo[W];
   // store 8 consecutive activations (fp32) of column block c0 as the A operand (hi, lo)
   auto store_a = [&](int c0, const float (&h)[8]) {
-    const size_t off = cm_offset(t, c0, W);
+    const size_t off = cm_offset(r, c0, W);
     float lo[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
@@ -198,7 +205,7 @@ __global__ void __launch_bounds__(128) k_pinn_chain_tc(PinnTcArgs ta) {
   const float gscale = (float)(Lb * (double)a.out_scale);
   const float invL = (float)(1.0 / Lb);
   const size_t sstride = (size_t)a.B * a.Mp;
-  const int j = (blockIdx.x + a.cta0) * TILE + t;
+  const int j = (blockIdx.x + a.cta0) * TILE + r;
   const bool ok = j < a.M;
   const double dS = Lb / (a.M + 1);
   const float s_over_L = (float)(((j + 1) * dS) / Lb);
@@ -209,12 +216,14 @@ __global__ void __launch_bounds__(128) k_pinn_chain_tc(PinnTcArgs ta) {
     double num = 0.0, den = 0.0;
     if (ok) {
       u = f[j];
-      const double dd = (double)u - (double)u0[j];
-      num = dd * dd;
-      den = (double)u * u;
+      if (hh == 0) {
+        const double dd = (double)u - (double)u0[j];
+        num = dd * dd;
+        den = (double)u * u;
+      }
     }
     __syncthreads();
-    if (ok) u0[j] = u;
+    if (ok && hh == 0) u0[j] = u;
     if (a.partials) {
       cta_reduce2(num, den, red);
       if (t == 0) {
@@ -244,7 +253,7 @@ __global__ void __launch_bounds__(128) k_pinn_chain_tc(PinnTcArgs ta) {
     }
     // ---- layer 0 (fp32) → A operand
 #pragma unroll 1
-    for (int c0 = 0; c0 < W; c0 += 8) {
+    for (int c0 = col0; c0 < col0 + WH; c0 += 8) {
       float h[8];
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
@@ -316,7 +325,7 @@ __global__ void __launch_bounds__(128) k_pinn_chain_tc(PinnTcArgs ta) {
       const float *bl = sP + W * IN + W + (size_t)(l - 1) * W;
       const bool last = l == a.LH - 1;
 #pragma unroll 1
-      for (int c0 = 0; c0 < W; c0 += 32) {
+      for (int c0 = col0; c0 < col0 + WH; c0 += 32) {
         float v[32];
         tmem_ld32(tlane + (uint32_t)c0, v);
 #pragma unroll
@@ -336,16 +345,21 @@ __global__ void __launch_bounds__(128) k_pinn_chain_tc(PinnTcArgs ta) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncthreads();
     }
+    if (HALVES > 1) {  // the output layer's column halves, added in a fixed order
+      if (hh == 1) s_y[r] = y;
+      __syncthreads();
+      if (hh == 0) y += s_y[r];
+    }
     y += bo;
     const float g = gscale * y;
     if (a.Gout) {
-      if (ok) a.Gout[(size_t)b * a.Mp + j] = g;
+      if (ok && hh == 0) a.Gout[(size_t)b * a.Mp + j] = g;
       break;
     }
     const size_t row = (size_t)ln * sstride + (size_t)b * a.Mp;
     float nv = 0.f;
     double num = 0.0, den = 0.0;
-    if (ok) {
+    if (ok && hh == 0) {
       nv = a.D ? g + a.D[row + j] : g;
       if (a.Gh) a.Gh[row + j] = g;
       if (a.partials) {
@@ -354,6 +368,11 @@ __global__ void __launch_bounds__(128) k_pinn_chain_tc(PinnTcArgs ta) {
         den = (double)nv * nv;
       }
       a.U[row + sstride + j] = nv;
+    }
+    if (HALVES > 1) {  // the next slice's feature U_{n+1} for the second half
+      if (hh == 0) s_u[r] = nv;
+      __syncthreads();
+      nv = s_u[r];
     }
     u = nv;
     if (a.partials) {
@@ -688,20 +707,27 @@ __global__ void __launch_bounds__(288, 1) k_pinn_chain_tc2(PinnTcArgs ta) {
 
 typedef void (*TcKernel)(PinnTcArgs);
 template <bool SPLIT, bool H16>
-static TcKernel tc_kernel_t(int IN, int W, int act) {
+static TcKernel tc_kernel_t(int IN, int W, int act, bool wide) {
   if (act != 0 && act != 1) return nullptr;
-#define PR_TC_CASE(IN_, W_)                                                       \
-  if (IN == IN_ && W == W_)                                                       \
-    return act ? k_pinn_chain_tc<IN_, W_, 1, SPLIT, H16> : k_pinn_chain_tc<IN_, W_, 0, SPLIT, H16>;
+#define PR_TC_CASE(IN_, W_)                                                                        \
+  if (IN == IN_ && W == W_)                                                                        \
+    return wide ? (act ? k_pinn_chain_tc<IN_, W_, 1, SPLIT, H16, 256> : k_pinn_chain_tc<IN_, W_, 0, SPLIT, H16, 256>) \
+                : (act ? k_pinn_chain_tc<IN_, W_, 1, SPLIT, H16> : k_pinn_chain_tc<IN_, W_, 0, SPLIT, H16>);
   PR_TC_CASE(4, 64) PR_TC_CASE(4, 128) PR_TC_CASE(4, 256) PR_TC_CASE(2, 64) PR_TC_CASE(2, 128) PR_TC_CASE(2, 256)
 #undef PR_TC_CASE
   return nullptr;
 }
 // mode: kTcSplit16 (hi + lo fp16, 3 MMAs), kTcBF16 (one bf16 pass), kTcF16 (one fp16 pass)
+// one-tile kernel width: 256 threads (two per tile row) unless PR_TC_WIDE=0 (A/B)
+static bool tc_wide() {
+  static const int v = getenv("PR_TC_WIDE") ? atoi(getenv("PR_TC_WIDE")) : 1;
+  return v != 0;
+}
 static TcKernel tc_kernel(int IN, int W, int act, int mode) {
-  return mode == kTcSplit16 ? tc_kernel_t<true, true>(IN, W, act)
-         : mode == kTcBF16  ? tc_kernel_t<false, false>(IN, W, act)
-                            : tc_kernel_t<false, true>(IN, W, act);
+  const bool wide = tc_wide();
+  return mode == kTcSplit16 ? tc_kernel_t<true, true>(IN, W, act, wide)
+         : mode == kTcBF16  ? tc_kernel_t<false, false>(IN, W, act, wide)
+                            : tc_kernel_t<false, true>(IN, W, act, wide);
 }
 
 bool pinn_tc_supported(int IN, int W, int act, int mode) { return tc_kernel(IN, W, act, mode) != nullptr; }
@@ -829,7 +855,7 @@ cudaError_t launch_pinn_tc(int IN, int W, int act, int mode, const PinnArgs &a, 
   ta.g = a;
   ta.wh = wh;
   ta.resident = resident ? 1 : 0;
-  k<<<grid, 128, smem, s>>>(ta);
+  k<<<grid, tc_wide() ? 256 : 128, smem, s>>>(ta);
   return cudaGetLastError();
 }
 
