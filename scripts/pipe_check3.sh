@@ -1,4 +1,4 @@
-# tagged-word PINN pipe: pipelined/headline/graph/determinism tests, the trace, a short bench
+# pipelined schedule: pipelined/headline/graph/determinism tests, the trace, a short bench
 O=gpurun_out/pipe3; mkdir -p $O
 timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -k "pipelined or headline or graph or determinism or pinn_fixed or k1_c2 or finite or device_entry or co_resident" 2>&1 | tail -5 > $O/pytest.txt; cat $O/pytest.txt
 timeout 120 python scripts/pipe_trace.py > $O/pipe_trace.txt 2>&1; head -12 $O/pipe_trace.txt
