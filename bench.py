@@ -279,13 +279,15 @@ def roofline(p, ph, K, world, rank, pk, pk_src, clk_mhz, n_sm, synth, dims=None,
         chain_s = ph["ms_coarse"] / (K + 1) / 1e3
         if p.coarse == synth.COARSE_PINN and tc_prec:
             fl = pinn_flops(dims)
-            roof = {"kernel": "k_pinn_chain_tc (K4, tcgen05 %s)" % tc_prec, "bound": "tensor",
+            w = dims[1] if dims else 0
+            kname = ("k_pinn_chain_tc3" if tc_prec == "fp16tc" and w == 256 else "k_pinn_chain_tc")
+            roof = {"kernel": "%s (K4, tcgen05 %s)" % (kname, tc_prec), "bound": "tensor",
                     "achieved": fl * evals / chain_s / 1e12,
                     "peak": float(pk["bf16_tflops"]), "unit": "TFLOP/s",
                     "peak_source": "measured dense bf16 (fp16 runs at the bf16 rate)",
                     "work_per_unit": "%.0f algorithmic flop per point-eval (the split-fp16 mode issues 3x)" % fl,
                     "launch_unit": "one coarse chain"}
-            tr = ncu_traffic("k_pinn_chain_tc")
+            tr = ncu_traffic(kname + ("<" if kname == "k_pinn_chain_tc" else ""))
         elif p.coarse == synth.COARSE_PINN:
             fl = pinn_flops(dims)
             roof = {"kernel": "k_pinn_chain* (K3, fp32 SIMT)", "bound": "alu",

@@ -705,6 +705,322 @@ __global__ void __launch_bounds__(288, 1) k_pinn_chain_tc2(PinnTcArgs ta) {
   }
 }
 
+// ---------------------------------------------------------------- K4 layer-pipelined one-tile kernel
+// One 128-point tile per CTA and 288 threads: warpgroups 0 and 1 (threads 0-255) share the tile's
+// epilogue — thread t owns row t & 127 and the 32-column blocks c ≡ t >> 7 (mod 2) of every layer —
+// and warp 8's lane 0 issues every MMA and weight load.  The accumulators are double-buffered in
+// TMEM (2W columns: layer l in half l & 1), so the MMAs of layer l+1 start as soon as the epilogue of
+// layer l has written the first 64 columns of their A operand: per 64-column step st the epilogue
+// threads arrive on bar_a[st] and the issuer runs that step's two K-chunks.  The tensor pipe and the
+// epilogue's MUFU/FMA work overlap within one tile, where k_pinn_chain_tc serialises them (ncu: 56 %
+// of its stall samples wait for the layer's MMAs).  One bar_a per step: a thread arrives on each
+// once per layer, and its next arrival on the same barrier comes after bar_mma of the next layer,
+// i.e. after the issuer consumed the phase (no run-ahead across phases).  Same per-point arithmetic
+// as k_pinn_chain_tc except the K-chunk accumulation order, which is unchanged (chunks 0 … NCH−1).
+template <int IN, int W, int ACT, bool SPLIT, bool H16, int NB>
+__global__ void __launch_bounds__(288, 1) k_pinn_chain_tc3(PinnTcArgs ta) {
+  using T = typename std::conditional<H16 || SPLIT, __half, __nv_bfloat16>::type;
+  constexpr int TILE = 128;
+  constexpr int NP = SPLIT ? 2 : 1;
+  constexpr uint32_t kIdesc = umma_idesc<!(H16 || SPLIT)>(TILE, W);
+  constexpr uint32_t kPlaneA = (uint32_t)TILE * W * 2;
+  constexpr uint32_t kPlaneB = (uint32_t)W * kTcKC * 2;
+  constexpr uint32_t kChunk = NP * kPlaneB;
+  constexpr int NCH = W / kTcKC;   // K-chunks per layer
+  constexpr int NSTEP = W / 64;    // 64-column steps per layer (two K-chunks each)
+  static_assert(kTcKC == 32 && W % 64 == 0, "two 32-column K-chunks per step");
+  const PinnArgs &a = ta.g;
+  extern __shared__ __align__(128) unsigned char tc_smem[];
+  T *sA = reinterpret_cast<T *>(tc_smem);  // NP planes [128 × W]
+  unsigned char *sB = tc_smem + NP * kPlaneA;
+  const int nchunks = ta.resident ? (a.LH - 1) * NCH : NB;
+  float *sP = reinterpret_cast<float *>(sB + (size_t)nchunks * kChunk);
+  __shared__ __align__(8) uint64_t bar_mma, bar_a[NSTEP], bar_w, bar_full[NB], bar_free[NB];
+  __shared__ uint32_t s_tmem;
+  __shared__ double red[16];
+  __shared__ float s_y[128], s_u[128];
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  for (int i = t; i < a.nfloats; i += blockDim.x) sP[i] = a.wts[i];
+  if (t == 0) {
+    tc_mbar_init_n(&bar_mma, 1);
+    for (int i = 0; i < NSTEP; ++i) tc_mbar_init_n(&bar_a[i], 256);
+    for (int i = 0; i < NB; ++i) {
+      tc_mbar_init_n(&bar_full[i], 1);
+      tc_mbar_init_n(&bar_free[i], 1);
+    }
+    tc_mbar_init_n(&bar_w, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 8) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tc_smem_u32(&s_tmem)),
+                 "r"((uint32_t)(2 * W)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = s_tmem;
+  const int ln_end = a.Gout ? a.ln0 + 1 : a.ln1;
+  const int nslices = ln_end - a.ln0;
+
+  if (warp == 8) {  // ---------------- the issuer (lane 0 of warp 8)
+    if (lane == 0 && a.LH > 1) {
+      const uint32_t aHi = tc_smem_u32(sA), aLo = aHi + kPlaneA, bBase = tc_smem_u32(sB);
+      const int nseq = (a.LH - 1) * NCH;  // chunks of one pass over the hidden layers
+      auto load_chunk = [&](unsigned g) {
+        tc_bulk_g2s(sB + (size_t)(g % NB) * kChunk, (const unsigned char *)ta.wh + (size_t)(g % nseq) * kChunk,
+                    kChunk, &bar_full[g % NB]);
+      };
+      if (ta.resident) {
+        tc_bulk_g2s(sB, ta.wh, (uint32_t)((a.LH - 1) * NCH) * kChunk, &bar_w);
+        tc_mbar_wait(&bar_w, 0);
+      } else {
+        for (unsigned d = 0; d + 1 < (unsigned)NB; ++d) load_chunk(d);
+      }
+      unsigned g = 0;
+      uint32_t ph_a = 0;  // every bar_a[st] completes once per layer: one shared phase bit per layer
+#pragma unroll 1
+      for (int sl = 0; sl < nslices; ++sl) {
+#pragma unroll 1
+        for (int l = 1; l < a.LH; ++l) {
+          const uint32_t dl = tmem + (uint32_t)((l & 1) * W);  // layer l's accumulator half
+#pragma unroll 1
+          for (int st = 0; st < NSTEP; ++st) {
+            tc_mbar_wait(&bar_a[st], ph_a);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll 1
+            for (int cc = 0; cc < 2; ++cc) {
+              const int c = 2 * st + cc;
+              uint32_t bc;
+              if (ta.resident) {
+                bc = bBase + (uint32_t)((l - 1) * NCH + c) * kChunk;
+              } else {
+                tc_mbar_wait(&bar_full[g % NB], (g / NB) & 1);
+                bc = bBase + (g % NB) * kChunk;
+              }
+#pragma unroll
+              for (int ks = 0; ks < kTcKC / 16; ++ks) {
+                const uint32_t ao = (uint32_t)(c * (kTcKC / 8) + 2 * ks) * 128, bo2 = (uint32_t)(2 * ks) * 128;
+                const uint64_t dah = umma_desc(aHi + ao, 128, 16 * W), dbh = umma_desc(bc + bo2, 128, 16 * kTcKC);
+                const uint32_t acc = (c > 0 || ks > 0) ? 1u : 0u;
+                asm volatile(
+                    "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                    "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(dl),
+                    "l"(dah), "l"(dbh), "r"(kIdesc), "r"(acc));
+                if (SPLIT) {  // + A_hi·B_lo + A_lo·B_hi
+                  const uint64_t dbl = umma_desc(bc + kPlaneB + bo2, 128, 16 * kTcKC);
+                  const uint64_t dal = umma_desc(aLo + ao, 128, 16 * W);
+                  asm volatile(
+                      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(dl),
+                      "l"(dah), "l"(dbl), "r"(kIdesc), "r"(1u));
+                  asm volatile(
+                      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(dl),
+                      "l"(dal), "l"(dbh), "r"(kIdesc), "r"(1u));
+                }
+              }
+              if (!ta.resident) {
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                                 tc_smem_u32(&bar_free[g % NB]))
+                             : "memory");
+                // the buffer of chunk g−1 takes chunk g + NB − 1 once chunk g−1's MMAs completed
+                if (g >= 1) tc_mbar_wait(&bar_free[(g - 1) % NB], ((g - 1) / NB) & 1);
+                load_chunk(g + NB - 1);
+                ++g;
+              }
+            }
+          }
+          ph_a ^= 1;
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                           tc_smem_u32(&bar_mma))
+                       : "memory");
+        }
+      }
+      if (!ta.resident)  // the prefetches still in flight
+        for (unsigned q = g; q + 1 < g + (unsigned)NB; ++q) tc_mbar_wait(&bar_full[q % NB], (q / NB) & 1);
+    }
+    __syncwarp();
+  } else {  // ---------------- the epilogue: row r, column blocks of parity hh
+    const int r = t & 127, hh = t >> 7;
+    const uint32_t tlane = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
+    const float *W0 = sP, *b0 = sP + W * IN;
+    const float *Wo = sP + W * IN + W + (size_t)(a.LH - 1) * W;
+    const float bo = Wo[W];
+    auto store_a = [&](int c0, const float (&h)[8]) {
+      const size_t off = cm_offset(r, c0, W);
+      *reinterpret_cast<uint4 *>(sA + off) =
+          make_uint4(pack2<T>(h[0], h[1]), pack2<T>(h[2], h[3]), pack2<T>(h[4], h[5]), pack2<T>(h[6], h[7]));
+      if (SPLIT) {
+        float lo[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) lo[q] = h[q] - __half2float(__float2half_rn(h[q]));
+        *reinterpret_cast<uint4 *>(sA + (size_t)TILE * W + off) = make_uint4(
+            pack2<T>(lo[0], lo[1]), pack2<T>(lo[2], lo[3]), pack2<T>(lo[4], lo[5]), pack2<T>(lo[6], lo[7]));
+      }
+    };
+    // fixed-order sum of (num, den) over the 256 epilogue threads; valid in thread 0
+    auto reduce256 = [&](double &num, double &den) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        num += __shfl_xor_sync(0xffffffffu, num, o);
+        den += __shfl_xor_sync(0xffffffffu, den, o);
+      }
+      epi_sync();
+      if (lane == 0) { red[2 * warp] = num; red[2 * warp + 1] = den; }
+      epi_sync();
+      if (t == 0) {
+        num = 0.0; den = 0.0;
+        for (int q = 0; q < 8; ++q) { num += red[2 * q]; den += red[2 * q + 1]; }
+      }
+    };
+    const int b = blockIdx.y;
+    const double Lb = a.Lb[b];
+    const float gscale = (float)(Lb * (double)a.out_scale);
+    const float invL = (float)(1.0 / Lb);
+    const size_t sstride = (size_t)a.B * a.Mp;
+    const int j = (blockIdx.x + a.cta0) * TILE + r;
+    const bool ok = j < a.M;
+    const double dS = Lb / (a.M + 1);
+    const float s_over_L = (float)(((j + 1) * dS) / Lb);
+    float *u0 = a.U + (size_t)a.ln0 * sstride + (size_t)b * a.Mp;
+    float u = 0.f;
+    if (a.Fcopy) {
+      const float *f = a.Fcopy + (size_t)b * a.Mp;
+      double num = 0.0, den = 0.0;
+      if (ok) {
+        u = f[j];
+        if (hh == 0) {
+          const double dd = (double)u - (double)u0[j];
+          num = dd * dd;
+          den = (double)u * u;
+        }
+      }
+      epi_sync();
+      if (ok && hh == 0) u0[j] = u;
+      if (a.partials) {
+        reduce256(num, den);
+        if (t == 0) {
+          double *pp = a.partials + (((size_t)a.ln0 * a.B + b) * a.nch + blockIdx.x + a.cta0) * 2;
+          pp[0] = num;
+          pp[1] = den;
+        }
+      }
+    } else if (ok) {
+      u = u0[j];
+    }
+    uint32_t ph_m = 0;
+#pragma unroll 1
+    for (int ln = a.ln0; ln < ln_end; ++ln) {
+      const int n = a.n_base + ln;
+      const float tf = (float)((a.T - n * a.dT) / a.T), tt = (float)((a.T - (n + 1) * a.dT) / a.T);
+      float x[IN];
+      if (IN == 4) {
+        x[0] = tf * a.cs0;
+        x[1] = tt * a.cs1;
+        x[2] = (u * invL) * a.cs2;
+        x[3] = s_over_L * a.cs3;
+      } else {
+        x[0] = tt * a.cs0;
+        x[IN - 1] = s_over_L * a.cs1;
+      }
+      // layer 0 (fp32) → A, one 32-column block per step, then the step's arrival
+#pragma unroll 1
+      for (int st = 0; st < NSTEP; ++st) {
+        const int cb = (2 * st + hh) * 32;
+#pragma unroll 1
+        for (int c0 = cb; c0 < cb + 32; c0 += 8) {
+          float h[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            float z = b0[c0 + q];
+#pragma unroll
+            for (int i = 0; i < IN; ++i) z = fmaf(W0[(c0 + q) * IN + i], x[i], z);
+            h[q] = act<ACT>(z);
+          }
+          store_a(c0, h);
+        }
+        if (a.LH > 1) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          tc_mbar_arrive(&bar_a[st]);
+        }
+      }
+      float y = 0.f;
+#pragma unroll 1
+      for (int l = 1; l < a.LH; ++l) {
+        tc_mbar_wait(&bar_mma, ph_m);
+        ph_m ^= 1;
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const float *bl = sP + W * IN + W + (size_t)(l - 1) * W;
+        const bool last = l == a.LH - 1;
+        const uint32_t tl = tlane + (uint32_t)((l & 1) * W);
+#pragma unroll 1
+        for (int st = 0; st < NSTEP; ++st) {
+          const int c0 = (2 * st + hh) * 32;
+          float v[32];
+          tmem_ld32(tl + (uint32_t)c0, v);
+#pragma unroll
+          for (int q = 0; q < 32; ++q) v[q] = act_tc<ACT, !H16 && !SPLIT>(v[q] + bl[c0 + q]);
+          if (last) {
+#pragma unroll
+            for (int q = 0; q < 32; ++q) y = fmaf(Wo[c0 + q], v[q], y);
+          } else {
+#pragma unroll
+            for (int q = 0; q < 32; q += 8) {
+              const float h[8] = {v[q], v[q + 1], v[q + 2], v[q + 3], v[q + 4], v[q + 5], v[q + 6], v[q + 7]};
+              store_a(c0 + q, h);
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            tc_mbar_arrive(&bar_a[st]);
+          }
+        }
+        if (last) asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      }
+      // the output layer's column halves, added in a fixed order
+      if (hh == 1) s_y[r] = y;
+      epi_sync();
+      if (hh == 0) y += s_y[r];
+      y += bo;
+      const float g = gscale * y;
+      if (a.Gout) {
+        if (ok && hh == 0) a.Gout[(size_t)b * a.Mp + j] = g;
+        continue;  // (ln_end = ln0 + 1)
+      }
+      const size_t row = (size_t)ln * sstride + (size_t)b * a.Mp;
+      float nv = 0.f;
+      double num = 0.0, den = 0.0;
+      if (ok && hh == 0) {
+        nv = a.D ? g + a.D[row + j] : g;
+        if (a.Gh) a.Gh[row + j] = g;
+        if (a.partials) {
+          const double dd = (double)nv - (double)a.U[row + sstride + j];
+          num = dd * dd;
+          den = (double)nv * nv;
+        }
+        a.U[row + sstride + j] = nv;
+      }
+      if (hh == 0) s_u[r] = nv;
+      epi_sync();
+      u = s_u[r];
+      if (a.partials) {
+        reduce256(num, den);
+        if (t == 0) {
+          double *pp = a.partials + (((size_t)(ln + 1) * a.B + b) * a.nch + blockIdx.x + a.cta0) * 2;
+          pp[0] = num;
+          pp[1] = den;
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 8) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((uint32_t)(2 * W)));
+  }
+}
+
 typedef void (*TcKernel)(PinnTcArgs);
 template <bool SPLIT, bool H16>
 static TcKernel tc_kernel_t(int IN, int W, int act, bool wide) {
@@ -786,6 +1102,28 @@ static TcKernel tc2_kernel(int IN, int W, int act, int mode) {
   if (mode == kTcSplit16) return W <= 128 ? tc2_kernel_t<true, true>(IN, W, act) : nullptr;
   return mode == kTcF16 ? tc2_kernel_t<true, false>(IN, W, act) : tc2_kernel_t<false, false>(IN, W, act);
 }
+// the layer-pipelined split kernel (k_pinn_chain_tc3): ring depth NB ∈ {2, 4} by shared memory
+template <int NB>
+static TcKernel tc3_kernel_nb(int IN, int W, int act) {
+#define PR_TC3_CASE(IN_, W_) \
+  if (IN == IN_ && W == W_) return act ? k_pinn_chain_tc3<IN_, W_, 1, true, true, NB> : k_pinn_chain_tc3<IN_, W_, 0, true, true, NB>;
+  PR_TC3_CASE(4, 64) PR_TC3_CASE(4, 128) PR_TC3_CASE(4, 256) PR_TC3_CASE(2, 64) PR_TC3_CASE(2, 128) PR_TC3_CASE(2, 256)
+#undef PR_TC3_CASE
+  return nullptr;
+}
+static size_t pinn_tc3_smem(int W, int LH, int nfloats, bool *resident, int *nb) {
+  const size_t a = 2 * (size_t)128 * W * 2, chunk = 2 * (size_t)W * kTcKC * 2, p = (size_t)nfloats * 4;
+  const size_t all = (size_t)(LH - 1) * (W / kTcKC) * chunk;
+  *resident = a + all + p <= 200 * 1024;
+  *nb = a + 4 * chunk + p <= 215 * 1024 ? 4 : 2;
+  return *resident ? a + all + p : a + (size_t)*nb * chunk + p;
+}
+// PR_TC_PIPE (tuning): 1 (default) the layer-pipelined kernel for the split mode at W = 256, 0 the
+// one-tile kernel
+static int tc3_env() {
+  static const int on = getenv("PR_TC_PIPE") ? atoi(getenv("PR_TC_PIPE")) : 1;
+  return on;
+}
 static size_t pinn_tc2_smem(int W, int LH, int nfloats, int np, bool *resident) {
   const size_t a = 2 * (size_t)np * 128 * W * 2, chunk = (size_t)np * W * kTcKC * 2, p = (size_t)nfloats * 4;
   const size_t all = (size_t)(LH - 1) * (W / kTcKC) * chunk;
@@ -843,6 +1181,25 @@ cudaError_t launch_pinn_tc(int IN, int W, int act, int mode, const PinnArgs &a, 
     ta.wh = wh;
     ta.resident = resident ? 1 : 0;
     k2<<<grid, 288, smem, s>>>(ta);  // two 128-point tiles per CTA
+    return cudaGetLastError();
+  }
+  // the layer-pipelined split kernel where the one-tile split kernel holds one CTA per SM anyway
+  // (W = 256: 8×256 122.8 → 95.7 ms per C5 chain pair, 4×256 56.8 → 44.2, scripts/tc_wide_ab.py);
+  // at W = 128 two one-tile CTAs per SM overlap each other's MMAs and epilogues already, and the
+  // pipelined kernel (one CTA per SM) is slower (4×128 16.8 → 21.8 ms)
+  if (mode == kTcSplit16 && W == 256 && tc3_env()) {
+    bool resident3 = false;
+    int nb = 2;
+    const size_t smem3 = pinn_tc3_smem(W, a.LH, a.nfloats, &resident3, &nb);
+    TcKernel k3 = nb == 4 ? tc3_kernel_nb<4>(IN, W, act) : tc3_kernel_nb<2>(IN, W, act);
+    if (!k3) return cudaErrorInvalidValue;
+    cudaError_t e = cudaFuncSetAttribute(k3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3);
+    if (e != cudaSuccess) return e;
+    PinnTcArgs ta;
+    ta.g = a;
+    ta.wh = wh;
+    ta.resident = resident3 ? 1 : 0;
+    k3<<<grid, 288, smem3, s>>>(ta);
     return cudaGetLastError();
   }
   TcKernel k = tc_kernel(IN, W, act, mode);
