@@ -1103,23 +1103,24 @@ static TcKernel tc2_kernel(int IN, int W, int act, int mode) {
   return mode == kTcF16 ? tc2_kernel_t<true, false>(IN, W, act) : tc2_kernel_t<false, false>(IN, W, act);
 }
 // the layer-pipelined split kernel (k_pinn_chain_tc3): ring depth NB ∈ {2, 4} by shared memory
-template <int NB>
+template <int NB, bool SPLIT = true, bool H16 = true>
 static TcKernel tc3_kernel_nb(int IN, int W, int act) {
 #define PR_TC3_CASE(IN_, W_) \
-  if (IN == IN_ && W == W_) return act ? k_pinn_chain_tc3<IN_, W_, 1, true, true, NB> : k_pinn_chain_tc3<IN_, W_, 0, true, true, NB>;
+  if (IN == IN_ && W == W_) return act ? k_pinn_chain_tc3<IN_, W_, 1, SPLIT, H16, NB> : k_pinn_chain_tc3<IN_, W_, 0, SPLIT, H16, NB>;
   PR_TC3_CASE(4, 64) PR_TC3_CASE(4, 128) PR_TC3_CASE(4, 256) PR_TC3_CASE(2, 64) PR_TC3_CASE(2, 128) PR_TC3_CASE(2, 256)
 #undef PR_TC3_CASE
   return nullptr;
 }
-static size_t pinn_tc3_smem(int W, int LH, int nfloats, bool *resident, int *nb) {
-  const size_t a = 2 * (size_t)128 * W * 2, chunk = 2 * (size_t)W * kTcKC * 2, p = (size_t)nfloats * 4;
+static size_t pinn_tc3_smem(int W, int LH, int nfloats, bool *resident, int *nb, int np = 2) {
+  const size_t a = (size_t)np * 128 * W * 2, chunk = (size_t)np * W * kTcKC * 2, p = (size_t)nfloats * 4;
   const size_t all = (size_t)(LH - 1) * (W / kTcKC) * chunk;
   *resident = a + all + p <= 200 * 1024;
   *nb = a + 4 * chunk + p <= 215 * 1024 ? 4 : 2;
   return *resident ? a + all + p : a + (size_t)*nb * chunk + p;
 }
 // PR_TC_PIPE (tuning): 1 (default) the layer-pipelined kernel for the split mode at W = 256, 0 the
-// one-tile kernel
+// one-tile kernel, 2 the layer-pipelined kernel for every mode at W = 256 (the single-pass modes are
+// slower with it: 8×256 fp16x1 55.5 → 65.5 ms, bf16 47.3 → 59.0 — their one-tile CTAs run two per SM)
 static int tc3_env() {
   static const int on = getenv("PR_TC_PIPE") ? atoi(getenv("PR_TC_PIPE")) : 1;
   return on;
@@ -1187,11 +1188,13 @@ cudaError_t launch_pinn_tc(int IN, int W, int act, int mode, const PinnArgs &a, 
   // (W = 256: 8×256 122.8 → 95.7 ms per C5 chain pair, 4×256 56.8 → 44.2, scripts/tc_wide_ab.py);
   // at W = 128 two one-tile CTAs per SM overlap each other's MMAs and epilogues already, and the
   // pipelined kernel (one CTA per SM) is slower (4×128 16.8 → 21.8 ms)
-  if (mode == kTcSplit16 && W == 256 && tc3_env()) {
+  if (W == 256 && (mode == kTcSplit16 ? tc3_env() : tc3_env() == 2)) {
     bool resident3 = false;
     int nb = 2;
-    const size_t smem3 = pinn_tc3_smem(W, a.LH, a.nfloats, &resident3, &nb);
-    TcKernel k3 = nb == 4 ? tc3_kernel_nb<4>(IN, W, act) : tc3_kernel_nb<2>(IN, W, act);
+    const size_t smem3 = pinn_tc3_smem(W, a.LH, a.nfloats, &resident3, &nb, mode == kTcSplit16 ? 2 : 1);
+    TcKernel k3 = mode == kTcSplit16 ? (nb == 4 ? tc3_kernel_nb<4>(IN, W, act) : tc3_kernel_nb<2>(IN, W, act))
+                  : mode == kTcF16 ? (nb == 4 ? tc3_kernel_nb<4, false, true>(IN, W, act) : tc3_kernel_nb<2, false, true>(IN, W, act))
+                                   : (nb == 4 ? tc3_kernel_nb<4, false, false>(IN, W, act) : tc3_kernel_nb<2, false, false>(IN, W, act));
     if (!k3) return cudaErrorInvalidValue;
     cudaError_t e = cudaFuncSetAttribute(k3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3);
     if (e != cudaSuccess) return e;
