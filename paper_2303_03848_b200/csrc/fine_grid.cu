@@ -36,6 +36,9 @@ constexpr int kGT = 256;        // threads per CTA
 constexpr int kGW = kGT / 32;   // warps per CTA
 constexpr long long kSpinMax = 1ll << 28;  // look-back wait bound (then the solve fails, no hang)
 constexpr int kPollRounds = 4;             // look-back rounds whose loads are in flight together
+// words between consecutive CTAs' published totals: each CTA's words on their own two 128-B lines
+// (no line shared by two CTAs' stores and polls)
+constexpr int kTotStride = 32;
 
 __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long *p) {
   unsigned long long v;
@@ -379,7 +382,7 @@ __global__ void __launch_bounds__(kGT, 1) k_fine_grid(GridArgs a) {
       //     pid+2 or pid+3 runs downward and waits for them)
       constexpr int WPC = NS * 4;     // words per CTA total
       constexpr int G = 32 / WPC;     // predecessors polled per round
-      unsigned long long *slot = a.tot + (size_t)(pid & 3) * nCTA * WPC;
+      unsigned long long *slot = a.tot + (size_t)(pid & 3) * nCTA * kTotStride;
       if (w == 0) {
         double T1[NS], T2[NS];  // the CTA total: all warps composed in pass order (every lane)
 #pragma unroll
@@ -402,7 +405,7 @@ __global__ void __launch_bounds__(kGT, 1) k_fine_grid(GridArgs a) {
           const double val = sT[lane >> 1];
           const unsigned long long bits = (unsigned long long)__double_as_longlong(val);
           const unsigned half = (lane & 1) ? (unsigned)(bits >> 32) : (unsigned)bits;
-          st_relaxed_u64(slot + (size_t)c * WPC + lane, ((unsigned long long)pid << 32) | half);
+          st_relaxed_u64(slot + (size_t)c * kTotStride + lane, ((unsigned long long)pid << 32) | half);
         }
         if (tr && lane == 0) tr[1] = gtime();
         // look-back: the totals of the W predecessors in pass direction, G per round
@@ -420,7 +423,7 @@ __global__ void __launch_bounds__(kGT, 1) k_fine_grid(GridArgs a) {
 #pragma unroll
           for (int r = 0; r < kPollRounds; ++r) {
             const int kq = base0 + r * G + gi + 1;  // predecessor distance
-            wd[r] = (gi < G && kq <= W) ? ld_relaxed_u64(slot + (size_t)(up ? c - kq : c + kq) * WPC + q) : 0ull;
+            wd[r] = (gi < G && kq <= W) ? ld_relaxed_u64(slot + (size_t)(up ? c - kq : c + kq) * kTotStride + q) : 0ull;
           }
 #pragma unroll
           for (int r = 0; r < kPollRounds; ++r) {
@@ -428,7 +431,7 @@ __global__ void __launch_bounds__(kGT, 1) k_fine_grid(GridArgs a) {
             const bool act = gi < G && kq <= W;
             unsigned half = 0;
             if (act) {
-              const unsigned long long *src = slot + (size_t)(up ? c - kq : c + kq) * WPC + q;
+              const unsigned long long *src = slot + (size_t)(up ? c - kq : c + kq) * kTotStride + q;
               long long spins = 0;
               while ((wd[r] >> 32) != pid) {
                 wd[r] = ld_relaxed_u64(src);
@@ -562,6 +565,7 @@ constexpr int kPTs[] = {4, 8, 16, 28};
 }  // namespace
 
 int fine_grid_ns(int PT, int nsys) { return ns_pick(PT, nsys); }
+size_t fine_grid_tot_words(int nblocks) { return (size_t)4 * nblocks * kTotStride; }
 size_t fine_grid_smem(int PT, int steps) {  // at the largest NS of PT (every launch fits)
   const int NS = ns_max(PT);
   const size_t lvl = NS == 3 ? (size_t)(6 + PT) : 30;  // chunk maps + smem state (NS = 3), else level coefficients

@@ -58,7 +58,7 @@ struct GridArgs {
   const double *lbP;                 // [2][nCTA][KW][3] look-back weights (maps between predecessor and CTA)
   const int *lbW;                    // [2][nCTA] look-back windows
   int KW;
-  unsigned long long *tot;           // [4][nCTA][NS·2][2] published CTA totals per pass slot: each
+  unsigned long long *tot;           // [4][nCTA][32] published CTA totals per pass slot (NS·4 words used): each
                                      // fp64 total as two words (32-bit half | pass id << 32), zeroed
                                      // before the launch
   int *err;                          // set when a look-back wait times out
@@ -70,6 +70,7 @@ struct GridArgs {
 size_t fine_grid_smem(int PT, int steps);
 int fine_grid_pt(int M, int nsm, int *nblocks);  // points per thread for M points (0: too large)
 int fine_grid_ns(int PT, int nsys);               // systems per group of a launch over nsys systems
+size_t fine_grid_tot_words(int nblocks);          // words of the look-back slots (GridArgs::tot)
 cudaError_t launch_fine_grid(const GridArgs &a, int PT, int nblocks, cudaStream_t s);
 // Pipelined Parareal on one GPU (pipe.cu, NEXT-2): PINN chain (latency mode) and K1 fine solves
 // in one cooperative kernel, synchronised per slice.

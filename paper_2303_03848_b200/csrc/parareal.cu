@@ -880,7 +880,7 @@ bool use_grid(const pr_ctx *c, int nsys) {
 pr_status ensure_grid(pr_ctx *c) {
   if (c->g_tot) return PR_OK;
   const int nb = c->fine.g_nb;
-  c->g_tot_words = (size_t)4 * nb * pr::fine_grid_ns(c->fine.g_pt, 1 << 30) * 4;
+  c->g_tot_words = pr::fine_grid_tot_words(nb);
   CU(cudaMalloc(&c->g_tot, c->g_tot_words * sizeof(unsigned long long)));
   CU(cudaHostAlloc((void **)&c->g_err_h, sizeof(int), cudaHostAllocMapped));
   *c->g_err_h = 0;
