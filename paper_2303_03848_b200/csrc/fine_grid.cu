@@ -7,16 +7,19 @@
 // 2-state recurrence; an n-step slice is n+1 passes.  Here one system (2^20 points at C3) spans
 // the whole GPU: CTA c (one per SM, cooperative launch) owns a contiguous range of 256·PT points,
 // thread t of it PT consecutive points, and NS systems (slices) are solved together.  The state
-// stays in registers (fp64) for all passes of a slice group — HBM is touched once per slice (load
-// U_n, store D_n) instead of 16 B per point and step — and the factors 1/p_j, 1/q_j of the CTA's
-// points sit in shared memory; the off-diagonals come from the closed forms
+// stays on chip (fp64) for all passes of a slice group — in registers, and at PT = 28 (C3) a third
+// system in shared memory (NS = 3) — so HBM is touched once per slice (load U_n, store D_n) instead
+// of 16 B per point and step; the factors 1/p_j, 1/q_j of the CTA's points sit in shared memory;
+// the off-diagonals come from the closed forms
 // l_j = −J(c1·J − c0), u_j = −J(c1·J + c0) (J = j+1, c0 = dτr/2, c1 = dτσ²/2).
 //
-// One pass: each thread runs its points from a zero entering state (chunk totals), a warp scan
-// of the 2-vector affine parts with per-lane level coefficients precomputed at kernel start, a
+// One pass: each thread runs its points from a zero entering state (chunk totals; the elimination
+// chain in scaled form), a warp scan of the 2-vector affine parts with per-lane level coefficients
+// precomputed at kernel start (recomputed per scan when NS = 3, whose third state takes their room), a
 // fold over the warps (constant warp maps in shared memory), the CTA total is published
-// (per-pass slot, tagged words) and the entering state of the CTA is composed from the totals of
-// its W predecessors in pass direction (decoupled look-back: every CTA publishes before it waits,
+// (per-pass slot, tagged words, 32-word stride per CTA) and the entering state of the CTA is
+// composed from the totals of its W predecessors in pass direction, all of a window's polling
+// rounds in flight together (decoupled look-back: every CTA publishes before it waits,
 // so the wait is one store-to-load propagation; W from the host, where the product of the predecessors'
 // maps falls below 1e-24 — the same truncation as K2; the weights Π of the CTA maps in between
 // are host tables), then each thread reruns its points from its exact entering state.
