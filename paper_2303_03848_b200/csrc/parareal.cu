@@ -191,6 +191,7 @@ struct pr_ctx {
   cudaGraphExec_t g_exec = nullptr;
   const float *g_vt = nullptr;
   float *g_v0 = nullptr;
+  bool g_dev = false;  // the captured solve took device pointers
   int g_K = 0;
   int64_t g_launches = 0;
   cudaEvent_t g_e0 = nullptr, g_e1 = nullptr;
@@ -1741,9 +1742,12 @@ pr_status solve_impl_(pr_ctx *c, const float *V_T, float *V_0, bool device_ptr, 
     }
     return at.type == cudaMemoryTypeHost;
   };
-  const bool use_graph = c->opt_graphs && c->tol == 0.0 && c->world == 1 &&
-                         (device_ptr || (pinned(V_T) && pinned(V_0)));
-  if (use_graph && c->g_exec && c->g_vt == V_T && c->g_v0 == V_0) {
+  // (a replay of the captured (V_T, V_0) pair was checked when it was captured: no attribute queries)
+  const bool replay = c->opt_graphs && c->tol == 0.0 && c->world == 1 && c->g_exec && c->g_vt == V_T &&
+                      c->g_v0 == V_0 && c->g_dev == device_ptr;
+  const bool use_graph = replay || (c->opt_graphs && c->tol == 0.0 && c->world == 1 &&
+                                    (device_ptr || (pinned(V_T) && pinned(V_0))));
+  if (replay) {
     CU(cudaGraphLaunch(c->g_exec, c->stream));
     c->launches += c->g_launches;
     if (c->opt_graphs == 2 && device_ptr) {  // stream-ordered replay: return once enqueued (no δ, no times)
@@ -1866,6 +1870,7 @@ pr_status solve_impl_(pr_ctx *c, const float *V_T, float *V_0, bool device_ptr, 
     c->ev_used = 0;
     c->g_vt = V_T;
     c->g_v0 = V_0;
+    c->g_dev = device_ptr;
     c->g_K = K;
     c->g_e0 = e0;
     c->g_e1 = e1;

@@ -251,12 +251,17 @@ class Context:
         self._check(lib().parareal_solve_device(self.h, _ptr(d_VT), _ptr(d_V0), C.byref(rep)))
         return self._rep_dict(rep, buf)
 
-    def solve_host_ptrs(self, V_T_ptr: Optional[int], V_0_ptr: Optional[int]) -> dict:
-        """parareal_solve with raw host pointers (e.g. pinned torch CPU tensors' data_ptr())."""
-        rep, buf = self._report()
+    def solve_host_ptrs(self, V_T_ptr: Optional[int], V_0_ptr: Optional[int], report: bool = True) -> Optional[dict]:
+        """parareal_solve with raw host pointers (e.g. pinned torch CPU tensors' data_ptr()); report=False
+        passes no report (the ABI's nullable rep) and returns None."""
         fp = C.POINTER(C.c_float)
-        self._check(lib().parareal_solve(self.h, C.cast(V_T_ptr, fp) if V_T_ptr else None,
-                                         C.cast(V_0_ptr, fp) if V_0_ptr else None, C.byref(rep)))
+        vt = C.cast(V_T_ptr, fp) if V_T_ptr else None
+        v0 = C.cast(V_0_ptr, fp) if V_0_ptr else None
+        if not report:
+            self._check(lib().parareal_solve(self.h, vt, v0, None))
+            return None
+        rep, buf = self._report()
+        self._check(lib().parareal_solve(self.h, vt, v0, C.byref(rep)))
         return self._rep_dict(rep, buf)
 
     def initial_state(self) -> np.ndarray:
