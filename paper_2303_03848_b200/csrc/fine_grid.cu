@@ -42,6 +42,13 @@ constexpr int kPollRounds = 4;             // look-back rounds whose loads are i
 // words between consecutive CTAs' published totals: each CTA's words on their own two 128-B lines
 // (no line shared by two CTAs' stores and polls)
 constexpr int kTotStride = 32;
+// PR_DEBUG_BOUNDS builds (test-only variant, compute-sanitizer being unavailable on the GPU pool):
+// index checks that trap on violation
+#ifdef PR_DEBUG_BOUNDS
+#define PR_CHECK(cond) do { if (!(cond)) __trap(); } while (0)
+#else
+#define PR_CHECK(cond) do { } while (0)
+#endif
 
 __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long *p) {
   unsigned long long v;
@@ -213,6 +220,7 @@ __global__ void __launch_bounds__(kGT, 1) k_fine_grid(GridArgs a) {
       const int k = q / a.steps, m = q - k * a.steps;
       const int n = a.n_base + a.ln0 + grp * NS + k;
       const double tau1 = (n * a.dT + m * a.dtau) + a.dtau;  // τ_{m+1} of slice n (the oracle's association)
+      PR_CHECK(grp * NS + k < ngroups * NS);
       sbc[q] = a.upper_bc ? 0.0 : a.bcoef * (a.Lb - a.Kb * exp(-a.rb * tau1));
     }
     __syncthreads();
@@ -408,6 +416,7 @@ __global__ void __launch_bounds__(kGT, 1) k_fine_grid(GridArgs a) {
           const double val = sT[lane >> 1];
           const unsigned long long bits = (unsigned long long)__double_as_longlong(val);
           const unsigned half = (lane & 1) ? (unsigned)(bits >> 32) : (unsigned)bits;
+          PR_CHECK(lane < kTotStride && c < nCTA);
           st_relaxed_u64(slot + (size_t)c * kTotStride + lane, ((unsigned long long)pid << 32) | half);
         }
         if (tr && lane == 0) tr[1] = gtime();
@@ -426,6 +435,7 @@ __global__ void __launch_bounds__(kGT, 1) k_fine_grid(GridArgs a) {
 #pragma unroll
           for (int r = 0; r < kPollRounds; ++r) {
             const int kq = base0 + r * G + gi + 1;  // predecessor distance
+            if (gi < G && kq <= W) PR_CHECK((up ? c - kq : c + kq) >= 0 && (up ? c - kq : c + kq) < nCTA && kq <= a.KW);
             wd[r] = (gi < G && kq <= W) ? ld_relaxed_u64(slot + (size_t)(up ? c - kq : c + kq) * kTotStride + q) : 0ull;
           }
 #pragma unroll

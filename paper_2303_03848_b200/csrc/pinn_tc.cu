@@ -25,6 +25,12 @@
 namespace pr {
 
 __device__ __forceinline__ uint32_t tc_smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+// PR_DEBUG_BOUNDS builds (test-only variant): index checks that trap on violation
+#ifdef PR_DEBUG_BOUNDS
+#define PR_CHECK(cond) do { if (!(cond)) __trap(); } while (0)
+#else
+#define PR_CHECK(cond) do { } while (0)
+#endif
 
 // UMMA shared-memory matrix descriptor (SWIZZLE_NONE, K-major): start >> 4 [0,14), LBO >> 4
 // [16,30), SBO >> 4 [32,46), version 1 [46,48) (sm_100), base offset 0, layout type 0.
@@ -793,11 +799,13 @@ __global__ void __launch_bounds__(288, 1) k_pinn_chain_tc3(PinnTcArgs ta) {
               const int c = 2 * st + cc;
               uint32_t bc;
               if (ta.resident) {
+                PR_CHECK((l - 1) * NCH + c < nchunks);
                 bc = bBase + (uint32_t)((l - 1) * NCH + c) * kChunk;
               } else {
                 tc_mbar_wait(&bar_full[g % NB], (g / NB) & 1);
                 bc = bBase + (g % NB) * kChunk;
               }
+              PR_CHECK(c < NCH);
 #pragma unroll
               for (int ks = 0; ks < kTcKC / 16; ++ks) {
                 const uint32_t ao = (uint32_t)(c * (kTcKC / 8) + 2 * ks) * 128, bo2 = (uint32_t)(2 * ks) * 128;
@@ -849,6 +857,7 @@ __global__ void __launch_bounds__(288, 1) k_pinn_chain_tc3(PinnTcArgs ta) {
     const float bo = Wo[W];
     auto store_a = [&](int c0, const float (&h)[8]) {
       const size_t off = cm_offset(r, c0, W);
+      PR_CHECK(c0 + 8 <= W && off + 8 <= (size_t)TILE * W);
       *reinterpret_cast<uint4 *>(sA + off) =
           make_uint4(pack2<T>(h[0], h[1]), pack2<T>(h[2], h[3]), pack2<T>(h[4], h[5]), pack2<T>(h[6], h[7]));
       if (SPLIT) {
