@@ -724,7 +724,7 @@ __global__ void __launch_bounds__(288, 1) k_pinn_chain_tc2(PinnTcArgs ta) {
 // i.e. after the issuer consumed the phase (no run-ahead across phases).  Same per-point arithmetic
 // as k_pinn_chain_tc except the K-chunk accumulation order, which is unchanged (chunks 0 … NCH−1).
 template <int IN, int W, int ACT, bool SPLIT, bool H16, int NB>
-__global__ void __launch_bounds__(288, 1) k_pinn_chain_tc3(PinnTcArgs ta) {
+__global__ void __launch_bounds__(288, W <= 128 ? 2 : 1) k_pinn_chain_tc3(PinnTcArgs ta) {
   using T = typename std::conditional<H16 || SPLIT, __half, __nv_bfloat16>::type;
   constexpr int TILE = 128;
   constexpr int NP = SPLIT ? 2 : 1;
@@ -1124,11 +1124,11 @@ static size_t pinn_tc3_smem(int W, int LH, int nfloats, bool *resident, int *nb,
   const size_t a = (size_t)np * 128 * W * 2, chunk = (size_t)np * W * kTcKC * 2, p = (size_t)nfloats * 4;
   const size_t all = (size_t)(LH - 1) * (W / kTcKC) * chunk;
   *resident = a + all + p <= 200 * 1024;
-  *nb = a + 4 * chunk + p <= 215 * 1024 ? 4 : 2;
+  *nb = (W > 128 && a + 4 * chunk + p <= 215 * 1024) ? 4 : 2;  // W ≤ 128: two CTAs per SM
   return *resident ? a + all + p : a + (size_t)*nb * chunk + p;
 }
-// PR_TC_PIPE (tuning): 1 (default) the layer-pipelined kernel for the split mode at W = 256, 0 the
-// one-tile kernel, 2 the layer-pipelined kernel for every mode at W = 256 (the single-pass modes are
+// PR_TC_PIPE (tuning): 1 (default) the layer-pipelined kernel for the split mode at W ≥ 128, 0 the
+// one-tile kernel, 2 the layer-pipelined kernel for every mode at W ≥ 128 (the single-pass modes are
 // slower with it: 8×256 fp16x1 55.5 → 65.5 ms, bf16 47.3 → 59.0 — their one-tile CTAs run two per SM)
 static int tc3_env() {
   static const int on = getenv("PR_TC_PIPE") ? atoi(getenv("PR_TC_PIPE")) : 1;
@@ -1193,11 +1193,12 @@ cudaError_t launch_pinn_tc(int IN, int W, int act, int mode, const PinnArgs &a, 
     k2<<<grid, 288, smem, s>>>(ta);  // two 128-point tiles per CTA
     return cudaGetLastError();
   }
-  // the layer-pipelined split kernel where the one-tile split kernel holds one CTA per SM anyway
-  // (W = 256: 8×256 122.8 → 95.7 ms per C5 chain pair, 4×256 56.8 → 44.2, scripts/tc_wide_ab.py);
-  // at W = 128 two one-tile CTAs per SM overlap each other's MMAs and epilogues already, and the
-  // pipelined kernel (one CTA per SM) is slower (4×128 16.8 → 21.8 ms)
-  if (W == 256 && (mode == kTcSplit16 ? tc3_env() : tc3_env() == 2)) {
+  // the layer-pipelined split kernel for W ≥ 128 where the ping-pong kernel is not used
+  // (scripts/tc_wide_ab.py, ms per C5 chain pair: 8×256 122.8 → 95.7, 4×256 56.8 → 44.2 with one
+  // CTA per SM and a 4-deep weight ring; 4×128 16.8 → 15.1, 8×128 34.5 → 30.7 with two CTAs per SM
+  // and a 2-deep ring — with one CTA per SM it was slower there: 21.8 / 45.1); W = 64: no gain
+  // (6×64 16.7 → 16.6, one 64-column step per layer).  PR_TC_PIPE = 3 forces it for every width.
+  if ((W >= 128 || tc3_env() == 3) && (mode == kTcSplit16 ? tc3_env() != 0 : tc3_env() == 2)) {
     bool resident3 = false;
     int nb = 2;
     const size_t smem3 = pinn_tc3_smem(W, a.LH, a.nfloats, &resident3, &nb, mode == kTcSplit16 ? 2 : 1);

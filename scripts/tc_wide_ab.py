@@ -6,7 +6,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2303_03848_b200 import parareal, synth  # noqa: E402
 for W, LH, prec, name in [(256, 8, parareal.PREC_FP16_TC, "split"), (256, 8, parareal.PREC_FP16X1_TC, "fp16x1"),
                           (256, 8, parareal.PREC_BF16_TC, "bf16"), (256, 4, parareal.PREC_FP16_TC, "split"),
-                          (128, 4, parareal.PREC_FP16_TC, "split"), (128, 8, parareal.PREC_FP16_TC, "split")]:
+                          (128, 4, parareal.PREC_FP16_TC, "split"), (128, 8, parareal.PREC_FP16_TC, "split"),
+                          (64, 4, parareal.PREC_FP16_TC, "split"), (64, 6, parareal.PREC_FP16_TC, "split")]:
     p = synth.config("C5", coarse=synth.COARSE_PINN, max_iter=1, tol=0.0)
     net = synth.kaiming_net([4] + [W] * LH + [1], seed=1)
     with parareal.Context(p) as c:
