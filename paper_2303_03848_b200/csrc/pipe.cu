@@ -161,16 +161,15 @@ __device__ void chain_role(const PipeArgs &pa, int k, int b, int chunk, const fl
       n0 = k;
     }
     // slice n's inputs (D_n and the old U_{n+1}) are fetched as soon as their flags are seen set:
-    // for the next slice, speculatively right after this one's stores (a non-blocking check), else
-    // at the top of the next slice (blocking wait)
+    // for the next slice, speculatively right after this one's stores (a non-blocking check of the
+    // flags lane 0 loaded at the top of this slice, so their L2 latency hides behind the network),
+    // else at the top of the next slice (blocking wait)
     float dn = 0.f, uo = 0.f;
     bool have = false;
-    auto flags_ready = [&](int n) -> bool {  // lane 0's view, broadcast
+    int fd_next = 0, fl_next = 0;  // lane 0: fdone[n+1], floaded[n+2] as loaded at the top of slice n
+    auto flags_ready = [&](int n) -> bool {  // lane 0's view of the early loads, broadcast
       bool r = true;
-      if (lane == 0) {
-        r = ld_flag(fdone + n) >= k;
-        if (r && n + 1 <= pa.N - 1) r = ld_flag(floaded + n + 1) >= k;
-      }
+      if (lane == 0) r = fd_next >= k && (n + 1 > pa.N - 1 || fl_next >= k);
       return __shfl_sync(0xffffffffu, r ? 1 : 0, 0) != 0;
     };
     auto fetch = [&](int n) {
@@ -188,6 +187,10 @@ __device__ void chain_role(const PipeArgs &pa, int k, int b, int chunk, const fl
         }
         __syncwarp();
         fetch(n);
+      }
+      if (k > 0 && lane == 0 && n + 1 < pa.N) {  // issued now, read after the evaluation
+        fd_next = ld_flag(fdone + n + 1);
+        fl_next = n + 2 <= pa.N - 1 ? ld_flag(floaded + n + 2) : k;
       }
       const size_t row = (size_t)n * sstride + (size_t)b * a.Mp;
       const int ng = a.n_base + n;
@@ -425,13 +428,19 @@ __global__ void __launch_bounds__(128) k_parareal_pipe_num(PipeArgs pa) {
   }
 }
 
-// CTAs [0, (K+1)·B·C): the chain of iteration k = blockIdx / (B·C) (each iteration its own CTAs,
-// so chain k+1 runs behind chain k instead of after it); then one CTA per fine system.
+// CTAs [0, S·B·C): chain CTA set s = blockIdx / (B·C) runs the chains of iterations k ≡ s (mod S),
+// one after the other (S = min(K+1, 2): chain k+1 still runs behind chain k on its own CTAs, while
+// chain k+2 — which starts only after chain k has finished at C2 — reuses chain k's CTAs; no chain
+// waits on a later one, so the reuse cannot deadlock); then one CTA per fine system.  With one set
+// per iteration the grid (160 CTAs at C2) exceeded the 148 SMs and the chain CTAs that shared an
+// SM paced every later iteration (1.7 vs 1.2 µs per slice).
+__host__ __device__ __forceinline__ int pipe_chain_sets(int K) { return K + 1 < 2 ? K + 1 : 2; }
 template <int P, bool CN, int IN, int W, int G, int ACT, int NWC>
 __global__ void __launch_bounds__(NWC * 32) k_parareal_pipe(PipeArgs pa) {
   extern __shared__ float sw[];
   const int per = pa.g.B * pa.C;
-  const int nchain = (pa.K + 1) * per;
+  const int S = pipe_chain_sets(pa.K);
+  const int nchain = S * per;
   if ((int)blockIdx.x < nchain) {
     const float *w = pa.g.wts;  // group kernels read the weights through L1
     if (G == 1 || (W == 20 && G == kPinnSplitG)) {  // smem weights (group chains read them through L1)
@@ -439,8 +448,12 @@ __global__ void __launch_bounds__(NWC * 32) k_parareal_pipe(PipeArgs pa) {
       __syncthreads();
       w = sw;
     }
-    const int k = blockIdx.x / per, r = blockIdx.x % per;
-    chain_role<IN, W, G, ACT, NWC>(pa, k, r / pa.C, r % pa.C, w);
+    const int s0 = blockIdx.x / per, r = blockIdx.x % per;
+#pragma unroll 1
+    for (int k = s0; k <= pa.K; k += S) {
+      chain_role<IN, W, G, ACT, NWC>(pa, k, r / pa.C, r % pa.C, w);
+      __syncthreads();  // (chain k's CTA-wide δ fold is done before chain k+S starts)
+    }
   } else {
     if (threadIdx.x >= 128) return;  // one K1 system per fine CTA (128 threads)
     const int f = blockIdx.x - nchain;
@@ -530,7 +543,7 @@ cudaError_t launch_parareal_pipe(const PipeArgs &pa, int M, bool cn, int IN, int
   const int nthreads = 32 * pipe_chain_warps(W, G);
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, nthreads, smem);
   if (e != cudaSuccess) return e;
-  const int grid = (pa.K + 1) * pa.g.B * pa.C + pa.g.B * pa.N;
+  const int grid = pipe_chain_sets(pa.K) * pa.g.B * pa.C + pa.g.B * pa.N;
   if (grid > occ * nsm) return cudaErrorCooperativeLaunchTooLarge;
   PipeArgs arg = pa;
   void *params[] = {&arg};

@@ -468,21 +468,24 @@ def test_device_entry_points():
     assert np.array_equal(v0, oracle.payoff(p).astype(np.float32))
 
 
-@pytest.mark.parametrize("name,M,N,B,theta,dims,act", [
-    ("C1", 64, 4, 1, 1.0, synth.PINN_3x20, synth.ACT_TANH), ("C2", 1024, 32, 1, 1.0, synth.PINN_3x20, synth.ACT_TANH),
-    ("C2", 1024, 32, 1, 0.5, synth.PINN_3x20, synth.ACT_TANH), ("portfolio", 256, 8, 6, 1.0, synth.PINN_3x20, synth.ACT_TANH),
-    ("odd", 700, 12, 1, 1.0, synth.PINN_3x20, synth.ACT_TANH),
-    ("C2 paper net", 1024, 32, 1, 1.0, synth.PINN_PAPER, synth.ACT_RELU),
-    ("paper net tanh", 300, 8, 2, 1.0, synth.PINN_PAPER, synth.ACT_TANH)])
-def test_pipelined_matches_blocking(name, M, N, B, theta, dims, act):
+@pytest.mark.parametrize("name,M,N,B,theta,dims,act,K", [
+    ("C1", 64, 4, 1, 1.0, synth.PINN_3x20, synth.ACT_TANH, 3), ("C2", 1024, 32, 1, 1.0, synth.PINN_3x20, synth.ACT_TANH, 3),
+    ("C2", 1024, 32, 1, 0.5, synth.PINN_3x20, synth.ACT_TANH, 3), ("portfolio", 256, 8, 6, 1.0, synth.PINN_3x20, synth.ACT_TANH, 3),
+    ("odd", 700, 12, 1, 1.0, synth.PINN_3x20, synth.ACT_TANH, 3),
+    ("C2 paper net", 1024, 32, 1, 1.0, synth.PINN_PAPER, synth.ACT_RELU, 3),
+    ("paper net tanh", 300, 8, 2, 1.0, synth.PINN_PAPER, synth.ACT_TANH, 3),
+    ("C2 K=8: chain CTAs reused (k, k+2, ...)", 1024, 32, 1, 1.0, synth.PINN_3x20, synth.ACT_TANH, 8),
+    ("C2 paper net K=8", 1024, 32, 1, 1.0, synth.PINN_PAPER, synth.ACT_RELU, 8)])
+def test_pipelined_matches_blocking(name, M, N, B, theta, dims, act, K):
     """PR_OPT_PIPELINE (NEXT-2): the overlapped single-kernel schedule gives the blocking
     schedule's iterates, output and δ bitwise (and is the one auto mode takes here), with the
-    latency-mode chain (3x20) and the one-thread-per-point chain (the paper's 10x50 net)."""
+    latency-mode chain (3x20) and the one-thread-per-point chain (the paper's 10x50 net); K = 8
+    runs several chains on each chain CTA (sets of iterations k ≡ s mod 2)."""
     if B > 1:
         p = synth.portfolio(n_k=B // 2 if B > 2 else 1, n_s=3 if B > 2 else 2, M=M, N=N, coarse=synth.COARSE_PINN,
-                            max_iter=3, tol=0.0)
+                            max_iter=K, tol=0.0)
     else:
-        p = synth.single(M, N, coarse=synth.COARSE_PINN, max_iter=3, tol=0.0, fine_theta=theta)
+        p = synth.single(M, N, coarse=synth.COARSE_PINN, max_iter=K, tol=0.0, fine_theta=theta)
     net = synth.kaiming_net(dims, seed=2, activation=act)
     with ctx_for(p, net) as c:
         a, ra = c.solve()
@@ -491,7 +494,7 @@ def test_pipelined_matches_blocking(name, M, N, B, theta, dims, act):
         b, rb = c.solve()
         it_b = c.copy_iterates(0, p.N + 1)
     assert ra["kernel_launches"] < rb["kernel_launches"], "auto mode did not pipeline"
-    assert ra["iterations"] == rb["iterations"] == 3
+    assert ra["iterations"] == rb["iterations"] == K
     assert np.array_equal(a, b) and np.array_equal(it_a, it_b)
     assert np.array_equal(ra["delta"], rb["delta"])
 
@@ -547,10 +550,11 @@ def test_errors_on_gpu():
 
 
 def test_pipeline_falls_back_when_not_co_resident():
-    """The pipelined kernel needs every CTA co-resident: the paper's 10x50 net at C2 with K = 8
-    needs 9 chains x 29 twelve-warp CTAs + 32 fine CTAs > 148 SMs, so auto mode must run the
-    blocking schedule (same launches as PR_OPT_PIPELINE=1) and give its results bitwise."""
-    p = synth.single(1024, 32, coarse=synth.COARSE_PINN, max_iter=8, tol=0.0)
+    """The pipelined kernel needs every CTA co-resident: the paper's 10x50 net on two C2 instances
+    needs 2 chain sets x 2 instances x 29 twelve-warp CTAs + 2 x 32 fine CTAs = 180 > 148 SMs, so
+    auto mode must run the blocking schedule (same launches as PR_OPT_PIPELINE=1) and give its
+    results bitwise."""
+    p = synth.portfolio(n_k=1, n_s=2, M=1024, N=32, coarse=synth.COARSE_PINN, max_iter=8, tol=0.0)
     net = synth.kaiming_net(synth.PINN_PAPER, seed=4)
     with ctx_for(p, net) as c:
         a, ra = c.solve()
