@@ -119,9 +119,12 @@ __device__ void chain_role(const PipeArgs &pa, int k, int b, int chunk, const fl
   // per-warp partial of (row ln) in this iteration's staging block:
   // stage[k][((ln·B·C) + cta)·NWC + wid]·2
   double *wst = pa.wstage + (size_t)k * (pa.N + 1) * a.B * pa.C * NWC * 2;
+  // (non-zero partials sit on the group leaders only — lanes ≡ 0 mod G — so for a power-of-two G the
+  // butterfly stops at distance G: the lower levels would add exact zeros to lane 0's sum)
+  constexpr int kLowLevel = (G & (G - 1)) == 0 ? G : 1;
   auto stage_partial = [&](int ln, double num, double den) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
+    for (int o = 16; o >= kLowLevel; o >>= 1) {
       num += __shfl_xor_sync(0xffffffffu, num, o);
       den += __shfl_xor_sync(0xffffffffu, den, o);
     }
