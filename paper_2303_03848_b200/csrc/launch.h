@@ -79,6 +79,7 @@ struct PipeArgs {
   PinnArgs g;              // coarse chain (same rows)
   ResidentArgs rc;         // numerical coarse G (PR_COARSE_IMPLICIT_EULER): its scheme (n_c steps)
   int N, K, C;             // slices, iterations, chain CTAs per instance
+  int S;                   // chain CTA sets (set s runs the chains k ≡ s mod S; set by the launcher)
   int cpub;                // chain publications per (instance, slice): chain warps (PINN) or 1 (numerical)
   double *partials;        // [K+1][pstride] δ partials per iteration
   size_t pstride;

@@ -170,9 +170,15 @@ __device__ void chain_role(const PipeArgs &pa, int k, int b, int chunk, const fl
     float dn = 0.f, uo = 0.f;
     bool have = false;
     int fd_next = 0, fl_next = 0;  // lane 0: fdone[n+1], floaded[n+2] as loaded at the top of slice n
-    auto flags_ready = [&](int n) -> bool {  // lane 0's view of the early loads, broadcast
-      bool r = true;
-      if (lane == 0) r = fd_next >= k && (n + 1 > pa.N - 1 || fl_next >= k);
+    auto flags_ready = [&](int n) -> bool {  // lane 0's view, broadcast: the early loads, else a fresh
+      bool r = true;                          // check (a long evaluation — the paper's net — may have
+      if (lane == 0) {                        // outlived the early values)
+        r = fd_next >= k && (n + 1 > pa.N - 1 || fl_next >= k);
+        if (!r) {
+          r = ld_flag(fdone + n) >= k;
+          if (r && n + 1 <= pa.N - 1) r = ld_flag(floaded + n + 1) >= k;
+        }
+      }
       return __shfl_sync(0xffffffffu, r ? 1 : 0, 0) != 0;
     };
     auto fetch = [&](int n) {
@@ -432,17 +438,18 @@ __global__ void __launch_bounds__(128) k_parareal_pipe_num(PipeArgs pa) {
 }
 
 // CTAs [0, S·B·C): chain CTA set s = blockIdx / (B·C) runs the chains of iterations k ≡ s (mod S),
-// one after the other (S = min(K+1, 2): chain k+1 still runs behind chain k on its own CTAs, while
-// chain k+2 — which starts only after chain k has finished at C2 — reuses chain k's CTAs; no chain
-// waits on a later one, so the reuse cannot deadlock); then one CTA per fine system.  With one set
-// per iteration the grid (160 CTAs at C2) exceeded the 148 SMs and the chain CTAs that shared an
-// SM paced every later iteration (1.7 vs 1.2 µs per slice).
-__host__ __device__ __forceinline__ int pipe_chain_sets(int K) { return K + 1 < 2 ? K + 1 : 2; }
+// one after the other; then one CTA per fine system.  S = K+1 (every chain its own CTAs) when that
+// grid fits one CTA per SM, else S = 2 (pa.S, host): chain k+1 still runs behind chain k on its own
+// CTAs while chain k+2 — which at C2 starts only after chain k has finished — reuses chain k's
+// CTAs; no chain waits on a later one, so the reuse cannot deadlock.  At C2 with the 3×20 net one
+// set per iteration is 160 CTAs > 148 SMs, and the chain CTAs that shared an SM paced every later
+// iteration (1.7 vs 1.2 µs per slice); with the paper's 10×50 net (12-warp chain CTAs, 148 CTAs)
+// the chains overlap in time, and reusing CTAs would serialise them (0.84 → 0.97 ms).
 template <int P, bool CN, int IN, int W, int G, int ACT, int NWC>
 __global__ void __launch_bounds__(NWC * 32) k_parareal_pipe(PipeArgs pa) {
   extern __shared__ float sw[];
   const int per = pa.g.B * pa.C;
-  const int S = pipe_chain_sets(pa.K);
+  const int S = pa.S;
   const int nchain = S * per;
   if ((int)blockIdx.x < nchain) {
     const float *w = pa.g.wts;  // group kernels read the weights through L1
@@ -546,9 +553,12 @@ cudaError_t launch_parareal_pipe(const PipeArgs &pa, int M, bool cn, int IN, int
   const int nthreads = 32 * pipe_chain_warps(W, G);
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, nthreads, smem);
   if (e != cudaSuccess) return e;
-  const int grid = pipe_chain_sets(pa.K) * pa.g.B * pa.C + pa.g.B * pa.N;
+  int S = pa.K + 1;
+  if ((long)S * pa.g.B * pa.C + (long)pa.g.B * pa.N > nsm) S = S < 2 ? S : 2;  // one CTA per SM, else two sets
+  const int grid = S * pa.g.B * pa.C + pa.g.B * pa.N;
   if (grid > occ * nsm) return cudaErrorCooperativeLaunchTooLarge;
   PipeArgs arg = pa;
+  arg.S = S;
   void *params[] = {&arg};
   return cudaLaunchCooperativeKernel((const void *)k, dim3(grid), dim3(nthreads), params, smem, s);
 }
