@@ -305,14 +305,17 @@ __device__ __forceinline__ float mlp_split(const float *__restrict__ sw, int LH,
   for (int l = 1; l < LH; ++l) {
 #pragma unroll
     for (int i = 0; i < W; ++i) h[i] = __shfl_sync(0xffffffffu, own[i % NPT], gbase + i / NPT);
+    // the NPT neurons' sums advance together input by input (NPT independent FMA chains in flight;
+    // each neuron's summation order is unchanged: bias, then inputs 0 … W−1)
+    float z[NPT];
 #pragma unroll
-    for (int k = 0; k < NPT; ++k) {
-      const int o = q * NPT + k;
-      float z = lw[W * W + o];
+    for (int k = 0; k < NPT; ++k) z[k] = lw[W * W + q * NPT + k];
 #pragma unroll
-      for (int i = 0; i < W; ++i) z = fmaf(lw[o * W + i], h[i], z);
-      own[k] = act<ACT>(z);
-    }
+    for (int i = 0; i < W; ++i)
+#pragma unroll
+      for (int k = 0; k < NPT; ++k) z[k] = fmaf(lw[(q * NPT + k) * W + i], h[i], z[k]);
+#pragma unroll
+    for (int k = 0; k < NPT; ++k) own[k] = act<ACT>(z[k]);
     lw += W * W + W;
   }
   float y = 0.f;
