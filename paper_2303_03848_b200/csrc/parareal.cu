@@ -669,7 +669,7 @@ size_t layout(pr_ctx *c, char *base) {
   c->U = (float *)take((size_t)(c->Nloc + 1) * row * sizeof(float));
   c->Gh = (float *)take((size_t)std::max(c->Nloc, 1) * row * sizeof(float));
   c->D = (float *)take((size_t)std::max(c->Nloc, 1) * row * sizeof(float));
-  c->Fk = (float *)take(row * sizeof(float));
+  c->Fk = (float *)take(2 * row * sizeof(float));  // (two rows for the pipelined schedule)
   c->tmp = (float *)take(2 * row * sizeof(float));
   c->partials = (double *)take((size_t)(c->Nloc + 1) * c->B * c->nch * 2 * sizeof(double));
   c->d_delta = (unsigned long long *)take((size_t)c->max_iter * sizeof(unsigned long long));

@@ -148,7 +148,7 @@ __device__ void chain_role(const PipeArgs &pa, int k, int b, int chunk, const fl
       float *uk = a.U + (size_t)k * sstride + (size_t)b * a.Mp;
       double num = 0.0, den = 0.0;
       if (ok) {
-        const float f = __ldcg(a.Fcopy + (size_t)b * a.Mp + j);
+        const float f = __ldcg(a.Fcopy + (size_t)(k & 1) * sstride + (size_t)b * a.Mp + j);
         if (leader) {
           const double dd = (double)f - (double)__ldcg(uk + j);
           num = dd * dd;
@@ -279,21 +279,32 @@ __device__ void fine_role(const PipeArgs &pa, int n, int b) {
   int *floaded = pa.floaded + (size_t)b * pa.N, *fdone = pa.fdone + (size_t)b * pa.N;
   const size_t row = ((size_t)n * a.B + b) * a.Mp;
   const int kmax = min(pa.K, n + 1);
+  const size_t fstride = (size_t)a.B * a.Mp;  // Fk holds two rows: F̂ of iteration k in row k & 1
   for (int k = 1; k <= kmax; ++k) {
-    if (n >= 1 && t == 0) wait_geq(cnt + (n - 1), k * C);  // U^{k−1}_n written
+    // U^{k−1}_n.  For n = k−1 ≥ 1 it is F̂^{k−1}_{k−2} (Q12), which chain k−1 copies into U_n: read
+    // it where fine(k−1, k−2) left it instead, as soon as that solve is done — the same floats,
+    // without waiting for the chain's copy (one hand-off less on the critical path).  fine(k+1, k)
+    // overwrites that row only after chain k−1 has passed slice k−1 (this CTA's iteration k waits
+    // on that), so the copy has read it first.
+    const bool from_f = n >= 1 && n == k - 1;
+    if (n >= 1 && t == 0) {
+      if (from_f) wait_geq(fdone + (n - 1), k - 1);  // F̂^{k−1}_{k−2} written
+      else wait_geq(cnt + (n - 1), k * C);           // U^{k−1}_n written
+    }
     PR_TRI_SYNC();
+    const float *src = from_f ? a.Fk + (size_t)((k - 1) & 1) * fstride + (size_t)b * a.Mp : a.U + row;
     double x[P];
 #pragma unroll
     for (int i = 0; i < P; ++i) {
       const int j = t * P + i;
-      x[i] = (j < a.M) ? (double)__ldcg(a.U + row + j) : 0.0;
+      x[i] = (j < a.M) ? (double)__ldcg(src + j) : 0.0;
     }
     PR_TRI_SYNC();
     if (t == 0) publish_set(floaded + n, k);
     if (pa.trace && b == 0 && t == 0) pa.trace[((size_t)k * pa.N + n) * 3 + 1] = gtimer();
     run_steps<P, NT, CN, ZZ>(tri, a, b, a.n_base + n, t, x, sh, bct);
     if (n == k - 1) {  // F̂_{k−1}: copied into U^k_k by chain k
-      float *o = a.Fk + (size_t)b * a.Mp;
+      float *o = a.Fk + (size_t)(k & 1) * fstride + (size_t)b * a.Mp;
 #pragma unroll
       for (int i = 0; i < P; ++i) {
         const int j = t * P + i;
@@ -352,7 +363,7 @@ __device__ void chain_role_num(const PipeArgs &pa, int k, int b) {
     }
     PR_TRI_SYNC();
     float *uk = U + (size_t)k * sstride + (size_t)b * a.Mp;
-    const float *f = pa.r.Fk + (size_t)b * a.Mp;
+    const float *f = pa.r.Fk + (size_t)(k & 1) * sstride + (size_t)b * a.Mp;
     double num = 0.0, den = 0.0;
 #pragma unroll
     for (int i = 0; i < P; ++i) {
