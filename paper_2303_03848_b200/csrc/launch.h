@@ -84,7 +84,11 @@ struct PipeArgs {
   double *partials;        // [K+1][pstride] δ partials per iteration
   size_t pstride;
   double *wstage;          // [N+1][B·C][4 warps][2] per-warp δ partials of the current iteration
-  int *cnt, *floaded, *fdone;  // [B][N] counters, zero at launch
+  int *cnt, *floaded, *fdone;  // [B][N] counters (contiguous), zero at launch; the kernel's tail
+                               // zeroes them again for the next launch
+  unsigned long long *gbar;    // grid-barrier counter of the tail: monotone across launches
+  unsigned long long *dmax;    // [K] δ^k (ordered double bits): zeroed at the start, set by the tail
+  int nch;                     // δ chunks per (slice, instance) row
   unsigned long long *trace;   // nullable: [K+1][N][3] %globaltimer (chain warp 0 of CTA 0 at each
                                // slice; fine (n, b=0) start and end), for PR_PIPE_TRACE
 };
@@ -98,6 +102,4 @@ cudaError_t launch_parareal_pipe(const PipeArgs &pa, int M, bool cn, int IN, int
 cudaError_t launch_payoff(float *U0, int M, int Mp, int B, const double *Lb, const double *Kb, cudaStream_t s);
 cudaError_t launch_delta(const double *partials, int B, int nch, int ln_lo, int ln_hi, unsigned long long *dmax,
                          cudaStream_t s);
-cudaError_t launch_delta_multi(const double *partials, size_t pstride, int B, int nch, int N, int K,
-                               unsigned long long *dmax, cudaStream_t s);
 }  // namespace pr

@@ -74,32 +74,10 @@ __global__ void k_delta_wide(const double *partials, int B, int nch, int ln_lo, 
   }
 }
 
-// δ^k for k = 1..K in one launch (pipelined schedule: per-iteration partial buffers of pstride
-// doubles; iteration k covers rows k..N).  Same per-row fixed-order sums as k_delta; dmax[K]
-// must be zero.
-__global__ void k_delta_multi(const double *partials, size_t pstride, int B, int nch, int N, int K,
-                              unsigned long long *dmax) {
-  const int k = blockIdx.y + 1;
-  const int row = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
-  const int total = (N - k + 1) * B;
-  if (row >= total) return;
-  const int ln = k + row / B, b = row % B;
-  const double rel = row_rel(partials + (size_t)k * pstride + (((size_t)ln * B + b) * nch) * 2, nch, lane);
-  if (lane == 0) atomicMax(dmax + (k - 1), (unsigned long long)__double_as_longlong(rel));
-}
-
-// Up to kDeltaWarpMax chunks a warp sums a row (k_delta, k_delta_multi: the same order in the
-// blocking and pipelined schedules; unused chunks are zero), beyond that a CTA per row does
+// Up to kDeltaWarpMax chunks a warp sums a row (k_delta, and the pipelined kernel's tail: the same
+// order in the blocking and pipelined schedules; unused chunks are zero), beyond that a CTA per row does
 // (k_delta_wide).
 constexpr int kDeltaWarpMax = 1024;
-cudaError_t launch_delta_multi(const double *partials, size_t pstride, int B, int nch, int N, int K,
-                               unsigned long long *dmax, cudaStream_t s) {
-  if (nch > kDeltaWarpMax) return cudaErrorInvalidValue;  // (the pipelined schedule runs small grids)
-  dim3 grid((N * B * 32 + 255) / 256, K);
-  k_delta_multi<<<grid, 256, 0, s>>>(partials, pstride, B, nch, N, K, dmax);
-  return cudaGetLastError();
-}
-
 cudaError_t launch_delta(const double *partials, int B, int nch, int ln_lo, int ln_hi, unsigned long long *dmax,
                          cudaStream_t s) {
   const int total = (ln_hi - ln_lo + 1) * B;

@@ -1374,7 +1374,9 @@ pr_status ensure_pipe(pr_ctx *c) {
   if (c->pipe_partials) return PR_OK;
   c->pipe_pstride = (size_t)(c->Nloc + 1) * c->B * c->nch * 2;
   CU(cudaMalloc(&c->pipe_partials, (size_t)(c->max_iter + 1) * c->pipe_pstride * sizeof(double)));
-  CU(cudaMalloc(&c->pipe_flags, (size_t)3 * c->B * c->N * sizeof(int)));
+  CU(cudaMalloc(&c->pipe_flags, (size_t)3 * c->B * c->N * sizeof(int) + 2 * sizeof(unsigned long long)));
+  // flags and the tail's grid-barrier counter zeroed once: every launch leaves the flags zero
+  CU(cudaMemset(c->pipe_flags, 0, (size_t)3 * c->B * c->N * sizeof(int) + 2 * sizeof(unsigned long long)));
   CU(cudaMalloc(&c->pipe_wstage, (size_t)(c->max_iter + 1) * (c->N + 1) * c->B * c->nch * 4 * 2 * sizeof(double)));
   CU(cudaMemset(c->pipe_partials, 0, (size_t)(c->max_iter + 1) * c->pipe_pstride * sizeof(double)));
   return PR_OK;
@@ -1383,7 +1385,6 @@ pr_status ensure_pipe(pr_ctx *c) {
 // All K iterations (and the k = 0 coarse sweep) in one cooperative launch, then the K δ's.
 // Returns PR_ERR_UNSUPPORTED (nothing enqueued) if the grid cannot be co-resident.
 pr_status solve_pipelined(pr_ctx *c) {
-  CU(cudaMemsetAsync(c->pipe_flags, 0, (size_t)3 * c->B * c->N * sizeof(int), c->stream));
   pr::PipeArgs pa;
   std::memset(&pa, 0, sizeof pa);
   pa.r = base_args(c, c->fine);
@@ -1431,6 +1432,9 @@ pr_status solve_pipelined(pr_ctx *c) {
   pa.cnt = c->pipe_flags;
   pa.floaded = c->pipe_flags + (size_t)c->B * c->N;
   pa.fdone = c->pipe_flags + (size_t)2 * c->B * c->N;
+  pa.gbar = (unsigned long long *)(c->pipe_flags + align_up((size_t)3 * c->B * c->N, 2));
+  pa.dmax = c->d_delta;
+  pa.nch = c->nch;
   const cudaError_t e =
       num ? pr::launch_parareal_pipe_num(pa, c->M, c->fine_theta != 1.0, c->stream)
           : pr::launch_parareal_pipe(pa, c->M, c->fine_theta != 1.0, c->IN, c->W, c->act, G,
@@ -1456,12 +1460,7 @@ pr_status solve_pipelined(pr_ctx *c) {
       fclose(f);
     }
   }
-  // δ^1..δ^K in one launch (fixed-order sums per row, as delta_reduce)
-  CU(cudaMemsetAsync(c->d_delta, 0, (size_t)c->max_iter * sizeof(unsigned long long), c->stream));
-  const cudaError_t de = pr::launch_delta_multi(c->pipe_partials, c->pipe_pstride, c->B, c->nch, c->N, c->max_iter,
-                                                c->d_delta, c->stream);
-  if (de != cudaSuccess) return fail(c, PR_ERR_CUDA, fmt("delta: %s", cudaGetErrorString(de)));
-  c->launches++;
+  // δ^1..δ^K: computed by the kernel's tail (k_delta's fixed-order sums per row)
   return PR_OK;
 }
 

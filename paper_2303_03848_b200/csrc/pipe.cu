@@ -13,7 +13,7 @@
 // so iteration k's fine solves start slice by slice behind chain k−1 and chain k trails them,
 // approaching Eq. (8)'s pipelined cost instead of the blocking sum.  Results are bitwise those of
 // the blocking schedule (same kernels' arithmetic, same orders).  The δ partial sums of each
-// iteration go to their own buffer and are reduced after the kernel.
+// iteration go to their own buffer and are reduced by the kernel's tail after a grid barrier.
 //
 // Roles: CTAs [0, (K+1)·B·C) run the PINN chain of iteration k = CTA / (B·C) in latency mode
 // (kPinnSplitG threads per point, 128/kPinnSplitG points per CTA, C chunks per instance), the
@@ -93,6 +93,61 @@ __device__ __forceinline__ float chain_eval(const float *sw, int LH, const float
 }
 
 constexpr int kChunkWarps = 4;  // warps per δ chunk: the blocking chain kernel's CTA (128 threads)
+
+// One row's δ chunks summed by one warp in k_delta's fixed order (misc.cu row_rel: lane l adds
+// chunks l, l+32, … in index order, then the xor-shuffle tree; lane 0's value is used).
+__device__ __forceinline__ double tail_row_rel(const double *p, int nch, int lane) {
+  double num = 0.0, den = 0.0;
+  for (int c = lane; c < nch; c += 32) { num += p[2 * c]; den += p[2 * c + 1]; }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    num += __shfl_xor_sync(0xffffffffu, num, o);
+    den += __shfl_xor_sync(0xffffffffu, den, o);
+  }
+  return (den > 0.0) ? sqrt(num) / sqrt(den) : sqrt(num);
+}
+
+// Kernel start: δ^1..δ^K zeroed (CTA 0) before the tail's barrier orders them before its maxima.
+__device__ __forceinline__ void pipe_head(const PipeArgs &pa) {
+  if (blockIdx.x == 0)
+    for (int k = threadIdx.x; k < pa.K; k += blockDim.x) pa.dmax[k] = 0ull;
+}
+// Kernel tail, in place of the flag memset, the δ memset and the δ launch that each solve needed:
+// a grid barrier (one arrival per CTA on a counter that is never reset: arrival `old` waits for
+// the next multiple of gridDim.x), then δ^1..δ^K from the per-iteration partials with
+// k_delta's per-row sums and max, and the flags zeroed for the next launch.  NT threads of
+// the CTA take part (the fine CTAs' first 128: their barrier is the named barrier 1).
+template <int NT, bool FINE>
+__device__ void pipe_tail(const PipeArgs &pa) {
+  __threadfence();
+  if (FINE) PR_TRI_SYNC(); else __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned long long n = gridDim.x;
+    const unsigned long long old = atomicAdd(pa.gbar, 1ull);
+    const unsigned long long target = (old / n + 1) * n;
+    for (;;) {
+      unsigned long long v;
+      asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(pa.gbar) : "memory");
+      if (v >= target) break;
+      __nanosleep(32);
+    }
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  }
+  if (FINE) PR_TRI_SYNC(); else __syncthreads();
+  const int B = pa.g.B, lane = threadIdx.x & 31;
+  constexpr int NW = NT / 32;
+  const int gw = blockIdx.x * NW + (threadIdx.x >> 5), nwarps = gridDim.x * NW;
+  for (int k = 1; k <= pa.K; ++k) {
+    const int total = (pa.N - k + 1) * B;
+    for (int row = gw; row < total; row += nwarps) {
+      const int ln = k + row / B, b = row % B;
+      const double *p = pa.partials + (size_t)k * pa.pstride + (((size_t)ln * B + b) * pa.nch) * 2;
+      const double rel = tail_row_rel(p, pa.nch, lane);
+      if (lane == 0) atomicMax(pa.dmax + (k - 1), (unsigned long long)__double_as_longlong(rel));
+    }
+  }
+  for (int i = blockIdx.x * NT + threadIdx.x; i < 3 * B * pa.N; i += gridDim.x * NT) pa.cnt[i] = 0;
+}
 
 template <int IN, int W, int G, int ACT, int NWC>
 __device__ void chain_role(const PipeArgs &pa, int k, int b, int chunk, const float *sw) {
@@ -439,6 +494,7 @@ __device__ void chain_role_num(const PipeArgs &pa, int k, int b) {
 
 template <int P, bool CN>
 __global__ void __launch_bounds__(128) k_parareal_pipe_num(PipeArgs pa) {
+  pipe_head(pa);
   const int nchain = (pa.K + 1) * pa.g.B;
   if ((int)blockIdx.x < nchain) {
     chain_role_num<P>(pa, blockIdx.x / pa.g.B, blockIdx.x % pa.g.B);
@@ -446,6 +502,7 @@ __global__ void __launch_bounds__(128) k_parareal_pipe_num(PipeArgs pa) {
     const int f = blockIdx.x - nchain;
     fine_role<P, CN, 4>(pa, f / pa.g.B, f % pa.g.B);
   }
+  pipe_tail<128, true>(pa);  // (128-thread CTAs: named barrier 1 is the whole CTA)
 }
 
 // CTAs [0, S·B·C): chain CTA set s = blockIdx / (B·C) runs the chains of iterations k ≡ s (mod S),
@@ -459,6 +516,7 @@ __global__ void __launch_bounds__(128) k_parareal_pipe_num(PipeArgs pa) {
 template <int P, bool CN, int IN, int W, int G, int ACT, int NWC>
 __global__ void __launch_bounds__(NWC * 32) k_parareal_pipe(PipeArgs pa) {
   extern __shared__ float sw[];
+  pipe_head(pa);
   const int per = pa.g.B * pa.C;
   const int S = pa.S;
   const int nchain = S * per;
@@ -475,10 +533,12 @@ __global__ void __launch_bounds__(NWC * 32) k_parareal_pipe(PipeArgs pa) {
       chain_role<IN, W, G, ACT, NWC>(pa, k, r / pa.C, r % pa.C, w);
       __syncthreads();  // (chain k's CTA-wide δ fold is done before chain k+S starts)
     }
+    pipe_tail<NWC * 32, false>(pa);
   } else {
     if (threadIdx.x >= 128) return;  // one K1 system per fine CTA (128 threads)
     const int f = blockIdx.x - nchain;
     fine_role<P, CN, NWC>(pa, f / pa.g.B, f % pa.g.B);
+    pipe_tail<128, true>(pa);
   }
 }
 
