@@ -86,7 +86,7 @@ struct PipeArgs {
   double *wstage;          // [N+1][B·C][4 warps][2] per-warp δ partials of the current iteration
   int *cnt, *floaded, *fdone;  // [B][N] counters (contiguous), zero at launch; the kernel's tail
                                // zeroes them again for the next launch
-  unsigned long long *gbar;    // grid-barrier counter of the tail: monotone across launches
+  unsigned long long *gbar;    // [2] the tail's grid barrier: arrival count (0 between launches), generation
   unsigned long long *dmax;    // [K] δ^k (ordered double bits): zeroed at the start, set by the tail
   int nch;                     // δ chunks per (slice, instance) row
   unsigned long long *trace;   // nullable: [K+1][N][3] %globaltimer (chain warp 0 of CTA 0 at each

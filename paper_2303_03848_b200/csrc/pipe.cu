@@ -95,10 +95,17 @@ __device__ __forceinline__ float chain_eval(const float *sw, int LH, const float
 constexpr int kChunkWarps = 4;  // warps per δ chunk: the blocking chain kernel's CTA (128 threads)
 
 // One row's δ chunks summed by one warp in k_delta's fixed order (misc.cu row_rel: lane l adds
-// chunks l, l+32, … in index order, then the xor-shuffle tree; lane 0's value is used).
-__device__ __forceinline__ double tail_row_rel(const double *p, int nch, int lane) {
+// chunks l, l+32, … in index order, then the xor-shuffle tree; lane 0's value is used).  The row
+// is left zero: a later launch whose chain covers fewer chunks (another net loaded into the
+// context: other chain-CTA widths) must not sum this launch's partials.
+__device__ __forceinline__ double tail_row_rel(double *p, int nch, int lane) {
   double num = 0.0, den = 0.0;
-  for (int c = lane; c < nch; c += 32) { num += p[2 * c]; den += p[2 * c + 1]; }
+  for (int c = lane; c < nch; c += 32) {
+    num += p[2 * c];
+    den += p[2 * c + 1];
+    p[2 * c] = 0.0;
+    p[2 * c + 1] = 0.0;
+  }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     num += __shfl_xor_sync(0xffffffffu, num, o);
@@ -113,23 +120,28 @@ __device__ __forceinline__ void pipe_head(const PipeArgs &pa) {
     for (int k = threadIdx.x; k < pa.K; k += blockDim.x) pa.dmax[k] = 0ull;
 }
 // Kernel tail, in place of the flag memset, the δ memset and the δ launch that each solve needed:
-// a grid barrier (one arrival per CTA on a counter that is never reset: arrival `old` waits for
-// the next multiple of gridDim.x), then δ^1..δ^K from the per-iteration partials with
-// k_delta's per-row sums and max, and the flags zeroed for the next launch.  NT threads of
+// a grid barrier (arrival count + generation word; the last arrival resets the count and bumps the
+// generation, so the barrier holds for any grid size a later launch on the same buffers uses), then δ^1..δ^K from the per-iteration partials with
+// k_delta's per-row sums and max (rows left zero), and the flags zeroed for the next launch.  NT threads of
 // the CTA take part (the fine CTAs' first 128: their barrier is the named barrier 1).
 template <int NT, bool FINE>
 __device__ void pipe_tail(const PipeArgs &pa) {
   __threadfence();
   if (FINE) PR_TRI_SYNC(); else __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned long long n = gridDim.x;
-    const unsigned long long old = atomicAdd(pa.gbar, 1ull);
-    const unsigned long long target = (old / n + 1) * n;
-    for (;;) {
-      unsigned long long v;
-      asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(pa.gbar) : "memory");
-      if (v >= target) break;
-      __nanosleep(32);
+  if (threadIdx.x == 0) {  // gbar[0]: arrivals (back to 0 after every barrier), gbar[1]: generation
+    unsigned long long gen, old;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(gen) : "l"(pa.gbar + 1) : "memory");
+    asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], 1;" : "=l"(old) : "l"(pa.gbar) : "memory");
+    if (old == (unsigned long long)gridDim.x - 1) {  // last arrival: reset the count, open the barrier
+      asm volatile("st.relaxed.gpu.global.u64 [%0], 0;" ::"l"(pa.gbar) : "memory");
+      asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(pa.gbar + 1), "l"(gen + 1) : "memory");
+    } else {
+      for (;;) {
+        unsigned long long v;
+        asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(pa.gbar + 1) : "memory");
+        if (v != gen) break;
+        __nanosleep(32);
+      }
     }
     asm volatile("fence.acq_rel.gpu;" ::: "memory");
   }
@@ -141,7 +153,7 @@ __device__ void pipe_tail(const PipeArgs &pa) {
     const int total = (pa.N - k + 1) * B;
     for (int row = gw; row < total; row += nwarps) {
       const int ln = k + row / B, b = row % B;
-      const double *p = pa.partials + (size_t)k * pa.pstride + (((size_t)ln * B + b) * pa.nch) * 2;
+      double *p = pa.partials + (size_t)k * pa.pstride + (((size_t)ln * B + b) * pa.nch) * 2;
       const double rel = tail_row_rel(p, pa.nch, lane);
       if (lane == 0) atomicMax(pa.dmax + (k - 1), (unsigned long long)__double_as_longlong(rel));
     }

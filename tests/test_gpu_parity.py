@@ -499,6 +499,24 @@ def test_pipelined_matches_blocking(name, M, N, B, theta, dims, act, K):
     assert np.array_equal(ra["delta"], rb["delta"])
 
 
+def test_pipelined_grid_changes_within_one_context():
+    """The pipelined kernel's tail (grid barrier, δ reduction, flag reset) leaves its buffers clean
+    for the next launch even when that launch has another grid: one context alternates the
+    latency-mode 3x20 chain (4-warp chain CTAs) and the paper's 10x50 net (12-warp chain CTAs,
+    another CTA count); every pipelined solve equals the blocking solve of the same net bitwise."""
+    p = synth.single(1024, 32, coarse=synth.COARSE_PINN, max_iter=3, tol=0.0)
+    nets = [synth.kaiming_net(synth.PINN_3x20, seed=2), synth.kaiming_net(synth.PINN_PAPER, seed=2, activation=synth.ACT_RELU)]
+    with ctx_for(p, nets[0]) as c:
+        for i in (0, 1, 0, 1, 1, 0):
+            c.load_weights(nets[i])
+            c.set_option(parareal.OPT_PIPELINE, 0)
+            a, ra = c.solve()
+            c.set_option(parareal.OPT_PIPELINE, 1)
+            b, rb = c.solve()
+            assert ra["kernel_launches"] < rb["kernel_launches"], "auto mode did not pipeline"
+            assert np.array_equal(a, b) and np.array_equal(ra["delta"], rb["delta"])
+
+
 def test_graph_replay_matches_eager():
     """PR_OPT_USE_GRAPHS: captured + replayed solves give the eager results bitwise, replays
     are repeatable, and new weights are picked up (the graph is re-captured)."""
