@@ -114,10 +114,15 @@ __device__ __forceinline__ double tail_row_rel(double *p, int nch, int lane) {
   return (den > 0.0) ? sqrt(num) / sqrt(den) : sqrt(num);
 }
 
-// Kernel start: δ^1..δ^K zeroed (CTA 0) before the tail's barrier orders them before its maxima.
-__device__ __forceinline__ void pipe_head(const PipeArgs &pa) {
+// Kernel start: δ^1..δ^K zeroed (CTA 0) before the tail's barrier orders them before its maxima;
+// returns the barrier's generation (it changes only when this launch's barrier opens, so it is
+// read here, off the tail's critical path).
+__device__ __forceinline__ unsigned long long pipe_head(const PipeArgs &pa) {
   if (blockIdx.x == 0)
     for (int k = threadIdx.x; k < pa.K; k += blockDim.x) pa.dmax[k] = 0ull;
+  unsigned long long gen = 0;
+  if (threadIdx.x == 0) asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(gen) : "l"(pa.gbar + 1) : "memory");
+  return gen;
 }
 // Kernel tail, in place of the flag memset, the δ memset and the δ launch that each solve needed:
 // a grid barrier (arrival count + generation word; the last arrival resets the count and bumps the
@@ -125,12 +130,11 @@ __device__ __forceinline__ void pipe_head(const PipeArgs &pa) {
 // k_delta's per-row sums and max (rows left zero), and the flags zeroed for the next launch.  NT threads of
 // the CTA take part (the fine CTAs' first 128: their barrier is the named barrier 1).
 template <int NT, bool FINE>
-__device__ void pipe_tail(const PipeArgs &pa) {
+__device__ void pipe_tail(const PipeArgs &pa, unsigned long long gen) {
   __threadfence();
   if (FINE) PR_TRI_SYNC(); else __syncthreads();
   if (threadIdx.x == 0) {  // gbar[0]: arrivals (back to 0 after every barrier), gbar[1]: generation
-    unsigned long long gen, old;
-    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(gen) : "l"(pa.gbar + 1) : "memory");
+    unsigned long long old;
     asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], 1;" : "=l"(old) : "l"(pa.gbar) : "memory");
     if (old == (unsigned long long)gridDim.x - 1) {  // last arrival: reset the count, open the barrier
       asm volatile("st.relaxed.gpu.global.u64 [%0], 0;" ::"l"(pa.gbar) : "memory");
@@ -506,7 +510,7 @@ __device__ void chain_role_num(const PipeArgs &pa, int k, int b) {
 
 template <int P, bool CN>
 __global__ void __launch_bounds__(128) k_parareal_pipe_num(PipeArgs pa) {
-  pipe_head(pa);
+  const unsigned long long gen = pipe_head(pa);
   const int nchain = (pa.K + 1) * pa.g.B;
   if ((int)blockIdx.x < nchain) {
     chain_role_num<P>(pa, blockIdx.x / pa.g.B, blockIdx.x % pa.g.B);
@@ -514,7 +518,7 @@ __global__ void __launch_bounds__(128) k_parareal_pipe_num(PipeArgs pa) {
     const int f = blockIdx.x - nchain;
     fine_role<P, CN, 4>(pa, f / pa.g.B, f % pa.g.B);
   }
-  pipe_tail<128, true>(pa);  // (128-thread CTAs: named barrier 1 is the whole CTA)
+  pipe_tail<128, true>(pa, gen);  // (128-thread CTAs: named barrier 1 is the whole CTA)
 }
 
 // CTAs [0, S·B·C): chain CTA set s = blockIdx / (B·C) runs the chains of iterations k ≡ s (mod S),
@@ -528,7 +532,7 @@ __global__ void __launch_bounds__(128) k_parareal_pipe_num(PipeArgs pa) {
 template <int P, bool CN, int IN, int W, int G, int ACT, int NWC>
 __global__ void __launch_bounds__(NWC * 32) k_parareal_pipe(PipeArgs pa) {
   extern __shared__ float sw[];
-  pipe_head(pa);
+  const unsigned long long gen = pipe_head(pa);
   const int per = pa.g.B * pa.C;
   const int S = pa.S;
   const int nchain = S * per;
@@ -545,12 +549,12 @@ __global__ void __launch_bounds__(NWC * 32) k_parareal_pipe(PipeArgs pa) {
       chain_role<IN, W, G, ACT, NWC>(pa, k, r / pa.C, r % pa.C, w);
       __syncthreads();  // (chain k's CTA-wide δ fold is done before chain k+S starts)
     }
-    pipe_tail<NWC * 32, false>(pa);
+    pipe_tail<NWC * 32, false>(pa, gen);
   } else {
     if (threadIdx.x >= 128) return;  // one K1 system per fine CTA (128 threads)
     const int f = blockIdx.x - nchain;
     fine_role<P, CN, NWC>(pa, f / pa.g.B, f % pa.g.B);
-    pipe_tail<128, true>(pa);
+    pipe_tail<128, true>(pa, gen);
   }
 }
 
